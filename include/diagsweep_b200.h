@@ -1,0 +1,234 @@
+/*
+ * diagsweep_b200.h — C-ABI of the B200-native diagonal-sweeping DDM hot path.
+ *
+ * Plain C types only (no torch / C++ types cross this boundary).  Every
+ * buffer argument named `*_dev` is a device pointer owned by the caller;
+ * the library owns factor storage and plan workspaces behind opaque
+ * handles and frees them in the matching *_destroy call.  All calls are
+ * asynchronous on the context's stream unless stated; they block the host
+ * only where a result must be read back (ds_fact_create's pivot check,
+ * ds_ddm_counters, ds_*_host helpers).
+ *
+ * Status codes: 0 ok; < 0 configuration error (bad shape/window/argument,
+ * maps to diagsweep.errors.ConfigurationError); > 0 solver error (zero
+ * pivot, non-finite factor, CUDA failure; maps to SolverError).  The
+ * message of the last failure on the calling thread is ds_last_error().
+ *
+ * Complex values are complex128: interleaved (re, im) float64, i.e. the
+ * memory layout of numpy.complex128 / torch.complex128.
+ *
+ * Layout convention ("RHS-minor"): a batched field over a window of shape
+ * (n0, n1[, n2]) with R right-hand sides is stored [n0][n1][n2][R], node
+ * C-order outermost, the RHS index fastest.  The Python host converts from
+ * the reference's [R, *counts] batches at the API boundary.
+ *
+ * Reference interfaces replaced (the reference is pure Python; these are the
+ * calls a ctypes binding of its hot path makes — see INTEGRATION.md):
+ *   ds_op_*        <- DiscreteOperator / assemble_operator / .apply
+ *                     (diagsweep/pml.py:75-188, :216-266)
+ *   ds_fact_*      <- factorize / FactorizationCache.get(op).solve(rhs)
+ *                     (diagsweep/subdomain.py:43-179)
+ *   ds_plan_*,
+ *   ds_ddm_apply   <- diagonal_sweep_solve (diagsweep/ddm.py:212-291) incl.
+ *                     restrict_source (:168-195), _accumulate (:206-209),
+ *                     cut bookkeeping (:82-110), psi (transfer.py:100-155)
+ *   ds_vec_*       <- the vector kernels of gmres (diagsweep/krylov.py:40-147)
+ */
+#ifndef DIAGSWEEP_B200_H
+#define DIAGSWEEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DS_API __attribute__((visibility("default")))
+#else
+#define DS_API
+#endif
+
+typedef struct ds_ctx ds_ctx;
+typedef struct ds_op ds_op;
+typedef struct ds_fact ds_fact;
+typedef struct ds_plan ds_plan;
+
+typedef struct {
+  double re, im;
+} ds_cplx;
+
+/* ---------------------------------------------------------------- context */
+
+DS_API int ds_abi_version(void);
+DS_API const char *ds_last_error(void);
+
+/* `stream` is a cudaStream_t (NULL = legacy default stream). */
+DS_API int ds_ctx_create(int device, void *stream, ds_ctx **out);
+DS_API int ds_ctx_set_stream(ds_ctx *ctx, void *stream);
+DS_API int ds_ctx_synchronize(ds_ctx *ctx);
+DS_API int ds_ctx_destroy(ds_ctx *ctx);
+
+/* --------------------------------------------------------------- operator
+ * One assembled PML Helmholtz operator on a window (pml.py:75-188).
+ * c_lo[a], c_hi[a]: host arrays of length shape[a] (complex128) — the
+ * couplings 1/(alpha_node*alpha_face*h^2) computed on the host bit-exactly.
+ * kappa2_kind: 0 'const' (1 value), 1 'axis' (shape[kappa2_axis] values),
+ * 2 'full' (prod(shape) values, C-order).  Host pointers; copied. */
+typedef struct {
+  int32_t dim;
+  int32_t shape[3];
+  const ds_cplx *c_lo[3];
+  const ds_cplx *c_hi[3];
+  int32_t kappa2_kind;
+  int32_t kappa2_axis;
+  const double *kappa2;
+} ds_op_desc;
+
+DS_API int ds_op_create(ds_ctx *ctx, const ds_op_desc *desc, ds_op **out);
+DS_API int ds_op_destroy(ds_op *op);
+
+/* out = L v on `region` (zero outside region), pml.py:135-159.
+ * region_lo: offsets of the region inside the operator window;
+ * region_shape: its shape.  layout 0: v_dev/out_dev are RHS-minor
+ * [*region_shape][nrhs]; layout 1: RHS-outer [nrhs][*region_shape]. */
+DS_API int ds_op_apply(ds_ctx *ctx, const ds_op *op, const ds_cplx *v_dev,
+                ds_cplx *out_dev, int32_t nrhs, const int32_t *region_lo,
+                const int32_t *region_shape, int32_t layout);
+
+/* ---------------------------------------------------------- factorization
+ * Block-tridiagonal LU of n operators along each window's longest axis
+ * (first on ties): S_0 = D_0, S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1}; the
+ * dense inverses S_k^{-1} (complex128, Gauss-Jordan with partial pivoting)
+ * are stored.  Replaces SeparableFactorization / SparseLuFactorization
+ * (subdomain.py:43-133).  Blocks until done; returns > 0 on a zero pivot or
+ * a non-finite inverse. */
+DS_API int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact **out);
+/* Per-operator layout info: block axis, number of blocks, block size,
+ * factor bytes. */
+DS_API int ds_fact_info(const ds_fact *fact, int32_t i, int32_t *block_axis,
+                 int32_t *nb, int32_t *m, int64_t *bytes);
+/* x = A_i^{-1} rhs for one operator; rhs_dev/x_dev: [*window][nrhs]
+ * (subdomain.py:77-106 `.solve`). */
+DS_API int ds_fact_solve(ds_ctx *ctx, const ds_fact *fact, int32_t i,
+                  const ds_cplx *rhs_dev, ds_cplx *x_dev, int32_t nrhs);
+DS_API int ds_fact_destroy(ds_fact *fact);
+
+/* ------------------------------------------------------------- sweep plan
+ * Static schedule of one diagonal-sweeping application (ddm.py:212-291),
+ * built once by the host from the bit-exact partition / routing metadata.
+ * All arrays are host arrays; copied into device tables.
+ *
+ * Subdomain s (C-order linear id over 1-based indices):
+ *   win_lo/win_shape   [nsub*3]  its window (partition.py:83-90)
+ *   own_lo/own_shape   [nsub*3]  restricted-source region (ddm.py:185-194)
+ *   sup_lo/sup_shape   [nsub*3]  beta00 support (partition.py:135-150)
+ *   beta00             concatenated per-axis beta00 ramps over the support,
+ *                      axis a of s at beta00 + beta00_off[s*3+a]
+ *   op_of_sub[s]       index into `ops`
+ *   fact_of_sub[s], fact_index[s]  the factorization handle of subdomain s
+ *                      and the operator index inside that handle
+ * Sweeps (2^dim) and steps: visit order of sweep w is
+ *   visit_sub[w*nsub + step_off[w*(nsteps+1)+t] ...
+ *             w*nsub + step_off[w*(nsteps+1)+t+1]) for step t (sorted).
+ * Transfers: for every (sweep w, subdomain s, direction k) with an in-range
+ * target, xfer_use[(w*nsub+s)*ndir+k] = use sweep (1-based, 0 = discarded,
+ * -1 = target out of range).  directions[ndir*3] in itertools.product
+ * order (ddm.py:75-79).  Geometry per (s, k): band_lo/band_shape/ext_lo/
+ * ext_shape [(s*ndir+k)*3], and the (1-beta) factors on ext per axis at
+ * xfac + xfac_off[(s*ndir+k)*3+a] (ones on zero axes).
+ * Arrays are int32 unless noted. */
+typedef struct {
+  int32_t dim, nsub, nsweeps, nsteps, ndir, nrhs_max;
+  int32_t grid_counts[3];
+  int32_t part_counts[3];
+  const int32_t *win_lo, *win_shape;
+  const int32_t *own_lo, *own_shape;
+  const int32_t *sup_lo, *sup_shape;
+  const double *beta00;
+  const int64_t *beta00_off;
+  int32_t nops;
+  ds_op *const *ops;
+  const int32_t *op_of_sub;
+  ds_fact *const *fact_of_sub;
+  const int32_t *fact_index;
+  const int32_t *visit_sub;
+  const int32_t *step_off;
+  const int32_t *directions;
+  const int32_t *xfer_use;
+  const int32_t *band_lo, *band_shape, *ext_lo, *ext_shape;
+  const double *xfac;
+  const int64_t *xfac_off;
+} ds_plan_desc;
+
+DS_API int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *desc, ds_plan **out);
+DS_API int64_t ds_plan_workspace_bytes(const ds_plan *plan);
+DS_API int ds_plan_destroy(ds_plan *plan);
+
+/* One application of the diagonal-sweeping DDM to nrhs sources at once.
+ * f_dev, u_dev: [*grid_counts][nrhs] (RHS-minor).  u = sum of beta00-blended
+ * local solutions.  Emission masks (cuts, exact-zero flags) are evaluated on
+ * the device with the reference semantics (ddm.py:82-110, :242-279).
+ * partials_dev: NULL, or [nsweeps][*grid_counts][nrhs] receiving a copy of
+ * the running sum after each sweep (collect_partials). */
+DS_API int ds_ddm_apply(ds_ctx *ctx, ds_plan *plan, const ds_cplx *f_dev,
+                 ds_cplx *u_dev, int32_t nrhs, ds_cplx *partials_dev);
+
+/* Per-RHS counters of the last ds_ddm_apply (blocks the host):
+ *   nonzero[r], discarded[r] (DdmReport fields, ddm.py:149-165), and when
+ *   the arrays are non-NULL the per-visit tables [nsweeps][nsub][nrhs]:
+ *   visit_nonzero, visit_consumed, visit_emitted and visit_cut (the solve
+ *   cut mask, bit 2a+(side>0) for cut (axis a, side)). */
+DS_API int ds_ddm_counters(ds_ctx *ctx, ds_plan *plan, int32_t nrhs,
+                    int32_t *nonzero, int32_t *discarded,
+                    int32_t *visit_nonzero, int32_t *visit_consumed,
+                    int32_t *visit_emitted, int32_t *visit_cut);
+
+/* Record / replay the whole application as one CUDA graph (same f/u
+ * pointers and nrhs); ds_ddm_apply uses the graph when it matches. */
+DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
+
+/* Launch count of the last ds_ddm_apply (kernel nodes issued). */
+DS_API int64_t ds_plan_last_launches(const ds_plan *plan);
+
+/* ---------------------------------------------------------- vector kernels
+ * Batched complex vector ops for GMRES (krylov.py:80, :97-106, :139-142);
+ * vectors are RHS-outer [nrhs][n] (the reference's batch layout), one
+ * scalar per RHS.  Reductions are deterministic (fixed two-level order). */
+/* out[r] = sum_i conj(x[r,i]) * y[r,i] (np.vdot semantics) */
+DS_API int ds_vec_dot(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x_dev,
+               const ds_cplx *y_dev, ds_cplx *out_dev);
+/* out[r] = ||x[r,:]||_2 */
+DS_API int ds_vec_norm(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x_dev,
+                double *out_dev);
+/* y[r,:] += alpha_sign * a[r] * x[r,:]  (alpha_sign = +1 or -1) */
+DS_API int ds_vec_axpy(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *a_dev,
+                double alpha_sign, const ds_cplx *x_dev, ds_cplx *y_dev);
+/* fused MGS step: y -= a_prev * xprev (if xprev != NULL), then
+ * out[r] = vdot(x, y).  Same arithmetic as the unfused pair. */
+DS_API int ds_vec_axpy_dot(ds_ctx *ctx, int64_t n, int32_t nrhs,
+                    const ds_cplx *a_prev_dev, const ds_cplx *xprev_dev,
+                    ds_cplx *y_dev, const ds_cplx *x_dev, ds_cplx *out_dev);
+/* y[r] += sum_j c[j*nrhs+r] * X_j[r]   (basis update x += Z^T y) */
+DS_API int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec,
+                   const ds_cplx *const *x_dev_list, const ds_cplx *c_dev,
+                   ds_cplx *y_dev);
+/* y[r] = x[r] / s[r]  (s real; rows with s[r] == 0 are set to zero) —
+ * the normalisations V[0] = r/beta and V[k+1] = w/norm_w of krylov.py */
+DS_API int ds_vec_scale(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x_dev,
+                 const double *s_dev, ds_cplx *y_dev);
+
+/* RHS-outer [R][n] <-> RHS-minor [n][R] layout conversion. */
+DS_API int ds_layout_to_minor(ds_ctx *ctx, int64_t n, int32_t nrhs,
+                       const ds_cplx *src_dev, ds_cplx *dst_dev);
+DS_API int ds_layout_to_outer(ds_ctx *ctx, int64_t n, int32_t nrhs,
+                       const ds_cplx *src_dev, ds_cplx *dst_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIAGSWEEP_B200_H */

@@ -1,0 +1,381 @@
+"""GPU runtime glue between the reference-shaped Python API and the C-ABI.
+
+PyTorch is used only as plumbing: CUDA device memory, the current stream
+and host<->device copies.  All arithmetic of the hot path runs in the
+hand-written kernels of `libdiagsweep_b200.so`; when no CUDA device or no
+library is present the calls raise `SolverError` (no CPU fallback).
+
+Layouts: user-facing batches are RHS-outer `[R, *shape]` (the reference's
+array layout with a leading batch axis); the sweep engine works RHS-minor
+internally and converts with the `ds_layout_*` kernels at its boundary.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import itertools
+import math
+import weakref
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigurationError, SolverError
+
+try:  # torch is plumbing only; imported lazily-safe for CPU-only test runs
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+_CTX: dict = {}
+
+
+def _require_cuda():
+    if torch is None or not torch.cuda.is_available():
+        raise SolverError(
+            "no CUDA device: the diagsweep_b200 hot path runs only on the GPU "
+            "(there is no CPU fallback)")
+
+
+def context():
+    """(lib, ctx) bound to torch's current device and stream."""
+    _require_cuda()
+    lib = N.load_library()
+    dev = torch.cuda.current_device()
+    h = _CTX.get(dev)
+    if h is None:
+        out = C.c_void_p()
+        N.check(lib.ds_ctx_create(dev, None, C.byref(out)), "ds_ctx_create")
+        h = out
+        _CTX[dev] = h
+    N.check(lib.ds_ctx_set_stream(h, C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return lib, h
+
+
+# ----------------------------------------------------------------- tensors
+
+def to_device_batch(v, shape):
+    """-> (tensor [R, *shape] complex128 contiguous on the GPU, kind, batched)."""
+    _require_cuda()
+    kind = "torch" if hasattr(v, "detach") else "numpy"
+    vshape = tuple(v.shape)
+    if vshape == tuple(shape):
+        batched = False
+    elif vshape[1:] == tuple(shape):
+        batched = True
+    else:
+        raise ConfigurationError(f"field shape {vshape} does not match window {tuple(shape)}")
+    if kind == "numpy":
+        t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.complex128))
+        t = t.to("cuda", non_blocking=False)
+    else:
+        t = v.detach()
+        if t.dtype != torch.complex128:
+            t = t.to(torch.complex128)
+        if not t.is_cuda:
+            t = t.to("cuda")
+        t = t.contiguous()
+    if not batched:
+        t = t.reshape((1,) + tuple(shape))
+    return t, kind, batched
+
+
+def from_device_batch(t, kind, batched):
+    if not batched:
+        t = t[0]
+    if kind == "numpy":
+        return t.cpu().numpy()
+    return t
+
+
+# --------------------------------------------------------------- operators
+
+KINDS = {"const": 0, "axis": 1, "full": 2}
+
+
+class DeviceOperator:
+    """Device copy of one DiscreteOperator's couplings and kappa^2."""
+
+    def __init__(self, op):
+        lib, ctx = context()
+        keep = []
+        desc = N.OpDesc()
+        desc.dim = op.dim
+        for a in range(op.dim):
+            lo, hi = op.couplings[a]
+            lo = np.ascontiguousarray(lo, dtype=np.complex128)
+            hi = np.ascontiguousarray(hi, dtype=np.complex128)
+            keep += [lo, hi]
+            desc.shape[a] = op.window.shape[a]
+            desc.c_lo[a] = lo.ctypes.data
+            desc.c_hi[a] = hi.ctypes.data
+        k2 = op.kappa2_array()
+        keep.append(k2)
+        desc.kappa2_kind = KINDS[op.kappa2_kind]
+        desc.kappa2_axis = op.kappa2_axis if op.kappa2_kind == "axis" else -1
+        desc.kappa2 = k2.ctypes.data
+        out = C.c_void_p()
+        N.check(lib.ds_op_create(ctx, C.byref(desc), C.byref(out)), "ds_op_create")
+        self.handle = out
+        self._finalizer = weakref.finalize(self, lib.ds_op_destroy, out)
+
+
+def device_operator(op) -> DeviceOperator:
+    if op._device is None:
+        op._device = DeviceOperator(op)
+    return op._device
+
+
+def apply_operator(op, v, region):
+    lib, ctx = context()
+    dop = device_operator(op)
+    t, kind, batched = to_device_batch(v, region.shape)
+    out = torch.empty_like(t)
+    lo = np.array([r - w for r, w in zip(region.lo, op.window.lo)] + [0] * (3 - op.dim),
+                  dtype=np.int32)
+    sh = np.array(list(region.shape) + [1] * (3 - op.dim), dtype=np.int32)
+    N.check(lib.ds_op_apply(ctx, dop.handle, t.data_ptr(), out.data_ptr(), t.shape[0],
+                            lo.ctypes.data_as(N.P_i32), sh.ctypes.data_as(N.P_i32), 1),
+            "ds_op_apply")
+    return from_device_batch(out, kind, batched)
+
+
+# ------------------------------------------------------------ factorization
+
+class FactorSet:
+    """One ds_fact handle holding the block-LU factors of several operators."""
+
+    def __init__(self, ops):
+        lib, ctx = context()
+        handles = [device_operator(op).handle for op in ops]
+        arr = (C.c_void_p * len(ops))(*[h.value for h in handles])
+        out = C.c_void_p()
+        N.check(lib.ds_fact_create(ctx, arr, len(ops), C.byref(out)), "ds_fact_create")
+        self.handle = out
+        self.n = len(ops)
+        self._ops = list(ops)  # operators must outlive the factors
+        self._finalizer = weakref.finalize(self, lib.ds_fact_destroy, out)
+
+    def info(self, i):
+        lib = N.load_library()
+        ba, nb, m = C.c_int32(), C.c_int32(), C.c_int32()
+        nbytes = C.c_int64()
+        N.check(lib.ds_fact_info(self.handle, i, C.byref(ba), C.byref(nb), C.byref(m),
+                                 C.byref(nbytes)))
+        return ba.value, nb.value, m.value, nbytes.value
+
+
+def fact_solve(fset: FactorSet, index: int, op, rhs):
+    lib, ctx = context()
+    t, kind, batched = to_device_batch(rhs, op.window.shape)
+    R = t.shape[0]
+    W = op.window.size
+    tmin = torch.empty((W, R), dtype=torch.complex128, device=t.device)
+    N.check(lib.ds_layout_to_minor(ctx, W, R, t.data_ptr(), tmin.data_ptr()))
+    xmin = torch.empty_like(tmin)
+    N.check(lib.ds_fact_solve(ctx, fset.handle, index, tmin.data_ptr(), xmin.data_ptr(), R),
+            "ds_fact_solve")
+    x = torch.empty_like(t)
+    N.check(lib.ds_layout_to_outer(ctx, W, R, xmin.data_ptr(), x.data_ptr()))
+    return from_device_batch(x, kind, batched)
+
+
+# -------------------------------------------------------------- sweep plan
+
+def source_directions(dim: int):
+    return tuple(d for d in itertools.product((-1, 0, 1), repeat=dim) if any(d))
+
+
+def _pad3(t, fill=0):
+    t = list(t)
+    return t + [fill] * (3 - len(t))
+
+
+class DevicePlan:
+    """Static device tables for one (partition, operators, sweep plan).
+
+    Built from the bit-exact host metadata: windows / owned regions /
+    beta00 supports (partition.py), step groups (`_step_groups`,
+    ddm.py:198-203), routing (`next_usable_sweep`, transfer.py:90-97) and
+    psi geometry (transfer.py:100-155).
+    """
+
+    def __init__(self, partition, operators, cache, directions, nrhs_max: int):
+        from .partition import steps_per_sweep, sweep_step_of
+        from .transfer import next_usable_sweep, transfer_geometry
+
+        lib, ctx = context()
+        dim = partition.dim
+        subs = list(partition.subdomains())
+        nsub = len(subs)
+        lin = {idx: s for s, idx in enumerate(subs)}
+        ops = [operators[idx] for idx in subs]
+        facts = cache.factorizations(ops)
+        self.partition = partition
+        self.dim = dim
+        self.nsub = nsub
+        self.nsweeps = len(directions)
+        self.directions = tuple(directions)
+        self.nrhs_max = nrhs_max
+        self.nnodes = partition.grid.node_count()
+        self._keep = [ops, facts]
+
+        win_lo, win_shape, own_lo, own_shape, sup_lo, sup_shape = [], [], [], [], [], []
+        beta_vals, beta_off = [], []
+        off = 0
+        for idx in subs:
+            w = partition.window(idx)
+            o = partition.owned_window(idx)
+            sp = partition.beta00_window(idx)
+            win_lo += _pad3(w.lo); win_shape += _pad3(w.shape, 1)
+            own_lo += _pad3(o.lo); own_shape += _pad3(o.shape, 1)
+            sup_lo += _pad3(sp.lo); sup_shape += _pad3(sp.shape, 1)
+            ramps = partition.beta00_axis_values(idx)
+            for a in range(3):
+                beta_off.append(off)
+                if a < dim:
+                    beta_vals.append(np.asarray(ramps[a], dtype=np.float64))
+                    off += ramps[a].size
+        dirs = source_directions(dim)
+        ndir = len(dirs)
+        nsteps = steps_per_sweep(partition.counts)
+        visit_sub, step_off = [], []
+        for sd in self.directions:
+            groups: dict = {}
+            for idx in subs:
+                groups.setdefault(sweep_step_of(idx, sd, partition.counts), []).append(idx)
+            order = []
+            offs = [0]
+            for t in range(1, nsteps + 1):
+                order += [lin[i] for i in sorted(groups.get(t, []))]
+                offs.append(len(order))
+            visit_sub += order
+            step_off += offs
+        geoms = {}
+        band_lo, band_shape, ext_lo, ext_shape, xfac_off = [], [], [], [], []
+        xfac_vals = []
+        foff = 0
+        for s, idx in enumerate(subs):
+            for k, dvec in enumerate(dirs):
+                g = transfer_geometry(partition, idx, dvec)
+                geoms[(s, k)] = g
+                if g is None:
+                    band_lo += [0] * 3; band_shape += [0] * 3
+                    ext_lo += [0] * 3; ext_shape += [0] * 3
+                    xfac_off += [0] * 3
+                    continue
+                band_lo += _pad3(g.band.lo); band_shape += _pad3(g.band.shape, 1)
+                ext_lo += _pad3(g.ext.lo); ext_shape += _pad3(g.ext.shape, 1)
+                for a in range(3):
+                    xfac_off.append(foff)
+                    if a < dim:
+                        xfac_vals.append(np.asarray(g.factors[a], dtype=np.float64))
+                        foff += g.factors[a].size
+        xfer_use = np.full((self.nsweeps, nsub, ndir), -1, dtype=np.int32)
+        for w in range(self.nsweeps):
+            for s in range(nsub):
+                for k, dvec in enumerate(dirs):
+                    if geoms[(s, k)] is None:
+                        continue
+                    use = next_usable_sweep(dvec, w + 1, self.directions)
+                    xfer_use[w, s, k] = 0 if use is None else use
+        self.xfer_use = xfer_use
+        self.geoms = geoms
+        self.subs = subs
+        self.dirs = dirs
+        self.nsteps = nsteps
+        self.visit_sub = np.asarray(visit_sub, dtype=np.int32)
+        self.step_off = np.asarray(step_off, dtype=np.int32)
+
+        arrays = dict(
+            win_lo=np.asarray(win_lo, np.int32), win_shape=np.asarray(win_shape, np.int32),
+            own_lo=np.asarray(own_lo, np.int32), own_shape=np.asarray(own_shape, np.int32),
+            sup_lo=np.asarray(sup_lo, np.int32), sup_shape=np.asarray(sup_shape, np.int32),
+            beta00=np.concatenate(beta_vals), beta00_off=np.asarray(beta_off, np.int64),
+            op_of_sub=np.arange(nsub, dtype=np.int32),
+            fact_index=np.asarray([f.index for f in facts], np.int32),
+            visit_sub=self.visit_sub, step_off=self.step_off,
+            directions=np.asarray([_pad3(dv) for dv in dirs], np.int32).ravel(),
+            xfer_use=xfer_use.ravel(),
+            band_lo=np.asarray(band_lo, np.int32), band_shape=np.asarray(band_shape, np.int32),
+            ext_lo=np.asarray(ext_lo, np.int32), ext_shape=np.asarray(ext_shape, np.int32),
+            xfac=np.concatenate(xfac_vals) if xfac_vals else np.zeros(1),
+            xfac_off=np.asarray(xfac_off, np.int64),
+        )
+        op_handles = (C.c_void_p * nsub)(*[device_operator(op).handle.value for op in ops])
+        fact_handles = (C.c_void_p * nsub)(*[f.fset.handle.value for f in facts])
+        desc = N.PlanDesc()
+        desc.dim, desc.nsub, desc.nsweeps = dim, nsub, self.nsweeps
+        desc.nsteps, desc.ndir, desc.nrhs_max = nsteps, ndir, nrhs_max
+        for a in range(3):
+            desc.grid_counts[a] = partition.grid.counts[a] if a < dim else 1
+            desc.part_counts[a] = partition.counts[a] if a < dim else 1
+        for name, arr in arrays.items():
+            setattr(desc, name, arr.ctypes.data)
+        desc.nops = nsub
+        desc.ops = C.cast(op_handles, C.c_void_p)
+        desc.fact_of_sub = C.cast(fact_handles, C.c_void_p)
+        out = C.c_void_p()
+        N.check(lib.ds_plan_create(ctx, C.byref(desc), C.byref(out)), "ds_plan_create")
+        self.handle = out
+        self._finalizer = weakref.finalize(self, lib.ds_plan_destroy, out)
+
+    @property
+    def workspace_bytes(self) -> int:
+        return N.load_library().ds_plan_workspace_bytes(self.handle)
+
+    def enable_graph(self, enable: bool = True):
+        lib, ctx = context()
+        N.check(lib.ds_ddm_enable_graph(ctx, self.handle, int(bool(enable))))
+
+    def last_launches(self) -> int:
+        return N.load_library().ds_plan_last_launches(self.handle)
+
+    def apply_minor(self, fmin, umin, nrhs: int, partials=None):
+        """One application on RHS-minor device buffers (no layout work)."""
+        lib, ctx = context()
+        N.check(lib.ds_ddm_apply(ctx, self.handle, fmin.data_ptr(), umin.data_ptr(), nrhs,
+                                 0 if partials is None else partials.data_ptr()),
+                "ds_ddm_apply")
+
+    def apply(self, f, collect_partials: bool = False):
+        """f: [R, N] complex128 CUDA tensor (RHS-outer) -> (u [R, N], partials)."""
+        lib, ctx = context()
+        R = f.shape[0]
+        n = self.nnodes
+        fmin = torch.empty((n, R), dtype=torch.complex128, device=f.device)
+        N.check(lib.ds_layout_to_minor(ctx, n, R, f.data_ptr(), fmin.data_ptr()))
+        umin = torch.empty_like(fmin)
+        partials = None
+        if collect_partials:
+            partials = torch.empty((self.nsweeps, n, R), dtype=torch.complex128, device=f.device)
+        self.apply_minor(fmin, umin, R, partials)
+        u = torch.empty((R, n), dtype=torch.complex128, device=f.device)
+        N.check(lib.ds_layout_to_outer(ctx, n, R, umin.data_ptr(), u.data_ptr()))
+        parts = None
+        if partials is not None:
+            parts = []
+            for w in range(self.nsweeps):
+                p = torch.empty((R, n), dtype=torch.complex128, device=f.device)
+                N.check(lib.ds_layout_to_outer(ctx, n, R, partials[w].data_ptr(), p.data_ptr()))
+                parts.append(p)
+        return u, parts
+
+    def counters(self, nrhs: int):
+        lib, ctx = context()
+        per = self.nsweeps * self.nsub * nrhs
+        nonzero = np.zeros(nrhs, np.int32)
+        discarded = np.zeros(nrhs, np.int32)
+        vnz = np.zeros(per, np.int32)
+        vcons = np.zeros(per, np.int32)
+        vemit = np.zeros(per, np.int32)
+        vcut = np.zeros(per, np.int32)
+        P = N.P_i32
+        N.check(lib.ds_ddm_counters(ctx, self.handle, nrhs, nonzero.ctypes.data_as(P),
+                                    discarded.ctypes.data_as(P), vnz.ctypes.data_as(P),
+                                    vcons.ctypes.data_as(P), vemit.ctypes.data_as(P),
+                                    vcut.ctypes.data_as(P)), "ds_ddm_counters")
+        shape = (self.nsweeps, self.nsub, nrhs)
+        return dict(nonzero=nonzero, discarded=discarded, visit_nonzero=vnz.reshape(shape),
+                    visit_consumed=vcons.reshape(shape), visit_emitted=vemit.reshape(shape),
+                    visit_cut=vcut.reshape(shape))

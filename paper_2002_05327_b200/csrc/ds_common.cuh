@@ -1,0 +1,148 @@
+// Shared device/host helpers of the diagsweep_b200 library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/diagsweep_b200.h"
+
+typedef double2 cplx;  // (re, im), same bytes as ds_cplx / complex128
+
+#define DS_HD __host__ __device__ __forceinline__
+
+DS_HD cplx cmk(double r, double i) { return make_double2(r, i); }
+DS_HD cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+DS_HD cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+DS_HD cplx cmul(cplx a, cplx b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+DS_HD cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+// acc += a * b
+DS_HD void cfma(cplx &acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+DS_HD void cfma_conj(cplx &acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+DS_HD cplx cinv(cplx a) {
+  // Smith's algorithm (robust reciprocal)
+  if (fabs(a.x) >= fabs(a.y)) {
+    double r = a.y / a.x, den = a.x + a.y * r;
+    return make_double2(1.0 / den, -r / den);
+  } else {
+    double r = a.x / a.y, den = a.x * r + a.y;
+    return make_double2(r / den, -1.0 / den);
+  }
+}
+DS_HD bool cnonzero(cplx a) { return a.x != 0.0 || a.y != 0.0; }
+DS_HD double cabs1(cplx a) { return fabs(a.x) + fabs(a.y); }
+
+// ----------------------------------------------------------- status codes
+enum {
+  DS_OK = 0,
+  DS_ECONFIG = -1,
+  DS_ESOLVER = 1,
+  DS_ECUDA = 2,
+};
+
+void ds_set_error(const std::string &msg);
+int ds_fail(int code, const std::string &msg);
+
+#define DS_CUDA(call)                                                      \
+  do {                                                                     \
+    cudaError_t _e = (call);                                               \
+    if (_e != cudaSuccess)                                                 \
+      return ds_fail(DS_ECUDA, std::string(#call) + ": " +                 \
+                                   cudaGetErrorString(_e));                \
+  } while (0)
+
+#define DS_CHECK_LAUNCH()                                                  \
+  do {                                                                     \
+    cudaError_t _e = cudaGetLastError();                                   \
+    if (_e != cudaSuccess)                                                 \
+      return ds_fail(DS_ECUDA, std::string("kernel launch: ") +            \
+                                   cudaGetErrorString(_e));                \
+  } while (0)
+
+// ------------------------------------------------------------- handles
+struct ds_ctx {
+  int device;
+  cudaStream_t stream;
+  int num_sms;
+  int64_t launches;  // kernel launches issued through this context
+  // scratch for reductions
+  void *scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+// device-side operator view (coefficient arrays are device pointers)
+struct OpDev {
+  int dim;
+  int shape[3];
+  int kappa2_kind;
+  int kappa2_axis;
+  const cplx *c_lo[3];
+  const cplx *c_hi[3];
+  const double *kappa2;
+};
+
+struct ds_op {
+  OpDev dev;
+  void *storage;  // single allocation holding all coefficient arrays
+  // host copies (used to assemble factor blocks)
+  std::vector<cplx> h_clo[3], h_chi[3];
+  std::vector<double> h_k2;
+};
+
+// per-operator factor layout
+struct FactDev {
+  int block_axis;
+  int nb, m;
+  int other[2];       // the in-block axes in C order (unused entries = -1)
+  int win_shape[3];
+  const cplx *sinv;   // nb * m * m, row-major blocks
+  const cplx *lcoef;  // nb: coupling of block k to k-1 (c_lo along axis)
+  const cplx *ucoef;  // nb: coupling of block k to k+1 (c_hi along axis)
+};
+
+struct ds_fact {
+  std::vector<FactDev> facts;
+  std::vector<void *> allocations;
+  int64_t bytes_total = 0;
+  std::vector<int64_t> bytes;
+};
+
+// window-local linear (C-order) index <-> block layout offset
+// perm offset of local coords c: (c[ba]*m + inblock(c)), inblock over the
+// other axes in C order.
+DS_HD int64_t block_offset(const FactDev &f, const int *c) {
+  int64_t ib = 0;
+  if (f.other[0] >= 0) ib = c[f.other[0]];
+  if (f.other[1] >= 0) ib = ib * f.win_shape[f.other[1]] + c[f.other[1]];
+  return (int64_t)c[f.block_axis] * f.m + ib;
+}
+
+// one (subdomain, step) solve of K3: rhs/x in block layout [nb][m][nrhs];
+// nz: per-RHS nonzero flags (NULL = solve all); all-zero visits are skipped
+struct SolveVisit {
+  const FactDev *f;
+  const cplx *rhs;
+  cplx *x;
+  const int *nz;
+};
+
+// launch K3 over a device table of visits (one cluster per visit x chunk)
+int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs,
+                          int max_m);
+
+int ceil_div(int a, int b);

@@ -1,0 +1,446 @@
+// Context, error handling, operators + stencil apply (K1), batched vector
+// kernels for GMRES (K7) and layout conversion.
+//
+// K1 restates DiscreteOperator.apply (diagsweep/pml.py:135-159):
+//   out = k2*v + sum_a [ -(c_lo+c_hi) v + c_lo[i] v[i-1] + c_hi[i] v[i+1] ]
+// with zero Dirichlet data outside `region`.  HBM-bound: 32 B/node/RHS
+// (+8 B for 'full' kappa^2); the RHS-minor layout makes every neighbour
+// access a contiguous run of nrhs complex values.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <string>
+
+#include "ds_common.cuh"
+
+static thread_local std::string g_last_error;
+
+void ds_set_error(const std::string &msg) { g_last_error = msg; }
+int ds_fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+extern "C" int ds_abi_version(void) { return DS_ABI_VERSION; }
+extern "C" const char *ds_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int ds_ctx_create(int device, void *stream, ds_ctx **out) {
+  if (!out) return ds_fail(DS_ECONFIG, "ds_ctx_create: null out");
+  int ndev = 0;
+  DS_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return ds_fail(DS_ECONFIG, "ds_ctx_create: bad device ordinal");
+  DS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  DS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return ds_fail(DS_ECONFIG, std::string("library built for sm_100a, device is ") +
+                                   prop.name);
+  ds_ctx *c = new ds_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->num_sms = prop.multiProcessorCount;
+  c->launches = 0;
+  c->scratch_bytes = 1 << 20;
+  if (cudaMalloc(&c->scratch, c->scratch_bytes) != cudaSuccess) {
+    delete c;
+    return ds_fail(DS_ECUDA, "ds_ctx_create: scratch allocation failed");
+  }
+  *out = c;
+  return DS_OK;
+}
+
+extern "C" int ds_ctx_set_stream(ds_ctx *ctx, void *stream) {
+  if (!ctx) return ds_fail(DS_ECONFIG, "null ctx");
+  ctx->stream = (cudaStream_t)stream;
+  return DS_OK;
+}
+
+extern "C" int ds_ctx_synchronize(ds_ctx *ctx) {
+  if (!ctx) return ds_fail(DS_ECONFIG, "null ctx");
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+extern "C" int ds_ctx_destroy(ds_ctx *ctx) {
+  if (!ctx) return DS_OK;
+  cudaFree(ctx->scratch);
+  delete ctx;
+  return DS_OK;
+}
+
+// ------------------------------------------------------------------ ops
+
+extern "C" int ds_op_create(ds_ctx *ctx, const ds_op_desc *d, ds_op **out) {
+  if (!ctx || !d || !out) return ds_fail(DS_ECONFIG, "ds_op_create: null argument");
+  if (d->dim != 2 && d->dim != 3) return ds_fail(DS_ECONFIG, "operator dim must be 2 or 3");
+  int64_t nodes = 1;
+  for (int a = 0; a < d->dim; ++a) {
+    if (d->shape[a] < 1) return ds_fail(DS_ECONFIG, "operator shape must be positive");
+    if (!d->c_lo[a] || !d->c_hi[a]) return ds_fail(DS_ECONFIG, "missing coupling array");
+    nodes *= d->shape[a];
+  }
+  int64_t nk2;
+  switch (d->kappa2_kind) {
+    case 0: nk2 = 1; break;
+    case 1:
+      if (d->kappa2_axis < 0 || d->kappa2_axis >= d->dim)
+        return ds_fail(DS_ECONFIG, "bad kappa2 axis");
+      nk2 = d->shape[d->kappa2_axis];
+      break;
+    case 2: nk2 = nodes; break;
+    default: return ds_fail(DS_ECONFIG, "bad kappa2 kind");
+  }
+  if (!d->kappa2) return ds_fail(DS_ECONFIG, "missing kappa2");
+  int64_t ncoef = 0;
+  for (int a = 0; a < d->dim; ++a) ncoef += 2 * d->shape[a];
+  size_t bytes = ncoef * sizeof(cplx) + nk2 * sizeof(double);
+  ds_op *op = new ds_op();
+  if (cudaMalloc(&op->storage, bytes) != cudaSuccess) {
+    delete op;
+    return ds_fail(DS_ECUDA, "ds_op_create: allocation failed");
+  }
+  OpDev &o = op->dev;
+  memset(&o, 0, sizeof(o));
+  o.dim = d->dim;
+  o.kappa2_kind = d->kappa2_kind;
+  o.kappa2_axis = d->kappa2_kind == 1 ? d->kappa2_axis : -1;
+  cplx *p = (cplx *)op->storage;
+  for (int a = 0; a < d->dim; ++a) {
+    o.shape[a] = d->shape[a];
+    cudaMemcpy(p, d->c_lo[a], d->shape[a] * sizeof(cplx), cudaMemcpyHostToDevice);
+    o.c_lo[a] = p;
+    p += d->shape[a];
+    cudaMemcpy(p, d->c_hi[a], d->shape[a] * sizeof(cplx), cudaMemcpyHostToDevice);
+    o.c_hi[a] = p;
+    p += d->shape[a];
+    op->h_clo[a].assign((const cplx *)d->c_lo[a], (const cplx *)d->c_lo[a] + d->shape[a]);
+    op->h_chi[a].assign((const cplx *)d->c_hi[a], (const cplx *)d->c_hi[a] + d->shape[a]);
+  }
+  for (int a = d->dim; a < 3; ++a) o.shape[a] = 1;
+  double *k2 = (double *)p;
+  DS_CUDA(cudaMemcpy(k2, d->kappa2, nk2 * sizeof(double), cudaMemcpyHostToDevice));
+  o.kappa2 = k2;
+  op->h_k2.assign(d->kappa2, d->kappa2 + nk2);
+  *out = op;
+  return DS_OK;
+}
+
+extern "C" int ds_op_destroy(ds_op *op) {
+  if (!op) return DS_OK;
+  cudaFree(op->storage);
+  delete op;
+  return DS_OK;
+}
+
+__device__ __forceinline__ double op_kappa2(const OpDev &o, const int *c) {
+  if (o.kappa2_kind == 0) return o.kappa2[0];
+  if (o.kappa2_kind == 1) return o.kappa2[c[o.kappa2_axis]];
+  int64_t lin = c[0];
+  for (int a = 1; a < o.dim; ++a) lin = lin * o.shape[a] + c[a];
+  return o.kappa2[lin];
+}
+
+// One thread per (region node, rhs).  rlo = region offset inside the
+// operator window.  Order of accumulation follows pml.py:144-158.
+// layout 0: RHS-minor [nodes][nrhs]; layout 1: RHS-outer [nrhs][nodes].
+__global__ void k_apply(OpDev o, const cplx *__restrict__ v, cplx *__restrict__ out,
+                        int nrhs, int rlo0, int rlo1, int rlo2, int rs0, int rs1,
+                        int rs2, int outer) {
+  const int64_t nodes = (int64_t)rs0 * rs1 * rs2;
+  int64_t total = nodes * nrhs;
+  int rlo[3] = {rlo0, rlo1, rlo2};
+  int rs[3] = {rs0, rs1, rs2};
+  const int64_t ns = outer ? 1 : nrhs;  // node stride
+  int64_t strides[3];
+  strides[2] = ns;
+  strides[1] = (int64_t)rs2 * ns;
+  strides[0] = (int64_t)rs1 * rs2 * ns;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t node = outer ? q % nodes : q / nrhs;
+    int e[3];
+    e[2] = node % rs2;
+    int64_t t = node / rs2;
+    e[1] = t % rs1;
+    e[0] = t / rs1;
+    int c[3] = {e[0] + rlo[0], e[1] + rlo[1], e[2] + rlo[2]};
+    cplx vc = v[q];
+    double k2 = op_kappa2(o, c);
+    cplx acc = cscale(vc, k2);
+    for (int a = 0; a < o.dim; ++a) {
+      cplx lo = o.c_lo[a][c[a]], hi = o.c_hi[a][c[a]];
+      acc = cadd(acc, cmul(make_double2(-(lo.x + hi.x), -(lo.y + hi.y)), vc));
+      if (e[a] > 0) acc = cadd(acc, cmul(lo, v[q - strides[a]]));
+      if (e[a] < rs[a] - 1) acc = cadd(acc, cmul(hi, v[q + strides[a]]));
+    }
+    out[q] = acc;
+  }
+}
+
+static int grid_for(ds_ctx *ctx, int64_t work, int threads) {
+  int64_t blocks = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)ctx->num_sms * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+extern "C" int ds_op_apply(ds_ctx *ctx, const ds_op *op, const ds_cplx *v, ds_cplx *out,
+                           int32_t nrhs, const int32_t *rlo, const int32_t *rs, int32_t layout) {
+  if (!ctx || !op || !v || !out || nrhs < 1)
+    return ds_fail(DS_ECONFIG, "ds_op_apply: bad argument");
+  const OpDev &o = op->dev;
+  int lo[3] = {0, 0, 0}, sh[3] = {1, 1, 1};
+  for (int a = 0; a < o.dim; ++a) {
+    lo[a] = rlo ? rlo[a] : 0;
+    sh[a] = rs ? rs[a] : o.shape[a];
+    if (lo[a] < 0 || sh[a] < 1 || lo[a] + sh[a] > o.shape[a])
+      return ds_fail(DS_ECONFIG, "ds_op_apply: region outside the operator window");
+  }
+  int64_t total = (int64_t)sh[0] * sh[1] * sh[2] * nrhs;
+  k_apply<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
+      o, (const cplx *)v, (cplx *)out, nrhs, lo[0], lo[1], lo[2], sh[0], sh[1], sh[2],
+      layout != 0);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+// ------------------------------------------------------- vector kernels
+// GMRES vectors are RHS-outer [nrhs][n] (the reference's batch layout), so
+// every per-RHS reduction runs over a contiguous vector.  Deterministic:
+// grid (B, nrhs); block b of RHS r reduces a fixed chunk in a fixed tree
+// order into partials[r][b]; a second kernel sums the B partials in order.
+
+#define VEC_THREADS 256
+#define VEC_BLOCKS_MAX 256
+
+__device__ __forceinline__ cplx block_reduce(cplx v, cplx *red) {
+  int t = threadIdx.x;
+  red[t] = v;
+  __syncthreads();
+  for (int s = VEC_THREADS / 2; s > 0; s >>= 1) {
+    if (t < s) red[t] = cadd(red[t], red[t + s]);
+    __syncthreads();
+  }
+  return red[0];
+}
+
+// MODE 0: vdot(x, y); 1: |x|^2; 2: y -= a_prev*xprev then vdot(x, y)
+template <int MODE>
+__global__ void __launch_bounds__(VEC_THREADS)
+    k_vec_reduce(int64_t n, const cplx *__restrict__ x, cplx *y, const cplx *__restrict__ a_prev,
+                 const cplx *__restrict__ xprev, cplx *partials, int64_t chunk) {
+  __shared__ cplx red[VEC_THREADS];
+  const int r = blockIdx.y, B = gridDim.x;
+  const int64_t base = (int64_t)r * n;
+  int64_t i0 = blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  cplx acc = make_double2(0.0, 0.0);
+  cplx s = make_double2(0.0, 0.0);
+  if (MODE == 2 && xprev) s = a_prev[r];
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += VEC_THREADS) {
+    cplx a = x[base + i];
+    if (MODE == 1) {
+      acc.x = fma(a.x, a.x, acc.x);
+      acc.x = fma(a.y, a.y, acc.x);
+    } else {
+      cplx yv = y[base + i];
+      if (MODE == 2 && xprev) {
+        yv = csub(yv, cmul(s, xprev[base + i]));
+        y[base + i] = yv;
+      }
+      cfma_conj(acc, a, yv);
+    }
+  }
+  cplx tot = block_reduce(acc, red);
+  if (threadIdx.x == 0) partials[(int64_t)r * B + blockIdx.x] = tot;
+}
+
+__global__ void k_reduce_final(int nblocks, int nrhs, const cplx *partials, cplx *out_c,
+                               double *out_norm) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrhs) return;
+  cplx s = make_double2(0.0, 0.0);
+  for (int b = 0; b < nblocks; ++b) s = cadd(s, partials[(int64_t)r * nblocks + b]);
+  if (out_c) out_c[r] = s;
+  if (out_norm) out_norm[r] = sqrt(s.x);
+}
+
+static int reduction_launch(ds_ctx *ctx, int mode, int64_t n, int nrhs, const cplx *x, cplx *y,
+                            const cplx *a_prev, const cplx *xprev, cplx *out_c,
+                            double *out_norm) {
+  if (nrhs < 1 || nrhs > 65535 || n < 1) return ds_fail(DS_ECONFIG, "vector op: bad sizes");
+  int64_t want = (int64_t)ctx->num_sms * 4 / nrhs;
+  int B = (int)std::max<int64_t>(1, std::min<int64_t>(VEC_BLOCKS_MAX, want));
+  int64_t chunk = (n + B - 1) / B;
+  B = (int)((n + chunk - 1) / chunk);
+  if ((size_t)B * nrhs * sizeof(cplx) > ctx->scratch_bytes)
+    return ds_fail(DS_ECONFIG, "reduction scratch too small");
+  cplx *partials = (cplx *)ctx->scratch;
+  dim3 grid(B, nrhs);
+  if (mode == 0)
+    k_vec_reduce<0><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, nullptr, nullptr, partials, chunk);
+  else if (mode == 1)
+    k_vec_reduce<1><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, nullptr, nullptr, partials, chunk);
+  else
+    k_vec_reduce<2><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, a_prev, xprev, partials, chunk);
+  k_reduce_final<<<ceil_div(nrhs, 128), 128, 0, ctx->stream>>>(B, nrhs, partials, out_c, out_norm);
+  ctx->launches += 2;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+extern "C" int ds_vec_dot(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x,
+                          const ds_cplx *y, ds_cplx *out) {
+  if (!ctx) return ds_fail(DS_ECONFIG, "null ctx");
+  return reduction_launch(ctx, 0, n, nrhs, (const cplx *)x, (cplx *)y, nullptr, nullptr,
+                          (cplx *)out, nullptr);
+}
+
+extern "C" int ds_vec_norm(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x,
+                           double *out) {
+  if (!ctx) return ds_fail(DS_ECONFIG, "null ctx");
+  return reduction_launch(ctx, 1, n, nrhs, (const cplx *)x, nullptr, nullptr, nullptr, nullptr,
+                          out);
+}
+
+extern "C" int ds_vec_axpy_dot(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *a_prev,
+                               const ds_cplx *xprev, ds_cplx *y, const ds_cplx *x,
+                               ds_cplx *out) {
+  if (!ctx) return ds_fail(DS_ECONFIG, "null ctx");
+  return reduction_launch(ctx, 2, n, nrhs, (const cplx *)x, (cplx *)y, (const cplx *)a_prev,
+                          (const cplx *)xprev, (cplx *)out, nullptr);
+}
+
+__global__ void k_axpy(int64_t n, const cplx *__restrict__ a, double sgn,
+                       const cplx *__restrict__ x, cplx *y) {
+  const int r = blockIdx.y;
+  cplx s = a[r];
+  s.x *= sgn;
+  s.y *= sgn;
+  const int64_t base = (int64_t)r * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[base + i] = cadd(y[base + i], cmul(s, x[base + i]));
+}
+
+static dim3 vec_grid(ds_ctx *ctx, int64_t n, int nrhs) {
+  int64_t per = std::max<int64_t>(1, (int64_t)ctx->num_sms * 8 / nrhs);
+  int64_t need = (n + 255) / 256;
+  return dim3((unsigned)std::max<int64_t>(1, std::min(per, need)), nrhs);
+}
+
+extern "C" int ds_vec_axpy(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *a,
+                           double sgn, const ds_cplx *x, ds_cplx *y) {
+  if (!ctx || nrhs < 1 || nrhs > 65535) return ds_fail(DS_ECONFIG, "ds_vec_axpy: bad argument");
+  k_axpy<<<vec_grid(ctx, n, nrhs), 256, 0, ctx->stream>>>(n, (const cplx *)a, sgn,
+                                                          (const cplx *)x, (cplx *)y);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+#define MAX_COMBINE 64
+struct CombineArgs {
+  const cplx *x[MAX_COMBINE];
+};
+
+// y[r] += sum_j c[j][r] * X_j[r]   (krylov.py:139, x + Z^T y)
+__global__ void k_combine(int64_t n, int nrhs, int nvec, CombineArgs args,
+                          const cplx *__restrict__ c, cplx *y) {
+  const int r = blockIdx.y;
+  const int64_t base = (int64_t)r * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < nvec; ++j) acc = cadd(acc, cmul(c[j * nrhs + r], args.x[j][base + i]));
+    y[base + i] = cadd(y[base + i], acc);
+  }
+}
+
+extern "C" int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec,
+                              const ds_cplx *const *xs, const ds_cplx *c, ds_cplx *y) {
+  if (!ctx || nrhs < 1 || nrhs > 65535 || nvec < 0 || nvec > MAX_COMBINE)
+    return ds_fail(DS_ECONFIG, "ds_vec_combine: bad argument");
+  if (nvec == 0) return DS_OK;
+  CombineArgs args;
+  for (int j = 0; j < nvec; ++j) args.x[j] = (const cplx *)xs[j];
+  k_combine<<<vec_grid(ctx, n, nrhs), 256, 0, ctx->stream>>>(n, nrhs, nvec, args,
+                                                             (const cplx *)c, (cplx *)y);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+__global__ void k_scale(int64_t n, const cplx *__restrict__ x, const double *__restrict__ s,
+                        cplx *y) {
+  const int r = blockIdx.y;
+  const double sc = s[r];
+  const int64_t base = (int64_t)r * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    cplx v = x[base + i];
+    y[base + i] = sc == 0.0 ? make_double2(0.0, 0.0) : make_double2(v.x / sc, v.y / sc);
+  }
+}
+
+extern "C" int ds_vec_scale(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x,
+                            const double *s, ds_cplx *y) {
+  if (!ctx || nrhs < 1 || nrhs > 65535) return ds_fail(DS_ECONFIG, "ds_vec_scale: bad argument");
+  k_scale<<<vec_grid(ctx, n, nrhs), 256, 0, ctx->stream>>>(n, (const cplx *)x, s, (cplx *)y);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+// ----------------------------------------------------- layout transpose
+// [R][n] <-> [n][R] through a 32x32 shared tile.
+__global__ void k_transpose(int64_t rows, int64_t cols, int64_t ntc,
+                            const cplx *__restrict__ src, cplx *__restrict__ dst) {
+  // src is [rows][cols], dst is [cols][rows]; 1D grid over 32x32 tiles
+  __shared__ cplx tile[32][33];
+  int64_t tr = blockIdx.x / ntc, tc = blockIdx.x % ntc;
+  int64_t r0 = tr * 32, c0 = tc * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
+static int transpose(ds_ctx *ctx, int64_t rows, int64_t cols, const cplx *src, cplx *dst) {
+  if (rows < 1 || cols < 1) return DS_OK;
+  if (rows == 1 || cols == 1) {
+    DS_CUDA(cudaMemcpyAsync(dst, src, rows * cols * sizeof(cplx), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    return DS_OK;
+  }
+  int64_t ntr = (rows + 31) / 32, ntc = (cols + 31) / 32;
+  if (ntr * ntc > 0x7fffffffLL) return ds_fail(DS_ECONFIG, "transpose: too large");
+  k_transpose<<<(unsigned)(ntr * ntc), dim3(32, 8), 0, ctx->stream>>>(rows, cols, ntc, src, dst);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+extern "C" int ds_layout_to_minor(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *src,
+                                  ds_cplx *dst) {
+  if (!ctx || src == dst) return ds_fail(DS_ECONFIG, "ds_layout_to_minor: bad argument");
+  // src [R][n] -> dst [n][R]
+  return transpose(ctx, nrhs, n, (const cplx *)src, (cplx *)dst);
+}
+
+extern "C" int ds_layout_to_outer(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *src,
+                                  ds_cplx *dst) {
+  if (!ctx || src == dst) return ds_fail(DS_ECONFIG, "ds_layout_to_outer: bad argument");
+  // src [n][R] -> dst [R][n]
+  return transpose(ctx, n, nrhs, (const cplx *)src, (cplx *)dst);
+}

@@ -1,0 +1,401 @@
+// K2: block-tridiagonal factorization of subdomain operators (2D windows).
+//
+// Replaces SeparableFactorization / SparseLuFactorization
+// (diagsweep/subdomain.py:43-133).  The window is cut into n_b slabs along
+// its longest axis (block axis); the operator is block tridiagonal with
+// diagonal blocks D_k (the in-slab stencil plus kappa^2 and the block-axis
+// diagonal) and scalar off-diagonal blocks l_k I, u_k I (c_lo/c_hi of the
+// block axis, pml.py:95-102).  Block LU:
+//     S_0 = D_0,   S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1},
+// and every S_k^{-1} is stored densely (complex128) so the substitution is
+// pure GEMV/GEMM work (K3).
+//
+// One thread-block cluster per operator walks the chain; each CTA owns a
+// column slice of S_k in shared memory and the cluster inverts it by
+// Gauss-Jordan elimination with partial pivoting (pivot column broadcast
+// through distributed shared memory, one cluster barrier per pivot).  The
+// explicit inverse keeps the backward error at ~1e-15 for these operators
+// (cond(S_k) ~ 1e2), measured against the reference's Schur/Sylvester
+// solver in DESIGN.md.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ds_common.cuh"
+
+namespace cg = cooperative_groups;
+
+struct FactJob {
+  OpDev op;
+  FactDev f;
+  cplx *sinv;
+};
+
+#define GJ_THREADS 512
+static const size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
+
+// D_k[i][c] of the block layout (i, c in-slab indices)
+__device__ __forceinline__ cplx d_entry(const FactJob &J, int k, int i, int c) {
+  const OpDev &o = J.op;
+  const FactDev &f = J.f;
+  int ba = f.block_axis;
+  if (f.other[1] < 0) {  // 2D: one in-slab axis
+    int oa = f.other[0];
+    if (c == i) {
+      int coord[3] = {0, 0, 0};
+      coord[ba] = k;
+      coord[oa] = i;
+      double k2;
+      if (o.kappa2_kind == 0) k2 = o.kappa2[0];
+      else if (o.kappa2_kind == 1) k2 = o.kappa2[coord[o.kappa2_axis]];
+      else k2 = o.kappa2[(int64_t)coord[0] * o.shape[1] + coord[1]];
+      cplx acc = make_double2(k2, 0.0);
+      for (int a = 0; a < 2; ++a) {
+        cplx lo = o.c_lo[a][coord[a]], hi = o.c_hi[a][coord[a]];
+        acc.x += -(lo.x + hi.x);
+        acc.y += -(lo.y + hi.y);
+      }
+      return acc;
+    }
+    if (c == i - 1) return o.c_lo[oa][i];
+    if (c == i + 1) return o.c_hi[oa][i];
+    return make_double2(0.0, 0.0);
+  }
+  // 3D: in-slab index i = i0 * n1 + i1 over axes other[0], other[1]
+  int o0 = f.other[0], o1 = f.other[1];
+  int n1 = f.win_shape[o1];
+  int i0 = i / n1, i1 = i % n1;
+  if (c == i) {
+    int coord[3];
+    coord[ba] = k;
+    coord[o0] = i0;
+    coord[o1] = i1;
+    double k2;
+    if (o.kappa2_kind == 0) k2 = o.kappa2[0];
+    else if (o.kappa2_kind == 1) k2 = o.kappa2[coord[o.kappa2_axis]];
+    else k2 = o.kappa2[((int64_t)coord[0] * o.shape[1] + coord[1]) * o.shape[2] + coord[2]];
+    cplx acc = make_double2(k2, 0.0);
+    for (int a = 0; a < 3; ++a) {
+      cplx lo = o.c_lo[a][coord[a]], hi = o.c_hi[a][coord[a]];
+      acc.x += -(lo.x + hi.x);
+      acc.y += -(lo.y + hi.y);
+    }
+    return acc;
+  }
+  if (c == i - 1 && i1 > 0) return o.c_lo[o1][i1];
+  if (c == i + 1 && i1 < n1 - 1) return o.c_hi[o1][i1];
+  if (c == i - n1) return o.c_lo[o0][i0];
+  if (c == i + n1) return o.c_hi[o0][i0];
+  return make_double2(0.0, 0.0);
+}
+
+__global__ void __launch_bounds__(GJ_THREADS, 1)
+    k_factor_gj(const FactJob *__restrict__ jobs, int mcper_max, int *status) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const FactJob &J = jobs[blockIdx.y];
+  const int m = J.f.m, nb = J.f.nb;
+  const int mcper = (m + C - 1) / C;
+  const int c0 = rank * mcper;
+  const int c1 = min(m, c0 + mcper);
+  const int mc = max(0, c1 - c0);
+  const int t = threadIdx.x, T = blockDim.x;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx *S = (cplx *)smem_raw;               // [m][mcper_max]
+  cplx *colj = S + (size_t)m * mcper_max;   // [2][m]
+  cplx *prow = colj + 2 * m;                // [mcper_max]
+  cplx *rowj_old = prow + mcper_max;        // [mcper_max]
+  int *piv = (int *)(rowj_old + mcper_max); // [m]
+  int *dst = piv + m;                       // [m]
+  __shared__ double red_v[GJ_THREADS / 32];
+  __shared__ int red_i[GJ_THREADS / 32];
+  __shared__ int s_bad;
+  if (t == 0) s_bad = 0;
+
+  const int ld = mcper_max;
+  const int ba = J.f.block_axis;
+  for (int k = 0; k < nb; ++k) {
+    // ---- S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1}  (my columns)
+    cplx lu = make_double2(0.0, 0.0);
+    if (k > 0) lu = cmul(J.op.c_lo[ba][k], J.op.c_hi[ba][k - 1]);
+    const cplx *prev = J.sinv + (size_t)(k > 0 ? k - 1 : 0) * m * m;
+    for (int e = t; e < m * mc; e += T) {
+      int i = e / mc, cc = e % mc, c = c0 + cc;
+      cplx v = d_entry(J, k, i, c);
+      if (k > 0) v = csub(v, cmul(lu, __ldcg(prev + (size_t)i * m + c)));
+      S[i * ld + cc] = v;
+    }
+    cluster.sync();
+    // ---- Gauss-Jordan inversion with partial pivoting
+    for (int j = 0; j < m; ++j) {
+      const int owner = j / mcper;
+      cplx *cj = colj + (j & 1) * m;
+      if (rank == owner) {
+        const int jj = j - c0;
+        double best = -1.0;
+        int bi = m;
+        for (int i = j + t; i < m; i += T) {
+          double v = cabs1(S[i * ld + jj]);
+          if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          double ov = __shfl_down_sync(0xffffffffu, best, off);
+          int oi = __shfl_down_sync(0xffffffffu, bi, off);
+          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+        }
+        if ((t & 31) == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bi; }
+        __syncthreads();
+        if (t == 0) {
+          double bv = red_v[0];
+          int bidx = red_i[0];
+          for (int w = 1; w < T / 32; ++w)
+            if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
+          red_i[0] = bidx;
+        }
+        __syncthreads();
+        const int p = red_i[0];
+        for (int q = 0; q < C; ++q) {
+          cplx *rc = cluster.map_shared_rank(cj, q);
+          int *rp = cluster.map_shared_rank(piv, q);
+          for (int i = t; i < m; i += T) rc[i] = S[i * ld + jj];
+          if (t == 0) rp[j] = p;
+        }
+      }
+      cluster.sync();
+      const int p = piv[j];
+      const cplx pivot = cj[p];
+      if (t == 0 && !(cabs1(pivot) > 0.0 && isfinite(pivot.x) && isfinite(pivot.y))) s_bad = 1;
+      const cplx inv = cinv(pivot);
+      for (int cc = t; cc < mc; cc += T) {
+        prow[cc] = cmul(S[p * ld + cc], inv);
+        rowj_old[cc] = S[j * ld + cc];
+      }
+      __syncthreads();
+      for (int e = t; e < m * mc; e += T) {
+        int i = e / mc, cc = e % mc, c = c0 + cc;
+        cplx fi = cj[i == j ? p : (i == p ? j : i)];
+        cplx nv;
+        if (c == j) {
+          nv = (i == j) ? inv : cmul(make_double2(-fi.x, -fi.y), inv);
+        } else if (i == j) {
+          nv = prow[cc];
+        } else {
+          cplx old = (i == p) ? rowj_old[cc] : S[i * ld + cc];
+          nv = csub(old, cmul(fi, prow[cc]));
+        }
+        S[i * ld + cc] = nv;
+      }
+      __syncthreads();
+    }
+    // ---- undo the column interchanges while storing S_k^{-1}
+    if (t == 0) {
+      for (int c = 0; c < m; ++c) dst[c] = c;  // dst used as src first
+      for (int j = m - 1; j >= 0; --j) {
+        int a = dst[j];
+        dst[j] = dst[piv[j]];
+        dst[piv[j]] = a;
+      }
+      // invert: src[c] -> dst[src[c]] = c ; reuse colj buffer (int view)
+      int *tmp = (int *)(colj);
+      for (int c = 0; c < m; ++c) tmp[dst[c]] = c;
+      for (int c = 0; c < m; ++c) dst[c] = tmp[c];
+    }
+    __syncthreads();
+    cplx *out = J.sinv + (size_t)k * m * m;
+    for (int e = t; e < m * mc; e += T) {
+      int i = e / mc, cc = e % mc;
+      out[(size_t)i * m + dst[c0 + cc]] = S[i * ld + cc];
+    }
+    cluster.sync();
+  }
+  if (t == 0 && s_bad) atomicExch(status, 1);
+}
+
+static int choose_cluster(int m, int *mcper_out, size_t *smem_out) {
+  for (int C = 1; C <= 8; C *= 2) {
+    int mcper = (m + C - 1) / C;
+    size_t smem = (size_t)m * mcper * sizeof(cplx) + 2 * (size_t)m * sizeof(cplx) +
+                  2 * (size_t)mcper * sizeof(cplx) + 2 * (size_t)m * sizeof(int);
+    if (smem <= kSmemLimit - 4096) {
+      *mcper_out = mcper;
+      *smem_out = smem;
+      return C;
+    }
+  }
+  return 0;
+}
+
+static void fill_layout(const OpDev &o, FactDev &f) {
+  int ba = 0;
+  for (int a = 1; a < o.dim; ++a)
+    if (o.shape[a] > o.shape[ba]) ba = a;
+  f.block_axis = ba;
+  f.nb = o.shape[ba];
+  f.m = 1;
+  f.other[0] = f.other[1] = -1;
+  int n = 0;
+  for (int a = 0; a < o.dim; ++a) {
+    f.win_shape[a] = o.shape[a];
+    if (a == ba) continue;
+    f.other[n++] = a;
+    f.m *= o.shape[a];
+  }
+  for (int a = o.dim; a < 3; ++a) f.win_shape[a] = 1;
+}
+
+extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact **out) {
+  if (!ctx || !ops || n < 1 || !out) return ds_fail(DS_ECONFIG, "ds_fact_create: bad argument");
+  ds_fact *F = new ds_fact();
+  std::vector<FactJob> jobs(n);
+  int maxm = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!ops[i]) {
+      delete F;
+      return ds_fail(DS_ECONFIG, "ds_fact_create: null operator");
+    }
+    const OpDev &o = ops[i]->dev;
+    FactDev f;
+    memset(&f, 0, sizeof(f));
+    fill_layout(o, f);
+    size_t bytes = (size_t)f.nb * f.m * f.m * sizeof(cplx) + 2 * (size_t)f.nb * sizeof(cplx);
+    void *mem = nullptr;
+    if (cudaMalloc(&mem, bytes) != cudaSuccess) {
+      for (void *p : F->allocations) cudaFree(p);
+      delete F;
+      return ds_fail(DS_ECUDA, "ds_fact_create: out of device memory for factors");
+    }
+    F->allocations.push_back(mem);
+    cplx *sinv = (cplx *)mem;
+    cplx *lc = sinv + (size_t)f.nb * f.m * f.m;
+    cplx *uc = lc + f.nb;
+    cudaMemcpy(lc, o.c_lo[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice);
+    cudaMemcpy(uc, o.c_hi[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice);
+    f.sinv = sinv;
+    f.lcoef = lc;
+    f.ucoef = uc;
+    F->facts.push_back(f);
+    F->bytes.push_back((int64_t)bytes);
+    F->bytes_total += bytes;
+    jobs[i].op = o;
+    jobs[i].f = f;
+    jobs[i].sinv = sinv;
+    maxm = std::max(maxm, f.m);
+  }
+  int mcper = 0;
+  size_t smem = 0;
+  int C = choose_cluster(maxm, &mcper, &smem);
+  if (C == 0) {
+    for (void *p : F->allocations) cudaFree(p);
+    delete F;
+    return ds_fail(DS_ECONFIG,
+                   "ds_fact_create: slab size m=" + std::to_string(maxm) +
+                       " exceeds the on-chip Gauss-Jordan path (3D windows need the "
+                       "blocked path)");
+  }
+  FactJob *djobs = nullptr;
+  int *dstatus = nullptr;
+  DS_CUDA(cudaMalloc(&djobs, n * sizeof(FactJob)));
+  DS_CUDA(cudaMalloc(&dstatus, sizeof(int)));
+  DS_CUDA(cudaMemcpy(djobs, jobs.data(), n * sizeof(FactJob), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemset(dstatus, 0, sizeof(int)));
+  DS_CUDA(cudaFuncSetAttribute(k_factor_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, n, 1);
+  cfg.blockDim = dim3(GJ_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_factor_gj, (const FactJob *)djobs, mcper, dstatus));
+  ctx->launches++;
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  int status = 0;
+  DS_CUDA(cudaMemcpy(&status, dstatus, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(djobs);
+  cudaFree(dstatus);
+  if (status) {
+    for (void *p : F->allocations) cudaFree(p);
+    delete F;
+    return ds_fail(DS_ESOLVER, "block LU: zero or non-finite pivot in a Schur complement");
+  }
+  *out = F;
+  return DS_OK;
+}
+
+extern "C" int ds_fact_info(const ds_fact *F, int32_t i, int32_t *ba, int32_t *nb, int32_t *m,
+                            int64_t *bytes) {
+  if (!F || i < 0 || i >= (int)F->facts.size()) return ds_fail(DS_ECONFIG, "ds_fact_info: bad index");
+  if (ba) *ba = F->facts[i].block_axis;
+  if (nb) *nb = F->facts[i].nb;
+  if (m) *m = F->facts[i].m;
+  if (bytes) *bytes = F->bytes[i];
+  return DS_OK;
+}
+
+extern "C" int ds_fact_destroy(ds_fact *F) {
+  if (!F) return DS_OK;
+  for (void *p : F->allocations) cudaFree(p);
+  delete F;
+  return DS_OK;
+}
+
+// window C-order [W][R]  <->  block layout [nb][m][R]
+__global__ void k_permute(FactDev f, const cplx *__restrict__ src, cplx *__restrict__ dst,
+                          int nrhs, int to_block) {
+  int64_t total = (int64_t)f.nb * f.m * nrhs;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int r = q % nrhs;
+    int64_t lin = q / nrhs;  // window C-order linear node
+    int c[3];
+    c[2] = lin % f.win_shape[2];
+    int64_t tt = lin / f.win_shape[2];
+    c[1] = tt % f.win_shape[1];
+    c[0] = tt / f.win_shape[1];
+    int64_t b = block_offset(f, c) * nrhs + r;
+    if (to_block) dst[b] = src[q];
+    else dst[q] = src[b];
+  }
+}
+
+
+extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_cplx *rhs,
+                             ds_cplx *x, int32_t nrhs) {
+  if (!ctx || !F || !rhs || !x || nrhs < 1 || i < 0 || i >= (int)F->facts.size())
+    return ds_fail(DS_ECONFIG, "ds_fact_solve: bad argument");
+  const FactDev &f = F->facts[i];
+  size_t n = (size_t)f.nb * f.m * nrhs;
+  cplx *tmp = nullptr;
+  void *vis = nullptr;
+  DS_CUDA(cudaMallocAsync((void **)&tmp, 2 * n * sizeof(cplx) + sizeof(FactDev) + 64, ctx->stream));
+  cplx *bin = tmp, *bout = tmp + n;
+  FactDev *fd = (FactDev *)(tmp + 2 * n);
+  DS_CUDA(cudaMallocAsync(&vis, sizeof(SolveVisit), ctx->stream));
+  SolveVisit hv{fd, bin, bout, nullptr};
+  DS_CUDA(cudaMemcpyAsync(fd, &f, sizeof(FactDev), cudaMemcpyHostToDevice, ctx->stream));
+  DS_CUDA(cudaMemcpyAsync(vis, &hv, sizeof(hv), cudaMemcpyHostToDevice, ctx->stream));
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);
+  k_permute<<<blocks, 256, 0, ctx->stream>>>(f, (const cplx *)rhs, bin, nrhs, 1);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  int rc = ds_launch_solve_table(ctx, vis, 1, nrhs, f.m);
+  if (rc) return rc;
+  k_permute<<<blocks, 256, 0, ctx->stream>>>(f, bout, (cplx *)x, nrhs, 0);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  DS_CUDA(cudaFreeAsync(tmp, ctx->stream));
+  DS_CUDA(cudaFreeAsync(vis, ctx->stream));
+  return DS_OK;
+}

@@ -1,0 +1,793 @@
+// The diagonal-sweeping engine: static plan tables, the per-step kernels
+// K6 (RHS assembly / restrict), K5 (beta00 accumulation), K4 (source
+// transfer) and the host loop that issues, per anti-diagonal step,
+//     assemble -> block solve (K3) -> accumulate -> transfer.
+//
+// Restates diagonal_sweep_solve (diagsweep/ddm.py:212-291):
+//  * restrict_source (ddm.py:168-195): breakpoint nodes go to the lower
+//    index, boundary subdomains own their collar (own window, host table);
+//  * local RHS = own source (sweep 1) + queued payloads (ddm.py:242-254);
+//    payloads live in per-(use sweep, target, direction) slots that the
+//    consumer zeroes after reading;
+//  * exact-zero flags and cut sets per (sweep, subdomain, RHS) evaluated on
+//    the device: has_own = any(src != 0) (ddm.py:248), nonzero = any(rhs)
+//    (ddm.py:256), solve_cuts = AND of arrival cuts unless has_own or no
+//    arrivals (ddm.py:96-100), emits (ddm.py:103-110), content_cuts
+//    (ddm.py:82-93) — cut bit (axis a, side s) = 1 << (2a + (s > 0));
+//  * _accumulate (ddm.py:206-209) with a fixed owner order where supports
+//    of same-step subdomains overlap (no atomics on field values);
+//  * psi (transfer.py:100-155): payload = s * (rhs|band + L_nb((w - 1) v)|band)
+//    with w = prod (1 - beta_a) on ext, evaluated node-wise with the
+//    neighbour operator's couplings, zero outside ext.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "ds_common.cuh"
+
+#define RMAX 256
+#define CUT_ALL 0x3f
+
+struct SubDev {
+  int win_lo[3], win_shape[3];
+  int own_lo[3], own_shape[3];
+  int sup_lo[3], sup_shape[3];
+  const double *beta[3];
+  const FactDev *f;
+  const OpDev *op;
+};
+
+struct SlotRef {
+  cplx *data;
+  int lo[3], shape[3];
+};
+
+struct VisitDev {
+  int sub, sweep, nslot, slot0;
+  cplx *rhs, *x;
+  int *nz;
+};
+
+struct XferDev {
+  int vidx;  // global visit index of the source visit
+  int src, dst, use;
+  int dirmask, content_base, keepmask;
+  double sign;
+  int band_lo[3], band_shape[3];
+  int ext_lo[3], ext_shape[3];
+  const double *fac[3];
+  cplx *slot;
+};
+
+struct ds_plan {
+  ds_ctx *ctx;
+  int dim, nsub, nsweeps, nsteps, ndir, nrhs_max, gmax, max_m, max_w;
+  int gcounts[3];
+  int64_t nnodes;
+  std::vector<int> vstep_off, xstep_off;  // host copies, size nsweeps*nsteps+1
+  // device tables
+  SubDev *subs = nullptr;
+  VisitDev *visits = nullptr;
+  SolveVisit *solvetab = nullptr;
+  SlotRef *slots = nullptr;
+  XferDev *xfers = nullptr;
+  FactDev *facts = nullptr;
+  OpDev *ops = nullptr;
+  // flags [nsweeps][nsub][nrhs] (stride = nrhs of the call)
+  int *flags = nullptr;  // own_nz | nz | arr_cnt | arr_cut | emit_cnt | discard
+  size_t flag_words = 0;
+  std::vector<void *> allocs;
+  int64_t workspace = 0;
+  int64_t last_launches = 0;
+  bool slots_dirty = false;
+  std::vector<std::pair<cplx *, size_t>> slot_bufs;  // for re-zeroing
+  // host copies of the visit tables; nz pointers are patched per nrhs stride
+  std::vector<VisitDev> h_visits;
+  std::vector<SolveVisit> h_solve;
+  int patched_nrhs = 0;
+  // graph
+  bool use_graph = false;
+  cudaGraphExec_t graph = nullptr;
+  const void *graph_f = nullptr;
+  void *graph_u = nullptr;
+  void *graph_partials = nullptr;
+  int graph_nrhs = 0;
+};
+
+static int plan_alloc(ds_plan *P, void **ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(ptr, bytes) != cudaSuccess)
+    return ds_fail(DS_ECUDA, "ds_plan_create: out of device memory (" + std::to_string(bytes) +
+                                 " bytes)");
+  P->allocs.push_back(*ptr);
+  P->workspace += bytes;
+  return DS_OK;
+}
+
+// -------------------------------------------------------------- helpers
+
+__device__ __forceinline__ bool in_box(const int *g, const int *lo, const int *shape, int dim) {
+  for (int a = 0; a < dim; ++a)
+    if (g[a] < lo[a] || g[a] >= lo[a] + shape[a]) return false;
+  return true;
+}
+
+__device__ __forceinline__ int64_t lin_of(const int *e, const int *shape, int dim) {
+  int64_t l = e[0];
+  for (int a = 1; a < dim; ++a) l = l * shape[a] + e[a];
+  return l;
+}
+
+__device__ __forceinline__ void unlin(int64_t l, const int *shape, int dim, int *e) {
+  for (int a = dim - 1; a >= 1; --a) {
+    e[a] = (int)(l % shape[a]);
+    l /= shape[a];
+  }
+  e[0] = (int)l;
+}
+
+// block layout offset -> window-local coordinates
+__device__ __forceinline__ void block_coords(const FactDev &f, int64_t blk, int *c) {
+  int k = (int)(blk / f.m), i = (int)(blk % f.m);
+  c[0] = c[1] = c[2] = 0;
+  c[f.block_axis] = k;
+  if (f.other[1] < 0) {
+    c[f.other[0]] = i;
+  } else {
+    int n1 = f.win_shape[f.other[1]];
+    c[f.other[0]] = i / n1;
+    c[f.other[1]] = i % n1;
+  }
+}
+
+// flags layout helpers (stride nrhs)
+struct Flags {
+  int *own_nz;    // [nsub][R]
+  int *nz;        // [nsweeps][nsub][R]
+  int *arr_cnt;   // [nsweeps][nsub][R]
+  int *arr_cut;   // [nsweeps][nsub][R]
+  int *emit_cnt;  // [nsweeps][nsub][R]
+  int *discard;   // [R]
+};
+
+static Flags flags_view(ds_plan *P, int nrhs) {
+  Flags F;
+  size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
+  F.own_nz = P->flags;
+  F.nz = F.own_nz + (size_t)P->nsub * nrhs;
+  F.arr_cnt = F.nz + per;
+  F.arr_cut = F.arr_cnt + per;
+  F.emit_cnt = F.arr_cut + per;
+  F.discard = F.emit_cnt + per;
+  return F;
+}
+
+__device__ __forceinline__ int solve_cut(const Flags &F, int sweep, int sub, int nsub, int r,
+                                         int nrhs) {
+  size_t vi = ((size_t)(sweep - 1) * nsub + sub) * nrhs + r;
+  if (sweep == 1 && F.own_nz[(size_t)sub * nrhs + r]) return 0;
+  if (F.arr_cnt[vi] == 0) return 0;
+  return F.arr_cut[vi] & CUT_ALL;
+}
+
+// ------------------------------------------------------------- K6 assemble
+__global__ void k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
+                           const SlotRef *__restrict__ slots, const cplx *__restrict__ f,
+                           int nrhs, int dim, int g0, int g1, int g2, Flags F) {
+  __shared__ int s_nz[RMAX], s_own[RMAX];
+  const VisitDev V = visits[blockIdx.y];
+  const SubDev &sd = subs[V.sub];
+  const FactDev fd = *sd.f;
+  for (int r = threadIdx.x; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
+  __syncthreads();
+  const int gc[3] = {g0, g1, g2};
+  const int64_t total = (int64_t)fd.nb * fd.m * nrhs;
+  const bool own = V.sweep == 1;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(q % nrhs);
+    int c[3];
+    block_coords(fd, q / nrhs, c);
+    int g[3];
+    for (int a = 0; a < 3; ++a) g[a] = sd.win_lo[a] + c[a];
+    cplx val = make_double2(0.0, 0.0);
+    if (own && in_box(g, sd.own_lo, sd.own_shape, dim)) {
+      cplx s = f[lin_of(g, gc, dim) * nrhs + r];
+      val = cadd(val, s);
+      if (cnonzero(s)) s_own[r] = 1;
+    }
+    for (int k = 0; k < V.nslot; ++k) {
+      const SlotRef &S = slots[V.slot0 + k];
+      if (!in_box(g, S.lo, S.shape, dim)) continue;
+      int e[3];
+      for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
+      int64_t idx = lin_of(e, S.shape, dim) * nrhs + r;
+      val = cadd(val, S.data[idx]);
+      S.data[idx] = make_double2(0.0, 0.0);
+    }
+    V.rhs[q] = val;
+    if (cnonzero(val)) s_nz[r] = 1;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
+    if (s_nz[r]) atomicOr(&V.nz[r], 1);
+    if (s_own[r]) atomicOr(&F.own_nz[(size_t)V.sub * nrhs + r], 1);
+  }
+}
+
+// ----------------------------------------------------------- K5 accumulate
+__global__ void k_accumulate(const VisitDev *__restrict__ visits, int G,
+                             const SubDev *__restrict__ subs, cplx *u, int nrhs, int dim, int g0,
+                             int g1, int g2) {
+  const int v = blockIdx.y;
+  const SubDev &sd = subs[visits[v].sub];
+  const int gc[3] = {g0, g1, g2};
+  int64_t nodes = (int64_t)sd.sup_shape[0] * sd.sup_shape[1] * (dim == 3 ? sd.sup_shape[2] : 1);
+  const int64_t total = nodes * nrhs;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(q % nrhs);
+    int e[3] = {0, 0, 0};
+    unlin(q / nrhs, sd.sup_shape, dim, e);
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) g[a] = sd.sup_lo[a] + e[a];
+    bool owner = true;
+    for (int w = 0; w < v && owner; ++w)
+      if (in_box(g, subs[visits[w].sub].sup_lo, subs[visits[w].sub].sup_shape, dim)) owner = false;
+    if (!owner) continue;
+    int64_t gi = lin_of(g, gc, dim) * nrhs + r;
+    cplx acc = u[gi];
+    bool touched = false;
+    for (int w = v; w < G; ++w) {
+      const VisitDev &W = visits[w];
+      const SubDev &sw = subs[W.sub];
+      if (w != v && !in_box(g, sw.sup_lo, sw.sup_shape, dim)) continue;
+      if (!W.nz[r]) continue;
+      double beta = 1.0;
+      for (int a = 0; a < dim; ++a) beta = beta * sw.beta[a][g[a] - sw.sup_lo[a]];
+      int c[3] = {0, 0, 0};
+      for (int a = 0; a < dim; ++a) c[a] = g[a] - sw.win_lo[a];
+      cplx xv = W.x[block_offset(*sw.f, c) * nrhs + r];
+      acc = cadd(acc, cscale(xv, beta));
+      touched = true;
+    }
+    if (touched) u[gi] = acc;
+  }
+}
+
+// ------------------------------------------------------------ K4 transfer
+__device__ __forceinline__ double op_k2(const OpDev &o, const int *c) {
+  if (o.kappa2_kind == 0) return o.kappa2[0];
+  if (o.kappa2_kind == 1) return o.kappa2[c[o.kappa2_axis]];
+  int64_t lin = c[0];
+  for (int a = 1; a < o.dim; ++a) lin = lin * o.shape[a] + c[a];
+  return o.kappa2[lin];
+}
+
+__global__ void k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
+                           const SubDev *__restrict__ subs, int nsub, int sweep, int nrhs, int dim,
+                           Flags F) {
+  const XferDev &X = xfers[blockIdx.y];
+  const VisitDev &V = visits[X.vidx];
+  // bookkeeping (ddm.py:262-279): one thread per RHS in block 0
+  if (blockIdx.x == 0) {
+    for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
+      if (!V.nz[r]) continue;
+      int cut = solve_cut(F, sweep, X.src, nsub, r, nrhs);
+      if (cut & X.dirmask) continue;
+      if (X.use == 0) {
+        atomicAdd(&F.discard[r], 1);
+      } else {
+        size_t ti = ((size_t)(X.use - 1) * nsub + X.dst) * nrhs + r;
+        atomicAdd(&F.arr_cnt[ti], 1);
+        atomicAnd(&F.arr_cut[ti], X.content_base | (cut & X.keepmask));
+        atomicAdd(&F.emit_cnt[((size_t)(sweep - 1) * nsub + X.src) * nrhs + r], 1);
+      }
+    }
+  }
+  if (X.use == 0) return;
+  const SubDev &ss = subs[X.src];
+  const SubDev &sn = subs[X.dst];
+  const FactDev fs = *ss.f;
+  const OpDev &on = *sn.op;
+  int64_t nodes = (int64_t)X.band_shape[0] * X.band_shape[1] * (dim == 3 ? X.band_shape[2] : 1);
+  const int64_t total = nodes * nrhs;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int r = (int)(q % nrhs);
+    if (!V.nz[r]) continue;
+    int cut = solve_cut(F, sweep, X.src, nsub, r, nrhs);
+    if (cut & X.dirmask) continue;
+    int e[3] = {0, 0, 0};
+    unlin(q / nrhs, X.band_shape, dim, e);
+    int g[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) g[a] = X.band_lo[a] + e[a];
+    // w(p) = (prod_a fac_a - 1) * v(p) on ext
+    auto wval = [&](const int *p) -> cplx {
+      double wt = 1.0;
+      for (int a = 0; a < dim; ++a) wt = wt * X.fac[a][p[a] - X.ext_lo[a]];
+      int c[3] = {0, 0, 0};
+      for (int a = 0; a < dim; ++a) c[a] = p[a] - ss.win_lo[a];
+      cplx v = V.x[block_offset(fs, c) * nrhs + r];
+      return cscale(v, wt - 1.0);
+    };
+    int cn[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) cn[a] = g[a] - sn.win_lo[a];
+    cplx w0 = wval(g);
+    cplx acc = cscale(w0, op_k2(on, cn));
+    for (int a = 0; a < dim; ++a) {
+      cplx lo = on.c_lo[a][cn[a]], hi = on.c_hi[a][cn[a]];
+      acc = cadd(acc, cmul(make_double2(-(lo.x + hi.x), -(lo.y + hi.y)), w0));
+      if (g[a] - 1 >= X.ext_lo[a]) {
+        int p[3] = {g[0], g[1], g[2]};
+        p[a] -= 1;
+        acc = cadd(acc, cmul(lo, wval(p)));
+      }
+      if (g[a] + 1 < X.ext_lo[a] + X.ext_shape[a]) {
+        int p[3] = {g[0], g[1], g[2]};
+        p[a] += 1;
+        acc = cadd(acc, cmul(hi, wval(p)));
+      }
+    }
+    int cs[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) cs[a] = g[a] - ss.win_lo[a];
+    cplx rv = V.rhs[block_offset(fs, cs) * nrhs + r];
+    cplx pay = cscale(cadd(rv, acc), X.sign);
+    int64_t si = (nodes == 0 ? 0 : (q / nrhs)) * nrhs + r;
+    X.slot[si] = cadd(X.slot[si], pay);
+  }
+}
+
+// ------------------------------------------------------------ plan create
+
+extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out) {
+  if (!ctx || !d || !out) return ds_fail(DS_ECONFIG, "ds_plan_create: null argument");
+  if (d->dim != 2 && d->dim != 3) return ds_fail(DS_ECONFIG, "plan dim must be 2 or 3");
+  if (d->nrhs_max < 1 || d->nrhs_max > RMAX)
+    return ds_fail(DS_ECONFIG, "nrhs_max must be in [1, 256]");
+  if (!d->fact_of_sub || !d->fact_index) return ds_fail(DS_ECONFIG, "plan needs factorizations");
+  const int dim = d->dim, nsub = d->nsub, nsw = d->nsweeps, nst = d->nsteps, ndir = d->ndir;
+  ds_plan *P = new ds_plan();
+  P->ctx = ctx;
+  P->dim = dim;
+  P->nsub = nsub;
+  P->nsweeps = nsw;
+  P->nsteps = nst;
+  P->ndir = ndir;
+  P->nrhs_max = d->nrhs_max;
+  P->nnodes = 1;
+  for (int a = 0; a < 3; ++a) {
+    P->gcounts[a] = a < dim ? d->grid_counts[a] : 1;
+    P->nnodes *= P->gcounts[a];
+  }
+  auto fail = [&](int code) {
+    for (void *p : P->allocs) cudaFree(p);
+    delete P;
+    return code;
+  };
+  // ---- operators and factor layouts in device memory
+  void *mem;
+  if (plan_alloc(P, &mem, sizeof(OpDev) * d->nops)) return fail(DS_ECUDA);
+  P->ops = (OpDev *)mem;
+  {
+    std::vector<OpDev> h(d->nops);
+    for (int i = 0; i < d->nops; ++i) h[i] = d->ops[i]->dev;
+    cudaMemcpy(P->ops, h.data(), sizeof(OpDev) * d->nops, cudaMemcpyHostToDevice);
+  }
+  // factor layout of every subdomain (device table, one entry per subdomain)
+  std::vector<FactDev> hf(nsub);
+  for (int s = 0; s < nsub; ++s) {
+    const ds_fact *FA = d->fact_of_sub[s];
+    int fi = d->fact_index[s];
+    if (!FA || fi < 0 || fi >= (int)FA->facts.size())
+      return fail(ds_fail(DS_ECONFIG, "bad factorization handle/index for a subdomain"));
+    hf[s] = FA->facts[fi];
+  }
+  if (plan_alloc(P, &mem, sizeof(FactDev) * nsub)) return fail(DS_ECUDA);
+  P->facts = (FactDev *)mem;
+  cudaMemcpy(P->facts, hf.data(), sizeof(FactDev) * nsub, cudaMemcpyHostToDevice);
+  // ---- beta00 ramps
+  int64_t nbeta = 0;
+  for (int s = 0; s < nsub; ++s)
+    for (int a = 0; a < dim; ++a)
+      nbeta = std::max<int64_t>(nbeta, d->beta00_off[s * 3 + a] + d->sup_shape[s * 3 + a]);
+  double *dbeta;
+  if (plan_alloc(P, &mem, sizeof(double) * nbeta)) return fail(DS_ECUDA);
+  dbeta = (double *)mem;
+  cudaMemcpy(dbeta, d->beta00, sizeof(double) * nbeta, cudaMemcpyHostToDevice);
+  // ---- subdomains
+  std::vector<SubDev> hs(nsub);
+  int max_w = 0;
+  P->max_m = 0;
+  for (int s = 0; s < nsub; ++s) {
+    SubDev &S = hs[s];
+    memset(&S, 0, sizeof(S));
+    int oi = d->op_of_sub[s];
+    if (oi < 0 || oi >= d->nops) return fail(ds_fail(DS_ECONFIG, "bad operator index"));
+    const FactDev &fd = hf[s];
+    int64_t wn = 1;
+    for (int a = 0; a < 3; ++a) {
+      bool ok = a < dim;
+      S.win_lo[a] = ok ? d->win_lo[s * 3 + a] : 0;
+      S.win_shape[a] = ok ? d->win_shape[s * 3 + a] : 1;
+      S.own_lo[a] = ok ? d->own_lo[s * 3 + a] : 0;
+      S.own_shape[a] = ok ? d->own_shape[s * 3 + a] : 1;
+      S.sup_lo[a] = ok ? d->sup_lo[s * 3 + a] : 0;
+      S.sup_shape[a] = ok ? d->sup_shape[s * 3 + a] : 1;
+      S.beta[a] = ok ? dbeta + d->beta00_off[s * 3 + a] : nullptr;
+      if (ok && S.win_shape[a] != fd.win_shape[a])
+        return fail(ds_fail(DS_ECONFIG, "window shape does not match its factorization"));
+      wn *= S.win_shape[a];
+    }
+    S.f = P->facts + s;
+    S.op = P->ops + oi;
+    max_w = std::max<int>(max_w, (int)wn);
+    P->max_w = max_w;
+    P->max_m = std::max(P->max_m, fd.m);
+  }
+  if (plan_alloc(P, &mem, sizeof(SubDev) * nsub)) return fail(DS_ECUDA);
+  P->subs = (SubDev *)mem;
+  cudaMemcpy(P->subs, hs.data(), sizeof(SubDev) * nsub, cudaMemcpyHostToDevice);
+  // ---- steps and visit buffers
+  P->gmax = 0;
+  for (int w = 0; w < nsw; ++w)
+    for (int t = 0; t < nst; ++t)
+      P->gmax = std::max(P->gmax, d->step_off[w * (nst + 1) + t + 1] - d->step_off[w * (nst + 1) + t]);
+  size_t vbuf = (size_t)max_w * d->nrhs_max;
+  cplx *bufs;
+  if (plan_alloc(P, &mem, sizeof(cplx) * vbuf * 2 * 2 * P->gmax)) return fail(DS_ECUDA);
+  bufs = (cplx *)mem;
+  // ---- flags
+  P->flag_words = (size_t)nsub * d->nrhs_max + 4 * (size_t)nsw * nsub * d->nrhs_max + d->nrhs_max;
+  if (plan_alloc(P, &mem, sizeof(int) * P->flag_words)) return fail(DS_ECUDA);
+  P->flags = (int *)mem;
+  // ---- payload slots keyed (use, target, direction)
+  std::map<std::tuple<int, int, int>, int> slot_id;
+  std::vector<SlotRef> hslots;
+  std::vector<std::vector<int>> slots_of_visit((size_t)nsw * nsub);
+  std::vector<int> slot_src_key;  // (s, k) that defines the band
+  auto dir_of = [&](int k, int a) { return d->directions[k * 3 + a]; };
+  auto sub_coords = [&](int s, int *idx) {
+    int rem = s;
+    for (int a = dim - 1; a >= 0; --a) {
+      idx[a] = rem % d->part_counts[a];
+      rem /= d->part_counts[a];
+    }
+  };
+  auto sub_linear = [&](const int *idx) {
+    int l = 0;
+    for (int a = 0; a < dim; ++a) l = l * d->part_counts[a] + idx[a];
+    return l;
+  };
+  size_t slot_elems = 0;
+  std::vector<size_t> slot_off;
+  for (int w = 0; w < nsw; ++w)
+    for (int s = 0; s < nsub; ++s)
+      for (int k = 0; k < ndir; ++k) {
+        int use = d->xfer_use[((size_t)w * nsub + s) * ndir + k];
+        if (use < 1) continue;
+        int idx[3];
+        sub_coords(s, idx);
+        for (int a = 0; a < dim; ++a) idx[a] += dir_of(k, a);
+        int dst = sub_linear(idx);
+        auto key = std::make_tuple(use - 1, dst, k);
+        if (slot_id.count(key)) continue;
+        int id = (int)hslots.size();
+        slot_id[key] = id;
+        SlotRef R;
+        memset(&R, 0, sizeof(R));
+        int64_t n = 1;
+        for (int a = 0; a < 3; ++a) {
+          bool ok = a < dim;
+          R.lo[a] = ok ? d->band_lo[((size_t)s * ndir + k) * 3 + a] : 0;
+          R.shape[a] = ok ? d->band_shape[((size_t)s * ndir + k) * 3 + a] : 1;
+          n *= R.shape[a];
+        }
+        slot_off.push_back(slot_elems);
+        slot_elems += n * d->nrhs_max;
+        hslots.push_back(R);
+        slots_of_visit[(size_t)(use - 1) * nsub + dst].push_back(id);
+      }
+  cplx *slotmem;
+  if (plan_alloc(P, &mem, sizeof(cplx) * std::max<size_t>(slot_elems, 1))) return fail(DS_ECUDA);
+  slotmem = (cplx *)mem;
+  cudaMemset(slotmem, 0, sizeof(cplx) * std::max<size_t>(slot_elems, 1));
+  P->slot_bufs.push_back({slotmem, sizeof(cplx) * std::max<size_t>(slot_elems, 1)});
+  for (size_t i = 0; i < hslots.size(); ++i) hslots[i].data = slotmem + slot_off[i];
+  // slot table ordered per visit (contiguous ranges)
+  std::vector<SlotRef> hslot_tab;
+  // ---- transfer (1 - beta) factors on ext
+  int64_t nfac = 0;
+  for (int s = 0; s < nsub; ++s)
+    for (int k = 0; k < ndir; ++k)
+      for (int a = 0; a < dim; ++a) {
+        size_t o = ((size_t)s * ndir + k) * 3 + a;
+        if (d->ext_shape[o] > 0) nfac = std::max<int64_t>(nfac, d->xfac_off[o] + d->ext_shape[o]);
+      }
+  double *dfac;
+  if (plan_alloc(P, &mem, sizeof(double) * std::max<int64_t>(nfac, 1))) return fail(DS_ECUDA);
+  dfac = (double *)mem;
+  if (nfac) cudaMemcpy(dfac, d->xfac, sizeof(double) * nfac, cudaMemcpyHostToDevice);
+  // ---- visits in execution order
+  std::vector<VisitDev> hv;
+  std::vector<SolveVisit> hsv;
+  std::vector<XferDev> hx;
+  P->vstep_off.assign((size_t)nsw * nst + 1, 0);
+  P->xstep_off.assign((size_t)nsw * nst + 1, 0);
+  std::vector<int> visit_of((size_t)nsw * nsub, -1);
+  int step_global = 0;
+  for (int w = 0; w < nsw; ++w) {
+    for (int t = 0; t < nst; ++t, ++step_global) {
+      int b = d->step_off[w * (nst + 1) + t], e = d->step_off[w * (nst + 1) + t + 1];
+      P->vstep_off[step_global] = (int)hv.size();
+      int parity = step_global & 1;
+      for (int g = b; g < e; ++g) {
+        int s = d->visit_sub[(size_t)w * nsub + g];
+        VisitDev V;
+        memset(&V, 0, sizeof(V));
+        V.sub = s;
+        V.sweep = w + 1;
+        V.slot0 = (int)hslot_tab.size();
+        for (int id : slots_of_visit[(size_t)w * nsub + s]) hslot_tab.push_back(hslots[id]);
+        V.nslot = (int)hslot_tab.size() - V.slot0;
+        int gi = g - b;
+        V.rhs = bufs + ((size_t)(parity * 2 + 0) * P->gmax + gi) * vbuf;
+        V.x = bufs + ((size_t)(parity * 2 + 1) * P->gmax + gi) * vbuf;
+        V.nz = nullptr;  // set per call (depends on nrhs stride)
+        visit_of[(size_t)w * nsub + s] = (int)hv.size();
+        hv.push_back(V);
+        SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr};
+        hsv.push_back(SV);
+      }
+      P->xstep_off[step_global] = (int)hx.size();
+      for (int g = b; g < e; ++g) {
+        int s = d->visit_sub[(size_t)w * nsub + g];
+        for (int k = 0; k < ndir; ++k) {
+          int use = d->xfer_use[((size_t)w * nsub + s) * ndir + k];
+          if (use < 0) continue;  // target out of range: psi returns None
+          XferDev X;
+          memset(&X, 0, sizeof(X));
+          X.vidx = visit_of[(size_t)w * nsub + s];
+          X.src = s;
+          int idx[3];
+          sub_coords(s, idx);
+          for (int a = 0; a < dim; ++a) idx[a] += dir_of(k, a);
+          X.dst = sub_linear(idx);
+          X.use = use;
+          int order = 0;
+          for (int a = 0; a < dim; ++a) {
+            int c = dir_of(k, a);
+            if (c) {
+              order++;
+              X.dirmask |= 1 << (2 * a + (c > 0));
+              X.content_base |= 1 << (2 * a + (-c > 0));
+            } else {
+              X.keepmask |= 3 << (2 * a);
+            }
+          }
+          X.sign = (order % 2 == 1) ? 1.0 : -1.0;
+          for (int a = 0; a < 3; ++a) {
+            bool ok = a < dim;
+            size_t o = ((size_t)s * ndir + k) * 3 + a;
+            X.band_lo[a] = ok ? d->band_lo[o] : 0;
+            X.band_shape[a] = ok ? d->band_shape[o] : 1;
+            X.ext_lo[a] = ok ? d->ext_lo[o] : 0;
+            X.ext_shape[a] = ok ? d->ext_shape[o] : 1;
+          }
+          for (int a = 0; a < dim; ++a)
+            X.fac[a] = dfac + d->xfac_off[((size_t)s * ndir + k) * 3 + a];
+          X.slot = nullptr;
+          if (use > 0) X.slot = hslots[slot_id[std::make_tuple(use - 1, X.dst, k)]].data;
+          hx.push_back(X);
+        }
+      }
+    }
+  }
+  P->vstep_off[step_global] = (int)hv.size();
+  P->xstep_off[step_global] = (int)hx.size();
+  // upload tables
+  if (plan_alloc(P, &mem, sizeof(SlotRef) * std::max<size_t>(hslot_tab.size(), 1))) return fail(DS_ECUDA);
+  P->slots = (SlotRef *)mem;
+  cudaMemcpy(P->slots, hslot_tab.data(), sizeof(SlotRef) * hslot_tab.size(), cudaMemcpyHostToDevice);
+  if (plan_alloc(P, &mem, sizeof(VisitDev) * hv.size())) return fail(DS_ECUDA);
+  P->visits = (VisitDev *)mem;
+  if (plan_alloc(P, &mem, sizeof(SolveVisit) * hsv.size())) return fail(DS_ECUDA);
+  P->solvetab = (SolveVisit *)mem;
+  if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
+  P->xfers = (XferDev *)mem;
+  cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice);
+  P->h_visits = hv;
+  P->h_solve = hsv;
+  P->patched_nrhs = 0;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess)
+    return fail(ds_fail(DS_ECUDA, std::string("ds_plan_create: ") + cudaGetErrorString(err)));
+  *out = P;
+  return DS_OK;
+}
+
+extern "C" int64_t ds_plan_workspace_bytes(const ds_plan *P) { return P ? P->workspace : -1; }
+extern "C" int64_t ds_plan_last_launches(const ds_plan *P) { return P ? P->last_launches : -1; }
+
+extern "C" int ds_plan_destroy(ds_plan *P) {
+  if (!P) return DS_OK;
+  if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (void *p : P->allocs) cudaFree(p);
+  delete P;
+  return DS_OK;
+}
+
+// point the per-visit nz flags at the [sweep][sub][nrhs] table of this stride
+static int patch_tables(ds_plan *P, int nrhs) {
+  if (P->patched_nrhs == nrhs) return DS_OK;
+  Flags F = flags_view(P, nrhs);
+  for (size_t i = 0; i < P->h_visits.size(); ++i) {
+    VisitDev &V = P->h_visits[i];
+    V.nz = F.nz + ((size_t)(V.sweep - 1) * P->nsub + V.sub) * nrhs;
+    P->h_solve[i].nz = V.nz;
+  }
+  DS_CUDA(cudaMemcpyAsync(P->visits, P->h_visits.data(), sizeof(VisitDev) * P->h_visits.size(),
+                          cudaMemcpyHostToDevice, P->ctx->stream));
+  DS_CUDA(cudaMemcpyAsync(P->solvetab, P->h_solve.data(), sizeof(SolveVisit) * P->h_solve.size(),
+                          cudaMemcpyHostToDevice, P->ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(P->ctx->stream));
+  P->patched_nrhs = nrhs;
+  if (P->graph) {
+    cudaGraphExecDestroy(P->graph);
+    P->graph = nullptr;
+  }
+  return DS_OK;
+}
+
+static int blocks_for(ds_ctx *ctx, int64_t work, int per_visit_cap) {
+  int64_t b = (work + 255) / 256;
+  if (b > per_visit_cap) b = per_visit_cap;
+  if (b < 1) b = 1;
+  (void)ctx;
+  return (int)b;
+}
+
+// issue the whole application on ctx->stream (capturable)
+static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials) {
+  ds_ctx *ctx = P->ctx;
+  cudaStream_t st = ctx->stream;
+  const int dim = P->dim;
+  Flags F = flags_view(P, nrhs);
+  int64_t launches0 = ctx->launches;
+  size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
+  DS_CUDA(cudaMemsetAsync(u, 0, sizeof(cplx) * P->nnodes * nrhs, st));
+  DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
+  DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
+  DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
+  const int cap = std::max(1, ctx->num_sms * 4);
+  for (int w = 0; w < P->nsweeps; ++w) {
+    for (int t = 0; t < P->nsteps; ++t) {
+      int q = w * P->nsteps + t;
+      int v0 = P->vstep_off[q], G = P->vstep_off[q + 1] - v0;
+      if (G == 0) continue;
+      const int64_t wmax = P->max_w, smax = P->max_w;
+      int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
+      k_assemble<<<dim3(bx, G), 256, 0, st>>>(P->visits + v0, P->subs, P->slots, f, nrhs, dim,
+                                              P->gcounts[0], P->gcounts[1], P->gcounts[2], F);
+      ctx->launches++;
+      DS_CHECK_LAUNCH();
+      int rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
+      if (rc) return rc;
+      DS_CHECK_LAUNCH();
+      int by = blocks_for(ctx, smax * nrhs / 4, std::max(1, cap / G));
+      k_accumulate<<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
+                                                P->gcounts[0], P->gcounts[1], P->gcounts[2]);
+      ctx->launches++;
+      DS_CHECK_LAUNCH();
+      int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
+      if (nx > 0) {
+        int bz = std::max(1, std::min(64, cap / nx));
+        k_transfer<<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, w + 1,
+                                                 nrhs, dim, F);
+        ctx->launches++;
+        DS_CHECK_LAUNCH();
+      }
+    }
+    if (partials)
+      DS_CUDA(cudaMemcpyAsync(partials + (size_t)w * P->nnodes * nrhs, u,
+                              sizeof(cplx) * P->nnodes * nrhs, cudaMemcpyDeviceToDevice, st));
+  }
+  P->last_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
+extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u, int32_t nrhs,
+                            ds_cplx *partials) {
+  if (!ctx || !P || !f || !u) return ds_fail(DS_ECONFIG, "ds_ddm_apply: null argument");
+  if (nrhs < 1 || nrhs > P->nrhs_max)
+    return ds_fail(DS_ECONFIG, "ds_ddm_apply: nrhs exceeds the plan's nrhs_max");
+  if (ctx != P->ctx) P->ctx = ctx;
+  int rc = patch_tables(P, nrhs);
+  if (rc) return rc;
+  if (P->slots_dirty) {
+    for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
+    P->slots_dirty = false;
+  }
+  if (P->use_graph) {
+    bool match = P->graph && P->graph_f == f && P->graph_u == u && P->graph_nrhs == nrhs &&
+                 P->graph_partials == partials;
+    if (!match) {
+      if (P->graph) {
+        cudaGraphExecDestroy(P->graph);
+        P->graph = nullptr;
+      }
+      cudaGraph_t g;
+      DS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      int64_t l0 = ctx->launches;
+      rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
+      cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+      if (rc) {
+        P->slots_dirty = true;
+        return rc;
+      }
+      if (e != cudaSuccess) return ds_fail(DS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+      DS_CUDA(cudaGraphInstantiate(&P->graph, g, 0));
+      cudaGraphDestroy(g);
+      P->graph_f = f;
+      P->graph_u = u;
+      P->graph_nrhs = nrhs;
+      P->graph_partials = partials;
+      ctx->launches = l0;
+    }
+    DS_CUDA(cudaGraphLaunch(P->graph, ctx->stream));
+    ctx->launches += P->last_launches;
+    return DS_OK;
+  }
+  rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
+  if (rc) P->slots_dirty = true;
+  return rc;
+}
+
+extern "C" int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *P, int32_t enable) {
+  if (!P) return ds_fail(DS_ECONFIG, "null plan");
+  (void)ctx;
+  P->use_graph = enable != 0;
+  if (!P->use_graph && P->graph) {
+    cudaGraphExecDestroy(P->graph);
+    P->graph = nullptr;
+  }
+  return DS_OK;
+}
+
+extern "C" int ds_ddm_counters(ds_ctx *ctx, ds_plan *P, int32_t nrhs, int32_t *nonzero,
+                               int32_t *discarded, int32_t *visit_nonzero,
+                               int32_t *visit_consumed, int32_t *visit_emitted,
+                               int32_t *visit_cut) {
+  if (!ctx || !P || nrhs < 1 || nrhs > P->nrhs_max)
+    return ds_fail(DS_ECONFIG, "ds_ddm_counters: bad argument");
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  Flags F = flags_view(P, nrhs);
+  size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
+  std::vector<int> nz(per), cnt, em;
+  DS_CUDA(cudaMemcpy(nz.data(), F.nz, sizeof(int) * per, cudaMemcpyDeviceToHost));
+  if (nonzero) {
+    for (int r = 0; r < nrhs; ++r) nonzero[r] = 0;
+    for (size_t i = 0; i < per; ++i) nonzero[i % nrhs] += nz[i] ? 1 : 0;
+  }
+  if (discarded) DS_CUDA(cudaMemcpy(discarded, F.discard, sizeof(int) * nrhs, cudaMemcpyDeviceToHost));
+  if (visit_nonzero)
+    for (size_t i = 0; i < per; ++i) visit_nonzero[i] = nz[i] ? 1 : 0;
+  if (visit_consumed) DS_CUDA(cudaMemcpy(visit_consumed, F.arr_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
+  if (visit_emitted) DS_CUDA(cudaMemcpy(visit_emitted, F.emit_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
+  if (visit_cut) {
+    std::vector<int> own((size_t)P->nsub * nrhs), cnt2(per), cut(per);
+    DS_CUDA(cudaMemcpy(own.data(), F.own_nz, sizeof(int) * own.size(), cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaMemcpy(cnt2.data(), F.arr_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
+    DS_CUDA(cudaMemcpy(cut.data(), F.arr_cut, sizeof(int) * per, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < per; ++i) {
+      size_t w = i / ((size_t)P->nsub * nrhs), rem = i % ((size_t)P->nsub * nrhs);
+      bool has_own = (w == 0) && own[rem];
+      visit_cut[i] = (has_own || cnt2[i] == 0) ? 0 : (cut[i] & CUT_ALL);
+    }
+  }
+  return DS_OK;
+}

@@ -1,0 +1,126 @@
+"""GPU factorization cache: the plugin point of the sweep engine.
+
+Drop-in for `FactorizationCache` / `factorize` (diagsweep/subdomain.py:
+139-179): `cache.get(op)` returns a factorization with `.solve(rhs)`,
+`.backend`, `.factor_bytes`, keyed by `op.fingerprint` so operators with
+identical coefficient bytes share one factorization (subdomain.py:153-171).
+
+The backend is the block-tridiagonal dense-block LU of K2 (csrc/ds_factor.cu)
+for every operator kind — it replaces both the Schur/Sylvester separable
+solver and SuperLU.  `method` keeps the reference's vocabulary and checks:
+'separable' on a non-separable operator raises ConfigurationError
+(subdomain.py:48-50), unknown methods raise ConfigurationError
+(subdomain.py:146).  Factorizations of many operators are created in one
+batched launch (`prepare`).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .errors import ConfigurationError
+
+_METHODS = ("auto", "separable", "splu", "block-lu")
+
+
+class GpuFactorization:
+    backend = "block-lu"
+
+    def __init__(self, fset, index: int, op):
+        self.fset = fset
+        self.index = index
+        self.window = op.window
+        self.shape = op.window.shape
+        self._op = op
+        ba, nb, m, nbytes = fset.info(index)
+        self.block_axis, self.n_blocks, self.block_size = ba, nb, m
+        self.factor_bytes = nbytes
+
+    def solve(self, rhs):
+        """x = A^{-1} rhs; rhs `[*window]` or batched `[R, *window]`."""
+        from . import _engine
+
+        shape = tuple(rhs.shape)
+        if shape != self.shape and shape[1:] != self.shape:
+            raise ConfigurationError(
+                f"rhs shape {shape} does not match window {self.shape}")
+        return _engine.fact_solve(self.fset, self.index, self._op, rhs)
+
+
+def _check_method(op, method: str):
+    if method not in _METHODS:
+        raise ConfigurationError(f"unknown factorization method {method!r}")
+    if method == "separable" and not op.separable:
+        raise ConfigurationError("operator kappa^2 is not tensor-structured")
+
+
+def factorize(op, method: str = "auto") -> GpuFactorization:
+    """Factor one operator on the GPU (block LU)."""
+    from . import _engine
+
+    _check_method(op, method)
+    return GpuFactorization(_engine.FactorSet([op]), 0, op)
+
+
+@dataclass
+class FactorizationCache:
+    method: str = "auto"
+    _store: dict = field(default_factory=dict)
+    hits: int = 0
+    misses: int = 0
+    _plans: dict = field(default_factory=dict, repr=False)
+
+    def prepare(self, ops) -> None:
+        """Factor every not-yet-cached distinct operator in one batched launch."""
+        from . import _engine
+
+        todo = {}
+        for op in ops:
+            _check_method(op, self.method)
+            key = op.fingerprint
+            if key not in self._store and key not in todo:
+                todo[key] = op
+        if not todo:
+            return
+        fset = _engine.FactorSet(list(todo.values()))
+        for i, (key, op) in enumerate(todo.items()):
+            self._store[key] = GpuFactorization(fset, i, op)
+
+    def get(self, op) -> GpuFactorization:
+        key = op.fingerprint
+        fact = self._store.get(key)
+        if fact is None:
+            self.prepare([op])
+            fact = self._store[key]
+            self.misses += 1
+        else:
+            self.hits += 1
+        return fact
+
+    def factorizations(self, ops) -> list:
+        """Factorizations for a list of operators (batched, counts like get)."""
+        missing = {op.fingerprint for op in ops if op.fingerprint not in self._store}
+        self.prepare(ops)
+        out = []
+        seen = set()
+        for op in ops:
+            key = op.fingerprint
+            if key in missing and key not in seen:
+                self.misses += 1
+                seen.add(key)
+            else:
+                self.hits += 1
+            out.append(self._store[key])
+        return out
+
+    @property
+    def count(self) -> int:
+        return len(self._store)
+
+    @property
+    def total_bytes(self) -> int:
+        return sum(f.factor_bytes for f in self._store.values())
+
+
+def solve(fact, rhs):
+    return fact.solve(rhs)

@@ -1,0 +1,232 @@
+"""CUDA path vs the CPU oracle on the same seeded inputs (parity proper).
+
+Tolerances (SURVEY §8 / BASELINE.json north star): relative L2 <= 1e-10 for
+solutions in complex128, GMRES iteration counts within +-1 (we require
+equality), counters / emission events / index maps exact.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ds_oracle as O
+from paper_2002_05327_b200 import (
+    FactorizationCache,
+    PmlProfile,
+    build_global_operator,
+    build_operators,
+    configs,
+    constant_model,
+    diagonal_sweep_solve,
+    gaussian_source,
+    gmres,
+    gmres_batched,
+    make_grid,
+    make_partition,
+    tuned_sigma_max,
+)
+from paper_2002_05327_b200.grid import Window
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    s = configs.spec(1)
+    b = configs.build(s)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    return s, b, prob, prob.operators()
+
+
+def mini_raster_spec(nrhs=3):
+    return configs.Spec("mini-raster", ((0.0, 2.4), (0.0, 0.8)), (240, 80), 10, 10, (4, 2),
+                        None, nrhs, "gmres", "raster", 3, c_range=(1.5, 3.0), noise=0.15,
+                        filt=10.0, src_depth_h=5.0)
+
+
+@pytest.fixture(scope="module")
+def raster():
+    s = mini_raster_spec()
+    b = configs.build(s)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    return s, b, prob, prob.operators()
+
+
+def test_stencil_apply_global_and_region(cuda, cfg1):
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(5)
+    gop = b["gop"]
+    v = rng.standard_normal((3,) + gop.window.shape) + 1j * rng.standard_normal((3,) + gop.window.shape)
+    out = gop.apply(v)
+    ogop = prob.global_operator()
+    for r in range(3):
+        assert rel(out[r], ogop.apply(v[r])) <= 1e-14
+    # sub-region with zero outside (pml.py:135-159)
+    op = b["ops"][(2, 3)]
+    w = op.window
+    reg = Window(tuple(l + 3 for l in w.lo), tuple(l + 20 for l in w.lo))
+    vr = rng.standard_normal(reg.shape) + 1j * rng.standard_normal(reg.shape)
+    got = op.apply(vr, region=reg)
+    want = oops[(2, 3)].apply(vr, reg.lo)
+    assert rel(got, want) <= 1e-14
+
+
+def test_stencil_apply_raster_kappa(cuda, raster):
+    s, b, prob, oops = raster
+    rng = np.random.default_rng(6)
+    for idx in [(1, 1), (2, 2), (4, 1)]:
+        op = b["ops"][idx]
+        v = rng.standard_normal(op.window.shape) + 1j * rng.standard_normal(op.window.shape)
+        assert rel(op.apply(v), oops[idx].apply(v)) <= 1e-14
+
+
+@pytest.mark.parametrize("which", ["cfg1", "raster"])
+def test_block_lu_solve_roundtrip(cuda, which, cfg1, raster):
+    s, b, prob, oops = cfg1 if which == "cfg1" else raster
+    cache = FactorizationCache()
+    rng = np.random.default_rng(7)
+    for idx in list(b["ops"])[:4]:
+        op = b["ops"][idx]
+        fact = cache.get(op)
+        rhs = rng.standard_normal((2,) + op.window.shape) + 1j * rng.standard_normal((2,) + op.window.shape)
+        x = fact.solve(rhs)
+        ref = O.factorize(oops[idx]).solve(rhs[0])
+        assert rel(x[0], ref) <= TOL
+        for r in range(2):
+            res = float(np.linalg.norm(oops[idx].apply(x[r]) - rhs[r]) / np.linalg.norm(rhs[r]))
+            assert res <= 1e-12, res
+
+
+def test_ddm_cfg1_parity_and_events(cuda, cfg1):
+    s, b, prob, oops = cfg1
+    f = configs.sources(s, b["grid"])
+    u, rep = diagonal_sweep_solve(f[0], b["partition"], b["ops"], FactorizationCache(),
+                                  record_events=True, warn_collar=False)
+    ref, orep = O.ddm_apply(prob, oops, O.Cache(), f[0], record=True)
+    assert rel(u.values, ref) <= TOL
+    assert rep.solves == orep["solves"] == 64
+    assert rep.nonzero_solves == orep["nonzero_solves"]
+    assert rep.discarded_sources == orep["discarded_sources"]
+    assert rep.events == orep["events"]
+
+
+def _compact_problem():
+    # the reference's test_ddm fixture (pkg/tests/test_ddm.py:27-53)
+    h = 0.01
+    n = 141
+    grid = make_grid(((0, h * (n - 1)),) * 2, (n, n))
+    part = make_partition(grid, (3, 3), overlap_d_points=5, pml_width_points=10)
+    kappa = 25.0
+    profile = PmlProfile(10, 5, tuned_sigma_max(kappa, 10 * h))
+    ops = build_operators(part, profile, constant_model(1.0), kappa)
+    a, bb = part.breaks[0][1], part.breaks[0][2]
+    c = grid.axis_coords(0)[(a + bb) // 2]
+    f = gaussian_source(grid, (c, c), kappa)
+    mask = np.zeros(grid.counts, dtype=bool)
+    inner = tuple(slice(sl.start + 1, sl.stop - 1) for sl in part.owned_slices((2, 2)))
+    mask[inner] = True
+    f = np.where(mask, f, 0)
+    prob = O.Problem(grid.extents, grid.counts, (3, 3), 5, 10, profile.sigma_max, 2, kappa,
+                     ("const", 1.0))
+    return grid, part, ops, f, prob
+
+
+def test_ddm_emission_pattern_compact_source(cuda):
+    """Golden emission pattern of pkg/tests/test_ddm.py:108-129 on the GPU."""
+    grid, part, ops, f, prob = _compact_problem()
+    u, report = diagonal_sweep_solve(f, part, ops, FactorizationCache(), record_events=True)
+    emitted = {}
+    for event in report.events:
+        if event["nonzero"]:
+            key = tuple(event["subdomain"])
+            assert key not in emitted
+            emitted[key] = (event["sweep"], event["sources_consumed"], event["sources_emitted"])
+    assert emitted[(2, 2)] == (1, 0, 8)
+    for edge in ((2, 3), (3, 2)):
+        assert emitted[edge] == (1, 1, 2)
+    assert emitted[(1, 2)] == (2, 1, 2)
+    assert emitted[(2, 1)] == (3, 1, 2)
+    for corner, sweep in (((3, 3), 1), ((1, 3), 2), ((3, 1), 3), ((1, 1), 4)):
+        assert emitted[corner] == (sweep, 3, 0)
+    oops = prob.operators()
+    ref, _ = O.ddm_apply(prob, oops, O.Cache(), f)
+    assert rel(u.values, ref) <= TOL
+
+
+def test_ddm_cfg2_batch_subset(cuda):
+    s = configs.spec(2)
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"])[:4]
+    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(),
+                                   warn_collar=False)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops = prob.operators()
+    cache = O.Cache()
+    for r in range(f.shape[0]):
+        ref, orep = O.ddm_apply(prob, oops, cache, f[r])
+        assert rel(u.values[r], ref) <= TOL
+        assert reps[r].nonzero_solves == orep["nonzero_solves"]
+        assert reps[r].discarded_sources == orep["discarded_sources"]
+
+
+def test_ddm_linearity_and_determinism(cuda, cfg1):
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(1)
+    shape = b["grid"].counts
+    f1 = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    f2 = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    cache = FactorizationCache()
+    batch = np.stack([2.5 * f1 + f2, f1, f2])
+    u, _ = diagonal_sweep_solve(batch, b["partition"], b["ops"], cache, warn_collar=False)
+    lhs = u.values[0]
+    rhs = 2.5 * u.values[1] + u.values[2]
+    assert np.linalg.norm(lhs - rhs) / np.linalg.norm(lhs) < 1e-10
+    u2, _ = diagonal_sweep_solve(batch, b["partition"], b["ops"], cache, warn_collar=False)
+    assert np.array_equal(u.values, u2.values)
+    # dense random source: every subdomain solve is nonzero
+    ref, _ = O.ddm_apply(prob, oops, O.Cache(), f1)
+    assert rel(u.values[1], ref) <= TOL
+
+
+def test_gmres_ddm_raster_parity(cuda, raster):
+    s, b, prob, oops = raster
+    f = configs.sources(s, b["grid"])
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    full = part.grid.full_window()
+
+    def apply_m(v):
+        return diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values
+
+    x, reps = gmres_batched(lambda v: gop.apply(v, region=full), apply_m, f, tol=1e-6)
+    ogop = prob.global_operator()
+    ocache = O.Cache()
+    for r in range(f.shape[0]):
+        xr, orep = O.gmres_ddm(prob, oops, ogop, ocache, f[r])
+        assert reps[r].n_iter == orep["n_iter"]
+        assert reps[r].converged and orep["converged"]
+        assert rel(x[r], xr) <= 1e-9, rel(x[r], xr)
+        np.testing.assert_allclose(reps[r].residuals, orep["residuals"], rtol=1e-6, atol=1e-12)
+
+
+def test_gmres_unbatched_matches_batched(cuda, raster):
+    s, b, prob, oops = raster
+    f = configs.sources(s, b["grid"])[:1]
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    full = part.grid.full_window()
+
+    def apply_m(v):
+        return diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values
+
+    x1, rep1 = gmres(lambda v: gop.apply(v, region=full), apply_m, f[0])
+    xb, repb = gmres_batched(lambda v: gop.apply(v, region=full), apply_m, f)
+    assert rep1.n_iter == repb[0].n_iter
+    assert rel(x1, xb[0]) <= 1e-12
