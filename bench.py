@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark: Helmholtz RHS/s of the diagonal-sweeping DDM (BASELINE.json).
+
+Default workload (`--config 2`, the metric's headline): 2D constant medium,
+433^2 nodes, 8x8 subdomains, 16 seeded Gaussian sources, one 4-sweep DDM
+application over the 16-RHS batch per step.  Inputs are
+generated on the host (NumPy float64, pinned seeds) exactly as the CPU
+oracle gets them.
+
+* `value`   RHS/s with the sources resident in HBM (device-timed, CUDA
+            events, max over ranks), `N * nrhs / t_step`.
+* `e2e`     the same metric through the public API `diagonal_sweep_solve`
+            with pinned host buffers: H2D of f and D2H of u inside the
+            timed region (plus the per-RHS report read-back).
+* `roofline` of the dominant kernel (K3 block substitution), timed live with
+            CUDA events bracketing every launch inside the timed region.
+* `cpu_baseline` the oracle port on a bounded sample, rank 0 at N=1.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port of the pure-Python reference; the reference itself cannot
+travel to the GPU box) on the same config, one RHS per step.
+
+Multi-GPU: RHS-parallel replicas (each rank its own seeded 16-RHS batch,
+factorizations replicated, no data-path collective), `scaling: weak`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2002_05327_b200 import configs  # noqa: E402
+
+L2_BYTES = 126 * 2**20
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm = p.get("hbm_gbs")
+    hbm_src = "measured (MEASURED_PEAKS.json)" if hbm else "fallback (B200_PROFILING.md)"
+    fp64 = None
+    fp64_src = "nominal B200 FP64 40 TFLOP/s (no measurement found)"
+    try:
+        q = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())
+        fp64 = q["dgemm_tflops"]
+        fp64_src = f"measured DGEMM (profiles/fp64_peak.json, {q.get('when', '?')})"
+    except Exception:
+        pass
+    return (hbm or 6650.0), hbm_src, (fp64 or 40.0), fp64_src
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_work(dp, nrhs):
+    """K3 flops and factor bytes per application: every
+    (sweep, subdomain) visit counts 16 n_b m^2 flop per RHS and streams its
+    2 n_b m^2 complex factor entries once per RHS chunk of 32."""
+    flops = 0
+    fbytes = 0
+    chunks = math.ceil(nrhs / 32)
+    for f in dp._keep[1]:
+        nb, m = f.n_blocks, f.block_size
+        flops += 16 * nb * m * m * nrhs
+        fbytes += 2 * nb * m * m * 16 * chunks
+    return flops * dp.nsweeps, fbytes * dp.nsweeps
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2002_05327_b200 import FactorizationCache, diagonal_sweep_solve
+    from paper_2002_05327_b200.ddm import SweepPlan, device_plan
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    s = configs.spec(args.config)
+    b = configs.build(s)
+    centers = configs.source_centers(s)
+    if world > 1 and rank > 0:  # each replica gets its own seeded batch
+        rng = np.random.default_rng(10_000 + rank)
+        centers = [tuple(c) for c in rng.uniform(0.05, 0.95, (len(centers), len(centers[0])))]
+    f_host = configs.sources(s, b["grid"], centers)
+    R = f_host.shape[0]
+    part, ops = b["partition"], b["ops"]
+    cache = FactorizationCache()
+
+    # ---- factorization (timed separately, amortised)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cache.prepare([ops[i] for i in part.subdomains()])
+    e1.record()
+    torch.cuda.synchronize()
+    factor_ms = e0.elapsed_time(e1)
+    factor_wall = time.perf_counter() - t0
+    dp = device_plan(part, ops, cache, SweepPlan.default(part.dim), R)
+    n = part.grid.node_count()
+    f_dev = torch.from_numpy(f_host.reshape(R, n)).to(dev)
+    nbytes_f = f_host.nbytes
+
+    # ---- warm-up (untimed)
+    for _ in range(args.warmup):
+        u, _ = dp.apply(f_dev)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K applications, inputs resident in HBM
+    if args.kernel_events:
+        dp.set_profiling(True)
+        dp.kernel_times(reset=True)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    launches = 0
+    for _ in range(args.steps):
+        u, _ = dp.apply(f_dev)
+        launches += dp.last_launches() + 2  # + the two layout kernels
+    en.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = st.elapsed_time(en) / args.steps
+    ktimes = dp.kernel_times(reset=True) if args.kernel_events else None
+    dp.set_profiling(False)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * R / (ms / 1e3)
+
+    # ---- e2e: public API, pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        f_pin = torch.from_numpy(f_host).pin_memory()
+        out_pin = torch.empty(f_host.shape, dtype=torch.complex128).pin_memory()
+        for _ in range(max(1, args.warmup // 2)):
+            uu, _ = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(args.steps):
+            uu, reps = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
+            out_pin.copy_(uu.values)  # result already host-side (input was host)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t1) * 1e3 / args.steps
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": world * R / (e2e_ms / 1e3), "unit": "RHS/s",
+               "h2d_bytes_per_step": int(nbytes_f), "d2h_bytes_per_step": int(nbytes_f),
+               "ms_per_step": e2e_ms, "api": "diagonal_sweep_solve(pinned host f) -> host u"}
+
+    # ---- roofline of the dominant kernel (K3)
+    hbm, hbm_src, fp64, fp64_src = peaks()
+    flops, fbytes = algorithmic_work(dp, R)
+    roofline = None
+    kernels = None
+    if ktimes:
+        kernels = {k: {"ms_per_app": v[0] / args.steps, "launches_per_app": v[1] / args.steps}
+                   for k, v in ktimes.items()}
+        solve_ms = ktimes["block_solve"][0] / args.steps
+        ach = flops / (solve_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "pipe": "fp64 (DFMA)", "achieved": ach, "peak": fp64,
+                    "unit": "TFLOP/s", "frac": ach / fp64, "traffic": None,
+                    "peak_source": fp64_src,
+                    "kernel": "k_block_solve (K3)",
+                    "algorithmic_per_app": {"flop": flops, "factor_bytes": fbytes},
+                    "hbm_view": {"achieved_gbs": fbytes / (solve_ms / 1e3) / 1e9, "peak_gbs": hbm,
+                                 "frac": fbytes / (solve_ms / 1e3) / 1e9 / hbm,
+                                 "peak_source": hbm_src},
+                    "share_of_step": solve_ms / ms}
+    # ---- parity spot check of the timed output (first RHS vs oracle is in tests)
+    res = {
+        "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2 else
+        f"Helmholtz RHS/s ({s.name})",
+        "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic (seeded Gaussian sources, SURVEY §8(d))",
+        "config": {"workload": s.name, "nrhs_per_gpu": R, "grid": list(part.grid.counts),
+                   "subdomains": list(part.counts), "sweeps": len(SweepPlan.default(part.dim).directions),
+                   "factor_ms": factor_ms, "factor_wall_s": factor_wall,
+                   "factor_bytes": cache.total_bytes, "distinct_factorizations": cache.count,
+                   "l2": "working set (factors %.2f GB) larger than L2; no flush needed" % (
+                       cache.total_bytes / 1e9),
+                   "parallelism": f"rhs-replicas x{world}"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "roofline": roofline,
+        "kernels": kernels,
+    }
+    return res
+
+
+def cpu_sample(s, b, n_rhs, threads):
+    """Oracle (port) DDM on n_rhs sources of the same workload."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import ds_oracle as O
+
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops = prob.operators()
+    f = configs.sources(s, b["grid"])
+    cache = O.Cache()
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        for idx in prob.subdomains:
+            cache.get(oops[idx])
+        tf = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        for r in range(n_rhs):
+            O.ddm_apply(prob, oops, cache, f[r % f.shape[0]])
+        ts = time.perf_counter() - t1
+    return tf, ts
+
+
+def run_reference(args):
+    s = configs.spec(args.config)
+    b = configs.build(s)
+    threads = os.cpu_count() or 1
+    from threadpoolctl import threadpool_limits
+
+    from oracle import ds_oracle as O
+
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops = prob.operators()
+    f = configs.sources(s, b["grid"])
+    cache = O.Cache()
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        for idx in prob.subdomains:
+            cache.get(oops[idx])
+        tf = time.perf_counter() - t0
+        for w in range(args.warmup):
+            O.ddm_apply(prob, oops, cache, f[w % f.shape[0]])
+        t1 = time.perf_counter()
+        for k in range(args.steps):
+            O.ddm_apply(prob, oops, cache, f[(args.warmup + k) % f.shape[0]])
+        ts = time.perf_counter() - t1
+    value = args.steps / ts
+    return {
+        "impl": "reference", "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2
+        else f"Helmholtz RHS/s ({s.name})",
+        "value": value, "unit": "RHS/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ts * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded, SURVEY §8(d))",
+        "config": {"workload": s.name, "step": "one DDM application for one RHS (reference API is single-RHS)",
+                   "factor_s": tf},
+        "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} single-RHS applications after {args.warmup} warm-up; "
+                                   f"factorization {tf:.2f} s excluded"},
+        "e2e": {"value": value, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def measure_fp64():
+    import torch
+
+    out = {}
+    for name, dt, mult in (("dgemm_tflops", torch.float64, 2), ("zgemm_tflops", torch.complex128, 8)):
+        nn = 8192 if dt == torch.float64 else 4096
+        a = torch.randn(nn, nn, dtype=dt, device="cuda")
+        bb = torch.randn(nn, nn, dtype=dt, device="cuda")
+        for _ in range(2):
+            torch.matmul(a, bb)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, bb)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = mult * nn**3 / (best / 1e3) / 1e12
+    out["when"] = time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())
+    out["how"] = "torch.matmul (cuBLAS) fp64 8192^3 and complex128 4096^3, best of 5, CUDA events"
+    out["gpu"] = torch.cuda.get_device_name()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rhs", type=int, default=3)
+    ap.add_argument("--no-kernel-events", dest="kernel_events", action="store_false")
+    ap.add_argument("--measure-fp64", action="store_true")
+    args = ap.parse_args()
+    args.config = int(args.config) if args.config.isdigit() else args.config
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.measure_fp64:
+        print(json.dumps(measure_fp64()))
+        return
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = configs.spec(args.config)
+        b = configs.build(s)
+        threads = os.cpu_count() or 1
+        tf, ts = cpu_sample(s, b, args.cpu_sample_rhs, threads)
+        res["cpu_baseline"] = {"value": args.cpu_sample_rhs / ts, "unit": "RHS/s", "cores": threads,
+                               "kind": "port",
+                               "sample": f"{args.cpu_sample_rhs} single-RHS DDM applications of "
+                                         f"{s.name} (oracle port, {threads} BLAS threads); "
+                                         f"factorization {tf:.2f} s excluded"}
+    if rank == 0:
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -191,6 +191,15 @@ DS_API int ds_ddm_counters(ds_ctx *ctx, ds_plan *plan, int32_t nrhs,
  * pointers and nrhs); ds_ddm_apply uses the graph when it matches. */
 DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
 
+/* Per-kernel-class timing: when enabled, ds_ddm_apply brackets every
+ * launch with CUDA events on the context stream (graph replay is bypassed).
+ * ds_plan_kernel_times returns summed milliseconds and launch counts for
+ * classes {0 assemble (K6), 1 block solve (K3), 2 accumulate (K5),
+ * 3 transfer (K4)} since the last reset; blocks the host. */
+DS_API int ds_plan_set_profiling(ds_plan *plan, int32_t enable);
+DS_API int ds_plan_kernel_times(ds_plan *plan, double *ms, int64_t *count,
+                                int32_t reset);
+
 /* Launch count of the last ds_ddm_apply (kernel nodes issued). */
 DS_API int64_t ds_plan_last_launches(const ds_plan *plan);
 

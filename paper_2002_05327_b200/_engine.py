@@ -57,7 +57,7 @@ def context():
 def to_device_batch(v, shape):
     """-> (tensor [R, *shape] complex128 contiguous on the GPU, kind, batched)."""
     _require_cuda()
-    kind = "torch" if hasattr(v, "detach") else "numpy"
+    kind = ("torch" if v.is_cuda else "torch_cpu") if hasattr(v, "detach") else "numpy"
     vshape = tuple(v.shape)
     if vshape == tuple(shape):
         batched = False
@@ -73,7 +73,7 @@ def to_device_batch(v, shape):
         if t.dtype != torch.complex128:
             t = t.to(torch.complex128)
         if not t.is_cuda:
-            t = t.to("cuda")
+            t = t.to("cuda", non_blocking=t.is_pinned())
         t = t.contiguous()
     if not batched:
         t = t.reshape((1,) + tuple(shape))
@@ -85,6 +85,8 @@ def from_device_batch(t, kind, batched):
         t = t[0]
     if kind == "numpy":
         return t.cpu().numpy()
+    if kind == "torch_cpu":
+        return t.cpu()
     return t
 
 
@@ -330,6 +332,18 @@ class DevicePlan:
 
     def last_launches(self) -> int:
         return N.load_library().ds_plan_last_launches(self.handle)
+
+    def set_profiling(self, enable: bool = True):
+        N.check(N.load_library().ds_plan_set_profiling(self.handle, int(bool(enable))))
+
+    KERNEL_CLASSES = ("assemble", "block_solve", "accumulate", "transfer")
+
+    def kernel_times(self, reset: bool = True) -> dict:
+        """{class: (total_ms, launches)} since the last reset (CUDA events)."""
+        ms = (C.c_double * 4)()
+        cnt = (C.c_int64 * 4)()
+        N.check(N.load_library().ds_plan_kernel_times(self.handle, ms, cnt, int(reset)))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
 
     def apply_minor(self, fmin, umin, nrhs: int, partials=None):
         """One application on RHS-minor device buffers (no layout work)."""

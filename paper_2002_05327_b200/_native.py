@@ -85,6 +85,8 @@ _SIGNATURES = [
     ("ds_ddm_counters", C.c_int, [vp, vp, i32, P_i32, P_i32, P_i32, P_i32, P_i32, P_i32]),
     ("ds_ddm_enable_graph", C.c_int, [vp, vp, i32]),
     ("ds_plan_last_launches", i64, [vp]),
+    ("ds_plan_set_profiling", C.c_int, [vp, i32]),
+    ("ds_plan_kernel_times", C.c_int, [vp, P_f64, P_i64, i32]),
     ("ds_vec_dot", C.c_int, [vp, i64, i32, vp, vp, vp]),
     ("ds_vec_norm", C.c_int, [vp, i64, i32, vp, vp]),
     ("ds_vec_axpy", C.c_int, [vp, i64, i32, vp, C.c_double, vp, vp]),

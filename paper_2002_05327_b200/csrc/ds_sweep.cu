@@ -96,6 +96,11 @@ struct ds_plan {
   void *graph_u = nullptr;
   void *graph_partials = nullptr;
   int graph_nrhs = 0;
+  // per-kernel-class timing (0 assemble, 1 solve, 2 accumulate, 3 transfer)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_class;
+  size_t ev_used = 0;
 };
 
 static int plan_alloc(ds_plan *P, void **ptr, size_t bytes) {
@@ -616,6 +621,7 @@ extern "C" int64_t ds_plan_last_launches(const ds_plan *P) { return P ? P->last_
 extern "C" int ds_plan_destroy(ds_plan *P) {
   if (!P) return DS_OK;
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (auto e : P->ev) cudaEventDestroy(e);
   for (void *p : P->allocs) cudaFree(p);
   delete P;
   return DS_OK;
@@ -651,6 +657,21 @@ static int blocks_for(ds_ctx *ctx, int64_t work, int per_visit_cap) {
   return (int)b;
 }
 
+static void prof_mark(ds_plan *P, int cls, cudaStream_t st) {
+  if (!P->profiling) return;
+  if (P->ev_used + 1 >= P->ev.size()) {
+    size_t n = P->ev.size() ? P->ev.size() : 1024;
+    for (size_t i = 0; i < n; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      P->ev.push_back(e);
+      P->ev_class.push_back(-1);
+    }
+  }
+  P->ev_class[P->ev_used] = cls;
+  cudaEventRecord(P->ev[P->ev_used++], st);
+}
+
 // issue the whole application on ctx->stream (capturable)
 static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials) {
   ds_ctx *ctx = P->ctx;
@@ -671,13 +692,16 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (G == 0) continue;
       const int64_t wmax = P->max_w, smax = P->max_w;
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
+      prof_mark(P, 0, st);
       k_assemble<<<dim3(bx, G), 256, 0, st>>>(P->visits + v0, P->subs, P->slots, f, nrhs, dim,
                                               P->gcounts[0], P->gcounts[1], P->gcounts[2], F);
       ctx->launches++;
       DS_CHECK_LAUNCH();
+      prof_mark(P, 1, st);
       int rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
       if (rc) return rc;
       DS_CHECK_LAUNCH();
+      prof_mark(P, 2, st);
       int by = blocks_for(ctx, smax * nrhs / 4, std::max(1, cap / G));
       k_accumulate<<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
                                                 P->gcounts[0], P->gcounts[1], P->gcounts[2]);
@@ -685,6 +709,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CHECK_LAUNCH();
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0) {
+        prof_mark(P, 3, st);
         int bz = std::max(1, std::min(64, cap / nx));
         k_transfer<<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, w + 1,
                                                  nrhs, dim, F);
@@ -696,6 +721,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CUDA(cudaMemcpyAsync(partials + (size_t)w * P->nnodes * nrhs, u,
                               sizeof(cplx) * P->nnodes * nrhs, cudaMemcpyDeviceToDevice, st));
   }
+  prof_mark(P, -1, st);
   P->last_launches = ctx->launches - launches0;
   return DS_OK;
 }
@@ -712,7 +738,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
     P->slots_dirty = false;
   }
-  if (P->use_graph) {
+  if (P->use_graph && !P->profiling) {
     bool match = P->graph && P->graph_f == f && P->graph_u == u && P->graph_nrhs == nrhs &&
                  P->graph_partials == partials;
     if (!match) {
@@ -789,5 +815,33 @@ extern "C" int ds_ddm_counters(ds_ctx *ctx, ds_plan *P, int32_t nrhs, int32_t *n
       visit_cut[i] = (has_own || cnt2[i] == 0) ? 0 : (cut[i] & CUT_ALL);
     }
   }
+  return DS_OK;
+}
+
+extern "C" int ds_plan_set_profiling(ds_plan *P, int32_t enable) {
+  if (!P) return ds_fail(DS_ECONFIG, "null plan");
+  P->profiling = enable != 0;
+  P->ev_used = 0;
+  return DS_OK;
+}
+
+// Sum of event-bracketed durations per kernel class since the last reset
+// (blocks the host).  ms[4], count[4]: assemble, solve, accumulate, transfer.
+extern "C" int ds_plan_kernel_times(ds_plan *P, double *ms, int64_t *count, int32_t reset) {
+  if (!P) return ds_fail(DS_ECONFIG, "null plan");
+  for (int c = 0; c < 4; ++c) {
+    if (ms) ms[c] = 0.0;
+    if (count) count[c] = 0;
+  }
+  if (P->ev_used > 0) DS_CUDA(cudaEventSynchronize(P->ev[P->ev_used - 1]));
+  for (size_t i = 0; i + 1 < P->ev_used; ++i) {
+    int c = P->ev_class[i];
+    if (c < 0 || c > 3) continue;
+    float t = 0.f;
+    DS_CUDA(cudaEventElapsedTime(&t, P->ev[i], P->ev[i + 1]));
+    if (ms) ms[c] += t;
+    if (count) count[c] += 1;
+  }
+  if (reset) P->ev_used = 0;
   return DS_OK;
 }

@@ -241,7 +241,7 @@ def _reports(dp, nrhs: int, plan: SweepPlan, partition: Partition, record_events
             for w in range(dp.nsweeps):
                 for t in range(dp.nsteps):
                     b, e = dp.step_off[w * (dp.nsteps + 1) + t], dp.step_off[w * (dp.nsteps + 1) + t + 1]
-                    for s in dp.visit_sub[b:e]:
+                    for s in dp.visit_sub[w * dp.nsub + b: w * dp.nsub + e]:
                         nz = bool(ctr["visit_nonzero"][w, s, r])
                         idx = dp.subs[s]
                         if record_events:
