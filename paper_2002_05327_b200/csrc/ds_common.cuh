@@ -108,6 +108,8 @@ struct ds_op {
 struct FactDev {
   int block_axis;
   int nb, m;
+  int twist;          // middle block t: blocks k < t hold S_k^{-1} (top-down),
+                      // k > t hold T_k^{-1} (bottom-up), k = t holds M_t^{-1}
   int other[2];       // the in-block axes in C order (unused entries = -1)
   int win_shape[3];
   const cplx *sinv;   // nb * m * m, row-major blocks
@@ -139,6 +141,7 @@ struct SolveVisit {
   const cplx *rhs;
   cplx *x;
   const int *nz;
+  cplx *xg;  // global exchange scratch: >= 4 * m * nrhs complex values
 };
 
 // launch K3 over a device table of visits (one cluster per visit x chunk)

@@ -10,8 +10,16 @@
 // and every S_k^{-1} is stored densely (complex128) so the substitution is
 // pure GEMV/GEMM work (K3).
 //
-// One thread-block cluster per operator walks the chain; each CTA owns a
-// column slice of S_k in shared memory and the cluster inverts it by
+// Twisted ("burn at both ends") variant: with t = n_b/2 the top chain
+// builds S_0..S_{t-1} as above while an independent bottom chain builds
+//     T_{n_b-1} = D_{n_b-1},  T_k = D_k - (u_k l_{k+1}) T_{k+1}^{-1},
+// and the middle block M_t = D_t - (l_t u_{t-1}) S_{t-1}^{-1}
+//                                - (u_t l_{t+1}) T_{t+1}^{-1}
+// closes the system.  Halving the chain length halves the latency of both
+// the factorization and every substitution (K3).
+//
+// One thread-block cluster per (operator, half) walks its chain; each CTA
+// owns a column slice of S_k in shared memory and the cluster inverts it by
 // Gauss-Jordan elimination with partial pivoting (pivot column broadcast
 // through distributed shared memory, one cluster barrier per pivot).  The
 // explicit inverse keeps the backward error at ~1e-15 for these operators
@@ -32,6 +40,7 @@ struct FactJob {
   OpDev op;
   FactDev f;
   cplx *sinv;
+  int half;  // 0 top chain, 1 bottom chain, 2 middle block
 };
 
 #define GJ_THREADS 512
@@ -98,7 +107,8 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
   const FactJob &J = jobs[blockIdx.y];
-  const int m = J.f.m, nb = J.f.nb;
+  const int m = J.f.m, nb = J.f.nb, tw = J.f.twist;
+  const int nsteps = J.half == 0 ? tw : (J.half == 1 ? nb - 1 - tw : 1);
   const int mcper = (m + C - 1) / C;
   const int c0 = rank * mcper;
   const int c1 = min(m, c0 + mcper);
@@ -119,15 +129,27 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
 
   const int ld = mcper_max;
   const int ba = J.f.block_axis;
-  for (int k = 0; k < nb; ++k) {
-    // ---- S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1}  (my columns)
-    cplx lu = make_double2(0.0, 0.0);
-    if (k > 0) lu = cmul(J.op.c_lo[ba][k], J.op.c_hi[ba][k - 1]);
-    const cplx *prev = J.sinv + (size_t)(k > 0 ? k - 1 : 0) * m * m;
+  for (int step = 0; step < nsteps; ++step) {
+    // ---- Schur complement of block k (my columns):
+    //   top    S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1}
+    //   bottom T_k = D_k - (u_k l_{k+1}) T_{k+1}^{-1}
+    //   middle M_t = D_t - (l_t u_{t-1}) S_{t-1}^{-1} - (u_t l_{t+1}) T_{t+1}^{-1}
+    const int k = J.half == 0 ? step : (J.half == 1 ? nb - 1 - step : tw);
+    cplx co1 = make_double2(0.0, 0.0), co2 = co1;
+    const cplx *p1 = nullptr, *p2 = nullptr;
+    if ((J.half == 0 || J.half == 2) && k > 0) {
+      co1 = cmul(J.op.c_lo[ba][k], J.op.c_hi[ba][k - 1]);
+      p1 = J.sinv + (size_t)(k - 1) * m * m;
+    }
+    if ((J.half == 1 || J.half == 2) && k < nb - 1) {
+      co2 = cmul(J.op.c_hi[ba][k], J.op.c_lo[ba][k + 1]);
+      p2 = J.sinv + (size_t)(k + 1) * m * m;
+    }
     for (int e = t; e < m * mc; e += T) {
       int i = e / mc, cc = e % mc, c = c0 + cc;
       cplx v = d_entry(J, k, i, c);
-      if (k > 0) v = csub(v, cmul(lu, __ldcg(prev + (size_t)i * m + c)));
+      if (p1) v = csub(v, cmul(co1, __ldcg(p1 + (size_t)i * m + c)));
+      if (p2) v = csub(v, cmul(co2, __ldcg(p2 + (size_t)i * m + c)));
       S[i * ld + cc] = v;
     }
     cluster.sync();
@@ -236,6 +258,7 @@ static void fill_layout(const OpDev &o, FactDev &f) {
     if (o.shape[a] > o.shape[ba]) ba = a;
   f.block_axis = ba;
   f.nb = o.shape[ba];
+  f.twist = f.nb / 2;
   f.m = 1;
   f.other[0] = f.other[1] = -1;
   int n = 0;
@@ -297,29 +320,50 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact
                        " exceeds the on-chip Gauss-Jordan path (3D windows need the "
                        "blocked path)");
   }
+  // jobs: [top chains | bottom chains] then [middle blocks]
+  std::vector<FactJob> chain_jobs, mid_jobs;
+  for (int i = 0; i < n; ++i) {
+    FactJob a = jobs[i];
+    a.half = 0;
+    chain_jobs.push_back(a);
+  }
+  for (int i = 0; i < n; ++i) {
+    FactJob a = jobs[i];
+    a.half = 1;
+    chain_jobs.push_back(a);
+  }
+  for (int i = 0; i < n; ++i) {
+    FactJob a = jobs[i];
+    a.half = 2;
+    mid_jobs.push_back(a);
+  }
   FactJob *djobs = nullptr;
   int *dstatus = nullptr;
-  DS_CUDA(cudaMalloc(&djobs, n * sizeof(FactJob)));
+  DS_CUDA(cudaMalloc(&djobs, 3 * n * sizeof(FactJob)));
   DS_CUDA(cudaMalloc(&dstatus, sizeof(int)));
-  DS_CUDA(cudaMemcpy(djobs, jobs.data(), n * sizeof(FactJob), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemcpy(djobs, chain_jobs.data(), 2 * n * sizeof(FactJob), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemcpy(djobs + 2 * n, mid_jobs.data(), n * sizeof(FactJob), cudaMemcpyHostToDevice));
   DS_CUDA(cudaMemset(dstatus, 0, sizeof(int)));
   DS_CUDA(cudaFuncSetAttribute(k_factor_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(C, n, 1);
-  cfg.blockDim = dim3(GJ_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  DS_CUDA(cudaLaunchKernelEx(&cfg, k_factor_gj, (const FactJob *)djobs, mcper, dstatus));
-  ctx->launches++;
+  for (int launch = 0; launch < 2; ++launch) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(C, launch == 0 ? 2 * n : n, 1);
+    cfg.blockDim = dim3(GJ_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DS_CUDA(cudaLaunchKernelEx(&cfg, k_factor_gj, (const FactJob *)(djobs + (launch ? 2 * n : 0)),
+                               mcper, dstatus));
+    ctx->launches++;
+  }
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
   int status = 0;
   DS_CUDA(cudaMemcpy(&status, dstatus, sizeof(int), cudaMemcpyDeviceToHost));
@@ -379,11 +423,11 @@ extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_
   size_t n = (size_t)f.nb * f.m * nrhs;
   cplx *tmp = nullptr;
   void *vis = nullptr;
-  DS_CUDA(cudaMallocAsync((void **)&tmp, 2 * n * sizeof(cplx) + sizeof(FactDev) + 64, ctx->stream));
-  cplx *bin = tmp, *bout = tmp + n;
-  FactDev *fd = (FactDev *)(tmp + 2 * n);
+  DS_CUDA(cudaMallocAsync((void **)&tmp, 6 * n * sizeof(cplx) + sizeof(FactDev) + 64, ctx->stream));
+  cplx *bin = tmp, *bout = tmp + n, *xg = tmp + 2 * n;
+  FactDev *fd = (FactDev *)(tmp + 6 * n);
   DS_CUDA(cudaMallocAsync(&vis, sizeof(SolveVisit), ctx->stream));
-  SolveVisit hv{fd, bin, bout, nullptr};
+  SolveVisit hv{fd, bin, bout, nullptr, xg};
   DS_CUDA(cudaMemcpyAsync(fd, &f, sizeof(FactDev), cudaMemcpyHostToDevice, ctx->stream));
   DS_CUDA(cudaMemcpyAsync(vis, &hv, sizeof(hv), cudaMemcpyHostToDevice, ctx->stream));
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8);

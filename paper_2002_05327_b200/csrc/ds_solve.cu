@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "ds_common.cuh"
@@ -41,16 +42,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Bounded spin: a protocol error traps (a CUDA error on the host) instead of
+// hanging the GPU.  ~2^22 polls of a suspending try_wait is seconds.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  for (uint32_t i = 0; !mbar_try(bar, parity); ++i)
+    if (i > (1u << 22)) __trap();
 }
 // TMA bulk copy global -> this CTA's shared memory, completing on `bar`
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
@@ -81,169 +90,298 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
-#define FAC_STAGES 3
+#define FAC_STAGES 2
+#define GMAX 4
 
-// Cluster rank q owns rows [q*rows_per, q*rows_per + nr) of every S_k^{-1}.
-// Stage s (s < n_b: forward block k = s; else backward block 2n_b-2-s):
-//   wait vec[s&1] (filled by all peers' bulk pushes) and the factor tile,
-//   acc = S_k^{-1}[rows, :] * vec          (2x2 register micro-tiles, K split)
-//   forward : y_k = acc, next = b_{k+1} - l_{k+1} y_k   (or y_k at the turn)
-//   backward: x_k = y_k - u_k acc, next = x_k
-//   push `next` rows to every peer's vec[(s+1)&1].
+#ifdef DS_SOLVE_TRACE
+__device__ long long g_solve_trace[2][1024][6];
+// slot 0: stage start; 1/2/3: top chain after wait / compute / epilogue;
+// 4/5: bottom chain after wait / epilogue
+#define TRACE(i)                                                                   \
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0 && rank < 2 && s < 1024)       \
+    g_solve_trace[rank][s][(i) == 0 ? 0 : (h == 0 ? (i) : ((i) == 1 ? 4 : ((i) == 3 ? 5 : 6)))] = clock64();
+#else
+#define TRACE(i)
+#endif
+
+// multicast TMA: global -> the same shared offset of every CTA in `mask`,
+// completing on each receiver's mbarrier at the same offset
+__device__ __forceinline__ void bulk_g2s_multicast(void *dst, const void *src, uint32_t bytes,
+                                                   uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// Twisted block substitution (see ds_factor.cu).  t = twist, nt = t top
+// blocks, nbt = n_b-1-t bottom blocks, F = max(nt, nbt); stages 0..2F:
+//   forward  top    k = s-(F-nt)        for s in [F-nt, F-1]
+//            bottom k = n_b-1-(s-(F-nbt)) for s in [F-nbt, F-1]
+//   middle   k = t at s = F, input (b_t - l_t y_{t-1}) + (-u_t z_{t+1})
+//   backward top    k = t-1-(s-F-1),  bottom k = t+1+(s-F-1)
+// Every (half, RHS group) is an independent chain; within a stage the CTA
+// walks its chains so one chain's all-gather (rows -> global -> multicast
+// TMA into every CTA's shared vector, completing on an mbarrier) overlaps
+// the other chains' compute.
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
-    k_block_solve(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+    k_block_solve(const SolveVisit *__restrict__ visits, int nrhs, int rc, int G, int rows_max) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
   const SolveVisit V = visits[blockIdx.y];
   const FactDev f = *V.f;
-  const int m = f.m, nb = f.nb;
+  const int m = f.m, nb = f.nb, tw = f.twist;
   const int chunk0 = blockIdx.z * rc;
   const int rcc = min(rc, nrhs - chunk0);
   const int t = threadIdx.x;
+  int s = 0;  // stage (also used by TRACE)
 
-  // skip visits whose right-hand sides are all exactly zero (ddm.py:256-258)
-  if (V.nz) {
+  if (V.nz) {  // skip visits whose right-hand sides are all exactly zero
     int any = 0;
     for (int r = 0; r < rcc; ++r) any |= V.nz[chunk0 + r];
     if (!any) return;  // uniform across the cluster (before any barrier)
   }
-
+  const int Gc = (rcc % G == 0) ? G : 1;  // groups must split the chunk evenly
+  const int rg = rcc / Gc;                // RHS per group
   const int rows_per = (m + C - 1) / C;
   const int r0 = rank * rows_per;
   const int nr = max(0, min(rows_per, m - r0));
+  const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
+  const size_t ldx = nrhs;
+  const uint16_t mask = (uint16_t)((1u << C) - 1);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  uint64_t *vbar = (uint64_t *)smem_raw;                 // [2]
-  uint64_t *fbar = vbar + 2;                             // [FAC_STAGES]
-  cplx *vec = (cplx *)(smem_raw + 128);                  // [2][m*rcc + 2]
-  const int vstride = m * rc + 2;
-  cplx *stg = vec + 2 * vstride;                         // [2][rows_max*rc]
-  cplx *fac = stg + 2 * rows_max * rc;                   // [FAC_STAGES][rows_max*m + 2]
+  uint64_t *vbar = (uint64_t *)smem_raw;          // [2 halves][GMAX][2]
+  uint64_t *fbar = vbar + 4 * GMAX;               // [2 halves][FAC_STAGES]
+  cplx *vec = (cplx *)(smem_raw + 256);           // [2][Gc][2][vstride]
+  const int vstride = m * rg + 2;
+  cplx *fac = vec + 4 * Gc * vstride;             // [2][FAC_STAGES][fstride]
   const int fstride = rows_max * m + 2;
-  cplx *red = fac + FAC_STAGES * fstride;                // [16 * rows_max * rc]
+  cplx *red = fac + 2 * FAC_STAGES * fstride;     // [16][rows_max * rg]
+  auto VEC = [&](int h, int g, int p) { return vec + ((h * Gc + g) * 2 + p) * vstride; };
+  auto VBAR = [&](int h, int g, int p) { return &vbar[(h * GMAX + g) * 2 + p]; };
+  // global exchange scratch of this cluster: [2][GMAX][2][m * rg]
+  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  auto XG = [&](int h, int g, int p) { return xg + ((size_t)(h * Gc + g) * 2 + p) * m * rg; };
 
-  const int S = 2 * nb - 1;
-  auto tile_of = [&](int s) { return s < nb ? s : 2 * nb - 2 - s; };
-  const uint32_t vec_bytes = (uint32_t)(m * rcc * sizeof(cplx));
-  const uint32_t push_bytes = (uint32_t)(nr * rcc * sizeof(cplx));
+  // block processed by half h at stage s (-1: idle).  kind 0 fwd, 1 mid, 2 bwd
+  auto block_of = [&](int h, int st, int &kind) -> int {
+    kind = st < F ? 0 : (st == F ? 1 : 2);
+    if (h == 0) {
+      if (st < F) return st >= F - nt ? st - (F - nt) : -1;
+      if (st == F) return tw;
+      int j = st - F - 1;
+      return j < nt ? tw - 1 - j : -1;
+    }
+    if (st < F) return st >= F - nbt ? nb - 1 - (st - (F - nbt)) : -1;
+    if (st == F) return -1;
+    int j = st - F - 1;
+    return j < nbt ? tw + 1 + j : -1;
+  };
+  // factor-ring sequence index of (half, stage)
+  auto fseq = [&](int h, int st) {
+    if (h == 0) return st - (F - nt);
+    return st < F ? st - (F - nbt) : st - (F - nbt) - 1;
+  };
   const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
-  const size_t ldx = nrhs;  // row stride of the global block vectors
+  const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
+  const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
+  auto load_tile = [&](int h, int st) {  // thread 0 only
+    int kind, k = block_of(h, st, kind);
+    if (k < 0) return;
+    int q = fseq(h, st), slot = q % FAC_STAGES;
+    uint64_t *bar = &fbar[h * FAC_STAGES + slot];
+    mbar_expect_tx(bar, fac_bytes);
+    if (fac_bytes)
+      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+  };
+  // push my rows of the next-stage vector (already in global) to every CTA
+  auto push = [&](int h, int g, int p) {  // thread 0 only, after the fence + barrier
+    if (push_bytes)
+      bulk_g2s_multicast(VEC(h, g, p) + r0 * rg, XG(h, g, p) + r0 * rg, push_bytes, VBAR(h, g, p), mask);
+  };
 
   if (t == 0) {
-    mbar_init(&vbar[0], 1);
-    mbar_init(&vbar[1], 1);
-    for (int i = 0; i < FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
+    for (int i = 0; i < 4 * GMAX; ++i) mbar_init(&vbar[i], 1);
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
     fence_mbar_init();
   }
-  cluster.sync();  // every peer's barriers are initialised before any push
+  cluster.sync();  // peers' barriers initialised before any multicast
+  // vector-buffer phase counters (uniform across threads)
+  int vph[2][GMAX][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int g = 0; g < GMAX; ++g) vph[h][g][0] = vph[h][g][1] = 0;
   if (t == 0) {
-    mbar_expect_tx(&vbar[0], vec_bytes);
-    if (S > 1) mbar_expect_tx(&vbar[1], vec_bytes);
-    for (int i = 0; i < FAC_STAGES - 1 && i < S; ++i) {
-      mbar_expect_tx(&fbar[i], fac_bytes);
-      if (fac_bytes)
-        bulk_g2s(fac + i * fstride, f.sinv + ((size_t)tile_of(i) * m + r0) * m, fac_bytes, &fbar[i]);
-    }
+    for (int h = 0; h < 2; ++h)
+      for (int g = 0; g < Gc; ++g) {
+        mbar_expect_tx(VBAR(h, g, 0), vec_bytes);
+        mbar_expect_tx(VBAR(h, g, 1), vec_bytes);
+      }
+    load_tile(0, 0);  // stage-0 tiles; the loop loads stage s+1 at stage s
+    load_tile(1, 0);
   }
-  // prologue: push my rows of b_0
-  for (int e = t; e < nr * rcc; e += SOLVE_THREADS) {
-    int row = e / rcc, c = e % rcc;
-    stg[e] = V.rhs[(size_t)(r0 + row) * ldx + chunk0 + c];
+  // prologue: b_0 for the top chain (stage F-nt), b_{n_b-1} for the bottom
+  // chain (stage F-nbt); written to the exchange scratch then multicast
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && nbt == 0) break;
+    const int st0 = h == 0 ? F - nt : F - nbt;
+    const int k0 = h == 0 ? 0 : nb - 1;
+    for (int g = 0; g < Gc; ++g)
+      for (int e = t; e < nr * rg; e += SOLVE_THREADS) {
+        int row = e / rg, c = e % rg;
+        XG(h, g, st0 & 1)[(r0 + row) * rg + c] =
+            V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + g * rg + c];
+      }
   }
-  fence_proxy_async();
+  fence_proxy_async_global();
   __syncthreads();
-  if (t == 0 && push_bytes)
-    for (int q = 0; q < C; ++q) bulk_s2peer(vec + r0 * rcc, stg, push_bytes, &vbar[0], q);
+  if (t == 0) {
+    for (int g = 0; g < Gc; ++g) push(0, g, (F - nt) & 1);
+    if (nbt > 0)
+      for (int g = 0; g < Gc; ++g) push(1, g, (F - nbt) & 1);
+  }
 
-  // compute decomposition: 2x2 (row, rhs) micro-tiles, K split into slices
-  const int TR = (nr + 1) / 2, TC = (rcc + 1) / 2;
+  const int TR = (nr + 1) / 2, TC = (rg + 1) / 2;
   const int ntile = TR * TC;
   int nslice = ntile > 0 ? SOLVE_THREADS / ntile : 1;
   nslice = max(1, min(16, nslice));
   const int ks = (m + nslice - 1) / nslice;
-  const int nout = nr * rcc;
+  const int nout = nr * rg;
+  const int orow = t / max(rg, 1), oc = t % max(rg, 1);
 
-  for (int s = 0; s < S; ++s) {
-    const int k = tile_of(s);
-    const bool fwd = s < nb;
-    const int b = s & 1;
-    // refill the factor ring (slot consumed at stage s-1)
-    if (t == 0 && s + FAC_STAGES - 1 < S) {
-      int sn = s + FAC_STAGES - 1, slot = sn % FAC_STAGES;
-      mbar_expect_tx(&fbar[slot], fac_bytes);
-      if (fac_bytes)
-        bulk_g2s(fac + slot * fstride, f.sinv + ((size_t)tile_of(sn) * m + r0) * m, fac_bytes,
-                 &fbar[slot]);
+  for (s = 0; s < S; ++s) {
+    const int p = s & 1;
+    { const int h = 0; (void)h; TRACE(0); }
+    // refill the factor rings for stage s+1 (slot consumed at stage s-1)
+    if (t == 0 && s + 1 < S) {
+      load_tile(0, s + 1);
+      load_tile(1, s + 1);
     }
-    // epilogue operands (independent of the chain): issue the loads early
-    cplx aux = make_double2(0.0, 0.0);
-    int orow = t / max(rcc, 1), oc = t % max(rcc, 1);
-    if (t < nout) {
-      if (fwd && k + 1 < nb)
-        aux = V.rhs[((size_t)(k + 1) * m + r0 + orow) * ldx + chunk0 + oc];
-      else if (!fwd)
-        aux = __ldcg(V.x + ((size_t)k * m + r0 + orow) * ldx + chunk0 + oc);
-    }
-    mbar_wait(&vbar[b], (s >> 1) & 1);
-    mbar_wait(&fbar[s % FAC_STAGES], (s / FAC_STAGES) & 1);
-    const cplx *A = fac + (s % FAC_STAGES) * fstride;
-    const cplx *X = vec + b * vstride;
-    for (int tile = ntile ? t % ntile : 0, sl = ntile ? t / ntile : nslice;
-         sl < nslice && tile < ntile; tile += SOLVE_THREADS) {
-      const int tr = tile / TC, tc = tile % TC;
-      const int row = 2 * tr, c = 2 * tc;
-      const int j0 = (ntile > SOLVE_THREADS) ? 0 : sl * ks;
-      const int j1 = (ntile > SOLVE_THREADS) ? m : min(m, j0 + ks);
-      cplx a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
-      const cplx *ar0 = A + (size_t)row * m;
-      const cplx *ar1 = ar0 + m;
+    int kindh[2], kh[2];
+    kh[0] = block_of(0, s, kindh[0]);
+    kh[1] = block_of(1, s, kindh[1]);
+    // epilogue operands, loaded early (independent of the chain)
+    cplx aux[2][GMAX];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) {
+        aux[h][g] = make_double2(0.0, 0.0);
+        if (g >= Gc || kh[h] < 0 || t >= nout) continue;
+        const int k = kh[h];
+        const int col = chunk0 + g * rg + oc;
+        if (kindh[h] == 0) {
+          int kn = h == 0 ? k + 1 : k - 1;  // next block of this chain
+          bool has_b = h == 0 ? true : (kn > tw);
+          if (has_b) aux[h][g] = V.rhs[((size_t)kn * m + r0 + orow) * ldx + col];
+        } else if (kindh[h] == 2) {
+          aux[h][g] = __ldcg(V.x + ((size_t)k * m + r0 + orow) * ldx + col);
+        }
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (kh[h] < 0) continue;
+      const int k = kh[h], kind = kindh[h];
+      const int q = fseq(h, s);
+      mbar_wait(&fbar[h * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+      const cplx *A = fac + (h * FAC_STAGES + q % FAC_STAGES) * fstride;
+#pragma unroll
+      for (int g = 0; g < GMAX; ++g) {
+        if (g >= Gc) break;
+        // wait for this chain's input vector (the bottom chain's first
+        // backward stage reads x_t from the top chain's buffer)
+        const int hb = (h == 1 && s == F + 1) ? 0 : h;
+        mbar_wait(VBAR(hb, g, p), vph[hb][g][p] & 1);
+        const cplx *X = VEC(hb, g, p);
+        const cplx *X2 = nullptr;
+        if (kind == 1 && nbt > 0) {  // middle: add the bottom chain's part
+          mbar_wait(VBAR(1, g, p), vph[1][g][p] & 1);
+          X2 = VEC(1, g, p);
+        }
+        TRACE(1);
+        // ---- rows [r0, r0+nr) of the block inverse times the vector
+        for (int tile = ntile ? t % ntile : 0, sl = ntile ? t / ntile : nslice;
+             sl < nslice && tile < ntile; tile += SOLVE_THREADS) {
+          const int tr = tile / TC, tc = tile % TC;
+          const int row = 2 * tr, c = 2 * tc;
+          const int j0 = (ntile > SOLVE_THREADS) ? 0 : sl * ks;
+          const int j1 = (ntile > SOLVE_THREADS) ? m : min(m, j0 + ks);
+          cplx a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
+          const cplx *ar0 = A + (size_t)row * m;
+          const cplx *ar1 = ar0 + m;
+          if (X2) {
+            for (int j = j0; j < j1; ++j) {
+              cplx x0 = cadd(X[j * rg + c], X2[j * rg + c]);
+              cplx x1 = cadd(X[j * rg + c + 1], X2[j * rg + c + 1]);
+              cplx f0 = ar0[j], f1 = ar1[j];
+              cfma(a00, f0, x0); cfma(a01, f0, x1); cfma(a10, f1, x0); cfma(a11, f1, x1);
+            }
+          } else {
 #pragma unroll 4
-      for (int j = j0; j < j1; ++j) {
-        cplx x0 = X[j * rcc + c], x1 = X[j * rcc + c + 1];
-        cplx f0 = ar0[j], f1 = ar1[j];
-        cfma(a00, f0, x0);
-        cfma(a01, f0, x1);
-        cfma(a10, f1, x0);
-        cfma(a11, f1, x1);
+            for (int j = j0; j < j1; ++j) {
+              cplx x0 = X[j * rg + c], x1 = X[j * rg + c + 1];
+              cplx f0 = ar0[j], f1 = ar1[j];
+              cfma(a00, f0, x0); cfma(a01, f0, x1); cfma(a10, f1, x0); cfma(a11, f1, x1);
+            }
+          }
+          cplx *rp = red + (size_t)((ntile > SOLVE_THREADS) ? 0 : sl) * rows_max * rg;
+          rp[row * rg + c] = a00;
+          if (c + 1 < rg) rp[row * rg + c + 1] = a01;
+          if (row + 1 < nr) {
+            rp[(row + 1) * rg + c] = a10;
+            if (c + 1 < rg) rp[(row + 1) * rg + c + 1] = a11;
+          }
+          if (ntile <= SOLVE_THREADS) break;
+        }
+        __syncthreads();
+        TRACE(2);
+        // the input phase(s) of this chain are consumed: re-arm for reuse.
+        // x_t (stage F+1) feeds both halves: its last consumer re-arms.
+        const bool shared_xt = (s == F + 1) && nbt > 0;
+        const bool consume = !(shared_xt && h == 0);
+        if (t == 0) {
+          if (consume) mbar_expect_tx(VBAR(hb, g, p), vec_bytes);
+          if (X2) mbar_expect_tx(VBAR(1, g, p), vec_bytes);
+        }
+        if (consume) vph[hb][g][p]++;
+        if (X2) vph[1][g][p]++;
+        // ---- epilogue: outputs and the next-stage vector rows
+        const bool last = s + 1 >= S;
+        if (t < nout) {
+          cplx acc = red[t];
+          if (ntile <= SOLVE_THREADS)
+            for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[(size_t)q2 * rows_max * rg + t]);
+          const size_t off = ((size_t)k * m + r0 + orow) * ldx + chunk0 + g * rg + oc;
+          cplx out, nxt;
+          if (kind == 0) {
+            out = acc;  // y_k (top) / z_k (bottom)
+            if (h == 0) nxt = csub(aux[h][g], cmul(f.lcoef[k + 1], acc));
+            else nxt = csub(aux[h][g], cmul(f.ucoef[k - 1], acc));
+          } else if (kind == 1) {
+            out = acc;  // x_t
+            nxt = acc;
+          } else {
+            out = csub(aux[h][g], cmul(h == 0 ? f.ucoef[k] : f.lcoef[k], acc));
+            nxt = out;
+          }
+          V.x[off] = out;
+          if (!last) XG(h == 1 && kind == 1 ? 0 : h, g, p ^ 1)[(r0 + orow) * rg + oc] = nxt;
+        }
+        fence_proxy_async_global();
+        __syncthreads();
+        TRACE(3);
+        if (t == 0 && !last) push(h, g, p ^ 1);
       }
-      cplx *rp = red + (size_t)((ntile > SOLVE_THREADS) ? 0 : sl) * rows_max * rc;
-      rp[row * rcc + c] = a00;
-      if (c + 1 < rcc) rp[row * rcc + c + 1] = a01;
-      if (row + 1 < nr) {
-        rp[(row + 1) * rcc + c] = a10;
-        if (c + 1 < rcc) rp[(row + 1) * rcc + c + 1] = a11;
-      }
-      if (ntile <= SOLVE_THREADS) break;
-    }
-    __syncthreads();
-    // next-stage block vector rows + outputs
-    if (t < nout) {
-      cplx acc = red[t];
-      if (ntile <= SOLVE_THREADS)
-        for (int q = 1; q < nslice; ++q) acc = cadd(acc, red[(size_t)q * rows_max * rc + t]);
-      size_t off = ((size_t)k * m + r0 + orow) * ldx + chunk0 + oc;
-      cplx nxt;
-      if (fwd) {
-        V.x[off] = acc;  // y_k
-        nxt = (k + 1 < nb) ? csub(aux, cmul(f.lcoef[k + 1], acc)) : acc;
-      } else {
-        cplx xk = csub(aux, cmul(f.ucoef[k], acc));
-        V.x[off] = xk;
-        nxt = xk;
-      }
-      stg[((s + 1) & 1) * rows_max * rc + t] = nxt;
-    }
-    if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[b], vec_bytes);  // phase for stage s+2
-    fence_proxy_async();
-    __syncthreads();
-    if (t == 0 && s + 1 < S && push_bytes) {
-      cplx *src = stg + ((s + 1) & 1) * rows_max * rc;
-      cplx *dst = vec + ((s + 1) & 1) * vstride + r0 * rcc;
-      for (int q = 0; q < C; ++q) bulk_s2peer(dst, src, push_bytes, &vbar[(s + 1) & 1], q);
     }
   }
-  cluster.sync();  // no CTA leaves while peers may still push into it
+  cluster.sync();  // no CTA leaves while multicasts into it may be in flight
 }
 
 static int solve_rows_max(int max_m, int C) {
@@ -251,75 +389,39 @@ static int solve_rows_max(int max_m, int C) {
   return r + (r & 1);  // even: 2-row micro-tiles may read one padding row
 }
 
-static size_t solve_smem(int max_m, int rc, int C) {
+static size_t solve_smem(int max_m, int rc, int C, int G) {
   size_t rows_max = solve_rows_max(max_m, C);
-  size_t elems = 2 * ((size_t)max_m * rc + 2) + 2 * rows_max * rc +
-                 FAC_STAGES * (rows_max * max_m + 2) + 16 * rows_max * rc;
-  return 128 + elems * sizeof(cplx);
+  size_t rg = (rc + G - 1) / G;
+  size_t elems = 4 * G * ((size_t)max_m * rg + 2) + 2 * FAC_STAGES * (rows_max * max_m + 2) +
+                 16 * rows_max * rg;
+  return 256 + elems * sizeof(cplx);
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 // Largest cluster (16 non-portable, then 8, 4) that the occupancy API
-// accepts for this shared-memory footprint.
-static int pick_cluster(int max_m, int rc, size_t *smem_out) {
-  static int cached_key_m = -1, cached_key_rc = -1, cached_C = 0;
-  static size_t cached_smem = 0;
-  if (max_m == cached_key_m && rc == cached_key_rc) {
-    *smem_out = cached_smem;
-    return cached_C;
-  }
-  cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int C : {16, 8, 4}) {
-    size_t smem = solve_smem(max_m, rc, C);
-    if (smem > 232448) continue;
-    if (cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3(C, 1, 1);
-    cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k_block_solve, &cfg) == cudaSuccess &&
-        nclusters > 0) {
-      cached_key_m = max_m;
-      cached_key_rc = rc;
-      cached_C = C;
-      cached_smem = smem;
-      *smem_out = smem;
-      return C;
-    }
-    cudaGetLastError();
-  }
-  return 0;
-}
+// accepts for this shared-memory footprint; RHS chunk rc and groups G.
+struct SolveCfg {
+  int C, rc, G, rows_max;
+  size_t smem;
+};
 
-int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs,
-                          int max_m) {
-  if (nvisit < 1) return DS_OK;
-  int rc = std::min(nrhs, SOLVE_MAX_RC);
-  int nchunks = (nrhs + rc - 1) / rc;
-  size_t smem = 0;
-  int C = pick_cluster(max_m, rc, &smem);
-  if (!C) return ds_fail(DS_ECONFIG, "block solve: no feasible cluster configuration");
-  DS_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
-  int rows_max = solve_rows_max(max_m, C);
+static bool try_cfg(int max_m, int rc, int G, int C, SolveCfg *out) {
+  size_t smem = solve_smem(max_m, rc, C, G);
+  if (smem > 232448) return false;
+  if (cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(C, nvisit, nchunks);
+  cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = C;
@@ -327,8 +429,74 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve, (const SolveVisit *)visits_dev, nrhs, rc,
-                             rows_max));
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k_block_solve, &cfg) != cudaSuccess ||
+      nclusters < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  *out = SolveCfg{C, rc, G, solve_rows_max(max_m, C), smem};
+  return true;
+}
+
+static int pick_cfg(int max_m, int nrhs, SolveCfg *out) {
+  static int key_m = -1, key_r = -1;
+  static SolveCfg cached;
+  if (max_m == key_m && nrhs == key_r) {
+    *out = cached;
+    return 1;
+  }
+  cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const int Cwant = env_int("DS_SOLVE_CLUSTER", 16);
+  const int Gwant = env_int("DS_SOLVE_GROUPS", 1);
+  for (int rc = std::min(nrhs, env_int("DS_SOLVE_RC", 32)); rc >= 1; rc = (rc + 1) / 2) {
+    for (int C : {16, 8, 4}) {
+      if (C > Cwant) continue;
+      int G = Gwant;
+      while (G > 1 && (rc % G != 0 || G > GMAX)) G /= 2;
+      if (try_cfg(max_m, rc, G, C, out)) {
+        key_m = max_m;
+        key_r = nrhs;
+        cached = *out;
+        return 1;
+      }
+    }
+    if (rc == 1) break;
+  }
+  return 0;
+}
+
+int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs,
+                          int max_m) {
+  if (nvisit < 1) return DS_OK;
+  SolveCfg sc;
+  if (!pick_cfg(max_m, nrhs, &sc))
+    return ds_fail(DS_ECONFIG, "block solve: no feasible cluster configuration");
+  DS_CUDA(cudaFuncSetAttribute(k_block_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sc.smem));
+  int nchunks = (nrhs + sc.rc - 1) / sc.rc;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(sc.C, nvisit, nchunks);
+  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = sc.smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = sc.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve, (const SolveVisit *)visits_dev, nrhs, sc.rc,
+                             sc.G, sc.rows_max));
   ctx->launches++;
   return DS_OK;
 }
+
+#ifdef DS_SOLVE_TRACE
+extern "C" DS_API int ds_debug_solve_trace(long long *out) {
+  DS_CUDA(cudaMemcpyFromSymbol(out, g_solve_trace, sizeof(long long) * 2 * 1024 * 6));
+  return DS_OK;
+}
+#endif

@@ -446,6 +446,11 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cplx *bufs;
   if (plan_alloc(P, &mem, sizeof(cplx) * vbuf * 2 * 2 * P->gmax)) return fail(DS_ECUDA);
   bufs = (cplx *)mem;
+  // K3 exchange scratch: 4 * m * nrhs per visit slot (2 parities x Gmax)
+  size_t xgbuf = 4 * (size_t)P->max_m * d->nrhs_max;
+  cplx *xgs;
+  if (plan_alloc(P, &mem, sizeof(cplx) * xgbuf * 2 * P->gmax)) return fail(DS_ECUDA);
+  xgs = (cplx *)mem;
   // ---- flags
   P->flag_words = (size_t)nsub * d->nrhs_max + 4 * (size_t)nsw * nsub * d->nrhs_max + d->nrhs_max;
   if (plan_alloc(P, &mem, sizeof(int) * P->flag_words)) return fail(DS_ECUDA);
@@ -545,7 +550,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
         V.nz = nullptr;  // set per call (depends on nrhs stride)
         visit_of[(size_t)w * nsub + s] = (int)hv.size();
         hv.push_back(V);
-        SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr};
+        SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr,
+                      xgs + ((size_t)parity * P->gmax + gi) * xgbuf};
         hsv.push_back(SV);
       }
       P->xstep_off[step_global] = (int)hx.size();
