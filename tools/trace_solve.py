@@ -36,18 +36,15 @@ dp.apply(fd)
 torch.cuda.synchronize()
 lib = N.load_library()
 fn = lib.ds_debug_solve_trace
-buf = (C.c_longlong * (2 * 1024 * 6))()
+buf = (C.c_longlong * (16 * 1024 * 6))()
 fn(buf)
-tr = np.frombuffer(buf, dtype=np.int64).reshape(2, 1024, 6)
-for rank in range(2):
-    t = tr[rank]
-    n = int(np.argmax(t[:, 0] == 0)) or 1024
-    t = t[:n].astype(np.float64)
-    stage = np.median(np.diff(t[:, 0]))
-    top_wait = np.median(t[:, 1] - t[:, 0])
-    top_comp = np.median(t[:, 2] - t[:, 1])
-    top_epi = np.median(t[:, 3] - t[:, 2])
-    bot_wait = np.median(t[:, 4] - t[:, 3])
-    bot_rest = np.median(t[:, 5] - t[:, 4])
-    print(f"rank {rank}: stages {n} median cycles: top wait {top_wait:.0f} compute {top_comp:.0f} "
-          f"epilogue {top_epi:.0f} | bottom wait {bot_wait:.0f} compute+epilogue {bot_rest:.0f} | stage {stage:.0f}")
+tr = np.frombuffer(buf, dtype=np.int64).reshape(16, 1024, 6)
+for rank in range(16):
+    tt = tr[rank].astype(np.float64)
+    n = int(np.argmax(tt[:, 0] == 0)) or 1024
+    if n < 3:
+        continue
+    tt = tt[:n]
+    print(f"rank {rank:2d}: items {n}  median cycles: to-first-panel {np.median(tt[:,1]-tt[:,0]):.0f}  "
+          f"panels {np.median(tt[:,2]-tt[:,1]):.0f} (of which waiting {np.median(tt[:,4]):.0f})  "
+          f"epilogue {np.median(tt[:,3]-tt[:,2]):.0f}  item {np.median(np.diff(tt[:,0])):.0f}")
