@@ -166,10 +166,36 @@ def run_ours(args, rank, world, local_rank):
     n = part.grid.node_count()
     f_dev = torch.from_numpy(f_host.reshape(R, n)).to(dev)
     nbytes_f = f_host.nbytes
+    gmres_mode = s.mode == "gmres"
+    rhs_apps = [0]  # RHS-applications of the DDM map (for the roofline)
+    iters = {}
+    if gmres_mode:
+        from paper_2002_05327_b200 import gmres_batched
+
+        gop = b["gop"]
+        full = part.grid.full_window()
+        counts = part.grid.counts
+
+        def apply_m(v):
+            rhs_apps[0] += v.shape[0]
+            uu, _ = dp.apply(v.reshape(v.shape[0], -1))
+            return uu.reshape(v.shape)
+
+        def step():
+            x, reps = gmres_batched(lambda v: gop.apply(v, region=full), apply_m,
+                                    f_dev.reshape((R,) + counts), tol=1e-6)
+            iters["n_iter"] = [r.n_iter for r in reps]
+            iters["converged"] = all(r.converged for r in reps)
+            return x
+    else:
+        def step():
+            rhs_apps[0] += R
+            u, _ = dp.apply(f_dev)
+            return u
 
     # ---- warm-up (untimed)
     for _ in range(args.warmup):
-        u, _ = dp.apply(f_dev)
+        step()
     torch.cuda.synchronize()
 
     # ---- timed region: K applications, inputs resident in HBM
@@ -186,9 +212,10 @@ def run_ours(args, rank, world, local_rank):
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
     launches = 0
+    rhs_apps[0] = 0
     for _ in range(args.steps):
-        u, _ = dp.apply(f_dev)
-        launches += dp.last_launches() + 2  # + the two layout kernels
+        step()
+        launches += dp.last_launches() + 2  # + the two layout kernels (per application)
     en.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -208,15 +235,26 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         f_pin = torch.from_numpy(f_host).pin_memory()
         out_pin = torch.empty(f_host.shape, dtype=torch.complex128).pin_memory()
+        if gmres_mode:
+            from paper_2002_05327_b200 import gmres_batched
+
+            def e2e_step():
+                x, _ = gmres_batched(lambda v: gop.apply(v, region=full),
+                                     lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
+                                     f_pin.reshape((R,) + counts), tol=1e-6)
+                return x
+        else:
+            def e2e_step():
+                uu, _ = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
+                return uu.values
         for _ in range(max(1, args.warmup // 2)):
-            uu, _ = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
+            e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         for _ in range(args.steps):
-            uu, reps = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
-            out_pin.copy_(uu.values)  # result already host-side (input was host)
+            out_pin.copy_(e2e_step())  # result already host-side (input was host)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t1) * 1e3 / args.steps
         if world > 1:
@@ -225,11 +263,16 @@ def run_ours(args, rank, world, local_rank):
             e2e_ms = float(tt.item())
         e2e = {"value": world * R / (e2e_ms / 1e3), "unit": "RHS/s",
                "h2d_bytes_per_step": int(nbytes_f), "d2h_bytes_per_step": int(nbytes_f),
-               "ms_per_step": e2e_ms, "api": "diagonal_sweep_solve(pinned host f) -> host u"}
+               "ms_per_step": e2e_ms,
+               "api": ("gmres_batched(gop.apply, diagonal_sweep_solve, pinned host f) -> host x"
+                       if gmres_mode else "diagonal_sweep_solve(pinned host f) -> host u")}
 
     # ---- roofline of the dominant kernel (K3)
     hbm, hbm_src, fp64, fp64_src = peaks()
-    flops, fbytes = algorithmic_work(dp, R)
+    flops1, fbytes1 = algorithmic_work(dp, 1)
+    apps = rhs_apps[0] / max(1, args.steps)  # RHS-applications per step
+    flops = flops1 * apps
+    fbytes = algorithmic_work(dp, R)[1] * (apps / R)
     roofline = None
     kernels = None
     if ktimes:
@@ -250,6 +293,7 @@ def run_ours(args, rank, world, local_rank):
     res = {
         "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2 else
         f"Helmholtz RHS/s ({s.name})",
+        "gmres": iters or None,
         "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
@@ -287,7 +331,10 @@ def cpu_sample(s, b, n_rhs, threads):
         tf = time.perf_counter() - t0
         t1 = time.perf_counter()
         for r in range(n_rhs):
-            O.ddm_apply(prob, oops, cache, f[r % f.shape[0]])
+            if s.mode == "gmres":
+                O.gmres_ddm(prob, oops, prob.global_operator(), cache, f[r % f.shape[0]])
+            else:
+                O.ddm_apply(prob, oops, cache, f[r % f.shape[0]])
         ts = time.perf_counter() - t1
     return tf, ts
 
@@ -309,11 +356,19 @@ def run_reference(args):
         for idx in prob.subdomains:
             cache.get(oops[idx])
         tf = time.perf_counter() - t0
+        gop = prob.global_operator() if s.mode == "gmres" else None
+
+        def one(r):
+            if gop is not None:
+                O.gmres_ddm(prob, oops, gop, cache, f[r % f.shape[0]])
+            else:
+                O.ddm_apply(prob, oops, cache, f[r % f.shape[0]])
+
         for w in range(args.warmup):
-            O.ddm_apply(prob, oops, cache, f[w % f.shape[0]])
+            one(w)
         t1 = time.perf_counter()
         for k in range(args.steps):
-            O.ddm_apply(prob, oops, cache, f[(args.warmup + k) % f.shape[0]])
+            one(args.warmup + k)
         ts = time.perf_counter() - t1
     value = args.steps / ts
     return {
@@ -322,7 +377,9 @@ def run_reference(args):
         "value": value, "unit": "RHS/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ts * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded, SURVEY §8(d))",
-        "config": {"workload": s.name, "step": "one DDM application for one RHS (reference API is single-RHS)",
+        "config": {"workload": s.name,
+                   "step": ("one GMRES-DDM solve" if s.mode == "gmres" else "one DDM application")
+                   + " for one RHS (the reference API is single-RHS)",
                    "factor_s": tf},
         "cpu_baseline": {"value": value, "unit": "RHS/s", "cores": threads, "kind": "port",
                          "sample": f"{args.steps} single-RHS applications after {args.warmup} warm-up; "
@@ -393,10 +450,13 @@ def main():
         s = configs.spec(args.config)
         b = configs.build(s)
         threads = os.cpu_count() or 1
-        tf, ts = cpu_sample(s, b, args.cpu_sample_rhs, threads)
+        nsample = args.cpu_sample_rhs if s.mode != "gmres" else 1
+        tf, ts = cpu_sample(s, b, nsample, threads)
+        args.cpu_sample_rhs = nsample
         res["cpu_baseline"] = {"value": args.cpu_sample_rhs / ts, "unit": "RHS/s", "cores": threads,
                                "kind": "port",
-                               "sample": f"{args.cpu_sample_rhs} single-RHS DDM applications of "
+                               "sample": f"{args.cpu_sample_rhs} single-RHS "
+                                         f"{'GMRES-DDM solves' if s.mode == 'gmres' else 'DDM applications'} of "
                                          f"{s.name} (oracle port, {threads} BLAS threads); "
                                          f"factorization {tf:.2f} s excluded"}
     if rank == 0:

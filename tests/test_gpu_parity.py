@@ -230,3 +230,50 @@ def test_gmres_unbatched_matches_batched(cuda, raster):
     xb, repb = gmres_batched(lambda v: gop.apply(v, region=full), apply_m, f)
     assert rep1.n_iter == repb[0].n_iter
     assert rel(x1, xb[0]) <= 1e-12
+
+
+# ---------------------------------------------------------------- goldens
+# direct comparisons with the reference's own outputs (tests/golden/)
+from pathlib import Path
+import json
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def test_gpu_vs_reference_golden_cfg1(cuda, cfg1):
+    s, b, prob, oops = cfg1
+    g = np.load(GOLD / "ddm_cfg1.npz")
+    f = configs.sources(s, b["grid"])[0]
+    u, rep = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(),
+                                  record_events=True, warn_collar=False)
+    assert rel(u.values, g["u"]) <= TOL
+    assert [rep.solves, rep.nonzero_solves, rep.discarded_sources] == list(g["counters"])
+    assert rep.events == json.loads(str(g["events"]))
+
+
+def test_gpu_vs_reference_golden_compact_and_random(cuda):
+    grid, part, ops, f, prob = _compact_problem()
+    g = np.load(GOLD / "ddm_compact.npz")
+    assert np.array_equal(f, g["source"])
+    rng = np.random.default_rng(2)
+    fr = rng.normal(size=grid.counts) + 1j * rng.normal(size=grid.counts)
+    u, reps = diagonal_sweep_solve(np.stack([f, fr]), part, ops, FactorizationCache(),
+                                   record_events=True, warn_collar=False)
+    assert rel(u.values[0], g["u"]) <= TOL
+    assert rel(u.values[1], g["u_random"]) <= TOL
+    assert reps[0].events == json.loads(str(g["events"]))
+
+
+def test_gpu_vs_reference_golden_raster_gmres(cuda, raster):
+    s, b, prob, oops = raster
+    g = np.load(GOLD / "raster_mini.npz")
+    f = configs.sources(s, b["grid"])[:1]
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    u, _ = diagonal_sweep_solve(f, part, ops, cache, warn_collar=False)
+    assert rel(u.values[0], g["u_ddm"]) <= TOL
+    full = part.grid.full_window()
+    x, reps = gmres_batched(lambda v: gop.apply(v, region=full),
+                            lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
+                            f)
+    assert reps[0].n_iter == int(g["n_iter"])
+    assert rel(x[0], g["x_gmres"]) <= 1e-9
