@@ -119,6 +119,7 @@ struct FactDev {
 
 struct ds_fact {
   std::vector<FactDev> facts;
+  std::vector<std::vector<cplx>> h_l, h_u;  // host copies of l_k, u_k per operator
   std::vector<void *> allocations;
   int64_t bytes_total = 0;
   std::vector<int64_t> bytes;
@@ -149,3 +150,14 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
                           int max_m);
 
 int ceil_div(int a, int b);
+
+// slabs above this size use the blocked factorization and the staged solve
+#define DS_LARGE_SLAB 160
+
+// K3g: staged solve (large slabs); host views of the visits and their
+// factor layouts / block-axis couplings; items_dev: scratch of
+// ds_stage_items_bytes(nvisit, max_nb) bytes
+int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const FactDev *facts_host,
+                           const cplx *const *l_host, const cplx *const *u_host, int nvisit,
+                           int nrhs, void *items_dev, size_t items_cap);
+size_t ds_stage_items_bytes(int nvisit, int max_nb);

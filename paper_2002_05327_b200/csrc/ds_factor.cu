@@ -33,73 +33,12 @@
 #include <vector>
 
 #include "ds_common.cuh"
+#include "ds_factor.cuh"
 
 namespace cg = cooperative_groups;
 
-struct FactJob {
-  OpDev op;
-  FactDev f;
-  cplx *sinv;
-  int half;  // 0 top chain, 1 bottom chain, 2 middle block
-};
-
 #define GJ_THREADS 512
 static const size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
-
-// D_k[i][c] of the block layout (i, c in-slab indices)
-__device__ __forceinline__ cplx d_entry(const FactJob &J, int k, int i, int c) {
-  const OpDev &o = J.op;
-  const FactDev &f = J.f;
-  int ba = f.block_axis;
-  if (f.other[1] < 0) {  // 2D: one in-slab axis
-    int oa = f.other[0];
-    if (c == i) {
-      int coord[3] = {0, 0, 0};
-      coord[ba] = k;
-      coord[oa] = i;
-      double k2;
-      if (o.kappa2_kind == 0) k2 = o.kappa2[0];
-      else if (o.kappa2_kind == 1) k2 = o.kappa2[coord[o.kappa2_axis]];
-      else k2 = o.kappa2[(int64_t)coord[0] * o.shape[1] + coord[1]];
-      cplx acc = make_double2(k2, 0.0);
-      for (int a = 0; a < 2; ++a) {
-        cplx lo = o.c_lo[a][coord[a]], hi = o.c_hi[a][coord[a]];
-        acc.x += -(lo.x + hi.x);
-        acc.y += -(lo.y + hi.y);
-      }
-      return acc;
-    }
-    if (c == i - 1) return o.c_lo[oa][i];
-    if (c == i + 1) return o.c_hi[oa][i];
-    return make_double2(0.0, 0.0);
-  }
-  // 3D: in-slab index i = i0 * n1 + i1 over axes other[0], other[1]
-  int o0 = f.other[0], o1 = f.other[1];
-  int n1 = f.win_shape[o1];
-  int i0 = i / n1, i1 = i % n1;
-  if (c == i) {
-    int coord[3];
-    coord[ba] = k;
-    coord[o0] = i0;
-    coord[o1] = i1;
-    double k2;
-    if (o.kappa2_kind == 0) k2 = o.kappa2[0];
-    else if (o.kappa2_kind == 1) k2 = o.kappa2[coord[o.kappa2_axis]];
-    else k2 = o.kappa2[((int64_t)coord[0] * o.shape[1] + coord[1]) * o.shape[2] + coord[2]];
-    cplx acc = make_double2(k2, 0.0);
-    for (int a = 0; a < 3; ++a) {
-      cplx lo = o.c_lo[a][coord[a]], hi = o.c_hi[a][coord[a]];
-      acc.x += -(lo.x + hi.x);
-      acc.y += -(lo.y + hi.y);
-    }
-    return acc;
-  }
-  if (c == i - 1 && i1 > 0) return o.c_lo[o1][i1];
-  if (c == i + 1 && i1 < n1 - 1) return o.c_hi[o1][i1];
-  if (c == i - n1) return o.c_lo[o0][i0];
-  if (c == i + n1) return o.c_hi[o0][i0];
-  return make_double2(0.0, 0.0);
-}
 
 __global__ void __launch_bounds__(GJ_THREADS, 1)
     k_factor_gj(const FactJob *__restrict__ jobs, int mcper_max, int *status) {
@@ -271,7 +210,8 @@ static void fill_layout(const OpDev &o, FactDev &f) {
   for (int a = o.dim; a < 3; ++a) f.win_shape[a] = 1;
 }
 
-extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact **out) {
+extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n_in, ds_fact **out) {
+  int n = n_in;
   if (!ctx || !ops || n < 1 || !out) return ds_fail(DS_ECONFIG, "ds_fact_create: bad argument");
   ds_fact *F = new ds_fact();
   std::vector<FactJob> jobs(n);
@@ -302,6 +242,8 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact
     f.lcoef = lc;
     f.ucoef = uc;
     F->facts.push_back(f);
+    F->h_l.push_back(ops[i]->h_clo[f.block_axis]);
+    F->h_u.push_back(ops[i]->h_chi[f.block_axis]);
     F->bytes.push_back((int64_t)bytes);
     F->bytes_total += bytes;
     jobs[i].op = o;
@@ -309,17 +251,57 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact
     jobs[i].sinv = sinv;
     maxm = std::max(maxm, f.m);
   }
+  (void)maxm;
+  // small slabs (2D windows): on-chip Gauss-Jordan chains; large (3D): blocked
+  std::vector<FactJob> small, large;
+  std::vector<const cplx *> large_l, large_u;
+  for (int i = 0; i < n; ++i) {
+    if (jobs[i].f.m <= DS_LARGE_SLAB) {
+      small.push_back(jobs[i]);
+    } else {
+      large.push_back(jobs[i]);
+      large_l.push_back(F->h_l[i].data());
+      large_u.push_back(F->h_u[i].data());
+    }
+  }
+  int status = 0;
+  if (!large.empty()) {
+    int *dst = nullptr;
+    DS_CUDA(cudaMalloc(&dst, sizeof(int)));
+    DS_CUDA(cudaMemset(dst, 0, sizeof(int)));
+    int rc = ds_blocked_factor(ctx, large.data(), (int)large.size(), large_l.data(),
+                               large_u.data(), dst);
+    if (rc) {
+      cudaFree(dst);
+      for (void *p : F->allocations) cudaFree(p);
+      delete F;
+      return rc;
+    }
+    DS_CUDA(cudaMemcpy(&status, dst, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dst);
+    if (status) {
+      for (void *p : F->allocations) cudaFree(p);
+      delete F;
+      return ds_fail(DS_ESOLVER, "blocked LU: zero or non-finite pivot in a Schur complement");
+    }
+  }
+  if (small.empty()) {
+    *out = F;
+    return DS_OK;
+  }
+  int smaxm = 0;
+  for (auto &j : small) smaxm = std::max(smaxm, j.f.m);
   int mcper = 0;
   size_t smem = 0;
-  int C = choose_cluster(maxm, &mcper, &smem);
+  int C = choose_cluster(smaxm, &mcper, &smem);
   if (C == 0) {
     for (void *p : F->allocations) cudaFree(p);
     delete F;
-    return ds_fail(DS_ECONFIG,
-                   "ds_fact_create: slab size m=" + std::to_string(maxm) +
-                       " exceeds the on-chip Gauss-Jordan path (3D windows need the "
-                       "blocked path)");
+    return ds_fail(DS_ECONFIG, "ds_fact_create: no on-chip configuration for m=" +
+                                   std::to_string(smaxm));
   }
+  n = (int)small.size();
+  jobs = small;
   // jobs: [top chains | bottom chains] then [middle blocks]
   std::vector<FactJob> chain_jobs, mid_jobs;
   for (int i = 0; i < n; ++i) {
@@ -365,7 +347,6 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n, ds_fact
     ctx->launches++;
   }
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
-  int status = 0;
   DS_CUDA(cudaMemcpy(&status, dstatus, sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(djobs);
   cudaFree(dstatus);
@@ -434,7 +415,18 @@ extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_
   k_permute<<<blocks, 256, 0, ctx->stream>>>(f, (const cplx *)rhs, bin, nrhs, 1);
   ctx->launches++;
   DS_CHECK_LAUNCH();
-  int rc = ds_launch_solve_table(ctx, vis, 1, nrhs, f.m);
+  int rc;
+  if (f.m > DS_LARGE_SLAB) {
+    SolveVisit hvis{fd, bin, bout, nullptr, xg};
+    const cplx *lh = F->h_l[i].data(), *uh = F->h_u[i].data();
+    size_t cap = ds_stage_items_bytes(1, f.nb);
+    void *items = nullptr;
+    DS_CUDA(cudaMallocAsync(&items, cap, ctx->stream));
+    rc = ds_launch_solve_staged(ctx, &hvis, &f, &lh, &uh, 1, nrhs, items, cap);
+    cudaFreeAsync(items, ctx->stream);
+  } else {
+    rc = ds_launch_solve_table(ctx, vis, 1, nrhs, f.m);
+  }
   if (rc) return rc;
   k_permute<<<blocks, 256, 0, ctx->stream>>>(f, bout, (cplx *)x, nrhs, 0);
   ctx->launches++;

@@ -1,0 +1,388 @@
+// K2b: blocked factorization for large slabs (3D windows, m ~ 460-4225).
+//
+// Same twisted block LU as the on-chip path (ds_factor.cu): every chain
+// (operator, half) walks its blocks; at each step the Schur complement
+//     S = D_k - c1 * S_prev1^{-1} - c2 * S_prev2^{-1}
+// is formed directly in the block's factor slot and inverted in place by a
+// right-looking blocked Gauss-Jordan with partial pivoting, panels of
+// BW = 32 columns:
+//   1. panel kernel: one thread-block cluster per matrix keeps the m x BW
+//      panel in distributed shared memory and runs the BW pivot steps
+//      (cluster-wide argmax, row interchange through DSMEM, elimination);
+//   2. the panel's row interchanges are applied to the other columns;
+//   3. rank-BW trailing update A += P' T  (P' = panel with I subtracted on the
+//      pivot rows, T = the pivot rows outside the panel) — a plain complex
+//      GEMM (cuBLAS zgemm), 8 m^2 BW flop per panel.
+// Column interchanges are undone at the end.  All chains of a step are
+// batched (one panel / swap / copy launch per step for every matrix).
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ds_common.cuh"
+#include "ds_factor.cuh"
+
+namespace cg = cooperative_groups;
+
+#define BW 32
+#define PANEL_THREADS 256
+
+struct BlkTask {   // one matrix being inverted at the current chain step
+  FactJob J;       // operator, layout, factor base
+  int k;           // block index
+  cplx co1, co2;   // Schur coefficients (0 if absent)
+  int p1, p2;      // previous blocks (-1 if absent)
+  cplx *A;         // the m x m matrix (factor slot k)
+  int *piv;        // [m] pivot rows
+  cplx *T;         // [BW][m]  pivot rows outside the panel
+  cplx *P;         // [m][BW]  panel with I subtracted on pivot rows
+};
+
+// S = D_k - co1 * A[p1] - co2 * A[p2]   (whole m x m, row-major)
+__global__ void k_form_schur(const BlkTask *__restrict__ tasks) {
+  const BlkTask &X = tasks[blockIdx.y];
+  const int m = X.J.f.m;
+  const cplx *s1 = X.p1 >= 0 ? X.J.sinv + (size_t)X.p1 * m * m : nullptr;
+  const cplx *s2 = X.p2 >= 0 ? X.J.sinv + (size_t)X.p2 * m * m : nullptr;
+  const int64_t total = (int64_t)m * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e / m), c = (int)(e % m);
+    cplx v = d_entry(X.J, X.k, i, c);
+    if (s1) v = csub(v, cmul(X.co1, s1[e]));
+    if (s2) v = csub(v, cmul(X.co2, s2[e]));
+    X.A[e] = v;
+  }
+}
+
+// Panel Gauss-Jordan on columns [p, p+BW) of every task's matrix.  Cluster
+// rank q holds rows [q*rpc, q*rpc + rpc) of the panel in shared memory.
+__global__ void __launch_bounds__(PANEL_THREADS, 1)
+    k_panel_gj(const BlkTask *__restrict__ tasks, int p, int rpc_max, int *status) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank(), C = (int)cluster.num_blocks();
+  const BlkTask &X = tasks[blockIdx.y];
+  const int m = X.J.f.m;
+  if (p >= m) return;  // uniform for the cluster
+  const int bw = min(BW, m - p);
+  const int rpc = (m + C - 1) / C;
+  const int r0 = rank * rpc, r1 = min(m, r0 + rpc);
+  const int t = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx *pan = (cplx *)smem_raw;            // [rpc_max][BW]
+  cplx *rowj = pan + (size_t)rpc_max * BW; // [BW]
+  cplx *rowp = rowj + BW;                  // [BW]
+  __shared__ double cand_v[1];
+  __shared__ int cand_i[1];
+  __shared__ double red_v[PANEL_THREADS / 32];
+  __shared__ int red_i[PANEL_THREADS / 32];
+  __shared__ int s_piv;
+
+  for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
+    int r = e / BW, c = e % BW;
+    pan[e] = c < bw ? X.A[(size_t)(r0 + r) * m + p + c] : make_double2(0.0, 0.0);
+  }
+  cluster.sync();
+  for (int jj = 0; jj < bw; ++jj) {
+    const int j = p + jj;
+    // (a) local argmax of |A[r][j]|_1 over my rows r >= j
+    double best = -1.0;
+    int bi = m;
+    for (int r = max(r0, j) + t; r < r1; r += PANEL_THREADS) {
+      double v = cabs1(pan[(r - r0) * BW + jj]);
+      if (v > best || (v == best && r < bi)) { best = v; bi = r; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      double ov = __shfl_down_sync(0xffffffffu, best, off);
+      int oi = __shfl_down_sync(0xffffffffu, bi, off);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if ((t & 31) == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bi; }
+    __syncthreads();
+    if (t == 0) {
+      double bv = red_v[0];
+      int bidx = red_i[0];
+      for (int w = 1; w < PANEL_THREADS / 32; ++w)
+        if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
+      cand_v[0] = bv;
+      cand_i[0] = bidx;
+    }
+    cluster.sync();
+    // (b) global pivot (same decision in every CTA)
+    if (t == 0) {
+      double bv = -1.0;
+      int bidx = m;
+      for (int q = 0; q < C; ++q) {
+        double v = *cluster.map_shared_rank(&cand_v[0], q);
+        int i = *cluster.map_shared_rank(&cand_i[0], q);
+        if (v > bv || (v == bv && i < bidx)) { bv = v; bidx = i; }
+      }
+      s_piv = bidx;
+      if (rank == 0) X.piv[j] = bidx;
+      if (!(bv > 0.0) || bidx >= m) atomicExch(status, 1);
+    }
+    __syncthreads();
+    const int pv = min(s_piv, m - 1);
+    // (c) fetch rows j and pv from their owners
+    if (t < BW) {
+      int qj = j / rpc, qp = pv / rpc;
+      cplx *pj = cluster.map_shared_rank(pan, qj);
+      cplx *pp = cluster.map_shared_rank(pan, qp);
+      rowj[t] = pj[(j - qj * rpc) * BW + t];
+      rowp[t] = pp[(pv - qp * rpc) * BW + t];
+    }
+    cluster.sync();  // all reads done before anyone writes
+    // (d) eliminate: new row j = old row pv scaled; other rows updated
+    const cplx pivot = rowp[jj];
+    const cplx inv = cinv(pivot);
+    for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
+      const int r = r0 + e / BW, c = e % BW;
+      if (c >= bw) continue;
+      const cplx v = r == j ? rowp[c] : (r == pv ? rowj[c] : pan[e]);
+      const cplx fr = r == j ? rowp[jj] : (r == pv ? rowj[jj] : pan[(r - r0) * BW + jj]);
+      cplx nv;
+      if (r == j) {
+        nv = c == jj ? inv : cmul(v, inv);
+      } else if (c == jj) {
+        nv = cmul(make_double2(-fr.x, -fr.y), inv);
+      } else {
+        nv = csub(v, cmul(fr, cmul(rowp[c], inv)));
+      }
+      pan[e] = nv;
+    }
+    cluster.sync();
+  }
+  for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
+    int r = e / BW, c = e % BW;
+    if (c < bw) X.A[(size_t)(r0 + r) * m + p + c] = pan[e];
+  }
+}
+
+// apply the panel's row interchanges to the columns outside the panel
+__global__ void k_row_swaps(const BlkTask *__restrict__ tasks, int p) {
+  const BlkTask &X = tasks[blockIdx.y];
+  const int m = X.J.f.m;
+  if (p >= m) return;
+  const int bw = min(BW, m - p);
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m; c += gridDim.x * blockDim.x) {
+    if (c >= p && c < p + bw) continue;
+    for (int jj = 0; jj < bw; ++jj) {
+      const int j = p + jj, pv = X.piv[j];
+      if (pv == j) continue;
+      cplx a = X.A[(size_t)j * m + c], b = X.A[(size_t)pv * m + c];
+      X.A[(size_t)j * m + c] = b;
+      X.A[(size_t)pv * m + c] = a;
+    }
+  }
+}
+
+// T = pivot rows outside the panel (zero on panel columns); P' = panel - I_R
+__global__ void k_panel_operands(const BlkTask *__restrict__ tasks, int p) {
+  const BlkTask &X = tasks[blockIdx.y];
+  const int m = X.J.f.m;
+  if (p >= m) return;
+  const int bw = min(BW, m - p);
+  const int64_t nT = (int64_t)BW * m, nP = (int64_t)m * BW;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nT + nP;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < nT) {
+      int tr = (int)(e / m), c = (int)(e % m);
+      cplx v = make_double2(0.0, 0.0);
+      if (tr < bw && !(c >= p && c < p + bw)) v = X.A[(size_t)(p + tr) * m + c];
+      X.T[e] = v;
+    } else {
+      int64_t f = e - nT;
+      int r = (int)(f / BW), tc = (int)(f % BW);
+      cplx v = make_double2(0.0, 0.0);
+      if (tc < bw) {
+        v = X.A[(size_t)r * m + p + tc];
+        if (r == p + tc) v.x -= 1.0;
+      }
+      X.P[f] = v;
+    }
+  }
+}
+
+// undo the column interchanges: A[r][c] <- A[r][src[c]] (one CTA per row)
+__global__ void k_col_unpermute(const BlkTask *__restrict__ tasks, int *srcbuf, int mmax) {
+  const BlkTask &X = tasks[blockIdx.y];
+  const int m = X.J.f.m;
+  int *src = srcbuf + (size_t)blockIdx.y * mmax;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx *row = (cplx *)smem_raw;
+  for (int r = blockIdx.x; r < m; r += gridDim.x) {
+    for (int c = threadIdx.x; c < m; c += blockDim.x) row[c] = X.A[(size_t)r * m + c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += blockDim.x) X.A[(size_t)r * m + c] = row[src[c]];
+    __syncthreads();
+  }
+}
+
+__global__ void k_src_map(const BlkTask *__restrict__ tasks, int *srcbuf, int mmax) {
+  const BlkTask &X = tasks[blockIdx.x];
+  const int m = X.J.f.m;
+  int *src = srcbuf + (size_t)blockIdx.x * mmax;
+  if (threadIdx.x != 0) return;
+  for (int c = 0; c < m; ++c) src[c] = c;
+  for (int j = m - 1; j >= 0; --j) {
+    int a = src[j];
+    src[j] = src[X.piv[j]];
+    src[X.piv[j]] = a;
+  }
+}
+
+static int launch_cluster(const void *kern, dim3 grid, int C, size_t smem, cudaStream_t st,
+                          void **args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(PANEL_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  return DS_OK;
+}
+
+int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *const *lh,
+                      const cplx *const *uh, int *status) {
+  if (njobs == 0) return DS_OK;
+  cudaStream_t st = ctx->stream;
+  int mmax = 0;
+  for (int i = 0; i < njobs; ++i) mmax = std::max(mmax, jobs[i].f.m);
+  // panel cluster: enough CTAs that the panel rows fit in shared memory
+  int PC = 4;
+  while (PC < 16 && ((size_t)((mmax + PC - 1) / PC) * BW + 2 * BW) * sizeof(cplx) > 200 * 1024) PC *= 2;
+  const int rpc_max = (mmax + PC - 1) / PC;
+  const size_t panel_smem = ((size_t)rpc_max * BW + 2 * BW) * sizeof(cplx);
+  if (panel_smem > 220 * 1024) return ds_fail(DS_ECONFIG, "blocked factorization: slab too large");
+  // per-chain workspaces (pivots, T, P', unpermute map)
+  std::vector<void *> ws;
+  auto alloc = [&](size_t bytes) -> void * {
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    ws.push_back(p);
+    return p;
+  };
+  const int nchains = 2 * njobs;
+  int *piv = (int *)alloc(sizeof(int) * (size_t)nchains * mmax);
+  int *srcb = (int *)alloc(sizeof(int) * (size_t)nchains * mmax);
+  cplx *Tb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * BW * mmax);
+  cplx *Pb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * BW * mmax);
+  BlkTask *dtasks = (BlkTask *)alloc(sizeof(BlkTask) * nchains);
+  auto cleanup = [&]() {
+    for (void *p : ws) cudaFree(p);
+  };
+  if (!piv || !srcb || !Tb || !Pb || !dtasks) {
+    cleanup();
+    return ds_fail(DS_ECUDA, "blocked factorization: out of device memory for workspaces");
+  }
+  cublasHandle_t hb;
+  if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) {
+    cleanup();
+    return ds_fail(DS_ECUDA, "cublasCreate failed");
+  }
+  cublasSetStream(hb, st);
+  cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem);
+  cudaFuncSetAttribute(k_col_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(mmax * sizeof(cplx)));
+  int rc = DS_OK;
+  // phases: 0 = chains (top and bottom halves together), 1 = middle blocks
+  for (int phase = 0; phase < 2 && rc == DS_OK; ++phase) {
+    int maxsteps = 0;
+    for (int i = 0; i < njobs; ++i) {
+      const FactDev &f = jobs[i].f;
+      maxsteps = std::max(maxsteps, phase == 0 ? std::max(f.twist, f.nb - 1 - f.twist) : 1);
+    }
+    for (int step = 0; step < maxsteps && rc == DS_OK; ++step) {
+      std::vector<BlkTask> tasks;
+      std::vector<int> task_job;
+      for (int i = 0; i < njobs; ++i) {
+        const FactJob &J = jobs[i];
+        const FactDev &f = J.f;
+        const int ba = f.block_axis, nb = f.nb, tw = f.twist;
+        for (int half = (phase == 0 ? 0 : 2); half <= (phase == 0 ? 1 : 2); ++half) {
+          int nsteps = half == 0 ? tw : (half == 1 ? nb - 1 - tw : 1);
+          if (step >= nsteps) continue;
+          BlkTask X;
+          memset(&X, 0, sizeof(X));
+          X.J = J;
+          X.k = half == 0 ? step : (half == 1 ? nb - 1 - step : tw);
+          X.p1 = X.p2 = -1;
+          const int k = X.k;
+          if ((half == 0 || half == 2) && k > 0) X.p1 = k - 1;
+          if ((half == 1 || half == 2) && k < nb - 1) X.p2 = k + 1;
+          // coefficients from the host copies held by the job's operator view
+          X.A = J.sinv + (size_t)k * f.m * f.m;
+          size_t slot = tasks.size();
+          X.piv = piv + slot * mmax;
+          X.T = Tb + slot * BW * mmax;
+          X.P = Pb + slot * BW * mmax;
+          (void)ba;
+          tasks.push_back(X);
+          task_job.push_back(i);
+        }
+      }
+      if (tasks.empty()) continue;
+      // Schur coefficients from the host copies of the block-axis couplings
+      for (size_t ti = 0; ti < tasks.size(); ++ti) {
+        BlkTask &X = tasks[ti];
+        const cplx *hl = lh[task_job[ti]], *hu = uh[task_job[ti]];
+        const int k = X.k;
+        if (X.p1 >= 0) X.co1 = cmul(hl[k], hu[k - 1]);  // l_k u_{k-1}
+        if (X.p2 >= 0) X.co2 = cmul(hu[k], hl[k + 1]);  // u_k l_{k+1}
+      }
+      const int nt = (int)tasks.size();
+      DS_CUDA(cudaMemcpyAsync(dtasks, tasks.data(), sizeof(BlkTask) * nt, cudaMemcpyHostToDevice, st));
+      int mstep = 0;
+      for (auto &X : tasks) mstep = std::max(mstep, X.J.f.m);
+      k_form_schur<<<dim3(std::max(1, std::min(1024, (int)((int64_t)mstep * mstep / 256 / 4))), nt), 256, 0, st>>>(dtasks);
+      ctx->launches++;
+      for (int p = 0; p < mstep && rc == DS_OK; p += BW) {
+        void *args[] = {(void *)&dtasks, (void *)&p, (void *)&rpc_max, (void *)&status};
+        rc = launch_cluster((const void *)k_panel_gj, dim3(PC, nt, 1), PC, panel_smem, st, args);
+        if (rc) break;
+        k_row_swaps<<<dim3((mstep + 255) / 256, nt), 256, 0, st>>>(dtasks, p);
+        k_panel_operands<<<dim3(std::max(1, (2 * BW * mstep + 255) / 256), nt), 256, 0, st>>>(dtasks, p);
+        ctx->launches += 3;
+        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+        for (auto &X : tasks) {
+          const int m = X.J.f.m;
+          if (p >= m) continue;
+          // row-major A(m x m) += P'(m x BW) T(BW x m)  ==  col-major A^T += T^T P'^T
+          cublasStatus_t cs = cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, BW, &one,
+                                          (const cuDoubleComplex *)X.T, m,
+                                          (const cuDoubleComplex *)X.P, BW, &one,
+                                          (cuDoubleComplex *)X.A, m);
+          if (cs != CUBLAS_STATUS_SUCCESS) {
+            rc = ds_fail(DS_ECUDA, "cublasZgemm failed in the blocked factorization");
+            break;
+          }
+          ctx->launches++;
+        }
+        DS_CHECK_LAUNCH();
+      }
+      if (rc) break;
+      k_src_map<<<nt, 32, 0, st>>>(dtasks, srcb, mmax);
+      k_col_unpermute<<<dim3(std::min(mstep, 512), nt), 256, mmax * sizeof(cplx), st>>>(dtasks, srcb, mmax);
+      ctx->launches += 2;
+      DS_CHECK_LAUNCH();
+      DS_CUDA(cudaStreamSynchronize(st));  // tasks vector reused next step
+    }
+  }
+  cublasDestroy(hb);
+  cudaStreamSynchronize(st);
+  cleanup();
+  return rc;
+}

@@ -88,6 +88,12 @@ struct ds_plan {
   // host copies of the visit tables; nz pointers are patched per nrhs stride
   std::vector<VisitDev> h_visits;
   std::vector<SolveVisit> h_solve;
+  // staged (large-slab) solve: host factor layouts and couplings per subdomain
+  bool staged = false;
+  std::vector<FactDev> h_facts;
+  std::vector<const cplx *> h_l, h_u;
+  void *stage_items = nullptr;
+  size_t stage_cap = 0;
   int patched_nrhs = 0;
   // graph
   bool use_graph = false;
@@ -394,6 +400,11 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   }
   if (plan_alloc(P, &mem, sizeof(FactDev) * nsub)) return fail(DS_ECUDA);
   P->facts = (FactDev *)mem;
+  P->h_facts = hf;
+  for (int s = 0; s < nsub; ++s) {
+    P->h_l.push_back(d->fact_of_sub[s]->h_l[d->fact_index[s]].data());
+    P->h_u.push_back(d->fact_of_sub[s]->h_u[d->fact_index[s]].data());
+  }
   cudaMemcpy(P->facts, hf.data(), sizeof(FactDev) * nsub, cudaMemcpyHostToDevice);
   // ---- beta00 ramps
   int64_t nbeta = 0;
@@ -439,6 +450,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cudaMemcpy(P->subs, hs.data(), sizeof(SubDev) * nsub, cudaMemcpyHostToDevice);
   // ---- steps and visit buffers
   P->gmax = 0;
+  int max_nb = 0;
+  for (int s = 0; s < nsub; ++s) max_nb = std::max(max_nb, hf[s].nb);
   for (int w = 0; w < nsw; ++w)
     for (int t = 0; t < nst; ++t)
       P->gmax = std::max(P->gmax, d->step_off[w * (nst + 1) + t + 1] - d->step_off[w * (nst + 1) + t]);
@@ -451,6 +464,11 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cplx *xgs;
   if (plan_alloc(P, &mem, sizeof(cplx) * xgbuf * 2 * P->gmax)) return fail(DS_ECUDA);
   xgs = (cplx *)mem;
+  P->staged = P->max_m > DS_LARGE_SLAB;
+  if (P->staged) {
+    P->stage_cap = ds_stage_items_bytes(P->gmax, max_nb);
+    if (plan_alloc(P, &P->stage_items, P->stage_cap)) return fail(DS_ECUDA);
+  }
   // ---- flags
   P->flag_words = (size_t)nsub * d->nrhs_max + 4 * (size_t)nsw * nsub * d->nrhs_max + d->nrhs_max;
   if (plan_alloc(P, &mem, sizeof(int) * P->flag_words)) return fail(DS_ECUDA);
@@ -704,7 +722,21 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       ctx->launches++;
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
-      int rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
+      int rc;
+      if (P->staged) {
+        std::vector<FactDev> fh(G);
+        std::vector<const cplx *> lh(G), uh(G);
+        for (int g = 0; g < G; ++g) {
+          int sub = P->h_visits[v0 + g].sub;
+          fh[g] = P->h_facts[sub];
+          lh[g] = P->h_l[sub];
+          uh[g] = P->h_u[sub];
+        }
+        rc = ds_launch_solve_staged(ctx, P->h_solve.data() + v0, fh.data(), lh.data(), uh.data(),
+                                    G, nrhs, P->stage_items, P->stage_cap);
+      } else {
+        rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
+      }
       if (rc) return rc;
       DS_CHECK_LAUNCH();
       prof_mark(P, 2, st);
@@ -744,7 +776,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
     P->slots_dirty = false;
   }
-  if (P->use_graph && !P->profiling) {
+  if (P->use_graph && !P->profiling && !P->staged) {
     bool match = P->graph && P->graph_f == f && P->graph_u == u && P->graph_nrhs == nrhs &&
                  P->graph_partials == partials;
     if (!match) {
