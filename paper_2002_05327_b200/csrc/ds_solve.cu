@@ -90,16 +90,21 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
 
+#ifndef FAC_STAGES
 #define FAC_STAGES 2
+#endif
 #define GMAX 4
 
 #ifdef DS_SOLVE_TRACE
 __device__ long long g_solve_trace[2][1024][6];
 // slot 0: stage start; 1/2/3: top chain after wait / compute / epilogue;
 // 4/5: bottom chain after wait / epilogue
+// slots: 0 stage start; top 1 after vec wait, 2 after compute, 3 after epilogue;
+// bottom 4 after vec wait, 5 after epilogue; 6/7 after the top/bottom factor wait
 #define TRACE(i)                                                                   \
-  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0 && rank < 2 && s < 1024)       \
-    g_solve_trace[rank][s][(i) == 0 ? 0 : (h == 0 ? (i) : ((i) == 1 ? 4 : ((i) == 3 ? 5 : 6)))] = clock64();
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0 && rank < 16 && s < 1024 &&    \
+      ((i) == 0 || h == 0 || (i) != 2))                                             \
+    g_solve_trace[rank][s][(i) == 0 ? 0 : (h == 0 ? (i) : ((i) == 1 ? 4 : 5))] = clock64();
 #else
 #define TRACE(i)
 #endif
@@ -224,8 +229,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         mbar_expect_tx(VBAR(h, g, 0), vec_bytes);
         mbar_expect_tx(VBAR(h, g, 1), vec_bytes);
       }
-    load_tile(0, 0);  // stage-0 tiles; the loop loads stage s+1 at stage s
-    load_tile(1, 0);
+    for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {  // ring prologue
+      load_tile(0, st);
+      load_tile(1, st);
+    }
   }
   // prologue: b_0 for the top chain (stage F-nt), b_{n_b-1} for the bottom
   // chain (stage F-nbt); written to the exchange scratch then multicast
@@ -259,10 +266,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   for (s = 0; s < S; ++s) {
     const int p = s & 1;
     { const int h = 0; (void)h; TRACE(0); }
-    // refill the factor rings for stage s+1 (slot consumed at stage s-1)
-    if (t == 0 && s + 1 < S) {
-      load_tile(0, s + 1);
-      load_tile(1, s + 1);
+    // refill the factor rings FAC_STAGES-1 stages ahead (slot freed at s-1)
+    if (t == 0 && s + FAC_STAGES - 1 < S) {
+      load_tile(0, s + FAC_STAGES - 1);
+      load_tile(1, s + FAC_STAGES - 1);
     }
     int kindh[2], kh[2];
     kh[0] = block_of(0, s, kindh[0]);
@@ -291,6 +298,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       const int k = kh[h], kind = kindh[h];
       const int q = fseq(h, s);
       mbar_wait(&fbar[h * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+#ifdef DS_SOLVE_TRACE
+      if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0 && rank < 16 && s < 1024)
+        g_solve_trace[rank][s][6 + h] = clock64();
+#endif
       const cplx *A = fac + (h * FAC_STAGES + q % FAC_STAGES) * fstride;
 #pragma unroll
       for (int g = 0; g < GMAX; ++g) {

@@ -81,6 +81,17 @@ __global__ void k_exchange(int rounds, int rows, int rc, double2 *gbuf, long lon
         uint32_t rb = mapa(&bar[b], t);
         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
       }
+    } else if (MODE == 4) {
+      // st.async: every thread stores its values straight into each peer's
+      // buffer; completion is counted by the peer's mbarrier (complete_tx)
+      for (int e = t; e < rows * rc; e += blockDim.x) {
+        double2 v = stg[b * rows * rc + e];
+        for (int q = 0; q < C; ++q) {
+          uint32_t dst = mapa(vec + b * n + rank * rows * rc + e, q), rb = mapa(&bar[b], q);
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                       ::"r"(dst), "d"(v.x), "d"(v.y), "r"(rb) : "memory");
+        }
+      }
     } else if (MODE == 3) {
       // own rows -> global, then one multicast bulk load of my rows to all CTAs
       double2 *g = gbuf + (size_t)blockIdx.y * 2 * n + b * n + rank * rows * rc;
@@ -146,6 +157,10 @@ void run(int C, int rows, int rc, int nclusters) {
 }
 
 int main() {
+  run<4>(16, 8, 16, 1);
+  run<4>(16, 8, 16, 7);
+  run<4>(16, 8, 8, 1);
+  run<4>(8, 15, 16, 1);
   run<3>(16, 8, 16, 1);
   run<3>(16, 8, 16, 7);
   run<0>(16, 8, 4, 1);

@@ -1,8 +1,6 @@
-"""Per-stage phase latencies of K3 from a DS_SOLVE_TRACE build.
-
-Builds a traced copy of the library into /tmp, runs one config-2 application
-and prints median cycles per phase: wait (vector + factor), compute (+ K
-reduction), epilogue + push.
+"""Per-stage phase latencies of K3 (row-split, twisted) from a DS_SOLVE_TRACE
+build: builds a traced copy of the library (TRACE_LIB, TRACE_FLAGS), runs one
+config-2 application and prints per-rank median cycles per phase.
 """
 import ctypes as C
 import os
@@ -12,8 +10,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-lib_path = "/tmp/libdiagsweep_trace.so"
-env = dict(os.environ, NVCC_APPEND_FLAGS="-DDS_SOLVE_TRACE")
+lib_path = os.environ.get("TRACE_LIB", "/tmp/libdiagsweep_trace.so")
+env = dict(os.environ, NVCC_APPEND_FLAGS=os.environ.get("TRACE_FLAGS", "-DDS_SOLVE_TRACE"))
 subprocess.run(["bash", str(ROOT / "paper_2002_05327_b200/csrc/build.sh"), lib_path], check=True, env=env)
 os.environ["DIAGSWEEP_B200_LIB"] = lib_path
 
@@ -35,16 +33,20 @@ fd = torch.from_numpy(f.reshape(f.shape[0], -1)).cuda()
 dp.apply(fd)
 torch.cuda.synchronize()
 lib = N.load_library()
-fn = lib.ds_debug_solve_trace
-buf = (C.c_longlong * (16 * 1024 * 6))()
-fn(buf)
-tr = np.frombuffer(buf, dtype=np.int64).reshape(16, 1024, 6)
+buf = (C.c_longlong * (16 * 1024 * 8))()
+lib.ds_debug_solve_trace(buf)
+tr = np.frombuffer(buf, dtype=np.int64).reshape(16, 1024, 8)
 for rank in range(16):
     tt = tr[rank].astype(np.float64)
     n = int(np.argmax(tt[:, 0] == 0)) or 1024
     if n < 3:
         continue
     tt = tt[:n]
-    print(f"rank {rank:2d}: items {n}  median cycles: to-first-panel {np.median(tt[:,1]-tt[:,0]):.0f}  "
-          f"panels {np.median(tt[:,2]-tt[:,1]):.0f} (of which waiting {np.median(tt[:,4]):.0f})  "
-          f"epilogue {np.median(tt[:,3]-tt[:,2]):.0f}  item {np.median(np.diff(tt[:,0])):.0f}")
+    med = lambda a: float(np.median(a))
+    print(f"rank {rank:2d}: stage {med(np.diff(tt[:,0])):.0f} | top: factor-wait {med(tt[:,6]-tt[:,0]):.0f} "
+          f"vec-wait {med(tt[:,1]-tt[:,6]):.0f} compute {med(tt[:,2]-tt[:,1]):.0f} epilogue {med(tt[:,3]-tt[:,2]):.0f} "
+          f"| bottom: factor-wait {med(tt[:,7]-tt[:,3]):.0f} vec-wait {med(tt[:,4]-tt[:,7]):.0f} "
+          f"compute+epi {med(tt[:,5]-tt[:,4]):.0f}")
+print("raw rank0 stage10:", tr[0, 10].tolist())
+print("raw rank5 stage10:", tr[5, 10].tolist())
+print("nonzero ranks:", [r for r in range(16) if tr[r].any()])
