@@ -160,4 +160,4 @@ int ceil_div(int a, int b);
 int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const FactDev *facts_host,
                            const cplx *const *l_host, const cplx *const *u_host, int nvisit,
                            int nrhs, void *items_dev, size_t items_cap);
-size_t ds_stage_items_bytes(int nvisit, int max_nb);
+size_t ds_stage_items_bytes(int nvisit, int max_nb, int max_m, int nrhs);

@@ -419,7 +419,7 @@ extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_
   if (f.m > DS_LARGE_SLAB) {
     SolveVisit hvis{fd, bin, bout, nullptr, xg};
     const cplx *lh = F->h_l[i].data(), *uh = F->h_u[i].data();
-    size_t cap = ds_stage_items_bytes(1, f.nb);
+    size_t cap = ds_stage_items_bytes(1, f.nb, f.m, nrhs);
     void *items = nullptr;
     DS_CUDA(cudaMallocAsync(&items, cap, ctx->stream));
     rc = ds_launch_solve_staged(ctx, &hvis, &f, &lh, &uh, 1, nrhs, items, cap);

@@ -20,8 +20,9 @@
 #include "ds_common.cuh"
 
 #define ST_THREADS 256
-#define ST_ROWS 64   // rows of the block inverse per CTA
-#define ST_KC 256    // vin rows per shared-memory chunk
+#define ST_ROWS 32   // rows of the block inverse per CTA
+#define ST_KL 8      // K lanes per row (lanes 8i..8i+7 share a row)
+#define ST_KC 128    // vin rows per shared-memory chunk (x2 buffers)
 #define ST_RC 8      // right-hand sides per grid.z chunk
 
 struct StageItem {
@@ -35,8 +36,39 @@ struct StageItem {
   cplx ecoef;                // bwd epilogue: x_k = aux - ecoef * acc
 };
 
-__global__ void __launch_bounds__(ST_THREADS)
-    k_stage_gemv(const StageItem *__restrict__ items, int nrhs) {
+// vin of every item of a stage, formed once: [item][m][nrhs] (global scratch)
+__global__ void k_stage_vin(const StageItem *__restrict__ items, int nrhs, cplx *vin_all,
+                            size_t vin_stride) {
+  const StageItem &I = items[blockIdx.y];
+  const int m = I.m;
+  const size_t ldx = nrhs;
+  cplx *vout = vin_all + blockIdx.y * vin_stride;
+  const int64_t total = (int64_t)m * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const size_t j = e / nrhs, col = e % nrhs;
+    cplx v;
+    if (I.kind == 2) {
+      v = I.x[((size_t)I.ka * m + j) * ldx + col];  // x_{k+-1}
+    } else {
+      v = I.has_b ? I.rhs[((size_t)I.k * m + j) * ldx + col] : make_double2(0.0, 0.0);
+      if (I.ka >= 0) v = csub(v, cmul(I.la, I.x[((size_t)I.ka * m + j) * ldx + col]));
+      if (I.kb >= 0) v = csub(v, cmul(I.lb, I.x[((size_t)I.kb * m + j) * ldx + col]));
+    }
+    vout[e] = v;
+  }
+}
+
+__device__ __forceinline__ void st_cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(ST_THREADS, 3)
+    k_stage_gemv(const StageItem *__restrict__ items, int nrhs, const cplx *vin_all,
+                 size_t vin_stride) {
   const StageItem &I = items[blockIdx.y];
   const int m = I.m;
   const int r0 = blockIdx.x * ST_ROWS;
@@ -45,47 +77,67 @@ __global__ void __launch_bounds__(ST_THREADS)
   const int rcc = min(ST_RC, nrhs - c0);
   if (rcc <= 0) return;
   const int t = threadIdx.x;
-  const int row = r0 + (t >> 2), kq = t & 3;
+  const int row = r0 + t / ST_KL, kq = t % ST_KL;
   const bool rvalid = row < m;
   const size_t ldx = nrhs;
   const cplx *A = I.f->sinv + ((size_t)I.k * m) * m;
-  __shared__ cplx vin[ST_KC][ST_RC];
+  const cplx *vg = vin_all + blockIdx.y * vin_stride;
+  // rows padded to ST_RC+1: the 8 K-lanes of a warp read 8 different rows,
+  // a 128-B row stride would put them all on the same 4 banks
+  __shared__ __align__(16) cplx vin[2][ST_KC][ST_RC + 1];
   cplx acc[ST_RC];
 #pragma unroll
   for (int c = 0; c < ST_RC; ++c) acc[c] = make_double2(0.0, 0.0);
-  for (int j0 = 0; j0 < m; j0 += ST_KC) {
-    const int jn = min(ST_KC, m - j0);
-    __syncthreads();
+  auto prefetch = [&](int chunk) {  // vin rows [chunk*KC, ...) -> buffer chunk&1
+    const int j0 = chunk * ST_KC, jn = min(ST_KC, m - j0);
+    cplx(*dst)[ST_RC + 1] = vin[chunk & 1];
     for (int e = t; e < jn * ST_RC; e += ST_THREADS) {
       const int jj = e / ST_RC, c = e % ST_RC;
-      cplx v = make_double2(0.0, 0.0);
-      if (c < rcc) {
-        const size_t col = c0 + c, j = j0 + jj;
-        if (I.has_b) v = I.rhs[((size_t)I.k * m + j) * ldx + col];
-        if (I.ka >= 0) v = csub(v, cmul(I.la, I.x[((size_t)I.ka * m + j) * ldx + col]));
-        if (I.kb >= 0) v = csub(v, cmul(I.lb, I.x[((size_t)I.kb * m + j) * ldx + col]));
-        if (I.kind == 2) v = I.x[((size_t)I.ka * m + j) * ldx + col];  // x_{k+-1}
-      }
-      vin[jj][c] = v;
+      if (c < rcc) st_cp_async16(&dst[jj][c], vg + (size_t)(j0 + jj) * ldx + c0 + c);
+      else dst[jj][c] = make_double2(0.0, 0.0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int nchunk = (m + ST_KC - 1) / ST_KC;
+  prefetch(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int j0 = ch * ST_KC, jn = min(ST_KC, m - j0);
+    if (ch + 1 < nchunk) {
+      prefetch(ch + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
+    cplx(*V)[ST_RC + 1] = vin[ch & 1];
     if (rvalid) {
+      // 8 independent 16-B factor loads in flight per thread, then the FMAs
       const cplx *a = A + (size_t)row * m + j0;
-#pragma unroll 4
-      for (int jj = kq; jj < jn; jj += 4) {
-        const cplx av = __ldg(a + jj);
+      int jj = kq;
+      for (; jj + 7 * ST_KL < jn; jj += 8 * ST_KL) {
+        cplx av[8];
 #pragma unroll
-        for (int c = 0; c < ST_RC; ++c) cfma(acc[c], av, vin[jj][c]);
+        for (int u = 0; u < 8; ++u) av[u] = __ldcs(a + jj + u * ST_KL);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int c = 0; c < ST_RC; ++c) cfma(acc[c], av[u], V[jj + u * ST_KL][c]);
+      }
+      for (; jj < jn; jj += ST_KL) {
+        const cplx av = __ldcs(a + jj);
+#pragma unroll
+        for (int c = 0; c < ST_RC; ++c) cfma(acc[c], av, V[jj][c]);
       }
     }
+    __syncthreads();  // buffer ch&1 is refilled two chunks later
   }
 #pragma unroll
-  for (int c = 0; c < ST_RC; ++c) {
-    acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, 1);
-    acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, 1);
-    acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, 2);
-    acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, 2);
-  }
+  for (int c = 0; c < ST_RC; ++c)
+#pragma unroll
+    for (int off = 1; off < ST_KL; off <<= 1) {
+      acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
+      acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
+    }
   if (rvalid && kq == 0) {
 #pragma unroll
     for (int c = 0; c < ST_RC; ++c) {
@@ -175,19 +227,28 @@ int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const Fac
     }
   }
   off[S] = (int)items.size();
-  if (items.size() * sizeof(StageItem) > items_cap)
-    return ds_fail(DS_ECONFIG, "staged solve: item table too small");
+
   DS_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(StageItem),
                           cudaMemcpyHostToDevice, ctx->stream));
   int mmax = 0;
   for (int v = 0; v < nvisit; ++v) mmax = std::max(mmax, facts_host[v].m);
   const int nchunks = (nrhs + ST_RC - 1) / ST_RC;
+  // vin scratch follows the item table in the workspace
+  const size_t item_bytes = ((items.size() * sizeof(StageItem) + 255) / 256) * 256;
+  const size_t vin_stride = (size_t)mmax * nrhs;
+  int maxn = 0;
+  for (int s = 0; s < S; ++s) maxn = std::max(maxn, off[s + 1] - off[s]);
+  if (item_bytes + (size_t)maxn * vin_stride * sizeof(cplx) > items_cap)
+    return ds_fail(DS_ECONFIG, "staged solve: workspace too small");
+  cplx *vin_all = (cplx *)((char *)items_dev + item_bytes);
   for (int s = 0; s < S; ++s) {
     int n = off[s + 1] - off[s];
     if (!n) continue;
+    int vb = (int)std::min<int64_t>(256, ((int64_t)mmax * nrhs + 255) / 256);
+    k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
     dim3 grid((mmax + ST_ROWS - 1) / ST_ROWS, n, nchunks);
-    k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(ditems + off[s], nrhs);
-    ctx->launches++;
+    k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
+    ctx->launches += 2;
   }
   DS_CHECK_LAUNCH();
   // the host item vector must outlive the async copy
@@ -195,6 +256,8 @@ int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const Fac
   return DS_OK;
 }
 
-size_t ds_stage_items_bytes(int nvisit, int max_nb) {
-  return sizeof(StageItem) * (size_t)nvisit * 2 * (2 * max_nb + 2);
+size_t ds_stage_items_bytes(int nvisit, int max_nb, int max_m, int nrhs) {
+  size_t items = sizeof(StageItem) * (size_t)nvisit * 2 * (2 * max_nb + 2);
+  items = ((items + 255) / 256) * 256;
+  return items + (size_t)nvisit * 2 * max_m * nrhs * sizeof(cplx);
 }

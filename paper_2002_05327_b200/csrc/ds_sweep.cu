@@ -466,7 +466,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   xgs = (cplx *)mem;
   P->staged = P->max_m > DS_LARGE_SLAB;
   if (P->staged) {
-    P->stage_cap = ds_stage_items_bytes(P->gmax, max_nb);
+    P->stage_cap = ds_stage_items_bytes(P->gmax, max_nb, P->max_m, d->nrhs_max);
     if (plan_alloc(P, &P->stage_items, P->stage_cap)) return fail(DS_ECUDA);
   }
   // ---- flags

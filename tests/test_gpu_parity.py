@@ -346,3 +346,26 @@ def test_cfg4_full_size_parity(cuda):
     assert rel(u.values[0], ref) <= TOL
     assert reps[0].nonzero_solves == orep["nonzero_solves"]
     assert reps[0].discarded_sources == orep["discarded_sources"]
+
+
+def test_cfg5r_gmres_vs_reference_golden(cuda):
+    """Config 5r (3D raster, 57^2x45, 4x4x4, the oracle-feasible stand-in for
+    config 5): batched GMRES-DDM vs the reference's own solution
+    (tests/golden/make_golden_5r.py, 64 SuperLU factorizations, ~5 min CPU)."""
+    import hashlib
+
+    g = np.load(GOLD / "gmres_cfg5r.npz")
+    s = configs.spec("5r")
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"])
+    assert hashlib.sha256(np.ascontiguousarray(f[0]).tobytes()).hexdigest() == str(g["source_sha"])
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    full = part.grid.full_window()
+    x, reps = gmres_batched(lambda v: gop.apply(v, region=full),
+                            lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
+                            f, tol=1e-6)
+    assert reps[0].n_iter == int(g["n_iter"]) and reps[0].converged
+    assert rel(x[0], g["x"]) <= 1e-9, rel(x[0], g["x"])
+    np.testing.assert_allclose(reps[0].residuals, g["residuals"], rtol=1e-6, atol=1e-12)
+    assert all(r.converged for r in reps)

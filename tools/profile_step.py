@@ -19,7 +19,7 @@ s = configs.spec(cfg)
 b = configs.build(s)
 f = configs.sources(s, b["grid"])
 part, ops = b["partition"], b["ops"]
-cache = FactorizationCache()
+cache = FactorizationCache(share_translates=(part.dim == 3 and s.medium == "constant"))
 dp = device_plan(part, ops, cache, SweepPlan.default(part.dim), f.shape[0])
 fd = torch.from_numpy(f.reshape(f.shape[0], -1)).cuda()
 for _ in range(napp):
