@@ -352,14 +352,24 @@ class DevicePlan:
                                  0 if partials is None else partials.data_ptr()),
                 "ds_ddm_apply")
 
+    def _minor_buffers(self, R, device):
+        """Persistent RHS-minor f/u buffers per batch size (stable pointers let
+        the native side replay its captured CUDA graph)."""
+        bufs = getattr(self, "_bufs", None)
+        if bufs is None:
+            bufs = self._bufs = {}
+        if R not in bufs:
+            fmin = torch.empty((self.nnodes, R), dtype=torch.complex128, device=device)
+            bufs[R] = (fmin, torch.empty_like(fmin))
+        return bufs[R]
+
     def apply(self, f, collect_partials: bool = False):
         """f: [R, N] complex128 CUDA tensor (RHS-outer) -> (u [R, N], partials)."""
         lib, ctx = context()
         R = f.shape[0]
         n = self.nnodes
-        fmin = torch.empty((n, R), dtype=torch.complex128, device=f.device)
+        fmin, umin = self._minor_buffers(R, f.device)
         N.check(lib.ds_layout_to_minor(ctx, n, R, f.data_ptr(), fmin.data_ptr()))
-        umin = torch.empty_like(fmin)
         partials = None
         if collect_partials:
             partials = torch.empty((self.nsweeps, n, R), dtype=torch.complex128, device=f.device)

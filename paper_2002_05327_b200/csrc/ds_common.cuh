@@ -161,3 +161,14 @@ int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const Fac
                            const cplx *const *l_host, const cplx *const *u_host, int nvisit,
                            int nrhs, void *items_dev, size_t items_cap);
 size_t ds_stage_items_bytes(int nvisit, int max_nb, int max_m, int nrhs);
+
+// stage programs: all stage items of all steps of a plan, built once; one
+// launch per stage (small slabs: fused PDL kernel; large: vin + GEMV)
+struct StageProgram;
+StageProgram *ds_stage_program_create(const std::vector<std::vector<SolveVisit>> &step_visits,
+                                      const std::vector<std::vector<FactDev>> &step_facts,
+                                      const std::vector<std::vector<const cplx *>> &step_l,
+                                      const std::vector<std::vector<const cplx *>> &step_u,
+                                      int nrhs_max, std::string *err);
+int ds_stage_program_launch_step(ds_ctx *ctx, StageProgram *P, int step, int nrhs);
+void ds_stage_program_destroy(StageProgram *P);

@@ -14,7 +14,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "ds_common.cuh"
@@ -260,4 +262,255 @@ size_t ds_stage_items_bytes(int nvisit, int max_nb, int max_m, int nrhs) {
   size_t items = sizeof(StageItem) * (size_t)nvisit * 2 * (2 * max_nb + 2);
   items = ((items + 255) / 256) * 256;
   return items + (size_t)nvisit * 2 * max_m * nrhs * sizeof(cplx);
+}
+
+// ------------------------------------------------------------------------
+// Small slabs (2D windows, m <= DS_LARGE_SLAB): one fused kernel per stage,
+// launched with programmatic dependent launch.  Before griddepcontrol.wait a
+// CTA only prefetches its rows of the block inverse (read-only, independent
+// of the chain), so the next stage's prologue overlaps the current stage.
+template <int RC>
+__global__ void __launch_bounds__(ST_THREADS)
+    k_stage_small(const StageItem *__restrict__ items, int nrhs, int rt) {
+  const StageItem &I = items[blockIdx.y];
+  const int m = I.m;
+  const int r0 = blockIdx.x * rt;
+  const int c0 = blockIdx.z * RC;
+  const int t = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx *At = (cplx *)smem_raw;        // [rt][m]
+  cplx *vin = At + (size_t)rt * m;    // [m][RC+1]
+  const bool active = r0 < m && c0 < nrhs;
+  const int nr = active ? min(rt, m - r0) : 0;
+  if (active) {
+    const cplx *src = I.f->sinv + ((size_t)I.k * m + r0) * m;
+    for (int e = t; e < nr * m; e += ST_THREADS) st_cp_async16(At + e, src + e);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (!active) return;
+  const int rcc = min(RC, nrhs - c0);
+  const size_t ldx = nrhs;
+  // form vin with every global load of a thread in flight at once (the loads
+  // are L2 round trips on the critical path of the chain)
+  constexpr int VPT = 12;  // m * RC <= 12 * ST_THREADS for m <= DS_LARGE_SLAB
+  {
+    cplx b[VPT], xa[VPT], xb[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int e = t + u * ST_THREADS;
+      const int j = e / RC, c = e % RC;
+      const bool ok = e < m * RC && c < rcc;
+      const size_t col = c0 + c;
+      b[u] = xa[u] = xb[u] = make_double2(0.0, 0.0);
+      if (ok) {
+        if (I.has_b) b[u] = I.rhs[((size_t)I.k * m + j) * ldx + col];
+        if (I.ka >= 0) xa[u] = I.x[((size_t)I.ka * m + j) * ldx + col];
+        if (I.kb >= 0) xb[u] = I.x[((size_t)I.kb * m + j) * ldx + col];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int e = t + u * ST_THREADS;
+      if (e >= m * RC) break;
+      const int j = e / RC, c = e % RC;
+      cplx v = xa[u];  // bwd: x_{k+-1}
+      if (I.kind != 2) v = csub(csub(b[u], cmul(I.la, xa[u])), cmul(I.lb, xb[u]));
+      vin[j * (RC + 1) + c] = v;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  // outputs (row, c) of this tile; KS lanes split K for each output
+  const int nout = rt * RC;
+  int KS = ST_THREADS / nout;
+  KS = KS >= 32 ? 32 : (KS >= 16 ? 16 : (KS >= 8 ? 8 : (KS >= 4 ? 4 : (KS >= 2 ? 2 : 1))));
+  for (int base = 0; base < nout; base += ST_THREADS / KS) {
+    const int o = base + t / KS, ks = t % KS;
+    const bool valid = o < nout;
+    const int row = valid ? o / RC : 0, c = valid ? o % RC : 0;
+    cplx a0 = make_double2(0.0, 0.0), a1 = a0;
+    if (valid && row < nr) {
+      const cplx *a = At + (size_t)row * m;
+      int j = ks;
+      for (; j + KS < m; j += 2 * KS) {
+        cfma(a0, a[j], vin[j * (RC + 1) + c]);
+        cfma(a1, a[j + KS], vin[(j + KS) * (RC + 1) + c]);
+      }
+      if (j < m) cfma(a0, a[j], vin[j * (RC + 1) + c]);
+    }
+    cplx acc = cadd(a0, a1);
+    for (int off = 1; off < KS; off <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (valid && row < nr && ks == 0 && c < rcc) {
+      const size_t off = ((size_t)I.k * m + r0 + row) * ldx + c0 + c;
+      if (I.kind == 2) {
+        const cplx aux = I.x[off];
+        I.x[off] = csub(aux, cmul(I.ecoef, acc));
+      } else {
+        I.x[off] = acc;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// Stage programs: every stage item of every step, built once per plan.
+struct StageProgram {
+  StageItem *items = nullptr;           // device
+  std::vector<std::vector<int>> off;    // [step][stage + 1] offsets into items
+  std::vector<int> base;                // [step] first item of the step
+  int max_m = 0;
+  bool small = true;
+  cplx *vin = nullptr;                  // large path scratch
+  size_t vin_elems = 0;
+  int max_items_stage = 0;
+};
+
+StageProgram *ds_stage_program_create(const std::vector<std::vector<SolveVisit>> &step_visits,
+                                      const std::vector<std::vector<FactDev>> &step_facts,
+                                      const std::vector<std::vector<const cplx *>> &step_l,
+                                      const std::vector<std::vector<const cplx *>> &step_u,
+                                      int nrhs_max, std::string *err) {
+  StageProgram *P = new StageProgram();
+  std::vector<StageItem> all;
+  for (size_t q = 0; q < step_visits.size(); ++q) {
+    const auto &vs = step_visits[q];
+    const auto &fs = step_facts[q];
+    P->base.push_back((int)all.size());
+    int S = 0;
+    for (auto &f : fs) {
+      S = std::max(S, 2 * std::max(f.twist, f.nb - 1 - f.twist) + 1);
+      P->max_m = std::max(P->max_m, f.m);
+    }
+    std::vector<int> off(S + 1, 0);
+    for (int s = 0; s < S; ++s) {
+      off[s] = (int)all.size();
+      for (size_t v = 0; v < vs.size(); ++v) {
+        const FactDev &f = fs[v];
+        const int Fv = std::max(f.twist, f.nb - 1 - f.twist);
+        if (s >= 2 * Fv + 1) continue;
+        for (int half = 0; half < 2; ++half) {
+          StageItem I;
+          memset(&I, 0, sizeof(I));
+          if (!stage_item(f, s, half, I)) continue;
+          I.f = vs[v].f;
+          I.rhs = vs[v].rhs;
+          I.x = vs[v].x;
+          const int k = I.k, tw = f.twist, nb = f.nb;
+          const cplx lk = step_l[q][v][k], uk = step_u[q][v][k];
+          if (I.kind == 0) {
+            I.has_b = 1;
+            if (half == 0 && k > 0) { I.ka = k - 1; I.la = lk; }
+            if (half == 1 && k < nb - 1) { I.ka = k + 1; I.la = uk; }
+          } else if (I.kind == 1) {
+            I.has_b = 1;
+            if (tw > 0) { I.ka = tw - 1; I.la = lk; }
+            if (tw < nb - 1) { I.kb = tw + 1; I.lb = uk; }
+          } else {
+            I.ka = half == 0 ? k + 1 : k - 1;
+            I.ecoef = half == 0 ? uk : lk;
+          }
+          all.push_back(I);
+        }
+      }
+      P->max_items_stage = std::max(P->max_items_stage, (int)all.size() - off[s]);
+    }
+    off[S] = (int)all.size();
+    for (auto &o : off) o -= P->base.back();
+    P->off.push_back(off);
+  }
+  P->small = P->max_m <= DS_LARGE_SLAB;
+  if (cudaMalloc(&P->items, std::max<size_t>(1, all.size()) * sizeof(StageItem)) != cudaSuccess) {
+    *err = "stage program: out of device memory";
+    delete P;
+    return nullptr;
+  }
+  cudaMemcpy(P->items, all.data(), all.size() * sizeof(StageItem), cudaMemcpyHostToDevice);
+  if (!P->small) {
+    P->vin_elems = (size_t)P->max_items_stage * P->max_m * nrhs_max;
+    if (cudaMalloc(&P->vin, std::max<size_t>(1, P->vin_elems) * sizeof(cplx)) != cudaSuccess) {
+      cudaFree(P->items);
+      *err = "stage program: out of device memory (vin scratch)";
+      delete P;
+      return nullptr;
+    }
+  }
+  return P;
+}
+
+void ds_stage_program_destroy(StageProgram *P) {
+  if (!P) return;
+  cudaFree(P->items);
+  cudaFree(P->vin);
+  delete P;
+}
+
+static int small_rows(int m, int nitems, int nchunk, int nsm) {
+  // rows per CTA (DS_STAGE_ROWS, default 16): every CTA re-forms the whole
+  // block vector from L2, so fewer, fatter tiles are cheaper
+  (void)m; (void)nitems; (void)nchunk; (void)nsm;
+  const char *v = getenv("DS_STAGE_ROWS");
+  return v && *v ? atoi(v) : 16;
+}
+
+template <int RC>
+static int launch_small(ds_ctx *ctx, const StageItem *items, int n, int nrhs, int m) {
+  const int nchunk = (nrhs + RC - 1) / RC;
+  const int rt = small_rows(m, n, nchunk, ctx->num_sms);
+  size_t smem = ((size_t)rt * m + (size_t)m * (RC + 1)) * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_stage_small<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((m + rt - 1) / rt, n, nchunk);
+  cfg.blockDim = dim3(ST_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_stage_small<RC>, items, nrhs, rt));
+  ctx->launches++;
+  return DS_OK;
+}
+
+int ds_stage_program_launch_step(ds_ctx *ctx, StageProgram *P, int step, int nrhs) {
+  const auto &off = P->off[step];
+  const StageItem *base = P->items + P->base[step];
+  const int S = (int)off.size() - 1;
+  const int m = P->max_m;
+  for (int s = 0; s < S; ++s) {
+    const int n = off[s + 1] - off[s];
+    if (!n) continue;
+    const StageItem *it = base + off[s];
+    int rc;
+    if (P->small) {
+      if (nrhs >= 16) rc = launch_small<16>(ctx, it, n, nrhs, m);
+      else if (nrhs >= 8) rc = launch_small<8>(ctx, it, n, nrhs, m);
+      else if (nrhs >= 4) rc = launch_small<4>(ctx, it, n, nrhs, m);
+      else if (nrhs >= 2) rc = launch_small<2>(ctx, it, n, nrhs, m);
+      else rc = launch_small<1>(ctx, it, n, nrhs, m);
+      if (rc) return rc;
+    } else {
+      const size_t vin_stride = (size_t)m * nrhs;
+      if ((size_t)n * vin_stride > P->vin_elems)
+        return ds_fail(DS_ECONFIG, "stage program: vin scratch too small");
+      int vb = (int)std::min<int64_t>(256, ((int64_t)m * nrhs + 255) / 256);
+      k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
+      dim3 grid((m + ST_ROWS - 1) / ST_ROWS, n, (nrhs + ST_RC - 1) / ST_RC);
+      k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
+      ctx->launches += 2;
+    }
+  }
+  DS_CHECK_LAUNCH();
+  return DS_OK;
 }

@@ -23,7 +23,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <map>
+#include <string>
 #include <tuple>
 #include <vector>
 
@@ -94,10 +96,13 @@ struct ds_plan {
   std::vector<const cplx *> h_l, h_u;
   void *stage_items = nullptr;
   size_t stage_cap = 0;
+  StageProgram *program = nullptr;  // stage-per-launch solve (large slabs, or DS_SOLVE_MODE=staged)
   int patched_nrhs = 0;
   // graph
   bool use_graph = false;
   cudaGraphExec_t graph = nullptr;
+  cudaStream_t gstream = nullptr;      // private stream for capture / replay
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   const void *graph_f = nullptr;
   void *graph_u = nullptr;
   void *graph_partials = nullptr;
@@ -464,11 +469,11 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cplx *xgs;
   if (plan_alloc(P, &mem, sizeof(cplx) * xgbuf * 2 * P->gmax)) return fail(DS_ECUDA);
   xgs = (cplx *)mem;
-  P->staged = P->max_m > DS_LARGE_SLAB;
-  if (P->staged) {
-    P->stage_cap = ds_stage_items_bytes(P->gmax, max_nb, P->max_m, d->nrhs_max);
-    if (plan_alloc(P, &P->stage_items, P->stage_cap)) return fail(DS_ECUDA);
+  {
+    const char *mode = getenv("DS_SOLVE_MODE");
+    P->staged = P->max_m > DS_LARGE_SLAB || (mode && std::string(mode) == "staged");
   }
+  (void)max_nb;
   // ---- flags
   P->flag_words = (size_t)nsub * d->nrhs_max + 4 * (size_t)nsw * nsub * d->nrhs_max + d->nrhs_max;
   if (plan_alloc(P, &mem, sizeof(int) * P->flag_words)) return fail(DS_ECUDA);
@@ -632,6 +637,27 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->h_visits = hv;
   P->h_solve = hsv;
   P->patched_nrhs = 0;
+  if (P->staged) {
+    std::vector<std::vector<SolveVisit>> sv;
+    std::vector<std::vector<FactDev>> sf;
+    std::vector<std::vector<const cplx *>> sl, su;
+    for (size_t q = 0; q + 1 < P->vstep_off.size(); ++q) {
+      sv.emplace_back();
+      sf.emplace_back();
+      sl.emplace_back();
+      su.emplace_back();
+      for (int i = P->vstep_off[q]; i < P->vstep_off[q + 1]; ++i) {
+        int sub = hv[i].sub;
+        sv.back().push_back(hsv[i]);
+        sf.back().push_back(hf[sub]);
+        sl.back().push_back(P->h_l[sub]);
+        su.back().push_back(P->h_u[sub]);
+      }
+    }
+    std::string err;
+    P->program = ds_stage_program_create(sv, sf, sl, su, d->nrhs_max, &err);
+    if (!P->program) return fail(ds_fail(DS_ECUDA, err));
+  }
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return fail(ds_fail(DS_ECUDA, std::string("ds_plan_create: ") + cudaGetErrorString(err)));
@@ -645,7 +671,11 @@ extern "C" int64_t ds_plan_last_launches(const ds_plan *P) { return P ? P->last_
 extern "C" int ds_plan_destroy(ds_plan *P) {
   if (!P) return DS_OK;
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  if (P->gstream) cudaStreamDestroy(P->gstream);
+  if (P->gev_in) cudaEventDestroy(P->gev_in);
+  if (P->gev_out) cudaEventDestroy(P->gev_out);
   for (auto e : P->ev) cudaEventDestroy(e);
+  ds_stage_program_destroy(P->program);
   for (void *p : P->allocs) cudaFree(p);
   delete P;
   return DS_OK;
@@ -723,17 +753,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
       int rc;
-      if (P->staged) {
-        std::vector<FactDev> fh(G);
-        std::vector<const cplx *> lh(G), uh(G);
-        for (int g = 0; g < G; ++g) {
-          int sub = P->h_visits[v0 + g].sub;
-          fh[g] = P->h_facts[sub];
-          lh[g] = P->h_l[sub];
-          uh[g] = P->h_u[sub];
-        }
-        rc = ds_launch_solve_staged(ctx, P->h_solve.data() + v0, fh.data(), lh.data(), uh.data(),
-                                    G, nrhs, P->stage_items, P->stage_cap);
+      if (P->program) {
+        rc = ds_stage_program_launch_step(ctx, P->program, q, nrhs);
       } else {
         rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
       }
@@ -776,19 +797,31 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
     P->slots_dirty = false;
   }
-  if (P->use_graph && !P->profiling && !P->staged) {
+  if (P->use_graph && !P->profiling) {
+    // capture / replay on a private stream (the caller's stream may be the
+    // legacy default stream, which cannot be captured), ordered by events
+    if (!P->gstream) {
+      DS_CUDA(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
+      DS_CUDA(cudaEventCreateWithFlags(&P->gev_in, cudaEventDisableTiming));
+      DS_CUDA(cudaEventCreateWithFlags(&P->gev_out, cudaEventDisableTiming));
+    }
+    cudaStream_t user = ctx->stream;
     bool match = P->graph && P->graph_f == f && P->graph_u == u && P->graph_nrhs == nrhs &&
                  P->graph_partials == partials;
+    DS_CUDA(cudaEventRecord(P->gev_in, user));
+    DS_CUDA(cudaStreamWaitEvent(P->gstream, P->gev_in, 0));
     if (!match) {
       if (P->graph) {
         cudaGraphExecDestroy(P->graph);
         P->graph = nullptr;
       }
       cudaGraph_t g;
-      DS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      ctx->stream = P->gstream;
+      DS_CUDA(cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal));
       int64_t l0 = ctx->launches;
       rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
-      cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+      cudaError_t e = cudaStreamEndCapture(P->gstream, &g);
+      ctx->stream = user;
       if (rc) {
         P->slots_dirty = true;
         return rc;
@@ -802,7 +835,9 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
       P->graph_partials = partials;
       ctx->launches = l0;
     }
-    DS_CUDA(cudaGraphLaunch(P->graph, ctx->stream));
+    DS_CUDA(cudaGraphLaunch(P->graph, P->gstream));
+    DS_CUDA(cudaEventRecord(P->gev_out, P->gstream));
+    DS_CUDA(cudaStreamWaitEvent(user, P->gev_out, 0));
     ctx->launches += P->last_launches;
     return DS_OK;
   }
