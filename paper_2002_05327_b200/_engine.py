@@ -86,7 +86,11 @@ def from_device_batch(t, kind, batched):
     if kind == "numpy":
         return t.cpu().numpy()
     if kind == "torch_cpu":
-        return t.cpu()
+        # host result in pinned memory (one DMA, no pageable staging copy)
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
     return t
 
 
