@@ -327,6 +327,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
           cplx a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
           const cplx *ar0 = A + (size_t)row * m;
           const cplx *ar1 = ar0 + m;
+#ifdef K3_NO_COMPUTE
+          if (true) {
+          } else
+#endif
           if (X2) {
             for (int j = j0; j < j1; ++j) {
               cplx x0 = cadd(X[j * rg + c], X2[j * rg + c]);
@@ -363,14 +367,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         }
         if (consume) vph[hb][g][p]++;
         if (X2) vph[1][g][p]++;
-        // ---- epilogue: outputs and the next-stage vector rows
+        // ---- epilogue: next-stage vector rows first (they gate the peers),
+        // the y/x outputs after the push so the proxy fence only waits for
+        // the exchange rows
         const bool last = s + 1 >= S;
+        cplx out = make_double2(0.0, 0.0);
+        size_t off = 0;
         if (t < nout) {
           cplx acc = red[t];
           if (ntile <= SOLVE_THREADS)
             for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[(size_t)q2 * rows_max * rg + t]);
-          const size_t off = ((size_t)k * m + r0 + orow) * ldx + chunk0 + g * rg + oc;
-          cplx out, nxt;
+          off = ((size_t)k * m + r0 + orow) * ldx + chunk0 + g * rg + oc;
+          cplx nxt;
           if (kind == 0) {
             out = acc;  // y_k (top) / z_k (bottom)
             if (h == 0) nxt = csub(aux[h][g], cmul(f.lcoef[k + 1], acc));
@@ -382,13 +390,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
             out = csub(aux[h][g], cmul(h == 0 ? f.ucoef[k] : f.lcoef[k], acc));
             nxt = out;
           }
-          V.x[off] = out;
           if (!last) XG(h == 1 && kind == 1 ? 0 : h, g, p ^ 1)[(r0 + orow) * rg + oc] = nxt;
         }
         fence_proxy_async_global();
         __syncthreads();
-        TRACE(3);
         if (t == 0 && !last) push(h, g, p ^ 1);
+        if (t < nout) V.x[off] = out;
+        TRACE(3);
       }
     }
   }
