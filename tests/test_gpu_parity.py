@@ -369,3 +369,74 @@ def test_cfg5r_gmres_vs_reference_golden(cuda):
     assert rel(x[0], g["x"]) <= 1e-9, rel(x[0], g["x"])
     np.testing.assert_allclose(reps[0].residuals, g["residuals"], rtol=1e-6, atol=1e-12)
     assert all(r.converged for r in reps)
+
+
+def test_cfg3_full_size_gmres_parity(cuda):
+    """Config 3 at full size (1241x441, 16x8 raster windows): RHS 0 of the
+    64-RHS batch against the oracle's SuperLU-based GMRES-DDM (iterations
+    equal, solution <= 1e-9, residual history to 1e-6)."""
+    s = configs.spec(3)
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"])[:2]
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    full = part.grid.full_window()
+    x, reps = gmres_batched(lambda v: gop.apply(v, region=full),
+                            lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
+                            f, tol=1e-6)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    xr, orep = O.gmres_ddm(prob, prob.operators(), prob.global_operator(), O.Cache(), f[0])
+    assert reps[0].n_iter == orep["n_iter"] and reps[0].converged
+    assert rel(x[0], xr) <= 1e-9, rel(x[0], xr)
+    np.testing.assert_allclose(reps[0].residuals, orep["residuals"], rtol=1e-6, atol=1e-12)
+
+
+def test_edge_cases_zero_sources_and_errors(cuda, cfg1):
+    """Exactly-zero sources (every visit skipped, zero counters), GMRES with
+    a zero right-hand side (krylov.py:58-64), and the reference's error
+    behaviour for mismatched shapes / unknown methods."""
+    from paper_2002_05327_b200 import ConfigurationError, factorize
+
+    s, b, prob, oops = cfg1
+    counts = b["grid"].counts
+    z = np.zeros((2,) + counts, dtype=np.complex128)
+    f = configs.sources(s, b["grid"])
+    batch = np.concatenate([z[:1], f[:1], z[1:]])
+    cache = FactorizationCache()
+    u, reps = diagonal_sweep_solve(batch, b["partition"], b["ops"], cache, warn_collar=False)
+    assert not np.any(u.values[0]) and not np.any(u.values[2])
+    assert reps[0].nonzero_solves == 0 and reps[0].discarded_sources == 0
+    assert reps[1].nonzero_solves > 0
+    ref, _ = O.ddm_apply(prob, oops, O.Cache(), f[0])
+    assert rel(u.values[1], ref) <= TOL
+    gop, full = b["gop"], b["partition"].grid.full_window()
+    x, rep = gmres(lambda v: gop.apply(v, region=full),
+                   lambda v: diagonal_sweep_solve(v, b["partition"], b["ops"], cache,
+                                                  warn_collar=False)[0].values, z[0])
+    assert rep.converged and rep.residuals == [0.0] and rep.n_iter == 0 and not np.any(x)
+    with pytest.raises(ConfigurationError):
+        diagonal_sweep_solve(np.zeros((5, 5), complex), b["partition"], b["ops"], cache)
+    op = b["ops"][(1, 1)]
+    with pytest.raises(ConfigurationError):
+        op.apply(np.zeros((3, 3), complex))
+    with pytest.raises(ConfigurationError):
+        cache.get(op).solve(np.zeros((4, 4), complex))
+    with pytest.raises(ConfigurationError):
+        factorize(op, "nope")
+
+
+def test_many_rhs_chunking(cuda, cfg1):
+    """More right-hand sides than one native launch takes (chunks of 256)."""
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(3)
+    counts = b["grid"].counts
+    base = rng.standard_normal((3,) + counts) + 1j * rng.standard_normal((3,) + counts)
+    coef = rng.standard_normal((260, 3))
+    batch = np.einsum("rk,k...->r...", coef, base)
+    u, reps = diagonal_sweep_solve(batch, b["partition"], b["ops"], FactorizationCache(),
+                                   warn_collar=False)
+    assert len(reps) == 260
+    ub, _ = diagonal_sweep_solve(base, b["partition"], b["ops"], FactorizationCache(),
+                                 warn_collar=False)
+    want = np.einsum("rk,k...->r...", coef, ub.values)
+    assert np.linalg.norm(u.values - want) / np.linalg.norm(want) < 1e-10
