@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "ds_common.cuh"
 
@@ -403,6 +404,251 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   cluster.sync();  // no CTA leaves while multicasts into it may be in flight
 }
 
+// K3 v5: the two half-chains fused into one pass per stage.  The ablation
+// in DESIGN.md shows the per-stage cost is dominated by fixed overheads
+// (barrier waits, two __syncthreads, reduction, proxy fence, push issue), so
+// both halves now share them: threads 0-127 compute the top block, 128-255
+// the bottom block, one mbarrier per stage parity collects both halves'
+// rows (expected bytes = halves delivering to that stage), and both halves'
+// rows are multicast back-to-back.
+__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+    k_block_solve5(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const SolveVisit V = visits[blockIdx.y];
+  const FactDev f = *V.f;
+  const int m = f.m, nb = f.nb, tw = f.twist;
+  const int chunk0 = blockIdx.z * rc;
+  const int rg = min(rc, nrhs - chunk0);
+  const int t = threadIdx.x;
+  const int hh = t >> 7, tl = t & 127;  // my half, my lane within the half
+  if (V.nz) {
+    int any = 0;
+    for (int r = 0; r < rg; ++r) any |= V.nz[chunk0 + r];
+    if (!any) return;
+  }
+  const int rows_per = (m + C - 1) / C;
+  const int r0 = rank * rows_per;
+  const int nr = max(0, min(rows_per, m - r0));
+  const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
+  const size_t ldx = nrhs;
+  const uint16_t mask = (uint16_t)((1u << C) - 1);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *vbar = (uint64_t *)smem_raw;  // [2 parity]
+  uint64_t *fbar = vbar + 2;              // [2 halves][FAC_STAGES]
+  cplx *vec = (cplx *)(smem_raw + 256);   // [2 halves][2 parity][vstride]
+  const int vstride = m * rc + 2;
+  cplx *fac = vec + 4 * vstride;          // [2 halves][FAC_STAGES][fstride]
+  const int fstride = rows_max * m + 2;
+  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][8 slices][rows_max*rc]
+  const int rstride = rows_max * rc;
+  auto VEC = [&](int h, int p) { return vec + (h * 2 + p) * vstride; };
+  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  auto XG = [&](int h, int p) { return xg + ((size_t)h * 2 + p) * m * rg; };
+
+  auto block_of = [&](int h, int st, int &kind) -> int {
+    kind = st < F ? 0 : (st == F ? 1 : 2);
+    if (h == 0) {
+      if (st < F) return st >= F - nt ? st - (F - nt) : -1;
+      if (st == F) return tw;
+      int j = st - F - 1;
+      return j < nt ? tw - 1 - j : -1;
+    }
+    if (st < F) return st >= F - nbt ? nb - 1 - (st - (F - nbt)) : -1;
+    if (st == F) return -1;
+    int j = st - F - 1;
+    return j < nbt ? tw + 1 + j : -1;
+  };
+  auto fseq = [&](int h, int st) {
+    if (h == 0) return st - (F - nt);
+    return st < F ? st - (F - nbt) : st - (F - nbt) - 1;
+  };
+  // halves delivering input vectors to stage st (one m x rg vector each)
+  auto deliveries = [&](int st) {
+    if (st < 0 || st >= S) return 0;
+    int kind, n = 0;
+    if (block_of(0, st, kind) >= 0) ++n;
+    if (block_of(1, st, kind) >= 0 && st != F + 1) ++n;
+    if (st == F && nbt > 0) ++n;
+    return n;
+  };
+  const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
+  const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
+  const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
+  auto load_tile = [&](int h, int st) {  // thread 0
+    int kind, k = block_of(h, st, kind);
+    if (k < 0) return;
+    int q = fseq(h, st), slot = q % FAC_STAGES;
+    uint64_t *bar = &fbar[h * FAC_STAGES + slot];
+    mbar_expect_tx(bar, fac_bytes);
+    if (fac_bytes)
+      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+  };
+  auto push = [&](int h, int p) {  // thread 0, after the fence + barrier
+    if (push_bytes)
+      bulk_g2s_multicast(VEC(h, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[p], mask);
+  };
+
+  if (t == 0) {
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();
+  if (t == 0) {
+    mbar_expect_tx(&vbar[0], deliveries(0) * vec_bytes);
+    if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
+    for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
+      load_tile(0, st);
+      load_tile(1, st);
+    }
+  }
+  // prologue: b_0 (top, stage F-nt) and b_{n_b-1} (bottom, stage F-nbt)
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && nbt == 0) break;
+    const int st0 = h == 0 ? F - nt : F - nbt;
+    const int k0 = h == 0 ? 0 : nb - 1;
+    for (int e = t; e < nr * rg; e += SOLVE_THREADS) {
+      int row = e / rg, c = e % rg;
+      XG(h, st0 & 1)[(r0 + row) * rg + c] = V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + c];
+    }
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+  if (t == 0) {
+    push(0, (F - nt) & 1);
+    if (nbt > 0) push(1, (F - nbt) & 1);
+  }
+
+  // per half: 2x2 (row, rhs) micro-tiles, K split over 128 / ntile slices
+  const int TR = (nr + 1) / 2, TC = (rg + 1) / 2;
+  const int ntile = TR * TC;
+  int nslice = ntile > 0 ? 128 / ntile : 1;
+  nslice = max(1, min(8, nslice));
+  const int ks = (m + nslice - 1) / nslice;
+  const int nout = nr * rg;  // outputs per half (<= 2 * 128)
+  int vph[2] = {0, 0};
+
+  for (int s = 0; s < S; ++s) {
+    const int p = s & 1;
+    if (t == 0 && s + FAC_STAGES - 1 < S) {
+      load_tile(0, s + FAC_STAGES - 1);
+      load_tile(1, s + FAC_STAGES - 1);
+    }
+    int kind, k = block_of(hh, s, kind);
+    const bool act = k >= 0;
+    // epilogue operands (independent of the chain), up to 2 outputs / thread
+    cplx aux[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int o = tl + u * 128;
+        if (o >= nout) break;
+        const int orow = o / rg, oc = o % rg;
+        const size_t col = chunk0 + oc;
+        if (kind == 0) {
+          const int kn = hh == 0 ? k + 1 : k - 1;
+          if (hh == 0 || kn > tw) aux[u] = V.rhs[((size_t)kn * m + r0 + orow) * ldx + col];
+        } else if (kind == 2) {
+          aux[u] = __ldcg(V.x + ((size_t)k * m + r0 + orow) * ldx + col);
+        }
+      }
+    }
+    mbar_wait(&vbar[p], vph[p] & 1);
+    if (act) {
+      const int q = fseq(hh, s);
+      mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+      const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
+      // input vector: own half; bottom at F+1 reads x_t (top buffer);
+      // the middle block adds the bottom chain's part
+      const cplx *X = VEC((hh == 1 && s == F + 1) ? 0 : hh, p);
+      const cplx *X2 = (kind == 1 && nbt > 0) ? VEC(1, p) : nullptr;
+      const int tile = ntile ? tl % ntile : 0, sl = ntile ? tl / ntile : nslice;
+      if (sl < nslice && tile < ntile) {
+        const int tr = tile / TC, tc = tile % TC;
+        const int row = 2 * tr, c = 2 * tc;
+        const int j0 = sl * ks, j1 = min(m, j0 + ks);
+        cplx a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
+        const cplx *ar0 = A + (size_t)row * m;
+        const cplx *ar1 = ar0 + m;
+        if (X2) {
+          for (int j = j0; j < j1; ++j) {
+            cplx x0 = cadd(X[j * rg + c], X2[j * rg + c]);
+            cplx x1 = cadd(X[j * rg + c + 1], X2[j * rg + c + 1]);
+            cplx f0 = ar0[j], f1 = ar1[j];
+            cfma(a00, f0, x0); cfma(a01, f0, x1); cfma(a10, f1, x0); cfma(a11, f1, x1);
+          }
+        } else {
+#pragma unroll 4
+          for (int j = j0; j < j1; ++j) {
+            cplx x0 = X[j * rg + c], x1 = X[j * rg + c + 1];
+            cplx f0 = ar0[j], f1 = ar1[j];
+            cfma(a00, f0, x0); cfma(a01, f0, x1); cfma(a10, f1, x0); cfma(a11, f1, x1);
+          }
+        }
+        cplx *rp = red + ((size_t)hh * 8 + sl) * rstride;
+        rp[row * rg + c] = a00;
+        if (c + 1 < rg) rp[row * rg + c + 1] = a01;
+        if (row + 1 < nr) {
+          rp[(row + 1) * rg + c] = a10;
+          if (c + 1 < rg) rp[(row + 1) * rg + c + 1] = a11;
+        }
+      }
+    }
+    __syncthreads();
+    if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
+    vph[p]++;
+    // epilogue: next-stage rows to the exchange scratch, outputs kept
+    const bool last = s + 1 >= S;
+    cplx outv[2];
+    size_t offs[2] = {0, 0};
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int o = tl + u * 128;
+        if (o >= nout) break;
+        const int orow = o / rg, oc = o % rg;
+        cplx acc = red[((size_t)hh * 8) * rstride + o];
+        for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[((size_t)hh * 8 + q2) * rstride + o]);
+        offs[u] = ((size_t)k * m + r0 + orow) * ldx + chunk0 + oc;
+        cplx out, nxt;
+        if (kind == 0) {
+          out = acc;
+          nxt = hh == 0 ? csub(aux[u], cmul(f.lcoef[k + 1], acc)) : csub(aux[u], cmul(f.ucoef[k - 1], acc));
+        } else if (kind == 1) {
+          out = acc;
+          nxt = acc;
+        } else {
+          out = csub(aux[u], cmul(hh == 0 ? f.ucoef[k] : f.lcoef[k], acc));
+          nxt = out;
+        }
+        outv[u] = out;
+        if (!last) XG(hh, p ^ 1)[(r0 + orow) * rg + oc] = nxt;
+      }
+    }
+    fence_proxy_async_global();  // (v5)
+    __syncthreads();
+    if (t == 0 && !last) {
+      // exactly the deliveries counted for stage s+1 (see deliveries())
+      int kd;
+      if (block_of(0, s, kd) >= 0 && block_of(0, s + 1, kd) >= 0) push(0, p ^ 1);
+      if (block_of(1, s, kd) >= 0 && (block_of(1, s + 1, kd) >= 0 || s + 1 == F)) push(1, p ^ 1);
+    }
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int o = tl + u * 128;
+        if (o >= nout) break;
+        V.x[offs[u]] = outv[u];
+      }
+    }
+  }
+  cluster.sync();
+}
+
 static int solve_rows_max(int max_m, int C) {
   int r = (max_m + C - 1) / C;
   return r + (r & 1);  // even: 2-row micro-tiles may read one padding row
@@ -485,9 +731,47 @@ static int pick_cfg(int max_m, int nrhs, SolveCfg *out) {
   return 0;
 }
 
+static size_t solve5_smem(int m, int rc, int C) {
+  size_t rows_max = solve_rows_max(m, C);
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_max * m + 2) + 16 * rows_max * rc;
+  return 256 + elems * sizeof(cplx);
+}
+
+static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
+  const int C = 16;
+  int rc = std::min(nrhs, 16);
+  while (rc > 1 && (solve5_smem(max_m, rc, C) > 232448 || solve_rows_max(max_m, C) * rc > 256))
+    rc = (rc + 1) / 2;
+  size_t smem = solve5_smem(max_m, rc, C);
+  if (smem > 232448) return ds_fail(DS_ECONFIG, "block solve v5: slab too large");
+  cudaFuncSetAttribute(k_block_solve5, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  DS_CUDA(cudaFuncSetAttribute(k_block_solve5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
+  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve5, (const SolveVisit *)visits_dev, nrhs, rc,
+                             solve_rows_max(max_m, C)));
+  ctx->launches++;
+  return DS_OK;
+}
+
 int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs,
                           int max_m) {
   if (nvisit < 1) return DS_OK;
+  {
+    const char *v = getenv("DS_K3");
+    if (!(v && std::string(v) == "v3")) return launch_v5(ctx, visits_dev, nvisit, nrhs, max_m);
+  }
   SolveCfg sc;
   if (!pick_cfg(max_m, nrhs, &sc))
     return ds_fail(DS_ECONFIG, "block solve: no feasible cluster configuration");
