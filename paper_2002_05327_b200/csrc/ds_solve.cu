@@ -18,9 +18,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "ds_common.cuh"
 
@@ -108,6 +110,17 @@ __device__ long long g_solve_trace[2][1024][6];
     g_solve_trace[rank][s][(i) == 0 ? 0 : (h == 0 ? (i) : ((i) == 1 ? 4 : 5))] = clock64();
 #else
 #define TRACE(i)
+#endif
+
+#ifdef DS_SOLVE_TRACE5
+// v5 phase trace: thread 0 of cluster rank 0 of the first (visit, chunk) of
+// every launch appends [stage][phase] clock64 stamps (tools/trace_solve5.py)
+__device__ long long g_tr5[64][160][8];
+__device__ int g_tr5_n;
+#define TRACE5(i)                                        \
+  if (tr5 >= 0 && t == 0 && s < 160) g_tr5[tr5][s][(i)] = clock64();
+#else
+#define TRACE5(i)
 #endif
 
 // multicast TMA: global -> the same shared offset of every CTA in `mask`,
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     const int p = s & 1;
     { const int h = 0; (void)h; TRACE(0); }
     // refill the factor rings FAC_STAGES-1 stages ahead (slot freed at s-1)
-    if (t == 0 && s + FAC_STAGES - 1 < S) {
+    if (t < 32 && s + FAC_STAGES - 1 < S) {
       load_tile(0, s + FAC_STAGES - 1);
       load_tile(1, s + FAC_STAGES - 1);
     }
@@ -411,8 +424,72 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 // the bottom block, one mbarrier per stage parity collects both halves'
 // rows (expected bytes = halves delivering to that stage), and both halves'
 // rows are multicast back-to-back.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// factor-tile row pitch: lda % 8 == 4 puts consecutive rows in opposite
+// halves of the 128-byte bank window, so the 8-row DMMA A fragments (and the
+// 2-row DFMA micro-tiles) load without bank conflicts for any m
+__host__ __device__ __forceinline__ int solve_lda(int m) { return m + (12 - m % 8) % 8; }
+
+// One warp's share of y = A x for an (8*MT)-row, (8*NT)-RHS tile over
+// k-steps [kb, ke) of 4 columns: complex product as four real m8n8k4 DMMAs
+// (re*re - im*im, re*im + im*re).  Fragments of step kq+1 are loaded into
+// registers before the DMMAs of step kq issue, hiding shared-memory latency.
+// X2 (the middle block's second input) is added while loading.
+template <int MT, int NT, bool HX2>
+__device__ __forceinline__ void mma_product(const cplx *__restrict__ A, int lda,
+                                            const cplx *__restrict__ X, const cplx *__restrict__ X2,
+                                            int rg, int m, int kb, int ke, int g, int tg,
+                                            double (&cr)[2][2][2], double (&ci)[2][2][2]) {
+  if (kb >= ke) return;
+  cplx a[MT], b[NT], an[MT], bn[NT];
+  auto load = [&](int kq, cplx(&aa)[MT], cplx(&bb)[NT]) {
+    const int kk = kq * 4 + tg;
+    const bool kin = kk < m;
+    const int kc = kin ? kk : 0;  // clamped address, value zeroed below
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      cplx v = X[kc * rg + nt * 8 + g];
+      if (HX2) v = cadd(v, X2[kc * rg + nt * 8 + g]);
+      bb[nt] = kin ? v : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      cplx v = A[(mt * 8 + g) * lda + kc];
+      aa[mt] = kin ? v : make_double2(0.0, 0.0);
+    }
+  };
+  load(kb, a, b);
+  for (int kq = kb; kq < ke; ++kq) {
+    if (kq + 1 < ke) load(kq + 1, an, bn);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(cr[mt][nt], a[mt].x, b[nt].x);
+        dmma(ci[mt][nt], a[mt].x, b[nt].y);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(cr[mt][nt], -a[mt].y, b[nt].y);
+        dmma(ci[mt][nt], a[mt].y, b[nt].x);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
+  }
+}
+
+template <bool MMA>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)
-    k_block_solve5(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+    k_block_solve5(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max, int nsl_max,
+                   int lda_pad) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
@@ -441,8 +518,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   cplx *vec = (cplx *)(smem_raw + 256);   // [2 halves][2 parity][vstride]
   const int vstride = m * rc + 2;
   cplx *fac = vec + 4 * vstride;          // [2 halves][FAC_STAGES][fstride]
-  const int fstride = rows_max * m + 2;
-  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][8 slices][rows_max*rc]
+  const int lda = lda_pad ? solve_lda(m) : m;
+  const int fstride = ((rows_max + 7) & ~7) * lda + 2;
+  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][nsl_max slices][rows_max*rc]
   const int rstride = rows_max * rc;
   auto VEC = [&](int h, int p) { return vec + (h * 2 + p) * vstride; };
   cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
@@ -477,20 +555,38 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
   const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
   const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
-  auto load_tile = [&](int h, int st) {  // thread 0
+  auto load_tile = [&](int h, int st) {  // warp 0: one bulk copy per row
     int kind, k = block_of(h, st, kind);
     if (k < 0) return;
     int q = fseq(h, st), slot = q % FAC_STAGES;
     uint64_t *bar = &fbar[h * FAC_STAGES + slot];
-    mbar_expect_tx(bar, fac_bytes);
-    if (fac_bytes)
-      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+    if (lda == m) {  // rows already conflict-free: one copy of the slice
+      if (t == 0) {
+        mbar_expect_tx(bar, fac_bytes);
+        if (fac_bytes)
+          bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m,
+                   fac_bytes, bar);
+      }
+      return;
+    }
+    if (t == 0) mbar_expect_tx(bar, fac_bytes);
+    __syncwarp();
+    for (int r = t; r < nr; r += 32)
+      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride + r * lda,
+               f.sinv + ((size_t)k * m + r0 + r) * m, (uint32_t)(m * sizeof(cplx)), bar);
   };
   auto push = [&](int h, int p) {  // thread 0, after the fence + barrier
     if (push_bytes)
       bulk_g2s_multicast(VEC(h, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[p], mask);
   };
 
+#ifdef DS_SOLVE_TRACE5
+  int tr5 = -1;
+  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    tr5 = atomicAdd(&g_tr5_n, 1);
+    if (tr5 >= 64) tr5 = -1;
+  }
+#endif
   if (t == 0) {
     mbar_init(&vbar[0], 1);
     mbar_init(&vbar[1], 1);
@@ -501,6 +597,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   if (t == 0) {
     mbar_expect_tx(&vbar[0], deliveries(0) * vec_bytes);
     if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
+  }
+  if (t < 32) {
     for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
       load_tile(0, st);
       load_tile(1, st);
@@ -527,14 +625,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const int TR = (nr + 1) / 2, TC = (rg + 1) / 2;
   const int ntile = TR * TC;
   int nslice = ntile > 0 ? 128 / ntile : 1;
-  nslice = max(1, min(8, nslice));
+  nslice = MMA ? 4 : max(1, min(nsl_max, nslice));
   const int ks = (m + nslice - 1) / nslice;
   const int nout = nr * rg;  // outputs per half (<= 2 * 128)
-  int vph[2] = {0, 0};
+  uint32_t vph = 0;  // bit p: phase of vbar[p] (a register, not a local array)
 
   for (int s = 0; s < S; ++s) {
     const int p = s & 1;
-    if (t == 0 && s + FAC_STAGES - 1 < S) {
+    TRACE5(0);
+    if (t < 32 && s + FAC_STAGES - 1 < S) {
       load_tile(0, s + FAC_STAGES - 1);
       load_tile(1, s + FAC_STAGES - 1);
     }
@@ -542,7 +641,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     const bool act = k >= 0;
     // epilogue operands (independent of the chain), up to 2 outputs / thread
     cplx aux[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    cplx coef = make_double2(0.0, 0.0);  // chain coefficient, off the critical path
     if (act) {
+      if (kind == 0) coef = hh == 0 ? f.lcoef[k + 1] : f.ucoef[k - 1];
+      else if (kind == 2) coef = hh == 0 ? f.ucoef[k] : f.lcoef[k];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int o = tl + u * 128;
@@ -557,23 +659,69 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         }
       }
     }
-    mbar_wait(&vbar[p], vph[p] & 1);
+#ifndef K3_NO_WAIT
+    mbar_wait(&vbar[p], (vph >> p) & 1);
+#endif
+    TRACE5(1);
     if (act) {
       const int q = fseq(hh, s);
       mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+      TRACE5(2);
       const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
       // input vector: own half; bottom at F+1 reads x_t (top buffer);
       // the middle block adds the bottom chain's part
       const cplx *X = VEC((hh == 1 && s == F + 1) ? 0 : hh, p);
       const cplx *X2 = (kind == 1 && nbt > 0) ? VEC(1, p) : nullptr;
+      if constexpr (MMA) {
+        // FP64 tensor cores: per warp all (8-row, 8-RHS) tiles of this
+        // half over a quarter of K; complex product as 4 real m8n8k4 DMMAs
+        const int warp = tl >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+        const int nk = (m + 3) >> 2, kb = (warp * nk) >> 2, ke = ((warp + 1) * nk) >> 2;
+        const int MT = (nr + 7) >> 3, NT = (rg + 7) >> 3;
+        double cr[2][2][2] = {}, ci[2][2][2] = {};
+#ifdef K3_NO_COMPUTE
+        if (false)
+#endif
+        {
+          const int sel = (MT > 1 ? 4 : 0) + (NT > 1 ? 2 : 0) + (X2 ? 1 : 0);
+#define K3_PRODUCT(mt_, nt_, x2_) \
+  mma_product<mt_, nt_, x2_>(A, lda, X, X2, rg, m, kb, ke, g, tg, cr, ci)
+          switch (sel) {
+            case 0: K3_PRODUCT(1, 1, false); break;
+            case 1: K3_PRODUCT(1, 1, true); break;
+            case 2: K3_PRODUCT(1, 2, false); break;
+            case 3: K3_PRODUCT(1, 2, true); break;
+            case 4: K3_PRODUCT(2, 1, false); break;
+            case 5: K3_PRODUCT(2, 1, true); break;
+            case 6: K3_PRODUCT(2, 2, false); break;
+            default: K3_PRODUCT(2, 2, true); break;
+          }
+#undef K3_PRODUCT
+        }
+        cplx *rp = red + ((size_t)hh * nsl_max + warp) * rstride;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = mt * 8 + g, col = nt * 8 + 2 * tg + e;
+              if (mt < MT && nt < NT && row < nr && col < rg)
+                rp[row * rg + col] = make_double2(cr[mt][nt][e], ci[mt][nt][e]);
+            }
+      } else {
       const int tile = ntile ? tl % ntile : 0, sl = ntile ? tl / ntile : nslice;
       if (sl < nslice && tile < ntile) {
         const int tr = tile / TC, tc = tile % TC;
         const int row = 2 * tr, c = 2 * tc;
         const int j0 = sl * ks, j1 = min(m, j0 + ks);
         cplx a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
-        const cplx *ar0 = A + (size_t)row * m;
-        const cplx *ar1 = ar0 + m;
+        const cplx *ar0 = A + (size_t)row * lda;
+        const cplx *ar1 = ar0 + lda;
+#ifdef K3_NO_COMPUTE
+        if (true) {
+        } else
+#endif
         if (X2) {
           for (int j = j0; j < j1; ++j) {
             cplx x0 = cadd(X[j * rg + c], X2[j * rg + c]);
@@ -589,7 +737,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
             cfma(a00, f0, x0); cfma(a01, f0, x1); cfma(a10, f1, x0); cfma(a11, f1, x1);
           }
         }
-        cplx *rp = red + ((size_t)hh * 8 + sl) * rstride;
+        cplx *rp = red + ((size_t)hh * nsl_max + sl) * rstride;
         rp[row * rg + c] = a00;
         if (c + 1 < rg) rp[row * rg + c + 1] = a01;
         if (row + 1 < nr) {
@@ -597,10 +745,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
           if (c + 1 < rg) rp[(row + 1) * rg + c + 1] = a11;
         }
       }
+      }
     }
+    TRACE5(3);
     __syncthreads();
+    TRACE5(4);
     if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
-    vph[p]++;
+    vph ^= 1u << p;
     // epilogue: next-stage rows to the exchange scratch, outputs kept
     const bool last = s + 1 >= S;
     cplx outv[2];
@@ -611,26 +762,30 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         const int o = tl + u * 128;
         if (o >= nout) break;
         const int orow = o / rg, oc = o % rg;
-        cplx acc = red[((size_t)hh * 8) * rstride + o];
-        for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[((size_t)hh * 8 + q2) * rstride + o]);
+        cplx acc = red[((size_t)hh * nsl_max) * rstride + o];
+        for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[((size_t)hh * nsl_max + q2) * rstride + o]);
         offs[u] = ((size_t)k * m + r0 + orow) * ldx + chunk0 + oc;
         cplx out, nxt;
         if (kind == 0) {
           out = acc;
-          nxt = hh == 0 ? csub(aux[u], cmul(f.lcoef[k + 1], acc)) : csub(aux[u], cmul(f.ucoef[k - 1], acc));
+          nxt = csub(aux[u], cmul(coef, acc));
         } else if (kind == 1) {
           out = acc;
           nxt = acc;
         } else {
-          out = csub(aux[u], cmul(hh == 0 ? f.ucoef[k] : f.lcoef[k], acc));
+          out = csub(aux[u], cmul(coef, acc));
           nxt = out;
         }
         outv[u] = out;
         if (!last) XG(hh, p ^ 1)[(r0 + orow) * rg + oc] = nxt;
       }
     }
+    TRACE5(5);
+#ifndef K3_NO_FENCE
     fence_proxy_async_global();  // (v5)
+#endif
     __syncthreads();
+    TRACE5(6);
     if (t == 0 && !last) {
       // exactly the deliveries counted for stage s+1 (see deliveries())
       int kd;
@@ -645,6 +800,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         V.x[offs[u]] = outv[u];
       }
     }
+    TRACE5(7);
   }
   cluster.sync();
 }
@@ -731,21 +887,97 @@ static int pick_cfg(int max_m, int nrhs, SolveCfg *out) {
   return 0;
 }
 
+// split-K slices per half: 8 for full chunks, up to 16 when the chunk is
+// narrow (fewer outputs per half leave more threads for the K split)
+static int solve5_nsl(int m, int rc, int C) {
+  int rstride = solve_rows_max(m, C) * rc;
+  return std::max(8, std::min(16, 1024 / std::max(1, rstride)));
+}
+
+// Dynamic shared memory of one CTA.  At least 118 KB, so a CTA always owns
+// its SM: the chain is latency bound, and two CTAs sharing an SM would
+// serialise their stages (the wave count below assumes one CTA per SM).
 static size_t solve5_smem(int m, int rc, int C) {
   size_t rows_max = solve_rows_max(m, C);
-  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_max * m + 2) + 16 * rows_max * rc;
-  return 256 + elems * sizeof(cplx);
+  size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * solve_lda(m) + 2) +
+                 2 * (size_t)solve5_nsl(m, rc, C) * rows_max * rc;
+  return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
+}
+
+typedef void (*Solve5Fn)(const SolveVisit *, int, int, int, int, int);
+
+// Co-resident clusters of C CTAs for this footprint (7 x 16 on a 148-SM B200).
+static int solve5_max_clusters(Solve5Fn fn, int C, size_t smem) {
+  static std::vector<std::pair<std::pair<int, size_t>, int>> memo;
+  for (auto &e : memo)
+    if (e.first.first == C && e.first.second == smem) return e.second;
+  cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (const void *)fn, &cfg) != cudaSuccess || n < 0) {
+    cudaGetLastError();
+    n = 0;
+  }
+  memo.push_back({{C, smem}, n});
+  return n;
 }
 
 static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
-  const int C = 16;
-  int rc = std::min(nrhs, 16);
-  while (rc > 1 && (solve5_smem(max_m, rc, C) > 232448 || solve_rows_max(max_m, C) * rc > 256))
-    rc = (rc + 1) / 2;
-  size_t smem = solve5_smem(max_m, rc, C);
-  if (smem > 232448) return ds_fail(DS_ECONFIG, "block solve v5: slab too large");
-  cudaFuncSetAttribute(k_block_solve5, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  DS_CUDA(cudaFuncSetAttribute(k_block_solve5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static const bool mma = env_int("DS_K3_MMA", 1) != 0;
+  static const int rc_min = std::max(1, env_int("DS_K3_RCMIN", 4));
+  static const int rc_max = std::max(1, env_int("DS_K3_RCMAX", 16));
+  static const int c_only = env_int("DS_K3_CLUSTER", 0);
+  static const int lda_pad = env_int("DS_K3_LDA_PAD", 0);
+  Solve5Fn fn = mma ? k_block_solve5<true> : k_block_solve5<false>;
+  // The step is latency bound (one cluster per (visit, RHS chunk), ~n_b
+  // dependent stages each).  Choose the (cluster size, chunk) that runs the
+  // step in the fewest waves of co-resident clusters, then with the least
+  // arithmetic per CTA and stage (rows per CTA x chunk width).
+  int bestC = 0, bestRc = 0;
+  long best_waves = 0, best_work = 0;
+  for (int C : {16, 8}) {
+    if (c_only && C != c_only) continue;
+    const int rows = solve_rows_max(max_m, C);
+    for (int rc = std::min(nrhs, rc_max); rc >= 1; rc = rc > 1 ? (rc + 1) / 2 : 0) {
+      if (rc < std::min(rc_min, nrhs) && bestC) break;
+      if (rows * rc > 256 || (mma && rows > 16)) continue;
+      size_t smem = solve5_smem(max_m, rc, C);
+      if (smem > 232448) continue;
+      int maxcl = solve5_max_clusters(fn, C, smem);
+      if (maxcl < 1) continue;
+      long ncl = (long)nvisit * ((nrhs + rc - 1) / rc);
+      long waves = (ncl + maxcl - 1) / maxcl;
+      long work = waves * (long)rows * rc;
+      if (!bestC || waves < best_waves || (waves == best_waves && work < best_work) ||
+          (waves == best_waves && work == best_work && C > bestC)) {
+        bestC = C;
+        bestRc = rc;
+        best_waves = waves;
+        best_work = work;
+      }
+      if (rc == 1) break;
+    }
+  }
+  if (!bestC) return ds_fail(DS_ECONFIG, "block solve v5: no feasible cluster configuration");
+  const int C = bestC, rc = bestRc;
+  const size_t smem = solve5_smem(max_m, rc, C);
+  if (env_int("DS_K3_DEBUG", 0))
+    fprintf(stderr, "K3 v5: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld maxcl %d smem %zu\n", nvisit,
+            nrhs, max_m, C, rc, best_waves, solve5_max_clusters(fn, C, smem), smem);
+  DS_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
@@ -759,8 +991,8 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve5, (const SolveVisit *)visits_dev, nrhs, rc,
-                             solve_rows_max(max_m, C)));
+  DS_CUDA(cudaLaunchKernelEx(&cfg, fn, (const SolveVisit *)visits_dev, nrhs, rc,
+                             solve_rows_max(max_m, C), solve5_nsl(max_m, rc, C), lda_pad));
   ctx->launches++;
   return DS_OK;
 }
@@ -800,6 +1032,20 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
 #ifdef DS_SOLVE_TRACE
 extern "C" DS_API int ds_debug_solve_trace(long long *out) {
   DS_CUDA(cudaMemcpyFromSymbol(out, g_solve_trace, sizeof(long long) * 2 * 1024 * 6));
+  return DS_OK;
+}
+#endif
+
+#ifdef DS_SOLVE_TRACE5
+extern "C" DS_API int ds_debug_solve_trace5(long long *out, int *count) {
+  DS_CUDA(cudaDeviceSynchronize());
+  DS_CUDA(cudaMemcpyFromSymbol(out, g_tr5, sizeof(long long) * 64 * 160 * 8));
+  DS_CUDA(cudaMemcpyFromSymbol(count, g_tr5_n, sizeof(int)));
+  return DS_OK;
+}
+extern "C" DS_API int ds_debug_solve_trace5_reset() {
+  int z = 0;
+  DS_CUDA(cudaMemcpyToSymbol(g_tr5_n, &z, sizeof(int)));
   return DS_OK;
 }
 #endif
