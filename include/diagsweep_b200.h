@@ -71,6 +71,9 @@ DS_API int ds_ctx_create(int device, void *stream, ds_ctx **out);
 DS_API int ds_ctx_set_stream(ds_ctx *ctx, void *stream);
 DS_API int ds_ctx_synchronize(ds_ctx *ctx);
 DS_API int ds_ctx_destroy(ds_ctx *ctx);
+/* Kernels this library has launched on `ctx` so far (graph replays count
+ * their captured launches).  Diagnostic: bench.py's `gpu_launches`. */
+DS_API int64_t ds_ctx_launches(const ds_ctx *ctx);
 
 /* --------------------------------------------------------------- operator
  * One assembled PML Helmholtz operator on a window (pml.py:75-188).

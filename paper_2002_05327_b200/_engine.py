@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import itertools
 import math
+import os
 import weakref
 
 import numpy as np
@@ -35,6 +36,12 @@ def _require_cuda():
         raise SolverError(
             "no CUDA device: the diagsweep_b200 hot path runs only on the GPU "
             "(there is no CPU fallback)")
+
+
+def launch_count() -> int:
+    """Kernels the native library has launched on this device's context."""
+    lib, ctx = context()
+    return int(lib.ds_ctx_launches(ctx))
 
 
 def context():
@@ -325,6 +332,10 @@ class DevicePlan:
         N.check(lib.ds_plan_create(ctx, C.byref(desc), C.byref(out)), "ds_plan_create")
         self.handle = out
         self._finalizer = weakref.finalize(self, lib.ds_plan_destroy, out)
+        # replay one captured CUDA graph per (buffers, nrhs): ~4 sweeps x
+        # n_steps x 4 launches per application (DS_GRAPH=0 disables)
+        if os.environ.get("DS_GRAPH", "1") != "0":
+            self.enable_graph(True)
 
     @property
     def workspace_bytes(self) -> int:

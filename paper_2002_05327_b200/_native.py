@@ -70,6 +70,7 @@ _SIGNATURES = [
     ("ds_ctx_create", C.c_int, [C.c_int, vp, C.POINTER(vp)]),
     ("ds_ctx_set_stream", C.c_int, [vp, vp]),
     ("ds_ctx_synchronize", C.c_int, [vp]),
+    ("ds_ctx_launches", i64, [vp]),
     ("ds_ctx_destroy", C.c_int, [vp]),
     ("ds_op_create", C.c_int, [vp, C.POINTER(OpDesc), C.POINTER(vp)]),
     ("ds_op_destroy", C.c_int, [vp]),

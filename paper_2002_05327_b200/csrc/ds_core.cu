@@ -65,6 +65,8 @@ extern "C" int ds_ctx_synchronize(ds_ctx *ctx) {
   return DS_OK;
 }
 
+extern "C" int64_t ds_ctx_launches(const ds_ctx *ctx) { return ctx ? ctx->launches : -1; }
+
 extern "C" int ds_ctx_destroy(ds_ctx *ctx) {
   if (!ctx) return DS_OK;
   cudaFree(ctx->scratch);

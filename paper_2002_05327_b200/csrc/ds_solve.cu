@@ -633,10 +633,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   for (int s = 0; s < S; ++s) {
     const int p = s & 1;
     TRACE5(0);
+#ifndef K3_NO_FACSTREAM
     if (t < 32 && s + FAC_STAGES - 1 < S) {
       load_tile(0, s + FAC_STAGES - 1);
       load_tile(1, s + FAC_STAGES - 1);
     }
+#endif
     int kind, k = block_of(hh, s, kind);
     const bool act = k >= 0;
     // epilogue operands (independent of the chain), up to 2 outputs / thread
@@ -665,7 +667,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     TRACE5(1);
     if (act) {
       const int q = fseq(hh, s);
+#ifndef K3_NO_FACSTREAM
       mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+#endif
       TRACE5(2);
       const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
       // input vector: own half; bottom at F+1 reads x_t (top buffer);

@@ -797,7 +797,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
     P->slots_dirty = false;
   }
-  if (P->use_graph && !P->profiling) {
+  if (P->use_graph && !P->profiling && !partials) {  // per-sweep partials: fresh buffers, eager
     // capture / replay on a private stream (the caller's stream may be the
     // legacy default stream, which cannot be captured), ordered by events
     if (!P->gstream) {
