@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "ds_common.cuh"
@@ -115,10 +116,10 @@ __device__ long long g_solve_trace[2][1024][6];
 #ifdef DS_SOLVE_TRACE5
 // v5 phase trace: thread 0 of cluster rank 0 of the first (visit, chunk) of
 // every launch appends [stage][phase] clock64 stamps (tools/trace_solve5.py)
-__device__ long long g_tr5[64][160][8];
+__device__ long long g_tr5[64][16][160][12];
 __device__ int g_tr5_n;
 #define TRACE5(i)                                        \
-  if (tr5 >= 0 && t == 0 && s < 160) g_tr5[tr5][s][(i)] = clock64();
+  if (tr5 >= 0 && t == 0 && s < 160) g_tr5[tr5][rank & 15][s][(i)] = clock64();
 #else
 #define TRACE5(i)
 #endif
@@ -464,6 +465,41 @@ __device__ __forceinline__ void mma_product(const cplx *__restrict__ A, int lda,
     }
   };
   load(kb, a, b);
+#ifndef K3_4M
+  // 3M complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
+  // Re = P1 - P2, Im = P3 - P1 - P2 (3 DMMAs per tile and k-step instead
+  // of 4; normwise error of the same order)
+  double p1[MT][NT][2] = {}, p2[MT][NT][2] = {}, p3[MT][NT][2] = {};
+  for (int kq = kb; kq < ke; ++kq) {
+    if (kq + 1 < ke) load(kq + 1, an, bn);
+    double bs[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) bs[nt] = b[nt].x + b[nt].y;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const double as = a[mt].x + a[mt].y;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        dmma(p1[mt][nt], a[mt].x, b[nt].x);
+        dmma(p2[mt][nt], a[mt].y, b[nt].y);
+        dmma(p3[mt][nt], as, bs[nt]);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
+  }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        cr[mt][nt][e] = p1[mt][nt][e] - p2[mt][nt][e];
+        ci[mt][nt][e] = p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e];
+      }
+#else
   for (int kq = kb; kq < ke; ++kq) {
     if (kq + 1 < ke) load(kq + 1, an, bn);
 #pragma unroll
@@ -484,6 +520,7 @@ __device__ __forceinline__ void mma_product(const cplx *__restrict__ A, int lda,
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
   }
+#endif
 }
 
 template <bool MMA>
@@ -555,13 +592,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
   const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
   const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
-  auto load_tile = [&](int h, int st) {  // warp 0: one bulk copy per row
+  // TMA issue blocks the issuing thread for ~150-400 cycles
+  // (tools/issue_latency_micro.cu), so the per-stage copies are issued by
+  // different warps: top/bottom multicast by warps 0/4, top/bottom factor
+  // tiles by warps 2/6 -- each fits in its warp's slack before the exchange
+  const int tile_thread[2] = {64, 192};
+  auto load_tile = [&](int h, int st) {  // thread tile_thread[h] (or warp 0 for per-row copies)
     int kind, k = block_of(h, st, kind);
     if (k < 0) return;
     int q = fseq(h, st), slot = q % FAC_STAGES;
     uint64_t *bar = &fbar[h * FAC_STAGES + slot];
     if (lda == m) {  // rows already conflict-free: one copy of the slice
-      if (t == 0) {
+      if (t == tile_thread[h]) {
         mbar_expect_tx(bar, fac_bytes);
         if (fac_bytes)
           bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m,
@@ -581,9 +623,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   };
 
 #ifdef DS_SOLVE_TRACE5
+  // every rank of cluster (0,0) traces; the launch index is the count of
+  // rank-0 CTAs seen before (rank 0 bumps it after the kernel's first sync)
   int tr5 = -1;
-  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
-    tr5 = atomicAdd(&g_tr5_n, 1);
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    tr5 = *(volatile int *)&g_tr5_n;
     if (tr5 >= 64) tr5 = -1;
   }
 #endif
@@ -594,12 +638,15 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     fence_mbar_init();
   }
   cluster.sync();
+#ifdef DS_SOLVE_TRACE5
+  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) atomicAdd(&g_tr5_n, 1);
+#endif
   if (t == 0) {
     mbar_expect_tx(&vbar[0], deliveries(0) * vec_bytes);
     if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
   }
-  if (t < 32) {
-    for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
+  for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
+    if (lda == m || t < 32) {
       load_tile(0, st);
       load_tile(1, st);
     }
@@ -634,11 +681,17 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     const int p = s & 1;
     TRACE5(0);
 #ifndef K3_NO_FACSTREAM
-    if (t < 32 && s + FAC_STAGES - 1 < S) {
-      load_tile(0, s + FAC_STAGES - 1);
-      load_tile(1, s + FAC_STAGES - 1);
+    if (s + FAC_STAGES - 1 < S) {
+      if (lda == m) {
+        if (t == tile_thread[0]) load_tile(0, s + FAC_STAGES - 1);
+        if (t == tile_thread[1]) load_tile(1, s + FAC_STAGES - 1);
+      } else if (t < 32) {
+        load_tile(0, s + FAC_STAGES - 1);
+        load_tile(1, s + FAC_STAGES - 1);
+      }
     }
 #endif
+    TRACE5(8);
     int kind, k = block_of(hh, s, kind);
     const bool act = k >= 0;
     // epilogue operands (independent of the chain), up to 2 outputs / thread
@@ -661,16 +714,23 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         }
       }
     }
+    TRACE5(9);
+    // factor tile first (streamed a stage ahead, normally complete), then
+    // the exchanged vectors; the exchange barrier is re-armed for stage s+2
+    // at once (its next phase needs this CTA's push of stage s+1, which
+    // follows every thread's pass through this wait)
+    const int q = act ? fseq(hh, s) : 0;
+#ifndef K3_NO_FACSTREAM
+    if (act) mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+#endif
+    TRACE5(1);
 #ifndef K3_NO_WAIT
     mbar_wait(&vbar[p], (vph >> p) & 1);
 #endif
-    TRACE5(1);
+    if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
+    vph ^= 1u << p;
+    TRACE5(2);
     if (act) {
-      const int q = fseq(hh, s);
-#ifndef K3_NO_FACSTREAM
-      mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
-#endif
-      TRACE5(2);
       const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
       // input vector: own half; bottom at F+1 reads x_t (top buffer);
       // the middle block adds the bottom chain's part
@@ -754,8 +814,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     TRACE5(3);
     __syncthreads();
     TRACE5(4);
-    if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
-    vph ^= 1u << p;
     // epilogue: next-stage rows to the exchange scratch, outputs kept
     const bool last = s + 1 >= S;
     cplx outv[2];
@@ -766,8 +824,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         const int o = tl + u * 128;
         if (o >= nout) break;
         const int orow = o / rg, oc = o % rg;
-        cplx acc = red[((size_t)hh * nsl_max) * rstride + o];
-        for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, red[((size_t)hh * nsl_max + q2) * rstride + o]);
+        const cplx *rq = red + (size_t)hh * nsl_max * rstride + o;
+        cplx acc = rq[0];
+        if constexpr (MMA) {  // 4 K-slices (warps); same summation order
+          const cplx r1 = rq[rstride], r2 = rq[2 * rstride], r3 = rq[3 * rstride];
+          acc = cadd(cadd(cadd(acc, r1), r2), r3);
+        } else {
+          for (int q2 = 1; q2 < nslice; ++q2) acc = cadd(acc, rq[(size_t)q2 * rstride]);
+        }
         offs[u] = ((size_t)k * m + r0 + orow) * ldx + chunk0 + oc;
         cplx out, nxt;
         if (kind == 0) {
@@ -790,11 +854,13 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 #endif
     __syncthreads();
     TRACE5(6);
-    if (t == 0 && !last) {
-      // exactly the deliveries counted for stage s+1 (see deliveries())
+    if ((t & 127) == 0 && !last) {
+      // exactly the deliveries counted for stage s+1 (see deliveries());
+      // thread 0 issues the top half's multicast, thread 128 the bottom's
       int kd;
-      if (block_of(0, s, kd) >= 0 && block_of(0, s + 1, kd) >= 0) push(0, p ^ 1);
-      if (block_of(1, s, kd) >= 0 && (block_of(1, s + 1, kd) >= 0 || s + 1 == F)) push(1, p ^ 1);
+      if (hh == 0 && block_of(0, s, kd) >= 0 && block_of(0, s + 1, kd) >= 0) push(0, p ^ 1);
+      if (hh == 1 && block_of(1, s, kd) >= 0 && (block_of(1, s + 1, kd) >= 0 || s + 1 == F))
+        push(1, p ^ 1);
     }
     if (act) {
 #pragma unroll
@@ -807,6 +873,566 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     TRACE5(7);
   }
   cluster.sync();
+}
+
+// K3 v6: v5 with warp specialisation and loop-invariant addressing.
+// The per-stage trace of v5 (tools/trace_solve5.py) showed ~2400 of ~4700
+// cycles per stage spent in scalar work on the critical path: thread 0
+// issuing the factor-tile bulk copies (the issue blocks while the TMA unit
+// is busy) and every thread recomputing output coordinates and 64-bit
+// addresses.  Here a ninth (producer) warp streams the factor tiles through
+// full/empty mbarrier pairs up to FAC_STAGES tiles ahead, the 8 compute warps
+// synchronise on named barrier 1 only, and all per-thread offsets are
+// computed once before the stage loop.  Arithmetic, exchange protocol and
+// results are those of v5.
+#define SOLVE6_THREADS 288
+#define SOLVE6_COMPUTE 256
+
+__device__ __forceinline__ void bar_compute() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(SOLVE6_COMPUTE) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(SOLVE6_THREADS, 1)
+    k_block_solve6(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const SolveVisit V = visits[blockIdx.y];
+  const FactDev f = *V.f;
+  const int m = f.m, nb = f.nb, tw = f.twist;
+  const int chunk0 = blockIdx.z * rc;
+  const int rg = min(rc, nrhs - chunk0);
+  const int t = threadIdx.x;
+  const bool producer = t >= SOLVE6_COMPUTE;
+  const int hh = (t >> 7) & 1, tl = t & 127;  // compute threads: half, lane in half
+  if (V.nz) {
+    int any = 0;
+    for (int r = 0; r < rg; ++r) any |= V.nz[chunk0 + r];
+    if (!any) return;
+  }
+  const int rows_per = (m + C - 1) / C;
+  const int r0 = rank * rows_per;
+  const int nr = max(0, min(rows_per, m - r0));
+  const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
+  const size_t ldx = nrhs;
+  const uint16_t mask = (uint16_t)((1u << C) - 1);
+  constexpr int NSL = 4;  // K-slices = warps per half
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *vbar = (uint64_t *)smem_raw;   // [2 parity]
+  uint64_t *full = vbar + 2;               // [2 halves][FAC_STAGES]
+  uint64_t *empty = full + 2 * FAC_STAGES; // [2 halves][FAC_STAGES]
+  cplx *vec = (cplx *)(smem_raw + 256);    // [2 halves][2 parity][vstride]
+  const int vstride = m * rc + 2;
+  cplx *fac = vec + 4 * vstride;           // [2 halves][FAC_STAGES][fstride]
+  const int fstride = ((rows_max + 7) & ~7) * m + 2;
+  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][NSL][rows_max*rc]
+  const int rstride = rows_max * rc;
+  auto VEC = [&](int h, int p) { return vec + (h * 2 + p) * vstride; };
+  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  auto XG = [&](int h, int p) { return xg + ((size_t)h * 2 + p) * m * rg; };
+
+  auto block_of = [&](int h, int st, int &kind) -> int {
+    kind = st < F ? 0 : (st == F ? 1 : 2);
+    if (h == 0) {
+      if (st < F) return st >= F - nt ? st - (F - nt) : -1;
+      if (st == F) return tw;
+      int j = st - F - 1;
+      return j < nt ? tw - 1 - j : -1;
+    }
+    if (st < F) return st >= F - nbt ? nb - 1 - (st - (F - nbt)) : -1;
+    if (st == F) return -1;
+    int j = st - F - 1;
+    return j < nbt ? tw + 1 + j : -1;
+  };
+  auto fseq = [&](int h, int st) {
+    if (h == 0) return st - (F - nt);
+    return st < F ? st - (F - nbt) : st - (F - nbt) - 1;
+  };
+  auto deliveries = [&](int st) {
+    if (st < 0 || st >= S) return 0;
+    int kind, n = 0;
+    if (block_of(0, st, kind) >= 0) ++n;
+    if (block_of(1, st, kind) >= 0 && st != F + 1) ++n;
+    if (st == F && nbt > 0) ++n;
+    return n;
+  };
+  const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
+  const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
+  const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
+  auto push = [&](int h, int p) {
+    if (push_bytes)
+      bulk_g2s_multicast(VEC(h, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[p], mask);
+  };
+
+#ifdef DS_SOLVE_TRACE5
+  // every rank of cluster (0,0) traces; the launch index is the count of
+  // rank-0 CTAs seen before (rank 0 bumps it after the kernel's first sync)
+  int tr5 = -1;
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    tr5 = *(volatile int *)&g_tr5_n;
+    if (tr5 >= 64) tr5 = -1;
+  }
+#endif
+  if (t == 0) {
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  cluster.sync();
+#ifdef DS_SOLVE_TRACE5
+  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) atomicAdd(&g_tr5_n, 1);
+#endif
+
+  if (producer) {
+    // ---- factor-tile stream: tiles in stage order, FAC_STAGES ahead
+    if (t == SOLVE6_COMPUTE) {
+      int kind;
+      for (int st = 0; st < S; ++st) {
+        for (int h = 0; h < 2; ++h) {
+          const int k = block_of(h, st, kind);
+          if (k < 0) continue;
+          const int q = fseq(h, st), slot = q % FAC_STAGES;
+          if (q >= FAC_STAGES) mbar_wait(&empty[h * FAC_STAGES + slot], ((q / FAC_STAGES) - 1) & 1);
+          mbar_expect_tx(&full[h * FAC_STAGES + slot], fac_bytes);
+          if (fac_bytes)
+            bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m,
+                     fac_bytes, &full[h * FAC_STAGES + slot]);
+        }
+      }
+    }
+  } else {
+    if (t == 0) {
+      mbar_expect_tx(&vbar[0], deliveries(0) * vec_bytes);
+      if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
+    }
+    // prologue: b_0 (top, stage F-nt) and b_{n_b-1} (bottom, stage F-nbt)
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && nbt == 0) break;
+      const int st0 = h == 0 ? F - nt : F - nbt;
+      const int k0 = h == 0 ? 0 : nb - 1;
+      for (int e = t; e < nr * rg; e += SOLVE6_COMPUTE) {
+        int row = e / rg, c = e % rg;
+        XG(h, st0 & 1)[(r0 + row) * rg + c] = V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + c];
+      }
+    }
+    fence_proxy_async_global();
+    bar_compute();
+    if (t == 0) {
+      push(0, (F - nt) & 1);
+      if (nbt > 0) push(1, (F - nbt) & 1);
+    }
+
+    // ---- loop invariants: my (up to 2) outputs of my half
+    const int nout = nr * rg;
+    const size_t blk = (size_t)m * ldx;  // one block of the [nb][m][nrhs] layout
+    int xoff[2];                          // exchange scratch offset (row-major m x rg)
+    size_t goff[2];                       // offset of (row, col) in a block of V.rhs / V.x
+    bool has[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int o = tl + u * 128;
+      has[u] = o < nout;
+      const int orow = has[u] ? o / rg : 0, oc = has[u] ? o % rg : 0;
+      xoff[u] = (r0 + orow) * rg + oc;
+      goff[u] = (size_t)(r0 + orow) * ldx + chunk0 + oc;
+    }
+    const int warp = tl >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+    const int nk = (m + 3) >> 2, kb = (warp * nk) >> 2, ke = ((warp + 1) * nk) >> 2;
+    const int MT = (nr + 7) >> 3, NT = (rg + 7) >> 3;
+    const int sel = (MT > 1 ? 4 : 0) + (NT > 1 ? 2 : 0);
+    cplx *rp = red + ((size_t)hh * NSL + warp) * rstride;
+    const cplx *rq = red + (size_t)hh * NSL * rstride;
+    uint32_t vph = 0;
+
+    for (int s = 0; s < S; ++s) {
+      const int p = s & 1;
+      TRACE5(0);
+      int kind, k = block_of(hh, s, kind);
+      const bool act = k >= 0;
+      // epilogue operands (independent of the chain)
+      cplx aux[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+      cplx coef = make_double2(0.0, 0.0);
+      if (act) {
+        if (kind == 0) {
+          coef = hh == 0 ? f.lcoef[k + 1] : f.ucoef[k - 1];
+          const int kn = hh == 0 ? k + 1 : k - 1;
+          if (hh == 0 || kn > tw) {
+            const cplx *src = V.rhs + (size_t)kn * blk;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              if (has[u]) aux[u] = src[goff[u]];
+          }
+        } else if (kind == 2) {
+          coef = hh == 0 ? f.ucoef[k] : f.lcoef[k];
+          const cplx *src = V.x + (size_t)k * blk;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (has[u]) aux[u] = __ldcg(src + goff[u]);
+        }
+      }
+      TRACE5(8);
+      const int q = act ? fseq(hh, s) : 0;
+      if (act) mbar_wait(&full[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+      TRACE5(1);
+      mbar_wait(&vbar[p], (vph >> p) & 1);
+      if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
+      vph ^= 1u << p;
+      TRACE5(2);
+      if (act) {
+        const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
+        const cplx *X = VEC((hh == 1 && s == F + 1) ? 0 : hh, p);
+        const cplx *X2 = (kind == 1 && nbt > 0) ? VEC(1, p) : nullptr;
+        double cr[2][2][2] = {}, ci[2][2][2] = {};
+#ifdef K3_NO_COMPUTE
+        if (false)
+#endif
+        {
+#define K3_PRODUCT(mt_, nt_, x2_) \
+  mma_product<mt_, nt_, x2_>(A, m, X, X2, rg, m, kb, ke, g, tg, cr, ci)
+          switch (sel + (X2 ? 1 : 0)) {
+            case 0: K3_PRODUCT(1, 1, false); break;
+            case 1: K3_PRODUCT(1, 1, true); break;
+            case 2: K3_PRODUCT(1, 2, false); break;
+            case 3: K3_PRODUCT(1, 2, true); break;
+            case 4: K3_PRODUCT(2, 1, false); break;
+            case 5: K3_PRODUCT(2, 1, true); break;
+            case 6: K3_PRODUCT(2, 2, false); break;
+            default: K3_PRODUCT(2, 2, true); break;
+          }
+#undef K3_PRODUCT
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int ntt = 0; ntt < 2; ++ntt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = mt * 8 + g, col = ntt * 8 + 2 * tg + e;
+              if (mt < MT && ntt < NT && row < nr && col < rg)
+                rp[row * rg + col] = make_double2(cr[mt][ntt][e], ci[mt][ntt][e]);
+            }
+      }
+      TRACE5(3);
+      bar_compute();
+      TRACE5(4);
+      // the factor tiles of this stage are consumed: hand the slots back
+      if (t == 0) {
+        int kd;
+        for (int h = 0; h < 2; ++h)
+          if (block_of(h, s, kd) >= 0) mbar_arrive(&empty[h * FAC_STAGES + fseq(h, s) % FAC_STAGES]);
+      }
+      // epilogue: split-K sum (fixed order), chain update, exchange rows
+      const bool last = s + 1 >= S;
+      cplx outv[2];
+      if (act) {
+        cplx *xgo = XG(hh, p ^ 1);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!has[u]) continue;
+          const int o = tl + u * 128;
+          const cplx r1 = rq[o + rstride], r2 = rq[o + 2 * rstride], r3 = rq[o + 3 * rstride];
+          const cplx acc = cadd(cadd(cadd(rq[o], r1), r2), r3);
+          cplx out, nxt;
+          if (kind == 0) {
+            out = acc;
+            nxt = csub(aux[u], cmul(coef, acc));
+          } else if (kind == 1) {
+            out = acc;
+            nxt = acc;
+          } else {
+            out = csub(aux[u], cmul(coef, acc));
+            nxt = out;
+          }
+          outv[u] = out;
+          if (!last) xgo[xoff[u]] = nxt;
+        }
+      }
+      TRACE5(5);
+      fence_proxy_async_global();
+      bar_compute();
+      TRACE5(6);
+      if (tl == 0 && !last) {
+        // exactly the deliveries counted for stage s+1 (see deliveries());
+        // thread 0 issues the top half's multicast, thread 128 the bottom's
+        int kd;
+        if (hh == 0 && block_of(0, s, kd) >= 0 && block_of(0, s + 1, kd) >= 0) push(0, p ^ 1);
+        if (hh == 1 && block_of(1, s, kd) >= 0 && (block_of(1, s + 1, kd) >= 0 || s + 1 == F))
+          push(1, p ^ 1);
+      }
+      if (act) {
+        cplx *dst = V.x + (size_t)k * blk;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (has[u]) dst[goff[u]] = outv[u];
+      }
+      TRACE5(7);
+    }
+  }
+  cluster.sync();  // no CTA leaves while multicasts into it may be in flight
+}
+
+// K3 v7: the two twisted half-chains staggered by half a stage.
+// The v5 stage is  exchange (~2000 cycles: rows -> L2 -> multicast, plus the
+// factor-tile stream sharing the SM's ingress) -> product -> epilogue, all
+// in series (tools/exchange_load_micro.cu, tools/trace_solve5.py).  The top
+// and bottom chains are independent until the middle block, so here all 8
+// warps compute one chain's block product while the other chain's exchange
+// is in flight: half-steps alternate top(s), bottom(s), top(s+1), ...
+// Exchange barriers are per (input buffer, parity); x_t is multicast into
+// both buffers so every buffer has exactly one reader per stage, and a peer
+// can only refill a buffer after this CTA's reader has passed its barrier
+// (the refill needs this CTA's push, which follows that reader).
+// Warps: n-tile = warp / KS, K-slice = warp % KS with KS = 8 / NT.
+__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+    k_block_solve7(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const SolveVisit V = visits[blockIdx.y];
+  const FactDev f = *V.f;
+  const int m = f.m, nb = f.nb, tw = f.twist;
+  const int chunk0 = blockIdx.z * rc;
+  const int rg = min(rc, nrhs - chunk0);
+  const int t = threadIdx.x;
+  if (V.nz) {
+    int any = 0;
+    for (int r = 0; r < rg; ++r) any |= V.nz[chunk0 + r];
+    if (!any) return;
+  }
+  const int rows_per = (m + C - 1) / C;
+  const int r0 = rank * rows_per;
+  const int nr = max(0, min(rows_per, m - r0));
+  const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
+  const size_t ldx = nrhs;
+  const uint16_t mask = (uint16_t)((1u << C) - 1);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *vbar = (uint64_t *)smem_raw;  // [2 buffers][2 parity]
+  uint64_t *fbar = vbar + 4;              // [2 halves][FAC_STAGES]
+  cplx *vec = (cplx *)(smem_raw + 256);   // [2 buffers][2 parity][vstride]
+  const int vstride = m * rc + 2;
+  cplx *fac = vec + 4 * vstride;          // [2 halves][FAC_STAGES][fstride]
+  const int fstride = ((rows_max + 7) & ~7) * m + 2;
+  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [KS][rows_max * rc]
+  const int rstride = rows_max * rc;
+  auto VEC = [&](int b, int p) { return vec + (b * 2 + p) * vstride; };
+  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  auto XG = [&](int h, int p) { return xg + ((size_t)h * 2 + p) * m * rg; };
+
+  auto block_of = [&](int h, int st, int &kind) -> int {
+    kind = st < F ? 0 : (st == F ? 1 : 2);
+    if (h == 0) {
+      if (st < F) return st >= F - nt ? st - (F - nt) : -1;
+      if (st == F) return tw;
+      int j = st - F - 1;
+      return j < nt ? tw - 1 - j : -1;
+    }
+    if (st < F) return st >= F - nbt ? nb - 1 - (st - (F - nbt)) : -1;
+    if (st == F) return -1;
+    int j = st - F - 1;
+    return j < nbt ? tw + 1 + j : -1;
+  };
+  // q-th tile of half h <-> stage
+  auto fseq = [&](int h, int st) {
+    if (h == 0) return st - (F - nt);
+    return st < F ? st - (F - nbt) : st - (F - nbt) - 1;
+  };
+  auto tile_stage = [&](int h, int q) {
+    if (h == 0) return q + (F - nt);
+    return q < nbt ? q + (F - nbt) : q + (F - nbt) + 1;
+  };
+  const int ntiles[2] = {2 * nt + 1, 2 * nbt};
+  // vectors delivered into buffer b for stage st (0 or 1)
+  auto deliv = [&](int b, int st) -> int {
+    if (st < 0 || st >= S) return 0;
+    if (b == 0) return st >= F - nt && st <= F + nt;
+    return nbt > 0 && st >= F - nbt && st <= F + nbt;
+  };
+  const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
+  const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
+  const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
+  auto load_tile = [&](int h, int q) {  // thread 0
+    if (q >= ntiles[h]) return;
+    int kind, k = block_of(h, tile_stage(h, q), kind);
+    const int slot = q % FAC_STAGES;
+    uint64_t *bar = &fbar[h * FAC_STAGES + slot];
+    mbar_expect_tx(bar, fac_bytes);
+    if (fac_bytes)
+      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+  };
+  auto push = [&](int b, int h, int p) {  // rows of XG(h, p) -> buffer (b, p) of every CTA
+    if (push_bytes)
+      bulk_g2s_multicast(VEC(b, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[b * 2 + p], mask);
+  };
+
+#ifdef DS_SOLVE_TRACE5
+  int tr5 = -1;
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    tr5 = *(volatile int *)&g_tr5_n;
+    if (tr5 >= 64) tr5 = -1;
+  }
+#endif
+  if (t == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&vbar[i], 1);
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();
+#ifdef DS_SOLVE_TRACE5
+  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) atomicAdd(&g_tr5_n, 1);
+#endif
+  if (t == 0) {
+    for (int b = 0; b < 2; ++b)
+      for (int st = 0; st < 2 && st < S; ++st) mbar_expect_tx(&vbar[b * 2 + st], deliv(b, st) * vec_bytes);
+    for (int q = 0; q < FAC_STAGES - 1; ++q) {
+      load_tile(0, q);
+      load_tile(1, q);
+    }
+  }
+  // prologue: b_0 (top, stage F-nt) and b_{n_b-1} (bottom, stage F-nbt)
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && nbt == 0) break;
+    const int st0 = h == 0 ? F - nt : F - nbt;
+    const int k0 = h == 0 ? 0 : nb - 1;
+    for (int e = t; e < nr * rg; e += SOLVE_THREADS) {
+      int row = e / rg, c = e % rg;
+      XG(h, st0 & 1)[(r0 + row) * rg + c] = V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + c];
+    }
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+  if (t == 0) {
+    push(0, 0, (F - nt) & 1);
+    if (nbt > 0) push(1, 1, (F - nbt) & 1);
+  }
+
+  // ---- loop invariants
+  const int nout = nr * rg;
+  const bool has = t < nout;
+  const int orow = has ? t / rg : 0, oc = has ? t % rg : 0;
+  const int xoff = (r0 + orow) * rg + oc;
+  const size_t goff = (size_t)(r0 + orow) * ldx + chunk0 + oc;
+  const size_t blk = (size_t)m * ldx;
+  const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+  const int MT = (nr + 7) >> 3, NT = (rg + 7) >> 3;
+  const int KS = NT > 1 ? 4 : 8;
+  const int ntw = warp / KS, ksl = warp % KS;
+  const int nk = (m + 3) >> 2, kb = (ksl * nk) / KS, ke = ((ksl + 1) * nk) / KS;
+  cplx *rp = red + (size_t)ksl * rstride;
+
+  for (int s = 0; s < S; ++s) {
+    const int p = s & 1;
+    const uint32_t par = (s >> 1) & 1;
+    for (int h = 0; h < 2; ++h) {
+      TRACE5(h ? 4 : 0);
+      int kind, k = block_of(h, s, kind);
+      const bool act = k >= 0;
+      cplx aux = make_double2(0.0, 0.0), coef = make_double2(0.0, 0.0);
+      if (act && has) {
+        if (kind == 0) {
+          coef = h == 0 ? f.lcoef[k + 1] : f.ucoef[k - 1];
+          const int kn = h == 0 ? k + 1 : k - 1;
+          if (h == 0 || kn > tw) aux = V.rhs[(size_t)kn * blk + goff];
+        } else if (kind == 2) {
+          coef = h == 0 ? f.ucoef[k] : f.lcoef[k];
+          aux = __ldcg(V.x + (size_t)k * blk + goff);
+        }
+      }
+      const int q = act ? fseq(h, s) : 0;
+      const bool x2 = h == 0 && kind == 1 && nbt > 0;
+      if (act) {
+        mbar_wait(&fbar[h * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+        mbar_wait(&vbar[h * 2 + p], par);
+        if (x2) mbar_wait(&vbar[2 + p], par);
+      }
+      TRACE5(h ? 5 : 1);
+      if (act) {
+        const cplx *A = fac + (h * FAC_STAGES + q % FAC_STAGES) * fstride;
+        const cplx *X = VEC(h, p) + ntw * 8;
+        const cplx *X2 = x2 ? VEC(1, p) + ntw * 8 : nullptr;
+        double cr[2][2][2] = {}, ci[2][2][2] = {};
+        if (ntw < NT) {
+#ifdef K3_NO_COMPUTE
+          if (false)
+#endif
+          {
+            const int sel = (MT > 1 ? 2 : 0) + (X2 ? 1 : 0);
+#define K3_PRODUCT(mt_, x2_) mma_product<mt_, 1, x2_>(A, m, X, X2, rg, m, kb, ke, g, tg, cr, ci)
+            switch (sel) {
+              case 0: K3_PRODUCT(1, false); break;
+              case 1: K3_PRODUCT(1, true); break;
+              case 2: K3_PRODUCT(2, false); break;
+              default: K3_PRODUCT(2, true); break;
+            }
+#undef K3_PRODUCT
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int row = mt * 8 + g, col = ntw * 8 + 2 * tg + e;
+              if (mt < MT && row < nr && col < rg)
+                rp[row * rg + col] = make_double2(cr[mt][0][e], ci[mt][0][e]);
+            }
+        }
+      }
+      TRACE5(h ? 6 : 2);
+      __syncthreads();
+      // buffer (h, p) has no other reader at stage s: re-arm it for s+2
+      if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[h * 2 + p], deliv(h, s + 2) * vec_bytes);
+      const bool last = s + 1 >= S;
+      cplx out = make_double2(0.0, 0.0);
+      if (act && has) {
+        cplx acc = red[t];
+        for (int q2 = 1; q2 < KS; ++q2) acc = cadd(acc, red[(size_t)q2 * rstride + t]);
+        cplx nxt;
+        if (kind == 0) {
+          out = acc;
+          nxt = csub(aux, cmul(coef, acc));
+        } else if (kind == 1) {
+          out = acc;
+          nxt = acc;
+        } else {
+          out = csub(aux, cmul(coef, acc));
+          nxt = out;
+        }
+        if (!last) XG(h, p ^ 1)[xoff] = nxt;
+      }
+      fence_proxy_async_global();
+      __syncthreads();
+      TRACE5(h ? 7 : 3);
+      if (t == 0) {
+        if (act && !last) {
+          int kd;
+          if (h == 0) {
+            if (block_of(0, s + 1, kd) >= 0) push(0, 0, p ^ 1);
+            if (kind == 1 && nbt > 0) push(1, 0, p ^ 1);  // x_t for the bottom chain
+          } else if (block_of(1, s + 1, kd) >= 0 || s + 1 == F) {
+            push(1, 1, p ^ 1);
+          }
+        }
+        if (act) load_tile(h, q + FAC_STAGES - 1);
+      }
+      if (act && has) V.x[(size_t)k * blk + goff] = out;
+    }
+  }
+  cluster.sync();  // no CTA leaves while multicasts into it may be in flight
+}
+
+static size_t solve7_smem(int m, int rc, int C) {
+  int r = (m + C - 1) / C;
+  size_t rows_max = r + (r & 1);
+  size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) + 8 * rows_max * rc;
+  return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
 }
 
 static int solve_rows_max(int max_m, int C) {
@@ -893,7 +1519,8 @@ static int pick_cfg(int max_m, int nrhs, SolveCfg *out) {
 
 // split-K slices per half: 8 for full chunks, up to 16 when the chunk is
 // narrow (fewer outputs per half leave more threads for the K split)
-static int solve5_nsl(int m, int rc, int C) {
+static int solve5_nsl(int m, int rc, int C, bool mma) {
+  if (mma) return 4;  // one K-slice per warp of a half
   int rstride = solve_rows_max(m, C) * rc;
   return std::max(8, std::min(16, 1024 / std::max(1, rstride)));
 }
@@ -901,27 +1528,29 @@ static int solve5_nsl(int m, int rc, int C) {
 // Dynamic shared memory of one CTA.  At least 118 KB, so a CTA always owns
 // its SM: the chain is latency bound, and two CTAs sharing an SM would
 // serialise their stages (the wave count below assumes one CTA per SM).
-static size_t solve5_smem(int m, int rc, int C) {
+static size_t solve5_smem(int m, int rc, int C, bool mma) {
   size_t rows_max = solve_rows_max(m, C);
   size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
   size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * solve_lda(m) + 2) +
-                 2 * (size_t)solve5_nsl(m, rc, C) * rows_max * rc;
+                 2 * (size_t)solve5_nsl(m, rc, C, mma) * rows_max * rc;
   return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
 }
 
 typedef void (*Solve5Fn)(const SolveVisit *, int, int, int, int, int);
 
 // Co-resident clusters of C CTAs for this footprint (7 x 16 on a 148-SM B200).
-static int solve5_max_clusters(Solve5Fn fn, int C, size_t smem) {
-  static std::vector<std::pair<std::pair<int, size_t>, int>> memo;
+static int solve_max_clusters(const void *fn, int threads, int C, size_t smem) {
+  static std::vector<std::tuple<const void *, int, int, size_t, int>> memo;
   for (auto &e : memo)
-    if (e.first.first == C && e.first.second == smem) return e.second;
-  cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (std::get<0>(e) == fn && std::get<1>(e) == threads && std::get<2>(e) == C &&
+        std::get<3>(e) == smem)
+      return std::get<4>(e);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -931,12 +1560,125 @@ static int solve5_max_clusters(Solve5Fn fn, int C, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, (const void *)fn, &cfg) != cudaSuccess || n < 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n < 0) {
     cudaGetLastError();
     n = 0;
   }
-  memo.push_back({{C, smem}, n});
+  memo.emplace_back(fn, threads, C, smem, n);
   return n;
+}
+static int solve5_max_clusters(Solve5Fn fn, int C, size_t smem) {
+  return solve_max_clusters((const void *)fn, SOLVE_THREADS, C, smem);
+}
+
+// Choose the (cluster size, RHS chunk) that runs a step of nvisit visits in
+// the fewest waves of co-resident clusters, then with the least arithmetic
+// per CTA and stage (rows per CTA x chunk width); larger clusters on ties.
+template <typename SmemFn>
+static bool pick_cluster_chunk(const void *fn, int threads, int nvisit, int nrhs, int max_m,
+                               bool mma, SmemFn smem_of, int *Cout, int *rcout, long *waves_out) {
+  static const int rc_min = std::max(1, env_int("DS_K3_RCMIN", 4));
+  static const int rc_max = std::max(1, env_int("DS_K3_RCMAX", 16));
+  static const int c_only = env_int("DS_K3_CLUSTER", 0);
+  int bestC = 0, bestRc = 0;
+  long best_waves = 0, best_work = 0;
+  for (int C : {16, 8}) {
+    if (c_only && C != c_only) continue;
+    const int rows = solve_rows_max(max_m, C);
+    for (int rc = std::min(nrhs, rc_max); rc >= 1; rc = rc > 1 ? (rc + 1) / 2 : 0) {
+      if (rc < std::min(rc_min, nrhs) && bestC) break;
+      if (rows * rc > 256 || (mma && rows > 16)) continue;
+      size_t smem = smem_of(rc, C);
+      if (smem > 232448) continue;
+      int maxcl = solve_max_clusters(fn, threads, C, smem);
+      if (maxcl < 1) continue;
+      long ncl = (long)nvisit * ((nrhs + rc - 1) / rc);
+      long waves = (ncl + maxcl - 1) / maxcl;
+      long work = waves * (long)rows * rc;
+      if (!bestC || waves < best_waves || (waves == best_waves && work < best_work) ||
+          (waves == best_waves && work == best_work && C > bestC)) {
+        bestC = C;
+        bestRc = rc;
+        best_waves = waves;
+        best_work = work;
+      }
+      if (rc == 1) break;
+    }
+  }
+  *Cout = bestC;
+  *rcout = bestRc;
+  *waves_out = best_waves;
+  return bestC != 0;
+}
+
+static size_t solve6_smem(int m, int rc, int C) {
+  size_t rows_max = solve_rows_max(m, C);
+  size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) +
+                 2 * 4 * rows_max * rc;
+  return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
+}
+
+static int launch_v7(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
+  const void *fn = (const void *)k_block_solve7;
+  int C, rc;
+  long waves;
+  if (!pick_cluster_chunk(fn, SOLVE_THREADS, nvisit, nrhs, max_m, true,
+                          [&](int r, int c) { return solve7_smem(max_m, r, c); }, &C, &rc, &waves))
+    return ds_fail(DS_ECONFIG, "block solve v7: no feasible cluster configuration");
+  const size_t smem = solve7_smem(max_m, rc, C);
+  if (env_int("DS_K3_DEBUG", 0))
+    fprintf(stderr, "K3 v7: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld smem %zu\n", nvisit,
+            nrhs, max_m, C, rc, waves, smem);
+  DS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
+  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve7, (const SolveVisit *)visits_dev, nrhs, rc,
+                             solve_rows_max(max_m, C)));
+  ctx->launches++;
+  return DS_OK;
+}
+
+static int launch_v6(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
+  const void *fn = (const void *)k_block_solve6;
+  int C, rc;
+  long waves;
+  if (!pick_cluster_chunk(fn, SOLVE6_THREADS, nvisit, nrhs, max_m, true,
+                          [&](int r, int c) { return solve6_smem(max_m, r, c); }, &C, &rc, &waves))
+    return ds_fail(DS_ECONFIG, "block solve v6: no feasible cluster configuration");
+  const size_t smem = solve6_smem(max_m, rc, C);
+  if (env_int("DS_K3_DEBUG", 0))
+    fprintf(stderr, "K3 v6: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld smem %zu\n", nvisit,
+            nrhs, max_m, C, rc, waves, smem);
+  DS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
+  cfg.blockDim = dim3(SOLVE6_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve6, (const SolveVisit *)visits_dev, nrhs, rc,
+                             solve_rows_max(max_m, C)));
+  ctx->launches++;
+  return DS_OK;
 }
 
 static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
@@ -958,7 +1700,7 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
     for (int rc = std::min(nrhs, rc_max); rc >= 1; rc = rc > 1 ? (rc + 1) / 2 : 0) {
       if (rc < std::min(rc_min, nrhs) && bestC) break;
       if (rows * rc > 256 || (mma && rows > 16)) continue;
-      size_t smem = solve5_smem(max_m, rc, C);
+      size_t smem = solve5_smem(max_m, rc, C, mma);
       if (smem > 232448) continue;
       int maxcl = solve5_max_clusters(fn, C, smem);
       if (maxcl < 1) continue;
@@ -977,7 +1719,7 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   }
   if (!bestC) return ds_fail(DS_ECONFIG, "block solve v5: no feasible cluster configuration");
   const int C = bestC, rc = bestRc;
-  const size_t smem = solve5_smem(max_m, rc, C);
+  const size_t smem = solve5_smem(max_m, rc, C, mma);
   if (env_int("DS_K3_DEBUG", 0))
     fprintf(stderr, "K3 v5: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld maxcl %d smem %zu\n", nvisit,
             nrhs, max_m, C, rc, best_waves, solve5_max_clusters(fn, C, smem), smem);
@@ -996,7 +1738,7 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   DS_CUDA(cudaLaunchKernelEx(&cfg, fn, (const SolveVisit *)visits_dev, nrhs, rc,
-                             solve_rows_max(max_m, C), solve5_nsl(max_m, rc, C), lda_pad));
+                             solve_rows_max(max_m, C), solve5_nsl(max_m, rc, C, mma), lda_pad));
   ctx->launches++;
   return DS_OK;
 }
@@ -1006,7 +1748,10 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
   if (nvisit < 1) return DS_OK;
   {
     const char *v = getenv("DS_K3");
-    if (!(v && std::string(v) == "v3")) return launch_v5(ctx, visits_dev, nvisit, nrhs, max_m);
+    const std::string k3 = v ? v : "v7";
+    if (k3 == "v7") return launch_v7(ctx, visits_dev, nvisit, nrhs, max_m);
+    if (k3 == "v6") return launch_v6(ctx, visits_dev, nvisit, nrhs, max_m);
+    if (k3 == "v5") return launch_v5(ctx, visits_dev, nvisit, nrhs, max_m);
   }
   SolveCfg sc;
   if (!pick_cfg(max_m, nrhs, &sc))
@@ -1043,7 +1788,7 @@ extern "C" DS_API int ds_debug_solve_trace(long long *out) {
 #ifdef DS_SOLVE_TRACE5
 extern "C" DS_API int ds_debug_solve_trace5(long long *out, int *count) {
   DS_CUDA(cudaDeviceSynchronize());
-  DS_CUDA(cudaMemcpyFromSymbol(out, g_tr5, sizeof(long long) * 64 * 160 * 8));
+  DS_CUDA(cudaMemcpyFromSymbol(out, g_tr5, sizeof(long long) * 64 * 16 * 160 * 12));
   DS_CUDA(cudaMemcpyFromSymbol(count, g_tr5_n, sizeof(int)));
   return DS_OK;
 }

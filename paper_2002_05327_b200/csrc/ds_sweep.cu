@@ -68,6 +68,7 @@ struct XferDev {
 struct ds_plan {
   ds_ctx *ctx;
   int dim, nsub, nsweeps, nsteps, ndir, nrhs_max, gmax, max_m, max_w;
+  int max_axis_sum = 0;  // max over windows of sum of extents (assemble masks)
   int gcounts[3];
   int64_t nnodes;
   std::vector<int> vstep_off, xstep_off;  // host copies, size nsweeps*nsteps+1
@@ -125,39 +126,71 @@ static int plan_alloc(ds_plan *P, void **ptr, size_t bytes) {
 }
 
 // -------------------------------------------------------------- helpers
+//
+// All coordinate triples live in registers: every loop over the axes is
+// unrolled with a compile-time index, and runtime axis numbers go through
+// sel3 (a dynamically indexed local array would sit in local memory).
+// Index arithmetic is 32-bit (a window or band has < 2^31 nodes); each thread
+// owns one RHS column r of one node, so the node geometry is computed once
+// per node and the nrhs lanes of a node read contiguous 16-byte values.
 
-__device__ __forceinline__ bool in_box(const int *g, const int *lo, const int *shape, int dim) {
-  for (int a = 0; a < dim; ++a)
-    if (g[a] < lo[a] || g[a] >= lo[a] + shape[a]) return false;
-  return true;
+__device__ __forceinline__ int sel3(const int (&a)[3], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]);
 }
 
-__device__ __forceinline__ int64_t lin_of(const int *e, const int *shape, int dim) {
-  int64_t l = e[0];
-  for (int a = 1; a < dim; ++a) l = l * shape[a] + e[a];
+__device__ __forceinline__ bool in_box(const int (&g)[3], const int *lo, const int *shape, int dim) {
+  bool in = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    if (a < dim) in = in && g[a] >= lo[a] && g[a] < lo[a] + shape[a];
+  return in;
+}
+
+__device__ __forceinline__ int lin_of(const int (&e)[3], const int *shape, int dim) {
+  int l = e[0];
+#pragma unroll
+  for (int a = 1; a < 3; ++a)
+    if (a < dim) l = l * shape[a] + e[a];
   return l;
 }
 
-__device__ __forceinline__ void unlin(int64_t l, const int *shape, int dim, int *e) {
-  for (int a = dim - 1; a >= 1; --a) {
-    e[a] = (int)(l % shape[a]);
-    l /= shape[a];
+__device__ __forceinline__ int64_t lin_of64(const int (&e)[3], const int *shape, int dim) {
+  int64_t l = e[0];
+#pragma unroll
+  for (int a = 1; a < 3; ++a)
+    if (a < dim) l = l * shape[a] + e[a];
+  return l;
+}
+
+__device__ __forceinline__ void unlin(int l, const int *shape, int dim, int (&e)[3]) {
+  e[0] = e[1] = e[2] = 0;
+  if (dim == 3) {
+    e[2] = l % shape[2];
+    l /= shape[2];
   }
-  e[0] = (int)l;
+  e[1] = l % shape[1];
+  e[0] = l / shape[1];
 }
 
 // block layout offset -> window-local coordinates
-__device__ __forceinline__ void block_coords(const FactDev &f, int64_t blk, int *c) {
-  int k = (int)(blk / f.m), i = (int)(blk % f.m);
-  c[0] = c[1] = c[2] = 0;
-  c[f.block_axis] = k;
-  if (f.other[1] < 0) {
-    c[f.other[0]] = i;
-  } else {
-    int n1 = f.win_shape[f.other[1]];
-    c[f.other[0]] = i / n1;
-    c[f.other[1]] = i % n1;
+__device__ __forceinline__ void block_coords(const FactDev &f, int blk, int (&c)[3]) {
+  const int k = blk / f.m, i = blk % f.m;
+  int j0 = i, j1 = 0;
+  if (f.other[1] >= 0) {
+    const int n1 = sel3(f.win_shape, f.other[1]);
+    j0 = i / n1;
+    j1 = i % n1;
   }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    c[a] = a == f.block_axis ? k : (a == f.other[0] ? j0 : (a == f.other[1] ? j1 : 0));
+}
+
+// window-local coordinates -> block layout offset (registers only)
+__device__ __forceinline__ int block_off(const FactDev &f, const int (&c)[3]) {
+  int ib = f.other[0] >= 0 ? sel3(c, f.other[0]) : 0;
+  if (f.other[1] >= 0) ib = ib * sel3(f.win_shape, f.other[1]) + sel3(c, f.other[1]);
+  return sel3(c, f.block_axis) * f.m + ib;
 }
 
 // flags layout helpers (stride nrhs)
@@ -190,72 +223,138 @@ __device__ __forceinline__ int solve_cut(const Flags &F, int sweep, int sub, int
   return F.arr_cut[vi] & CUT_ALL;
 }
 
+#define SLOT_SMEM 32
+
 // ------------------------------------------------------------- K6 assemble
-__global__ void k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
-                           const SlotRef *__restrict__ slots, const cplx *__restrict__ f,
-                           int nrhs, int dim, int g0, int g1, int g2, Flags F) {
+// rhs (block layout [nb][m][R]) = own restricted source (sweep 1) + the
+// visit's queued payload slots in slot order; slots are zeroed as consumed.
+// Slot membership is separable (boxes), so each block first builds, per
+// window axis and coordinate, the bitmask of slots (bit 31: the own box)
+// covering it; a node's slot set is then the AND of its axis masks.
+__global__ void __launch_bounds__(256)
+    k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
+               const SlotRef *__restrict__ slots, const cplx *__restrict__ f, int nrhs, int dim,
+               int g0, int g1, int g2, Flags F) {
   __shared__ int s_nz[RMAX], s_own[RMAX];
+  __shared__ SlotRef s_slot[SLOT_SMEM];
+  extern __shared__ uint32_t s_mask[];  // [E0 | E1 | E2]
   const VisitDev V = visits[blockIdx.y];
   const SubDev &sd = subs[V.sub];
   const FactDev fd = *sd.f;
-  for (int r = threadIdx.x; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
-  __syncthreads();
-  const int gc[3] = {g0, g1, g2};
-  const int64_t total = (int64_t)fd.nb * fd.m * nrhs;
+  const int t = threadIdx.x;
+  for (int r = t; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
+  const int ns = V.nslot;
+  for (int k = t; k < min(ns, SLOT_SMEM); k += blockDim.x) s_slot[k] = slots[V.slot0 + k];
   const bool own = V.sweep == 1;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(q % nrhs);
-    int c[3];
-    block_coords(fd, q / nrhs, c);
-    int g[3];
-    for (int a = 0; a < 3; ++a) g[a] = sd.win_lo[a] + c[a];
-    cplx val = make_double2(0.0, 0.0);
-    if (own && in_box(g, sd.own_lo, sd.own_shape, dim)) {
-      cplx s = f[lin_of(g, gc, dim) * nrhs + r];
-      val = cadd(val, s);
-      if (cnonzero(s)) s_own[r] = 1;
+  const bool masks = ns <= 31;
+  const int E0 = sd.win_shape[0], E1 = sd.win_shape[1], E2 = dim == 3 ? sd.win_shape[2] : 0;
+  __syncthreads();
+  if (masks) {
+    for (int x = t; x < E0 + E1 + E2; x += blockDim.x) {
+      const int a = x < E0 ? 0 : (x < E0 + E1 ? 1 : 2);
+      const int gx = sd.win_lo[a] + x - (a == 0 ? 0 : (a == 1 ? E0 : E0 + E1));
+      uint32_t mk = 0;
+      for (int k = 0; k < ns; ++k)
+        if (gx >= s_slot[k].lo[a] && gx < s_slot[k].lo[a] + s_slot[k].shape[a]) mk |= 1u << k;
+      if (own && gx >= sd.own_lo[a] && gx < sd.own_lo[a] + sd.own_shape[a]) mk |= 1u << 31;
+      s_mask[x] = mk;
     }
-    for (int k = 0; k < V.nslot; ++k) {
-      const SlotRef &S = slots[V.slot0 + k];
-      if (!in_box(g, S.lo, S.shape, dim)) continue;
-      int e[3];
-      for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
-      int64_t idx = lin_of(e, S.shape, dim) * nrhs + r;
-      val = cadd(val, S.data[idx]);
-      S.data[idx] = make_double2(0.0, 0.0);
-    }
-    V.rhs[q] = val;
-    if (cnonzero(val)) s_nz[r] = 1;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
-    if (s_nz[r]) atomicOr(&V.nz[r], 1);
-    if (s_own[r]) atomicOr(&F.own_nz[(size_t)V.sub * nrhs + r], 1);
+  const int gc[3] = {g0, g1, g2};
+  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  const int nodes = fd.nb * fd.m;
+  int wlo[3], olo[3], osh[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    wlo[a] = sd.win_lo[a];
+    olo[a] = sd.own_lo[a];
+    osh[a] = sd.own_shape[a];
+  }
+  bool any = false, anyown = false;
+  if (ln < npb) {
+    for (int blk = blockIdx.x * npb + ln; blk < nodes; blk += gridDim.x * npb) {
+      int c[3], g[3];
+      block_coords(fd, blk, c);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) g[a] = wlo[a] + c[a];
+      cplx val = make_double2(0.0, 0.0);
+      if (masks) {
+        uint32_t mk = s_mask[c[0]] & s_mask[E0 + c[1]];
+        if (dim == 3) mk &= s_mask[E0 + E1 + c[2]];
+        if (mk >> 31) {
+          cplx sv = f[lin_of64(g, gc, dim) * nrhs + r];
+          val = cadd(val, sv);
+          anyown |= cnonzero(sv);
+        }
+        mk &= 0x7fffffffu;
+        while (mk) {
+          const int k = __ffs(mk) - 1;
+          mk &= mk - 1;
+          const SlotRef &S = s_slot[k];
+          int e[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
+          const int64_t idx = (int64_t)lin_of(e, S.shape, dim) * nrhs + r;
+          val = cadd(val, S.data[idx]);
+          S.data[idx] = make_double2(0.0, 0.0);
+        }
+      } else {
+        if (own && in_box(g, olo, osh, dim)) {
+          cplx sv = f[lin_of64(g, gc, dim) * nrhs + r];
+          val = cadd(val, sv);
+          anyown |= cnonzero(sv);
+        }
+        for (int k = 0; k < ns; ++k) {
+          const SlotRef &S = k < SLOT_SMEM ? s_slot[k] : slots[V.slot0 + k];
+          if (!in_box(g, S.lo, S.shape, dim)) continue;
+          int e[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
+          const int64_t idx = (int64_t)lin_of(e, S.shape, dim) * nrhs + r;
+          val = cadd(val, S.data[idx]);
+          S.data[idx] = make_double2(0.0, 0.0);
+        }
+      }
+      V.rhs[(int64_t)blk * nrhs + r] = val;
+      any |= cnonzero(val);
+    }
+  }
+  if (any) s_nz[r] = 1;
+  if (anyown) s_own[r] = 1;
+  __syncthreads();
+  for (int q = t; q < nrhs; q += blockDim.x) {
+    if (s_nz[q]) atomicOr(&V.nz[q], 1);
+    if (s_own[q]) atomicOr(&F.own_nz[(size_t)V.sub * nrhs + q], 1);
   }
 }
 
 // ----------------------------------------------------------- K5 accumulate
-__global__ void k_accumulate(const VisitDev *__restrict__ visits, int G,
-                             const SubDev *__restrict__ subs, cplx *u, int nrhs, int dim, int g0,
-                             int g1, int g2) {
+// u += beta00 * x over the visit's support; where supports of same-step
+// visits overlap the first visit owning the node sums all of them in visit
+// order (deterministic, no atomics on field values).
+__global__ void __launch_bounds__(256)
+    k_accumulate(const VisitDev *__restrict__ visits, int G, const SubDev *__restrict__ subs,
+                 cplx *u, int nrhs, int dim, int g0, int g1, int g2) {
   const int v = blockIdx.y;
   const SubDev &sd = subs[visits[v].sub];
   const int gc[3] = {g0, g1, g2};
-  int64_t nodes = (int64_t)sd.sup_shape[0] * sd.sup_shape[1] * (dim == 3 ? sd.sup_shape[2] : 1);
-  const int64_t total = nodes * nrhs;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(q % nrhs);
-    int e[3] = {0, 0, 0};
-    unlin(q / nrhs, sd.sup_shape, dim, e);
-    int g[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) g[a] = sd.sup_lo[a] + e[a];
+  const int t = threadIdx.x;
+  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  if (ln >= npb) return;
+  const int nodes = sd.sup_shape[0] * sd.sup_shape[1] * (dim == 3 ? sd.sup_shape[2] : 1);
+  for (int node = blockIdx.x * npb + ln; node < nodes; node += gridDim.x * npb) {
+    int e[3], g[3];
+    unlin(node, sd.sup_shape, dim, e);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) g[a] = a < dim ? sd.sup_lo[a] + e[a] : 0;
     bool owner = true;
-    for (int w = 0; w < v && owner; ++w)
-      if (in_box(g, subs[visits[w].sub].sup_lo, subs[visits[w].sub].sup_shape, dim)) owner = false;
+    for (int w = 0; w < v && owner; ++w) {
+      const SubDev &so = subs[visits[w].sub];
+      if (in_box(g, so.sup_lo, so.sup_shape, dim)) owner = false;
+    }
     if (!owner) continue;
-    int64_t gi = lin_of(g, gc, dim) * nrhs + r;
+    const int64_t gi = lin_of64(g, gc, dim) * nrhs + r;
     cplx acc = u[gi];
     bool touched = false;
     for (int w = v; w < G; ++w) {
@@ -264,10 +363,13 @@ __global__ void k_accumulate(const VisitDev *__restrict__ visits, int G,
       if (w != v && !in_box(g, sw.sup_lo, sw.sup_shape, dim)) continue;
       if (!W.nz[r]) continue;
       double beta = 1.0;
-      for (int a = 0; a < dim; ++a) beta = beta * sw.beta[a][g[a] - sw.sup_lo[a]];
-      int c[3] = {0, 0, 0};
-      for (int a = 0; a < dim; ++a) c[a] = g[a] - sw.win_lo[a];
-      cplx xv = W.x[block_offset(*sw.f, c) * nrhs + r];
+      int c[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (a < dim) beta = beta * sw.beta[a][g[a] - sw.sup_lo[a]];
+        c[a] = a < dim ? g[a] - sw.win_lo[a] : 0;
+      }
+      cplx xv = W.x[(int64_t)block_off(*sw.f, c) * nrhs + r];
       acc = cadd(acc, cscale(xv, beta));
       touched = true;
     }
@@ -276,20 +378,24 @@ __global__ void k_accumulate(const VisitDev *__restrict__ visits, int G,
 }
 
 // ------------------------------------------------------------ K4 transfer
-__device__ __forceinline__ double op_k2(const OpDev &o, const int *c) {
+__device__ __forceinline__ double op_k2(const OpDev &o, const int (&c)[3]) {
   if (o.kappa2_kind == 0) return o.kappa2[0];
-  if (o.kappa2_kind == 1) return o.kappa2[c[o.kappa2_axis]];
-  int64_t lin = c[0];
-  for (int a = 1; a < o.dim; ++a) lin = lin * o.shape[a] + c[a];
+  if (o.kappa2_kind == 1) return o.kappa2[sel3(c, o.kappa2_axis)];
+  int lin = c[0];
+#pragma unroll
+  for (int a = 1; a < 3; ++a)
+    if (a < o.dim) lin = lin * o.shape[a] + c[a];
   return o.kappa2[lin];
 }
 
-__global__ void k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
-                           const SubDev *__restrict__ subs, int nsub, int sweep, int nrhs, int dim,
-                           Flags F) {
+// psi (transfer.py:100-155): payload = s * (rhs|band + L_nb((w - 1) v)|band),
+// w = prod_a fac_a on ext; block 0 also does the arrival/emission bookkeeping
+// (ddm.py:262-279), one thread per RHS.
+__global__ void __launch_bounds__(256)
+    k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
+               const SubDev *__restrict__ subs, int nsub, int sweep, int nrhs, int dim, Flags F) {
   const XferDev &X = xfers[blockIdx.y];
   const VisitDev &V = visits[X.vidx];
-  // bookkeeping (ddm.py:262-279): one thread per RHS in block 0
   if (blockIdx.x == 0) {
     for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
       if (!V.nz[r]) continue;
@@ -306,54 +412,69 @@ __global__ void k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__
     }
   }
   if (X.use == 0) return;
+  const int t = threadIdx.x;
+  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  if (ln >= npb) return;
+  if (!V.nz[r]) return;
+  if (solve_cut(F, sweep, X.src, nsub, r, nrhs) & X.dirmask) return;
   const SubDev &ss = subs[X.src];
   const SubDev &sn = subs[X.dst];
   const FactDev fs = *ss.f;
   const OpDev &on = *sn.op;
-  int64_t nodes = (int64_t)X.band_shape[0] * X.band_shape[1] * (dim == 3 ? X.band_shape[2] : 1);
-  const int64_t total = nodes * nrhs;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int r = (int)(q % nrhs);
-    if (!V.nz[r]) continue;
-    int cut = solve_cut(F, sweep, X.src, nsub, r, nrhs);
-    if (cut & X.dirmask) continue;
-    int e[3] = {0, 0, 0};
-    unlin(q / nrhs, X.band_shape, dim, e);
-    int g[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) g[a] = X.band_lo[a] + e[a];
-    // w(p) = (prod_a fac_a - 1) * v(p) on ext
-    auto wval = [&](const int *p) -> cplx {
-      double wt = 1.0;
-      for (int a = 0; a < dim; ++a) wt = wt * X.fac[a][p[a] - X.ext_lo[a]];
-      int c[3] = {0, 0, 0};
-      for (int a = 0; a < dim; ++a) c[a] = p[a] - ss.win_lo[a];
-      cplx v = V.x[block_offset(fs, c) * nrhs + r];
-      return cscale(v, wt - 1.0);
-    };
-    int cn[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) cn[a] = g[a] - sn.win_lo[a];
+  int blo[3], elo[3], ehi[3], swlo[3], snlo[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    blo[a] = X.band_lo[a];
+    elo[a] = X.ext_lo[a];
+    ehi[a] = X.ext_lo[a] + X.ext_shape[a];
+    swlo[a] = ss.win_lo[a];
+    snlo[a] = sn.win_lo[a];
+  }
+  const int nodes = X.band_shape[0] * X.band_shape[1] * (dim == 3 ? X.band_shape[2] : 1);
+  // (w(p) - 1) v(p) with w = prod_a fac_a(p_a) on ext
+  auto wval = [&](const int (&p)[3]) -> cplx {
+    double wt = 1.0;
+    int c[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a < dim) wt = wt * X.fac[a][p[a] - elo[a]];
+      c[a] = a < dim ? p[a] - swlo[a] : 0;
+    }
+    cplx v = V.x[(int64_t)block_off(fs, c) * nrhs + r];
+    return cscale(v, wt - 1.0);
+  };
+  for (int node = blockIdx.x * npb + ln; node < nodes; node += gridDim.x * npb) {
+    int e[3], g[3], cn[3];
+    unlin(node, X.band_shape, dim, e);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      g[a] = a < dim ? blo[a] + e[a] : 0;
+      cn[a] = a < dim ? g[a] - snlo[a] : 0;
+    }
     cplx w0 = wval(g);
     cplx acc = cscale(w0, op_k2(on, cn));
-    for (int a = 0; a < dim; ++a) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dim) break;
       cplx lo = on.c_lo[a][cn[a]], hi = on.c_hi[a][cn[a]];
       acc = cadd(acc, cmul(make_double2(-(lo.x + hi.x), -(lo.y + hi.y)), w0));
-      if (g[a] - 1 >= X.ext_lo[a]) {
+      if (g[a] - 1 >= elo[a]) {
         int p[3] = {g[0], g[1], g[2]};
         p[a] -= 1;
         acc = cadd(acc, cmul(lo, wval(p)));
       }
-      if (g[a] + 1 < X.ext_lo[a] + X.ext_shape[a]) {
+      if (g[a] + 1 < ehi[a]) {
         int p[3] = {g[0], g[1], g[2]};
         p[a] += 1;
         acc = cadd(acc, cmul(hi, wval(p)));
       }
     }
-    int cs[3] = {0, 0, 0};
-    for (int a = 0; a < dim; ++a) cs[a] = g[a] - ss.win_lo[a];
-    cplx rv = V.rhs[block_offset(fs, cs) * nrhs + r];
+    int cs[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cs[a] = a < dim ? g[a] - swlo[a] : 0;
+    cplx rv = V.rhs[(int64_t)block_off(fs, cs) * nrhs + r];
     cplx pay = cscale(cadd(rv, acc), X.sign);
-    int64_t si = (nodes == 0 ? 0 : (q / nrhs)) * nrhs + r;
+    const int64_t si = (int64_t)node * nrhs + r;
     X.slot[si] = cadd(X.slot[si], pay);
   }
 }
@@ -448,6 +569,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     S.op = P->ops + oi;
     max_w = std::max<int>(max_w, (int)wn);
     P->max_w = max_w;
+    P->max_axis_sum = std::max(P->max_axis_sum, S.win_shape[0] + S.win_shape[1] + S.win_shape[2]);
     P->max_m = std::max(P->max_m, fd.m);
   }
   if (plan_alloc(P, &mem, sizeof(SubDev) * nsub)) return fail(DS_ECUDA);
@@ -747,7 +869,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       const int64_t wmax = P->max_w, smax = P->max_w;
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
       prof_mark(P, 0, st);
-      k_assemble<<<dim3(bx, G), 256, 0, st>>>(P->visits + v0, P->subs, P->slots, f, nrhs, dim,
+      k_assemble<<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
+          P->visits + v0, P->subs, P->slots, f, nrhs, dim,
                                               P->gcounts[0], P->gcounts[1], P->gcounts[2], F);
       ctx->launches++;
       DS_CHECK_LAUNCH();
@@ -769,7 +892,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0) {
         prof_mark(P, 3, st);
-        int bz = std::max(1, std::min(64, cap / nx));
+        int bz = std::max(1, std::min(64, 2 * cap / nx));
         k_transfer<<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, w + 1,
                                                  nrhs, dim, F);
         ctx->launches++;

@@ -3,8 +3,8 @@
 Builds a traced copy of the library, runs one warm config-2 application,
 and prints, per K3 launch (anti-diagonal step), the median cycles of each
 phase seen by thread 0 of cluster rank 0 of the first (visit, chunk):
-  wait   stage top -> exchange mbarrier complete (peers' rows landed)
-  fwait  -> factor tile mbarrier complete
+  fwait  stage top -> factor tile mbarrier complete
+  wait   -> exchange mbarrier complete (peers' rows landed), re-armed
   comp   -> own warp's product done
   sync1  -> all warps done (split-K partials in shared memory)
   epi    -> split-K sum, chain update, exchange rows stored
@@ -45,13 +45,24 @@ torch.cuda.synchronize()
 lib.ds_debug_solve_trace5_reset()
 dp.apply(fd)
 torch.cuda.synchronize()
-buf = (C.c_longlong * (64 * 160 * 8))()
+buf = (C.c_longlong * (64 * 16 * 160 * 12))()
 cnt = C.c_int(0)
 lib.ds_debug_solve_trace5(buf, C.byref(cnt))
-tr = np.frombuffer(buf, dtype=np.int64).reshape(64, 160, 8).astype(np.float64)
-names = ["wait", "fwait", "comp", "sync1", "epi", "sync2", "tail"]
+tr_all = np.frombuffer(buf, dtype=np.int64).reshape(64, 16, 160, 12).astype(np.float64)
+RANK = int(os.environ.get("TRACE_RANK", "0"))
+tr = tr_all[:, RANK]
+# stamp order within a stage (slot numbers of TRACE5 in ds_solve.cu)
+if os.environ.get("DS_K3", "v7") == "v7":  # half-steps: top 0-3, bottom 4-7
+    order = [0, 1, 2, 3, 4, 5, 6, 7]
+    names = ["T.wait", "T.comp", "T.epi", "T.tail", "B.wait", "B.comp", "B.epi"]
+elif tr_all[..., 9].any():  # v5: tile issue (8) and operand issue (9) stamped
+    order = [0, 8, 9, 1, 2, 3, 4, 5, 6, 7]
+    names = ["tile", "aux", "fwait", "wait", "comp", "sync1", "epi", "sync2", "tail"]
+else:  # v6: the producer warp streams tiles; 8 = operands issued
+    order = [0, 8, 1, 2, 3, 4, 5, 6, 7]
+    names = ["aux", "fwait", "wait", "comp", "sync1", "epi", "sync2", "tail"]
 print("launch stages  stage_cyc | " + " ".join(f"{n:>6s}" for n in names))
-tot = np.zeros(8)
+tot = np.zeros(len(names) + 1)
 for L in range(min(cnt.value, 64)):
     t = tr[L]
     n = int(np.argmax(t[:, 0] == 0)) or 160
@@ -59,8 +70,22 @@ for L in range(min(cnt.value, 64)):
         continue
     t = t[1:n - 1]  # skip prologue-affected first and the last stage
     stage = np.median(np.diff(t[:, 0]))
-    ph = [np.median(t[:, i + 1] - t[:, i]) for i in range(7)]
-    tot[:7] += ph
-    tot[7] += 1
+    ph = [np.median(t[:, order[i + 1]] - t[:, order[i]]) for i in range(len(names))]
+    tot[:len(names)] += ph
+    tot[-1] += 1
     print(f"{L:6d} {n:6d} {stage:9.0f} | " + " ".join(f"{v:6.0f}" for v in ph))
-print("mean over launches         | " + " ".join(f"{v / max(1, tot[7]):6.0f}" for v in tot[:7]))
+print("mean over launches         | " + " ".join(f"{v / max(1, tot[-1]):6.0f}" for v in tot[:-1]))
+
+# per-rank view of one launch (the middle one): mean cycles per phase
+L = int(os.environ.get("TRACE_LAUNCH", str(max(0, min(cnt.value, 64) // 2))))
+print(f"\nlaunch {L}: per rank")
+print("rank   stage | " + " ".join(f"{n:>6s}" for n in names))
+for rk in range(16):
+    t = tr_all[L, rk]
+    n = int(np.argmax(t[:, 0] == 0)) or 160
+    if n < 4:
+        continue
+    t = t[1:n - 1]
+    stage = np.median(np.diff(t[:, 0]))
+    ph = [np.median(t[:, order[i + 1]] - t[:, order[i]]) for i in range(len(names))]
+    print(f"{rk:4d} {stage:7.0f} | " + " ".join(f"{v:6.0f}" for v in ph))
