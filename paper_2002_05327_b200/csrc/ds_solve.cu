@@ -1748,7 +1748,7 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
   if (nvisit < 1) return DS_OK;
   {
     const char *v = getenv("DS_K3");
-    const std::string k3 = v ? v : "v7";
+    const std::string k3 = v ? v : "v5";
     if (k3 == "v7") return launch_v7(ctx, visits_dev, nvisit, nrhs, max_m);
     if (k3 == "v6") return launch_v6(ctx, visits_dev, nvisit, nrhs, max_m);
     if (k3 == "v5") return launch_v5(ctx, visits_dev, nvisit, nrhs, max_m);
