@@ -304,4 +304,8 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
     x = X.reshape((R,) + shape) if batched else X.reshape(shape)
     if not is_torch:
         x = x.cpu().numpy()
+    elif not bt.is_cuda:  # results return where the input lives (pinned in -> pinned out)
+        x = x.to("cpu", non_blocking=False)
+        if bt.is_pinned():
+            x = x.pin_memory()
     return (x, reports) if batched else (x, reports[0])
