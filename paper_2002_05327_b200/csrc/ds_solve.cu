@@ -1427,6 +1427,278 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   cluster.sync();  // no CTA leaves while multicasts into it may be in flight
 }
 
+// K3 v8: v5's schedule (fused halves, 256 threads, TMA issue spread over
+// warps 0/4 (multicasts) and 2/6 (factor tiles)) with v6's loop-invariant
+// addressing and the row-tile count MT as a template parameter (1 for
+// 16-CTA clusters, 2 for 8-CTA ones), so only the (NT, X2) product variants
+// are inlined: fewer registers, no spills, no per-stage integer division.
+template <int MT>
+__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+    k_block_solve8(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int C = (int)cluster.num_blocks();
+  const SolveVisit V = visits[blockIdx.y];
+  const FactDev f = *V.f;
+  const int m = f.m, nb = f.nb, tw = f.twist;
+  const int chunk0 = blockIdx.z * rc;
+  const int rg = min(rc, nrhs - chunk0);
+  const int t = threadIdx.x;
+  const int hh = t >> 7, tl = t & 127;
+  if (V.nz) {
+    int any = 0;
+    for (int r = 0; r < rg; ++r) any |= V.nz[chunk0 + r];
+    if (!any) return;
+  }
+  const int rows_per = (m + C - 1) / C;
+  const int r0 = rank * rows_per;
+  const int nr = max(0, min(rows_per, m - r0));
+  const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
+  const size_t ldx = nrhs;
+  const uint16_t mask = (uint16_t)((1u << C) - 1);
+  constexpr int NSL = 4;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t *vbar = (uint64_t *)smem_raw;   // [2 parity]
+  uint64_t *fbar = vbar + 2;               // [2 halves][FAC_STAGES]
+  cplx *vec = (cplx *)(smem_raw + 256);    // [2 halves][2 parity][vstride]
+  const int vstride = m * rc + 2;
+  cplx *fac = vec + 4 * vstride;           // [2 halves][FAC_STAGES][fstride]
+  const int fstride = ((rows_max + 7) & ~7) * m + 2;
+  cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][NSL][rows_max*rc]
+  const int rstride = rows_max * rc;
+  auto VEC = [&](int h, int p) { return vec + (h * 2 + p) * vstride; };
+  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  auto XG = [&](int h, int p) { return xg + ((size_t)h * 2 + p) * m * rg; };
+
+  auto block_of = [&](int h, int st, int &kind) -> int {
+    kind = st < F ? 0 : (st == F ? 1 : 2);
+    if (h == 0) {
+      if (st < F) return st >= F - nt ? st - (F - nt) : -1;
+      if (st == F) return tw;
+      int j = st - F - 1;
+      return j < nt ? tw - 1 - j : -1;
+    }
+    if (st < F) return st >= F - nbt ? nb - 1 - (st - (F - nbt)) : -1;
+    if (st == F) return -1;
+    int j = st - F - 1;
+    return j < nbt ? tw + 1 + j : -1;
+  };
+  auto fseq = [&](int h, int st) {
+    if (h == 0) return st - (F - nt);
+    return st < F ? st - (F - nbt) : st - (F - nbt) - 1;
+  };
+  auto deliveries = [&](int st) {
+    if (st < 0 || st >= S) return 0;
+    int kind, n = 0;
+    if (block_of(0, st, kind) >= 0) ++n;
+    if (block_of(1, st, kind) >= 0 && st != F + 1) ++n;
+    if (st == F && nbt > 0) ++n;
+    return n;
+  };
+  const uint32_t vec_bytes = (uint32_t)(m * rg * sizeof(cplx));
+  const uint32_t fac_bytes = (uint32_t)(nr * m * sizeof(cplx));
+  const uint32_t push_bytes = (uint32_t)(nr * rg * sizeof(cplx));
+  auto load_tile = [&](int h, int st) {
+    int kind, k = block_of(h, st, kind);
+    if (k < 0) return;
+    const int q = fseq(h, st), slot = q % FAC_STAGES;
+    uint64_t *bar = &fbar[h * FAC_STAGES + slot];
+    mbar_expect_tx(bar, fac_bytes);
+    if (fac_bytes)
+      bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+  };
+  auto push = [&](int h, int p) {
+    if (push_bytes)
+      bulk_g2s_multicast(VEC(h, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[p], mask);
+  };
+  constexpr int TILE_T[2] = {64, 192};  // factor-tile issuers (warps 2 and 6)
+
+#ifdef DS_SOLVE_TRACE5
+  int tr5 = -1;
+  if (t == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    tr5 = *(volatile int *)&g_tr5_n;
+    if (tr5 >= 64) tr5 = -1;
+  }
+#endif
+  if (t == 0) {
+    mbar_init(&vbar[0], 1);
+    mbar_init(&vbar[1], 1);
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
+    fence_mbar_init();
+  }
+  cluster.sync();
+#ifdef DS_SOLVE_TRACE5
+  if (t == 0 && rank == 0 && blockIdx.y == 0 && blockIdx.z == 0) atomicAdd(&g_tr5_n, 1);
+#endif
+  if (t == 0) {
+    mbar_expect_tx(&vbar[0], deliveries(0) * vec_bytes);
+    if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
+  }
+  for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
+    if (t == TILE_T[0]) load_tile(0, st);
+    if (t == TILE_T[1]) load_tile(1, st);
+  }
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && nbt == 0) break;
+    const int st0 = h == 0 ? F - nt : F - nbt;
+    const int k0 = h == 0 ? 0 : nb - 1;
+    for (int e = t; e < nr * rg; e += SOLVE_THREADS) {
+      int row = e / rg, c = e % rg;
+      XG(h, st0 & 1)[(r0 + row) * rg + c] = V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + c];
+    }
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+  if (t == 0) push(0, (F - nt) & 1);
+  if (t == 128 && nbt > 0) push(1, (F - nbt) & 1);
+
+  // ---- loop invariants: my (up to 2) outputs of my half
+  const int nout = nr * rg;
+  const size_t blk = (size_t)m * ldx;
+  int xoff[2];
+  size_t goff[2];
+  bool has[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int o = tl + u * 128;
+    has[u] = o < nout;
+    const int orow = has[u] ? o / rg : 0, oc = has[u] ? o % rg : 0;
+    xoff[u] = (r0 + orow) * rg + oc;
+    goff[u] = (size_t)(r0 + orow) * ldx + chunk0 + oc;
+  }
+  const int warp = tl >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+  const int nk = (m + 3) >> 2, kb = (warp * nk) >> 2, ke = ((warp + 1) * nk) >> 2;
+  const int NT = (rg + 7) >> 3;
+  cplx *rp = red + ((size_t)hh * NSL + warp) * rstride;
+  const cplx *rq = red + (size_t)hh * NSL * rstride;
+  uint32_t vph = 0;
+
+  for (int s = 0; s < S; ++s) {
+    const int p = s & 1;
+    TRACE5(0);
+    if (s + FAC_STAGES - 1 < S) {
+      if (t == TILE_T[0]) load_tile(0, s + FAC_STAGES - 1);
+      if (t == TILE_T[1]) load_tile(1, s + FAC_STAGES - 1);
+    }
+    TRACE5(8);
+    int kind, k = block_of(hh, s, kind);
+    const bool act = k >= 0;
+    cplx aux[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    cplx coef = make_double2(0.0, 0.0);
+    if (act) {
+      if (kind == 0) {
+        coef = hh == 0 ? f.lcoef[k + 1] : f.ucoef[k - 1];
+        const int kn = hh == 0 ? k + 1 : k - 1;
+        if (hh == 0 || kn > tw) {
+          const cplx *src = V.rhs + (size_t)kn * blk;
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (has[u]) aux[u] = src[goff[u]];
+        }
+      } else if (kind == 2) {
+        coef = hh == 0 ? f.ucoef[k] : f.lcoef[k];
+        const cplx *src = V.x + (size_t)k * blk;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (has[u]) aux[u] = __ldcg(src + goff[u]);
+      }
+    }
+    TRACE5(9);
+    const int q = act ? fseq(hh, s) : 0;
+    if (act) mbar_wait(&fbar[hh * FAC_STAGES + q % FAC_STAGES], (q / FAC_STAGES) & 1);
+    TRACE5(1);
+    mbar_wait(&vbar[p], (vph >> p) & 1);
+    if (t == 0 && s + 2 < S) mbar_expect_tx(&vbar[p], deliveries(s + 2) * vec_bytes);
+    vph ^= 1u << p;
+    TRACE5(2);
+    if (act) {
+      const cplx *A = fac + (hh * FAC_STAGES + q % FAC_STAGES) * fstride;
+      const cplx *X = VEC((hh == 1 && s == F + 1) ? 0 : hh, p);
+      const cplx *X2 = (kind == 1 && nbt > 0) ? VEC(1, p) : nullptr;
+      double cr[2][2][2] = {}, ci[2][2][2] = {};
+#ifdef K3_NO_COMPUTE
+      if (false)
+#endif
+      {
+        const int sel = (NT > 1 ? 2 : 0) + (X2 ? 1 : 0);
+#define K3_PRODUCT(nt_, x2_) mma_product<MT, nt_, x2_>(A, m, X, X2, rg, m, kb, ke, g, tg, cr, ci)
+        switch (sel) {
+          case 0: K3_PRODUCT(1, false); break;
+          case 1: K3_PRODUCT(1, true); break;
+          case 2: K3_PRODUCT(2, false); break;
+          default: K3_PRODUCT(2, true); break;
+        }
+#undef K3_PRODUCT
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int ntt = 0; ntt < 2; ++ntt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = mt * 8 + g, col = ntt * 8 + 2 * tg + e;
+            if (ntt < NT && row < nr && col < rg)
+              rp[row * rg + col] = make_double2(cr[mt][ntt][e], ci[mt][ntt][e]);
+          }
+    }
+    TRACE5(3);
+    __syncthreads();
+    TRACE5(4);
+    const bool last = s + 1 >= S;
+    cplx outv[2];
+    if (act) {
+      cplx *xgo = XG(hh, p ^ 1);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!has[u]) continue;
+        const int o = tl + u * 128;
+        const cplx r1 = rq[o + rstride], r2 = rq[o + 2 * rstride], r3 = rq[o + 3 * rstride];
+        const cplx acc = cadd(cadd(cadd(rq[o], r1), r2), r3);
+        cplx out, nxt;
+        if (kind == 0) {
+          out = acc;
+          nxt = csub(aux[u], cmul(coef, acc));
+        } else if (kind == 1) {
+          out = acc;
+          nxt = acc;
+        } else {
+          out = csub(aux[u], cmul(coef, acc));
+          nxt = out;
+        }
+        outv[u] = out;
+        if (!last) xgo[xoff[u]] = nxt;
+      }
+    }
+    TRACE5(5);
+    fence_proxy_async_global();
+    __syncthreads();
+    TRACE5(6);
+    if (tl == 0 && !last) {
+      int kd;
+      if (hh == 0 && block_of(0, s, kd) >= 0 && block_of(0, s + 1, kd) >= 0) push(0, p ^ 1);
+      if (hh == 1 && block_of(1, s, kd) >= 0 && (block_of(1, s + 1, kd) >= 0 || s + 1 == F))
+        push(1, p ^ 1);
+    }
+    if (act) {
+      cplx *dst = V.x + (size_t)k * blk;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (has[u]) dst[goff[u]] = outv[u];
+    }
+    TRACE5(7);
+  }
+  cluster.sync();
+}
+
+static size_t solve8_smem(int m, int rc, int C) {
+  int r = (m + C - 1) / C;
+  size_t rows_max = r + (r & 1);
+  size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) + 2 * 4 * rows_max * rc;
+  return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
+}
+
 static size_t solve7_smem(int m, int rc, int C) {
   int r = (m + C - 1) / C;
   size_t rows_max = r + (r & 1);
@@ -1650,6 +1922,45 @@ static int launch_v7(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   return DS_OK;
 }
 
+static int launch_v8(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
+  // both instantiations share one footprint model; MT follows the cluster size
+  const void *fn16 = (const void *)k_block_solve8<1>;
+  int C, rc;
+  long waves;
+  if (!pick_cluster_chunk(fn16, SOLVE_THREADS, nvisit, nrhs, max_m, true,
+                          [&](int r, int c) { return solve8_smem(max_m, r, c); }, &C, &rc, &waves))
+    return ds_fail(DS_ECONFIG, "block solve v8: no feasible cluster configuration");
+  const int rows = solve_rows_max(max_m, C);
+  const void *fn = rows > 8 ? (const void *)k_block_solve8<2> : fn16;
+  const size_t smem = solve8_smem(max_m, rc, C);
+  if (env_int("DS_K3_DEBUG", 0))
+    fprintf(stderr, "K3 v8: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld smem %zu\n", nvisit,
+            nrhs, max_m, C, rc, waves, smem);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  DS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
+  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const SolveVisit *vt = (const SolveVisit *)visits_dev;
+  const int rmax = solve_rows_max(max_m, C);
+  if (rows > 8)
+    DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<2>, vt, nrhs, rc, rmax));
+  else
+    DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<1>, vt, nrhs, rc, rmax));
+  ctx->launches++;
+  return DS_OK;
+}
+
 static int launch_v6(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
   const void *fn = (const void *)k_block_solve6;
   int C, rc;
@@ -1748,7 +2059,8 @@ int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int n
   if (nvisit < 1) return DS_OK;
   {
     const char *v = getenv("DS_K3");
-    const std::string k3 = v ? v : "v5";
+    const std::string k3 = v ? v : "v8";
+    if (k3 == "v8") return launch_v8(ctx, visits_dev, nvisit, nrhs, max_m);
     if (k3 == "v7") return launch_v7(ctx, visits_dev, nvisit, nrhs, max_m);
     if (k3 == "v6") return launch_v6(ctx, visits_dev, nvisit, nrhs, max_m);
     if (k3 == "v5") return launch_v5(ctx, visits_dev, nvisit, nrhs, max_m);
