@@ -547,6 +547,61 @@ def ddm_apply(prob: Problem, ops, cache: Cache, f, directions=None, record=False
     return u, rep
 
 
+def additive_apply(prob: Problem, ops, cache: Cache, f):
+    """additive_ddm_solve restated (ddm.py:294-349) for one RHS: every step
+    solves every subdomain; a target at step s gathers psi of each in-range
+    source idx - c solved at level s - |c|_1 that emits towards it."""
+    t0 = time.perf_counter()
+    dim = prob.dim
+    dirs = source_directions(dim)
+    own = {}
+    for idx in prob.subdomains:  # restrict_source (ddm.py:168-195)
+        olo, ohi = prob.owned(idx)
+        own[idx] = (olo, ohi, np.ascontiguousarray(f[_sl(olo, ohi)], dtype=np.complex128))
+    u = np.zeros(prob.counts, dtype=np.complex128)
+    total = sum(prob.part_counts) - dim + 1
+    rep = {"solves": 0, "nonzero_solves": 0, "discarded_sources": 0, "first_nonzero_step": {}}
+    history = {}
+    for step in range(1, total + 1):
+        current = {}
+        for idx in sorted(prob.subdomains):
+            wlo, whi = prob.window(idx)
+            rhs = np.zeros(tuple(h - l + 1 for l, h in zip(wlo, whi)), dtype=np.complex128)
+            arrivals = []
+            has_own = False
+            if step == 1:
+                olo, ohi, vals = own[idx]
+                has_own = bool(np.any(vals))
+                rhs[_sl(olo, ohi, wlo)] += vals
+            else:
+                for dvec in dirs:
+                    level = step - sum(abs(c) for c in dvec)
+                    src = tuple(i - c for i, c in zip(idx, dvec))
+                    if level < 1 or any(not 1 <= i <= n for i, n in zip(src, prob.part_counts)):
+                        continue
+                    entry = history.get(level, {}).get(src)
+                    if entry is None or not emits(dvec, entry[2]):
+                        continue
+                    res = psi(prob, ops, src, dvec, entry[0], entry[1])
+                    target, (blo, bhi), payload = res
+                    rhs[_sl(blo, bhi, wlo)] += payload
+                    arrivals.append(content_cuts(dvec, entry[2]))
+            rep["solves"] += 1
+            if np.any(rhs):
+                ul = cache.get(ops[idx]).solve(rhs)
+                rep["nonzero_solves"] += 1
+                (slo, shi), beta = prob.beta00_support(idx)
+                u[_sl(slo, shi)] += beta * ul[_sl(slo, shi, wlo)]
+                current[idx] = (ul, rhs, solve_cuts(arrivals, has_own))
+                rep["first_nonzero_step"].setdefault(idx, step)
+            else:
+                current[idx] = None
+        history[step] = current
+        history.pop(step - dim, None)
+    rep["wall_time"] = time.perf_counter() - t0
+    return u, rep
+
+
 def gmres(apply_A, apply_M, b, tol=1e-6, restart=30, max_iter=200):
     """Right-preconditioned restarted GMRES restated (krylov.py:40-147)."""
     shape = b.shape

@@ -14,6 +14,7 @@ from .ddm import (
     build_global_operator,
     build_operators,
     content_cuts,
+    additive_ddm_solve,
     diagonal_sweep_solve,
     emits,
     octant_exactness_check,
@@ -46,7 +47,7 @@ __all__ = [
     "FactorizationCache", "Grid", "LayeredModel", "ModelError", "Partition", "PmlProfile",
     "RasterModel", "SolveReport", "SolverError", "SweepPlan", "Window", "assemble_operator",
     "beta_hat", "build_global_operator", "build_operators", "constant_model", "content_cuts",
-    "diagonal_sweep_solve", "emits", "factorize", "gaussian_source", "gmres", "gmres_batched",
+    "additive_ddm_solve", "diagonal_sweep_solve", "emits", "factorize", "gaussian_source", "gmres", "gmres_batched",
     "layered_model", "make_grid", "make_partition", "next_usable_sweep",
     "octant_exactness_check", "point_shots", "raster_model", "restrict_source", "rule_allows",
     "similar_direction", "solve_cuts", "source_directions", "steps_per_sweep", "sweep_step_of",

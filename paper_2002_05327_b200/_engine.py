@@ -213,9 +213,20 @@ class DevicePlan:
     psi geometry (transfer.py:100-155).
     """
 
-    def __init__(self, partition, operators, cache, directions, nrhs_max: int):
+    def __init__(self, partition, operators, cache, directions, nrhs_max: int,
+                 schedule: str = "diagonal"):
+        """schedule "diagonal": one device sweep per sweep direction, visits
+        grouped by anti-diagonal step (ddm.py:212-291).  schedule "additive":
+        the additive overlapping DDM (ddm.py:294-349) on the same kernels --
+        one device sweep per step, every subdomain visited, and a payload
+        emitted at step s in direction d consumed at step s + |d|_1 (dropped
+        silently past the last step, as the reference never reads it)."""
         from .partition import steps_per_sweep, sweep_step_of
         from .transfer import next_usable_sweep, transfer_geometry
+
+        if schedule not in ("diagonal", "additive"):
+            raise ConfigurationError(f"unknown DDM schedule {schedule!r}")
+        self.schedule = schedule
 
         lib, ctx = context()
         dim = partition.dim
@@ -227,8 +238,9 @@ class DevicePlan:
         self.partition = partition
         self.dim = dim
         self.nsub = nsub
-        self.nsweeps = len(directions)
-        self.directions = tuple(directions)
+        total_steps = sum(partition.counts) - dim + 1
+        self.nsweeps = len(directions) if schedule == "diagonal" else total_steps
+        self.directions = tuple(directions) if schedule == "diagonal" else ()
         self.nrhs_max = nrhs_max
         self.nnodes = partition.grid.node_count()
         self._keep = [ops, facts]
@@ -251,8 +263,15 @@ class DevicePlan:
                     off += ramps[a].size
         dirs = source_directions(dim)
         ndir = len(dirs)
-        nsteps = steps_per_sweep(partition.counts)
         visit_sub, step_off = [], []
+        if schedule == "additive":
+            nsteps = 1
+            order = [lin[i] for i in sorted(subs)]
+            for _ in range(self.nsweeps):
+                visit_sub += order
+                step_off += [0, len(order)]
+        else:
+            nsteps = steps_per_sweep(partition.counts)
         for sd in self.directions:
             groups: dict = {}
             for idx in subs:
@@ -289,6 +308,10 @@ class DevicePlan:
             for s in range(nsub):
                 for k, dvec in enumerate(dirs):
                     if geoms[(s, k)] is None:
+                        continue
+                    if schedule == "additive":
+                        use = w + 1 + sum(abs(c) for c in dvec)
+                        xfer_use[w, s, k] = use if use <= self.nsweeps else -1
                         continue
                     use = next_usable_sweep(dvec, w + 1, self.directions)
                     xfer_use[w, s, k] = 0 if use is None else use

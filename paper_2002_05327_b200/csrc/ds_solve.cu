@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "ds_common.cuh"
+#include "ds_mma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -425,103 +426,10 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 // the bottom block, one mbarrier per stage parity collects both halves'
 // rows (expected bytes = halves delivering to that stage), and both halves'
 // rows are multicast back-to-back.
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
 // factor-tile row pitch: lda % 8 == 4 puts consecutive rows in opposite
 // halves of the 128-byte bank window, so the 8-row DMMA A fragments (and the
 // 2-row DFMA micro-tiles) load without bank conflicts for any m
 __host__ __device__ __forceinline__ int solve_lda(int m) { return m + (12 - m % 8) % 8; }
-
-// One warp's share of y = A x for an (8*MT)-row, (8*NT)-RHS tile over
-// k-steps [kb, ke) of 4 columns: complex product as four real m8n8k4 DMMAs
-// (re*re - im*im, re*im + im*re).  Fragments of step kq+1 are loaded into
-// registers before the DMMAs of step kq issue, hiding shared-memory latency.
-// X2 (the middle block's second input) is added while loading.
-template <int MT, int NT, bool HX2>
-__device__ __forceinline__ void mma_product(const cplx *__restrict__ A, int lda,
-                                            const cplx *__restrict__ X, const cplx *__restrict__ X2,
-                                            int rg, int m, int kb, int ke, int g, int tg,
-                                            double (&cr)[2][2][2], double (&ci)[2][2][2]) {
-  if (kb >= ke) return;
-  cplx a[MT], b[NT], an[MT], bn[NT];
-  auto load = [&](int kq, cplx(&aa)[MT], cplx(&bb)[NT]) {
-    const int kk = kq * 4 + tg;
-    const bool kin = kk < m;
-    const int kc = kin ? kk : 0;  // clamped address, value zeroed below
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      cplx v = X[kc * rg + nt * 8 + g];
-      if (HX2) v = cadd(v, X2[kc * rg + nt * 8 + g]);
-      bb[nt] = kin ? v : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      cplx v = A[(mt * 8 + g) * lda + kc];
-      aa[mt] = kin ? v : make_double2(0.0, 0.0);
-    }
-  };
-  load(kb, a, b);
-#ifndef K3_4M
-  // 3M complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);
-  // Re = P1 - P2, Im = P3 - P1 - P2 (3 DMMAs per tile and k-step instead
-  // of 4; normwise error of the same order)
-  double p1[MT][NT][2] = {}, p2[MT][NT][2] = {}, p3[MT][NT][2] = {};
-  for (int kq = kb; kq < ke; ++kq) {
-    if (kq + 1 < ke) load(kq + 1, an, bn);
-    double bs[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bs[nt] = b[nt].x + b[nt].y;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const double as = a[mt].x + a[mt].y;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        dmma(p1[mt][nt], a[mt].x, b[nt].x);
-        dmma(p2[mt][nt], a[mt].y, b[nt].y);
-        dmma(p3[mt][nt], as, bs[nt]);
-      }
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
-  }
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        cr[mt][nt][e] = p1[mt][nt][e] - p2[mt][nt][e];
-        ci[mt][nt][e] = p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e];
-      }
-#else
-  for (int kq = kb; kq < ke; ++kq) {
-    if (kq + 1 < ke) load(kq + 1, an, bn);
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        dmma(cr[mt][nt], a[mt].x, b[nt].x);
-        dmma(ci[mt][nt], a[mt].x, b[nt].y);
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        dmma(cr[mt][nt], -a[mt].y, b[nt].y);
-        dmma(ci[mt][nt], a[mt].y, b[nt].x);
-      }
-    }
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) a[mt] = an[mt];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[nt] = bn[nt];
-  }
-#endif
-}
 
 template <bool MMA>
 __global__ void __launch_bounds__(SOLVE_THREADS, 1)

@@ -161,21 +161,23 @@ def _warn_collar(f, partition: Partition):
         warnings.warn("source support leaks into the global PML collar")
 
 
-def _plan_key(partition, operators, directions):
-    return (partition, tuple(id(operators[i]) for i in partition.subdomains()), directions)
+def _plan_key(partition, operators, directions, schedule="diagonal"):
+    return (partition, tuple(id(operators[i]) for i in partition.subdomains()), directions,
+            schedule)
 
 
 def device_plan(partition, operators, cache: FactorizationCache, plan: SweepPlan | None,
-                nrhs: int):
-    """The cached native sweep plan for (partition, operators, sweep order)."""
+                nrhs: int, schedule: str = "diagonal"):
+    """The cached native plan for (partition, operators, sweep order, schedule)."""
     from . import _engine
 
     plan = plan or SweepPlan.default(partition.dim)
-    key = _plan_key(partition, operators, plan.directions)
+    directions = plan.directions if schedule == "diagonal" else ()
+    key = _plan_key(partition, operators, directions, schedule)
     dp = cache._plans.get(key)
     if dp is None or dp.nrhs_max < nrhs:
         nmax = max(nrhs, dp.nrhs_max if dp else 0)
-        dp = _engine.DevicePlan(partition, operators, cache, plan.directions, nmax)
+        dp = _engine.DevicePlan(partition, operators, cache, directions, nmax, schedule)
         cache._plans[key] = dp
     return dp
 
@@ -224,6 +226,55 @@ def diagonal_sweep_solve(f, partition: Partition, operators: dict,
     values = _engine.from_device_batch(u, kind, batched)
     field_out = ComplexField(partition.grid, values)
     return field_out, (reports if batched else reports[0])
+
+
+def additive_ddm_solve(f, partition: Partition, operators: dict,
+                       cache: FactorizationCache | None = None, *, warn_collar: bool = True):
+    """The additive overlapping DDM baseline (all subdomains at every step),
+    `additive_ddm_solve` (ddm.py:294-349), batched over RHS, on the same
+    kernels as the diagonal sweep (one device "sweep" per step; see
+    `_engine.DevicePlan`).  Returns (ComplexField, DdmReport or [DdmReport])."""
+    from . import _engine
+
+    t0 = time.perf_counter()
+    counts = partition.grid.counts
+    shape = tuple(f.shape)
+    if shape != counts and shape[1:] != counts:
+        raise ConfigurationError("source shape does not match the grid")
+    if cache is None:
+        cache = FactorizationCache()
+    if not isinstance(cache, FactorizationCache):
+        raise ConfigurationError("cache must be a paper_2002_05327_b200 FactorizationCache")
+    if warn_collar:
+        _warn_collar(f, partition)
+    fdev, kind, batched = _engine.to_device_batch(f, counts)
+    R = fdev.shape[0]
+    chunk = 256
+    us, reports = [], []
+    for r0 in range(0, R, chunk):
+        fr = fdev[r0:r0 + chunk].reshape(min(chunk, R - r0), -1)
+        dp = device_plan(partition, operators, cache, None, fr.shape[0], schedule="additive")
+        u, _ = dp.apply(fr)
+        us.append(u)
+        ctr = dp.counters(fr.shape[0])
+        for r in range(fr.shape[0]):
+            rep = DdmReport(solves=dp.nsweeps * dp.nsub, nonzero_solves=int(ctr["nonzero"][r]),
+                            discarded_sources=int(ctr["discarded"][r]))
+            vnz = ctr["visit_nonzero"][:, :, r]
+            for s, idx in enumerate(dp.subs):
+                steps = np.nonzero(vnz[:, s])[0]
+                if steps.size:
+                    rep.first_nonzero_step[idx] = int(steps[0]) + 1
+            reports.append(rep)
+    import torch
+
+    u = torch.cat(us, 0).reshape((R,) + counts) if len(us) > 1 else us[0].reshape((R,) + counts)
+    torch.cuda.current_stream().synchronize()
+    wall = time.perf_counter() - t0
+    for rep in reports:
+        rep.wall_time = wall
+    values = _engine.from_device_batch(u, kind, batched)
+    return ComplexField(partition.grid, values), (reports if batched else reports[0])
 
 
 def _reports(dp, nrhs: int, plan: SweepPlan, partition: Partition, record_events: bool,

@@ -263,6 +263,36 @@ def test_gpu_vs_reference_golden_compact_and_random(cuda):
     assert reps[0].events == json.loads(str(g["events"]))
 
 
+def test_gpu_additive_vs_reference_golden(cuda):
+    """additive_ddm_solve (ddm.py:294-349) on the same kernels: vs the
+    reference's own outputs (tests/golden/make_golden_additive.py), counters,
+    first_nonzero_step, and the reference's additive-vs-diagonal check
+    (pkg/tests/test_ddm.py:132-141)."""
+    from paper_2002_05327_b200 import additive_ddm_solve
+
+    grid, part, ops, f, prob = _compact_problem()
+    g = np.load(GOLD / "ddm_additive.npz")
+    assert np.array_equal(f, g["source"])
+    rng = np.random.default_rng(7)
+    fr = rng.normal(size=grid.counts) + 1j * rng.normal(size=grid.counts)
+    cache = FactorizationCache()
+    u, reps = additive_ddm_solve(np.stack([f, fr]), part, ops, cache, warn_collar=False)
+    assert rel(u.values[0], g["u"]) <= TOL
+    assert rel(u.values[1], g["u_random"]) <= TOL
+    assert [reps[0].solves, reps[0].nonzero_solves, reps[0].discarded_sources] == list(g["counters"])
+    assert [reps[1].solves, reps[1].nonzero_solves, reps[1].discarded_sources] == \
+        list(g["counters_random"])
+    fns = {" ".join(map(str, k)): v for k, v in reps[0].first_nonzero_step.items()}
+    assert fns == json.loads(str(g["first_nonzero_step"]))
+    assert reps[0].first_nonzero_step[(2, 2)] == 1 and reps[0].first_nonzero_step[(1, 1)] == 3
+    ud, _ = diagonal_sweep_solve(f, part, ops, cache, warn_collar=False)
+    assert rel(u.values[0], ud.values) < 1e-12
+    # single RHS in -> single report out, NumPy in -> NumPy out
+    u1, rep1 = additive_ddm_solve(f, part, ops, cache, warn_collar=False)
+    assert isinstance(u1.values, np.ndarray) and rep1.solves == reps[0].solves
+    assert rel(u1.values, g["u"]) <= TOL
+
+
 def test_gpu_vs_reference_golden_raster_gmres(cuda, raster):
     s, b, prob, oops = raster
     g = np.load(GOLD / "raster_mini.npz")

@@ -127,6 +127,28 @@ def test_oracle_compact_and_random_sources():
     assert rel(ur, g["u_random"]) <= 1e-12
 
 
+def test_oracle_additive_against_reference():
+    """additive_ddm_solve (ddm.py:294-349): oracle vs the reference's own
+    outputs (tests/golden/make_golden_additive.py)."""
+    g = np.load(GOLD / "ddm_additive.npz")
+    prob = _compact_prob(float(g["sigma_max"]))
+    ops = prob.operators()
+    cache = O.Cache()
+    u, rep = O.additive_apply(prob, ops, cache, g["source"])
+    assert rel(u, g["u"]) <= 1e-12
+    assert rel(u, g["u_diag"]) <= 1e-12  # the reference's own cross-check (test_ddm.py:132-141)
+    assert [rep["solves"], rep["nonzero_solves"], rep["discarded_sources"]] == list(g["counters"])
+    fns = {" ".join(map(str, k)): v for k, v in rep["first_nonzero_step"].items()}
+    assert fns == json.loads(str(g["first_nonzero_step"]))
+    rng = np.random.default_rng(7)
+    fr = rng.normal(size=prob.counts) + 1j * rng.normal(size=prob.counts)
+    assert sha(fr) == str(g["random_sha"])
+    ur, rep_r = O.additive_apply(prob, ops, cache, fr)
+    assert rel(ur, g["u_random"]) <= 1e-12
+    assert [rep_r["solves"], rep_r["nonzero_solves"], rep_r["discarded_sources"]] == \
+        list(g["counters_random"])
+
+
 def mini_raster():
     return configs.Spec("mini-raster", ((0.0, 2.4), (0.0, 0.8)), (240, 80), 10, 10, (4, 2),
                         None, 3, "gmres", "raster", 3, c_range=(1.5, 3.0), noise=0.15,
