@@ -1243,6 +1243,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
       TRACE5(h ? 4 : 0);
       int kind, k = block_of(h, s, kind);
       const bool act = k >= 0;
+      // next factor tile of this half, a stage ahead, issued before this
+      // half-step's waits so the TMA unit has finished it before the
+      // half-step's multicast is issued (a multicast queued behind an HBM
+      // load would carry the load's latency into the exchange)
+      if (t == 64 + 128 * h && act) load_tile(h, fseq(h, s) + FAC_STAGES - 1);
       cplx aux = make_double2(0.0, 0.0), coef = make_double2(0.0, 0.0);
       if (act && has) {
         if (kind == 0) {
@@ -1327,7 +1332,6 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
             push(1, 1, p ^ 1);
           }
         }
-        if (act) load_tile(h, q + FAC_STAGES - 1);
       }
       if (act && has) V.x[(size_t)k * blk + goff] = out;
     }
