@@ -225,12 +225,22 @@ __device__ __forceinline__ int solve_cut(const Flags &F, int sweep, int sub, int
 
 #define SLOT_SMEM 32
 
+// Thread mapping of K4/K5/K6: a thread owns RV RHS columns of one node --
+// lane l of the node's LPN = nrhs / RV lanes takes columns l, l + LPN, ... --
+// so the node's geometry (block coordinates, slot masks, stencil neighbours,
+// beta) is computed once per RV values while every load instruction of the
+// node's lanes still covers LPN consecutive 16-byte values (K4, K5); the
+// store-dominated K6 instead gives each lane RV consecutive columns.  ncu on the 8-visit step of config 2
+// showed the one-RHS-per-thread version instruction-bound (~140 instructions
+// per value, IPC 0.6).
+
 // ------------------------------------------------------------- K6 assemble
 // rhs (block layout [nb][m][R]) = own restricted source (sweep 1) + the
 // visit's queued payload slots in slot order; slots are zeroed as consumed.
 // Slot membership is separable (boxes), so each block first builds, per
 // window axis and coordinate, the bitmask of slots (bit 31: the own box)
 // covering it; a node's slot set is then the AND of its axis masks.
+template <int RV>
 __global__ void __launch_bounds__(256)
     k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
                const SlotRef *__restrict__ slots, const cplx *__restrict__ f, int nrhs, int dim,
@@ -262,7 +272,8 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   const int gc[3] = {g0, g1, g2};
-  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  const int lpn = nrhs / RV;
+  const int npb = blockDim.x / lpn, rl = (t % lpn) * RV, ln = t / lpn;  // consecutive columns (stores)
   const int nodes = fd.nb * fd.m;
   int wlo[3], olo[3], osh[3];
 #pragma unroll
@@ -271,22 +282,33 @@ __global__ void __launch_bounds__(256)
     olo[a] = sd.own_lo[a];
     osh[a] = sd.own_shape[a];
   }
-  bool any = false, anyown = false;
+  bool any[RV] = {}, anyown[RV] = {};
   if (ln < npb) {
     for (int blk = blockIdx.x * npb + ln; blk < nodes; blk += gridDim.x * npb) {
       int c[3], g[3];
       block_coords(fd, blk, c);
 #pragma unroll
       for (int a = 0; a < 3; ++a) g[a] = wlo[a] + c[a];
-      cplx val = make_double2(0.0, 0.0);
+      cplx val[RV];
+#pragma unroll
+      for (int j = 0; j < RV; ++j) val[j] = make_double2(0.0, 0.0);
+      uint32_t mk;
       if (masks) {
-        uint32_t mk = s_mask[c[0]] & s_mask[E0 + c[1]];
+        mk = s_mask[c[0]] & s_mask[E0 + c[1]];
         if (dim == 3) mk &= s_mask[E0 + E1 + c[2]];
-        if (mk >> 31) {
-          cplx sv = f[lin_of64(g, gc, dim) * nrhs + r];
-          val = cadd(val, sv);
-          anyown |= cnonzero(sv);
+      } else {
+        mk = (own && in_box(g, olo, osh, dim)) ? 1u << 31 : 0u;
+      }
+      if (mk >> 31) {
+        const cplx *src = f + lin_of64(g, gc, dim) * nrhs + rl;
+#pragma unroll
+        for (int j = 0; j < RV; ++j) {
+          const cplx sv = src[j];
+          val[j] = cadd(val[j], sv);
+          anyown[j] |= cnonzero(sv);
         }
+      }
+      if (masks) {
         mk &= 0x7fffffffu;
         while (mk) {
           const int k = __ffs(mk) - 1;
@@ -295,33 +317,41 @@ __global__ void __launch_bounds__(256)
           int e[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
-          const int64_t idx = (int64_t)lin_of(e, S.shape, dim) * nrhs + r;
-          val = cadd(val, S.data[idx]);
-          S.data[idx] = make_double2(0.0, 0.0);
+          cplx *sp = S.data + (int64_t)lin_of(e, S.shape, dim) * nrhs + rl;
+#pragma unroll
+          for (int j = 0; j < RV; ++j) {
+            val[j] = cadd(val[j], sp[j]);
+            sp[j] = make_double2(0.0, 0.0);
+          }
         }
       } else {
-        if (own && in_box(g, olo, osh, dim)) {
-          cplx sv = f[lin_of64(g, gc, dim) * nrhs + r];
-          val = cadd(val, sv);
-          anyown |= cnonzero(sv);
-        }
         for (int k = 0; k < ns; ++k) {
           const SlotRef &S = k < SLOT_SMEM ? s_slot[k] : slots[V.slot0 + k];
           if (!in_box(g, S.lo, S.shape, dim)) continue;
           int e[3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) e[a] = g[a] - S.lo[a];
-          const int64_t idx = (int64_t)lin_of(e, S.shape, dim) * nrhs + r;
-          val = cadd(val, S.data[idx]);
-          S.data[idx] = make_double2(0.0, 0.0);
+          cplx *sp = S.data + (int64_t)lin_of(e, S.shape, dim) * nrhs + rl;
+#pragma unroll
+          for (int j = 0; j < RV; ++j) {
+            val[j] = cadd(val[j], sp[j]);
+            sp[j] = make_double2(0.0, 0.0);
+          }
         }
       }
-      V.rhs[(int64_t)blk * nrhs + r] = val;
-      any |= cnonzero(val);
+      cplx *dst = V.rhs + (int64_t)blk * nrhs + rl;
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        dst[j] = val[j];
+        any[j] |= cnonzero(val[j]);
+      }
     }
   }
-  if (any) s_nz[r] = 1;
-  if (anyown) s_own[r] = 1;
+#pragma unroll
+  for (int j = 0; j < RV; ++j) {
+    if (any[j]) s_nz[rl + j] = 1;
+    if (anyown[j]) s_own[rl + j] = 1;
+  }
   __syncthreads();
   for (int q = t; q < nrhs; q += blockDim.x) {
     if (s_nz[q]) atomicOr(&V.nz[q], 1);
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(256)
 // u += beta00 * x over the visit's support; where supports of same-step
 // visits overlap the first visit owning the node sums all of them in visit
 // order (deterministic, no atomics on field values).
+template <int RV>
 __global__ void __launch_bounds__(256)
     k_accumulate(const VisitDev *__restrict__ visits, int G, const SubDev *__restrict__ subs,
                  cplx *u, int nrhs, int dim, int g0, int g1, int g2) {
@@ -340,7 +371,8 @@ __global__ void __launch_bounds__(256)
   const SubDev &sd = subs[visits[v].sub];
   const int gc[3] = {g0, g1, g2};
   const int t = threadIdx.x;
-  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  const int lpn = nrhs / RV;
+  const int npb = blockDim.x / lpn, rl = t % lpn, ln = t / lpn;
   if (ln >= npb) return;
   const int nodes = sd.sup_shape[0] * sd.sup_shape[1] * (dim == 3 ? sd.sup_shape[2] : 1);
   for (int node = blockIdx.x * npb + ln; node < nodes; node += gridDim.x * npb) {
@@ -354,14 +386,15 @@ __global__ void __launch_bounds__(256)
       if (in_box(g, so.sup_lo, so.sup_shape, dim)) owner = false;
     }
     if (!owner) continue;
-    const int64_t gi = lin_of64(g, gc, dim) * nrhs + r;
-    cplx acc = u[gi];
+    cplx *up = u + lin_of64(g, gc, dim) * nrhs + rl;
+    cplx acc[RV];
+#pragma unroll
+    for (int j = 0; j < RV; ++j) acc[j] = up[j * lpn];
     bool touched = false;
     for (int w = v; w < G; ++w) {
       const VisitDev &W = visits[w];
       const SubDev &sw = subs[W.sub];
       if (w != v && !in_box(g, sw.sup_lo, sw.sup_shape, dim)) continue;
-      if (!W.nz[r]) continue;
       double beta = 1.0;
       int c[3];
 #pragma unroll
@@ -369,11 +402,18 @@ __global__ void __launch_bounds__(256)
         if (a < dim) beta = beta * sw.beta[a][g[a] - sw.sup_lo[a]];
         c[a] = a < dim ? g[a] - sw.win_lo[a] : 0;
       }
-      cplx xv = W.x[(int64_t)block_off(*sw.f, c) * nrhs + r];
-      acc = cadd(acc, cscale(xv, beta));
-      touched = true;
+      const cplx *xp = W.x + (int64_t)block_off(*sw.f, c) * nrhs + rl;
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        if (!W.nz[rl + j * lpn]) continue;
+        acc[j] = cadd(acc[j], cscale(xp[j * lpn], beta));
+        touched = true;
+      }
     }
-    if (touched) u[gi] = acc;
+    if (touched) {
+#pragma unroll
+      for (int j = 0; j < RV; ++j) up[j * lpn] = acc[j];
+    }
   }
 }
 
@@ -390,7 +430,9 @@ __device__ __forceinline__ double op_k2(const OpDev &o, const int (&c)[3]) {
 
 // psi (transfer.py:100-155): payload = s * (rhs|band + L_nb((w - 1) v)|band),
 // w = prod_a fac_a on ext; block 0 also does the arrival/emission bookkeeping
-// (ddm.py:262-279), one thread per RHS.
+// (ddm.py:262-279), one thread per RHS.  RHS columns that do not emit
+// (zero visit, or cut towards this direction) contribute nothing.
+template <int RV>
 __global__ void __launch_bounds__(256)
     k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
                const SubDev *__restrict__ subs, int nsub, int sweep, int nrhs, int dim, Flags F) {
@@ -413,10 +455,17 @@ __global__ void __launch_bounds__(256)
   }
   if (X.use == 0) return;
   const int t = threadIdx.x;
-  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  const int lpn = nrhs / RV;
+  const int npb = blockDim.x / lpn, rl = t % lpn, ln = t / lpn;
   if (ln >= npb) return;
-  if (!V.nz[r]) return;
-  if (solve_cut(F, sweep, X.src, nsub, r, nrhs) & X.dirmask) return;
+  bool emit[RV];
+  bool anyemit = false;
+#pragma unroll
+  for (int j = 0; j < RV; ++j) {
+    emit[j] = V.nz[rl + j * lpn] && !(solve_cut(F, sweep, X.src, nsub, rl + j * lpn, nrhs) & X.dirmask);
+    anyemit |= emit[j];
+  }
+  if (!anyemit) return;
   const SubDev &ss = subs[X.src];
   const SubDev &sn = subs[X.dst];
   const FactDev fs = *ss.f;
@@ -431,8 +480,8 @@ __global__ void __launch_bounds__(256)
     snlo[a] = sn.win_lo[a];
   }
   const int nodes = X.band_shape[0] * X.band_shape[1] * (dim == 3 ? X.band_shape[2] : 1);
-  // (w(p) - 1) v(p) with w = prod_a fac_a(p_a) on ext
-  auto wval = [&](const int (&p)[3]) -> cplx {
+  // acc[j] += coef * (w(p) - 1) v_j(p), w = prod_a fac_a(p_a) on ext
+  auto add_w = [&](cplx(&acc)[RV], cplx coef, const int (&p)[3]) {
     double wt = 1.0;
     int c[3];
 #pragma unroll
@@ -440,8 +489,9 @@ __global__ void __launch_bounds__(256)
       if (a < dim) wt = wt * X.fac[a][p[a] - elo[a]];
       c[a] = a < dim ? p[a] - swlo[a] : 0;
     }
-    cplx v = V.x[(int64_t)block_off(fs, c) * nrhs + r];
-    return cscale(v, wt - 1.0);
+    const cplx *vp = V.x + (int64_t)block_off(fs, c) * nrhs + rl;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(coef, cscale(vp[j * lpn], wt - 1.0)));
   };
   for (int node = blockIdx.x * npb + ln; node < nodes; node += gridDim.x * npb) {
     int e[3], g[3], cn[3];
@@ -451,31 +501,50 @@ __global__ void __launch_bounds__(256)
       g[a] = a < dim ? blo[a] + e[a] : 0;
       cn[a] = a < dim ? g[a] - snlo[a] : 0;
     }
-    cplx w0 = wval(g);
-    cplx acc = cscale(w0, op_k2(on, cn));
+    // the centre term: (k2 - sum_a (lo_a + hi_a)) * w0, accumulated in the
+    // same order as the one-RHS kernel: k2*w0, then per axis -(lo+hi)*w0,
+    // lo*w(p-e_a), hi*w(p+e_a)
+    double wt0 = 1.0;
+    int c0[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a < dim) wt0 = wt0 * X.fac[a][g[a] - elo[a]];
+      c0[a] = a < dim ? g[a] - swlo[a] : 0;
+    }
+    const cplx *v0 = V.x + (int64_t)block_off(fs, c0) * nrhs + rl;
+    cplx w0[RV], acc[RV];
+    const double k2 = op_k2(on, cn);
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      w0[j] = cscale(v0[j * lpn], wt0 - 1.0);
+      acc[j] = cscale(w0[j], k2);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (a >= dim) break;
-      cplx lo = on.c_lo[a][cn[a]], hi = on.c_hi[a][cn[a]];
-      acc = cadd(acc, cmul(make_double2(-(lo.x + hi.x), -(lo.y + hi.y)), w0));
+      const cplx lo = on.c_lo[a][cn[a]], hi = on.c_hi[a][cn[a]];
+      const cplx mlh = make_double2(-(lo.x + hi.x), -(lo.y + hi.y));
+#pragma unroll
+      for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(mlh, w0[j]));
       if (g[a] - 1 >= elo[a]) {
         int p[3] = {g[0], g[1], g[2]};
         p[a] -= 1;
-        acc = cadd(acc, cmul(lo, wval(p)));
+        add_w(acc, lo, p);
       }
       if (g[a] + 1 < ehi[a]) {
         int p[3] = {g[0], g[1], g[2]};
         p[a] += 1;
-        acc = cadd(acc, cmul(hi, wval(p)));
+        add_w(acc, hi, p);
       }
     }
     int cs[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) cs[a] = a < dim ? g[a] - swlo[a] : 0;
-    cplx rv = V.rhs[(int64_t)block_off(fs, cs) * nrhs + r];
-    cplx pay = cscale(cadd(rv, acc), X.sign);
-    const int64_t si = (int64_t)node * nrhs + r;
-    X.slot[si] = cadd(X.slot[si], pay);
+    const cplx *rv = V.rhs + (int64_t)block_off(fs, cs) * nrhs + rl;
+    cplx *sp = X.slot + (int64_t)node * nrhs + rl;
+#pragma unroll
+    for (int j = 0; j < RV; ++j)
+      if (emit[j]) sp[j * lpn] = cadd(sp[j * lpn], cscale(cadd(rv[j * lpn], acc[j]), X.sign));
   }
 }
 
@@ -869,9 +938,14 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       const int64_t wmax = P->max_w, smax = P->max_w;
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
       prof_mark(P, 0, st);
-      k_assemble<<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
-          P->visits + v0, P->subs, P->slots, f, nrhs, dim,
-                                              P->gcounts[0], P->gcounts[1], P->gcounts[2], F);
+      if (nrhs % 4 == 0)
+        k_assemble<4><<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
+            P->visits + v0, P->subs, P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
+            P->gcounts[2], F);
+      else
+        k_assemble<1><<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
+            P->visits + v0, P->subs, P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
+            P->gcounts[2], F);
       ctx->launches++;
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
@@ -885,16 +959,24 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CHECK_LAUNCH();
       prof_mark(P, 2, st);
       int by = blocks_for(ctx, smax * nrhs / 4, std::max(1, cap / G));
-      k_accumulate<<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
-                                                P->gcounts[0], P->gcounts[1], P->gcounts[2]);
+      if (nrhs % 4 == 0)
+        k_accumulate<4><<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
+                                                     P->gcounts[0], P->gcounts[1], P->gcounts[2]);
+      else
+        k_accumulate<1><<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
+                                                     P->gcounts[0], P->gcounts[1], P->gcounts[2]);
       ctx->launches++;
       DS_CHECK_LAUNCH();
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0) {
         prof_mark(P, 3, st);
         int bz = std::max(1, std::min(64, 2 * cap / nx));
-        k_transfer<<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, w + 1,
-                                                 nrhs, dim, F);
+        if (nrhs % 4 == 0)
+          k_transfer<4><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
+                                                      w + 1, nrhs, dim, F);
+        else
+          k_transfer<1><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
+                                                      w + 1, nrhs, dim, F);
         ctx->launches++;
         DS_CHECK_LAUNCH();
       }
