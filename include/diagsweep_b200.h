@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 1
+#define DS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -143,6 +143,14 @@ DS_API int ds_fact_destroy(ds_fact *fact);
  * order (ddm.py:75-79).  Geometry per (s, k): band_lo/band_shape/ext_lo/
  * ext_shape [(s*ndir+k)*3], and the (1-beta) factors on ext per axis at
  * xfac + xfac_off[(s*ndir+k)*3+a] (ones on zero axes).
+ * Launch schedule (optional, ABI 2): nlaunch = 0 runs the visits sweep by
+ * sweep, step by step (the reference order).  nlaunch > 0 runs launch l over
+ * the visits launch_visits[2*i] (0-based sweep), launch_visits[2*i+1]
+ * (subdomain) for i in [launch_off[l], launch_off[l+1]); every visit exactly
+ * once, each after the visits it depends on (its step predecessors and the
+ * sources routed to it) and after any earlier writer of the same payload
+ * slot (the host's list scheduler, _engine.launch_schedule).  Per-sweep
+ * partials need nlaunch = 0.
  * Arrays are int32 unless noted. */
 typedef struct {
   int32_t dim, nsub, nsweeps, nsteps, ndir, nrhs_max;
@@ -165,6 +173,9 @@ typedef struct {
   const int32_t *band_lo, *band_shape, *ext_lo, *ext_shape;
   const double *xfac;
   const int64_t *xfac_off;
+  int32_t nlaunch;
+  const int32_t *launch_off;
+  const int32_t *launch_visits;
 } ds_plan_desc;
 
 DS_API int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *desc, ds_plan **out);

@@ -204,6 +204,58 @@ def _pad3(t, fill=0):
     return t + [fill] * (3 - len(t))
 
 
+def launch_schedule(nsweeps: int, nsub: int, order, xfer_use, dirs, sub_index, in_range,
+                    cap: int):
+    """List-schedule the (sweep, subdomain) visits of one application.
+
+    `order` is the sequential visit order (sweep by sweep, step by step); a
+    visit depends on every source visit routed to it (xfer_use; this covers
+    its step predecessors) and on the previous writer of each payload slot
+    it writes (slots accumulate non-atomically, and the fixed writer order
+    keeps the sums deterministic).  Ready visits are taken longest remaining
+    path first, at most `cap` per launch.  Returns a list of launches, each a
+    list of (sweep 0-based, subdomain) in launch order."""
+    pos = {v: i for i, v in enumerate(order)}
+    deps = {v: set() for v in order}
+    last_writer = {}
+    for (w, s) in order:
+        for k, d in enumerate(dirs):
+            use = int(xfer_use[w, s, k])
+            if use < 1:
+                continue
+            t = sub_index(s, d)
+            deps[(use - 1, t)].add((w, s))
+            key = (use - 1, t, k)
+            if key in last_writer:
+                deps[(w, s)].add(last_writer[key])
+            last_writer[key] = (w, s)
+    succ = {v: [] for v in order}
+    for v, ds in deps.items():
+        for x in ds:
+            if pos[x] >= pos[v]:
+                raise ConfigurationError("launch schedule: dependency against the sweep order")
+            succ[x].append(v)
+    prio = {}
+    for v in reversed(order):
+        prio[v] = 1 + max((prio[x] for x in succ[v]), default=0)
+    missing = {v: len(ds) for v, ds in deps.items()}
+    ready = [v for v in order if missing[v] == 0]
+    launches = []
+    while ready:
+        ready.sort(key=lambda v: (-prio[v], pos[v]))
+        pick, ready = ready[:cap], ready[cap:]
+        pick.sort(key=lambda v: pos[v])
+        launches.append(pick)
+        for v in pick:
+            for x in succ[v]:
+                missing[x] -= 1
+                if missing[x] == 0:
+                    ready.append(x)
+    if sum(len(l) for l in launches) != len(order):
+        raise ConfigurationError("launch schedule: dependency cycle")
+    return launches
+
+
 class DevicePlan:
     """Static device tables for one (partition, operators, sweep plan).
 
@@ -214,7 +266,7 @@ class DevicePlan:
     """
 
     def __init__(self, partition, operators, cache, directions, nrhs_max: int,
-                 schedule: str = "diagonal"):
+                 schedule: str = "diagonal", pipelined: bool = False):
         """schedule "diagonal": one device sweep per sweep direction, visits
         grouped by anti-diagonal step (ddm.py:212-291).  schedule "additive":
         the additive overlapping DDM (ddm.py:294-349) on the same kernels --
@@ -316,6 +368,32 @@ class DevicePlan:
                     use = next_usable_sweep(dvec, w + 1, self.directions)
                     xfer_use[w, s, k] = 0 if use is None else use
         self.xfer_use = xfer_use
+        # ---- launch schedule: visits of several sweeps per launch as soon as
+        # their sources are done (the dependency DAG of the sweep is shallower
+        # than sweeps x steps); the cluster solve fits ~7 visits per wave
+        self.launches = None
+        if pipelined and schedule == "diagonal":
+            order = []
+            for w in range(self.nsweeps):
+                b0 = w * (nsteps + 1)
+                for t in range(nsteps):
+                    for i in range(step_off[b0 + t], step_off[b0 + t + 1]):
+                        order.append((w, visit_sub[w * nsub + i]))
+            pc = partition.counts
+
+            def sub_index(sv, d):
+                idx = tuple(i + c for i, c in zip(subs[sv], d))
+                return lin[idx]
+
+            max_m = 0
+            for idx in subs:
+                shp = partition.window(idx).shape
+                ax = int(np.argmax(shp))
+                max_m = max(max_m, int(np.prod([n for a, n in enumerate(shp) if a != ax])))
+            cap_env = os.environ.get("DS_LAUNCH_CAP")
+            cap = int(cap_env) if cap_env else (7 if max_m <= 160 else nsub * self.nsweeps)
+            self.launches = launch_schedule(self.nsweeps, nsub, order, xfer_use, dirs, sub_index,
+                                            None, max(1, cap))
         self.geoms = geoms
         self.subs = subs
         self.dirs = dirs
@@ -351,6 +429,18 @@ class DevicePlan:
         desc.nops = nsub
         desc.ops = C.cast(op_handles, C.c_void_p)
         desc.fact_of_sub = C.cast(fact_handles, C.c_void_p)
+        if self.launches:
+            l_off = np.zeros(len(self.launches) + 1, np.int32)
+            l_vis = []
+            for i, L in enumerate(self.launches):
+                l_off[i + 1] = l_off[i] + len(L)
+                for (w, sv) in L:
+                    l_vis += [w, sv]
+            l_vis = np.asarray(l_vis, np.int32)
+            arrays["launch_off"], arrays["launch_visits"] = l_off, l_vis  # keep alive
+            desc.nlaunch = len(self.launches)
+            desc.launch_off = l_off.ctypes.data
+            desc.launch_visits = l_vis.ctypes.data
         out = C.c_void_p()
         N.check(lib.ds_plan_create(ctx, C.byref(desc), C.byref(out)), "ds_plan_create")
         self.handle = out

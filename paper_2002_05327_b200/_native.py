@@ -60,6 +60,9 @@ class PlanDesc(C.Structure):
         ("band_lo", vp), ("band_shape", vp), ("ext_lo", vp), ("ext_shape", vp),
         ("xfac", vp),
         ("xfac_off", vp),
+        ("nlaunch", i32),
+        ("launch_off", vp),
+        ("launch_visits", vp),
     ]
 
 
@@ -120,7 +123,7 @@ def load_library(path: Path | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ds_abi_version() != 1:
+        if lib.ds_abi_version() != 2:
             raise SolverError("diagsweep_b200 ABI version mismatch")
         if path is None:
             _lib = lib

@@ -99,6 +99,7 @@ struct ds_plan {
   size_t stage_cap = 0;
   StageProgram *program = nullptr;  // stage-per-launch solve (large slabs, or DS_SOLVE_MODE=staged)
   int patched_nrhs = 0;
+  int nlaunch = 0;  // > 0: explicit launch schedule (visits of several sweeps per launch)
   // graph
   bool use_graph = false;
   cudaGraphExec_t graph = nullptr;
@@ -435,9 +436,10 @@ __device__ __forceinline__ double op_k2(const OpDev &o, const int (&c)[3]) {
 template <int RV>
 __global__ void __launch_bounds__(256)
     k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
-               const SubDev *__restrict__ subs, int nsub, int sweep, int nrhs, int dim, Flags F) {
+               const SubDev *__restrict__ subs, int nsub, int nrhs, int dim, Flags F) {
   const XferDev &X = xfers[blockIdx.y];
   const VisitDev &V = visits[X.vidx];
+  const int sweep = V.sweep;  // a launch may hold visits of several sweeps
   if (blockIdx.x == 0) {
     for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
       if (!V.nz[r]) continue;
@@ -648,9 +650,27 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->gmax = 0;
   int max_nb = 0;
   for (int s = 0; s < nsub; ++s) max_nb = std::max(max_nb, hf[s].nb);
-  for (int w = 0; w < nsw; ++w)
-    for (int t = 0; t < nst; ++t)
-      P->gmax = std::max(P->gmax, d->step_off[w * (nst + 1) + t + 1] - d->step_off[w * (nst + 1) + t]);
+  const bool sched = d->nlaunch > 0;
+  if (sched) {
+    if (!d->launch_off || !d->launch_visits)
+      return fail(ds_fail(DS_ECONFIG, "launch schedule without launch_off/launch_visits"));
+    if (d->launch_off[0] != 0 || d->launch_off[d->nlaunch] != nsw * nsub)
+      return fail(ds_fail(DS_ECONFIG, "launch schedule must cover every (sweep, subdomain) once"));
+    std::vector<char> seen((size_t)nsw * nsub, 0);
+    for (int l = 0; l < d->nlaunch; ++l) {
+      P->gmax = std::max(P->gmax, d->launch_off[l + 1] - d->launch_off[l]);
+      for (int i = d->launch_off[l]; i < d->launch_off[l + 1]; ++i) {
+        int w = d->launch_visits[2 * i], s = d->launch_visits[2 * i + 1];
+        if (w < 0 || w >= nsw || s < 0 || s >= nsub || seen[(size_t)w * nsub + s]++)
+          return fail(ds_fail(DS_ECONFIG, "launch schedule: bad or repeated visit"));
+      }
+    }
+  } else {
+    for (int w = 0; w < nsw; ++w)
+      for (int t = 0; t < nst; ++t)
+        P->gmax = std::max(P->gmax, d->step_off[w * (nst + 1) + t + 1] - d->step_off[w * (nst + 1) + t]);
+  }
+  P->nlaunch = d->nlaunch;
   size_t vbuf = (size_t)max_w * d->nrhs_max;
   cplx *bufs;
   if (plan_alloc(P, &mem, sizeof(cplx) * vbuf * 2 * 2 * P->gmax)) return fail(DS_ECUDA);
@@ -740,17 +760,37 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   std::vector<VisitDev> hv;
   std::vector<SolveVisit> hsv;
   std::vector<XferDev> hx;
-  P->vstep_off.assign((size_t)nsw * nst + 1, 0);
-  P->xstep_off.assign((size_t)nsw * nst + 1, 0);
+  const int nq = sched ? d->nlaunch : nsw * nst;
+  P->vstep_off.assign((size_t)nq + 1, 0);
+  P->xstep_off.assign((size_t)nq + 1, 0);
   std::vector<int> visit_of((size_t)nsw * nsub, -1);
+  // visit i of launch q: (sweep, subdomain)
+  auto visit_at = [&](int q, int i, int &w, int &s) {
+    if (sched) {
+      w = d->launch_visits[2 * i];
+      s = d->launch_visits[2 * i + 1];
+    } else {
+      w = q / nst;
+      s = d->visit_sub[(size_t)w * nsub + i];
+    }
+  };
   int step_global = 0;
-  for (int w = 0; w < nsw; ++w) {
-    for (int t = 0; t < nst; ++t, ++step_global) {
-      int b = d->step_off[w * (nst + 1) + t], e = d->step_off[w * (nst + 1) + t + 1];
+  for (int q = 0; q < nq; ++q, ++step_global) {
+    {
+      int b, e;
+      if (sched) {
+        b = d->launch_off[q];
+        e = d->launch_off[q + 1];
+      } else {
+        const int w = q / nst, t = q % nst;
+        b = d->step_off[w * (nst + 1) + t];
+        e = d->step_off[w * (nst + 1) + t + 1];
+      }
       P->vstep_off[step_global] = (int)hv.size();
       int parity = step_global & 1;
       for (int g = b; g < e; ++g) {
-        int s = d->visit_sub[(size_t)w * nsub + g];
+        int w, s;
+        visit_at(q, g, w, s);
         VisitDev V;
         memset(&V, 0, sizeof(V));
         V.sub = s;
@@ -770,7 +810,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
       }
       P->xstep_off[step_global] = (int)hx.size();
       for (int g = b; g < e; ++g) {
-        int s = d->visit_sub[(size_t)w * nsub + g];
+        int w, s;
+        visit_at(q, g, w, s);
         for (int k = 0; k < ndir; ++k) {
           int use = d->xfer_use[((size_t)w * nsub + s) * ndir + k];
           if (use < 0) continue;  // target out of range: psi returns None
@@ -930,9 +971,11 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
   DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
   const int cap = std::max(1, ctx->num_sms * 4);
-  for (int w = 0; w < P->nsweeps; ++w) {
-    for (int t = 0; t < P->nsteps; ++t) {
-      int q = w * P->nsteps + t;
+  if (partials && P->nlaunch > 0)
+    return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
+  const int nq = (int)P->vstep_off.size() - 1;
+  for (int q = 0; q < nq; ++q) {
+    {
       int v0 = P->vstep_off[q], G = P->vstep_off[q + 1] - v0;
       if (G == 0) continue;
       const int64_t wmax = P->max_w, smax = P->max_w;
@@ -973,16 +1016,16 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         int bz = std::max(1, std::min(64, 2 * cap / nx));
         if (nrhs % 4 == 0)
           k_transfer<4><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      w + 1, nrhs, dim, F);
+                                                      nrhs, dim, F);
         else
           k_transfer<1><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      w + 1, nrhs, dim, F);
+                                                      nrhs, dim, F);
         ctx->launches++;
         DS_CHECK_LAUNCH();
       }
     }
-    if (partials)
-      DS_CUDA(cudaMemcpyAsync(partials + (size_t)w * P->nnodes * nrhs, u,
+    if (partials && (q + 1) % P->nsteps == 0)
+      DS_CUDA(cudaMemcpyAsync(partials + (size_t)(q / P->nsteps) * P->nnodes * nrhs, u,
                               sizeof(cplx) * P->nnodes * nrhs, cudaMemcpyDeviceToDevice, st));
   }
   prof_mark(P, -1, st);

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import itertools
 import json
+import os
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -161,23 +162,32 @@ def _warn_collar(f, partition: Partition):
         warnings.warn("source support leaks into the global PML collar")
 
 
-def _plan_key(partition, operators, directions, schedule="diagonal"):
+def _plan_key(partition, operators, directions, schedule="diagonal", pipelined=False):
     return (partition, tuple(id(operators[i]) for i in partition.subdomains()), directions,
-            schedule)
+            schedule, pipelined)
 
 
 def device_plan(partition, operators, cache: FactorizationCache, plan: SweepPlan | None,
-                nrhs: int, schedule: str = "diagonal"):
-    """The cached native plan for (partition, operators, sweep order, schedule)."""
+                nrhs: int, schedule: str = "diagonal", pipelined: bool | None = None):
+    """The cached native plan for (partition, operators, sweep order, schedule).
+
+    pipelined (diagonal schedule; default on, DS_PIPELINE=0 turns it off):
+    visits of different sweeps share a launch as soon as their sources are
+    done (`_engine.launch_schedule`); the map is unchanged, sums stay
+    deterministic.  Per-sweep partials need the sweep-ordered plan."""
     from . import _engine
 
     plan = plan or SweepPlan.default(partition.dim)
     directions = plan.directions if schedule == "diagonal" else ()
-    key = _plan_key(partition, operators, directions, schedule)
+    if pipelined is None:
+        pipelined = schedule == "diagonal" and os.environ.get("DS_PIPELINE", "1") != "0"
+    pipelined = bool(pipelined) and schedule == "diagonal"
+    key = _plan_key(partition, operators, directions, schedule, pipelined)
     dp = cache._plans.get(key)
     if dp is None or dp.nrhs_max < nrhs:
         nmax = max(nrhs, dp.nrhs_max if dp else 0)
-        dp = _engine.DevicePlan(partition, operators, cache, directions, nmax, schedule)
+        dp = _engine.DevicePlan(partition, operators, cache, directions, nmax, schedule,
+                                pipelined=pipelined)
         cache._plans[key] = dp
     return dp
 
@@ -207,7 +217,8 @@ def diagonal_sweep_solve(f, partition: Partition, operators: dict,
     us, parts_all, reports = [], [], []
     for r0 in range(0, R, chunk):
         fr = fdev[r0:r0 + chunk].reshape(min(chunk, R - r0), -1)
-        dp = device_plan(partition, operators, cache, plan, fr.shape[0])
+        dp = device_plan(partition, operators, cache, plan, fr.shape[0],
+                         pipelined=None if not collect_partials else False)
         u, parts = dp.apply(fr, collect_partials=collect_partials)
         us.append(u)
         parts_all.append(parts)
