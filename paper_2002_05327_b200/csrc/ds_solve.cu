@@ -1344,8 +1344,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 // addressing and the row-tile count MT as a template parameter (1 for
 // 16-CTA clusters, 2 for 8-CTA ones), so only the (NT, X2) product variants
 // are inlined: fewer registers, no spills, no per-stage integer division.
-template <int MT>
-__global__ void __launch_bounds__(SOLVE_THREADS, 1)
+template <int MT, int NW>
+__global__ void __launch_bounds__(64 * NW, 1)
     k_block_solve8(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -1356,7 +1356,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const int chunk0 = blockIdx.z * rc;
   const int rg = min(rc, nrhs - chunk0);
   const int t = threadIdx.x;
-  const int hh = t >> 7, tl = t & 127;
+  constexpr int HT = 32 * NW, NT_ = 2 * HT;  // threads per half / per CTA
+  const int hh = t / HT, tl = t % HT;
   if (V.nz) {
     int any = 0;
     for (int r = 0; r < rg; ++r) any |= V.nz[chunk0 + r];
@@ -1368,7 +1369,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   const int nt = tw, nbt = nb - 1 - tw, F = max(nt, nbt), S = 2 * F + 1;
   const size_t ldx = nrhs;
   const uint16_t mask = (uint16_t)((1u << C) - 1);
-  constexpr int NSL = 4;
+  constexpr int NSL = NW;  // K-slices = warps per half
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint64_t *vbar = (uint64_t *)smem_raw;   // [2 parity]
@@ -1424,7 +1425,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     if (push_bytes)
       bulk_g2s_multicast(VEC(h, p) + r0 * rg, XG(h, p) + r0 * rg, push_bytes, &vbar[p], mask);
   };
-  constexpr int TILE_T[2] = {64, 192};  // factor-tile issuers (warps 2 and 6)
+  constexpr int TILE_T[2] = {64, HT + 64};  // factor-tile issuers (warp 2 of each half)
 
 #ifdef DS_SOLVE_TRACE5
   int tr5 = -1;
@@ -1455,7 +1456,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     if (h == 1 && nbt == 0) break;
     const int st0 = h == 0 ? F - nt : F - nbt;
     const int k0 = h == 0 ? 0 : nb - 1;
-    for (int e = t; e < nr * rg; e += SOLVE_THREADS) {
+    for (int e = t; e < nr * rg; e += NT_) {
       int row = e / rg, c = e % rg;
       XG(h, st0 & 1)[(r0 + row) * rg + c] = V.rhs[((size_t)k0 * m + r0 + row) * ldx + chunk0 + c];
     }
@@ -1463,24 +1464,25 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   fence_proxy_async_global();
   __syncthreads();
   if (t == 0) push(0, (F - nt) & 1);
-  if (t == 128 && nbt > 0) push(1, (F - nbt) & 1);
+  if (t == HT && nbt > 0) push(1, (F - nbt) & 1);
 
   // ---- loop invariants: my (up to 2) outputs of my half
   const int nout = nr * rg;
   const size_t blk = (size_t)m * ldx;
-  int xoff[2];
-  size_t goff[2];
-  bool has[2];
+  constexpr int NU = NW >= 8 ? 1 : 2;  // outputs per thread (<= 256 per half)
+  int xoff[NU];
+  size_t goff[NU];
+  bool has[NU];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int o = tl + u * 128;
+  for (int u = 0; u < NU; ++u) {
+    const int o = tl + u * HT;
     has[u] = o < nout;
     const int orow = has[u] ? o / rg : 0, oc = has[u] ? o % rg : 0;
     xoff[u] = (r0 + orow) * rg + oc;
     goff[u] = (size_t)(r0 + orow) * ldx + chunk0 + oc;
   }
   const int warp = tl >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
-  const int nk = (m + 3) >> 2, kb = (warp * nk) >> 2, ke = ((warp + 1) * nk) >> 2;
+  const int nk = (m + 3) >> 2, kb = (warp * nk) / NW, ke = ((warp + 1) * nk) / NW;
   const int NT = (rg + 7) >> 3;
   cplx *rp = red + ((size_t)hh * NSL + warp) * rstride;
   const cplx *rq = red + (size_t)hh * NSL * rstride;
@@ -1496,7 +1498,9 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     TRACE5(8);
     int kind, k = block_of(hh, s, kind);
     const bool act = k >= 0;
-    cplx aux[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    cplx aux[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) aux[u] = make_double2(0.0, 0.0);
     cplx coef = make_double2(0.0, 0.0);
     if (act) {
       if (kind == 0) {
@@ -1505,14 +1509,14 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
         if (hh == 0 || kn > tw) {
           const cplx *src = V.rhs + (size_t)kn * blk;
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+          for (int u = 0; u < NU; ++u)
             if (has[u]) aux[u] = src[goff[u]];
         }
       } else if (kind == 2) {
         coef = hh == 0 ? f.ucoef[k] : f.lcoef[k];
         const cplx *src = V.x + (size_t)k * blk;
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < NU; ++u)
           if (has[u]) aux[u] = __ldcg(src + goff[u]);
       }
     }
@@ -1558,15 +1562,16 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     __syncthreads();
     TRACE5(4);
     const bool last = s + 1 >= S;
-    cplx outv[2];
+    cplx outv[NU];
     if (act) {
       cplx *xgo = XG(hh, p ^ 1);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < NU; ++u) {
         if (!has[u]) continue;
-        const int o = tl + u * 128;
-        const cplx r1 = rq[o + rstride], r2 = rq[o + 2 * rstride], r3 = rq[o + 3 * rstride];
-        const cplx acc = cadd(cadd(cadd(rq[o], r1), r2), r3);
+        const int o = tl + u * HT;
+        cplx acc = rq[o];  // K-slices in a fixed order (deterministic)
+#pragma unroll
+        for (int q2 = 1; q2 < NSL; ++q2) acc = cadd(acc, rq[o + q2 * rstride]);
         cplx out, nxt;
         if (kind == 0) {
           out = acc;
@@ -1595,7 +1600,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
     if (act) {
       cplx *dst = V.x + (size_t)k * blk;
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < NU; ++u)
         if (has[u]) dst[goff[u]] = outv[u];
     }
     TRACE5(7);
@@ -1603,11 +1608,11 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
   cluster.sync();
 }
 
-static size_t solve8_smem(int m, int rc, int C) {
+static size_t solve8_smem(int m, int rc, int C, int nw = 4) {
   int r = (m + C - 1) / C;
   size_t rows_max = r + (r & 1);
   size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
-  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) + 2 * 4 * rows_max * rc;
+  size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) + 2 * (size_t)nw * rows_max * rc;
   return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
 }
 
@@ -1835,25 +1840,29 @@ static int launch_v7(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
 }
 
 static int launch_v8(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, int max_m) {
-  // both instantiations share one footprint model; MT follows the cluster size
-  const void *fn16 = (const void *)k_block_solve8<1>;
+  // warps per half: 4 (256 threads) or 8 (512 threads, more latency hiding
+  // for the lockstep DMMA product, 128 registers)
+  static const int nw = env_int("DS_K3_NW", 4) >= 8 ? 8 : 4;
+  const int threads = 64 * nw;
+  const void *fn16 = nw == 8 ? (const void *)k_block_solve8<1, 8> : (const void *)k_block_solve8<1, 4>;
   int C, rc;
   long waves;
-  if (!pick_cluster_chunk(fn16, SOLVE_THREADS, nvisit, nrhs, max_m, true,
-                          [&](int r, int c) { return solve8_smem(max_m, r, c); }, &C, &rc, &waves))
+  if (!pick_cluster_chunk(fn16, threads, nvisit, nrhs, max_m, true,
+                          [&](int r, int c) { return solve8_smem(max_m, r, c, nw); }, &C, &rc, &waves))
     return ds_fail(DS_ECONFIG, "block solve v8: no feasible cluster configuration");
   const int rows = solve_rows_max(max_m, C);
-  const void *fn = rows > 8 ? (const void *)k_block_solve8<2> : fn16;
-  const size_t smem = solve8_smem(max_m, rc, C);
+  const void *fn = rows > 8 ? (nw == 8 ? (const void *)k_block_solve8<2, 8> : (const void *)k_block_solve8<2, 4>)
+                            : fn16;
+  const size_t smem = solve8_smem(max_m, rc, C, nw);
   if (env_int("DS_K3_DEBUG", 0))
-    fprintf(stderr, "K3 v8: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld smem %zu\n", nvisit,
-            nrhs, max_m, C, rc, waves, smem);
+    fprintf(stderr, "K3 v8: nvisit %d nrhs %d m %d -> C %d rc %d waves %ld smem %zu nw %d\n", nvisit,
+            nrhs, max_m, C, rc, waves, smem, nw);
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   DS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
-  cfg.blockDim = dim3(SOLVE_THREADS, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
   cudaLaunchAttribute attr[1];
@@ -1865,10 +1874,17 @@ static int launch_v8(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   cfg.numAttrs = 1;
   const SolveVisit *vt = (const SolveVisit *)visits_dev;
   const int rmax = solve_rows_max(max_m, C);
-  if (rows > 8)
-    DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<2>, vt, nrhs, rc, rmax));
-  else
-    DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<1>, vt, nrhs, rc, rmax));
+  if (nw == 8) {
+    if (rows > 8)
+      DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<2, 8>, vt, nrhs, rc, rmax));
+    else
+      DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<1, 8>, vt, nrhs, rc, rmax));
+  } else {
+    if (rows > 8)
+      DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<2, 4>, vt, nrhs, rc, rmax));
+    else
+      DS_CUDA(cudaLaunchKernelEx(&cfg, k_block_solve8<1, 4>, vt, nrhs, rc, rmax));
+  }
   ctx->launches++;
   return DS_OK;
 }
