@@ -260,17 +260,26 @@ def run_ours(args, rank, world, local_rank):
             def e2e_step():
                 uu, _ = diagonal_sweep_solve(f_pin, part, ops, cache, warn_collar=False)
                 return uu.values
+        # warm-up as the timed loop runs it (the previous result stays alive
+        # while the next is produced), so the host allocator has both pinned
+        # result buffers before timing
+        u_host = None
         for _ in range(max(3, args.warmup)):
-            e2e_step()
+            u_host = e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
+        stamps = []
         for _ in range(args.steps):
             u_host = e2e_step()  # pinned host result (input was a pinned host tensor)
+            stamps.append(time.perf_counter())
         assert not u_host.is_cuda
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t1) * 1e3 / args.steps
+        if os.environ.get("BENCH_DEBUG"):
+            print("e2e step ms:", [round((b - a) * 1e3, 2) for a, b in zip([t1] + stamps, stamps)],
+                  file=sys.stderr)
         if world > 1:
             tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
