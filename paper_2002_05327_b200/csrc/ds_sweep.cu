@@ -105,6 +105,13 @@ struct ds_plan {
   cudaGraphExec_t graph = nullptr;
   cudaStream_t gstream = nullptr;      // private stream for capture / replay
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  // K5 (accumulate) runs on a side stream: nothing later in the application
+  // reads u, so it leaves the critical path; ordering: K5 after its launch's
+  // K3 (ev_k3), K5s serial among themselves (u summation order unchanged),
+  // and the K3 that next overwrites a parity's solution buffers after the
+  // K5 that read them (ev_k5[parity]); joined back at the end (ev_join)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_k3 = nullptr, ev_k5[2] = {nullptr, nullptr}, ev_join = nullptr;
   const void *graph_f = nullptr;
   void *graph_u = nullptr;
   void *graph_partials = nullptr;
@@ -893,6 +900,14 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return fail(ds_fail(DS_ECUDA, std::string("ds_plan_create: ") + cudaGetErrorString(err)));
+  if (getenv("DS_K5_SIDE") == nullptr || std::string(getenv("DS_K5_SIDE")) != "0") {
+    if (cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_k5[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_k5[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return fail(ds_fail(DS_ECUDA, "ds_plan_create: side stream/events"));
+  }
   *out = P;
   return DS_OK;
 }
@@ -904,6 +919,9 @@ extern "C" int ds_plan_destroy(ds_plan *P) {
   if (!P) return DS_OK;
   if (P->graph) cudaGraphExecDestroy(P->graph);
   if (P->gstream) cudaStreamDestroy(P->gstream);
+  if (P->side) cudaStreamDestroy(P->side);
+  for (cudaEvent_t e : {P->ev_k3, P->ev_k5[0], P->ev_k5[1], P->ev_join})
+    if (e) cudaEventDestroy(e);
   if (P->gev_in) cudaEventDestroy(P->gev_in);
   if (P->gev_out) cudaEventDestroy(P->gev_out);
   for (auto e : P->ev) cudaEventDestroy(e);
@@ -974,6 +992,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
   const int nq = (int)P->vstep_off.size() - 1;
+  // K5 stream (see ds_plan::side); single-stream when profiling or
+  // collecting per-sweep partials (both read the stream in program order)
+  const cudaStream_t s5 = (P->side && !P->profiling && !partials) ? P->side : st;
+  bool k5_pending[2] = {false, false};
   for (int q = 0; q < nq; ++q) {
     {
       int v0 = P->vstep_off[q], G = P->vstep_off[q + 1] - v0;
@@ -992,6 +1014,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       ctx->launches++;
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
+      if (s5 != st && k5_pending[q & 1]) DS_CUDA(cudaStreamWaitEvent(st, P->ev_k5[q & 1], 0));
       int rc;
       if (P->program) {
         rc = ds_stage_program_launch_step(ctx, P->program, q, nrhs);
@@ -1002,14 +1025,22 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CHECK_LAUNCH();
       prof_mark(P, 2, st);
       int by = blocks_for(ctx, smax * nrhs / 4, std::max(1, cap / G));
+      if (s5 != st) {
+        DS_CUDA(cudaEventRecord(P->ev_k3, st));
+        DS_CUDA(cudaStreamWaitEvent(s5, P->ev_k3, 0));
+      }
       if (nrhs % 4 == 0)
-        k_accumulate<4><<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
+        k_accumulate<4><<<dim3(by, G), 256, 0, s5>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
                                                      P->gcounts[0], P->gcounts[1], P->gcounts[2]);
       else
-        k_accumulate<1><<<dim3(by, G), 256, 0, st>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
+        k_accumulate<1><<<dim3(by, G), 256, 0, s5>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
                                                      P->gcounts[0], P->gcounts[1], P->gcounts[2]);
       ctx->launches++;
       DS_CHECK_LAUNCH();
+      if (s5 != st) {
+        DS_CUDA(cudaEventRecord(P->ev_k5[q & 1], s5));
+        k5_pending[q & 1] = true;
+      }
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0) {
         prof_mark(P, 3, st);
@@ -1027,6 +1058,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     if (partials && (q + 1) % P->nsteps == 0)
       DS_CUDA(cudaMemcpyAsync(partials + (size_t)(q / P->nsteps) * P->nnodes * nrhs, u,
                               sizeof(cplx) * P->nnodes * nrhs, cudaMemcpyDeviceToDevice, st));
+  }
+  if (s5 != st && (k5_pending[0] || k5_pending[1])) {  // join: u complete on the caller's stream
+    DS_CUDA(cudaEventRecord(P->ev_join, s5));
+    DS_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
   }
   prof_mark(P, -1, st);
   P->last_launches = ctx->launches - launches0;
