@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 2
+#define DS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -151,6 +151,14 @@ DS_API int ds_fact_destroy(ds_fact *fact);
  * sources routed to it) and after any earlier writer of the same payload
  * slot (the host's list scheduler, _engine.launch_schedule).  Per-sweep
  * partials need nlaunch = 0.
+ * Subdomain sharding (optional, ABI 3): nranks > 1
+ * makes this plan rank `rank` of a sweep whose subdomain s is owned by rank
+ * owner[s].  fact_of_sub may be NULL for subdomains this rank does not own;
+ * the launch schedule (required) lists only owned visits, with the same
+ * launch boundaries on every rank.  Payload slots live on the rank owning
+ * their target; after ds_plan_set_peers, the transfer kernel writes payloads
+ * and arrival flags of remote targets directly into the owner's memory
+ * (peer / IPC-mapped pointers over NVLink) -- no separate exchange step.
  * Arrays are int32 unless noted. */
 typedef struct {
   int32_t dim, nsub, nsweeps, nsteps, ndir, nrhs_max;
@@ -176,6 +184,8 @@ typedef struct {
   int32_t nlaunch;
   const int32_t *launch_off;
   const int32_t *launch_visits;
+  int32_t nranks, rank;
+  const int32_t *owner;
 } ds_plan_desc;
 
 DS_API int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *desc, ds_plan **out);
@@ -216,6 +226,28 @@ DS_API int ds_plan_kernel_times(ds_plan *plan, double *ms, int64_t *count,
 
 /* Launch count of the last ds_ddm_apply (kernel nodes issued). */
 DS_API int64_t ds_plan_last_launches(const ds_plan *plan);
+
+/* ---------------------------------------------------------- sharded sweep
+ * Device memory a sharded plan exposes to its peers: the payload slots and
+ * the flag words ([own_nz | nz | arrivals | cuts | emitted | discards],
+ * stride nrhs of the call).  Every rank's layout is identical. */
+DS_API int ds_plan_shard_info(const ds_plan *plan, void **slot_base, int64_t *slot_bytes,
+                              void **flag_base, int64_t *flag_bytes);
+/* Pointers (valid in this process: local, peer or IPC-mapped) to every
+ * rank's slot and flag memory, index = rank; must be called before the
+ * first ds_ddm_apply_range of a sharded plan. */
+DS_API int ds_plan_set_peers(ds_ctx *ctx, ds_plan *plan, int32_t nranks,
+                             void *const *slot_bases, void *const *flag_bases);
+/* Number of launches of the plan's schedule. */
+DS_API int32_t ds_plan_nlaunch(const ds_plan *plan);
+/* Launches [l0, l1) of one application (eager, on the context stream).
+ * mode bit 0: initialise (zero u and this rank's flags) before l0;
+ * bit 1: finalise (join the side stream into the context stream) after l1.
+ * A sharded application is: init on every rank, then per launch every rank
+ * runs [l, l+1) with a cross-rank barrier between launches, then finalise;
+ * u of the sweep is the sum over ranks of their u. */
+DS_API int ds_ddm_apply_range(ds_ctx *ctx, ds_plan *plan, const ds_cplx *f_dev, ds_cplx *u_dev,
+                              int32_t nrhs, int32_t l0, int32_t l1, int32_t mode);
 
 /* ---------------------------------------------------------- vector kernels
  * Batched complex vector ops for GMRES (krylov.py:80, :97-106, :139-142);

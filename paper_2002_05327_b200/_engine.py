@@ -266,7 +266,7 @@ class DevicePlan:
     """
 
     def __init__(self, partition, operators, cache, directions, nrhs_max: int,
-                 schedule: str = "diagonal", pipelined: bool = False):
+                 schedule: str = "diagonal", pipelined: bool = False, shard=None):
         """schedule "diagonal": one device sweep per sweep direction, visits
         grouped by anti-diagonal step (ddm.py:212-291).  schedule "additive":
         the additive overlapping DDM (ddm.py:294-349) on the same kernels --
@@ -286,7 +286,16 @@ class DevicePlan:
         nsub = len(subs)
         lin = {idx: s for s, idx in enumerate(subs)}
         ops = [operators[idx] for idx in subs]
-        facts = cache.factorizations(ops)
+        # shard = (nranks, rank, owner[s]): this plan runs only its rank's
+        # visits and factorizes only its rank's operators (sharded.py)
+        self.shard = shard
+        if shard is not None:
+            nranks, rank, owner = shard
+            owned = [s for s in range(nsub) if owner[s] == rank]
+            ofacts = dict(zip(owned, cache.factorizations([ops[s] for s in owned])))
+            facts = [ofacts.get(s) for s in range(nsub)]
+        else:
+            facts = cache.factorizations(ops)
         self.partition = partition
         self.dim = dim
         self.nsub = nsub
@@ -372,7 +381,7 @@ class DevicePlan:
         # their sources are done (the dependency DAG of the sweep is shallower
         # than sweeps x steps); the cluster solve fits ~7 visits per wave
         self.launches = None
-        if pipelined and schedule == "diagonal":
+        if (pipelined or shard is not None) and schedule == "diagonal":
             order = []
             for w in range(self.nsweeps):
                 b0 = w * (nsteps + 1)
@@ -392,8 +401,18 @@ class DevicePlan:
                 max_m = max(max_m, int(np.prod([n for a, n in enumerate(shp) if a != ax])))
             cap_env = os.environ.get("DS_LAUNCH_CAP")
             cap = int(cap_env) if cap_env else (7 if max_m <= 160 else nsub * self.nsweeps)
-            self.launches = launch_schedule(self.nsweeps, nsub, order, xfer_use, dirs, sub_index,
-                                            None, max(1, cap))
+            if not pipelined:  # sweep-ordered launches (one per (sweep, step))
+                self.launches = []
+                for w in range(self.nsweeps):
+                    b0 = w * (nsteps + 1)
+                    for t in range(nsteps):
+                        self.launches.append([(w, visit_sub[w * nsub + i])
+                                              for i in range(step_off[b0 + t], step_off[b0 + t + 1])])
+            else:
+                self.launches = launch_schedule(self.nsweeps, nsub, order, xfer_use, dirs, sub_index,
+                                                None, max(1, cap))
+            if shard is not None:  # same launch boundaries on every rank, own visits only
+                self.launches = [[v for v in L if shard[2][v[1]] == shard[1]] for L in self.launches]
         self.geoms = geoms
         self.subs = subs
         self.dirs = dirs
@@ -407,7 +426,7 @@ class DevicePlan:
             sup_lo=np.asarray(sup_lo, np.int32), sup_shape=np.asarray(sup_shape, np.int32),
             beta00=np.concatenate(beta_vals), beta00_off=np.asarray(beta_off, np.int64),
             op_of_sub=np.arange(nsub, dtype=np.int32),
-            fact_index=np.asarray([f.index for f in facts], np.int32),
+            fact_index=np.asarray([f.index if f is not None else 0 for f in facts], np.int32),
             visit_sub=self.visit_sub, step_off=self.step_off,
             directions=np.asarray([_pad3(dv) for dv in dirs], np.int32).ravel(),
             xfer_use=xfer_use.ravel(),
@@ -417,7 +436,8 @@ class DevicePlan:
             xfac_off=np.asarray(xfac_off, np.int64),
         )
         op_handles = (C.c_void_p * nsub)(*[device_operator(op).handle.value for op in ops])
-        fact_handles = (C.c_void_p * nsub)(*[f.fset.handle.value for f in facts])
+        fact_handles = (C.c_void_p * nsub)(*[f.fset.handle.value if f is not None else None
+                                             for f in facts])
         desc = N.PlanDesc()
         desc.dim, desc.nsub, desc.nsweeps = dim, nsub, self.nsweeps
         desc.nsteps, desc.ndir, desc.nrhs_max = nsteps, ndir, nrhs_max
@@ -429,7 +449,11 @@ class DevicePlan:
         desc.nops = nsub
         desc.ops = C.cast(op_handles, C.c_void_p)
         desc.fact_of_sub = C.cast(fact_handles, C.c_void_p)
-        if self.launches:
+        if shard is not None:
+            owner_arr = np.asarray(shard[2], np.int32)
+            arrays["owner"] = owner_arr  # keep alive
+            desc.nranks, desc.rank, desc.owner = shard[0], shard[1], owner_arr.ctypes.data
+        if self.launches is not None:
             l_off = np.zeros(len(self.launches) + 1, np.int32)
             l_vis = []
             for i, L in enumerate(self.launches):
@@ -447,7 +471,7 @@ class DevicePlan:
         self._finalizer = weakref.finalize(self, lib.ds_plan_destroy, out)
         # replay one captured CUDA graph per (buffers, nrhs): ~4 sweeps x
         # n_steps x 4 launches per application (DS_GRAPH=0 disables)
-        if os.environ.get("DS_GRAPH", "1") != "0":
+        if os.environ.get("DS_GRAPH", "1") != "0" and shard is None:
             self.enable_graph(True)
 
     @property
@@ -457,6 +481,31 @@ class DevicePlan:
     def enable_graph(self, enable: bool = True):
         lib, ctx = context()
         N.check(lib.ds_ddm_enable_graph(ctx, self.handle, int(bool(enable))))
+
+    # ---- sharded plans (sharded.py)
+    def shard_info(self):
+        """(slot_base, slot_bytes, flag_base, flag_bytes) device memory peers write into."""
+        lib = N.load_library()
+        sb, fb = C.c_void_p(), C.c_void_p()
+        sn, fn = C.c_int64(), C.c_int64()
+        N.check(lib.ds_plan_shard_info(self.handle, C.byref(sb), C.byref(sn), C.byref(fb),
+                                       C.byref(fn)), "ds_plan_shard_info")
+        return sb.value, sn.value, fb.value, fn.value
+
+    def set_peers(self, slot_bases, flag_bases):
+        lib, ctx = context()
+        n = len(slot_bases)
+        sa = (C.c_void_p * n)(*slot_bases)
+        fa = (C.c_void_p * n)(*flag_bases)
+        N.check(lib.ds_plan_set_peers(ctx, self.handle, n, sa, fa), "ds_plan_set_peers")
+
+    def nlaunch(self) -> int:
+        return int(N.load_library().ds_plan_nlaunch(self.handle))
+
+    def apply_range(self, fmin, umin, nrhs: int, l0: int, l1: int, mode: int):
+        lib, ctx = context()
+        N.check(lib.ds_ddm_apply_range(ctx, self.handle, fmin.data_ptr(), umin.data_ptr(), nrhs,
+                                       l0, l1, mode), "ds_ddm_apply_range")
 
     def last_launches(self) -> int:
         return N.load_library().ds_plan_last_launches(self.handle)

@@ -63,6 +63,9 @@ class PlanDesc(C.Structure):
         ("nlaunch", i32),
         ("launch_off", vp),
         ("launch_visits", vp),
+        ("nranks", i32),
+        ("rank", i32),
+        ("owner", vp),
     ]
 
 
@@ -89,6 +92,10 @@ _SIGNATURES = [
     ("ds_ddm_counters", C.c_int, [vp, vp, i32, P_i32, P_i32, P_i32, P_i32, P_i32, P_i32]),
     ("ds_ddm_enable_graph", C.c_int, [vp, vp, i32]),
     ("ds_plan_last_launches", i64, [vp]),
+    ("ds_plan_shard_info", C.c_int, [vp, C.POINTER(vp), P_i64, C.POINTER(vp), P_i64]),
+    ("ds_plan_set_peers", C.c_int, [vp, vp, i32, C.POINTER(vp), C.POINTER(vp)]),
+    ("ds_plan_nlaunch", i32, [vp]),
+    ("ds_ddm_apply_range", C.c_int, [vp, vp, vp, vp, i32, i32, i32, i32]),
     ("ds_plan_set_profiling", C.c_int, [vp, i32]),
     ("ds_plan_kernel_times", C.c_int, [vp, P_f64, P_i64, i32]),
     ("ds_vec_dot", C.c_int, [vp, i64, i32, vp, vp, vp]),
@@ -123,7 +130,7 @@ def load_library(path: Path | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ds_abi_version() != 2:
+        if lib.ds_abi_version() != 3:
             raise SolverError("diagsweep_b200 ABI version mismatch")
         if path is None:
             _lib = lib

@@ -57,6 +57,7 @@ struct VisitDev {
 struct XferDev {
   int vidx;  // global visit index of the source visit
   int src, dst, use;
+  int owner;  // rank owning dst (sharded plans; its slot and flags may be remote)
   int dirmask, content_base, keepmask;
   double sign;
   int band_lo[3], band_shape[3];
@@ -100,6 +101,16 @@ struct ds_plan {
   StageProgram *program = nullptr;  // stage-per-launch solve (large slabs, or DS_SOLVE_MODE=staged)
   int patched_nrhs = 0;
   int nlaunch = 0;  // > 0: explicit launch schedule (visits of several sweeps per launch)
+  // sharding: this plan is rank `rank` of `nranks`; subdomain s owned by owner[s]
+  int nranks = 1, rank = 0;
+  std::vector<int> owner;
+  bool peers_set = false;
+  std::vector<XferDev> h_xfers;
+  std::vector<size_t> xfer_slot_off;  // element offset of each transfer's slot
+  cplx *slot_base = nullptr;
+  size_t slot_bytes = 0;
+  int **d_flag_bases = nullptr;  // [nranks] flag words of every rank (device table)
+  bool k5_pending[2] = {false, false};
   // graph
   bool use_graph = false;
   cudaGraphExec_t graph = nullptr;
@@ -229,6 +240,15 @@ __device__ __forceinline__ int solve_cut(const Flags &F, int sweep, int sub, int
   if (sweep == 1 && F.own_nz[(size_t)sub * nrhs + r]) return 0;
   if (F.arr_cnt[vi] == 0) return 0;
   return F.arr_cut[vi] & CUT_ALL;
+}
+
+// arrival words (counts, cut masks) of a rank's flag block for stride nrhs
+// (the layout of flags_view)
+__device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, int nrhs,
+                                              int *&arr_cnt, int *&arr_cut) {
+  const size_t per = (size_t)nsweeps * nsub * nrhs;
+  arr_cnt = base + (size_t)nsub * nrhs + per;
+  arr_cut = arr_cnt + per;
 }
 
 #define SLOT_SMEM 32
@@ -443,11 +463,16 @@ __device__ __forceinline__ double op_k2(const OpDev &o, const int (&c)[3]) {
 template <int RV>
 __global__ void __launch_bounds__(256)
     k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
-               const SubDev *__restrict__ subs, int nsub, int nrhs, int dim, Flags F) {
+               const SubDev *__restrict__ subs, int nsub, int nrhs, int dim, Flags F,
+               int *const *__restrict__ flag_bases, int nsweeps) {
   const XferDev &X = xfers[blockIdx.y];
   const VisitDev &V = visits[X.vidx];
   const int sweep = V.sweep;  // a launch may hold visits of several sweeps
   if (blockIdx.x == 0) {
+    // arrivals go to the flags of the rank owning the target (sharded plans:
+    // a peer's memory over NVLink; otherwise this plan's own flags)
+    int *arr_cnt = F.arr_cnt, *arr_cut = F.arr_cut;
+    if (flag_bases) arrival_words(flag_bases[X.owner], nsweeps, nsub, nrhs, arr_cnt, arr_cut);
     for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
       if (!V.nz[r]) continue;
       int cut = solve_cut(F, sweep, X.src, nsub, r, nrhs);
@@ -456,8 +481,8 @@ __global__ void __launch_bounds__(256)
         atomicAdd(&F.discard[r], 1);
       } else {
         size_t ti = ((size_t)(X.use - 1) * nsub + X.dst) * nrhs + r;
-        atomicAdd(&F.arr_cnt[ti], 1);
-        atomicAnd(&F.arr_cut[ti], X.content_base | (cut & X.keepmask));
+        atomicAdd_system(&arr_cnt[ti], 1);
+        atomicAnd_system(&arr_cut[ti], X.content_base | (cut & X.keepmask));
         atomicAdd(&F.emit_cnt[((size_t)(sweep - 1) * nsub + X.src) * nrhs + r], 1);
       }
     }
@@ -555,6 +580,7 @@ __global__ void __launch_bounds__(256)
     for (int j = 0; j < RV; ++j)
       if (emit[j]) sp[j * lpn] = cadd(sp[j * lpn], cscale(cadd(rv[j * lpn], acc[j]), X.sign));
   }
+  if (flag_bases) __threadfence_system();  // sharded: peer-memory payloads before the barrier
 }
 
 // ------------------------------------------------------------ plan create
@@ -574,6 +600,23 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->nsteps = nst;
   P->ndir = ndir;
   P->nrhs_max = d->nrhs_max;
+  const bool sharded = d->nranks > 1;
+  P->nranks = sharded ? d->nranks : 1;
+  P->rank = sharded ? d->rank : 0;
+  P->owner.assign(nsub, 0);
+  if (sharded) {
+    if (!d->owner || d->rank < 0 || d->rank >= d->nranks) {
+      delete P;
+      return ds_fail(DS_ECONFIG, "sharded plan: bad rank/owner table");
+    }
+    for (int s = 0; s < nsub; ++s) {
+      P->owner[s] = d->owner[s];
+      if (P->owner[s] < 0 || P->owner[s] >= d->nranks) {
+        delete P;
+        return ds_fail(DS_ECONFIG, "sharded plan: owner out of range");
+      }
+    }
+  }
   P->nnodes = 1;
   for (int a = 0; a < 3; ++a) {
     P->gcounts[a] = a < dim ? d->grid_counts[a] : 1;
@@ -598,6 +641,10 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   for (int s = 0; s < nsub; ++s) {
     const ds_fact *FA = d->fact_of_sub[s];
     int fi = d->fact_index[s];
+    if (P->owner[s] != P->rank && !FA) {  // remote subdomain: no local factors
+      memset(&hf[s], 0, sizeof(FactDev));
+      continue;
+    }
     if (!FA || fi < 0 || fi >= (int)FA->facts.size())
       return fail(ds_fail(DS_ECONFIG, "bad factorization handle/index for a subdomain"));
     hf[s] = FA->facts[fi];
@@ -606,8 +653,9 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->facts = (FactDev *)mem;
   P->h_facts = hf;
   for (int s = 0; s < nsub; ++s) {
-    P->h_l.push_back(d->fact_of_sub[s]->h_l[d->fact_index[s]].data());
-    P->h_u.push_back(d->fact_of_sub[s]->h_u[d->fact_index[s]].data());
+    const bool local = d->fact_of_sub[s] != nullptr;
+    P->h_l.push_back(local ? d->fact_of_sub[s]->h_l[d->fact_index[s]].data() : nullptr);
+    P->h_u.push_back(local ? d->fact_of_sub[s]->h_u[d->fact_index[s]].data() : nullptr);
   }
   cudaMemcpy(P->facts, hf.data(), sizeof(FactDev) * nsub, cudaMemcpyHostToDevice);
   // ---- beta00 ramps
@@ -639,7 +687,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
       S.sup_lo[a] = ok ? d->sup_lo[s * 3 + a] : 0;
       S.sup_shape[a] = ok ? d->sup_shape[s * 3 + a] : 1;
       S.beta[a] = ok ? dbeta + d->beta00_off[s * 3 + a] : nullptr;
-      if (ok && S.win_shape[a] != fd.win_shape[a])
+      if (ok && P->owner[s] == P->rank && S.win_shape[a] != fd.win_shape[a])
         return fail(ds_fail(DS_ECONFIG, "window shape does not match its factorization"));
       wn *= S.win_shape[a];
     }
@@ -648,7 +696,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     max_w = std::max<int>(max_w, (int)wn);
     P->max_w = max_w;
     P->max_axis_sum = std::max(P->max_axis_sum, S.win_shape[0] + S.win_shape[1] + S.win_shape[2]);
-    P->max_m = std::max(P->max_m, fd.m);
+    if (P->owner[s] == P->rank) P->max_m = std::max(P->max_m, fd.m);
   }
   if (plan_alloc(P, &mem, sizeof(SubDev) * nsub)) return fail(DS_ECUDA);
   P->subs = (SubDev *)mem;
@@ -658,18 +706,23 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   int max_nb = 0;
   for (int s = 0; s < nsub; ++s) max_nb = std::max(max_nb, hf[s].nb);
   const bool sched = d->nlaunch > 0;
+  if (sharded && !sched)
+    return fail(ds_fail(DS_ECONFIG, "a sharded plan needs a launch schedule"));
   if (sched) {
     if (!d->launch_off || !d->launch_visits)
       return fail(ds_fail(DS_ECONFIG, "launch schedule without launch_off/launch_visits"));
-    if (d->launch_off[0] != 0 || d->launch_off[d->nlaunch] != nsw * nsub)
-      return fail(ds_fail(DS_ECONFIG, "launch schedule must cover every (sweep, subdomain) once"));
+    int nown = 0;
+    for (int s = 0; s < nsub; ++s) nown += P->owner[s] == P->rank;
+    if (d->launch_off[0] != 0 || d->launch_off[d->nlaunch] != nsw * nown)
+      return fail(ds_fail(DS_ECONFIG, "launch schedule must cover every owned (sweep, subdomain) once"));
     std::vector<char> seen((size_t)nsw * nsub, 0);
     for (int l = 0; l < d->nlaunch; ++l) {
       P->gmax = std::max(P->gmax, d->launch_off[l + 1] - d->launch_off[l]);
       for (int i = d->launch_off[l]; i < d->launch_off[l + 1]; ++i) {
         int w = d->launch_visits[2 * i], s = d->launch_visits[2 * i + 1];
-        if (w < 0 || w >= nsw || s < 0 || s >= nsub || seen[(size_t)w * nsub + s]++)
-          return fail(ds_fail(DS_ECONFIG, "launch schedule: bad or repeated visit"));
+        if (w < 0 || w >= nsw || s < 0 || s >= nsub || P->owner[s] != P->rank ||
+            seen[(size_t)w * nsub + s]++)
+          return fail(ds_fail(DS_ECONFIG, "launch schedule: bad, remote or repeated visit"));
       }
     }
   } else {
@@ -749,6 +802,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cudaMemset(slotmem, 0, sizeof(cplx) * std::max<size_t>(slot_elems, 1));
   P->slot_bufs.push_back({slotmem, sizeof(cplx) * std::max<size_t>(slot_elems, 1)});
   for (size_t i = 0; i < hslots.size(); ++i) hslots[i].data = slotmem + slot_off[i];
+  P->slot_base = slotmem;
+  P->slot_bytes = sizeof(cplx) * std::max<size_t>(slot_elems, 1);
   // slot table ordered per visit (contiguous ranges)
   std::vector<SlotRef> hslot_tab;
   // ---- transfer (1 - beta) factors on ext
@@ -854,7 +909,15 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
           for (int a = 0; a < dim; ++a)
             X.fac[a] = dfac + d->xfac_off[((size_t)s * ndir + k) * 3 + a];
           X.slot = nullptr;
-          if (use > 0) X.slot = hslots[slot_id[std::make_tuple(use - 1, X.dst, k)]].data;
+          X.owner = P->owner[X.dst];
+          size_t soff = 0;
+          if (use > 0) {
+            const int sid = slot_id[std::make_tuple(use - 1, X.dst, k)];
+            soff = slot_off[sid];
+            // a remote target's slot lives on its owner: set by ds_plan_set_peers
+            X.slot = X.owner == P->rank ? hslots[sid].data : nullptr;
+          }
+          P->xfer_slot_off.push_back(soff);
           hx.push_back(X);
         }
       }
@@ -873,6 +936,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
   cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice);
+  P->h_xfers = hx;
+  P->peers_set = !sharded;
   P->h_visits = hv;
   P->h_solve = hsv;
   P->patched_nrhs = 0;
@@ -977,26 +1042,32 @@ static void prof_mark(ds_plan *P, int cls, cudaStream_t st) {
 }
 
 // issue the whole application on ctx->stream (capturable)
-static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials) {
+// issue launches [q0, q1) of one application on ctx->stream (capturable);
+// mode bit 0: zero u and the flags first; bit 1: join the K5 side stream
+static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials, int q0 = 0,
+                       int q1 = -1, int mode = 3) {
   ds_ctx *ctx = P->ctx;
   cudaStream_t st = ctx->stream;
   const int dim = P->dim;
   Flags F = flags_view(P, nrhs);
   int64_t launches0 = ctx->launches;
   size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
-  DS_CUDA(cudaMemsetAsync(u, 0, sizeof(cplx) * P->nnodes * nrhs, st));
-  DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
-  DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
-  DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
+  if (mode & 1) {
+    DS_CUDA(cudaMemsetAsync(u, 0, sizeof(cplx) * P->nnodes * nrhs, st));
+    DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
+    DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
+    DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
+    P->k5_pending[0] = P->k5_pending[1] = false;
+  }
   const int cap = std::max(1, ctx->num_sms * 4);
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
-  const int nq = (int)P->vstep_off.size() - 1;
+  const int nq = q1 < 0 ? (int)P->vstep_off.size() - 1 : q1;
   // K5 stream (see ds_plan::side); single-stream when profiling or
   // collecting per-sweep partials (both read the stream in program order)
   const cudaStream_t s5 = (P->side && !P->profiling && !partials) ? P->side : st;
-  bool k5_pending[2] = {false, false};
-  for (int q = 0; q < nq; ++q) {
+  bool *k5_pending = P->k5_pending;
+  for (int q = q0; q < nq; ++q) {
     {
       int v0 = P->vstep_off[q], G = P->vstep_off[q + 1] - v0;
       if (G == 0) continue;
@@ -1047,10 +1118,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         int bz = std::max(1, std::min(64, 2 * cap / nx));
         if (nrhs % 4 == 0)
           k_transfer<4><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      nrhs, dim, F);
+                                                      nrhs, dim, F, P->d_flag_bases, P->nsweeps);
         else
           k_transfer<1><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      nrhs, dim, F);
+                                                      nrhs, dim, F, P->d_flag_bases, P->nsweeps);
         ctx->launches++;
         DS_CHECK_LAUNCH();
       }
@@ -1059,7 +1130,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CUDA(cudaMemcpyAsync(partials + (size_t)(q / P->nsteps) * P->nnodes * nrhs, u,
                               sizeof(cplx) * P->nnodes * nrhs, cudaMemcpyDeviceToDevice, st));
   }
-  if (s5 != st && (k5_pending[0] || k5_pending[1])) {  // join: u complete on the caller's stream
+  if ((mode & 2) && s5 != st && (k5_pending[0] || k5_pending[1])) {  // join: u complete on st
     DS_CUDA(cudaEventRecord(P->ev_join, s5));
     DS_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
   }
@@ -1073,6 +1144,8 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
   if (!ctx || !P || !f || !u) return ds_fail(DS_ECONFIG, "ds_ddm_apply: null argument");
   if (nrhs < 1 || nrhs > P->nrhs_max)
     return ds_fail(DS_ECONFIG, "ds_ddm_apply: nrhs exceeds the plan's nrhs_max");
+  if (P->nranks > 1)
+    return ds_fail(DS_ECONFIG, "ds_ddm_apply: a sharded plan runs through ds_ddm_apply_range");
   if (ctx != P->ctx) P->ctx = ctx;
   int rc = patch_tables(P, nrhs);
   if (rc) return rc;
@@ -1125,6 +1198,61 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     return DS_OK;
   }
   rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
+  if (rc) P->slots_dirty = true;
+  return rc;
+}
+
+extern "C" int ds_plan_shard_info(const ds_plan *P, void **slot_base, int64_t *slot_bytes,
+                                  void **flag_base, int64_t *flag_bytes) {
+  if (!P) return ds_fail(DS_ECONFIG, "null plan");
+  if (slot_base) *slot_base = P->slot_base;
+  if (slot_bytes) *slot_bytes = (int64_t)P->slot_bytes;
+  if (flag_base) *flag_base = P->flags;
+  if (flag_bytes) *flag_bytes = (int64_t)(P->flag_words * sizeof(int));
+  return DS_OK;
+}
+
+extern "C" int ds_plan_set_peers(ds_ctx *ctx, ds_plan *P, int32_t nranks, void *const *slot_bases,
+                                 void *const *flag_bases) {
+  if (!ctx || !P || !slot_bases || !flag_bases) return ds_fail(DS_ECONFIG, "ds_plan_set_peers: null argument");
+  if (nranks != P->nranks) return ds_fail(DS_ECONFIG, "ds_plan_set_peers: rank count mismatch");
+  for (int r = 0; r < nranks; ++r)
+    if (!slot_bases[r] || !flag_bases[r]) return ds_fail(DS_ECONFIG, "ds_plan_set_peers: null peer pointer");
+  std::vector<XferDev> hx = P->h_xfers;
+  for (size_t i = 0; i < hx.size(); ++i)
+    if (hx[i].use > 0) hx[i].slot = (cplx *)slot_bases[hx[i].owner] + P->xfer_slot_off[i];
+  DS_CUDA(cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice));
+  P->h_xfers = hx;
+  if (!P->d_flag_bases) {
+    void *mem;
+    if (plan_alloc(P, &mem, sizeof(int *) * nranks)) return ds_fail(DS_ECUDA, "ds_plan_set_peers: alloc");
+    P->d_flag_bases = (int **)mem;
+  }
+  DS_CUDA(cudaMemcpy(P->d_flag_bases, flag_bases, sizeof(int *) * nranks, cudaMemcpyHostToDevice));
+  P->peers_set = true;
+  return DS_OK;
+}
+
+extern "C" int32_t ds_plan_nlaunch(const ds_plan *P) {
+  return P ? (int32_t)P->vstep_off.size() - 1 : -1;
+}
+
+extern "C" int ds_ddm_apply_range(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u, int32_t nrhs,
+                                  int32_t l0, int32_t l1, int32_t mode) {
+  if (!ctx || !P || !f || !u) return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: null argument");
+  if (nrhs < 1 || nrhs > P->nrhs_max)
+    return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: nrhs exceeds the plan's nrhs_max");
+  const int nq = (int)P->vstep_off.size() - 1;
+  if (l0 < 0 || l1 < l0 || l1 > nq) return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: bad launch range");
+  if (!P->peers_set) return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: ds_plan_set_peers not called");
+  if (ctx != P->ctx) P->ctx = ctx;
+  int rc = patch_tables(P, nrhs);
+  if (rc) return rc;
+  if (P->slots_dirty) {
+    for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
+    P->slots_dirty = false;
+  }
+  rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, nullptr, l0, l1, mode);
   if (rc) P->slots_dirty = true;
   return rc;
 }
