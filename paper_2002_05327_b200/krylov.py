@@ -305,7 +305,8 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
     if not is_torch:
         x = x.cpu().numpy()
     elif not bt.is_cuda:  # results return where the input lives (pinned in -> pinned out)
-        x = x.to("cpu", non_blocking=False)
-        if bt.is_pinned():
-            x = x.pin_memory()
+        out = torch.empty(x.shape, dtype=x.dtype, pin_memory=bt.is_pinned())
+        out.copy_(x, non_blocking=bt.is_pinned())  # one DMA into a cached pinned block
+        torch.cuda.current_stream().synchronize()
+        x = out
     return (x, reports) if batched else (x, reports[0])
