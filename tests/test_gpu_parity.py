@@ -263,6 +263,30 @@ def test_gpu_vs_reference_golden_compact_and_random(cuda):
     assert reps[0].events == json.loads(str(g["events"]))
 
 
+def test_octant_partials_converge_by_sweep(cuda):
+    """collect_partials (the sweep-ordered plan): the running sum after each
+    sweep is exact on that sweep's octant region up to the PML error
+    (pkg/tests/test_ddm.py:144-155: subdomain counts [4, 2, 2, 1], relative
+    error < 1e-3 against a global direct solve -- here the oracle's SuperLU
+    of the global operator)."""
+    from paper_2002_05327_b200.ddm import octant_exactness_check
+
+    grid, part, ops, f, prob = _compact_problem()
+    u_ref = O.SparseLU(prob.global_operator()).solve(f)
+    u, report = diagonal_sweep_solve(f, part, ops, FactorizationCache(), collect_partials=True,
+                                     warn_collar=False)
+    assert len(report.partials) == 4
+    checks = octant_exactness_check(report.partials, u_ref, part, (2, 2))
+    assert [c["subdomains"] for c in checks] == [4, 2, 2, 1]
+    for c in checks:
+        assert c["relative_error"] < 1e-3
+    # the last partial is the full sweep result; the pipelined plan (default,
+    # different launch order) gives the same u up to summation order
+    assert rel(np.asarray(report.partials[-1]), u.values) <= 1e-15
+    u_pipe, _ = diagonal_sweep_solve(f, part, ops, FactorizationCache(), warn_collar=False)
+    assert rel(u_pipe.values, u.values) <= 1e-12
+
+
 def test_gpu_additive_vs_reference_golden(cuda):
     """additive_ddm_solve (ddm.py:294-349) on the same kernels: vs the
     reference's own outputs (tests/golden/make_golden_additive.py), counters,
