@@ -38,6 +38,15 @@
 namespace cg = cooperative_groups;
 
 #define GJ_THREADS 512
+
+// old - a * b with four fused multiply-adds (the rank-1 update's only
+// arithmetic; cmul + csub would issue 6 FP64 instructions)
+__device__ __forceinline__ cplx cfms(cplx old, cplx a, cplx b) {
+  cplx r;
+  r.x = fma(a.y, b.y, fma(-a.x, b.x, old.x));
+  r.y = fma(-a.y, b.x, fma(-a.x, b.y, old.y));
+  return r;
+}
 static const size_t kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
 
 __global__ void __launch_bounds__(GJ_THREADS, 1)
@@ -68,6 +77,13 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
 
   const int ld = mcper_max;
   const int ba = J.f.block_axis;
+  // fixed 2D thread mapping over my m x mc slice: thread t owns column
+  // cc = t % mc and rows i0, i0 + istep, ... (no per-element division; the
+  // pivot row entries of its column stay in registers for a whole pivot)
+  const int cc_t = mc > 0 ? t % mc : 0;
+  const int i0_t = mc > 0 ? t / mc : m;
+  const int istep = mc > 0 ? T / mc : 1;
+  const bool col_thread = mc > 0 && t < istep * mc;
   for (int step = 0; step < nsteps; ++step) {
     // ---- Schur complement of block k (my columns):
     //   top    S_k = D_k - (l_k u_{k-1}) S_{k-1}^{-1}
@@ -84,12 +100,14 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
       co2 = cmul(J.op.c_hi[ba][k], J.op.c_lo[ba][k + 1]);
       p2 = J.sinv + (size_t)(k + 1) * m * m;
     }
-    for (int e = t; e < m * mc; e += T) {
-      int i = e / mc, cc = e % mc, c = c0 + cc;
-      cplx v = d_entry(J, k, i, c);
-      if (p1) v = csub(v, cmul(co1, __ldcg(p1 + (size_t)i * m + c)));
-      if (p2) v = csub(v, cmul(co2, __ldcg(p2 + (size_t)i * m + c)));
-      S[i * ld + cc] = v;
+    if (col_thread) {
+      const int cc = cc_t, c = c0 + cc;
+      for (int i = i0_t; i < m; i += istep) {
+        cplx v = d_entry(J, k, i, c);
+        if (p1) v = csub(v, cmul(co1, __ldcg(p1 + (size_t)i * m + c)));
+        if (p2) v = csub(v, cmul(co2, __ldcg(p2 + (size_t)i * m + c)));
+        S[i * ld + cc] = v;
+      }
     }
     cluster.sync();
     // ---- Gauss-Jordan inversion with partial pivoting
@@ -127,7 +145,10 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
           if (t == 0) rp[j] = p;
         }
       }
-      cluster.sync();
+      if (C == 1)
+        __syncthreads();
+      else
+        cluster.sync();
       const int p = piv[j];
       const cplx pivot = cj[p];
       if (t == 0 && !(cabs1(pivot) > 0.0 && isfinite(pivot.x) && isfinite(pivot.y))) s_bad = 1;
@@ -137,19 +158,26 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
         rowj_old[cc] = S[j * ld + cc];
       }
       __syncthreads();
-      for (int e = t; e < m * mc; e += T) {
-        int i = e / mc, cc = e % mc, c = c0 + cc;
-        cplx fi = cj[i == j ? p : (i == p ? j : i)];
-        cplx nv;
+      if (col_thread) {
+        const int cc = cc_t, c = c0 + cc;
+        const cplx pr = prow[cc], ro = rowj_old[cc];
         if (c == j) {
-          nv = (i == j) ? inv : cmul(make_double2(-fi.x, -fi.y), inv);
-        } else if (i == j) {
-          nv = prow[cc];
+          for (int i = i0_t; i < m; i += istep) {
+            const cplx fi = cj[i == j ? p : (i == p ? j : i)];
+            S[i * ld + cc] = (i == j) ? inv : cmul(make_double2(-fi.x, -fi.y), inv);
+          }
         } else {
-          cplx old = (i == p) ? rowj_old[cc] : S[i * ld + cc];
-          nv = csub(old, cmul(fi, prow[cc]));
+          // rows: i == j takes the scaled pivot row, i == p the old row j,
+          // every other row S_i -= f_i * prow (branch-free selects)
+#pragma unroll 4
+          for (int i = i0_t; i < m; i += istep) {
+            const cplx fi = cj[i == p ? j : i];
+            cplx old = S[i * ld + cc];
+            old = (i == p) ? ro : old;
+            const cplx nv = cfms(old, fi, pr);
+            S[i * ld + cc] = (i == j) ? pr : nv;
+          }
         }
-        S[i * ld + cc] = nv;
       }
       __syncthreads();
     }
@@ -168,9 +196,9 @@ __global__ void __launch_bounds__(GJ_THREADS, 1)
     }
     __syncthreads();
     cplx *out = J.sinv + (size_t)k * m * m;
-    for (int e = t; e < m * mc; e += T) {
-      int i = e / mc, cc = e % mc;
-      out[(size_t)i * m + dst[c0 + cc]] = S[i * ld + cc];
+    if (col_thread) {
+      const int cc = cc_t, dc = dst[c0 + cc];
+      for (int i = i0_t; i < m; i += istep) out[(size_t)i * m + dc] = S[i * ld + cc];
     }
     cluster.sync();
   }
