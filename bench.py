@@ -122,15 +122,54 @@ class ClockSampler:
 def algorithmic_work(dp, nrhs):
     """K3 flops and factor bytes per application: every
     (sweep, subdomain) visit counts 16 n_b m^2 flop per RHS and streams its
-    2 n_b m^2 complex factor entries once per RHS chunk of 32."""
+    2 n_b m^2 complex factor entries once per RHS chunk (K3 clusters take at
+    most 16 RHS)."""
     flops = 0
     fbytes = 0
-    chunks = math.ceil(nrhs / 32)
+    chunks = math.ceil(nrhs / 16)
     for f in dp._keep[1]:
         nb, m = f.n_blocks, f.block_size
         flops += 16 * nb * m * m * nrhs
         fbytes += 2 * nb * m * m * 16 * chunks
     return flops * dp.nsweeps, fbytes * dp.nsweeps
+
+
+def step_kernel_bytes(dp, nrhs):
+    """Algorithmic HBM bytes per application of the step kernels (SURVEY
+    §8(d)), from the last application's counters and the transfer geometry:
+      K6 assemble   16 W per visit and RHS (rhs init) + 32 per copied node
+                    (own source in sweep 1, every arriving payload band node);
+      K5 accumulate 48 |support| per nonzero visit and RHS;
+      K4 transfer   16 |ext| + 48 |band| per emitted, non-discarded source
+                    and RHS (the cut / emission rules of ddm.py:82-110)."""
+    import numpy as np
+
+    from paper_2002_05327_b200.ddm import cut_mask_to_set, emits
+
+    ctr = dp.counters(nrhs)
+    vnz, vcut = ctr["visit_nonzero"], ctr["visit_cut"]
+    part = dp.partition
+    W = [int(np.prod(part.window(i).shape)) for i in dp.subs]
+    own = [int(np.prod(part.owned_window(i).shape)) for i in dp.subs]
+    sup = [int(np.prod(part.beta00_window(i).shape)) for i in dp.subs]
+    k4 = k5 = k6 = 0
+    arrived = 0
+    for w in range(dp.nsweeps):
+        for s in range(dp.nsub):
+            k6 += 16 * W[s] * nrhs + (32 * own[s] * nrhs if w == 0 else 0)
+            nz = vnz[w, s]
+            k5 += 48 * sup[s] * int(nz.sum())
+            for r in np.nonzero(nz)[0]:
+                cuts = cut_mask_to_set(int(vcut[w, s, r]), dp.dim)
+                for k, d in enumerate(dp.dirs):
+                    g = dp.geoms[(s, k)]
+                    if g is None or int(dp.xfer_use[w, s, k]) <= 0 or not emits(d, cuts):
+                        continue
+                    band, ext = int(np.prod(g.band.shape)), int(np.prod(g.ext.shape))
+                    k4 += 16 * ext + 48 * band
+                    arrived += band
+    k6 += 32 * arrived
+    return {"assemble": k6, "accumulate": k5, "transfer": k4}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -303,7 +342,8 @@ def run_ours(args, rank, world, local_rank):
                    for k, v in ktimes.items()}
         solve_ms = ktimes["block_solve"][0] / args.steps
         ach = flops / (solve_ms / 1e3) / 1e12
-        roofline = {"bound": "tensor", "pipe": "fp64 (DFMA)", "achieved": ach, "peak": fp64,
+        roofline = {"bound": "tensor", "pipe": "fp64 tensor (DMMA m8n8k4)", "achieved": ach,
+                    "peak": fp64,
                     "unit": "TFLOP/s", "frac": ach / fp64, "traffic": None,
                     "peak_source": fp64_src,
                     "kernel": "k_block_solve (K3)",
@@ -312,6 +352,17 @@ def run_ours(args, rank, world, local_rank):
                                  "frac": fbytes / (solve_ms / 1e3) / 1e9 / hbm,
                                  "peak_source": hbm_src},
                     "share_of_step": solve_ms / ms}
+    # ---- HBM rooflines of the step kernels (K4/K5/K6; SURVEY §8(d) bytes)
+    kernel_rooflines = None
+    if ktimes:
+        kb = step_kernel_bytes(dp, R)  # per application of the R-RHS batch
+        kernel_rooflines = {}
+        for cls, nbytes in kb.items():
+            kms = ktimes[cls][0] / args.steps
+            gbs = nbytes * (apps / R) / (kms / 1e3) / 1e9 if kms > 0 else None
+            kernel_rooflines[cls] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                                     "frac": gbs / hbm if gbs else None,
+                                     "algorithmic_bytes_per_app": nbytes, "peak_source": hbm_src}
     # ---- parity spot check of the timed output (first RHS vs oracle is in tests)
     res = {
         "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2 else
@@ -332,6 +383,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
         "e2e": e2e,
         "roofline": roofline,
+        "kernel_rooflines": kernel_rooflines,
         "kernels": kernels,
     }
     return res
