@@ -342,9 +342,20 @@ def run_ours(args, rank, world, local_rank):
                    for k, v in ktimes.items()}
         solve_ms = ktimes["block_solve"][0] / args.steps
         ach = flops / (solve_ms / 1e3) / 1e12
+        # DRAM traffic of one K3 launch from the committed ncu --set full capture
+        # (profiles/k3_traffic_r01.json), beside that launch's algorithmic bytes
+        traffic, traffic_note = None, None
+        tpath = ROOT / "profiles" / "k3_traffic_r01.json"
+        if tpath.exists() and args.config in (2, "2"):
+            tj = json.loads(tpath.read_text())
+            traffic = tj["dram_bytes"]
+            traffic_note = {"launch": tj["launch"], "algorithmic_factor_bytes": tj["algorithmic_factor_bytes"],
+                            "traffic_over_algorithmic": tj["traffic_over_algorithmic"],
+                            "duration_us": tj["duration_us"], "source": str(tpath.relative_to(ROOT))}
         roofline = {"bound": "tensor", "pipe": "fp64 tensor (DMMA m8n8k4)", "achieved": ach,
                     "peak": fp64,
-                    "unit": "TFLOP/s", "frac": ach / fp64, "traffic": None,
+                    "unit": "TFLOP/s", "frac": ach / fp64, "traffic": traffic,
+                    "traffic_per_launch": traffic_note,
                     "peak_source": fp64_src,
                     "kernel": "k_block_solve (K3)",
                     "algorithmic_per_app": {"flop": flops, "factor_bytes": fbytes},
