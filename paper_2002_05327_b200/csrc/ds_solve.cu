@@ -1344,6 +1344,18 @@ __global__ void __launch_bounds__(SOLVE_THREADS, 1)
 // addressing and the row-tile count MT as a template parameter (1 for
 // 16-CTA clusters, 2 for 8-CTA ones), so only the (NT, X2) product variants
 // are inlined: fewer registers, no spills, no per-stage integer division.
+#ifdef K3_TILE_CPASYNC
+// factor tiles by per-thread cp.async (LDGSTS) instead of TMA bulk copies:
+// leaves the SM's TMA unit to the exchange multicasts; each thread's copies
+// arrive on the tile mbarrier (count = threads) when they complete
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+#endif
+
 template <int MT, int NW>
 __global__ void __launch_bounds__(64 * NW, 1)
     k_block_solve8(const SolveVisit *__restrict__ visits, int nrhs, int rc, int rows_max) {
@@ -1417,9 +1429,17 @@ __global__ void __launch_bounds__(64 * NW, 1)
     if (k < 0) return;
     const int q = fseq(h, st), slot = q % FAC_STAGES;
     uint64_t *bar = &fbar[h * FAC_STAGES + slot];
+#ifdef K3_TILE_CPASYNC
+    // all threads: 16-byte pieces, then an arrival when they complete
+    const char *src = (const char *)(f.sinv + ((size_t)k * m + r0) * m);
+    char *dst = (char *)(fac + (h * FAC_STAGES + slot) * fstride);
+    for (uint32_t b = (uint32_t)t * 16; b < fac_bytes; b += 16 * NT_) cp_async16(dst + b, src + b);
+    cp_async_arrive(bar);
+#else
     mbar_expect_tx(bar, fac_bytes);
     if (fac_bytes)
       bulk_g2s(fac + (h * FAC_STAGES + slot) * fstride, f.sinv + ((size_t)k * m + r0) * m, fac_bytes, bar);
+#endif
   };
   auto push = [&](int h, int p) {
     if (push_bytes)
@@ -1437,7 +1457,11 @@ __global__ void __launch_bounds__(64 * NW, 1)
   if (t == 0) {
     mbar_init(&vbar[0], 1);
     mbar_init(&vbar[1], 1);
+#ifdef K3_TILE_CPASYNC
+    for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], NT_);
+#else
     for (int i = 0; i < 2 * FAC_STAGES; ++i) mbar_init(&fbar[i], 1);
+#endif
     fence_mbar_init();
   }
   cluster.sync();
@@ -1449,8 +1473,13 @@ __global__ void __launch_bounds__(64 * NW, 1)
     if (S > 1) mbar_expect_tx(&vbar[1], deliveries(1) * vec_bytes);
   }
   for (int st = 0; st < FAC_STAGES - 1 && st < S; ++st) {
+#ifdef K3_TILE_CPASYNC
+    load_tile(0, st);
+    load_tile(1, st);
+#else
     if (t == TILE_T[0]) load_tile(0, st);
     if (t == TILE_T[1]) load_tile(1, st);
+#endif
   }
   for (int h = 0; h < 2; ++h) {
     if (h == 1 && nbt == 0) break;
@@ -1492,8 +1521,13 @@ __global__ void __launch_bounds__(64 * NW, 1)
     const int p = s & 1;
     TRACE5(0);
     if (s + FAC_STAGES - 1 < S) {
+#ifdef K3_TILE_CPASYNC
+      load_tile(0, s + FAC_STAGES - 1);
+      load_tile(1, s + FAC_STAGES - 1);
+#else
       if (t == TILE_T[0]) load_tile(0, s + FAC_STAGES - 1);
       if (t == TILE_T[1]) load_tile(1, s + FAC_STAGES - 1);
+#endif
     }
     TRACE5(8);
     int kind, k = block_of(hh, s, kind);
