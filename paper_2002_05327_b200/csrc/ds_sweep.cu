@@ -460,11 +460,12 @@ __device__ __forceinline__ double op_k2(const OpDev &o, const int (&c)[3]) {
 // w = prod_a fac_a on ext; block 0 also does the arrival/emission bookkeeping
 // (ddm.py:262-279), one thread per RHS.  RHS columns that do not emit
 // (zero visit, or cut towards this direction) contribute nothing.
-template <int RV>
+template <int RV, int DIM>
 __global__ void __launch_bounds__(256)
     k_transfer(const XferDev *__restrict__ xfers, const VisitDev *__restrict__ visits,
-               const SubDev *__restrict__ subs, int nsub, int nrhs, int dim, Flags F,
+               const SubDev *__restrict__ subs, int nsub, int nrhs, int dim_unused, Flags F,
                int *const *__restrict__ flag_bases, int nsweeps) {
+  constexpr int dim = DIM, NP = 1 + 2 * DIM;  // stencil points
   const XferDev &X = xfers[blockIdx.y];
   const VisitDev &V = visits[X.vidx];
   const int sweep = V.sweep;  // a launch may hold visits of several sweeps
@@ -514,8 +515,9 @@ __global__ void __launch_bounds__(256)
     snlo[a] = sn.win_lo[a];
   }
   const int nodes = X.band_shape[0] * X.band_shape[1] * (dim == 3 ? X.band_shape[2] : 1);
-  // acc[j] += coef * (w(p) - 1) v_j(p), w = prod_a fac_a(p_a) on ext
-  auto add_w = [&](cplx(&acc)[RV], cplx coef, const int (&p)[3]) {
+  // (w(p) - 1) and the V.x column pointer of stencil point p (w = prod_a
+  // fac_a(p_a) on ext)
+  auto point = [&](const int (&p)[3], double &wm1, const cplx *&vp) {
     double wt = 1.0;
     int c[3];
 #pragma unroll
@@ -523,9 +525,8 @@ __global__ void __launch_bounds__(256)
       if (a < dim) wt = wt * X.fac[a][p[a] - elo[a]];
       c[a] = a < dim ? p[a] - swlo[a] : 0;
     }
-    const cplx *vp = V.x + (int64_t)block_off(fs, c) * nrhs + rl;
-#pragma unroll
-    for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(coef, cscale(vp[j * lpn], wt - 1.0)));
+    wm1 = wt - 1.0;
+    vp = V.x + (int64_t)block_off(fs, c) * nrhs + rl;
   };
   for (int node = blockIdx.x * npb + ln; node < nodes; node += gridDim.x * npb) {
     int e[3], g[3], cn[3];
@@ -535,50 +536,78 @@ __global__ void __launch_bounds__(256)
       g[a] = a < dim ? blo[a] + e[a] : 0;
       cn[a] = a < dim ? g[a] - snlo[a] : 0;
     }
-    // the centre term: (k2 - sum_a (lo_a + hi_a)) * w0, accumulated in the
-    // same order as the one-RHS kernel: k2*w0, then per axis -(lo+hi)*w0,
-    // lo*w(p-e_a), hi*w(p+e_a)
-    double wt0 = 1.0;
-    int c0[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a < dim) wt0 = wt0 * X.fac[a][g[a] - elo[a]];
-      c0[a] = a < dim ? g[a] - swlo[a] : 0;
-    }
-    const cplx *v0 = V.x + (int64_t)block_off(fs, c0) * nrhs + rl;
-    cplx w0[RV], acc[RV];
-    const double k2 = op_k2(on, cn);
-#pragma unroll
-    for (int j = 0; j < RV; ++j) {
-      w0[j] = cscale(v0[j * lpn], wt0 - 1.0);
-      acc[j] = cscale(w0[j], k2);
-    }
+    // phase 1: every load of the node is issued before any arithmetic (the
+    // gathers of the 2*dim+1 stencil points, couplings, rhs and slot);
+    // neighbours outside ext load the centre and are skipped in phase 2
+    double wm[NP];
+    const cplx *vp[NP];
+    bool ok[NP];
+    point(g, wm[0], vp[0]);
+    ok[0] = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (a >= dim) break;
-      const cplx lo = on.c_lo[a][cn[a]], hi = on.c_hi[a][cn[a]];
-      const cplx mlh = make_double2(-(lo.x + hi.x), -(lo.y + hi.y));
-#pragma unroll
-      for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(mlh, w0[j]));
-      if (g[a] - 1 >= elo[a]) {
-        int p[3] = {g[0], g[1], g[2]};
-        p[a] -= 1;
-        add_w(acc, lo, p);
-      }
-      if (g[a] + 1 < ehi[a]) {
-        int p[3] = {g[0], g[1], g[2]};
-        p[a] += 1;
-        add_w(acc, hi, p);
-      }
+      int pm[3] = {g[0], g[1], g[2]}, pp[3] = {g[0], g[1], g[2]};
+      pm[a] -= 1;
+      pp[a] += 1;
+      ok[1 + 2 * a] = g[a] - 1 >= elo[a];
+      ok[2 + 2 * a] = g[a] + 1 < ehi[a];
+      if (ok[1 + 2 * a]) point(pm, wm[1 + 2 * a], vp[1 + 2 * a]);
+      else { wm[1 + 2 * a] = 0.0; vp[1 + 2 * a] = vp[0]; }
+      if (ok[2 + 2 * a]) point(pp, wm[2 + 2 * a], vp[2 + 2 * a]);
+      else { wm[2 + 2 * a] = 0.0; vp[2 + 2 * a] = vp[0]; }
     }
+    cplx v[NP][RV];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+#pragma unroll
+      for (int j = 0; j < RV; ++j) v[q][j] = vp[q][j * lpn];
+    }
+    cplx lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dim) break;
+      lo[a] = on.c_lo[a][cn[a]];
+      hi[a] = on.c_hi[a][cn[a]];
+    }
+    const double k2 = op_k2(on, cn);
     int cs[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) cs[a] = a < dim ? g[a] - swlo[a] : 0;
     const cplx *rv = V.rhs + (int64_t)block_off(fs, cs) * nrhs + rl;
     cplx *sp = X.slot + (int64_t)node * nrhs + rl;
+    cplx rvv[RV], spv[RV];
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      rvv[j] = rv[j * lpn];
+      spv[j] = sp[j * lpn];
+    }
+    // phase 2: the centre term k2*w0, then per axis -(lo+hi)*w0, lo*w(p-e_a),
+    // hi*w(p+e_a) -- the same order as before the load hoisting
+    cplx w0[RV], acc[RV];
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      w0[j] = cscale(v[0][j], wm[0]);
+      acc[j] = cscale(w0[j], k2);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dim) break;
+      const cplx mlh = make_double2(-(lo[a].x + hi[a].x), -(lo[a].y + hi[a].y));
+#pragma unroll
+      for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(mlh, w0[j]));
+      if (ok[1 + 2 * a]) {
+#pragma unroll
+        for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(lo[a], cscale(v[1 + 2 * a][j], wm[1 + 2 * a])));
+      }
+      if (ok[2 + 2 * a]) {
+#pragma unroll
+        for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(hi[a], cscale(v[2 + 2 * a][j], wm[2 + 2 * a])));
+      }
+    }
 #pragma unroll
     for (int j = 0; j < RV; ++j)
-      if (emit[j]) sp[j * lpn] = cadd(sp[j * lpn], cscale(cadd(rv[j * lpn], acc[j]), X.sign));
+      if (emit[j]) sp[j * lpn] = cadd(spv[j], cscale(cadd(rvv[j], acc[j]), X.sign));
   }
   if (flag_bases) __threadfence_system();  // sharded: peer-memory payloads before the barrier
 }
@@ -1116,12 +1145,24 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (nx > 0) {
         prof_mark(P, 3, st);
         int bz = std::max(1, std::min(64, 2 * cap / nx));
-        if (nrhs % 4 == 0)
-          k_transfer<4><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      nrhs, dim, F, P->d_flag_bases, P->nsweeps);
-        else
-          k_transfer<1><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub,
-                                                      nrhs, dim, F, P->d_flag_bases, P->nsweeps);
+        static const int k4rv = [] {
+          const char *v = getenv("DS_K4_RV");  // 1 measured fastest (config 2: 1.32 vs 1.51-1.59 ms)
+          return v && *v ? atoi(v) : 1;
+        }();
+#define K4_LAUNCH(RV_, D_)                                                                       \
+  k_transfer<RV_, D_><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, \
+                                                    nrhs, dim, F, P->d_flag_bases, P->nsweeps)
+        const int rv = (k4rv == 4 && nrhs % 4 == 0) ? 4 : ((k4rv >= 2 && nrhs % 2 == 0) ? 2 : 1);
+        if (dim == 2) {
+          if (rv == 4) K4_LAUNCH(4, 2);
+          else if (rv == 2) K4_LAUNCH(2, 2);
+          else K4_LAUNCH(1, 2);
+        } else {
+          if (rv == 4) K4_LAUNCH(4, 3);
+          else if (rv == 2) K4_LAUNCH(2, 3);
+          else K4_LAUNCH(1, 3);
+        }
+#undef K4_LAUNCH
         ctx->launches++;
         DS_CHECK_LAUNCH();
       }
