@@ -460,7 +460,8 @@ def run_reference(args):
     return {
         "impl": "reference", "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2
         else f"Helmholtz RHS/s ({s.name})",
-        "value": value, "unit": "RHS/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "RHS/s", "n_gpus": args.gpus, "device": "host CPU (rank 0)",
+        "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ts * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (seeded, SURVEY §8(d))",
         "config": {"workload": s.name,
