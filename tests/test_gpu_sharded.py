@@ -87,3 +87,17 @@ def test_distributed_sharded_world1(cuda):
         assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) <= 1e-12
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_3d_staged_path(cuda):
+    """Sharding on the 3D staged solve (K2b + K3g): 2x2x2 subdomains, 2 ranks."""
+    s = configs.Spec("mini-3d", ((0.0, 1.0),) * 3, (24, 24, 24), 4, 4, (2, 2, 2), 2 * np.pi * 3,
+                     1, "direct", "constant", 9, centers=((0.3, 0.55, 0.4),))
+    b = configs.build(s)
+    part, ops = b["partition"], b["ops"]
+    f = configs.sources(s, b["grid"])[:1]
+    fd = torch.from_numpy(f.reshape(1, -1)).cuda()
+    u_ref, _ = device_plan(part, ops, FactorizationCache(), None, 1).apply(fd)
+    sh = ShardedSweep(part, ops, 2, 1)
+    u = sh.apply(fd)
+    assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) <= 1e-12
