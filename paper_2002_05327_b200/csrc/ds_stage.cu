@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "ds_common.cuh"
+#include "ds_mma.cuh"
 
 #define ST_THREADS 256
 #define ST_ROWS 32   // rows of the block inverse per CTA
@@ -155,6 +156,102 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
   }
 }
 
+// K3g on the FP64 tensor cores.  ncu on config 4 showed k_stage_gemv bound
+// by L1/shared-memory throughput (92% L1TEX, shared wavefronts 74% of peak,
+// DRAM 35%): every streamed factor element was multiplied with 8 RHS values
+// read from shared memory.  Here each warp owns an 8-row x 8-RHS tile over the
+// whole K: the factor rows are streamed from HBM as DMMA A fragments (8 loads
+// in flight per thread), the block vector is read from shared memory once per
+// k-step as the B fragment, and the complex product uses 3 real m8n8k4 DMMAs.
+#define SM_WARPS 8
+#define SM_KC 128  // vin rows per shared-memory chunk (x2 buffers)
+__global__ void __launch_bounds__(32 * SM_WARPS, 2)
+    k_stage_gemv_mma(const StageItem *__restrict__ items, int nrhs, const cplx *vin_all,
+                     size_t vin_stride) {
+  const StageItem &I = items[blockIdx.y];
+  const int m = I.m;
+  const int r0 = blockIdx.x * (8 * SM_WARPS);
+  if (r0 >= m) return;
+  const int c0 = blockIdx.z * ST_RC;
+  const int rcc = min(ST_RC, nrhs - c0);
+  if (rcc <= 0) return;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+  const int row = r0 + warp * 8 + g;  // A-fragment row of this lane
+  const bool rvalid = row < m;
+  const size_t ldx = nrhs;
+  const cplx *A = I.f->sinv + ((size_t)I.k * m) * m + (size_t)(rvalid ? row : 0) * m;
+  const cplx *vg = vin_all + blockIdx.y * vin_stride;
+  __shared__ __align__(16) cplx vin[2][SM_KC][ST_RC];
+  double p1[2] = {0.0, 0.0}, p2[2] = {0.0, 0.0}, p3[2] = {0.0, 0.0};
+  auto prefetch = [&](int chunk) {
+    const int j0 = chunk * SM_KC, jn = min(SM_KC, m - j0);
+    cplx(*dst)[ST_RC] = vin[chunk & 1];
+    for (int e = t; e < SM_KC * ST_RC; e += 32 * SM_WARPS) {
+      const int jj = e / ST_RC, c = e % ST_RC;
+      if (jj < jn && c < rcc) st_cp_async16(&dst[jj][c], vg + (size_t)(j0 + jj) * ldx + c0 + c);
+      else dst[jj][c] = make_double2(0.0, 0.0);  // K tail and RHS tail read as zero
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  const int nchunk = (m + SM_KC - 1) / SM_KC;
+  prefetch(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int j0 = ch * SM_KC, jn = min(SM_KC, m - j0);
+    if (ch + 1 < nchunk) {
+      prefetch(ch + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    cplx(*V)[ST_RC] = vin[ch & 1];
+    const int nks = (jn + 3) >> 2;
+    for (int kg = 0; kg < nks; kg += 8) {
+      cplx a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // 8 independent factor loads in flight
+        const int kk = (kg + u) * 4 + tg;
+        a[u] = (rvalid && kg + u < nks && kk < jn) ? __ldcs(A + j0 + kk) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (kg + u >= nks) break;
+        const cplx b = V[(kg + u) * 4 + tg][g];
+        const double as = a[u].x + a[u].y, bs = b.x + b.y;
+        dmma(p1, a[u].x, b.x);
+        dmma(p2, a[u].y, b.y);
+        dmma(p3, as, bs);
+      }
+    }
+    __syncthreads();  // buffer ch&1 is refilled two chunks later
+  }
+  // C fragment: row r0 + 8 warp + g, columns 2 tg, 2 tg + 1 of the chunk
+  const int orow = r0 + warp * 8 + g;
+  if (orow < m) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 2 * tg + e;
+      if (c >= rcc) continue;
+      const cplx acc = make_double2(p1[e] - p2[e], p3[e] - p1[e] - p2[e]);
+      const size_t off = ((size_t)I.k * m + orow) * ldx + c0 + c;
+      if (I.kind == 2) {
+        cplx aux = I.x[off];  // y_k / z_k from the forward pass
+        I.x[off] = csub(aux, cmul(I.ecoef, acc));
+      } else {
+        I.x[off] = acc;
+      }
+    }
+  }
+}
+
+static bool stage_mma_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("DS_K3G_MMA");
+    return !(v && *v == '0');
+  }();
+  return on;
+}
+
 // host: the twisted schedule of one visit
 static bool stage_item(const FactDev &f, int s, int half, StageItem &I) {
   const int nb = f.nb, tw = f.twist, nt = tw, nbt = nb - 1 - tw;
@@ -248,8 +345,14 @@ int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const Fac
     if (!n) continue;
     int vb = (int)std::min<int64_t>(256, ((int64_t)mmax * nrhs + 255) / 256);
     k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
-    dim3 grid((mmax + ST_ROWS - 1) / ST_ROWS, n, nchunks);
-    k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
+    if (stage_mma_enabled()) {
+      dim3 grid((mmax + 8 * SM_WARPS - 1) / (8 * SM_WARPS), n, nchunks);
+      k_stage_gemv_mma<<<grid, 32 * SM_WARPS, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all,
+                                                                vin_stride);
+    } else {
+      dim3 grid((mmax + ST_ROWS - 1) / ST_ROWS, n, nchunks);
+      k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
+    }
     ctx->launches += 2;
   }
   DS_CHECK_LAUNCH();
@@ -506,8 +609,13 @@ int ds_stage_program_launch_step(ds_ctx *ctx, StageProgram *P, int step, int nrh
         return ds_fail(DS_ECONFIG, "stage program: vin scratch too small");
       int vb = (int)std::min<int64_t>(256, ((int64_t)m * nrhs + 255) / 256);
       k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
-      dim3 grid((m + ST_ROWS - 1) / ST_ROWS, n, (nrhs + ST_RC - 1) / ST_RC);
-      k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
+      if (stage_mma_enabled()) {
+        dim3 grid((m + 8 * SM_WARPS - 1) / (8 * SM_WARPS), n, (nrhs + ST_RC - 1) / ST_RC);
+        k_stage_gemv_mma<<<grid, 32 * SM_WARPS, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
+      } else {
+        dim3 grid((m + ST_ROWS - 1) / ST_ROWS, n, (nrhs + ST_RC - 1) / ST_RC);
+        k_stage_gemv<<<grid, ST_THREADS, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
+      }
       ctx->launches += 2;
     }
   }

@@ -12,7 +12,9 @@ from paper_2002_05327_b200.ddm import SweepPlan, device_plan
 s = configs.spec(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 b = configs.build(s)
 f = configs.sources(s, b["grid"])
-cache = FactorizationCache()
+part0 = b["partition"]
+# 3D constant media: translation classes share factorizations (bench.py does the same)
+cache = FactorizationCache(share_translates=part0.dim == 3 and s.medium == "constant")
 dp = device_plan(b["partition"], b["ops"], cache, SweepPlan.default(b["partition"].dim), f.shape[0])
 dp.enable_graph(False)
 fd = torch.from_numpy(f.reshape(f.shape[0], -1)).cuda()
