@@ -165,7 +165,13 @@ __global__ void __launch_bounds__(ST_THREADS, 3)
 // k-step as the B fragment, and the complex product uses 3 real m8n8k4 DMMAs.
 #define SM_WARPS 8
 #define SM_KC 128  // vin rows per shared-memory chunk (x2 buffers)
-__global__ void __launch_bounds__(32 * SM_WARPS, 2)
+#ifndef SM_DEPTH
+#define SM_DEPTH 8  // factor k-steps loaded per batch (loads in flight per thread)
+#endif
+#ifndef SM_MINB
+#define SM_MINB 3  // measured best (config 4: 10.0 vs 9.8 RHS/s at 2, 8.3 with 16-deep)
+#endif
+__global__ void __launch_bounds__(32 * SM_WARPS, SM_MINB)
     k_stage_gemv_mma(const StageItem *__restrict__ items, int nrhs, const cplx *vin_all,
                      size_t vin_stride) {
   const StageItem &I = items[blockIdx.y];
@@ -206,15 +212,15 @@ __global__ void __launch_bounds__(32 * SM_WARPS, 2)
     __syncthreads();
     cplx(*V)[ST_RC] = vin[ch & 1];
     const int nks = (jn + 3) >> 2;
-    for (int kg = 0; kg < nks; kg += 8) {
-      cplx a[8];
+    for (int kg = 0; kg < nks; kg += SM_DEPTH) {
+      cplx a[SM_DEPTH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // 8 independent factor loads in flight
+      for (int u = 0; u < SM_DEPTH; ++u) {  // SM_DEPTH independent factor loads in flight
         const int kk = (kg + u) * 4 + tg;
         a[u] = (rvalid && kg + u < nks && kk < jn) ? __ldcs(A + j0 + kk) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < SM_DEPTH; ++u) {
         if (kg + u >= nks) break;
         const cplx b = V[(kg + u) * 4 + tg][g];
         const double as = a[u].x + a[u].y, bs = b.x + b.y;
