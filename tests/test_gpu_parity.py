@@ -494,3 +494,22 @@ def test_many_rhs_chunking(cuda, cfg1):
                                  warn_collar=False)
     want = np.einsum("rk,k...->r...", coef, ub.values)
     assert np.linalg.norm(u.values - want) / np.linalg.norm(want) < 1e-10
+
+
+@pytest.mark.parametrize("nrhs", [1, 5, 17, 33])
+def test_ragged_rhs_counts(cuda, cfg1, nrhs):
+    """RHS counts that leave partial DMMA tiles and ragged RHS chunks (K3
+    chunks of 16, step kernels with 1- and 4-column lanes): every RHS equals
+    the same combination of three solved bases (the map is linear)."""
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(40 + nrhs)
+    counts = b["grid"].counts
+    base = rng.standard_normal((3,) + counts) + 1j * rng.standard_normal((3,) + counts)
+    coef = rng.standard_normal((nrhs, 3)) + 1j * rng.standard_normal((nrhs, 3))
+    batch = np.einsum("rk,k...->r...", coef, base)
+    cache = FactorizationCache()
+    u, reps = diagonal_sweep_solve(batch, b["partition"], b["ops"], cache, warn_collar=False)
+    ub, _ = diagonal_sweep_solve(base, b["partition"], b["ops"], cache, warn_collar=False)
+    want = np.einsum("rk,k...->r...", coef, ub.values)
+    assert len(reps) == nrhs
+    assert np.linalg.norm(u.values - want) / np.linalg.norm(want) < 1e-10
