@@ -1647,7 +1647,12 @@ static size_t solve8_smem(int m, int rc, int C, int nw = 4) {
   size_t rows_max = r + (r & 1);
   size_t rows_alloc = (rows_max + 7) & ~(size_t)7;
   size_t elems = 4 * ((size_t)m * rc + 2) + 2 * FAC_STAGES * (rows_alloc * m + 2) + 2 * (size_t)nw * rows_max * rc;
-  return std::max<size_t>(256 + elems * sizeof(cplx), 118 * 1024);
+  // floor: one CTA per SM (DS_K3_SMEM_FLOOR=0 lets two small CTAs share an SM)
+  static const size_t floor_b = [] {
+    const char *v = getenv("DS_K3_SMEM_FLOOR");
+    return v && *v ? (size_t)atol(v) : (size_t)118 * 1024;
+  }();
+  return std::max<size_t>(256 + elems * sizeof(cplx), floor_b);
 }
 
 static size_t solve7_smem(int m, int rc, int C) {
@@ -1804,7 +1809,7 @@ static bool pick_cluster_chunk(const void *fn, int threads, int nvisit, int nrhs
   static const int rc_max = std::max(1, env_int("DS_K3_RCMAX", 16));
   static const int c_only = env_int("DS_K3_CLUSTER", 0);
   int bestC = 0, bestRc = 0;
-  long best_waves = 0, best_work = 0;
+  long best_waves = 0, best_work = 0, best_waste = 0;
   for (int C : {16, 8}) {
     if (c_only && C != c_only) continue;
     const int rows = solve_rows_max(max_m, C);
@@ -1818,12 +1823,20 @@ static bool pick_cluster_chunk(const void *fn, int threads, int nvisit, int nrhs
       long ncl = (long)nvisit * ((nrhs + rc - 1) / rc);
       long waves = (ncl + maxcl - 1) / maxcl;
       long work = waves * (long)rows * rc;
-      if (!bestC || waves < best_waves || (waves == best_waves && work < best_work) ||
-          (waves == best_waves && work == best_work && C > bestC)) {
+      // DMMA tile padding: rows and RHS are computed in 8 x 8 tiles
+      long waste = (long)((rows + 7) / 8 * 8) * ((rc + 7) / 8 * 8) - (long)rows * rc;
+      // ties (same waves and work per CTA): less padding, then the smaller
+      // cluster -- config 2 measured 8 CTAs x (16 rows, 8 RHS) faster than
+      // 16 CTAs x (8 rows, 16 RHS): half as many CTAs in every exchange
+      bool better = !bestC || waves < best_waves || (waves == best_waves && work < best_work);
+      if (!better && waves == best_waves && work == best_work)
+        better = waste < best_waste || (waste == best_waste && C < bestC);
+      if (better) {
         bestC = C;
         bestRc = rc;
         best_waves = waves;
         best_work = work;
+        best_waste = waste;
       }
       if (rc == 1) break;
     }
@@ -1966,7 +1979,7 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   // step in the fewest waves of co-resident clusters, then with the least
   // arithmetic per CTA and stage (rows per CTA x chunk width).
   int bestC = 0, bestRc = 0;
-  long best_waves = 0, best_work = 0;
+  long best_waves = 0, best_work = 0, best_waste = 0;
   for (int C : {16, 8}) {
     if (c_only && C != c_only) continue;
     const int rows = solve_rows_max(max_m, C);
@@ -1980,12 +1993,20 @@ static int launch_v5(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
       long ncl = (long)nvisit * ((nrhs + rc - 1) / rc);
       long waves = (ncl + maxcl - 1) / maxcl;
       long work = waves * (long)rows * rc;
-      if (!bestC || waves < best_waves || (waves == best_waves && work < best_work) ||
-          (waves == best_waves && work == best_work && C > bestC)) {
+      // DMMA tile padding: rows and RHS are computed in 8 x 8 tiles
+      long waste = (long)((rows + 7) / 8 * 8) * ((rc + 7) / 8 * 8) - (long)rows * rc;
+      // ties (same waves and work per CTA): less padding, then the smaller
+      // cluster -- config 2 measured 8 CTAs x (16 rows, 8 RHS) faster than
+      // 16 CTAs x (8 rows, 16 RHS): half as many CTAs in every exchange
+      bool better = !bestC || waves < best_waves || (waves == best_waves && work < best_work);
+      if (!better && waves == best_waves && work == best_work)
+        better = waste < best_waste || (waste == best_waste && C < bestC);
+      if (better) {
         bestC = C;
         bestRc = rc;
         best_waves = waves;
         best_work = work;
+        best_waste = waste;
       }
       if (rc == 1) break;
     }
