@@ -42,7 +42,7 @@ def tables(cfg):
     return len(plan), len(subs), order, xfer_use, dirs, sub_index
 
 
-@pytest.mark.parametrize("cfg,cap,expect", [(2, 7, 50), (1, 7, None), (4, 10**6, 50)])
+@pytest.mark.parametrize("cfg,cap,expect", [(2, 7, 50), (2, 8, 46), (1, 7, None), (4, 10**6, 50)])
 def test_launch_schedule_respects_dependencies(cfg, cap, expect):
     nsw, nsub, order, xu, dirs, sub_index = tables(cfg)
     launches = launch_schedule(nsw, nsub, order, xu, dirs, sub_index, None, cap)
