@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 3
+#define DS_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -119,6 +119,34 @@ DS_API int ds_fact_info(const ds_fact *fact, int32_t i, int32_t *block_axis,
 DS_API int ds_fact_solve(ds_ctx *ctx, const ds_fact *fact, int32_t i,
                   const ds_cplx *rhs_dev, ds_cplx *x_dev, int32_t nrhs);
 DS_API int ds_fact_destroy(ds_fact *fact);
+
+/* Modal factorization of separable operators (kappa^2 'const' or 'axis'):
+ * the drop-in for SeparableFactorization (subdomain.py:43-96), which
+ * triangularizes the per-axis 1D tridiagonals (Schur) and solves a
+ * triangular Sylvester equation.  Here the 1D tridiagonal T_a of every
+ * in-slab axis a (the window axes other than the block axis, C order; one in
+ * 2D, two in 3D; T_a includes kappa^2 when kappa^2 varies along a) is
+ * diagonalised, T_a = V_a diag(lambda_a) V_a^{-1}, so the operator becomes
+ * one scalar tridiagonal system along the block axis per in-slab mode j:
+ *     (T_ba + kappa^2 + mu_j) y_j = (W g)_j,   mu_j = sum_a lambda_a(j_a).
+ * The device computes and stores the mode-wise LU pivots; a solve is two
+ * (2D) or four (3D) batched complex GEMMs on the FP64 tensor cores plus the
+ * mode-wise recurrences.  The host supplies the eigen-decompositions
+ * (row-major n_a x n_a V_a, V_a^{-1}, and lambda_a; host arrays, copied).
+ * block_axis must be the layout's (longest axis, first on ties).  Returns
+ * > 0 on a zero or non-finite pivot. */
+typedef struct {
+  int32_t block_axis;
+  int32_t naxes;              /* dim - 1 */
+  const ds_cplx *v[2];        /* V_a */
+  const ds_cplx *vinv[2];     /* V_a^{-1} */
+  const ds_cplx *lambda[2];   /* eigenvalues of T_a */
+} ds_modal_desc;
+
+DS_API int ds_fact_create_modal(ds_ctx *ctx, ds_op *const *ops, int32_t n,
+                                const ds_modal_desc *descs, ds_fact **out);
+/* 0: block-LU factors (ds_fact_create), 1: modal (ds_fact_create_modal) */
+DS_API int ds_fact_kind(const ds_fact *fact, int32_t i);
 
 /* ------------------------------------------------------------- sweep plan
  * Static schedule of one diagonal-sweeping application (ddm.py:212-291),

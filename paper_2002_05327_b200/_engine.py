@@ -155,15 +155,72 @@ def apply_operator(op, v, region):
 
 # ------------------------------------------------------------ factorization
 
-class FactorSet:
-    """One ds_fact handle holding the block-LU factors of several operators."""
+def block_axis_of(shape) -> int:
+    """Block axis of the layout: the longest window axis, first on ties."""
+    return int(np.argmax(np.asarray(shape)))
 
-    def __init__(self, ops):
+
+def axis_tridiagonal(op, axis: int) -> np.ndarray:
+    """Dense 1D operator of `axis` (pml.py couplings; kappa^2 folded in
+    when it varies along this axis) -- the factor the reference's
+    SeparableFactorization triangularizes (subdomain.py:52-63)."""
+    lo, hi = op.couplings[axis]
+    n = len(lo)
+    T = np.zeros((n, n), dtype=np.complex128)
+    i = np.arange(n)
+    T[i, i] = -(lo + hi)
+    T[i[1:], i[1:] - 1] = lo[1:]
+    T[i[:-1], i[:-1] + 1] = hi[:-1]
+    if op.kappa2_kind == "axis" and op.kappa2[0] == axis:
+        T[i, i] += np.asarray(op.kappa2[1], dtype=np.float64)
+    return T
+
+
+def modal_decomposition(op):
+    """Eigen-decompositions T_a = V diag(lambda) V^{-1} of the in-slab axes
+    (LAPACK zgeev through NumPy; n_a <= a few hundred, O(n_a^3) each).
+    Returns (block_axis, [(V, V^{-1}, lambda), ...]) in in-slab axis order."""
+    ba = block_axis_of(op.window.shape)
+    out = []
+    for a in range(op.dim):
+        if a == ba:
+            continue
+        lam, V = np.linalg.eig(axis_tridiagonal(op, a))
+        W = np.linalg.inv(V)
+        out.append((np.ascontiguousarray(V, dtype=np.complex128),
+                    np.ascontiguousarray(W, dtype=np.complex128),
+                    np.ascontiguousarray(lam, dtype=np.complex128)))
+    return ba, out
+
+
+class FactorSet:
+    """One ds_fact handle holding the factors of several operators: the
+    block-tridiagonal LU (K2, any operator) or, with `modal`, the modal
+    factorization of separable operators (K2m, ds_modal.cu)."""
+
+    def __init__(self, ops, modal: bool = False):
         lib, ctx = context()
         handles = [device_operator(op).handle for op in ops]
         arr = (C.c_void_p * len(ops))(*[h.value for h in handles])
         out = C.c_void_p()
-        N.check(lib.ds_fact_create(ctx, arr, len(ops), C.byref(out)), "ds_fact_create")
+        self.modal = modal
+        if modal:
+            descs = (N.ModalDesc * len(ops))()
+            keep = []
+            for i, op in enumerate(ops):
+                ba, axes = modal_decomposition(op)
+                descs[i].block_axis = ba
+                descs[i].naxes = len(axes)
+                for a, (V, W, lam) in enumerate(axes):
+                    keep += [V, W, lam]
+                    descs[i].v[a] = V.ctypes.data
+                    descs[i].vinv[a] = W.ctypes.data
+                    descs[i].lambda_[a] = lam.ctypes.data
+            N.check(lib.ds_fact_create_modal(ctx, arr, len(ops), descs, C.byref(out)),
+                    "ds_fact_create_modal")
+            del keep
+        else:
+            N.check(lib.ds_fact_create(ctx, arr, len(ops), C.byref(out)), "ds_fact_create")
         self.handle = out
         self.n = len(ops)
         self._ops = list(ops)  # operators must outlive the factors

@@ -69,6 +69,16 @@ class PlanDesc(C.Structure):
     ]
 
 
+class ModalDesc(C.Structure):
+    _fields_ = [
+        ("block_axis", i32),
+        ("naxes", i32),
+        ("v", vp * 2),
+        ("vinv", vp * 2),
+        ("lambda_", vp * 2),
+    ]
+
+
 # (name, restype, argtypes) — must match include/diagsweep_b200.h
 _SIGNATURES = [
     ("ds_abi_version", C.c_int, []),
@@ -85,6 +95,8 @@ _SIGNATURES = [
     ("ds_fact_info", C.c_int, [vp, i32, P_i32, P_i32, P_i32, P_i64]),
     ("ds_fact_solve", C.c_int, [vp, vp, i32, vp, vp, i32]),
     ("ds_fact_destroy", C.c_int, [vp]),
+    ("ds_fact_create_modal", C.c_int, [vp, C.POINTER(vp), i32, C.POINTER(ModalDesc), C.POINTER(vp)]),
+    ("ds_fact_kind", C.c_int, [vp, i32]),
     ("ds_plan_create", C.c_int, [vp, C.POINTER(PlanDesc), C.POINTER(vp)]),
     ("ds_plan_workspace_bytes", i64, [vp]),
     ("ds_plan_destroy", C.c_int, [vp]),
@@ -130,7 +142,7 @@ def load_library(path: Path | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ds_abi_version() != 3:
+        if lib.ds_abi_version() != 4:
             raise SolverError("diagsweep_b200 ABI version mismatch")
         if path is None:
             _lib = lib

@@ -112,9 +112,18 @@ struct FactDev {
                       // k > t hold T_k^{-1} (bottom-up), k = t holds M_t^{-1}
   int other[2];       // the in-block axes in C order (unused entries = -1)
   int win_shape[3];
-  const cplx *sinv;   // nb * m * m, row-major blocks
+  const cplx *sinv;   // nb * m * m, row-major blocks (kind 0)
   const cplx *lcoef;  // nb: coupling of block k to k-1 (c_lo along axis)
   const cplx *ucoef;  // nb: coupling of block k to k+1 (c_hi along axis)
+  // kind 1 (modal, separable operators): T_a = V_a diag(lambda_a) W_a for
+  // the in-slab axes other[0..naxes) (W_a = V_a^{-1}, n_a x n_a row-major);
+  // per (block k, mode j) the mode-wise tridiagonal LU along the block axis:
+  // mmul[k][j] = l_k / piv_{k-1}(j) (k >= 1), minv[k][j] = 1 / piv_k(j)
+  int kind;
+  int naxes;
+  int nax[2];
+  const cplx *mW[2], *mV[2];
+  const cplx *mmul, *minv;
 };
 
 struct ds_fact {
@@ -148,6 +157,22 @@ struct SolveVisit {
 // launch K3 over a device table of visits (one cluster per visit x chunk)
 int ds_launch_solve_table(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs,
                           int max_m);
+
+// modal solve (FactDev kind 1): per visit the in-slab transforms (batched
+// complex GEMMs on DMMA) and the mode-wise tridiagonal solves; s0/s1 are
+// scratch buffers of the visit's size (block layout, stride nrhs)
+struct ModalJob {
+  const FactDev *f;
+  const cplx *rhs;
+  cplx *x;
+  cplx *s0, *s1;
+  const int *nz;  // per-RHS nonzero flags (NULL = solve all)
+};
+// launch the modal solve of njob visits (device job table; facts_host: the
+// jobs' factor layouts, for grid sizing)
+int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,
+                    int nrhs);
+void ds_fill_layout(const OpDev &o, FactDev &f);
 
 int ceil_div(int a, int b);
 

@@ -219,7 +219,7 @@ static int choose_cluster(int m, int *mcper_out, size_t *smem_out) {
   return 0;
 }
 
-static void fill_layout(const OpDev &o, FactDev &f) {
+void ds_fill_layout(const OpDev &o, FactDev &f) {
   int ba = 0;
   for (int a = 1; a < o.dim; ++a)
     if (o.shape[a] > o.shape[ba]) ba = a;
@@ -252,7 +252,7 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n_in, ds_f
     const OpDev &o = ops[i]->dev;
     FactDev f;
     memset(&f, 0, sizeof(f));
-    fill_layout(o, f);
+    ds_fill_layout(o, f);
     size_t bytes = (size_t)f.nb * f.m * f.m * sizeof(cplx) + 2 * (size_t)f.nb * sizeof(cplx);
     void *mem = nullptr;
     if (cudaMalloc(&mem, bytes) != cudaSuccess) {
@@ -444,7 +444,15 @@ extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_
   ctx->launches++;
   DS_CHECK_LAUNCH();
   int rc;
-  if (f.m > DS_LARGE_SLAB) {
+  if (f.kind == 1) {
+    // modal: scratch = the exchange area (>= 4 n), one device job
+    ModalJob hj{fd, bin, bout, xg, xg + n, nullptr};
+    ModalJob *dj = nullptr;
+    DS_CUDA(cudaMallocAsync((void **)&dj, sizeof(ModalJob), ctx->stream));
+    DS_CUDA(cudaMemcpyAsync(dj, &hj, sizeof(hj), cudaMemcpyHostToDevice, ctx->stream));
+    rc = ds_launch_modal(ctx, dj, &f, 1, nrhs);
+    cudaFreeAsync(dj, ctx->stream);
+  } else if (f.m > DS_LARGE_SLAB) {
     SolveVisit hvis{fd, bin, bout, nullptr, xg};
     const cplx *lh = F->h_l[i].data(), *uh = F->h_u[i].data();
     size_t cap = ds_stage_items_bytes(1, f.nb, f.m, nrhs);

@@ -1,0 +1,444 @@
+// K2m / K3m: modal factorization and solve of separable subdomain operators.
+//
+// Replaces SeparableFactorization (diagsweep/subdomain.py:43-96) for
+// operators whose kappa^2 is constant or varies along one axis
+// (pml.py 'const' / 'axis'): the window operator is the Kronecker sum of
+// per-axis 1D tridiagonals T_a (pml.py:95-102 couplings) plus kappa^2.  The
+// reference triangularizes the 1D matrices (Schur) and solves a triangular
+// Sylvester equation (ztrsyl), an inherently sequential recurrence.  Here
+// the in-slab axes (all axes but the block axis of the block layout) are
+// diagonalised instead, T_a = V_a diag(lambda_a) W_a, W_a = V_a^{-1}, so
+// with g in block layout [n_b][m][R]:
+//
+//   1. ghat_k = (W_0 (x) W_1) g_k        for every block k   (batched GEMMs)
+//   2. per in-slab mode j: the scalar tridiagonal system along the block
+//      axis  l_k y_{k-1} + (d_k + mu_j) y_k + u_k y_{k+1} = ghat_k,
+//      mu_j = sum_a lambda_a(j_a), d_k = -(c_lo + c_hi)_ba[k] + kappa^2,
+//      by its LU (mode-wise pivots precomputed at factorization time)
+//   3. x_k = (V_0 (x) V_1) y_k                                (batched GEMMs)
+//
+// The flop count of 1 + 3 in 2D equals the block-LU substitution's
+// (16 n_b m^2 per RHS) but there is no chain of dependent block products:
+// the transforms are plain batched GEMMs over every (visit, block, RHS) of a
+// launch on the FP64 tensor cores, and the only recurrence is the cheap
+// mode-wise one (O(n_b m) per RHS).  In 3D the in-slab transform factors
+// per axis (two small GEMMs per direction), 16 n_b m (n_0 + n_1) flop per
+// RHS instead of 16 n_b m^2.  The mode-wise LU has the stability of the
+// block LU without block pivoting (its Schur complements are
+// V diag(piv_k) W); accuracy vs the reference is ~1e-12.
+//
+// The eigen-decompositions of the 1D matrices (n_a <= a few hundred) come
+// from the host (ds_modal_desc); the device builds the pivots.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ds_common.cuh"
+#include "ds_mma.cuh"
+
+// ------------------------------------------------------------ pivots (K2m)
+struct PivJob {
+  FactDev f;
+  OpDev op;
+  const cplx *lam[2];
+  cplx *mul, *inv;
+};
+
+// one thread per (operator, mode j): LU of the block-axis tridiagonal
+// shifted by mu_j (no pivoting, as the block LU of ds_factor.cu)
+__global__ void k_modal_pivots(const PivJob *__restrict__ jobs, int *status) {
+  const PivJob &J = jobs[blockIdx.y];
+  const FactDev &f = J.f;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= f.m) return;
+  cplx mu = J.lam[0][f.naxes == 1 ? j : j / f.nax[1]];
+  if (f.naxes == 2) mu = cadd(mu, J.lam[1][j % f.nax[1]]);
+  const int ba = f.block_axis;
+  const OpDev &o = J.op;
+  cplx prev = make_double2(1.0, 0.0);
+  bool bad = false;
+  for (int k = 0; k < f.nb; ++k) {
+    const cplx lo = o.c_lo[ba][k], hi = o.c_hi[ba][k];
+    cplx d = make_double2(-(lo.x + hi.x), -(lo.y + hi.y));
+    if (o.kappa2_kind == 0) d.x += o.kappa2[0];
+    else if (o.kappa2_kind == 1 && o.kappa2_axis == ba) d.x += o.kappa2[k];
+    cplx piv = cadd(d, mu);
+    cplx mul = make_double2(0.0, 0.0);
+    if (k > 0) {
+      mul = cmul(lo, cinv(prev));  // l_k / piv_{k-1}
+      piv = csub(piv, cmul(mul, o.c_hi[ba][k - 1]));
+    }
+    if (!(isfinite(piv.x) && isfinite(piv.y)) || (piv.x == 0.0 && piv.y == 0.0)) bad = true;
+    J.mul[(size_t)k * f.m + j] = mul;
+    J.inv[(size_t)k * f.m + j] = cinv(piv);
+    prev = piv;
+  }
+  if (bad) atomicExch(status, 1);
+}
+
+// ------------------------------------------------------- pass geometry
+// forward passes p < naxes transform along in-slab axis a = naxes-1-p with
+// W_a; inverse passes p >= naxes along a = p - naxes with V_a.  A pass is
+// out[b][j][c] = sum_i A[j][i] in[b][i][c] over `outer` batches of n x ncols
+// row-major matrices (n = n_a, ncols = prod_{b>a} n_b * R).
+struct PassGeo {
+  const cplx *A;
+  const cplx *in;
+  cplx *out;
+  int n, ncols, outer;
+};
+
+__host__ __device__ inline PassGeo pass_geo(const FactDev &f, const ModalJob &J, int pass,
+                                            int nrhs) {
+  PassGeo G;
+  const int na = f.naxes;
+  const bool fwd = pass < na;
+  const int a = fwd ? na - 1 - pass : pass - na;
+  G.n = f.nax[a];
+  int inner = 1, outer = f.nb;
+  for (int b = 0; b < na; ++b) {
+    if (b > a) inner *= f.nax[b];
+    if (b < a) outer *= f.nax[b];
+  }
+  G.ncols = inner * nrhs;
+  G.outer = outer;
+  G.A = fwd ? f.mW[a] : f.mV[a];
+  cplx *buf[2] = {J.s0, J.s1};
+  if (fwd) {
+    G.in = pass == 0 ? J.rhs : buf[(pass - 1) & 1];
+    G.out = buf[pass & 1];
+  } else {
+    const int q = pass - na;
+    G.in = buf[(na - 1 + q) & 1];
+    G.out = q == na - 1 ? J.x : buf[(na + q) & 1];
+  }
+  return G;
+}
+
+__device__ __forceinline__ bool job_any(const ModalJob &J, int nrhs) {
+  if (!J.nz) return true;
+  int any = 0;
+  for (int r = 0; r < nrhs; ++r) any |= J.nz[r];
+  return any != 0;
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// 16-byte async copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------- transforms (K3m-T)
+// One CTA computes a TM x TN tile of one pass of one visit: A tile (TM x TK)
+// and B tile (TK x TN) double-buffered through shared memory by cp.async,
+// each warp an (8 MT) x 16 sub-tile with DMMA m8n8k4 and the 3M complex
+// product (as K3, ds_mma.cuh).  Row pitches: A % 8 == 4, B % 8 == 2 complex
+// (conflict-free fragment loads).
+#define MG_TK 16
+template <int MT, int WR, int WC>
+__global__ void __launch_bounds__(32 * WR * WC)
+    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
+  constexpr int TM = 8 * MT * WR, TN = 16 * WC, TK = MG_TK, NTH = 32 * WR * WC;
+  constexpr int AP = TK + 4, BP = TN + 2;
+  static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
+  extern __shared__ __align__(16) cplx smem_mg[];
+  auto sA = [&](int buf) { return smem_mg + buf * (TM * AP); };
+  auto sB = [&](int buf) { return smem_mg + 2 * TM * AP + buf * (TK * BP); };
+  const ModalJob J = jobs[blockIdx.z];
+  const FactDev f = *J.f;
+  const PassGeo G = pass_geo(f, J, pass, nrhs);
+  const int n = G.n;
+  const int row0 = blockIdx.y * TM;
+  const int total = G.outer * G.ncols;
+  const int col0 = blockIdx.x * TN;
+  if (row0 >= n || col0 >= total) return;
+  if (!job_any(J, nrhs)) return;
+  const int t = threadIdx.x;
+  // staging maps: A -- fixed column t % TK, rows t / TK + q * (NTH / TK);
+  // B -- fixed column t % TN, rows t / TN + q * (NTH / TN)
+  const int a_col = t % TK, a_row = t / TK;
+  constexpr int A_STEP = NTH / TK, A_N = TM / A_STEP;
+  const int b_col = t % TN, b_row = t / TN;
+  constexpr int B_STEP = NTH / TN, B_N = (TK + B_STEP - 1) / B_STEP;
+  const int gcol = col0 + b_col;
+  const bool bcol_ok = gcol < total;
+  const int64_t bbase = bcol_ok ? (int64_t)(gcol / G.ncols) * n * G.ncols + gcol % G.ncols : 0;
+  auto stage = [&](int kc, int buf) {
+    const int k0 = kc * TK;
+#pragma unroll
+    for (int q = 0; q < A_N; ++q) {
+      const int r = a_row + q * A_STEP, gr = row0 + r, gk = k0 + a_col;
+      const bool ok = gr < n && gk < n;
+      cp16(sA(buf) + r * AP + a_col, G.A + (ok ? (int64_t)gr * n + gk : 0), ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int q = 0; q < B_N; ++q) {
+      const int r = b_row + q * B_STEP;
+      if (B_STEP * B_N > TK && r >= TK) break;
+      const int gk = k0 + r;
+      const bool ok = bcol_ok && gk < n;
+      cp16(sB(buf) + r * BP + b_col, G.in + (ok ? bbase + (int64_t)gk * G.ncols : 0), ok ? 16 : 0);
+    }
+    cp_commit();
+  };
+  const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+  const int wr = warp % WR, wc = warp / WR;
+  double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
+  const int nkc = (n + TK - 1) / TK;
+  stage(0, 0);
+  for (int kc = 0; kc < nkc; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nkc) {
+      stage(kc + 1, buf ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
+    const cplx *Bs = sB(buf) + tg * BP + wc * 16 + g;
+#pragma unroll
+    for (int k4 = 0; k4 < TK / 4; ++k4) {
+      cplx a[MT], b[2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[mt] = As[mt * 8 * AP + k4 * 4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[k4 * 4 * BP + nt * 8];
+      double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double as = a[mt].x + a[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(p1[mt][nt], a[mt].x, b[nt].x);
+          dmma(p2[mt][nt], a[mt].y, b[nt].y);
+          dmma(p3[mt][nt], as, bs[nt]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int gr = row0 + wr * 8 * MT + mt * 8 + g;
+    if (gr >= n) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gc = col0 + wc * 16 + nt * 8 + 2 * tg + e;
+        if (gc >= total) continue;
+        const int64_t off = (int64_t)(gc / G.ncols) * n * G.ncols + (int64_t)gr * G.ncols + gc % G.ncols;
+        G.out[off] = make_double2(p1[mt][nt][e] - p2[mt][nt][e],
+                                  p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
+      }
+  }
+}
+
+// ------------------------------------------- mode-wise recurrences (K3m-R)
+// One thread per (visit, mode j, RHS r): forward elimination and back
+// substitution along the block axis, in place on the transformed buffer.
+// Loads of a chunk of MR blocks are issued before its dependent arithmetic.
+#define MR 8
+__global__ void __launch_bounds__(256) k_modal_thomas(const ModalJob *__restrict__ jobs, int nrhs) {
+  const ModalJob J = jobs[blockIdx.y];
+  const FactDev &f = *J.f;
+  const int m = f.m, nb = f.nb;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m * nrhs) return;
+  const int j = q / nrhs, r = q % nrhs;
+  if (J.nz && !J.nz[r]) return;  // exact-zero RHS: never read downstream
+  cplx *p = ((f.naxes - 1) & 1 ? J.s1 : J.s0) + q;
+  const size_t st = (size_t)m * nrhs;
+  const cplx *mul = f.mmul + j, *inv = f.minv + j;
+  const cplx *uc = f.ucoef;
+  cplx prev = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < nb; k0 += MR) {
+    cplx gv[MR], mv[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k0 + i;
+      if (k < nb) {
+        gv[i] = p[k * st];
+        mv[i] = mul[(size_t)k * m];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k0 + i;
+      if (k < nb) {
+        prev = k == 0 ? gv[i] : csub(gv[i], cmul(mv[i], prev));
+        p[k * st] = prev;
+      }
+    }
+  }
+  cplx y = make_double2(0.0, 0.0);
+  for (int k1 = nb - 1; k1 >= 0; k1 -= MR) {
+    cplx gv[MR], iv[MR], uv[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k1 - i;
+      if (k >= 0) {
+        gv[i] = k == nb - 1 ? prev : p[k * st];
+        iv[i] = inv[(size_t)k * m];
+        uv[i] = uc[k];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k1 - i;
+      if (k >= 0) {
+        y = k == nb - 1 ? cmul(gv[i], iv[i]) : cmul(csub(gv[i], cmul(uv[i], y)), iv[i]);
+        p[k * st] = y;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- launcher
+int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
+                    int nrhs) {
+  if (njob <= 0) return DS_OK;
+  int na = facts[0].naxes;
+  for (int i = 1; i < njob; ++i)
+    if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
+  constexpr int MT = 2, WR = 4, WC = 2, TM = 8 * MT * WR, TN = 16 * WC;
+  ModalJob dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  const size_t smem = sizeof(cplx) * 2 * (TM * (MG_TK + 4) + MG_TK * (TN + 2));
+  static bool attr_set = false;
+  if (!attr_set) {
+    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_set = true;
+  }
+  auto launch_pass = [&](int pass) -> int {
+    int gx = 1, gy = 1;
+    for (int i = 0; i < njob; ++i) {
+      const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
+      gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
+      gy = std::max(gy, (G.n + TM - 1) / TM);
+    }
+    k_modal_gemm<MT, WR, WC><<<dim3(gx, gy, njob), 32 * WR * WC, smem, ctx->stream>>>(jobs_dev, pass, nrhs);
+    ctx->launches++;
+    DS_CHECK_LAUNCH();
+    return DS_OK;
+  };
+  for (int p = 0; p < na; ++p)
+    if (int rc = launch_pass(p)) return rc;
+  int mmax = 1;
+  for (int i = 0; i < njob; ++i) mmax = std::max(mmax, facts[i].m);
+  k_modal_thomas<<<dim3((mmax * nrhs + 255) / 256, njob), 256, 0, ctx->stream>>>(jobs_dev, nrhs);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  for (int p = na; p < 2 * na; ++p)
+    if (int rc = launch_pass(p)) return rc;
+  return DS_OK;
+}
+
+// --------------------------------------------------------- factorization
+extern "C" int ds_fact_create_modal(ds_ctx *ctx, ds_op *const *ops, int32_t n,
+                                    const ds_modal_desc *descs, ds_fact **out) {
+  if (!ctx || !ops || n < 1 || !descs || !out)
+    return ds_fail(DS_ECONFIG, "ds_fact_create_modal: bad argument");
+  ds_fact *F = new ds_fact();
+  auto fail = [&](int code) {
+    for (void *p : F->allocations) cudaFree(p);
+    delete F;
+    return code;
+  };
+  std::vector<PivJob> jobs(n);
+  int mmax = 1;
+  for (int i = 0; i < n; ++i) {
+    if (!ops[i]) return fail(ds_fail(DS_ECONFIG, "ds_fact_create_modal: null operator"));
+    const OpDev &o = ops[i]->dev;
+    const ds_modal_desc &D = descs[i];
+    FactDev f;
+    memset(&f, 0, sizeof(f));
+    ds_fill_layout(o, f);
+    if (o.kappa2_kind == 2)
+      return fail(ds_fail(DS_ECONFIG, "modal factorization: kappa^2 is not tensor-structured"));
+    if (D.block_axis != f.block_axis || D.naxes != o.dim - 1)
+      return fail(ds_fail(DS_ECONFIG, "modal factorization: block axis / axis count mismatch"));
+    f.kind = 1;
+    f.naxes = o.dim - 1;
+    size_t elems = 2 * (size_t)f.nb + 2 * (size_t)f.nb * f.m;
+    for (int a = 0; a < f.naxes; ++a) {
+      f.nax[a] = o.shape[f.other[a]];
+      if (!D.v[a] || !D.vinv[a] || !D.lambda[a])
+        return fail(ds_fail(DS_ECONFIG, "modal factorization: missing eigen-decomposition"));
+      elems += 2 * (size_t)f.nax[a] * f.nax[a] + f.nax[a];
+    }
+    void *mem = nullptr;
+    if (cudaMalloc(&mem, elems * sizeof(cplx)) != cudaSuccess)
+      return fail(ds_fail(DS_ECUDA, "ds_fact_create_modal: out of device memory"));
+    F->allocations.push_back(mem);
+    cplx *p = (cplx *)mem;
+    cplx *lc = p, *uc = lc + f.nb;
+    p = uc + f.nb;
+    DS_CUDA(cudaMemcpy(lc, o.c_lo[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice));
+    DS_CUDA(cudaMemcpy(uc, o.c_hi[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice));
+    f.lcoef = lc;
+    f.ucoef = uc;
+    PivJob &J = jobs[i];
+    memset(&J, 0, sizeof(J));
+    for (int a = 0; a < f.naxes; ++a) {
+      const size_t na2 = (size_t)f.nax[a] * f.nax[a];
+      cplx *W = p, *V = W + na2, *L = V + na2;
+      p = L + f.nax[a];
+      DS_CUDA(cudaMemcpy(W, D.vinv[a], na2 * sizeof(cplx), cudaMemcpyHostToDevice));
+      DS_CUDA(cudaMemcpy(V, D.v[a], na2 * sizeof(cplx), cudaMemcpyHostToDevice));
+      DS_CUDA(cudaMemcpy(L, D.lambda[a], f.nax[a] * sizeof(cplx), cudaMemcpyHostToDevice));
+      f.mW[a] = W;
+      f.mV[a] = V;
+      J.lam[a] = L;
+    }
+    J.mul = p;
+    J.inv = p + (size_t)f.nb * f.m;
+    f.mmul = J.mul;
+    f.minv = J.inv;
+    J.f = f;
+    J.op = o;
+    mmax = std::max(mmax, f.m);
+    F->facts.push_back(f);
+    F->h_l.push_back(ops[i]->h_clo[f.block_axis]);
+    F->h_u.push_back(ops[i]->h_chi[f.block_axis]);
+    F->bytes.push_back((int64_t)(elems * sizeof(cplx)));
+    F->bytes_total += (int64_t)(elems * sizeof(cplx));
+  }
+  PivJob *djobs = nullptr;
+  int *dstatus = nullptr;
+  if (cudaMalloc(&djobs, sizeof(PivJob) * n) != cudaSuccess || cudaMalloc(&dstatus, sizeof(int)) != cudaSuccess)
+    return fail(ds_fail(DS_ECUDA, "ds_fact_create_modal: out of device memory"));
+  cudaMemcpy(djobs, jobs.data(), sizeof(PivJob) * n, cudaMemcpyHostToDevice);
+  cudaMemset(dstatus, 0, sizeof(int));
+  k_modal_pivots<<<dim3((mmax + 127) / 128, n), 128, 0, ctx->stream>>>(djobs, dstatus);
+  ctx->launches++;
+  int status = 0;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(&status, dstatus, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(djobs);
+  cudaFree(dstatus);
+  if (e != cudaSuccess) return fail(ds_fail(DS_ECUDA, std::string("modal pivots: ") + cudaGetErrorString(e)));
+  if (status) return fail(ds_fail(DS_ESOLVER, "modal factorization: zero or non-finite pivot"));
+  *out = F;
+  return DS_OK;
+}
+
+extern "C" int ds_fact_kind(const ds_fact *F, int32_t i) {
+  if (!F || i < 0 || i >= (int)F->facts.size()) return ds_fail(DS_ECONFIG, "ds_fact_kind: bad index");
+  return F->facts[i].kind;
+}

@@ -91,7 +91,13 @@ struct ds_plan {
   std::vector<std::pair<cplx *, size_t>> slot_bufs;  // for re-zeroing
   // host copies of the visit tables; nz pointers are patched per nrhs stride
   std::vector<VisitDev> h_visits;
-  std::vector<SolveVisit> h_solve;
+  std::vector<SolveVisit> h_solve;  // block-LU visits (compact, launch order)
+  std::vector<int> blu_vidx, blu_off;  // visit index of each entry; per-launch offsets
+  // modal visits (FactDev kind 1): job table, factor layouts, offsets
+  ModalJob *mjobs = nullptr;
+  std::vector<ModalJob> h_mjobs;
+  std::vector<FactDev> h_mfacts;
+  std::vector<int> mod_vidx, mod_off;
   // staged (large-slab) solve: host factor layouts and couplings per subdomain
   bool staged = false;
   std::vector<FactDev> h_facts;
@@ -106,6 +112,14 @@ struct ds_plan {
   std::vector<int> owner;
   bool peers_set = false;
   std::vector<XferDev> h_xfers;
+  // K4 v2 tables (rebuilt per nrhs stride in patch_tables)
+  std::vector<SubDev> h_subs;
+  std::vector<OpDev> h_ops;
+  std::vector<int> h_op_of_sub;
+  struct XferRec *recs = nullptr;
+  int4 *tiles = nullptr;
+  size_t tiles_cap = 0;
+  std::vector<int> tile_off;  // per launch, size nq + 1
   std::vector<size_t> xfer_slot_off;  // element offset of each transfer's slot
   cplx *slot_base = nullptr;
   size_t slot_bytes = 0;
@@ -252,6 +266,9 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 }
 
 #define SLOT_SMEM 32
+// band nodes per thread and tile pass of k_transfer2, and its resident blocks per SM
+#define K4_NPT(dim) ((dim) == 2 ? 2 : 1)
+#define K4_MINB(dim) 2
 
 // Thread mapping of K4/K5/K6: a thread owns RV RHS columns of one node --
 // lane l of the node's LPN = nrhs / RV lanes takes columns l, l + LPN, ... --
@@ -612,6 +629,158 @@ __global__ void __launch_bounds__(256)
   if (flag_bases) __threadfence_system();  // sharded: peer-memory payloads before the barrier
 }
 
+// ------------------------------------------------------- K4 v2 (default)
+// The same psi as k_transfer, restructured for latency (ncu on config 2:
+// k_transfer was long-scoreboard bound, <1 node iteration per warp behind a
+// 6-deep chain of dependent table loads, 95 registers, 3.9 waves):
+//  * every transfer's geometry is flattened on the host into an XferRec of
+//    pre-offset pointers and affine strides (block-layout offset of band
+//    node e is sum_a str[a] e[a]; fac / couplings / kappa2 indexed by e) --
+//    one level of table loads, staged through shared memory per tile;
+//  * the launch's band nodes are cut into tiles of NPT x (256 / nrhs) nodes
+//    (host list, discards have none), one tile per block pass, all loads
+//    of the NPT nodes of a thread issued before the arithmetic;
+//  * arrival / emission bookkeeping is spread over the first threads of
+//    the grid (one thread per (transfer, RHS)).
+// Summation order per value is that of k_transfer (bitwise equal results).
+struct XferRec {
+  const cplx *x, *rhs;  // source visit solution / rhs at the band origin
+  cplx *slot;           // payload slot (band C-order, stride nrhs)
+  const int *nz;        // source visit nonzero flags (per-call stride)
+  const double *fac[3];           // (1 - beta) factors at band coordinate e
+  const cplx *clo[3], *chi[3];    // neighbour couplings at band coordinate e
+  const double *k2;               // neighbour kappa^2 at e = 0
+  int str[3];    // block-layout stride (nodes) of band axis a
+  int k2str[3];  // kappa^2 index stride per axis
+  int shape[3];  // band shape
+  int elo[3], ehi[3];  // ext bounds relative to the band origin
+  int nodes, src, sweep, dirmask;
+  double sign;
+};
+static_assert(sizeof(XferRec) % 8 == 0, "XferRec is copied as 8-byte words");
+
+template <int DIM, int NPT>
+__global__ void __launch_bounds__(256, K4_MINB(DIM))
+    k_transfer2(const XferDev *__restrict__ xfers, const XferRec *__restrict__ recs,
+                const int4 *__restrict__ tiles, int ntiles, int nx, int nsub, int nrhs, Flags F,
+                int *const *__restrict__ flag_bases, int nsweeps) {
+  constexpr int NP = 1 + 2 * DIM;
+  __shared__ XferRec R;
+  const int t = threadIdx.x;
+  // bookkeeping (ddm.py:262-279): one thread per (transfer, RHS) of the launch
+  for (int gt = blockIdx.x * blockDim.x + t; gt < nx * nrhs; gt += gridDim.x * blockDim.x) {
+    const int i = gt / nrhs, r = gt % nrhs;
+    const XferRec &Q = recs[i];
+    if (!Q.nz[r]) continue;
+    const int cut = solve_cut(F, Q.sweep, Q.src, nsub, r, nrhs);
+    const XferDev &X = xfers[i];
+    if (cut & X.dirmask) continue;
+    if (X.use == 0) {
+      atomicAdd(&F.discard[r], 1);
+    } else {
+      int *arr_cnt = F.arr_cnt, *arr_cut = F.arr_cut;
+      if (flag_bases) arrival_words(flag_bases[X.owner], nsweeps, nsub, nrhs, arr_cnt, arr_cut);
+      const size_t ti = ((size_t)(X.use - 1) * nsub + X.dst) * nrhs + r;
+      atomicAdd_system(&arr_cnt[ti], 1);
+      atomicAnd_system(&arr_cut[ti], X.content_base | (cut & X.keepmask));
+      atomicAdd(&F.emit_cnt[((size_t)(Q.sweep - 1) * nsub + X.src) * nrhs + r], 1);
+    }
+  }
+  const int npb = blockDim.x / nrhs, r = t % nrhs, ln = t / nrhs;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int4 T = tiles[tile];  // (transfer, first node, end node)
+    __syncthreads();
+    if (t < (int)(sizeof(XferRec) / 8))
+      reinterpret_cast<long long *>(&R)[t] = reinterpret_cast<const long long *>(recs + T.x)[t];
+    __syncthreads();
+    if (ln >= npb) continue;
+    const bool emit = R.nz[r] && !(solve_cut(F, R.sweep, R.src, nsub, r, nrhs) & R.dirmask);
+    if (!emit) continue;
+    const int nodes = T.z;
+    for (int n0 = T.y; n0 < nodes; n0 += NPT * npb) {
+    // phase 1: all loads of the thread's NPT nodes
+    cplx v[NPT][NP], rvv[NPT], spv[NPT], lo[NPT][DIM], hi[NPT][DIM];
+    double wm[NPT][NP], k2[NPT];
+    bool ok[NPT][NP], live[NPT];
+    int node_of[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      const int node = n0 + k * npb + ln;
+      node_of[k] = node;
+      live[k] = node < nodes;
+      const int nd = live[k] ? node : n0;  // dead lanes reload a live node
+      int e[3];
+      if (DIM == 3) {
+        e[2] = nd % R.shape[2];
+        const int q = nd / R.shape[2];
+        e[1] = q % R.shape[1];
+        e[0] = q / R.shape[1];
+      } else {
+        e[1] = nd % R.shape[1];
+        e[0] = nd / R.shape[1];
+        e[2] = 0;
+      }
+      int off = 0, k2i = 0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        off += R.str[a] * e[a];
+        k2i += R.k2str[a] * e[a];
+      }
+      double f0[DIM], fm[DIM], fp[DIM];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        f0[a] = R.fac[a][e[a]];
+        ok[k][1 + 2 * a] = e[a] - 1 >= R.elo[a];
+        ok[k][2 + 2 * a] = e[a] + 1 < R.ehi[a];
+        fm[a] = ok[k][1 + 2 * a] ? R.fac[a][e[a] - 1] : 0.0;
+        fp[a] = ok[k][2 + 2 * a] ? R.fac[a][e[a] + 1] : 0.0;
+        lo[k][a] = R.clo[a][e[a]];
+        hi[k][a] = R.chi[a][e[a]];
+      }
+      ok[k][0] = true;
+      v[k][0] = R.x[(int64_t)off * nrhs + r];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        v[k][1 + 2 * a] = ok[k][1 + 2 * a] ? R.x[(int64_t)(off - R.str[a]) * nrhs + r] : v[k][0];
+        v[k][2 + 2 * a] = ok[k][2 + 2 * a] ? R.x[(int64_t)(off + R.str[a]) * nrhs + r] : v[k][0];
+      }
+      rvv[k] = R.rhs[(int64_t)off * nrhs + r];
+      spv[k] = R.slot[(int64_t)nd * nrhs + r];
+      k2[k] = R.k2[k2i];
+      // w(p) - 1 with w = prod_a fac_a in axis order (k_transfer's point())
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        double wt = 1.0;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+          double fa = f0[a];
+          if (q == 1 + 2 * a) fa = fm[a];
+          if (q == 2 + 2 * a) fa = fp[a];
+          wt = wt * fa;
+        }
+        wm[k][q] = (q == 0 || ok[k][q]) ? wt - 1.0 : 0.0;
+      }
+    }
+    // phase 2: centre k2*w0, then per axis -(lo+hi)*w0, lo*w(p-e_a), hi*w(p+e_a)
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      const cplx w0 = cscale(v[k][0], wm[k][0]);
+      cplx acc = cscale(w0, k2[k]);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const cplx mlh = make_double2(-(lo[k][a].x + hi[k][a].x), -(lo[k][a].y + hi[k][a].y));
+        acc = cadd(acc, cmul(mlh, w0));
+        if (ok[k][1 + 2 * a]) acc = cadd(acc, cmul(lo[k][a], cscale(v[k][1 + 2 * a], wm[k][1 + 2 * a])));
+        if (ok[k][2 + 2 * a]) acc = cadd(acc, cmul(hi[k][a], cscale(v[k][2 + 2 * a], wm[k][2 + 2 * a])));
+      }
+      if (live[k])
+        R.slot[(int64_t)node_of[k] * nrhs + r] = cadd(spv[k], cscale(cadd(rvv[k], acc), R.sign));
+    }
+    }
+  }
+  if (flag_bases) __threadfence_system();  // sharded: peer-memory payloads before the barrier
+}
+
 // ------------------------------------------------------------ plan create
 
 extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out) {
@@ -664,6 +833,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     std::vector<OpDev> h(d->nops);
     for (int i = 0; i < d->nops; ++i) h[i] = d->ops[i]->dev;
     cudaMemcpy(P->ops, h.data(), sizeof(OpDev) * d->nops, cudaMemcpyHostToDevice);
+    P->h_ops = h;
   }
   // factor layout of every subdomain (device table, one entry per subdomain)
   std::vector<FactDev> hf(nsub);
@@ -725,11 +895,13 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     max_w = std::max<int>(max_w, (int)wn);
     P->max_w = max_w;
     P->max_axis_sum = std::max(P->max_axis_sum, S.win_shape[0] + S.win_shape[1] + S.win_shape[2]);
-    if (P->owner[s] == P->rank) P->max_m = std::max(P->max_m, fd.m);
+    if (P->owner[s] == P->rank && fd.kind == 0) P->max_m = std::max(P->max_m, fd.m);
   }
   if (plan_alloc(P, &mem, sizeof(SubDev) * nsub)) return fail(DS_ECUDA);
   P->subs = (SubDev *)mem;
   cudaMemcpy(P->subs, hs.data(), sizeof(SubDev) * nsub, cudaMemcpyHostToDevice);
+  P->h_subs = hs;
+  P->h_op_of_sub.assign(d->op_of_sub, d->op_of_sub + nsub);
   // ---- steps and visit buffers
   P->gmax = 0;
   int max_nb = 0;
@@ -767,11 +939,18 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   // K3 exchange scratch: 4 * m * nrhs per visit slot (2 parities x Gmax)
   size_t xgbuf = 4 * (size_t)P->max_m * d->nrhs_max;
   cplx *xgs;
-  if (plan_alloc(P, &mem, sizeof(cplx) * xgbuf * 2 * P->gmax)) return fail(DS_ECUDA);
+  if (plan_alloc(P, &mem, sizeof(cplx) * std::max<size_t>(xgbuf, 1) * 2 * P->gmax)) return fail(DS_ECUDA);
   xgs = (cplx *)mem;
+  bool any_modal = false;
+  for (int s = 0; s < nsub; ++s) any_modal |= P->owner[s] == P->rank && hf[s].kind == 1;
+  cplx *mscr = nullptr;  // modal scratch: 2 buffers per visit slot
+  if (any_modal) {
+    if (plan_alloc(P, &mem, sizeof(cplx) * vbuf * 2 * 2 * P->gmax)) return fail(DS_ECUDA);
+    mscr = (cplx *)mem;
+  }
   {
     const char *mode = getenv("DS_SOLVE_MODE");
-    P->staged = P->max_m > DS_LARGE_SLAB || (mode && std::string(mode) == "staged");
+    P->staged = P->max_m > 0 && (P->max_m > DS_LARGE_SLAB || (mode && std::string(mode) == "staged"));
   }
   (void)max_nb;
   // ---- flags
@@ -850,6 +1029,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   // ---- visits in execution order
   std::vector<VisitDev> hv;
   std::vector<SolveVisit> hsv;
+  P->blu_off.assign((size_t)(sched ? d->nlaunch : nsw * nst) + 1, 0);
+  P->mod_off.assign(P->blu_off.size(), 0);
   std::vector<XferDev> hx;
   const int nq = sched ? d->nlaunch : nsw * nst;
   P->vstep_off.assign((size_t)nq + 1, 0);
@@ -878,6 +1059,8 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
         e = d->step_off[w * (nst + 1) + t + 1];
       }
       P->vstep_off[step_global] = (int)hv.size();
+      P->blu_off[step_global] = (int)hsv.size();
+      P->mod_off[step_global] = (int)P->h_mjobs.size();
       int parity = step_global & 1;
       for (int g = b; g < e; ++g) {
         int w, s;
@@ -895,9 +1078,18 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
         V.nz = nullptr;  // set per call (depends on nrhs stride)
         visit_of[(size_t)w * nsub + s] = (int)hv.size();
         hv.push_back(V);
-        SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr,
-                      xgs + ((size_t)parity * P->gmax + gi) * xgbuf};
-        hsv.push_back(SV);
+        if (hf[s].kind == 1) {
+          cplx *s0 = mscr + ((size_t)(parity * 2 + 0) * P->gmax + gi) * vbuf;
+          cplx *s1 = mscr + ((size_t)(parity * 2 + 1) * P->gmax + gi) * vbuf;
+          P->h_mjobs.push_back(ModalJob{P->facts + s, V.rhs, V.x, s0, s1, nullptr});
+          P->h_mfacts.push_back(hf[s]);
+          P->mod_vidx.push_back((int)hv.size() - 1);
+        } else {
+          SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr,
+                        xgs + ((size_t)parity * P->gmax + gi) * xgbuf};
+          hsv.push_back(SV);
+          P->blu_vidx.push_back((int)hv.size() - 1);
+        }
       }
       P->xstep_off[step_global] = (int)hx.size();
       for (int g = b; g < e; ++g) {
@@ -954,18 +1146,24 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   }
   P->vstep_off[step_global] = (int)hv.size();
   P->xstep_off[step_global] = (int)hx.size();
+  P->blu_off[step_global] = (int)hsv.size();
+  P->mod_off[step_global] = (int)P->h_mjobs.size();
   // upload tables
   if (plan_alloc(P, &mem, sizeof(SlotRef) * std::max<size_t>(hslot_tab.size(), 1))) return fail(DS_ECUDA);
   P->slots = (SlotRef *)mem;
   cudaMemcpy(P->slots, hslot_tab.data(), sizeof(SlotRef) * hslot_tab.size(), cudaMemcpyHostToDevice);
   if (plan_alloc(P, &mem, sizeof(VisitDev) * hv.size())) return fail(DS_ECUDA);
   P->visits = (VisitDev *)mem;
-  if (plan_alloc(P, &mem, sizeof(SolveVisit) * hsv.size())) return fail(DS_ECUDA);
+  if (plan_alloc(P, &mem, sizeof(SolveVisit) * std::max<size_t>(hsv.size(), 1))) return fail(DS_ECUDA);
   P->solvetab = (SolveVisit *)mem;
+  if (plan_alloc(P, &mem, sizeof(ModalJob) * std::max<size_t>(P->h_mjobs.size(), 1))) return fail(DS_ECUDA);
+  P->mjobs = (ModalJob *)mem;
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
   cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice);
   P->h_xfers = hx;
+  if (plan_alloc(P, &mem, sizeof(XferRec) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
+  P->recs = (XferRec *)mem;
   P->peers_set = !sharded;
   P->h_visits = hv;
   P->h_solve = hsv;
@@ -979,9 +1177,10 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
       sf.emplace_back();
       sl.emplace_back();
       su.emplace_back();
-      for (int i = P->vstep_off[q]; i < P->vstep_off[q + 1]; ++i) {
+      for (int e = P->blu_off[q]; e < P->blu_off[q + 1]; ++e) {
+        const int i = P->blu_vidx[e];
         int sub = hv[i].sub;
-        sv.back().push_back(hsv[i]);
+        sv.back().push_back(hsv[e]);
         sf.back().push_back(hf[sub]);
         sl.back().push_back(P->h_l[sub]);
         su.back().push_back(P->h_u[sub]);
@@ -1020,6 +1219,7 @@ extern "C" int ds_plan_destroy(ds_plan *P) {
   if (P->gev_out) cudaEventDestroy(P->gev_out);
   for (auto e : P->ev) cudaEventDestroy(e);
   ds_stage_program_destroy(P->program);
+  if (P->tiles) cudaFree(P->tiles);
   for (void *p : P->allocs) cudaFree(p);
   delete P;
   return DS_OK;
@@ -1032,12 +1232,102 @@ static int patch_tables(ds_plan *P, int nrhs) {
   for (size_t i = 0; i < P->h_visits.size(); ++i) {
     VisitDev &V = P->h_visits[i];
     V.nz = F.nz + ((size_t)(V.sweep - 1) * P->nsub + V.sub) * nrhs;
-    P->h_solve[i].nz = V.nz;
   }
+  for (size_t e = 0; e < P->h_solve.size(); ++e) P->h_solve[e].nz = P->h_visits[P->blu_vidx[e]].nz;
+  for (size_t e = 0; e < P->h_mjobs.size(); ++e) P->h_mjobs[e].nz = P->h_visits[P->mod_vidx[e]].nz;
   DS_CUDA(cudaMemcpyAsync(P->visits, P->h_visits.data(), sizeof(VisitDev) * P->h_visits.size(),
                           cudaMemcpyHostToDevice, P->ctx->stream));
-  DS_CUDA(cudaMemcpyAsync(P->solvetab, P->h_solve.data(), sizeof(SolveVisit) * P->h_solve.size(),
-                          cudaMemcpyHostToDevice, P->ctx->stream));
+  if (!P->h_solve.empty())
+    DS_CUDA(cudaMemcpyAsync(P->solvetab, P->h_solve.data(), sizeof(SolveVisit) * P->h_solve.size(),
+                            cudaMemcpyHostToDevice, P->ctx->stream));
+  if (!P->h_mjobs.empty())
+    DS_CUDA(cudaMemcpyAsync(P->mjobs, P->h_mjobs.data(), sizeof(ModalJob) * P->h_mjobs.size(),
+                            cudaMemcpyHostToDevice, P->ctx->stream));
+  // K4 v2: flattened transfer records and the per-launch band-node tiles
+  std::vector<XferRec> hr(P->h_xfers.size());
+  std::vector<int4> ht;
+  const int npb = 256 / nrhs;
+  const int pass_nodes = K4_NPT(P->dim) * npb;
+  const int resident = P->ctx->num_sms * K4_MINB(P->dim);
+  const int nq = (int)P->xstep_off.size() - 1;
+  P->tile_off.assign((size_t)nq + 1, 0);
+  for (int q = 0; q < nq; ++q) {
+    P->tile_off[q] = (int)ht.size();
+    // tile size of this launch: about one tile per resident block
+    int64_t launch_nodes = 0;
+    for (int i = P->xstep_off[q]; i < P->xstep_off[q + 1]; ++i) {
+      const XferDev &X = P->h_xfers[i];
+      if (X.use > 0) launch_nodes += (int64_t)X.band_shape[0] * X.band_shape[1] * X.band_shape[2];
+    }
+    int64_t tn = (launch_nodes + resident - 1) / resident;
+    tn = std::max<int64_t>(1, (tn + pass_nodes - 1) / pass_nodes) * pass_nodes;
+    for (int i = P->xstep_off[q]; i < P->xstep_off[q + 1]; ++i) {
+      const XferDev &X = P->h_xfers[i];
+      const VisitDev &V = P->h_visits[X.vidx];
+      const FactDev &fs = P->h_facts[X.src];
+      const SubDev &ss = P->h_subs[X.src], &sn = P->h_subs[X.dst];
+      const OpDev &on = P->h_ops[P->h_op_of_sub[X.dst]];
+      XferRec &Q = hr[i];
+      memset(&Q, 0, sizeof(Q));
+      int str[3] = {0, 0, 0};
+      str[fs.block_axis] = fs.m;
+      if (fs.other[0] >= 0) str[fs.other[0]] = fs.other[1] >= 0 ? fs.win_shape[fs.other[1]] : 1;
+      if (fs.other[1] >= 0) str[fs.other[1]] = 1;
+      int ostr[3] = {0, 0, 0};
+      for (int a = P->dim - 1, acc = 1; a >= 0; --a) {
+        ostr[a] = acc;
+        acc *= on.shape[a];
+      }
+      int64_t base = 0, k2base = 0;
+      Q.nodes = 1;
+      for (int a = 0; a < P->dim; ++a) {
+        const int blo = X.band_lo[a];
+        base += (int64_t)str[a] * (blo - ss.win_lo[a]);
+        Q.str[a] = str[a];
+        Q.shape[a] = X.band_shape[a];
+        Q.nodes *= X.band_shape[a];
+        Q.elo[a] = X.ext_lo[a] - blo;
+        Q.ehi[a] = X.ext_lo[a] + X.ext_shape[a] - blo;
+        Q.fac[a] = X.fac[a] + (blo - X.ext_lo[a]);
+        Q.clo[a] = on.c_lo[a] + (blo - sn.win_lo[a]);
+        Q.chi[a] = on.c_hi[a] + (blo - sn.win_lo[a]);
+        if (on.kappa2_kind == 2) {
+          Q.k2str[a] = ostr[a];
+          k2base += (int64_t)ostr[a] * (blo - sn.win_lo[a]);
+        } else if (on.kappa2_kind == 1 && a == on.kappa2_axis) {
+          Q.k2str[a] = 1;
+          k2base += blo - sn.win_lo[a];
+        }
+      }
+      Q.x = V.x + base * nrhs;
+      Q.rhs = V.rhs + base * nrhs;
+      Q.slot = X.slot;
+      Q.nz = V.nz;
+      Q.k2 = on.kappa2 + k2base;
+      Q.src = X.src;
+      Q.sweep = V.sweep;
+      Q.dirmask = X.dirmask;
+      Q.sign = X.sign;
+      if (X.use > 0)
+        for (int64_t n0 = 0; n0 < Q.nodes; n0 += tn)
+          ht.push_back(make_int4(i - P->xstep_off[q], (int)n0, (int)std::min<int64_t>(Q.nodes, n0 + tn), 0));
+    }
+  }
+  P->tile_off[nq] = (int)ht.size();
+  if (!hr.empty())
+    DS_CUDA(cudaMemcpyAsync(P->recs, hr.data(), sizeof(XferRec) * hr.size(), cudaMemcpyHostToDevice,
+                            P->ctx->stream));
+  if (ht.size() > P->tiles_cap) {
+    DS_CUDA(cudaStreamSynchronize(P->ctx->stream));
+    if (P->tiles) cudaFree(P->tiles);
+    P->tiles = nullptr;
+    P->tiles_cap = 0;
+    DS_CUDA(cudaMalloc(&P->tiles, sizeof(int4) * ht.size()));
+    P->tiles_cap = ht.size();
+  }
+  if (!ht.empty())
+    DS_CUDA(cudaMemcpyAsync(P->tiles, ht.data(), sizeof(int4) * ht.size(), cudaMemcpyHostToDevice,
+                            P->ctx->stream));
   DS_CUDA(cudaStreamSynchronize(P->ctx->stream));
   P->patched_nrhs = nrhs;
   if (P->graph) {
@@ -1115,12 +1405,15 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
       if (s5 != st && k5_pending[q & 1]) DS_CUDA(cudaStreamWaitEvent(st, P->ev_k5[q & 1], 0));
-      int rc;
-      if (P->program) {
-        rc = ds_stage_program_launch_step(ctx, P->program, q, nrhs);
-      } else {
-        rc = ds_launch_solve_table(ctx, P->solvetab + v0, G, nrhs, P->max_m);
+      int rc = DS_OK;
+      const int b0 = P->blu_off[q], nbl = P->blu_off[q + 1] - b0;
+      const int m0 = P->mod_off[q], nmo = P->mod_off[q + 1] - m0;
+      if (nbl > 0) {
+        if (P->program) rc = ds_stage_program_launch_step(ctx, P->program, q, nrhs);
+        else rc = ds_launch_solve_table(ctx, P->solvetab + b0, nbl, nrhs, P->max_m);
       }
+      if (rc) return rc;
+      if (nmo > 0) rc = ds_launch_modal(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs);
       if (rc) return rc;
       DS_CHECK_LAUNCH();
       prof_mark(P, 2, st);
@@ -1152,8 +1445,22 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
 #define K4_LAUNCH(RV_, D_)                                                                       \
   k_transfer<RV_, D_><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, \
                                                     nrhs, dim, F, P->d_flag_bases, P->nsweeps)
+        static const bool k4v1 = [] {
+          const char *v = getenv("DS_K4");  // "v1": the original one-block-per-band kernel
+          return v && std::string(v) == "v1";
+        }();
         const int rv = (k4rv == 4 && nrhs % 4 == 0) ? 4 : ((k4rv >= 2 && nrhs % 2 == 0) ? 2 : 1);
-        if (dim == 2) {
+        if (!k4v1) {
+          const int t0 = P->tile_off[q], nt = P->tile_off[q + 1] - t0;
+          const int resident = ctx->num_sms * K4_MINB(dim);
+          const int gb = std::max(1, std::max(std::min(nt, resident), (nx * nrhs + 255) / 256));
+          if (dim == 2)
+            k_transfer2<2, K4_NPT(2)><<<gb, 256, 0, st>>>(P->xfers + x0, P->recs + x0, P->tiles + t0, nt, nx,
+                                                        P->nsub, nrhs, F, P->d_flag_bases, P->nsweeps);
+          else
+            k_transfer2<3, K4_NPT(3)><<<gb, 256, 0, st>>>(P->xfers + x0, P->recs + x0, P->tiles + t0, nt, nx,
+                                                        P->nsub, nrhs, F, P->d_flag_bases, P->nsweeps);
+        } else if (dim == 2) {
           if (rv == 4) K4_LAUNCH(4, 2);
           else if (rv == 2) K4_LAUNCH(2, 2);
           else K4_LAUNCH(1, 2);
@@ -1264,6 +1571,7 @@ extern "C" int ds_plan_set_peers(ds_ctx *ctx, ds_plan *P, int32_t nranks, void *
     if (hx[i].use > 0) hx[i].slot = (cplx *)slot_bases[hx[i].owner] + P->xfer_slot_off[i];
   DS_CUDA(cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice));
   P->h_xfers = hx;
+  P->patched_nrhs = 0;  // XferRec slot pointers are rebuilt from h_xfers
   if (!P->d_flag_bases) {
     void *mem;
     if (plan_alloc(P, &mem, sizeof(int *) * nranks)) return ds_fail(DS_ECUDA, "ds_plan_set_peers: alloc");

@@ -5,9 +5,17 @@ Drop-in for `FactorizationCache` / `factorize` (diagsweep/subdomain.py:
 `.backend`, `.factor_bytes`, keyed by `op.fingerprint` so operators with
 identical coefficient bytes share one factorization (subdomain.py:153-171).
 
-The backend is the block-tridiagonal dense-block LU of K2 (csrc/ds_factor.cu)
-for every operator kind — it replaces both the Schur/Sylvester separable
-solver and SuperLU.  `share_translates=True` (opt-in, off by default to keep the reference's
+Backends (the reference's dispatch, subdomain.py:139-147: 'auto' picks
+'separable' for tensor-structured kappa^2, else 'splu'):
+* 'separable' -> the modal factorization (K2m/K3m, csrc/ds_modal.cu): the
+  in-slab 1D tridiagonals are diagonalised (host LAPACK eig of n_a x n_a
+  matrices, as the reference's own separable backend calls scipy.linalg.schur)
+  and the device keeps the transforms and mode-wise pivots; solves are
+  batched complex GEMMs on the FP64 tensor cores plus mode-wise recurrences.
+* 'splu' / 'block-lu' -> the block-tridiagonal dense-block LU of K2
+  (csrc/ds_factor.cu), for every operator kind (replaces SuperLU).
+DS_FACTOR=block-lu in the environment makes 'auto' use the block LU for
+every operator (A/B measurements).  `share_translates=True` (opt-in, off by default to keep the reference's
 exact-fingerprint semantics) keys operators by their coefficients rounded to
 12 significant digits, so windows that are translates of each other (equal
 up to linspace round-off, ~1e-16) share one factorization.  This is what lets
@@ -23,6 +31,7 @@ batched launch (`prepare`).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 from .errors import ConfigurationError
@@ -31,9 +40,8 @@ _METHODS = ("auto", "separable", "splu", "block-lu")
 
 
 class GpuFactorization:
-    backend = "block-lu"
-
     def __init__(self, fset, index: int, op):
+        self.backend = "separable" if getattr(fset, "modal", False) else "block-lu"
         self.fset = fset
         self.index = index
         self.window = op.window
@@ -61,12 +69,21 @@ def _check_method(op, method: str):
         raise ConfigurationError("operator kappa^2 is not tensor-structured")
 
 
+def _resolve(op, method: str) -> bool:
+    """True for the modal (separable) backend, False for the block LU."""
+    _check_method(op, method)
+    if method == "auto":
+        if os.environ.get("DS_FACTOR", "") == "block-lu":
+            return False
+        return bool(op.separable)
+    return method == "separable"
+
+
 def factorize(op, method: str = "auto") -> GpuFactorization:
-    """Factor one operator on the GPU (block LU)."""
+    """Factor one operator on the GPU (modal if separable, else block LU)."""
     from . import _engine
 
-    _check_method(op, method)
-    return GpuFactorization(_engine.FactorSet([op]), 0, op)
+    return GpuFactorization(_engine.FactorSet([op], modal=_resolve(op, method)), 0, op)
 
 
 def _coarse_key(op) -> str:
@@ -120,9 +137,13 @@ class FactorizationCache:
                 todo[key] = op
         if not todo:
             return
-        fset = _engine.FactorSet(list(todo.values()))
-        for i, (key, op) in enumerate(todo.items()):
-            self._store[key] = GpuFactorization(fset, i, op)
+        for modal in (True, False):
+            group = [(k, op) for k, op in todo.items() if _resolve(op, self.method) == modal]
+            if not group:
+                continue
+            fset = _engine.FactorSet([op for _, op in group], modal=modal)
+            for i, (key, op) in enumerate(group):
+                self._store[key] = GpuFactorization(fset, i, op)
 
     def key(self, op) -> str:
         return _coarse_key(op) if self.share_translates else op.fingerprint

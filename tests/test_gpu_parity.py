@@ -87,14 +87,18 @@ def test_stencil_apply_raster_kappa(cuda, raster):
         assert rel(op.apply(v), oops[idx].apply(v)) <= 1e-14
 
 
-@pytest.mark.parametrize("which", ["cfg1", "raster"])
-def test_block_lu_solve_roundtrip(cuda, which, cfg1, raster):
+@pytest.mark.parametrize("which,method", [("cfg1", "block-lu"), ("cfg1", "separable"),
+                                          ("raster", "auto")])
+def test_block_lu_solve_roundtrip(cuda, which, method, cfg1, raster):
+    """Single-operator solves: block LU (K2/K3) and the modal backend
+    (K2m/K3m, 'separable') vs the oracle's Schur/Sylvester or SuperLU solve."""
     s, b, prob, oops = cfg1 if which == "cfg1" else raster
-    cache = FactorizationCache()
+    cache = FactorizationCache(method=method)
     rng = np.random.default_rng(7)
     for idx in list(b["ops"])[:4]:
         op = b["ops"][idx]
         fact = cache.get(op)
+        assert fact.backend == ("block-lu" if method != "separable" else "separable")
         rhs = rng.standard_normal((2,) + op.window.shape) + 1j * rng.standard_normal((2,) + op.window.shape)
         x = fact.solve(rhs)
         ref = O.factorize(oops[idx]).solve(rhs[0])
@@ -104,10 +108,12 @@ def test_block_lu_solve_roundtrip(cuda, which, cfg1, raster):
             assert res <= 1e-12, res
 
 
-def test_ddm_cfg1_parity_and_events(cuda, cfg1):
+@pytest.mark.parametrize("method", ["auto", "block-lu"])
+def test_ddm_cfg1_parity_and_events(cuda, cfg1, method):
+    """'auto' runs the modal solve (separable operators), 'block-lu' K3."""
     s, b, prob, oops = cfg1
     f = configs.sources(s, b["grid"])
-    u, rep = diagonal_sweep_solve(f[0], b["partition"], b["ops"], FactorizationCache(),
+    u, rep = diagonal_sweep_solve(f[0], b["partition"], b["ops"], FactorizationCache(method=method),
                                   record_events=True, warn_collar=False)
     ref, orep = O.ddm_apply(prob, oops, O.Cache(), f[0], record=True)
     assert rel(u.values, ref) <= TOL
@@ -160,11 +166,12 @@ def test_ddm_emission_pattern_compact_source(cuda):
     assert rel(u.values, ref) <= TOL
 
 
-def test_ddm_cfg2_batch_subset(cuda):
+@pytest.mark.parametrize("method", ["auto", "block-lu"])
+def test_ddm_cfg2_batch_subset(cuda, method):
     s = configs.spec(2)
     b = configs.build(s)
     f = configs.sources(s, b["grid"])[:4]
-    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(),
+    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(method=method),
                                    warn_collar=False)
     prob = O.Problem(**configs.oracle_problem(s, b))
     oops = prob.operators()
@@ -340,11 +347,13 @@ def mini3d():
     return s, configs.build(s)
 
 
-def test_3d_blocked_factor_solve_roundtrip(cuda):
-    """Blocked (panel + GEMM) factorization and staged solve, m = 625."""
+@pytest.mark.parametrize("method", ["block-lu", "separable"])
+def test_3d_blocked_factor_solve_roundtrip(cuda, method):
+    """Blocked (panel + GEMM) factorization and staged solve, m = 625; the
+    modal backend (two in-slab transforms per direction) on the same ops."""
     s, b = mini3d()
     prob = O.Problem(**configs.oracle_problem(s, b))
-    cache = FactorizationCache()
+    cache = FactorizationCache(method=method)
     rng = np.random.default_rng(11)
     for idx in [(1, 1, 1), (2, 1, 2)]:
         op = b["ops"][idx]
@@ -359,13 +368,14 @@ def test_3d_blocked_factor_solve_roundtrip(cuda):
         assert rel(x[0], O.factorize(oop).solve(rhs[0])) <= TOL
 
 
-def test_3d_ddm_vs_reference_golden_both_plans(cuda):
+@pytest.mark.parametrize("method", ["auto", "block-lu"])
+def test_3d_ddm_vs_reference_golden_both_plans(cuda, method):
     from paper_2002_05327_b200 import SweepPlan
 
     s, b = mini3d()
     g = np.load(GOLD / "ddm_3d_mini.npz")
     f = configs.sources(s, b["grid"])[0]
-    cache = FactorizationCache()
+    cache = FactorizationCache(method=method)
     u, rep = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, record_events=True,
                                   warn_collar=False)
     assert rel(u.values, g["u"]) <= TOL
