@@ -120,18 +120,38 @@ class ClockSampler:
 
 
 def algorithmic_work(dp, nrhs):
-    """K3 flops and factor bytes per application: every
-    (sweep, subdomain) visit counts 16 n_b m^2 flop per RHS and streams its
-    2 n_b m^2 complex factor entries once per RHS chunk (K3 clusters take at
-    most 16 RHS)."""
-    flops = 0
-    fbytes = 0
+    """Subdomain-solve flops and factor bytes per application,
+    every (sweep, subdomain) visit counted (the paper's count):
+    * block LU (K3): 16 n_b m^2 flop per RHS; the 2 n_b m^2 complex factor
+      entries stream once per RHS chunk (K3 clusters take at most 16 RHS);
+    * modal (K3m-T, separable operators): two in-slab transforms per
+      direction, 16 n_b m (sum_a n_a) flop per RHS (= 16 n_b m^2 in 2D);
+      the transform matrices are L2-resident (n_a^2 entries each).
+    Returns (flops, factor_bytes, canonical_flops) where canonical_flops is
+    SURVEY's 16 n_b m^2 per RHS whatever the backend."""
+    flops = fbytes = canon = 0
     chunks = math.ceil(nrhs / 16)
     for f in dp._keep[1]:
         nb, m = f.n_blocks, f.block_size
-        flops += 16 * nb * m * m * nrhs
-        fbytes += 2 * nb * m * m * 16 * chunks
-    return flops * dp.nsweeps, fbytes * dp.nsweeps
+        canon += 16 * nb * m * m * nrhs
+        if f.backend == "separable":
+            flops += 16 * nb * m * (sum(f.shape) - f.shape[f.block_axis]) * nrhs
+        else:
+            flops += 16 * nb * m * m * nrhs
+            fbytes += 2 * nb * m * m * 16 * chunks
+    return flops * dp.nsweeps, fbytes * dp.nsweeps, canon * dp.nsweeps
+
+
+def recurrence_bytes(dp, nrhs):
+    """K3m-R (mode-wise recurrences) algorithmic bytes per application: per
+    visit and RHS the transformed block is read and the solution written
+    (32 n_b m), plus the mode-wise multipliers / inverse pivots once per
+    visit (32 n_b m)."""
+    tot = 0
+    for f in dp._keep[1]:
+        if f.backend == "separable":
+            tot += 32 * f.n_blocks * f.block_size * (nrhs + 1)
+    return tot * dp.nsweeps
 
 
 def step_kernel_bytes(dp, nrhs):
@@ -191,7 +211,7 @@ def run_ours(args, rank, world, local_rank):
     part, ops = b["partition"], b["ops"]
     # 3D constant media: share factorizations across translation classes
     # (config 4: 27 classes, 76 GB instead of 203 GB)
-    share = part.dim == 3 and s.medium == "constant"
+    share = part.dim == 3 and s.medium == "constant" and os.environ.get("DS_FACTOR") == "block-lu"
     cache = FactorizationCache(share_translates=share)
 
     # ---- factorization (timed separately, amortised)
@@ -249,21 +269,26 @@ def run_ours(args, rank, world, local_rank):
 
         dist.barrier()
     torch.cuda.synchronize()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.record()
+    # L2 flush between timed steps: a 256 MiB zero-fill (twice the 126 MB L2)
+    # before every step, outside that step's event pair
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     from paper_2002_05327_b200._engine import launch_count
 
     launches0 = launch_count()
     rhs_apps[0] = 0
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record()
         step()
-    en.record()
+        evs[i][1].record()
     launches = launch_count() - launches0  # every kernel of ours in the timed region
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = st.elapsed_time(en) / args.steps
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     # ---- kernel breakdown: the same K applications again, eager, with CUDA
     # events around every launch group (not part of `value`)
     ktimes = None
@@ -331,10 +356,11 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (K3)
     hbm, hbm_src, fp64, fp64_src = peaks()
-    flops1, fbytes1 = algorithmic_work(dp, 1)
+    flops1, _, canon1 = algorithmic_work(dp, 1)
     apps = rhs_apps[0] / max(1, args.steps)  # RHS-applications per step
     flops = flops1 * apps
     fbytes = algorithmic_work(dp, R)[1] * (apps / R)
+    modal = any(f.backend == "separable" for f in dp._keep[1])
     roofline = None
     kernels = None
     if ktimes:
@@ -352,21 +378,41 @@ def run_ours(args, rank, world, local_rank):
             traffic_note = {"launch": tj["launch"], "algorithmic_factor_bytes": tj["algorithmic_factor_bytes"],
                             "traffic_over_algorithmic": tj["traffic_over_algorithmic"],
                             "duration_us": tj["duration_us"], "source": str(tpath.relative_to(ROOT))}
-        roofline = {"bound": "tensor", "pipe": "fp64 tensor (DMMA m8n8k4)", "achieved": ach,
-                    "peak": fp64,
-                    "unit": "TFLOP/s", "frac": ach / fp64, "traffic": traffic,
-                    "traffic_per_launch": traffic_note,
-                    "peak_source": fp64_src,
-                    "kernel": "k_block_solve (K3)",
-                    "algorithmic_per_app": {"flop": flops, "factor_bytes": fbytes},
-                    "hbm_view": {"achieved_gbs": fbytes / (solve_ms / 1e3) / 1e9, "peak_gbs": hbm,
-                                 "frac": fbytes / (solve_ms / 1e3) / 1e9 / hbm,
-                                 "peak_source": hbm_src},
-                    "share_of_step": solve_ms / ms}
+        if modal:
+            tpath = ROOT / "profiles" / f"k3m_traffic_cfg{args.config}.json"
+            traffic, traffic_note = None, None
+            if tpath.exists():
+                tj = json.loads(tpath.read_text())
+                traffic = tj["dram_bytes"]
+                traffic_note = {k: tj[k] for k in tj if k != "dram_bytes"}
+                traffic_note["source"] = str(tpath.relative_to(ROOT))
+            roofline = {"bound": "tensor", "pipe": "fp64 tensor (DMMA m8n8k4, 3M complex)",
+                        "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64,
+                        "traffic": traffic, "traffic_per_launch": traffic_note,
+                        "peak_source": fp64_src,
+                        "kernel": "k_modal_gemm (K3m-T, in-slab transforms of the modal solve)",
+                        "algorithmic_per_app": {"flop": flops, "canonical_block_lu_flop": canon1 * apps,
+                                                "note": "flop counted as 8 per complex multiply-add "
+                                                        "(the 3M product issues 6)"},
+                        "share_of_step": solve_ms / ms}
+        else:
+            roofline = {"bound": "tensor", "pipe": "fp64 tensor (DMMA m8n8k4)", "achieved": ach,
+                        "peak": fp64,
+                        "unit": "TFLOP/s", "frac": ach / fp64, "traffic": traffic,
+                        "traffic_per_launch": traffic_note,
+                        "peak_source": fp64_src,
+                        "kernel": "k_block_solve (K3)",
+                        "algorithmic_per_app": {"flop": flops, "factor_bytes": fbytes},
+                        "hbm_view": {"achieved_gbs": fbytes / (solve_ms / 1e3) / 1e9, "peak_gbs": hbm,
+                                     "frac": fbytes / (solve_ms / 1e3) / 1e9 / hbm,
+                                     "peak_source": hbm_src},
+                        "share_of_step": solve_ms / ms}
     # ---- HBM rooflines of the step kernels (K4/K5/K6; SURVEY §8(d) bytes)
     kernel_rooflines = None
     if ktimes:
         kb = step_kernel_bytes(dp, R)  # per application of the R-RHS batch
+        if modal:
+            kb["modal_recurrence"] = recurrence_bytes(dp, R)
         kernel_rooflines = {}
         for cls, nbytes in kb.items():
             kms = ktimes[cls][0] / args.steps
@@ -387,8 +433,9 @@ def run_ours(args, rank, world, local_rank):
                    "subdomains": list(part.counts), "sweeps": len(SweepPlan.default(part.dim).directions),
                    "factor_ms": factor_ms, "factor_wall_s": factor_wall,
                    "factor_bytes": cache.total_bytes, "distinct_factorizations": cache.count,
-                   "l2": "working set (factors %.2f GB) larger than L2; no flush needed" % (
-                       cache.total_bytes / 1e9),
+                   "l2": "flushed before every timed step (256 MiB zero-fill outside the "
+                         "per-step CUDA events); factors %.2f GB" % (cache.total_bytes / 1e9),
+                   "factor_backend": sorted({f.backend for f in dp._keep[1]}),
                    "parallelism": f"rhs-replicas x{world}"},
         "gpu_launches": int(launches),
         "clocks": clk,

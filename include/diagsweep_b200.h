@@ -246,8 +246,9 @@ DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
 /* Per-kernel-class timing: when enabled, ds_ddm_apply brackets every
  * launch with CUDA events on the context stream (graph replay is bypassed).
  * ds_plan_kernel_times returns summed milliseconds and launch counts for
- * classes {0 assemble (K6), 1 block solve (K3), 2 accumulate (K5),
- * 3 transfer (K4)} since the last reset; blocks the host. */
+ * classes {0 assemble (K6), 1 block solve (K3) / modal transforms (K3m-T),
+ * 2 accumulate (K5), 3 transfer (K4), 4 modal recurrences (K3m-R)} since
+ * the last reset (ms[5], count[5]); blocks the host. */
 DS_API int ds_plan_set_profiling(ds_plan *plan, int32_t enable);
 DS_API int ds_plan_kernel_times(ds_plan *plan, double *ms, int64_t *count,
                                 int32_t reset);

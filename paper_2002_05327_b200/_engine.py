@@ -572,12 +572,13 @@ class DevicePlan:
     def set_profiling(self, enable: bool = True):
         N.check(N.load_library().ds_plan_set_profiling(self.handle, int(bool(enable))))
 
-    KERNEL_CLASSES = ("assemble", "block_solve", "accumulate", "transfer")
+    KERNEL_CLASSES = ("assemble", "block_solve", "accumulate", "transfer", "modal_recurrence")
 
     def kernel_times(self, reset: bool = True) -> dict:
-        """{class: (total_ms, launches)} since the last reset (CUDA events)."""
-        ms = (C.c_double * 4)()
-        cnt = (C.c_int64 * 4)()
+        """{class: (total_ms, launches)} since the last reset (CUDA events);
+        'block_solve' is K3 or the modal transforms (K3m-T)."""
+        ms = (C.c_double * 5)()
+        cnt = (C.c_int64 * 5)()
         N.check(N.load_library().ds_plan_kernel_times(self.handle, ms, cnt, int(reset)))
         return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
 

@@ -172,6 +172,9 @@ struct ModalJob {
 // jobs' factor layouts, for grid sizing)
 int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,
                     int nrhs);
+// one phase of it: 0 forward transforms, 1 recurrences, 2 inverse transforms
+int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host,
+                          int njob, int nrhs, int phase);
 void ds_fill_layout(const OpDev &o, FactDev &f);
 
 int ceil_div(int a, int b);

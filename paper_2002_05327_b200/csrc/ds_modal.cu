@@ -96,24 +96,20 @@ __host__ __device__ inline PassGeo pass_geo(const FactDev &f, const ModalJob &J,
   PassGeo G;
   const int na = f.naxes;
   const bool fwd = pass < na;
-  const int a = fwd ? na - 1 - pass : pass - na;
-  G.n = f.nax[a];
-  int inner = 1, outer = f.nb;
-  for (int b = 0; b < na; ++b) {
-    if (b > a) inner *= f.nax[b];
-    if (b < a) outer *= f.nax[b];
-  }
+  const int a = fwd ? na - 1 - pass : pass - na;  // na <= 2: selects, no local arrays
+  G.n = a == 0 ? f.nax[0] : f.nax[1];
+  const int inner = (a == 0 && na == 2) ? f.nax[1] : 1;
+  G.outer = f.nb * (a == 1 ? f.nax[0] : 1);
   G.ncols = inner * nrhs;
-  G.outer = outer;
-  G.A = fwd ? f.mW[a] : f.mV[a];
-  cplx *buf[2] = {J.s0, J.s1};
+  G.A = fwd ? (a == 0 ? f.mW[0] : f.mW[1]) : (a == 0 ? f.mV[0] : f.mV[1]);
+  auto buf = [&](int i) { return (i & 1) ? J.s1 : J.s0; };
   if (fwd) {
-    G.in = pass == 0 ? J.rhs : buf[(pass - 1) & 1];
-    G.out = buf[pass & 1];
+    G.in = pass == 0 ? J.rhs : buf(pass - 1);
+    G.out = buf(pass);
   } else {
     const int q = pass - na;
-    G.in = buf[(na - 1 + q) & 1];
-    G.out = q == na - 1 ? J.x : buf[(na + q) & 1];
+    G.in = buf(na - 1 + q);
+    G.out = q == na - 1 ? J.x : buf(na + q);
   }
   return G;
 }
@@ -307,16 +303,96 @@ __global__ void __launch_bounds__(256) k_modal_thomas(const ModalJob *__restrict
   }
 }
 
+// K3m-R v2: one half-warp block per 16 consecutive (mode, RHS) columns of a visit.  The
+// whole column block (n_b rows of 256 contiguous bytes) is staged into
+// shared memory with one cp.async per (row, lane), all in flight at once --
+// the v1 kernel above was bound by memory-level parallelism (ncu, config 2:
+// 66 us per launch, 58 SMs with 8 outstanding loads per thread) -- then the
+// recurrences run out of shared memory and the block is written back
+// coalesced.  Arithmetic and order are v1's.
+#define TQ 16
+// mode columns a TQ-column block can touch
+__host__ __device__ inline int thomas_modes(int nrhs) { return (TQ - 1) / nrhs + 2 < TQ ? (TQ - 1) / nrhs + 2 : TQ; }
+__global__ void __launch_bounds__(TQ) k_modal_thomas2(const ModalJob *__restrict__ jobs, int nrhs) {
+  extern __shared__ __align__(16) cplx smem_th[];
+  const ModalJob J = jobs[blockIdx.y];
+  const FactDev &f = *J.f;
+  const int m = f.m, nb = f.nb;
+  const int q0 = blockIdx.x * TQ, t = threadIdx.x, q = q0 + t;
+  if (q0 >= m * nrhs) return;
+  if (!job_any(J, nrhs)) return;
+  const bool live = q < m * nrhs;
+  const int JM = thomas_modes(nrhs), j0 = q0 / nrhs;
+  const int nj = min(JM, m - j0);
+  cplx *sg = smem_th;                  // [nb][TQ] the columns
+  cplx *sm = sg + (size_t)nb * TQ;     // [nb][JM] multipliers
+  cplx *si = sm + (size_t)nb * JM;     // [nb][JM] inverse pivots
+  cplx *su = si + (size_t)nb * JM;     // [nb] block-axis couplings u_k
+  cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
+  const size_t st = (size_t)m * nrhs;
+  for (int k = 0; k < nb; ++k)
+    cp16(sg + k * TQ + t, T + (live ? k * st + q : 0), live ? 16 : 0);
+  for (int e = t; e < nb * nj; e += TQ) {
+    const int k = e / nj, jj = e % nj;
+    cp16(sm + k * JM + jj, f.mmul + (size_t)k * m + j0 + jj, 16);
+    cp16(si + k * JM + jj, f.minv + (size_t)k * m + j0 + jj, 16);
+  }
+  for (int k = t; k < nb; k += TQ) cp16(su + k, f.ucoef + k, 16);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  if (!live) return;
+  const int j = q / nrhs, r = q % nrhs, jj = j - j0;
+  if (J.nz && !J.nz[r]) return;  // exact-zero RHS: never read downstream
+  cplx *p = sg + t;
+  cplx prev = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < nb; k0 += MR) {
+    cplx gv[MR], mv[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k0 + i;
+      if (k < nb) {
+        gv[i] = p[k * TQ];
+        mv[i] = sm[k * JM + jj];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k0 + i;
+      if (k < nb) {
+        prev = k == 0 ? gv[i] : csub(gv[i], cmul(mv[i], prev));
+        p[k * TQ] = prev;
+      }
+    }
+  }
+  cplx y = make_double2(0.0, 0.0);
+  for (int k1 = nb - 1; k1 >= 0; k1 -= MR) {
+    cplx gv[MR], iv[MR], uv[MR];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k1 - i;
+      if (k >= 0) {
+        gv[i] = p[k * TQ];
+        iv[i] = si[k * JM + jj];
+        uv[i] = su[k];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int k = k1 - i;
+      if (k >= 0) {
+        y = k == nb - 1 ? cmul(gv[i], iv[i]) : cmul(csub(gv[i], cmul(uv[i], y)), iv[i]);
+        T[k * st + q] = y;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- launcher
-int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
-                    int nrhs) {
-  if (njob <= 0) return DS_OK;
-  int na = facts[0].naxes;
-  for (int i = 1; i < njob; ++i)
-    if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
-  constexpr int MT = 2, WR = 4, WC = 2, TM = 8 * MT * WR, TN = 16 * WC;
-  ModalJob dummy;
-  memset(&dummy, 0, sizeof(dummy));
+template <int MT, int WR, int WC>
+static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
+                       int pass, int nrhs) {
+  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
   const size_t smem = sizeof(cplx) * 2 * (TM * (MG_TK + 4) + MG_TK * (TN + 2));
   static bool attr_set = false;
   if (!attr_set) {
@@ -324,28 +400,73 @@ int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts,
                                  (int)smem));
     attr_set = true;
   }
-  auto launch_pass = [&](int pass) -> int {
-    int gx = 1, gy = 1;
-    for (int i = 0; i < njob; ++i) {
-      const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
-      gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
-      gy = std::max(gy, (G.n + TM - 1) / TM);
-    }
-    k_modal_gemm<MT, WR, WC><<<dim3(gx, gy, njob), 32 * WR * WC, smem, ctx->stream>>>(jobs_dev, pass, nrhs);
-    ctx->launches++;
-    DS_CHECK_LAUNCH();
-    return DS_OK;
-  };
-  for (int p = 0; p < na; ++p)
-    if (int rc = launch_pass(p)) return rc;
-  int mmax = 1;
-  for (int i = 0; i < njob; ++i) mmax = std::max(mmax, facts[i].m);
-  k_modal_thomas<<<dim3((mmax * nrhs + 255) / 256, njob), 256, 0, ctx->stream>>>(jobs_dev, nrhs);
+  ModalJob dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  int gx = 1, gy = 1;
+  for (int i = 0; i < njob; ++i) {
+    const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
+    gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
+    gy = std::max(gy, (G.n + TM - 1) / TM);
+  }
+  k_modal_gemm<MT, WR, WC><<<dim3(gx, gy, njob), 32 * WR * WC, smem, ctx->stream>>>(jobs_dev, pass, nrhs);
   ctx->launches++;
   DS_CHECK_LAUNCH();
-  for (int p = na; p < 2 * na; ++p)
-    if (int rc = launch_pass(p)) return rc;
   return DS_OK;
+}
+
+// phase 0: forward transforms, 1: mode-wise recurrences, 2: inverse
+// transforms, -1: all three
+int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
+                          int nrhs, int phase) {
+  if (njob <= 0) return DS_OK;
+  const int na = facts[0].naxes;
+  for (int i = 1; i < njob; ++i)
+    if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
+  // transform tile shape (DS_MG: a 64x32, b 40x32, c 120x16, d 64x64)
+  static const char variant = [] {
+    const char *v = getenv("DS_MG");
+    return v && *v ? v[0] : 'a';
+  }();
+  auto launch_pass = [&](int pass) -> int {
+    switch (variant) {
+      case 'b': return launch_gemm<1, 5, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'c': return launch_gemm<3, 5, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'd': return launch_gemm<2, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      default: return launch_gemm<2, 4, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
+    }
+  };
+  if (phase == 0 || phase == -1)
+    for (int p = 0; p < na; ++p)
+      if (int rc = launch_pass(p)) return rc;
+  if (phase == 1 || phase == -1) {
+    int mmax = 1, nbmax = 1;
+    for (int i = 0; i < njob; ++i) {
+      mmax = std::max(mmax, facts[i].m);
+      nbmax = std::max(nbmax, facts[i].nb);
+    }
+    const size_t tsm = sizeof(cplx) * (size_t)nbmax * (TQ + 2 * thomas_modes(nrhs) + 1);
+    static int th_attr = 0;
+    if (tsm <= 200 * 1024 && !getenv("DS_THOMAS_V1")) {
+      if ((int)tsm > th_attr) {
+        DS_CUDA(cudaFuncSetAttribute(k_modal_thomas2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        th_attr = (int)tsm;
+      }
+      k_modal_thomas2<<<dim3((mmax * nrhs + TQ - 1) / TQ, njob), TQ, tsm, ctx->stream>>>(jobs_dev, nrhs);
+    } else {
+      k_modal_thomas<<<dim3((mmax * nrhs + 255) / 256, njob), 256, 0, ctx->stream>>>(jobs_dev, nrhs);
+    }
+    ctx->launches++;
+    DS_CHECK_LAUNCH();
+  }
+  if (phase == 2 || phase == -1)
+    for (int p = na; p < 2 * na; ++p)
+      if (int rc = launch_pass(p)) return rc;
+  return DS_OK;
+}
+
+int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
+                    int nrhs) {
+  return ds_launch_modal_phase(ctx, jobs_dev, facts, njob, nrhs, -1);
 }
 
 // --------------------------------------------------------- factorization

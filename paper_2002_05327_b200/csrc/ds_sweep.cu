@@ -1413,7 +1413,12 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         else rc = ds_launch_solve_table(ctx, P->solvetab + b0, nbl, nrhs, P->max_m);
       }
       if (rc) return rc;
-      if (nmo > 0) rc = ds_launch_modal(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs);
+      if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
+        for (int ph = 0; ph < 3 && !rc; ++ph) {
+          if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
+          rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph);
+        }
+      }
       if (rc) return rc;
       DS_CHECK_LAUNCH();
       prof_mark(P, 2, st);
@@ -1659,17 +1664,18 @@ extern "C" int ds_plan_set_profiling(ds_plan *P, int32_t enable) {
 }
 
 // Sum of event-bracketed durations per kernel class since the last reset
-// (blocks the host).  ms[4], count[4]: assemble, solve, accumulate, transfer.
+// (blocks the host).  ms[5], count[5]: assemble, solve (K3 / modal
+// transforms), accumulate, transfer, modal recurrences.
 extern "C" int ds_plan_kernel_times(ds_plan *P, double *ms, int64_t *count, int32_t reset) {
   if (!P) return ds_fail(DS_ECONFIG, "null plan");
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < 5; ++c) {
     if (ms) ms[c] = 0.0;
     if (count) count[c] = 0;
   }
   if (P->ev_used > 0) DS_CUDA(cudaEventSynchronize(P->ev[P->ev_used - 1]));
   for (size_t i = 0; i + 1 < P->ev_used; ++i) {
     int c = P->ev_class[i];
-    if (c < 0 || c > 3) continue;
+    if (c < 0 || c > 4) continue;
     float t = 0.f;
     DS_CUDA(cudaEventElapsedTime(&t, P->ev[i], P->ev[i + 1]));
     if (ms) ms[c] += t;
