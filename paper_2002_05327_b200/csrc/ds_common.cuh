@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include <string>
 #include <vector>
 
@@ -73,6 +75,39 @@ int ds_fail(int code, const std::string &msg);
       return ds_fail(DS_ECUDA, std::string("kernel launch: ") +            \
                                    cudaGetErrorString(_e));                \
   } while (0)
+
+// ---------------------------------------------- programmatic dependent launch
+// Kernels on the sweep's critical path are launched with programmatic stream
+// serialization: a kernel's CTAs may be scheduled while the previous
+// kernel's last CTAs drain, read only static tables, and wait in
+// griddepcontrol.wait until the previous grid has completed and flushed
+// before touching data it produced.  The wait is a no-op without PDL.
+// DS_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+inline bool ds_pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("DS_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = ds_pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
 
 // ------------------------------------------------------------- handles
 struct ds_ctx {

@@ -142,11 +142,10 @@ __device__ __forceinline__ void cp_wait() {
 // each warp an (8 MT) x 16 sub-tile with DMMA m8n8k4 and the 3M complex
 // product (as K3, ds_mma.cuh).  Row pitches: A % 8 == 4, B % 8 == 2 complex
 // (conflict-free fragment loads).
-#define MG_TK 16
-template <int MT, int WR, int WC>
-__global__ void __launch_bounds__(32 * WR * WC)
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
+__global__ void __launch_bounds__(32 * WR * WC, MINB)
     k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
-  constexpr int TM = 8 * MT * WR, TN = 16 * WC, TK = MG_TK, NTH = 32 * WR * WC;
+  constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
   extern __shared__ __align__(16) cplx smem_mg[];
@@ -160,6 +159,7 @@ __global__ void __launch_bounds__(32 * WR * WC)
   const int total = G.outer * G.ncols;
   const int col0 = blockIdx.x * TN;
   if (row0 >= n || col0 >= total) return;
+  pdl_wait();
   if (!job_any(J, nrhs)) return;
   const int t = threadIdx.x;
   // staging maps: A -- fixed column t % TK, rows t / TK + q * (NTH / TK);
@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(TQ) k_modal_thomas2(const ModalJob *__restrict
   const int m = f.m, nb = f.nb;
   const int q0 = blockIdx.x * TQ, t = threadIdx.x, q = q0 + t;
   if (q0 >= m * nrhs) return;
+  pdl_wait();
   if (!job_any(J, nrhs)) return;
   const bool live = q < m * nrhs;
   const int JM = thomas_modes(nrhs), j0 = q0 / nrhs;
@@ -388,16 +389,134 @@ __global__ void __launch_bounds__(TQ) k_modal_thomas2(const ModalJob *__restrict
   }
 }
 
+// K3m-R v3 (default): segmented recurrences.  v2 above was a single-warp
+// latency chain (ncu: ~39k cycles per block for 2 x 115 dependent complex
+// steps plus issue-bound copy loops, IPC 0.5).  Both sweeps are first-order
+// linear recurrences z_k = b_k + a_k z_{k-1} (forward: a_k = -mul_k,
+// b_k = ghat_k; backward, downwards: a_k = -inv_k u_k, b_k = inv_k g'_k),
+// so each is split into NSEG segments of L blocks: warp s runs segment s
+// for 32 consecutive (mode, RHS) columns from a zero carry while tracking
+// the segment's partial products, warp 0 chains the segment carries
+// (NSEG steps), and every warp adds partial product x carry.  Critical path
+// L + NSEG + 1 steps instead of n_b; forward values stay in registers for
+// the backward sweep; loads are 512-byte coalesced rows.
+template <int L>
+__global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restrict__ jobs, int nrhs) {
+  __shared__ cplx sP[16][32], sZ[16][32], sC[16][32];
+  const ModalJob J = jobs[blockIdx.y];
+  const FactDev &f = *J.f;
+  const int m = f.m, nb = f.nb;
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int nseg = (nb + L - 1) / L;
+  const int q = blockIdx.x * 32 + lane;
+  if (blockIdx.x * 32 >= m * nrhs) return;
+  pdl_wait();
+  if (!job_any(J, nrhs)) return;
+  const bool live = q < m * nrhs;
+  const int qq = live ? q : 0;
+  const int j = qq / nrhs;
+  cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
+  const size_t st = (size_t)m * nrhs;
+  const int k0 = seg * L;
+  const bool act = seg < nseg;
+  // loads of the segment: data, multipliers, inverse pivots, couplings
+  cplx g[L], mu[L], iv[L], uc[L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const int k = k0 + i;
+    const bool in = act && k < nb;
+    g[i] = in ? T[k * st + qq] : make_double2(0.0, 0.0);
+    mu[i] = in ? f.mmul[(size_t)k * m + j] : make_double2(0.0, 0.0);
+  }
+  // ---- forward: z_k = g_k - mul_k z_{k-1}  (mul_0 = 0)
+  cplx P[L];
+  {
+    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const cplx a = make_double2(-mu[i].x, -mu[i].y);
+      z = cadd(g[i], cmul(a, z));
+      pp = cmul(a, pp);
+      g[i] = z;
+      P[i] = pp;
+    }
+    if (act) {
+      sP[seg][lane] = pp;
+      sZ[seg][lane] = z;
+    }
+  }
+  // backward-sweep operands, in flight across the carry chain
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const int k = k0 + i;
+    const bool in = act && k < nb;
+    iv[i] = in ? f.minv[(size_t)k * m + j] : make_double2(0.0, 0.0);
+    uc[i] = in ? f.ucoef[k] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  if (seg == 0) {  // carries into every segment
+    cplx c = make_double2(0.0, 0.0);
+    for (int s2 = 0; s2 < nseg; ++s2) {
+      sC[s2][lane] = c;
+      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const cplx c = sC[seg][lane];
+#pragma unroll
+    for (int i = 0; i < L; ++i) g[i] = cadd(g[i], cmul(P[i], c));  // g'_k
+  }
+  __syncthreads();
+  // ---- backward (k descending): y_k = inv_k g'_k - inv_k u_k y_{k+1}
+  {
+    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      const int k = k0 + i;
+      const bool last = k >= nb - 1;  // k = nb-1 starts the chain (a = 0); k >= nb: padding
+      const cplx b = cmul(iv[i], g[i]);
+      const cplx iu = cmul(iv[i], uc[i]);
+      const cplx a = last ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
+      z = cadd(b, cmul(a, z));
+      pp = cmul(a, pp);
+      g[i] = z;
+      P[i] = pp;
+    }
+    if (act) {
+      sP[seg][lane] = pp;
+      sZ[seg][lane] = z;
+    }
+  }
+  __syncthreads();
+  if (seg == 0) {
+    cplx c = make_double2(0.0, 0.0);
+    for (int s2 = nseg - 1; s2 >= 0; --s2) {
+      sC[s2][lane] = c;
+      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
+    }
+  }
+  __syncthreads();
+  if (!act || !live) return;
+  if (J.nz && !J.nz[q % nrhs]) return;  // exact-zero RHS: never read downstream
+  const cplx c = sC[seg][lane];
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const int k = k0 + i;
+    if (k < nb) T[k * st + q] = cadd(g[i], cmul(P[i], c));
+  }
+}
+
 // ------------------------------------------------------------- launcher
-template <int MT, int WR, int WC>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
                        int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
-  const size_t smem = sizeof(cplx) * 2 * (TM * (MG_TK + 4) + MG_TK * (TN + 2));
+  const size_t smem = sizeof(cplx) * 2 * (TM * (TK + 4) + TK * (TN + 2));
   static bool attr_set = false;
   if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
   ModalJob dummy;
@@ -408,7 +527,8 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
     gy = std::max(gy, (G.n + TM - 1) / TM);
   }
-  k_modal_gemm<MT, WR, WC><<<dim3(gx, gy, njob), 32 * WR * WC, smem, ctx->stream>>>(jobs_dev, pass, nrhs);
+  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
+                     ctx->stream, jobs_dev, pass, nrhs));
   ctx->launches++;
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -422,17 +542,26 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   const int na = facts[0].naxes;
   for (int i = 1; i < njob; ++i)
     if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
-  // transform tile shape (DS_MG: a 64x32, b 40x32, c 120x16, d 64x64)
+  // transform tile shape (DS_MG: a 64x32, b 40x32, c 120x16, d 64x64, e/f a with 3 CTAs/SM or
+  // TK 32, g 32x32 x 4 CTAs/SM, h (default) 16x32 x 8, i 32x16 x 8, j 8x32 x 16, k 16x16 x 16)
   static const char variant = [] {
     const char *v = getenv("DS_MG");
-    return v && *v ? v[0] : 'a';
+    return v && *v ? v[0] : 'h';
   }();
   auto launch_pass = [&](int pass) -> int {
     switch (variant) {
       case 'b': return launch_gemm<1, 5, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'c': return launch_gemm<3, 5, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'd': return launch_gemm<2, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      default: return launch_gemm<2, 4, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'e': return launch_gemm<2, 4, 2, 16, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'f': return launch_gemm<2, 4, 2, 32, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'a': return launch_gemm<2, 4, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'h': return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'i': return launch_gemm<1, 4, 1, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'g': return launch_gemm<1, 4, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'j': return launch_gemm<1, 1, 2, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'k': return launch_gemm<1, 2, 1, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      default: return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
     }
   };
   if (phase == 0 || phase == -1)
@@ -446,12 +575,24 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
     }
     const size_t tsm = sizeof(cplx) * (size_t)nbmax * (TQ + 2 * thomas_modes(nrhs) + 1);
     static int th_attr = 0;
-    if (tsm <= 200 * 1024 && !getenv("DS_THOMAS_V1")) {
+    static const int thv = [] {
+      const char *v = getenv("DS_THOMAS");
+      return v && *v ? atoi(v) : 3;
+    }();
+    if (thv == 3 && nbmax > 64 && nbmax <= 16 * 16) {  // short chains (3D): v2 streams better
+      const int L = nbmax <= 64 ? 4 : (nbmax <= 128 ? 8 : 16);
+      const int nseg = (nbmax + L - 1) / L;
+      const dim3 grid((mmax * nrhs + 31) / 32, njob);
+      if (L == 4) DS_CUDA(launch_pdl(k_modal_thomas3<4>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
+      else if (L == 8) DS_CUDA(launch_pdl(k_modal_thomas3<8>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
+      else DS_CUDA(launch_pdl(k_modal_thomas3<16>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
+    } else if (tsm <= 200 * 1024 && thv >= 2) {
       if ((int)tsm > th_attr) {
         DS_CUDA(cudaFuncSetAttribute(k_modal_thomas2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         th_attr = (int)tsm;
       }
-      k_modal_thomas2<<<dim3((mmax * nrhs + TQ - 1) / TQ, njob), TQ, tsm, ctx->stream>>>(jobs_dev, nrhs);
+      DS_CUDA(launch_pdl(k_modal_thomas2, dim3((mmax * nrhs + TQ - 1) / TQ, njob), dim3(TQ), tsm,
+                         ctx->stream, jobs_dev, nrhs));
     } else {
       k_modal_thomas<<<dim3((mmax * nrhs + 255) / 256, njob), 256, 0, ctx->stream>>>(jobs_dev, nrhs);
     }

@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256)
   const SubDev &sd = subs[V.sub];
   const FactDev fd = *sd.f;
   const int t = threadIdx.x;
+  pdl_wait();
   for (int r = t; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
   const int ns = V.nslot;
   for (int k = t; k < min(ns, SLOT_SMEM); k += blockDim.x) s_slot[k] = slots[V.slot0 + k];
@@ -667,6 +668,7 @@ __global__ void __launch_bounds__(256, K4_MINB(DIM))
   constexpr int NP = 1 + 2 * DIM;
   __shared__ XferRec R;
   const int t = threadIdx.x;
+  pdl_wait();
   // bookkeeping (ddm.py:262-279): one thread per (transfer, RHS) of the launch
   for (int gt = blockIdx.x * blockDim.x + t; gt < nx * nrhs; gt += gridDim.x * blockDim.x) {
     const int i = gt / nrhs, r = gt % nrhs;
@@ -1394,13 +1396,15 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
       prof_mark(P, 0, st);
       if (nrhs % 4 == 0)
-        k_assemble<4><<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
-            P->visits + v0, P->subs, P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
-            P->gcounts[2], F);
+        DS_CUDA(launch_pdl(k_assemble<4>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
+                           (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
+                           (const SlotRef *)P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
+                           P->gcounts[2], F));
       else
-        k_assemble<1><<<dim3(bx, G), 256, sizeof(uint32_t) * P->max_axis_sum, st>>>(
-            P->visits + v0, P->subs, P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
-            P->gcounts[2], F);
+        DS_CUDA(launch_pdl(k_assemble<1>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
+                           (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
+                           (const SlotRef *)P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
+                           P->gcounts[2], F));
       ctx->launches++;
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
@@ -1459,12 +1463,16 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
           const int t0 = P->tile_off[q], nt = P->tile_off[q + 1] - t0;
           const int resident = ctx->num_sms * K4_MINB(dim);
           const int gb = std::max(1, std::max(std::min(nt, resident), (nx * nrhs + 255) / 256));
+          const XferDev *xd = P->xfers + x0;
+          const XferRec *xr = P->recs + x0;
+          const int4 *tl = P->tiles + t0;
+          int *const *fb = P->d_flag_bases;
           if (dim == 2)
-            k_transfer2<2, K4_NPT(2)><<<gb, 256, 0, st>>>(P->xfers + x0, P->recs + x0, P->tiles + t0, nt, nx,
-                                                        P->nsub, nrhs, F, P->d_flag_bases, P->nsweeps);
+            DS_CUDA(launch_pdl(k_transfer2<2, K4_NPT(2)>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
+                               P->nsub, nrhs, F, fb, P->nsweeps));
           else
-            k_transfer2<3, K4_NPT(3)><<<gb, 256, 0, st>>>(P->xfers + x0, P->recs + x0, P->tiles + t0, nt, nx,
-                                                        P->nsub, nrhs, F, P->d_flag_bases, P->nsweeps);
+            DS_CUDA(launch_pdl(k_transfer2<3, K4_NPT(3)>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
+                               P->nsub, nrhs, F, fb, P->nsweeps));
         } else if (dim == 2) {
           if (rv == 4) K4_LAUNCH(4, 2);
           else if (rv == 2) K4_LAUNCH(2, 2);
