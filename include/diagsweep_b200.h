@@ -243,6 +243,16 @@ DS_API int ds_ddm_counters(ds_ctx *ctx, ds_plan *plan, int32_t nrhs,
  * pointers and nrhs); ds_ddm_apply uses the graph when it matches. */
 DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
 
+/* One application from pinned HOST buffers: f_host / u_host are RHS-outer
+ * [nrhs][N] complex128 in page-locked memory.  The source upload runs in
+ * axis-0 row chunks on a copy stream overlapped with the first sweep (each
+ * assembly waits only for the chunks it reads) and every chunk of u is
+ * copied back as soon as the last accumulation touching it has run; the
+ * call is asynchronous on the context stream (synchronize before reading
+ * u_host).  CUDA-graph replay keyed on (f_host, u_host, nrhs). */
+DS_API int ds_ddm_apply_host(ds_ctx *ctx, ds_plan *plan, const ds_cplx *f_host,
+                             ds_cplx *u_host, int32_t nrhs);
+
 /* Per-kernel-class timing: when enabled, ds_ddm_apply brackets every
  * launch with CUDA events on the context stream (graph replay is bypassed).
  * ds_plan_kernel_times returns summed milliseconds and launch counts for

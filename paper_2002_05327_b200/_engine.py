@@ -61,6 +61,11 @@ def context():
 
 # ----------------------------------------------------------------- tensors
 
+def is_pinned_host(v) -> bool:
+    """A page-locked CPU torch tensor (the zero-staging host path)."""
+    return hasattr(v, "detach") and not v.is_cuda and v.is_pinned()
+
+
 def to_device_batch(v, shape):
     """-> (tensor [R, *shape] complex128 contiguous on the GPU, kind, batched)."""
     _require_cuda()
@@ -621,6 +626,16 @@ class DevicePlan:
                 N.check(lib.ds_layout_to_outer(ctx, n, R, partials[w].data_ptr(), p.data_ptr()))
                 parts.append(p)
         return u, parts
+
+    def apply_host(self, f_host, u_host):
+        """One application from a pinned host tensor f_host [R, N] into the
+        pinned host tensor u_host [R, N] (ds_ddm_apply_host: chunked uploads
+        and downloads overlapped with the sweep); synchronous on return."""
+        lib, ctx = context()
+        R = f_host.shape[0]
+        N.check(lib.ds_ddm_apply_host(ctx, self.handle, f_host.data_ptr(), u_host.data_ptr(), R),
+                "ds_ddm_apply_host")
+        torch.cuda.current_stream().synchronize()
 
     def counters(self, nrhs: int):
         lib, ctx = context()

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <map>
@@ -141,6 +142,27 @@ struct ds_plan {
   void *graph_u = nullptr;
   void *graph_partials = nullptr;
   int graph_nrhs = 0;
+  // host-buffer application (ds_ddm_apply_host): node chunks along axis 0,
+  // per launch the chunks of f its assembly needs, per chunk the launch of
+  // the last accumulation touching it; device staging buffers; graph cache
+  bool hio_ready = false;
+  std::vector<struct HioBox> hio_boxes;  // in upload order
+  std::vector<int> hio_need;             // per launch: chunks [0, need) resident
+  std::vector<std::vector<int>> hio_out_at;  // per launch: chunks final after its K5
+  std::vector<int> hio_out_early;        // chunks no K5 touches (zero rows)
+  cplx *hio_fo = nullptr, *hio_fm = nullptr, *hio_uo = nullptr, *hio_um = nullptr;
+  cudaStream_t cstream = nullptr;
+  int side_priority = 0;  // K5 / copy stream priority
+  std::vector<cudaEvent_t> hio_ev_in, hio_ev_out;
+  cudaEvent_t hio_fork = nullptr, hio_join = nullptr;
+  struct HGraph {
+    const void *fh;
+    void *uh;
+    int nrhs;
+    cudaGraphExec_t exec;
+    int64_t launches;
+  };
+  std::vector<HGraph> hgraphs;
   // per-kernel-class timing (0 assemble, 1 solve, 2 accumulate, 3 transfer)
   bool profiling = false;
   std::vector<cudaEvent_t> ev;
@@ -1196,7 +1218,13 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (err != cudaSuccess)
     return fail(ds_fail(DS_ECUDA, std::string("ds_plan_create: ") + cudaGetErrorString(err)));
   if (getenv("DS_K5_SIDE") == nullptr || std::string(getenv("DS_K5_SIDE")) != "0") {
-    if (cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking) != cudaSuccess ||
+    // the K5 and copy streams run at the highest priority (graphs are
+    // instantiated with node priorities): their small grids take SMs as
+    // soon as critical-path CTAs retire instead of queueing behind them
+    int lo_pri = 0, hi_pri = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
+    if (!getenv("DS_NO_PRIORITY")) P->side_priority = hi_pri;
+    if (cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, P->side_priority) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_k5[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_k5[1], cudaEventDisableTiming) != cudaSuccess ||
@@ -1213,6 +1241,12 @@ extern "C" int64_t ds_plan_last_launches(const ds_plan *P) { return P ? P->last_
 extern "C" int ds_plan_destroy(ds_plan *P) {
   if (!P) return DS_OK;
   if (P->graph) cudaGraphExecDestroy(P->graph);
+  for (auto &g : P->hgraphs) cudaGraphExecDestroy(g.exec);
+  if (P->cstream) cudaStreamDestroy(P->cstream);
+  for (auto e : P->hio_ev_in) cudaEventDestroy(e);
+  for (auto e : P->hio_ev_out) cudaEventDestroy(e);
+  if (P->hio_fork) cudaEventDestroy(P->hio_fork);
+  if (P->hio_join) cudaEventDestroy(P->hio_join);
   if (P->gstream) cudaStreamDestroy(P->gstream);
   if (P->side) cudaStreamDestroy(P->side);
   for (cudaEvent_t e : {P->ev_k3, P->ev_k5[0], P->ev_k5[1], P->ev_join})
@@ -1336,6 +1370,8 @@ static int patch_tables(ds_plan *P, int nrhs) {
     cudaGraphExecDestroy(P->graph);
     P->graph = nullptr;
   }
+  for (auto &g : P->hgraphs) cudaGraphExecDestroy(g.exec);  // tables may have moved
+  P->hgraphs.clear();
   return DS_OK;
 }
 
@@ -1365,8 +1401,15 @@ static void prof_mark(ds_plan *P, int cls, cudaStream_t st) {
 // issue the whole application on ctx->stream (capturable)
 // issue launches [q0, q1) of one application on ctx->stream (capturable);
 // mode bit 0: zero u and the flags first; bit 1: join the K5 side stream
+struct HostIO {
+  const cplx *fh;  // pinned host sources, RHS-outer [R][N]
+  cplx *uh;        // pinned host result, RHS-outer [R][N]
+};
+static int hio_in_chunks(ds_plan *P, const HostIO *hio, int nrhs, cudaStream_t cs);
+static int hio_out_chunk(ds_plan *P, const HostIO *hio, int nrhs, int c, cudaStream_t cs);
+
 static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials, int q0 = 0,
-                       int q1 = -1, int mode = 3) {
+                       int q1 = -1, int mode = 3, const HostIO *hio = nullptr) {
   ds_ctx *ctx = P->ctx;
   cudaStream_t st = ctx->stream;
   const int dim = P->dim;
@@ -1380,6 +1423,14 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
     P->k5_pending[0] = P->k5_pending[1] = false;
   }
+  if (hio) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
+    DS_CUDA(cudaEventRecord(P->hio_fork, st));
+    DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_fork, 0));
+    if (int rc = hio_in_chunks(P, hio, nrhs, P->cstream)) return rc;
+    for (int c : P->hio_out_early)
+      if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
+  }
+  int hio_waited = 0;
   const int cap = std::max(1, ctx->num_sms * 4);
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
@@ -1394,6 +1445,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (G == 0) continue;
       const int64_t wmax = P->max_w, smax = P->max_w;
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
+      if (hio && P->hio_need[q] > hio_waited) {  // f chunks this assembly reads
+        hio_waited = P->hio_need[q];
+        DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 1], 0));
+      }
       prof_mark(P, 0, st);
       if (nrhs % 4 == 0)
         DS_CUDA(launch_pdl(k_assemble<4>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
@@ -1443,6 +1498,12 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         DS_CUDA(cudaEventRecord(P->ev_k5[q & 1], s5));
         k5_pending[q & 1] = true;
       }
+      if (hio)  // u chunks whose last accumulation this was: transpose + D2H
+        for (int c : P->hio_out_at[q]) {
+          DS_CUDA(cudaEventRecord(P->hio_ev_out[c], s5));
+          DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_ev_out[c], 0));
+          if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
+        }
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0) {
         prof_mark(P, 3, st);
@@ -1495,8 +1556,260 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaEventRecord(P->ev_join, s5));
     DS_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
   }
+  if (hio) {  // join the copy stream: every u chunk is on the host
+    DS_CUDA(cudaEventRecord(P->hio_join, P->cstream));
+    DS_CUDA(cudaStreamWaitEvent(st, P->hio_join, 0));
+  }
   prof_mark(P, -1, st);
   P->last_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
+// ------------------------------------------- host-buffer application
+// Boxes of the grid (axis 0 x axis 1, axis 2 whole) moved between host and
+// device as units.  Uploads go in the order the first sweep needs them; a
+// box of u goes back as soon as the last accumulation touching it ran.
+struct HioBox {
+  int a0, a1, c0, c1;  // axis-0 rows, axis-1 columns
+};
+
+// box of RHS-outer [R][N] <-> RHS-minor [N][R]: run i (axis-0 row a0 + i) is
+// the contiguous node range [base_i, base_i + L); to_minor: dst[n][r] =
+// src[r][n], else dst[r][n] = src[n][r]; grid (32-tiles of R x L, runs)
+__global__ void k_box_transpose(int R, int L, int64_t N, int64_t base0, int64_t run_stride,
+                                const cplx *__restrict__ src, cplx *__restrict__ dst, int to_minor) {
+  __shared__ cplx tile[32][33];
+  const int ntc = (L + 31) / 32;
+  const int r0 = (blockIdx.x / ntc) * 32, e0 = (blockIdx.x % ntc) * 32;
+  const int64_t base = base0 + (int64_t)blockIdx.y * run_stride;
+  if (to_minor) {
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int r = r0 + i, e = e0 + threadIdx.x;
+      if (r < R && e < L) tile[i][threadIdx.x] = src[(int64_t)r * N + base + e];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int e = e0 + i, r = r0 + threadIdx.x;
+      if (r < R && e < L) dst[(base + e) * R + r] = tile[threadIdx.x][i];
+    }
+  } else {
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int e = e0 + i, r = r0 + threadIdx.x;
+      if (r < R && e < L) tile[threadIdx.x][i] = src[(base + e) * R + r];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int r = r0 + i, e = e0 + threadIdx.x;
+      if (r < R && e < L) dst[(int64_t)r * N + base + e] = tile[i][threadIdx.x];
+    }
+  }
+}
+
+// chunk tables (nrhs-independent) and staging buffers (nrhs_max)
+static int hio_setup(ds_plan *P) {
+  if (P->hio_ready) return DS_OK;
+  // box grid "B0xB1" (DS_HIO_BOXES): axis-1 splits shorten the copy segments
+  // (3D copies of sub-4 KB rows run far below the copy engine's rate)
+  static const std::pair<int, int> split = [] {
+    const char *v = getenv("DS_HIO_BOXES");
+    int a = 8, b = 2;
+    if (v && *v) sscanf(v, "%dx%d", &a, &b);
+    return std::make_pair(std::max(1, a), std::max(1, b));
+  }();
+  const int B0 = std::min(split.first, P->gcounts[0]), B1 = std::min(split.second, P->gcounts[1]);
+  std::vector<HioBox> boxes;
+  for (int i = 0; i < B0; ++i)
+    for (int j = 0; j < B1; ++j)
+      boxes.push_back({(int)((int64_t)P->gcounts[0] * i / B0), (int)((int64_t)P->gcounts[0] * (i + 1) / B0),
+                       (int)((int64_t)P->gcounts[1] * j / B1), (int)((int64_t)P->gcounts[1] * (j + 1) / B1)});
+  const int C = (int)boxes.size();
+  auto meets = [&](const HioBox &B, const int *lo, const int *sh) {
+    return sh[0] > 0 && sh[1] > 0 && lo[0] < B.a1 && lo[0] + sh[0] > B.a0 && lo[1] < B.c1 &&
+           lo[1] + sh[1] > B.c0;
+  };
+  const int nq = (int)P->vstep_off.size() - 1;
+  std::vector<int> first(C, nq), last(C, -1);
+  for (int q = 0; q < nq; ++q)
+    for (int i = P->vstep_off[q]; i < P->vstep_off[q + 1]; ++i) {
+      const VisitDev &V = P->h_visits[i];
+      const SubDev &S = P->h_subs[V.sub];
+      for (int c = 0; c < C; ++c) {
+        if (V.sweep == 1 && meets(boxes[c], S.own_lo, S.own_shape)) first[c] = std::min(first[c], q);
+        if (meets(boxes[c], S.sup_lo, S.sup_shape)) last[c] = q;
+      }
+    }
+  // upload order: by first use (boxes no assembly reads go last)
+  std::vector<int> order(C);
+  for (int c = 0; c < C; ++c) order[c] = c;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return first[x] < first[y]; });
+  P->hio_boxes.clear();
+  for (int c : order) P->hio_boxes.push_back(boxes[c]);
+  std::vector<int> pos(C);
+  for (int k = 0; k < C; ++k) pos[order[k]] = k;
+  P->hio_need.assign(nq, 0);
+  int need = 0;
+  for (int q = 0; q < nq; ++q) {
+    for (int c = 0; c < C; ++c)
+      if (first[c] == q) need = std::max(need, pos[c] + 1);
+    P->hio_need[q] = need;
+  }
+  P->hio_out_at.assign(nq, {});
+  P->hio_out_early.clear();
+  for (int c = 0; c < C; ++c) {
+    if (last[c] < 0) P->hio_out_early.push_back(pos[c]);
+    else P->hio_out_at[last[c]].push_back(pos[c]);
+  }
+  if (getenv("DS_HIO_DEBUG")) {
+    fprintf(stderr, "hio: %d boxes, %d launches; uploads needed by launch:", C, nq);
+    for (int q = 0; q < nq; ++q) fprintf(stderr, " %d", P->hio_need[q]);
+    fprintf(stderr, "\nhio: boxes final after launch:");
+    for (int q = 0; q < nq; ++q) fprintf(stderr, " %d", (int)P->hio_out_at[q].size());
+    fprintf(stderr, "\n");
+  }
+  const size_t bytes = sizeof(cplx) * (size_t)P->nnodes * P->nrhs_max;
+  void *mem;
+  for (cplx **b : {&P->hio_fo, &P->hio_fm, &P->hio_uo, &P->hio_um}) {
+    if (plan_alloc(P, &mem, bytes)) return DS_ECUDA;
+    *b = (cplx *)mem;
+  }
+  DS_CUDA(cudaStreamCreateWithPriority(&P->cstream, cudaStreamNonBlocking, P->side_priority));
+  P->hio_ev_in.resize(C);
+  P->hio_ev_out.resize(C);
+  for (int c = 0; c < C; ++c) {
+    DS_CUDA(cudaEventCreateWithFlags(&P->hio_ev_in[c], cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&P->hio_ev_out[c], cudaEventDisableTiming));
+  }
+  DS_CUDA(cudaEventCreateWithFlags(&P->hio_fork, cudaEventDisableTiming));
+  DS_CUDA(cudaEventCreateWithFlags(&P->hio_join, cudaEventDisableTiming));
+  P->hio_ready = true;
+  return DS_OK;
+}
+
+// one box between pinned host [R][N] and the device staging copy (3D copy:
+// R slices x box rows x box row bytes), plus the layout transpose
+static int hio_box(ds_plan *P, const HostIO *hio, int nrhs, int k, cudaStream_t cs, bool in) {
+  static const int skip = [] {  // diagnostics only: 1 skips uploads, 2 downloads (wrong results)
+    const char *v = getenv("DS_HIO_SKIP");
+    return v && *v ? atoi(v) : 0;
+  }();
+  if ((skip & 1) && in) return DS_OK;
+  if ((skip & 2) && !in) return DS_OK;
+  const HioBox &B = P->hio_boxes[k];
+  const int64_t N = P->nnodes, S1 = P->gcounts[2], S0 = (int64_t)P->gcounts[1] * S1;
+  const int L = (int)((B.c1 - B.c0) * S1), runs = B.a1 - B.a0;
+  if (L <= 0 || runs <= 0) return DS_OK;
+  cudaMemcpy3DParms m = {};
+  cplx *dev = in ? P->hio_fo : P->hio_uo;
+  cplx *host = in ? (cplx *)hio->fh : hio->uh;
+  cudaPitchedPtr hp = make_cudaPitchedPtr(host, sizeof(cplx) * S0, sizeof(cplx) * S0, P->gcounts[0]);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, sizeof(cplx) * S0, sizeof(cplx) * S0, P->gcounts[0]);
+  const cudaPos at = make_cudaPos(sizeof(cplx) * B.c0 * S1, B.a0, 0);
+  m.extent = make_cudaExtent(sizeof(cplx) * L, runs, nrhs);
+  const int64_t base0 = (int64_t)B.a0 * S0 + (int64_t)B.c0 * S1;
+  const dim3 grid((unsigned)(((nrhs + 31) / 32) * ((L + 31) / 32)), runs);
+  if (in) {
+    m.srcPtr = hp;
+    m.srcPos = at;
+    m.dstPtr = dp;
+    m.dstPos = at;
+    m.kind = cudaMemcpyHostToDevice;
+    DS_CUDA(cudaMemcpy3DAsync(&m, cs));
+    k_box_transpose<<<grid, dim3(32, 8), 0, cs>>>(nrhs, L, N, base0, S0, P->hio_fo, P->hio_fm, 1);
+  } else {
+    k_box_transpose<<<grid, dim3(32, 8), 0, cs>>>(nrhs, L, N, base0, S0, P->hio_um, P->hio_uo, 0);
+  }
+  P->ctx->launches++;
+  DS_CHECK_LAUNCH();
+  if (!in) {
+    m.srcPtr = dp;
+    m.srcPos = at;
+    m.dstPtr = hp;
+    m.dstPos = at;
+    m.kind = cudaMemcpyDeviceToHost;
+    DS_CUDA(cudaMemcpy3DAsync(&m, cs));
+  }
+  return DS_OK;
+}
+
+// uploads of every source box in first-use order, one event per box
+static int hio_in_chunks(ds_plan *P, const HostIO *hio, int nrhs, cudaStream_t cs) {
+  for (int k = 0; k < (int)P->hio_boxes.size(); ++k) {
+    if (int rc = hio_box(P, hio, nrhs, k, cs, true)) return rc;
+    DS_CUDA(cudaEventRecord(P->hio_ev_in[k], cs));
+  }
+  return DS_OK;
+}
+
+static int hio_out_chunk(ds_plan *P, const HostIO *hio, int nrhs, int k, cudaStream_t cs) {
+  return hio_box(P, hio, nrhs, k, cs, false);
+}
+
+// One application from pinned host buffers (RHS-outer [R][N]) to pinned host
+// buffers: the source H2D runs in axis-0 row chunks on a copy stream while
+// the first sweep's launches start (each assembly waits only for the chunks
+// it reads), and every chunk of u is transposed and copied back as soon as
+// the last accumulation touching it has run.  CUDA-graph replay keyed on the
+// host pointers (up to 4 cached graphs).
+extern "C" int ds_ddm_apply_host(ds_ctx *ctx, ds_plan *P, const ds_cplx *f_host, ds_cplx *u_host,
+                                 int32_t nrhs) {
+  if (!ctx || !P || !f_host || !u_host) return ds_fail(DS_ECONFIG, "ds_ddm_apply_host: null argument");
+  if (nrhs < 1 || nrhs > P->nrhs_max)
+    return ds_fail(DS_ECONFIG, "ds_ddm_apply_host: nrhs exceeds the plan's nrhs_max");
+  if (P->nranks > 1) return ds_fail(DS_ECONFIG, "ds_ddm_apply_host: sharded plans run through ds_ddm_apply_range");
+  if (ctx != P->ctx) P->ctx = ctx;
+  int rc = patch_tables(P, nrhs);
+  if (rc) return rc;
+  if ((rc = hio_setup(P))) return rc;
+  if (P->slots_dirty) {
+    for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
+    P->slots_dirty = false;
+  }
+  HostIO hio{(const cplx *)f_host, (cplx *)u_host};
+  if (!P->use_graph || P->profiling) {
+    rc = issue_apply(P, P->hio_fm, P->hio_um, nrhs, nullptr, 0, -1, 3, &hio);
+    if (rc) P->slots_dirty = true;
+    return rc;
+  }
+  if (!P->gstream) {
+    DS_CUDA(cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking));
+    DS_CUDA(cudaEventCreateWithFlags(&P->gev_in, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&P->gev_out, cudaEventDisableTiming));
+  }
+  cudaStream_t user = ctx->stream;
+  ds_plan::HGraph *G = nullptr;
+  for (auto &g : P->hgraphs)
+    if (g.fh == f_host && g.uh == u_host && g.nrhs == nrhs) G = &g;
+  DS_CUDA(cudaEventRecord(P->gev_in, user));
+  DS_CUDA(cudaStreamWaitEvent(P->gstream, P->gev_in, 0));
+  if (!G) {
+    if (P->hgraphs.size() >= 4) {
+      cudaGraphExecDestroy(P->hgraphs.front().exec);
+      P->hgraphs.erase(P->hgraphs.begin());
+    }
+    cudaGraph_t g;
+    ctx->stream = P->gstream;
+    DS_CUDA(cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = ctx->launches;
+    rc = issue_apply(P, P->hio_fm, P->hio_um, nrhs, nullptr, 0, -1, 3, &hio);
+    cudaError_t e = cudaStreamEndCapture(P->gstream, &g);
+    ctx->stream = user;
+    if (rc) {
+      P->slots_dirty = true;
+      return rc;
+    }
+    if (e != cudaSuccess) return ds_fail(DS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    ds_plan::HGraph h{f_host, u_host, nrhs, nullptr, ctx->launches - l0};
+    DS_CUDA(cudaGraphInstantiate(&h.exec, g, cudaGraphInstantiateFlagUseNodePriority));
+    cudaGraphDestroy(g);
+    ctx->launches = l0;
+    P->hgraphs.push_back(h);
+    G = &P->hgraphs.back();
+  }
+  DS_CUDA(cudaGraphLaunch(G->exec, P->gstream));
+  DS_CUDA(cudaEventRecord(P->gev_out, P->gstream));
+  DS_CUDA(cudaStreamWaitEvent(user, P->gev_out, 0));
+  ctx->launches += G->launches;
+  P->last_launches = G->launches;
   return DS_OK;
 }
 
@@ -1544,7 +1857,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
         return rc;
       }
       if (e != cudaSuccess) return ds_fail(DS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-      DS_CUDA(cudaGraphInstantiate(&P->graph, g, 0));
+      DS_CUDA(cudaGraphInstantiate(&P->graph, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
       P->graph_f = f;
       P->graph_u = u;

@@ -211,6 +211,27 @@ def diagonal_sweep_solve(f, partition: Partition, operators: dict,
     if warn_collar:
         _warn_collar(f, partition)
     plan = plan or SweepPlan.default(partition.dim)
+    if (_engine.is_pinned_host(f) and not collect_partials
+            and (f.shape[0] if shape[1:] == counts else 1) <= 256):
+        # pinned host sources: uploads / downloads overlapped with the sweep
+        # inside the library (ds_ddm_apply_host); result in pinned memory
+        import torch
+
+        batched = shape[1:] == counts
+        fh = f if batched else f.reshape((1,) + counts)
+        fh = fh.reshape(fh.shape[0], -1)
+        if fh.dtype != torch.complex128 or not fh.is_contiguous():
+            fh = fh.to(torch.complex128).contiguous().pin_memory()
+        R = fh.shape[0]
+        dp = device_plan(partition, operators, cache, plan, R)
+        uh = torch.empty(fh.shape, dtype=torch.complex128, pin_memory=True)
+        dp.apply_host(fh, uh)
+        reports = _reports(dp, R, plan, partition, record_events, record_transfers)
+        wall = time.perf_counter() - t0
+        for rep in reports:
+            rep.wall_time = wall
+        values = uh.reshape((R,) + counts) if batched else uh.reshape(counts)
+        return ComplexField(partition.grid, values), (reports if batched else reports[0])
     fdev, kind, batched = _engine.to_device_batch(f, counts)
     R = fdev.shape[0]
     chunk = 256
