@@ -181,21 +181,32 @@ def axis_tridiagonal(op, axis: int) -> np.ndarray:
     return T
 
 
+_EIG_CACHE: dict = {}
+
+
+def _axis_eig(T: np.ndarray):
+    """(V, V^{-1}, lambda) of one 1D matrix, memoised on its bytes (windows
+    of a partition share most of their per-axis operators)."""
+    key = T.tobytes()
+    hit = _EIG_CACHE.get(key)
+    if hit is None:
+        lam, V = np.linalg.eig(T)
+        W = np.linalg.inv(V)
+        hit = (np.ascontiguousarray(V, dtype=np.complex128),
+               np.ascontiguousarray(W, dtype=np.complex128),
+               np.ascontiguousarray(lam, dtype=np.complex128))
+        if len(_EIG_CACHE) > 4096:
+            _EIG_CACHE.clear()
+        _EIG_CACHE[key] = hit
+    return hit
+
+
 def modal_decomposition(op):
     """Eigen-decompositions T_a = V diag(lambda) V^{-1} of the in-slab axes
     (LAPACK zgeev through NumPy; n_a <= a few hundred, O(n_a^3) each).
     Returns (block_axis, [(V, V^{-1}, lambda), ...]) in in-slab axis order."""
     ba = block_axis_of(op.window.shape)
-    out = []
-    for a in range(op.dim):
-        if a == ba:
-            continue
-        lam, V = np.linalg.eig(axis_tridiagonal(op, a))
-        W = np.linalg.inv(V)
-        out.append((np.ascontiguousarray(V, dtype=np.complex128),
-                    np.ascontiguousarray(W, dtype=np.complex128),
-                    np.ascontiguousarray(lam, dtype=np.complex128)))
-    return ba, out
+    return ba, [_axis_eig(axis_tridiagonal(op, a)) for a in range(op.dim) if a != ba]
 
 
 class FactorSet:
