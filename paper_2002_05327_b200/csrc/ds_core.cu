@@ -149,37 +149,56 @@ __device__ __forceinline__ double op_kappa2(const OpDev &o, const int *c) {
 // One thread per (region node, rhs).  rlo = region offset inside the
 // operator window.  Order of accumulation follows pml.py:144-158.
 // layout 0: RHS-minor [nodes][nrhs]; layout 1: RHS-outer [nrhs][nodes].
-__global__ void k_apply(OpDev o, const cplx *__restrict__ v, cplx *__restrict__ out,
+// Index arithmetic is 32-bit (a region has < 2^31 nodes; RHS-outer: one
+// grid row per RHS, RHS-minor: (node, rhs) pairs < 2^31 checked by the
+// launcher) -- the first version's 64-bit div/mod per element made it
+// instruction-bound at 34% of HBM (config 3, tools/k1_k7_bench.py).
+__global__ void __launch_bounds__(256) k_apply(OpDev o, const cplx *__restrict__ v, cplx *__restrict__ out,
                         int nrhs, int rlo0, int rlo1, int rlo2, int rs0, int rs1,
                         int rs2, int outer) {
-  const int64_t nodes = (int64_t)rs0 * rs1 * rs2;
-  int64_t total = nodes * nrhs;
-  int rlo[3] = {rlo0, rlo1, rlo2};
-  int rs[3] = {rs0, rs1, rs2};
-  const int64_t ns = outer ? 1 : nrhs;  // node stride
-  int64_t strides[3];
-  strides[2] = ns;
-  strides[1] = (int64_t)rs2 * ns;
-  strides[0] = (int64_t)rs1 * rs2 * ns;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int64_t node = outer ? q % nodes : q / nrhs;
-    int e[3];
-    e[2] = node % rs2;
-    int64_t t = node / rs2;
-    e[1] = t % rs1;
-    e[0] = t / rs1;
-    int c[3] = {e[0] + rlo[0], e[1] + rlo[1], e[2] + rlo[2]};
-    cplx vc = v[q];
-    double k2 = op_kappa2(o, c);
-    cplx acc = cscale(vc, k2);
-    for (int a = 0; a < o.dim; ++a) {
-      cplx lo = o.c_lo[a][c[a]], hi = o.c_hi[a][c[a]];
-      acc = cadd(acc, cmul(make_double2(-(lo.x + hi.x), -(lo.y + hi.y)), vc));
-      if (e[a] > 0) acc = cadd(acc, cmul(lo, v[q - strides[a]]));
-      if (e[a] < rs[a] - 1) acc = cadd(acc, cmul(hi, v[q + strides[a]]));
+  const int nodes = rs0 * rs1 * rs2;
+  const int ns = outer ? 1 : nrhs;  // node stride
+  const int st2 = ns, st1 = rs2 * ns, st0 = rs1 * rs2 * ns;
+  const int total = outer ? nodes : nodes * nrhs;
+  const int64_t base = outer ? (int64_t)blockIdx.y * nodes : 0;
+  const cplx *__restrict__ vb = v + base;
+  cplx *__restrict__ ob = out + base;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < total; q += gridDim.x * blockDim.x) {
+    const int node = outer ? q : q / nrhs;
+    const int e2 = node % rs2, t = node / rs2;
+    const int e1 = t % rs1, e0 = t / rs1;
+    const int c[3] = {e0 + rlo0, e1 + rlo1, e2 + rlo2};
+    const int e[3] = {e0, e1, e2};
+    const int rs[3] = {rs0, rs1, rs2};
+    const int str[3] = {st0, st1, st2};
+    // all loads first: centre, neighbours, couplings, kappa^2
+    const cplx vc = vb[q];
+    cplx vm[3], vp[3], lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= o.dim) break;
+      vm[a] = e[a] > 0 ? vb[q - str[a]] : vc;
+      vp[a] = e[a] < rs[a] - 1 ? vb[q + str[a]] : vc;
+      lo[a] = o.c_lo[a][c[a]];
+      hi[a] = o.c_hi[a][c[a]];
     }
-    out[q] = acc;
+    double k2;
+    if (o.kappa2_kind == 0) k2 = o.kappa2[0];
+    else if (o.kappa2_kind == 1) k2 = o.kappa2[c[o.kappa2_axis]];
+    else {
+      int64_t lin = c[0];
+      for (int a = 1; a < o.dim; ++a) lin = lin * o.shape[a] + c[a];
+      k2 = o.kappa2[lin];
+    }
+    cplx acc = cscale(vc, k2);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= o.dim) break;
+      acc = cadd(acc, cmul(make_double2(-(lo[a].x + hi[a].x), -(lo[a].y + hi[a].y)), vc));
+      if (e[a] > 0) acc = cadd(acc, cmul(lo[a], vm[a]));
+      if (e[a] < rs[a] - 1) acc = cadd(acc, cmul(hi[a], vp[a]));
+    }
+    ob[q] = acc;
   }
 }
 
@@ -203,10 +222,18 @@ extern "C" int ds_op_apply(ds_ctx *ctx, const ds_op *op, const ds_cplx *v, ds_cp
     if (lo[a] < 0 || sh[a] < 1 || lo[a] + sh[a] > o.shape[a])
       return ds_fail(DS_ECONFIG, "ds_op_apply: region outside the operator window");
   }
-  int64_t total = (int64_t)sh[0] * sh[1] * sh[2] * nrhs;
-  k_apply<<<grid_for(ctx, total, 256), 256, 0, ctx->stream>>>(
-      o, (const cplx *)v, (cplx *)out, nrhs, lo[0], lo[1], lo[2], sh[0], sh[1], sh[2],
-      layout != 0);
+  const int64_t nodes = (int64_t)sh[0] * sh[1] * sh[2];
+  if (nodes * (layout != 0 ? 1 : nrhs) >= (int64_t)1 << 31 || nrhs > 65535)
+    return ds_fail(DS_ECONFIG, "ds_op_apply: region too large for one launch");
+  if (layout != 0) {
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((nodes + 255) / 256,
+                                                               (int64_t)ctx->num_sms * 16 / nrhs + 1));
+    k_apply<<<dim3(bx, nrhs), 256, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, nrhs, lo[0], lo[1],
+                                                     lo[2], sh[0], sh[1], sh[2], 1);
+  } else {
+    k_apply<<<grid_for(ctx, nodes * nrhs, 256), 256, 0, ctx->stream>>>(
+        o, (const cplx *)v, (cplx *)out, nrhs, lo[0], lo[1], lo[2], sh[0], sh[1], sh[2], 0);
+  }
   ctx->launches++;
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -359,8 +386,10 @@ __global__ void k_combine(int64_t n, int nrhs, int nvec, CombineArgs args,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     cplx acc = make_double2(0.0, 0.0);
-    for (int j = 0; j < nvec; ++j) acc = cadd(acc, cmul(c[j * nrhs + r], args.x[j][base + i]));
-    y[base + i] = cadd(y[base + i], acc);
+    const cplx yv = y[base + i];
+#pragma unroll 8
+    for (int j = 0; j < nvec; ++j) acc = cadd(acc, cmul(__ldg(c + j * nrhs + r), args.x[j][base + i]));
+    y[base + i] = cadd(yv, acc);
   }
 }
 

@@ -142,25 +142,18 @@ __device__ __forceinline__ void cp_wait() {
 // each warp an (8 MT) x 16 sub-tile with DMMA m8n8k4 and the 3M complex
 // product (as K3, ds_mma.cuh).  Row pitches: A % 8 == 4, B % 8 == 2 complex
 // (conflict-free fragment loads).
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
-__global__ void __launch_bounds__(32 * WR * WC, MINB)
-    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
+// The tile body: rows [row0, row0 + TM) x columns [col0, col0 + colw),
+// colw <= TN (columns past colw are zero-filled and not stored; warps whose
+// 16 columns are all past colw skip the products).
+template <int MT, int WR, int WC, int TK>
+__device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw,
+                                          cplx *smem_mg) {
   constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
-  extern __shared__ __align__(16) cplx smem_mg[];
   auto sA = [&](int buf) { return smem_mg + buf * (TM * AP); };
   auto sB = [&](int buf) { return smem_mg + 2 * TM * AP + buf * (TK * BP); };
-  const ModalJob J = jobs[blockIdx.z];
-  const FactDev f = *J.f;
-  const PassGeo G = pass_geo(f, J, pass, nrhs);
   const int n = G.n;
-  const int row0 = blockIdx.y * TM;
-  const int total = G.outer * G.ncols;
-  const int col0 = blockIdx.x * TN;
-  if (row0 >= n || col0 >= total) return;
-  pdl_wait();
-  if (!job_any(J, nrhs)) return;
   const int t = threadIdx.x;
   // staging maps: A -- fixed column t % TK, rows t / TK + q * (NTH / TK);
   // B -- fixed column t % TN, rows t / TN + q * (NTH / TN)
@@ -169,7 +162,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   const int b_col = t % TN, b_row = t / TN;
   constexpr int B_STEP = NTH / TN, B_N = (TK + B_STEP - 1) / B_STEP;
   const int gcol = col0 + b_col;
-  const bool bcol_ok = gcol < total;
+  const bool bcol_ok = b_col < colw;
   const int64_t bbase = bcol_ok ? (int64_t)(gcol / G.ncols) * n * G.ncols + gcol % G.ncols : 0;
   auto stage = [&](int kc, int buf) {
     const int k0 = kc * TK;
@@ -191,6 +184,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   };
   const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
   const int wr = warp % WR, wc = warp / WR;
+  const bool wact = wc * 16 < colw;
   double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
   const int nkc = (n + TK - 1) / TK;
   stage(0, 0);
@@ -203,29 +197,32 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
       cp_wait<0>();
     }
     __syncthreads();
-    const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
-    const cplx *Bs = sB(buf) + tg * BP + wc * 16 + g;
+    if (wact) {
+      const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
+      const cplx *Bs = sB(buf) + tg * BP + wc * 16 + g;
 #pragma unroll
-    for (int k4 = 0; k4 < TK / 4; ++k4) {
-      cplx a[MT], b[2];
+      for (int k4 = 0; k4 < TK / 4; ++k4) {
+        cplx a[MT], b[2];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) a[mt] = As[mt * 8 * AP + k4 * 4];
+        for (int mt = 0; mt < MT; ++mt) a[mt] = As[mt * 8 * AP + k4 * 4];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[k4 * 4 * BP + nt * 8];
-      double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
+        for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[k4 * 4 * BP + nt * 8];
+        double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const double as = a[mt].x + a[mt].y;
+        for (int mt = 0; mt < MT; ++mt) {
+          const double as = a[mt].x + a[mt].y;
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma(p1[mt][nt], a[mt].x, b[nt].x);
-          dmma(p2[mt][nt], a[mt].y, b[nt].y);
-          dmma(p3[mt][nt], as, bs[nt]);
+          for (int nt = 0; nt < 2; ++nt) {
+            dmma(p1[mt][nt], a[mt].x, b[nt].x);
+            dmma(p2[mt][nt], a[mt].y, b[nt].y);
+            dmma(p3[mt][nt], as, bs[nt]);
+          }
         }
       }
     }
     __syncthreads();
   }
+  if (!wact) return;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int gr = row0 + wr * 8 * MT + mt * 8 + g;
@@ -234,13 +231,32 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int gc = col0 + wc * 16 + nt * 8 + 2 * tg + e;
-        if (gc >= total) continue;
+        const int cc = wc * 16 + nt * 8 + 2 * tg + e;
+        if (cc >= colw) continue;
+        const int gc = col0 + cc;
         const int64_t off = (int64_t)(gc / G.ncols) * n * G.ncols + (int64_t)gr * G.ncols + gc % G.ncols;
         G.out[off] = make_double2(p1[mt][nt][e] - p2[mt][nt][e],
                                   p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
       }
   }
+}
+
+// one tile per CTA: grid (column tiles, row tiles, visits)
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
+__global__ void __launch_bounds__(32 * WR * WC, MINB)
+    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
+  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
+  extern __shared__ __align__(16) cplx smem_mg[];
+  const ModalJob J = jobs[blockIdx.z];
+  const FactDev f = *J.f;
+  const PassGeo G = pass_geo(f, J, pass, nrhs);
+  const int row0 = blockIdx.y * TM;
+  const int total = G.outer * G.ncols;
+  const int col0 = blockIdx.x * TN;
+  if (row0 >= G.n || col0 >= total) return;
+  pdl_wait();
+  if (!job_any(J, nrhs)) return;
+  gemm_tile<MT, WR, WC, TK>(G, row0, col0, min(TN, total - col0), smem_mg);
 }
 
 // ------------------------------------------- mode-wise recurrences (K3m-R)
@@ -529,6 +545,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
   }
   DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
                      ctx->stream, jobs_dev, pass, nrhs));
+
   ctx->launches++;
   DS_CHECK_LAUNCH();
   return DS_OK;
