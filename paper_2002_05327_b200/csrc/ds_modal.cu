@@ -523,6 +523,103 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
   }
 }
 
+// K3m-R v4 (DS_THOMAS=4): v3's segmented recurrences with the column block staged
+// in shared memory (cp.async, every row in flight at once) and the segment
+// values recomputed from the exact carry instead of kept as partial
+// products: a handful of registers per thread, so three 480-thread blocks
+// share an SM (v3 needed ~160 registers for g, P and the coefficients: one
+// block per SM, 3.1 waves on an 8-visit launch of config 2).  Measured under
+// graph replay it ties v3 on config 2 (the recurrences cost ~0.56 ms of a
+// 5.7 ms application either way, DS_SKIP=4) and loses to v2 on config 4.
+__global__ void __launch_bounds__(512) k_modal_thomas4(const ModalJob *__restrict__ jobs, int nrhs,
+                                                       int L) {
+  extern __shared__ __align__(16) cplx sg[];  // [nb][32]
+  __shared__ cplx sP[16][32], sZ[16][32], sC[16][32];
+  const ModalJob J = jobs[blockIdx.y];
+  const FactDev &f = *J.f;
+  const int m = f.m, nb = f.nb;
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nseg = (nb + L - 1) / L;
+  const int q0 = blockIdx.x * 32, q = q0 + lane;
+  if (q0 >= m * nrhs) return;
+  pdl_wait();
+  if (!job_any(J, nrhs)) return;
+  const bool live = q < m * nrhs;
+  const int j = (live ? q : q0) / nrhs;
+  cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
+  const size_t st = (size_t)m * nrhs;
+  for (int k = seg; k < nb; k += nw)
+    cp16(sg + k * 32 + lane, T + (live ? k * st + q : 0), live ? 16 : 0);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  const cplx *mul = f.mmul + j, *inv = f.minv + j, *uc = f.ucoef;
+  const int k0 = seg * L, k1 = min(nb, k0 + L);
+  const bool act = seg < nseg;
+  // ---- forward z_k = g_k - mul_k z_{k-1}: segment totals from a zero carry
+  if (act) {
+    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
+    for (int k = k0; k < k1; ++k) {
+      const cplx mk = __ldg(mul + (size_t)k * m);
+      const cplx a = make_double2(-mk.x, -mk.y);
+      z = cadd(sg[k * 32 + lane], cmul(a, z));
+      pp = cmul(a, pp);
+    }
+    sP[seg][lane] = pp;
+    sZ[seg][lane] = z;
+  }
+  __syncthreads();
+  if (seg == 0) {
+    cplx c = make_double2(0.0, 0.0);
+    for (int s2 = 0; s2 < nseg; ++s2) {
+      sC[s2][lane] = c;
+      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
+    }
+  }
+  __syncthreads();
+  if (act) {  // the segment again from its exact carry: g'_k
+    cplx x = sC[seg][lane];
+    for (int k = k0; k < k1; ++k) {
+      const cplx mk = __ldg(mul + (size_t)k * m);
+      x = cadd(sg[k * 32 + lane], cmul(make_double2(-mk.x, -mk.y), x));
+      sg[k * 32 + lane] = x;
+    }
+  }
+  __syncthreads();
+  // ---- backward (k descending): y_k = inv_k g'_k - inv_k u_k y_{k+1}
+  if (act) {
+    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
+    for (int k = k1 - 1; k >= k0; --k) {
+      const cplx ik = __ldg(inv + (size_t)k * m);
+      const cplx iu = cmul(ik, __ldg(uc + k));
+      const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
+      z = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, z));
+      pp = cmul(a, pp);
+    }
+    sP[seg][lane] = pp;
+    sZ[seg][lane] = z;
+  }
+  __syncthreads();
+  if (seg == 0) {
+    cplx c = make_double2(0.0, 0.0);
+    for (int s2 = nseg - 1; s2 >= 0; --s2) {
+      sC[s2][lane] = c;
+      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
+    }
+  }
+  __syncthreads();
+  if (!act || !live) return;
+  if (J.nz && !J.nz[q % nrhs]) return;  // exact-zero RHS: never read downstream
+  cplx y = sC[seg][lane];
+  for (int k = k1 - 1; k >= k0; --k) {
+    const cplx ik = __ldg(inv + (size_t)k * m);
+    const cplx iu = cmul(ik, __ldg(uc + k));
+    const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
+    y = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, y));
+    T[k * st + q] = y;
+  }
+}
+
 // ------------------------------------------------------------- launcher
 template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
@@ -560,10 +657,11 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   for (int i = 1; i < njob; ++i)
     if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
   // transform tile shape (DS_MG: a 64x32, b 40x32, c 120x16, d 64x64, e/f a with 3 CTAs/SM or
-  // TK 32, g 32x32 x 4 CTAs/SM, h (default) 16x32 x 8, i 32x16 x 8, j 8x32 x 16, k 16x16 x 16)
+  // TK 32, g 32x32 x 4 CTAs/SM, h 16x32 x 8, i 32x16 x 8, j 8x32 x 16, k 16x16 x 16,
+  // n 16x64 x 4, o (default) 32x32 with 2x2 warps of 16x16, p TK 32, q 8x64)
   static const char variant = [] {
     const char *v = getenv("DS_MG");
-    return v && *v ? v[0] : 'h';
+    return v && *v ? v[0] : 'o';
   }();
   auto launch_pass = [&](int pass) -> int {
     switch (variant) {
@@ -578,6 +676,10 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
       case 'g': return launch_gemm<1, 4, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'j': return launch_gemm<1, 1, 2, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'k': return launch_gemm<1, 2, 1, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'n': return launch_gemm<1, 2, 4, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'o': return launch_gemm<2, 2, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'p': return launch_gemm<1, 2, 2, 32, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'q': return launch_gemm<1, 1, 4, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
       default: return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
     }
   };
@@ -596,7 +698,18 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
       const char *v = getenv("DS_THOMAS");
       return v && *v ? atoi(v) : 3;
     }();
-    if (thv == 3 && nbmax > 64 && nbmax <= 16 * 16) {  // short chains (3D): v2 streams better
+    if (thv == 4 && nbmax <= 200) {
+      const int L = std::max(4, (nbmax + 15) / 16);
+      const int nseg = (nbmax + L - 1) / L;
+      const size_t sm4 = sizeof(cplx) * (size_t)nbmax * 32;
+      static int th4_attr = 0;
+      if ((int)sm4 > th4_attr) {
+        DS_CUDA(cudaFuncSetAttribute(k_modal_thomas4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4));
+        th4_attr = (int)sm4;
+      }
+      DS_CUDA(launch_pdl(k_modal_thomas4, dim3((mmax * nrhs + 31) / 32, njob), dim3(32 * nseg), sm4,
+                         ctx->stream, jobs_dev, nrhs, L));
+    } else if (thv == 3 && nbmax > 64 && nbmax <= 16 * 16) {  // short chains (3D): v2 streams better
       const int L = nbmax <= 64 ? 4 : (nbmax <= 128 ? 8 : 16);
       const int nseg = (nbmax + L - 1) / L;
       const dim3 grid((mmax * nrhs + 31) / 32, njob);

@@ -1431,6 +1431,13 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
   }
   int hio_waited = 0;
+  // diagnostics only (wrong results): DS_SKIP bitmask drops kernel classes
+  // from the schedule to measure their marginal time under graph replay
+  // (1 K6, 2 modal transforms, 4 modal recurrences, 8 K4, 16 K5)
+  static const int skip_cls = [] {
+    const char *v = getenv("DS_SKIP");
+    return v && *v ? atoi(v) : 0;
+  }();
   const int cap = std::max(1, ctx->num_sms * 4);
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
@@ -1450,7 +1457,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 1], 0));
       }
       prof_mark(P, 0, st);
-      if (nrhs % 4 == 0)
+      if (skip_cls & 1) {
+      } else if (nrhs % 4 == 0)
         DS_CUDA(launch_pdl(k_assemble<4>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
                            (const SlotRef *)P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
@@ -1475,6 +1483,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
         for (int ph = 0; ph < 3 && !rc; ++ph) {
           if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
+          if (skip_cls & (ph == 1 ? 4 : 2)) continue;
           rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph);
         }
       }
@@ -1486,7 +1495,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         DS_CUDA(cudaEventRecord(P->ev_k3, st));
         DS_CUDA(cudaStreamWaitEvent(s5, P->ev_k3, 0));
       }
-      if (nrhs % 4 == 0)
+      if (skip_cls & 16) {
+      } else if (nrhs % 4 == 0)
         k_accumulate<4><<<dim3(by, G), 256, 0, s5>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
                                                      P->gcounts[0], P->gcounts[1], P->gcounts[2]);
       else
@@ -1505,7 +1515,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
           if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
         }
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
-      if (nx > 0) {
+      if (nx > 0 && !(skip_cls & 8)) {
         prof_mark(P, 3, st);
         int bz = std::max(1, std::min(64, 2 * cap / nx));
         static const int k4rv = [] {
