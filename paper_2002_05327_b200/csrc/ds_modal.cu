@@ -39,6 +39,8 @@
 #include "ds_common.cuh"
 #include "ds_mma.cuh"
 
+#define RMAX_MODAL 256
+
 // ------------------------------------------------------------ pivots (K2m)
 struct PivJob {
   FactDev f;
@@ -88,7 +90,8 @@ struct PassGeo {
   const cplx *A;
   const cplx *in;
   cplx *out;
-  int n, ncols, outer;
+  int n, ncols, outer;  // ncols = inner * nrhs: row stride of a batch matrix
+  int inner;            // inner in-slab extent (3D pass along axis 0), else 1
 };
 
 __host__ __device__ inline PassGeo pass_geo(const FactDev &f, const ModalJob &J, int pass,
@@ -101,6 +104,7 @@ __host__ __device__ inline PassGeo pass_geo(const FactDev &f, const ModalJob &J,
   const int inner = (a == 0 && na == 2) ? f.nax[1] : 1;
   G.outer = f.nb * (a == 1 ? f.nax[0] : 1);
   G.ncols = inner * nrhs;
+  G.inner = inner;
   G.A = fwd ? (a == 0 ? f.mW[0] : f.mW[1]) : (a == 0 ? f.mV[0] : f.mV[1]);
   auto buf = [&](int i) { return (i & 1) ? J.s1 : J.s0; };
   if (fwd) {
@@ -119,6 +123,36 @@ __device__ __forceinline__ bool job_any(const ModalJob &J, int nrhs) {
   int any = 0;
   for (int r = 0; r < nrhs; ++r) any |= J.nz[r];
   return any != 0;
+}
+
+// Active (nonzero) RHS columns of a visit, in order, into shared memory:
+// the reference skips exact-zero solves (ddm.py:256-258); here the
+// transforms and recurrences also skip the exact-zero RHS columns of
+// visits with some nonzero RHS (config 2: 42% of the (visit, RHS) pairs are
+// nonzero, 87% of the visits).  Returns the count; call from all threads.
+__device__ __forceinline__ int active_rhs(const ModalJob &J, int nrhs, int *act) {
+  if (threadIdx.x < 32) {
+    int base = 0;
+    for (int r0 = 0; r0 < nrhs; r0 += 32) {
+      const int r = r0 + (int)threadIdx.x;
+      const bool on = r < nrhs && (!J.nz || J.nz[r]);
+      const unsigned mk = __ballot_sync(0xffffffffu, on);
+      if (on) act[base + __popc(mk & ((1u << threadIdx.x) - 1))] = r;
+      base += __popc(mk);
+    }
+    if (threadIdx.x == 0) act[RMAX_MODAL] = base;
+  }
+  __syncthreads();
+  return act[RMAX_MODAL];
+}
+
+// compact column c (outer x inner x active) -> element offset of row 0
+__device__ __forceinline__ int64_t col_offset(const PassGeo &G, int c, int A, const int *act,
+                                              int nrhs) {
+  const int ia = G.inner * A;
+  const int b = c / ia, rem = c - b * ia;
+  const int ii = rem / A, a = rem - ii * A;
+  return (int64_t)b * G.n * G.ncols + (int64_t)ii * nrhs + act[a];
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -147,7 +181,7 @@ __device__ __forceinline__ void cp_wait() {
 // 16 columns are all past colw skip the products).
 template <int MT, int WR, int WC, int TK>
 __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw,
-                                          cplx *smem_mg) {
+                                          cplx *smem_mg, const int *act, int A, int nrhs) {
   constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
@@ -163,7 +197,7 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
   constexpr int B_STEP = NTH / TN, B_N = (TK + B_STEP - 1) / B_STEP;
   const int gcol = col0 + b_col;
   const bool bcol_ok = b_col < colw;
-  const int64_t bbase = bcol_ok ? (int64_t)(gcol / G.ncols) * n * G.ncols + gcol % G.ncols : 0;
+  const int64_t bbase = bcol_ok ? col_offset(G, gcol, A, act, nrhs) : 0;
   auto stage = [&](int kc, int buf) {
     const int k0 = kc * TK;
 #pragma unroll
@@ -233,8 +267,7 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
       for (int e = 0; e < 2; ++e) {
         const int cc = wc * 16 + nt * 8 + 2 * tg + e;
         if (cc >= colw) continue;
-        const int gc = col0 + cc;
-        const int64_t off = (int64_t)(gc / G.ncols) * n * G.ncols + (int64_t)gr * G.ncols + gc % G.ncols;
+        const int64_t off = col_offset(G, col0 + cc, A, act, nrhs) + (int64_t)gr * G.ncols;
         G.out[off] = make_double2(p1[mt][nt][e] - p2[mt][nt][e],
                                   p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
       }
@@ -247,16 +280,18 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
   extern __shared__ __align__(16) cplx smem_mg[];
+  __shared__ int act[RMAX_MODAL + 1];
   const ModalJob J = jobs[blockIdx.z];
   const FactDev f = *J.f;
   const PassGeo G = pass_geo(f, J, pass, nrhs);
   const int row0 = blockIdx.y * TM;
-  const int total = G.outer * G.ncols;
   const int col0 = blockIdx.x * TN;
-  if (row0 >= G.n || col0 >= total) return;
+  if (row0 >= G.n || col0 >= G.outer * G.ncols) return;
   pdl_wait();
-  if (!job_any(J, nrhs)) return;
-  gemm_tile<MT, WR, WC, TK>(G, row0, col0, min(TN, total - col0), smem_mg);
+  const int A = active_rhs(J, nrhs, act);
+  const int total = G.outer * G.inner * A;  // compact columns
+  if (col0 >= total) return;
+  gemm_tile<MT, WR, WC, TK>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
 }
 
 // ------------------------------------------- mode-wise recurrences (K3m-R)
@@ -424,13 +459,17 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
   const int m = f.m, nb = f.nb;
   const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
   const int nseg = (nb + L - 1) / L;
-  const int q = blockIdx.x * 32 + lane;
+  __shared__ int actl[RMAX_MODAL + 1];
   if (blockIdx.x * 32 >= m * nrhs) return;
   pdl_wait();
-  if (!job_any(J, nrhs)) return;
-  const bool live = q < m * nrhs;
-  const int qq = live ? q : 0;
-  const int j = qq / nrhs;
+  const int A = active_rhs(J, nrhs, actl);  // compact (mode, active RHS) columns
+  if (blockIdx.x * 32 >= m * A) return;
+  const int qc = blockIdx.x * 32 + lane;
+  const bool live = qc < m * A;
+  const int qcc = live ? qc : 0;
+  const int j = qcc / A;
+  const int q = j * nrhs + actl[qcc - j * A];  // full-layout column of this thread
+  const int qq = q;
   cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
   const size_t st = (size_t)m * nrhs;
   const int k0 = seg * L;
@@ -514,7 +553,6 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
   }
   __syncthreads();
   if (!act || !live) return;
-  if (J.nz && !J.nz[q % nrhs]) return;  // exact-zero RHS: never read downstream
   const cplx c = sC[seg][lane];
 #pragma unroll
   for (int i = 0; i < L; ++i) {
