@@ -176,6 +176,44 @@ def recurrence_bytes(dp, nrhs):
     return tot
 
 
+def step_kernel_bytes(dp, nrhs):
+    """Algorithmic HBM bytes per application of the step kernels (SURVEY
+    §8(d)), from the last application's counters and the transfer geometry:
+      K6 assemble   16 W per visit and RHS (rhs init) + 32 per copied node
+                    (own source in sweep 1, every arriving payload band node);
+      K5 accumulate 48 |support| per nonzero visit and RHS;
+      K4 transfer   16 |ext| + 48 |band| per emitted, non-discarded source
+                    and RHS (the cut / emission rules of ddm.py:82-110)."""
+    import numpy as np
+
+    from paper_2002_05327_b200.ddm import cut_mask_to_set, emits
+
+    ctr = dp.counters(nrhs)
+    vnz, vcut = ctr["visit_nonzero"], ctr["visit_cut"]
+    part = dp.partition
+    W = [int(np.prod(part.window(i).shape)) for i in dp.subs]
+    own = [int(np.prod(part.owned_window(i).shape)) for i in dp.subs]
+    sup = [int(np.prod(part.beta00_window(i).shape)) for i in dp.subs]
+    k4 = k5 = k6 = 0
+    arrived = 0
+    for w in range(dp.nsweeps):
+        for s in range(dp.nsub):
+            k6 += 16 * W[s] * nrhs + (32 * own[s] * nrhs if w == 0 else 0)
+            nz = vnz[w, s]
+            k5 += 48 * sup[s] * int(nz.sum())
+            for r in np.nonzero(nz)[0]:
+                cuts = cut_mask_to_set(int(vcut[w, s, r]), dp.dim)
+                for k, d in enumerate(dp.dirs):
+                    g = dp.geoms[(s, k)]
+                    if g is None or int(dp.xfer_use[w, s, k]) <= 0 or not emits(d, cuts):
+                        continue
+                    band, ext = int(np.prod(g.band.shape)), int(np.prod(g.ext.shape))
+                    k4 += 16 * ext + 48 * band
+                    arrived += band
+    k6 += 32 * arrived
+    return {"assemble": k6, "accumulate": k5, "transfer": k4}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 

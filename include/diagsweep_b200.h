@@ -243,6 +243,12 @@ DS_API int ds_ddm_counters(ds_ctx *ctx, ds_plan *plan, int32_t nrhs,
  * pointers and nrhs); ds_ddm_apply uses the graph when it matches. */
 DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
 
+/* ds_ddm_apply on RHS-outer device buffers f_dev / u_dev ([nrhs][N], the
+ * batched API layout): the assembly reads and the accumulation writes that
+ * layout directly (no layout transposes); no per-sweep partials. */
+DS_API int ds_ddm_apply_outer(ds_ctx *ctx, ds_plan *plan, const ds_cplx *f_dev,
+                              ds_cplx *u_dev, int32_t nrhs);
+
 /* One application from pinned HOST buffers: f_host / u_host are RHS-outer
  * [nrhs][N] complex128 in page-locked memory.  The source upload runs in
  * axis-0 row chunks on a copy stream overlapped with the first sweep (each

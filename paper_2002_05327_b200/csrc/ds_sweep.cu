@@ -142,6 +142,13 @@ struct ds_plan {
   void *graph_u = nullptr;
   void *graph_partials = nullptr;
   int graph_nrhs = 0;
+  bool graph_outer = false;
+  // {f, u} of the current application, read by K6 / K5 / the zeroing: the
+  // captured graphs replay for any field buffers (set by set_io before each
+  // application, stream-ordered)
+  cplx **d_io = nullptr;
+  const void *io_f = nullptr;
+  void *io_u = nullptr;
   // host-buffer application (ds_ddm_apply_host): node chunks along axis 0,
   // per launch the chunks of f its assembly needs, per chunk the launch of
   // the last accumulation touching it; device staging buffers; graph cache
@@ -150,7 +157,7 @@ struct ds_plan {
   std::vector<int> hio_need;             // per launch: chunks [0, need) resident
   std::vector<std::vector<int>> hio_out_at;  // per launch: chunks final after its K5
   std::vector<int> hio_out_early;        // chunks no K5 touches (zero rows)
-  cplx *hio_fo = nullptr, *hio_fm = nullptr, *hio_uo = nullptr, *hio_um = nullptr;
+  cplx *hio_fo = nullptr, *hio_fm = nullptr, *hio_uo = nullptr, *hio_um = nullptr;  // f/u staging: RHS-outer (copies), RHS-minor (sweep)
   cudaStream_t cstream = nullptr;
   int side_priority = 0;  // K5 / copy stream priority
   std::vector<cudaEvent_t> hio_ev_in, hio_ev_out;
@@ -301,17 +308,24 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 // showed the one-RHS-per-thread version instruction-bound (~140 instructions
 // per value, IPC 0.6).
 
+// u = 0 through the pointer table (graphs replay for any f / u buffers)
+__global__ void k_zero_io(cplx *const *__restrict__ io, int64_t n) {
+  cplx *u = io[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    u[i] = make_double2(0.0, 0.0);
+}
+
 // ------------------------------------------------------------- K6 assemble
 // rhs (block layout [nb][m][R]) = own restricted source (sweep 1) + the
 // visit's queued payload slots in slot order; slots are zeroed as consumed.
 // Slot membership is separable (boxes), so each block first builds, per
 // window axis and coordinate, the bitmask of slots (bit 31: the own box)
 // covering it; a node's slot set is then the AND of its axis masks.
-template <int RV>
+template <int RV, bool OUTER>
 __global__ void __launch_bounds__(256)
     k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
-               const SlotRef *__restrict__ slots, const cplx *__restrict__ f, int nrhs, int dim,
-               int g0, int g1, int g2, Flags F) {
+               const SlotRef *__restrict__ slots, const cplx *__restrict__ f, int nrhs,
+               int dim, int g0, int g1, int g2, Flags F, int64_t nnodes) {
   __shared__ int s_nz[RMAX], s_own[RMAX];
   __shared__ SlotRef s_slot[SLOT_SMEM];
   extern __shared__ uint32_t s_mask[];  // [E0 | E1 | E2]
@@ -368,10 +382,12 @@ __global__ void __launch_bounds__(256)
         mk = (own && in_box(g, olo, osh, dim)) ? 1u << 31 : 0u;
       }
       if (mk >> 31) {
-        const cplx *src = f + lin_of64(g, gc, dim) * nrhs + rl;
+        // f element (node, rhs): RHS-minor node * nrhs + rhs, RHS-outer rhs * N + node
+        const int64_t lin = lin_of64(g, gc, dim);
+        const cplx *src = OUTER ? f + rl * nnodes + lin : f + lin * nrhs + rl;
 #pragma unroll
         for (int j = 0; j < RV; ++j) {
-          const cplx sv = src[j];
+          const cplx sv = OUTER ? src[j * nnodes] : src[j];
           val[j] = cadd(val[j], sv);
           anyown[j] |= cnonzero(sv);
         }
@@ -431,10 +447,12 @@ __global__ void __launch_bounds__(256)
 // u += beta00 * x over the visit's support; where supports of same-step
 // visits overlap the first visit owning the node sums all of them in visit
 // order (deterministic, no atomics on field values).
-template <int RV>
+template <int RV, bool OUTER>
 __global__ void __launch_bounds__(256)
     k_accumulate(const VisitDev *__restrict__ visits, int G, const SubDev *__restrict__ subs,
-                 cplx *u, int nrhs, int dim, int g0, int g1, int g2) {
+                 cplx *const *__restrict__ io, int nrhs, int dim, int g0, int g1, int g2,
+                 int64_t nnodes) {
+  cplx *u = io[1];  // result field of this application (ds_plan::d_io)
   const int v = blockIdx.y;
   const SubDev &sd = subs[visits[v].sub];
   const int gc[3] = {g0, g1, g2};
@@ -454,10 +472,12 @@ __global__ void __launch_bounds__(256)
       if (in_box(g, so.sup_lo, so.sup_shape, dim)) owner = false;
     }
     if (!owner) continue;
-    cplx *up = u + lin_of64(g, gc, dim) * nrhs + rl;
+    const int64_t lin = lin_of64(g, gc, dim);
+    cplx *up = OUTER ? u + rl * nnodes + lin : u + lin * nrhs + rl;  // RHS-outer / -minor
+    const int64_t cstride = OUTER ? (int64_t)lpn * nnodes : lpn;  // column j * lpn
     cplx acc[RV];
 #pragma unroll
-    for (int j = 0; j < RV; ++j) acc[j] = up[j * lpn];
+    for (int j = 0; j < RV; ++j) acc[j] = up[j * cstride];
     bool touched = false;
     for (int w = v; w < G; ++w) {
       const VisitDev &W = visits[w];
@@ -480,7 +500,7 @@ __global__ void __launch_bounds__(256)
     }
     if (touched) {
 #pragma unroll
-      for (int j = 0; j < RV; ++j) up[j * lpn] = acc[j];
+      for (int j = 0; j < RV; ++j) up[j * cstride] = acc[j];
     }
   }
 }
@@ -1401,6 +1421,22 @@ static void prof_mark(ds_plan *P, int cls, cudaStream_t st) {
 // issue the whole application on ctx->stream (capturable)
 // issue launches [q0, q1) of one application on ctx->stream (capturable);
 // mode bit 0: zero u and the flags first; bit 1: join the K5 side stream
+static int set_io(ds_plan *P, const void *f, void *u, cudaStream_t st) {
+  if (!P->d_io) {
+    void *mem;
+    if (plan_alloc(P, &mem, 2 * sizeof(void *))) return DS_ECUDA;
+    P->d_io = (cplx **)mem;
+    P->io_f = nullptr;
+    P->io_u = nullptr;
+  }
+  if (P->io_f == f && P->io_u == u) return DS_OK;
+  const void *h[2] = {f, u};
+  DS_CUDA(cudaMemcpyAsync(P->d_io, h, sizeof(h), cudaMemcpyHostToDevice, st));
+  P->io_f = f;
+  P->io_u = u;
+  return DS_OK;
+}
+
 struct HostIO {
   const cplx *fh;  // pinned host sources, RHS-outer [R][N]
   cplx *uh;        // pinned host result, RHS-outer [R][N]
@@ -1409,7 +1445,8 @@ static int hio_in_chunks(ds_plan *P, const HostIO *hio, int nrhs, cudaStream_t c
 static int hio_out_chunk(ds_plan *P, const HostIO *hio, int nrhs, int c, cudaStream_t cs);
 
 static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *partials, int q0 = 0,
-                       int q1 = -1, int mode = 3, const HostIO *hio = nullptr) {
+                       int q1 = -1, int mode = 3, const HostIO *hio = nullptr, bool outer = false) {
+  // field layout of f and u: RHS-minor [N][R] or RHS-outer [R][N] (outer)
   ds_ctx *ctx = P->ctx;
   cudaStream_t st = ctx->stream;
   const int dim = P->dim;
@@ -1417,7 +1454,13 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   int64_t launches0 = ctx->launches;
   size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
   if (mode & 1) {
-    DS_CUDA(cudaMemsetAsync(u, 0, sizeof(cplx) * P->nnodes * nrhs, st));
+    {
+      const int64_t n = P->nnodes * nrhs;
+      k_zero_io<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
+          P->d_io, n);
+      ctx->launches++;
+      DS_CHECK_LAUNCH();
+    }
     DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
     DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
     DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
@@ -1459,15 +1502,17 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       prof_mark(P, 0, st);
       if (skip_cls & 1) {
       } else if (nrhs % 4 == 0)
-        DS_CUDA(launch_pdl(k_assemble<4>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
+        DS_CUDA(launch_pdl(outer ? k_assemble<4, true> : k_assemble<4, false>, dim3(bx, G), dim3(256),
+                           sizeof(uint32_t) * P->max_axis_sum, st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
-                           (const SlotRef *)P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
-                           P->gcounts[2], F));
+                           (const SlotRef *)P->slots, f, nrhs, dim,
+                           P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
       else
-        DS_CUDA(launch_pdl(k_assemble<1>, dim3(bx, G), dim3(256), sizeof(uint32_t) * P->max_axis_sum, st,
+        DS_CUDA(launch_pdl(outer ? k_assemble<1, true> : k_assemble<1, false>, dim3(bx, G), dim3(256),
+                           sizeof(uint32_t) * P->max_axis_sum, st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
-                           (const SlotRef *)P->slots, f, nrhs, dim, P->gcounts[0], P->gcounts[1],
-                           P->gcounts[2], F));
+                           (const SlotRef *)P->slots, f, nrhs, dim,
+                           P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
       ctx->launches++;
       DS_CHECK_LAUNCH();
       prof_mark(P, 1, st);
@@ -1497,11 +1542,13 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       }
       if (skip_cls & 16) {
       } else if (nrhs % 4 == 0)
-        k_accumulate<4><<<dim3(by, G), 256, 0, s5>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
-                                                     P->gcounts[0], P->gcounts[1], P->gcounts[2]);
+        (outer ? k_accumulate<4, true> : k_accumulate<4, false>)<<<dim3(by, G), 256, 0, s5>>>(
+            P->visits + v0, G, P->subs, P->d_io, nrhs, dim, P->gcounts[0], P->gcounts[1], P->gcounts[2],
+            (int64_t)P->nnodes);
       else
-        k_accumulate<1><<<dim3(by, G), 256, 0, s5>>>(P->visits + v0, G, P->subs, u, nrhs, dim,
-                                                     P->gcounts[0], P->gcounts[1], P->gcounts[2]);
+        (outer ? k_accumulate<1, true> : k_accumulate<1, false>)<<<dim3(by, G), 256, 0, s5>>>(
+            P->visits + v0, G, P->subs, P->d_io, nrhs, dim, P->gcounts[0], P->gcounts[1], P->gcounts[2],
+            (int64_t)P->nnodes);
       ctx->launches++;
       DS_CHECK_LAUNCH();
       if (s5 != st) {
@@ -1775,6 +1822,7 @@ extern "C" int ds_ddm_apply_host(ds_ctx *ctx, ds_plan *P, const ds_cplx *f_host,
     P->slots_dirty = false;
   }
   HostIO hio{(const cplx *)f_host, (cplx *)u_host};
+  if ((rc = set_io(P, P->hio_fm, P->hio_um, ctx->stream))) return rc;
   if (!P->use_graph || P->profiling) {
     rc = issue_apply(P, P->hio_fm, P->hio_um, nrhs, nullptr, 0, -1, 3, &hio);
     if (rc) P->slots_dirty = true;
@@ -1823,8 +1871,10 @@ extern "C" int ds_ddm_apply_host(ds_ctx *ctx, ds_plan *P, const ds_cplx *f_host,
   return DS_OK;
 }
 
-extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u, int32_t nrhs,
-                            ds_cplx *partials) {
+static int ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u, int32_t nrhs,
+                     ds_cplx *partials, bool outer) {
+  if (ctx && P && f && u)
+    if (int rc0 = set_io(P, f, u, ctx->stream)) return rc0;
   if (!ctx || !P || !f || !u) return ds_fail(DS_ECONFIG, "ds_ddm_apply: null argument");
   if (nrhs < 1 || nrhs > P->nrhs_max)
     return ds_fail(DS_ECONFIG, "ds_ddm_apply: nrhs exceeds the plan's nrhs_max");
@@ -1846,8 +1896,9 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
       DS_CUDA(cudaEventCreateWithFlags(&P->gev_out, cudaEventDisableTiming));
     }
     cudaStream_t user = ctx->stream;
-    bool match = P->graph && P->graph_f == f && P->graph_u == u && P->graph_nrhs == nrhs &&
-                 P->graph_partials == partials;
+    // the graph reads u through d_io and f as a kernel parameter
+    bool match = P->graph && P->graph_f == f && P->graph_nrhs == nrhs &&
+                 P->graph_partials == partials && P->graph_outer == outer;
     DS_CUDA(cudaEventRecord(P->gev_in, user));
     DS_CUDA(cudaStreamWaitEvent(P->gstream, P->gev_in, 0));
     if (!match) {
@@ -1859,7 +1910,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
       ctx->stream = P->gstream;
       DS_CUDA(cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal));
       int64_t l0 = ctx->launches;
-      rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
+      rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials, 0, -1, 3, nullptr, outer);
       cudaError_t e = cudaStreamEndCapture(P->gstream, &g);
       ctx->stream = user;
       if (rc) {
@@ -1873,6 +1924,7 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
       P->graph_u = u;
       P->graph_nrhs = nrhs;
       P->graph_partials = partials;
+      P->graph_outer = outer;
       ctx->launches = l0;
     }
     DS_CUDA(cudaGraphLaunch(P->graph, P->gstream));
@@ -1881,9 +1933,20 @@ extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *
     ctx->launches += P->last_launches;
     return DS_OK;
   }
-  rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials);
+  rc = issue_apply(P, (const cplx *)f, (cplx *)u, nrhs, (cplx *)partials, 0, -1, 3, nullptr, outer);
   if (rc) P->slots_dirty = true;
   return rc;
+}
+
+extern "C" int ds_ddm_apply(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u, int32_t nrhs,
+                            ds_cplx *partials) {
+  return ddm_apply(ctx, P, f, u, nrhs, partials, false);
+}
+
+// the same on RHS-outer [R][N] device buffers (no layout transposes)
+extern "C" int ds_ddm_apply_outer(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_cplx *u,
+                                  int32_t nrhs) {
+  return ddm_apply(ctx, P, f, u, nrhs, nullptr, true);
 }
 
 extern "C" int ds_plan_shard_info(const ds_plan *P, void **slot_base, int64_t *slot_bytes,
@@ -1931,6 +1994,7 @@ extern "C" int ds_ddm_apply_range(ds_ctx *ctx, ds_plan *P, const ds_cplx *f, ds_
   if (l0 < 0 || l1 < l0 || l1 > nq) return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: bad launch range");
   if (!P->peers_set) return ds_fail(DS_ECONFIG, "ds_ddm_apply_range: ds_plan_set_peers not called");
   if (ctx != P->ctx) P->ctx = ctx;
+  if (int rc0 = set_io(P, f, u, ctx->stream)) return rc0;
   int rc = patch_tables(P, nrhs);
   if (rc) return rc;
   if (P->slots_dirty) {
@@ -1959,27 +2023,30 @@ extern "C" int ds_ddm_counters(ds_ctx *ctx, ds_plan *P, int32_t nrhs, int32_t *n
                                int32_t *visit_cut) {
   if (!ctx || !P || nrhs < 1 || nrhs > P->nrhs_max)
     return ds_fail(DS_ECONFIG, "ds_ddm_counters: bad argument");
-  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  // the flag block (own | nz | arr_cnt | arr_cut | emit_cnt | discard) is
+  // contiguous for this stride: one device-to-host copy (ordered after the
+  // application on the context stream)
   Flags F = flags_view(P, nrhs);
-  size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
-  std::vector<int> nz(per), cnt, em;
-  DS_CUDA(cudaMemcpy(nz.data(), F.nz, sizeof(int) * per, cudaMemcpyDeviceToHost));
+  const size_t per = (size_t)P->nsweeps * P->nsub * nrhs;
+  const size_t own_n = (size_t)P->nsub * nrhs;
+  const size_t words = own_n + 4 * per + nrhs;
+  std::vector<int> h(words);
+  DS_CUDA(cudaMemcpyAsync(h.data(), F.own_nz, sizeof(int) * words, cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int *own = h.data(), *nz = own + own_n, *cnt2 = nz + per, *cut = cnt2 + per,
+            *em = cut + per, *disc = em + per;
   if (nonzero) {
     for (int r = 0; r < nrhs; ++r) nonzero[r] = 0;
     for (size_t i = 0; i < per; ++i) nonzero[i % nrhs] += nz[i] ? 1 : 0;
   }
-  if (discarded) DS_CUDA(cudaMemcpy(discarded, F.discard, sizeof(int) * nrhs, cudaMemcpyDeviceToHost));
+  if (discarded) memcpy(discarded, disc, sizeof(int) * nrhs);
   if (visit_nonzero)
     for (size_t i = 0; i < per; ++i) visit_nonzero[i] = nz[i] ? 1 : 0;
-  if (visit_consumed) DS_CUDA(cudaMemcpy(visit_consumed, F.arr_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
-  if (visit_emitted) DS_CUDA(cudaMemcpy(visit_emitted, F.emit_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
+  if (visit_consumed) memcpy(visit_consumed, cnt2, sizeof(int) * per);
+  if (visit_emitted) memcpy(visit_emitted, em, sizeof(int) * per);
   if (visit_cut) {
-    std::vector<int> own((size_t)P->nsub * nrhs), cnt2(per), cut(per);
-    DS_CUDA(cudaMemcpy(own.data(), F.own_nz, sizeof(int) * own.size(), cudaMemcpyDeviceToHost));
-    DS_CUDA(cudaMemcpy(cnt2.data(), F.arr_cnt, sizeof(int) * per, cudaMemcpyDeviceToHost));
-    DS_CUDA(cudaMemcpy(cut.data(), F.arr_cut, sizeof(int) * per, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < per; ++i) {
-      size_t w = i / ((size_t)P->nsub * nrhs), rem = i % ((size_t)P->nsub * nrhs);
+      size_t w = i / own_n, rem = i % own_n;
       bool has_own = (w == 0) && own[rem];
       visit_cut[i] = (has_own || cnt2[i] == 0) ? 0 : (cut[i] & CUT_ALL);
     }
