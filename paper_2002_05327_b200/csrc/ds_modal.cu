@@ -179,14 +179,16 @@ __device__ __forceinline__ void cp_wait() {
 // The tile body: rows [row0, row0 + TM) x columns [col0, col0 + colw),
 // colw <= TN (columns past colw are zero-filled and not stored; warps whose
 // 16 columns are all past colw skip the products).
-template <int MT, int WR, int WC, int TK>
+// NS-stage cp.async ring: chunk kc lives in buffer kc % NS; NS - 1 chunks
+// are in flight while one is multiplied (NS = 2: double buffering).
+template <int MT, int WR, int WC, int TK, int NS = 2>
 __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw,
                                           cplx *smem_mg, const int *act, int A, int nrhs) {
   constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
   auto sA = [&](int buf) { return smem_mg + buf * (TM * AP); };
-  auto sB = [&](int buf) { return smem_mg + 2 * TM * AP + buf * (TK * BP); };
+  auto sB = [&](int buf) { return smem_mg + NS * TM * AP + buf * (TK * BP); };
   const int n = G.n;
   const int t = threadIdx.x;
   // staging maps: A -- fixed column t % TK, rows t / TK + q * (NTH / TK);
@@ -221,16 +223,18 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
   const bool wact = wc * 16 < colw;
   double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
   const int nkc = (n + TK - 1) / TK;
-  stage(0, 0);
+  // prologue: chunks 0 .. NS-2 (empty commit groups keep the group count)
+#pragma unroll
+  for (int i = 0; i < NS - 1; ++i) {
+    if (i < nkc) stage(i, i);
+    else cp_commit();
+  }
   for (int kc = 0; kc < nkc; ++kc) {
-    const int buf = kc & 1;
-    if (kc + 1 < nkc) {
-      stage(kc + 1, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
+    const int buf = kc % NS;
+    cp_wait<NS - 2>();  // chunk kc landed (this thread's copies)
+    __syncthreads();    // ... and every thread's; buffer (kc - 1) % NS is free
+    if (kc + NS - 1 < nkc) stage(kc + NS - 1, (kc + NS - 1) % NS);
+    else cp_commit();
     if (wact) {
       const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
       const cplx *Bs = sB(buf) + tg * BP + wc * 16 + g;
@@ -254,8 +258,9 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
         }
       }
     }
-    __syncthreads();
   }
+  cp_wait<0>();
+  __syncthreads();  // the CTA's next tile restages the ring
   if (!wact) return;
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -275,7 +280,7 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
 }
 
 // one tile per CTA: grid (column tiles, row tiles, visits)
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 __global__ void __launch_bounds__(32 * WR * WC, MINB)
     k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   const int A = active_rhs(J, nrhs, act);
   const int total = G.outer * G.inner * A;  // compact columns
   if (col0 >= total) return;
-  gemm_tile<MT, WR, WC, TK>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
+  gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
 }
 
 // ------------------------------------------- mode-wise recurrences (K3m-R)
@@ -659,14 +664,14 @@ __global__ void __launch_bounds__(512) k_modal_thomas4(const ModalJob *__restric
 }
 
 // ------------------------------------------------------------- launcher
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
                        int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
-  const size_t smem = sizeof(cplx) * 2 * (TM * (TK + 4) + TK * (TN + 2));
+  const size_t smem = sizeof(cplx) * NS * (TM * (TK + 4) + TK * (TN + 2));
   static bool attr_set = false;
   if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB>,
+    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB, NS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
@@ -678,7 +683,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
     gy = std::max(gy, (G.n + TM - 1) / TM);
   }
-  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
+  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
                      ctx->stream, jobs_dev, pass, nrhs));
 
   ctx->launches++;
@@ -699,7 +704,7 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   // n 16x64 x 4, o (default) 32x32 with 2x2 warps of 16x16, p TK 32, q 8x64)
   static const char variant = [] {
     const char *v = getenv("DS_MG");
-    return v && *v ? v[0] : 'o';
+    return v && *v ? v[0] : 'u';
   }();
   auto launch_pass = [&](int pass) -> int {
     switch (variant) {
@@ -718,6 +723,14 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
       case 'o': return launch_gemm<2, 2, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'p': return launch_gemm<1, 2, 2, 32, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'q': return launch_gemm<1, 1, 4, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'r': return launch_gemm<2, 2, 2, 16, 3, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 's': return launch_gemm<2, 2, 2, 16, 2, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 't': return launch_gemm<1, 2, 2, 16, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'u': return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'v': return launch_gemm<2, 2, 2, 8, 4, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'w': return launch_gemm<2, 2, 2, 8, 6, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'x': return launch_gemm<1, 2, 2, 8, 8, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'y': return launch_gemm<2, 2, 2, 4, 4, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
       default: return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
     }
   };
