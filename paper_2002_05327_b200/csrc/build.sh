@@ -6,7 +6,7 @@ out="${1:-$here/../lib/libdiagsweep_b200.so}"
 mkdir -p "$(dirname "$out")"
 NVCC="${NVCC:-nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17
-       -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr)
+       -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr ${DS_EXTRA_FLAGS:-})
 objs=()
 tmp="$(mktemp -d)"
 trap 'rm -rf "$tmp"' EXIT

@@ -149,6 +149,10 @@ __device__ __forceinline__ int active_rhs(const ModalJob &J, int nrhs, int *act)
 // compact column c (outer x inner x active) -> element offset of row 0
 __device__ __forceinline__ int64_t col_offset(const PassGeo &G, int c, int A, const int *act,
                                               int nrhs) {
+  if (A == nrhs) {  // every RHS active: the plain batched layout
+    const int b = c / G.ncols;
+    return (int64_t)b * G.n * G.ncols + (c - b * G.ncols);
+  }
   const int ia = G.inner * A;
   const int b = c / ia, rem = c - b * ia;
   const int ii = rem / A, a = rem - ii * A;

@@ -159,6 +159,8 @@ struct ds_plan {
   std::vector<int> hio_out_early;        // chunks no K5 touches (zero rows)
   cplx *hio_fo = nullptr, *hio_fm = nullptr, *hio_uo = nullptr, *hio_um = nullptr;  // f/u staging: RHS-outer (copies), RHS-minor (sweep)
   cudaStream_t cstream = nullptr;
+  cudaStream_t cstream2 = nullptr;  // second copy stream: boxes alternate between the two
+  cudaEvent_t hio_fork2 = nullptr, hio_join2 = nullptr;
   int side_priority = 0;  // K5 / copy stream priority
   std::vector<cudaEvent_t> hio_ev_in, hio_ev_out;
   cudaEvent_t hio_fork = nullptr, hio_join = nullptr;
@@ -297,7 +299,11 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 #define SLOT_SMEM 32
 // band nodes per thread and tile pass of k_transfer2, and its resident blocks per SM
 #define K4_NPT(dim) ((dim) == 2 ? 2 : 1)
-#define K4_MINB(dim) 2
+#define K4_MINB(dim) ((dim) == 2 ? 2 : K4_MINB3)
+#ifndef K4_MINB3
+#define K4_MINB3 2
+#endif
+
 
 // Thread mapping of K4/K5/K6: a thread owns RV RHS columns of one node --
 // lane l of the node's LPN = nrhs / RV lanes takes columns l, l + LPN, ... --
@@ -1263,6 +1269,9 @@ extern "C" int ds_plan_destroy(ds_plan *P) {
   if (P->graph) cudaGraphExecDestroy(P->graph);
   for (auto &g : P->hgraphs) cudaGraphExecDestroy(g.exec);
   if (P->cstream) cudaStreamDestroy(P->cstream);
+  if (P->cstream2) cudaStreamDestroy(P->cstream2);
+  if (P->hio_fork2) cudaEventDestroy(P->hio_fork2);
+  if (P->hio_join2) cudaEventDestroy(P->hio_join2);
   for (auto e : P->hio_ev_in) cudaEventDestroy(e);
   for (auto e : P->hio_ev_out) cudaEventDestroy(e);
   if (P->hio_fork) cudaEventDestroy(P->hio_fork);
@@ -1441,6 +1450,21 @@ struct HostIO {
   const cplx *fh;  // pinned host sources, RHS-outer [R][N]
   cplx *uh;        // pinned host result, RHS-outer [R][N]
 };
+
+// DS_HIO_TRACE (eager host path only): timestamps of uploads, launches and
+// downloads, printed after the application (diagnostics)
+static std::vector<std::pair<std::string, cudaEvent_t>> g_trace;
+static bool hio_trace_on() {
+  static const bool on = getenv("DS_HIO_TRACE") != nullptr;
+  return on;
+}
+static void trace_mark(const std::string &what, cudaStream_t st) {
+  if (!hio_trace_on()) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_trace.push_back({what, e});
+}
 static int hio_in_chunks(ds_plan *P, const HostIO *hio, int nrhs, cudaStream_t cs);
 static int hio_out_chunk(ds_plan *P, const HostIO *hio, int nrhs, int c, cudaStream_t cs);
 
@@ -1469,11 +1493,12 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   if (hio) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
     DS_CUDA(cudaEventRecord(P->hio_fork, st));
     DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_fork, 0));
+    DS_CUDA(cudaStreamWaitEvent(P->cstream2, P->hio_fork, 0));
     if (int rc = hio_in_chunks(P, hio, nrhs, P->cstream)) return rc;
     for (int c : P->hio_out_early)
       if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
   }
-  int hio_waited = 0;
+  int hio_waited = 0, hio_nout = 0;
   // diagnostics only (wrong results): DS_SKIP bitmask drops kernel classes
   // from the schedule to measure their marginal time under graph replay
   // (1 K6, 2 modal transforms, 4 modal recurrences, 8 K4, 16 K5)
@@ -1495,10 +1520,12 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (G == 0) continue;
       const int64_t wmax = P->max_w, smax = P->max_w;
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
-      if (hio && P->hio_need[q] > hio_waited) {  // f chunks this assembly reads
-        hio_waited = P->hio_need[q];
+      if (hio && P->hio_need[q] > hio_waited) {  // f boxes [0, need) this assembly may read:
+        hio_waited = P->hio_need[q];               // the last of them on each copy stream
         DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 1], 0));
+        if (hio_waited >= 2) DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 2], 0));
       }
+      if (hio) trace_mark("launch " + std::to_string(q), st);
       prof_mark(P, 0, st);
       if (skip_cls & 1) {
       } else if (nrhs % 4 == 0)
@@ -1557,9 +1584,12 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       }
       if (hio)  // u chunks whose last accumulation this was: transpose + D2H
         for (int c : P->hio_out_at[q]) {
+          cudaStream_t cs = (hio_nout++ & 1) ? P->cstream2 : P->cstream;
           DS_CUDA(cudaEventRecord(P->hio_ev_out[c], s5));
-          DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_ev_out[c], 0));
-          if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
+          DS_CUDA(cudaStreamWaitEvent(cs, P->hio_ev_out[c], 0));
+          trace_mark("  K5 done for box " + std::to_string(c) + " (launch " + std::to_string(q) + ")", cs);
+          if (int rc = hio_out_chunk(P, hio, nrhs, c, cs)) return rc;
+          trace_mark("  download done box " + std::to_string(c), cs);
         }
       int x0 = P->xstep_off[q], nx = P->xstep_off[q + 1] - x0;
       if (nx > 0 && !(skip_cls & 8)) {
@@ -1616,6 +1646,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   if (hio) {  // join the copy stream: every u chunk is on the host
     DS_CUDA(cudaEventRecord(P->hio_join, P->cstream));
     DS_CUDA(cudaStreamWaitEvent(st, P->hio_join, 0));
+    DS_CUDA(cudaEventRecord(P->hio_join2, P->cstream2));
+    DS_CUDA(cudaStreamWaitEvent(st, P->hio_join2, 0));
   }
   prof_mark(P, -1, st);
   P->last_launches = ctx->launches - launches0;
@@ -1730,6 +1762,9 @@ static int hio_setup(ds_plan *P) {
     *b = (cplx *)mem;
   }
   DS_CUDA(cudaStreamCreateWithPriority(&P->cstream, cudaStreamNonBlocking, P->side_priority));
+  DS_CUDA(cudaStreamCreateWithPriority(&P->cstream2, cudaStreamNonBlocking, P->side_priority));
+  DS_CUDA(cudaEventCreateWithFlags(&P->hio_fork2, cudaEventDisableTiming));
+  DS_CUDA(cudaEventCreateWithFlags(&P->hio_join2, cudaEventDisableTiming));
   P->hio_ev_in.resize(C);
   P->hio_ev_out.resize(C);
   for (int c = 0; c < C; ++c) {
@@ -1789,10 +1824,14 @@ static int hio_box(ds_plan *P, const HostIO *hio, int nrhs, int k, cudaStream_t 
 }
 
 // uploads of every source box in first-use order, one event per box
+// box k goes on copy stream k % 2 (two boxes in flight: one box's layout
+// transpose runs under the other's copy, and two copy engines share PCIe)
 static int hio_in_chunks(ds_plan *P, const HostIO *hio, int nrhs, cudaStream_t cs) {
   for (int k = 0; k < (int)P->hio_boxes.size(); ++k) {
-    if (int rc = hio_box(P, hio, nrhs, k, cs, true)) return rc;
-    DS_CUDA(cudaEventRecord(P->hio_ev_in[k], cs));
+    cudaStream_t c = (k & 1) ? P->cstream2 : cs;
+    if (int rc = hio_box(P, hio, nrhs, k, c, true)) return rc;
+    DS_CUDA(cudaEventRecord(P->hio_ev_in[k], c));
+    trace_mark("  upload done box " + std::to_string(k), c);
   }
   return DS_OK;
 }
@@ -1824,8 +1863,20 @@ extern "C" int ds_ddm_apply_host(ds_ctx *ctx, ds_plan *P, const ds_cplx *f_host,
   HostIO hio{(const cplx *)f_host, (cplx *)u_host};
   if ((rc = set_io(P, P->hio_fm, P->hio_um, ctx->stream))) return rc;
   if (!P->use_graph || P->profiling) {
+    trace_mark("start", ctx->stream);
     rc = issue_apply(P, P->hio_fm, P->hio_um, nrhs, nullptr, 0, -1, 3, &hio);
+    trace_mark("end", ctx->stream);
     if (rc) P->slots_dirty = true;
+    if (hio_trace_on() && !g_trace.empty()) {
+      cudaDeviceSynchronize();
+      for (auto &t : g_trace) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_trace.front().second, t.second);
+        fprintf(stderr, "hio %8.3f ms  %s\n", ms, t.first.c_str());
+      }
+      for (auto &t : g_trace) cudaEventDestroy(t.second);
+      g_trace.clear();
+    }
     return rc;
   }
   if (!P->gstream) {
