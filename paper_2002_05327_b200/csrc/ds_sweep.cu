@@ -153,7 +153,8 @@ struct ds_plan {
   // per launch the chunks of f its assembly needs, per chunk the launch of
   // the last accumulation touching it; device staging buffers; graph cache
   bool hio_ready = false;
-  std::vector<struct HioBox> hio_boxes;  // in upload order
+  std::vector<struct HioBox> hio_boxes;   // upload boxes, in upload order
+  std::vector<struct HioBox> hio_oboxes;  // download boxes
   std::vector<int> hio_need;             // per launch: chunks [0, need) resident
   std::vector<std::vector<int>> hio_out_at;  // per launch: chunks final after its K5
   std::vector<int> hio_out_early;        // chunks no K5 touches (zero rows)
@@ -298,7 +299,10 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 
 #define SLOT_SMEM 32
 // band nodes per thread and tile pass of k_transfer2, and its resident blocks per SM
-#define K4_NPT(dim) ((dim) == 2 ? 2 : 1)
+#ifndef K4_NPT3
+#define K4_NPT3 1
+#endif
+#define K4_NPT(dim) ((dim) == 2 ? 2 : K4_NPT3)
 #define K4_MINB(dim) ((dim) == 2 ? 2 : K4_MINB3)
 #ifndef K4_MINB3
 #define K4_MINB3 2
@@ -1695,59 +1699,67 @@ __global__ void k_box_transpose(int R, int L, int64_t N, int64_t base0, int64_t 
 }
 
 // chunk tables (nrhs-independent) and staging buffers (nrhs_max)
-static int hio_setup(ds_plan *P) {
-  if (P->hio_ready) return DS_OK;
-  // box grid "B0xB1" (DS_HIO_BOXES): axis-1 splits shorten the copy segments
-  // (3D copies of sub-4 KB rows run far below the copy engine's rate)
-  static const std::pair<int, int> split = [] {
-    const char *v = getenv("DS_HIO_BOXES");
-    int a = 8, b = 2;
-    if (v && *v) sscanf(v, "%dx%d", &a, &b);
-    return std::make_pair(std::max(1, a), std::max(1, b));
-  }();
-  const int B0 = std::min(split.first, P->gcounts[0]), B1 = std::min(split.second, P->gcounts[1]);
+static std::vector<HioBox> hio_grid(const ds_plan *P, const char *env, int a, int b) {
+  const char *v = getenv(env);
+  if (v && *v) sscanf(v, "%dx%d", &a, &b);
+  const int B0 = std::min(std::max(1, a), P->gcounts[0]), B1 = std::min(std::max(1, b), P->gcounts[1]);
   std::vector<HioBox> boxes;
   for (int i = 0; i < B0; ++i)
     for (int j = 0; j < B1; ++j)
       boxes.push_back({(int)((int64_t)P->gcounts[0] * i / B0), (int)((int64_t)P->gcounts[0] * (i + 1) / B0),
                        (int)((int64_t)P->gcounts[1] * j / B1), (int)((int64_t)P->gcounts[1] * (j + 1) / B1)});
-  const int C = (int)boxes.size();
+  return boxes;
+}
+
+static int hio_setup(ds_plan *P) {
+  if (P->hio_ready) return DS_OK;
+  // upload boxes (DS_HIO_IN, default 8x4) in first-use order and download
+  // boxes (DS_HIO_BOXES, default 12x2) in finalization order; measured on
+  // config 2 (tools/e2e_probe.py): whole-row bands 16x1 5.61 ms, 8x2 / 8x2
+  // 5.29, 8x4 / 12x2 5.18 -- finer boxes start the sweep earlier, but 3D
+  // copies of sub-4 KB rows run below the copy engine's rate
+  const std::vector<HioBox> ib = hio_grid(P, "DS_HIO_IN", 8, 4);
+  const std::vector<HioBox> ob = hio_grid(P, "DS_HIO_BOXES", 12, 2);
+  const int CI = (int)ib.size(), CO = (int)ob.size();
   auto meets = [&](const HioBox &B, const int *lo, const int *sh) {
     return sh[0] > 0 && sh[1] > 0 && lo[0] < B.a1 && lo[0] + sh[0] > B.a0 && lo[1] < B.c1 &&
            lo[1] + sh[1] > B.c0;
   };
   const int nq = (int)P->vstep_off.size() - 1;
-  std::vector<int> first(C, nq), last(C, -1);
+  std::vector<int> first(CI, nq), last(CO, -1);
   for (int q = 0; q < nq; ++q)
     for (int i = P->vstep_off[q]; i < P->vstep_off[q + 1]; ++i) {
       const VisitDev &V = P->h_visits[i];
       const SubDev &S = P->h_subs[V.sub];
-      for (int c = 0; c < C; ++c) {
-        if (V.sweep == 1 && meets(boxes[c], S.own_lo, S.own_shape)) first[c] = std::min(first[c], q);
-        if (meets(boxes[c], S.sup_lo, S.sup_shape)) last[c] = q;
-      }
+      if (V.sweep == 1)
+        for (int c = 0; c < CI; ++c)
+          if (meets(ib[c], S.own_lo, S.own_shape)) first[c] = std::min(first[c], q);
+      for (int c = 0; c < CO; ++c)
+        if (meets(ob[c], S.sup_lo, S.sup_shape)) last[c] = q;
     }
   // upload order: by first use (boxes no assembly reads go last)
-  std::vector<int> order(C);
-  for (int c = 0; c < C; ++c) order[c] = c;
+  std::vector<int> order(CI);
+  for (int c = 0; c < CI; ++c) order[c] = c;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return first[x] < first[y]; });
   P->hio_boxes.clear();
-  for (int c : order) P->hio_boxes.push_back(boxes[c]);
-  std::vector<int> pos(C);
-  for (int k = 0; k < C; ++k) pos[order[k]] = k;
+  for (int c : order) P->hio_boxes.push_back(ib[c]);
+  std::vector<int> pos(CI);
+  for (int k = 0; k < CI; ++k) pos[order[k]] = k;
   P->hio_need.assign(nq, 0);
   int need = 0;
   for (int q = 0; q < nq; ++q) {
-    for (int c = 0; c < C; ++c)
+    for (int c = 0; c < CI; ++c)
       if (first[c] == q) need = std::max(need, pos[c] + 1);
     P->hio_need[q] = need;
   }
+  P->hio_oboxes = ob;
   P->hio_out_at.assign(nq, {});
   P->hio_out_early.clear();
-  for (int c = 0; c < C; ++c) {
-    if (last[c] < 0) P->hio_out_early.push_back(pos[c]);
-    else P->hio_out_at[last[c]].push_back(pos[c]);
+  for (int c = 0; c < CO; ++c) {
+    if (last[c] < 0) P->hio_out_early.push_back(c);
+    else P->hio_out_at[last[c]].push_back(c);
   }
+  const int C = std::max(CI, CO);
   if (getenv("DS_HIO_DEBUG")) {
     fprintf(stderr, "hio: %d boxes, %d launches; uploads needed by launch:", C, nq);
     for (int q = 0; q < nq; ++q) fprintf(stderr, " %d", P->hio_need[q]);
@@ -1786,7 +1798,7 @@ static int hio_box(ds_plan *P, const HostIO *hio, int nrhs, int k, cudaStream_t 
   }();
   if ((skip & 1) && in) return DS_OK;
   if ((skip & 2) && !in) return DS_OK;
-  const HioBox &B = P->hio_boxes[k];
+  const HioBox &B = in ? P->hio_boxes[k] : P->hio_oboxes[k];
   const int64_t N = P->nnodes, S1 = P->gcounts[2], S0 = (int64_t)P->gcounts[1] * S1;
   const int L = (int)((B.c1 - B.c0) * S1), runs = B.a1 - B.a0;
   if (L <= 0 || runs <= 0) return DS_OK;
