@@ -547,3 +547,30 @@ def test_pinned_host_path_matches_device_path(cuda, cfg1):
             assert [r.nonzero_solves for r in rep_h] == [r.nonzero_solves for r in rep_dev]
     oref, _ = O.ddm_apply(prob, oops, O.Cache(), f[0])
     assert rel(ref[0], oref) <= TOL
+
+
+def test_rhs_groups_bitwise_equal_to_one_plan(cuda, cfg1):
+    """GroupedPlan (RHS groups on separate streams, the device path for
+    batches >= 16 RHS) is bitwise the single-plan map, counters included."""
+    import torch
+
+    from paper_2002_05327_b200.ddm import SweepPlan, device_plan
+
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(21)
+    shape = (16,) + b["grid"].counts
+    f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    f[3] = 0.0  # an all-zero RHS inside a group
+    fd = torch.from_numpy(f.reshape(16, -1)).cuda()
+    cache = FactorizationCache()
+    dg = device_plan(b["partition"], b["ops"], cache, SweepPlan.default(2), 16, grouped=True)
+    d1 = device_plan(b["partition"], b["ops"], cache, SweepPlan.default(2), 16)
+    assert getattr(dg, "groups", 1) == 2 and getattr(d1, "groups", 1) == 1
+    ug, _ = dg.apply(fd)
+    u1, _ = d1.apply(fd)
+    assert torch.equal(ug, u1)
+    cg, c1 = dg.counters(16), d1.counters(16)
+    for k in c1:
+        assert np.array_equal(cg[k], c1[k]), k
+    oref, _ = O.ddm_apply(prob, oops, O.Cache(), f[0])
+    assert rel(u1[0].cpu().numpy().reshape(b["grid"].counts), oref) <= TOL
