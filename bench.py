@@ -316,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     clk = clocks.stop()
     ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if os.environ.get("BENCH_DEBUG"):
+        print("device step ms:", [round(a.elapsed_time(b), 3) for a, b in evs], file=sys.stderr)
     # ---- kernel breakdown: the same K applications again, eager, with CUDA
     # events around every launch group (not part of `value`)
     ktimes = None

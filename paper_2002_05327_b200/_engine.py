@@ -616,8 +616,9 @@ class DevicePlan:
             bufs[R] = (fmin, torch.empty_like(fmin))
         return bufs[R]
 
-    def apply(self, f, collect_partials: bool = False):
-        """f: [R, N] complex128 CUDA tensor (RHS-outer) -> (u [R, N], partials)."""
+    def apply(self, f, collect_partials: bool = False, out=None):
+        """f: [R, N] complex128 CUDA tensor (RHS-outer) -> (u [R, N], partials);
+        `out` (optional, contiguous [R, N]) receives u."""
         lib, ctx = context()
         R = f.shape[0]
         n = self.nnodes
@@ -627,7 +628,7 @@ class DevicePlan:
         if collect_partials:
             partials = torch.empty((self.nsweeps, n, R), dtype=torch.complex128, device=f.device)
         self.apply_minor(fmin, umin, R, partials)
-        u = torch.empty((R, n), dtype=torch.complex128, device=f.device)
+        u = out if out is not None else torch.empty((R, n), dtype=torch.complex128, device=f.device)
         N.check(lib.ds_layout_to_outer(ctx, n, R, umin.data_ptr(), u.data_ptr()))
         parts = None
         if partials is not None:
@@ -703,18 +704,15 @@ class GroupedPlan:
             return self.plans[0].apply(f, collect_partials)  # one group (nrhs_max covers it)
         bounds = self._bounds(R)
         main = torch.cuda.current_stream()
-        outs = []
+        u = torch.empty((R, f.shape[1]), dtype=torch.complex128, device=f.device)
         for (r0, r1), p, st in zip(bounds, self.plans, self._streams):
             st.wait_stream(main)
             with torch.cuda.stream(st):
-                u, _ = p.apply(f[r0:r1])
-                outs.append(u)
+                p.apply(f[r0:r1], out=u[r0:r1])  # each group writes its rows in place
         for st in self._streams[:len(bounds)]:
             main.wait_stream(st)
-        for u, st in zip(outs, self._streams):
-            u.record_stream(main)
         self._split = bounds
-        return torch.cat(outs, 0), None
+        return u, None
 
     def counters(self, nrhs: int):
         bounds = self._split if self._split and self._split[-1][1] == nrhs else None

@@ -53,6 +53,7 @@ struct VisitDev {
   int sub, sweep, nslot, slot0;
   cplx *rhs, *x;
   int *nz;
+  const int *arr;  // arrival counts of this visit [nrhs] (per-call stride)
 };
 
 struct XferDev {
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256)
     k_assemble(const VisitDev *__restrict__ visits, const SubDev *__restrict__ subs,
                const SlotRef *__restrict__ slots, const cplx *__restrict__ f, int nrhs,
                int dim, int g0, int g1, int g2, Flags F, int64_t nnodes) {
-  __shared__ int s_nz[RMAX], s_own[RMAX];
+  __shared__ int s_nz[RMAX], s_own[RMAX], s_live[RMAX];
   __shared__ SlotRef s_slot[SLOT_SMEM];
   extern __shared__ uint32_t s_mask[];  // [E0 | E1 | E2]
   const VisitDev V = visits[blockIdx.y];
@@ -344,7 +345,14 @@ __global__ void __launch_bounds__(256)
   const FactDev fd = *sd.f;
   const int t = threadIdx.x;
   pdl_wait();
-  for (int r = t; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
+  // RHS columns that can be nonzero: an own source (sweep 1) or an arrival
+  // (K4's counts).  The others are exactly zero: their rhs entries are not
+  // written -- nothing reads them (the solves skip exact-zero columns, the
+  // transfer only reads emitting ones)
+  for (int r = t; r < nrhs; r += blockDim.x) {
+    s_nz[r] = s_own[r] = 0;
+    s_live[r] = V.sweep == 1 || V.arr[r] > 0;
+  }
   const int ns = V.nslot;
   for (int k = t; k < min(ns, SLOT_SMEM); k += blockDim.x) s_slot[k] = slots[V.slot0 + k];
   const bool own = V.sweep == 1;
@@ -436,7 +444,7 @@ __global__ void __launch_bounds__(256)
       cplx *dst = V.rhs + (int64_t)blk * nrhs + rl;
 #pragma unroll
       for (int j = 0; j < RV; ++j) {
-        dst[j] = val[j];
+        if (s_live[rl + j]) dst[j] = val[j];
         any[j] |= cnonzero(val[j]);
       }
     }
@@ -1301,6 +1309,7 @@ static int patch_tables(ds_plan *P, int nrhs) {
   for (size_t i = 0; i < P->h_visits.size(); ++i) {
     VisitDev &V = P->h_visits[i];
     V.nz = F.nz + ((size_t)(V.sweep - 1) * P->nsub + V.sub) * nrhs;
+    V.arr = F.arr_cnt + ((size_t)(V.sweep - 1) * P->nsub + V.sub) * nrhs;
   }
   for (size_t e = 0; e < P->h_solve.size(); ++e) P->h_solve[e].nz = P->h_visits[P->blu_vidx[e]].nz;
   for (size_t e = 0; e < P->h_mjobs.size(); ++e) P->h_mjobs[e].nz = P->h_visits[P->mod_vidx[e]].nz;
