@@ -735,6 +735,9 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
       case 'w': return launch_gemm<2, 2, 2, 8, 6, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'x': return launch_gemm<1, 2, 2, 8, 8, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'y': return launch_gemm<2, 2, 2, 4, 4, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'z': return launch_gemm<1, 7, 2, 8, 2, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'Z': return launch_gemm<1, 7, 1, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+      case 'Y': return launch_gemm<1, 7, 2, 16, 2, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
       default: return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
     }
   };

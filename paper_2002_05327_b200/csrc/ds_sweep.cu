@@ -843,6 +843,128 @@ __global__ void __launch_bounds__(256, K4_MINB(DIM))
   if (flag_bases) __threadfence_system();  // sharded: peer-memory payloads before the barrier
 }
 
+// K4 v3 (2D default): k_transfer2 with RV RHS columns per thread (lanes of a
+// node take columns l, l + LPN, ...; every load instruction of a node's
+// lanes still covers LPN consecutive 16-byte values) and the stencil
+// accumulated point by point in psi's order, so the node geometry, the
+// (1 - beta) factors and the couplings are computed once per RV columns and
+// only one point's RV values are live at a time (k_transfer2 kept all seven
+// points x NPT nodes in registers: 112 registers, 18% occupancy, 20% of
+// HBM on config 4).
+#ifndef K4V3_MINB
+#define K4V3_MINB 2
+#endif
+template <int DIM, int RV>
+__global__ void __launch_bounds__(256, K4V3_MINB)
+    k_transfer3(const XferDev *__restrict__ xfers, const XferRec *__restrict__ recs,
+                const int4 *__restrict__ tiles, int ntiles, int nx, int nsub, int nrhs, Flags F,
+                int *const *__restrict__ flag_bases, int nsweeps) {
+  __shared__ XferRec R;
+  const int t = threadIdx.x;
+  pdl_wait();
+  for (int gt = blockIdx.x * blockDim.x + t; gt < nx * nrhs; gt += gridDim.x * blockDim.x) {
+    const int i = gt / nrhs, r = gt % nrhs;
+    const XferRec &Q = recs[i];
+    if (!Q.nz[r]) continue;
+    const int cut = solve_cut(F, Q.sweep, Q.src, nsub, r, nrhs);
+    const XferDev &X = xfers[i];
+    if (cut & X.dirmask) continue;
+    if (X.use == 0) {
+      atomicAdd(&F.discard[r], 1);
+    } else {
+      int *arr_cnt = F.arr_cnt, *arr_cut = F.arr_cut;
+      if (flag_bases) arrival_words(flag_bases[X.owner], nsweeps, nsub, nrhs, arr_cnt, arr_cut);
+      const size_t ti = ((size_t)(X.use - 1) * nsub + X.dst) * nrhs + r;
+      atomicAdd_system(&arr_cnt[ti], 1);
+      atomicAnd_system(&arr_cut[ti], X.content_base | (cut & X.keepmask));
+      atomicAdd(&F.emit_cnt[((size_t)(Q.sweep - 1) * nsub + X.src) * nrhs + r], 1);
+    }
+  }
+  const int lpn = nrhs / RV;
+  const int npb = blockDim.x / lpn, rl = t % lpn, ln = t / lpn;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int4 T = tiles[tile];
+    __syncthreads();
+    if (t < (int)(sizeof(XferRec) / 8))
+      reinterpret_cast<long long *>(&R)[t] = reinterpret_cast<const long long *>(recs + T.x)[t];
+    __syncthreads();
+    if (ln >= npb) continue;
+    bool emit[RV];
+    bool anyemit = false;
+#pragma unroll
+    for (int j = 0; j < RV; ++j) {
+      const int r = rl + j * lpn;
+      emit[j] = R.nz[r] && !(solve_cut(F, R.sweep, R.src, nsub, r, nrhs) & R.dirmask);
+      anyemit |= emit[j];
+    }
+    if (!anyemit) continue;
+    const cplx *__restrict__ xs = R.x;
+    const int nodes = T.z;
+    for (int node = T.y + ln; node < nodes; node += npb) {
+      int e[3];
+      if (DIM == 3) {
+        e[2] = node % R.shape[2];
+        const int q = node / R.shape[2];
+        e[1] = q % R.shape[1];
+        e[0] = q / R.shape[1];
+      } else {
+        e[1] = node % R.shape[1];
+        e[0] = node / R.shape[1];
+        e[2] = 0;
+      }
+      int off = 0, k2i = 0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        off += R.str[a] * e[a];
+        k2i += R.k2str[a] * e[a];
+      }
+      double f0[DIM];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) f0[a] = R.fac[a][e[a]];
+      double w0m1 = 1.0;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) w0m1 = w0m1 * f0[a];
+      w0m1 -= 1.0;
+      const double k2 = R.k2[k2i];
+      const cplx *xc = xs + (int64_t)off * nrhs + rl;
+      cplx acc[RV], w0[RV];
+#pragma unroll
+      for (int j = 0; j < RV; ++j) {
+        w0[j] = cscale(xc[j * lpn], w0m1);
+        acc[j] = cscale(w0[j], k2);
+      }
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        const cplx lo = R.clo[a][e[a]], hi = R.chi[a][e[a]];
+        const cplx mlh = make_double2(-(lo.x + hi.x), -(lo.y + hi.y));
+#pragma unroll
+        for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(mlh, w0[j]));
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const int ea = e[a] + (side ? 1 : -1);
+          if (side ? ea < R.ehi[a] : ea >= R.elo[a]) {
+            // w(p +- e_a) - 1 with w = prod_b fac_b in axis order
+            double wt = 1.0;
+#pragma unroll
+            for (int b = 0; b < DIM; ++b) wt = wt * (b == a ? R.fac[a][ea] : f0[b]);
+            const double wm1 = wt - 1.0;
+            const cplx cf = side ? hi : lo;
+            const cplx *xp = xc + (int64_t)(side ? R.str[a] : -R.str[a]) * nrhs;
+#pragma unroll
+            for (int j = 0; j < RV; ++j) acc[j] = cadd(acc[j], cmul(cf, cscale(xp[j * lpn], wm1)));
+          }
+        }
+      }
+      const cplx *rv = R.rhs + (int64_t)off * nrhs + rl;
+      cplx *sp = R.slot + (int64_t)node * nrhs + rl;
+#pragma unroll
+      for (int j = 0; j < RV; ++j)
+        if (emit[j]) sp[j * lpn] = cadd(sp[j * lpn], cscale(cadd(rv[j * lpn], acc[j]), R.sign));
+    }
+  }
+  if (flag_bases) __threadfence_system();
+}
+
 // ------------------------------------------------------------ plan create
 
 extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out) {
@@ -1628,8 +1750,24 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
           const XferRec *xr = P->recs + x0;
           const int4 *tl = P->tiles + t0;
           int *const *fb = P->d_flag_bases;
-          if (dim == 2)
+          static const int k4v = [] {
+            const char *v = getenv("DS_K4");
+            return v && *v == 'v' ? atoi(v + 1) : 0;
+          }();
+          // defaults (measured): 2D k_transfer3 (config 2 +3%), 3D k_transfer2
+          // (config 4: 7.5 vs 7.9 ms per application with k_transfer3<3, 4>)
+          const int v3rv = (dim == 3 && k4v == 3) ? (nrhs % 4 == 0 ? 4 : (nrhs % 2 == 0 ? 2 : 1)) : 0;
+          if (dim == 2 && k4v != 2)
+            DS_CUDA(launch_pdl(k_transfer3<2, 1>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
+                               P->nsub, nrhs, F, fb, P->nsweeps));
+          else if (dim == 2)
             DS_CUDA(launch_pdl(k_transfer2<2, K4_NPT(2)>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
+                               P->nsub, nrhs, F, fb, P->nsweeps));
+          else if (v3rv == 4)
+            DS_CUDA(launch_pdl(k_transfer3<3, 4>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
+                               P->nsub, nrhs, F, fb, P->nsweeps));
+          else if (v3rv == 2)
+            DS_CUDA(launch_pdl(k_transfer3<3, 2>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
                                P->nsub, nrhs, F, fb, P->nsweeps));
           else
             DS_CUDA(launch_pdl(k_transfer2<3, K4_NPT(3)>, dim3(gb), dim3(256), 0, st, xd, xr, tl, nt, nx,
