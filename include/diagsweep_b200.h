@@ -243,6 +243,14 @@ DS_API int ds_ddm_counters(ds_ctx *ctx, ds_plan *plan, int32_t nrhs,
  * pointers and nrhs); ds_ddm_apply uses the graph when it matches. */
 DS_API int ds_ddm_enable_graph(ds_ctx *ctx, ds_plan *plan, int32_t enable);
 
+/* ds_ddm_apply_host for a batch split into G contiguous RHS groups, one
+ * identical plan per group (plans[g] covers RHS [nrhs g / G, nrhs (g+1) / G)):
+ * the groups sweep concurrently on their own streams while one shared copy
+ * pipeline uploads each source box once and downloads each result box once
+ * every group has finalized it.  Results are bitwise those of one plan. */
+DS_API int ds_ddm_apply_host_groups(ds_ctx *ctx, ds_plan *const *plans, int32_t ngroups,
+                                    const ds_cplx *f_host, ds_cplx *u_host, int32_t nrhs);
+
 /* ds_ddm_apply on RHS-outer device buffers f_dev / u_dev ([nrhs][N], the
  * batched API layout): the assembly reads and the accumulation writes that
  * layout directly (no layout transposes); no per-sweep partials. */

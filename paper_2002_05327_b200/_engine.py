@@ -714,6 +714,18 @@ class GroupedPlan:
         self._split = bounds
         return u, None
 
+    def apply_host(self, f_host, u_host):
+        """Pinned host f [R, N] -> pinned host u: the groups sweep
+        concurrently, one shared copy pipeline (ds_ddm_apply_host_groups)."""
+        R = f_host.shape[0]
+        G = min(self.groups, R)
+        lib, ctx = context()
+        arr = (C.c_void_p * G)(*[p.handle.value for p in self.plans[:G]])
+        N.check(lib.ds_ddm_apply_host_groups(ctx, arr, G, f_host.data_ptr(), u_host.data_ptr(), R),
+                "ds_ddm_apply_host_groups")
+        torch.cuda.current_stream().synchronize()
+        self._split = self._bounds(R)
+
     def counters(self, nrhs: int):
         bounds = self._split if self._split and self._split[-1][1] == nrhs else None
         if bounds is None:

@@ -103,6 +103,7 @@ _SIGNATURES = [
     ("ds_ddm_apply", C.c_int, [vp, vp, vp, vp, i32, vp]),
     ("ds_ddm_apply_host", C.c_int, [vp, vp, vp, vp, i32]),
     ("ds_ddm_apply_outer", C.c_int, [vp, vp, vp, vp, i32]),
+    ("ds_ddm_apply_host_groups", C.c_int, [vp, C.POINTER(vp), i32, vp, vp, i32]),
     ("ds_ddm_counters", C.c_int, [vp, vp, i32, P_i32, P_i32, P_i32, P_i32, P_i32, P_i32]),
     ("ds_ddm_enable_graph", C.c_int, [vp, vp, i32]),
     ("ds_plan_last_launches", i64, [vp]),

@@ -1425,8 +1425,11 @@ extern "C" int ds_plan_destroy(ds_plan *P) {
 }
 
 // point the per-visit nz flags at the [sweep][sub][nrhs] table of this stride
+static int64_t g_patch_gen = 0;  // bumped whenever a plan's tables are rebuilt (grouped graphs)
+
 static int patch_tables(ds_plan *P, int nrhs) {
   if (P->patched_nrhs == nrhs) return DS_OK;
+  ++g_patch_gen;
   Flags F = flags_view(P, nrhs);
   for (size_t i = 0; i < P->h_visits.size(); ++i) {
     VisitDev &V = P->h_visits[i];
@@ -1584,6 +1587,12 @@ static int set_io(ds_plan *P, const void *f, void *u, cudaStream_t st) {
 struct HostIO {
   const cplx *fh;  // pinned host sources, RHS-outer [R][N]
   cplx *uh;        // pinned host result, RHS-outer [R][N]
+  // external mode (RHS groups, ds_ddm_apply_host_groups): the caller issues
+  // the copies; the sweep only waits on the shared upload events and records
+  // its per-box finalization events
+  bool ext = false;
+  const cudaEvent_t *ev_in = nullptr;
+  cudaEvent_t *ev_out = nullptr;
 };
 
 // DS_HIO_TRACE (eager host path only): timestamps of uploads, launches and
@@ -1625,7 +1634,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
     P->k5_pending[0] = P->k5_pending[1] = false;
   }
-  if (hio) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
+  if (hio && !hio->ext) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
     DS_CUDA(cudaEventRecord(P->hio_fork, st));
     DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_fork, 0));
     DS_CUDA(cudaStreamWaitEvent(P->cstream2, P->hio_fork, 0));
@@ -1657,8 +1666,9 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
       if (hio && P->hio_need[q] > hio_waited) {  // f boxes [0, need) this assembly may read:
         hio_waited = P->hio_need[q];               // the last of them on each copy stream
-        DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 1], 0));
-        if (hio_waited >= 2) DS_CUDA(cudaStreamWaitEvent(st, P->hio_ev_in[hio_waited - 2], 0));
+        const cudaEvent_t *evi = hio->ext ? hio->ev_in : P->hio_ev_in.data();
+        DS_CUDA(cudaStreamWaitEvent(st, evi[hio_waited - 1], 0));
+        if (hio_waited >= 2) DS_CUDA(cudaStreamWaitEvent(st, evi[hio_waited - 2], 0));
       }
       if (hio) trace_mark("launch " + std::to_string(q), st);
       prof_mark(P, 0, st);
@@ -1717,7 +1727,9 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         DS_CUDA(cudaEventRecord(P->ev_k5[q & 1], s5));
         k5_pending[q & 1] = true;
       }
-      if (hio)  // u chunks whose last accumulation this was: transpose + D2H
+      if (hio && hio->ext)  // the caller downloads: mark the boxes this accumulation finalized
+        for (int c : P->hio_out_at[q]) DS_CUDA(cudaEventRecord(hio->ev_out[c], s5));
+      if (hio && !hio->ext)  // u chunks whose last accumulation this was: transpose + D2H
         for (int c : P->hio_out_at[q]) {
           cudaStream_t cs = (hio_nout++ & 1) ? P->cstream2 : P->cstream;
           DS_CUDA(cudaEventRecord(P->hio_ev_out[c], s5));
@@ -1794,7 +1806,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaEventRecord(P->ev_join, s5));
     DS_CUDA(cudaStreamWaitEvent(st, P->ev_join, 0));
   }
-  if (hio) {  // join the copy stream: every u chunk is on the host
+  if (hio && !hio->ext) {  // join the copy stream: every u chunk is on the host
     DS_CUDA(cudaEventRecord(P->hio_join, P->cstream));
     DS_CUDA(cudaStreamWaitEvent(st, P->hio_join, 0));
     DS_CUDA(cudaEventRecord(P->hio_join2, P->cstream2));
@@ -2290,5 +2302,211 @@ extern "C" int ds_plan_kernel_times(ds_plan *P, double *ms, int64_t *count, int3
     if (count) count[c] += 1;
   }
   if (reset) P->ev_used = 0;
+  return DS_OK;
+}
+
+
+// ---------------------------------------------------------------------
+// One application of an RHS-grouped batch from pinned host buffers: groups
+// g = 0..G-1 (identical plans over contiguous RHS ranges) sweep concurrently
+// on their own streams (the device path's GroupedPlan), while one shared
+// copy pipeline moves each source box once (all RHS) and transposes its
+// rows into every group's RHS-minor buffer, and downloads each result box
+// once both groups have finalized it.
+struct GroupHost {
+  cplx *fo = nullptr, *uo = nullptr;  // RHS-outer staging [R][N]
+  size_t cap = 0;                     // complex elements
+  std::vector<cudaStream_t> gs;
+  std::vector<cudaEvent_t> gjoin;
+  struct G {
+    const void *fh;
+    void *uh;
+    int nrhs, groups;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    int64_t gen;  // g_patch_gen at capture
+    std::vector<const ds_plan *> plans;
+  };
+  std::vector<G> graphs;
+};
+static GroupHost *g_group_host = nullptr;  // one per process (plans of one device)
+
+static int box_transpose(ds_plan *P0, const HioBox &B, int R, const cplx *src, cplx *dst, int to_minor,
+                         cudaStream_t cs) {
+  const int64_t N = P0->nnodes, S1 = P0->gcounts[2], S0 = (int64_t)P0->gcounts[1] * S1;
+  const int L = (int)((B.c1 - B.c0) * S1), runs = B.a1 - B.a0;
+  if (L <= 0 || runs <= 0 || R <= 0) return DS_OK;
+  const int64_t base0 = (int64_t)B.a0 * S0 + (int64_t)B.c0 * S1;
+  const dim3 grid((unsigned)(((R + 31) / 32) * ((L + 31) / 32)), runs);
+  k_box_transpose<<<grid, dim3(32, 8), 0, cs>>>(R, L, N, base0, S0, src, dst, to_minor);
+  P0->ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+static int box_copy(ds_plan *P0, const HioBox &B, int R, cplx *host, cplx *dev, bool h2d, cudaStream_t cs) {
+  const int64_t S1 = P0->gcounts[2], S0 = (int64_t)P0->gcounts[1] * S1;
+  const int L = (int)((B.c1 - B.c0) * S1), runs = B.a1 - B.a0;
+  if (L <= 0 || runs <= 0) return DS_OK;
+  cudaMemcpy3DParms m = {};
+  cudaPitchedPtr hp = make_cudaPitchedPtr(host, sizeof(cplx) * S0, sizeof(cplx) * S0, P0->gcounts[0]);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, sizeof(cplx) * S0, sizeof(cplx) * S0, P0->gcounts[0]);
+  const cudaPos at = make_cudaPos(sizeof(cplx) * B.c0 * S1, B.a0, 0);
+  m.extent = make_cudaExtent(sizeof(cplx) * L, runs, R);
+  m.srcPtr = h2d ? hp : dp;
+  m.dstPtr = h2d ? dp : hp;
+  m.srcPos = at;
+  m.dstPos = at;
+  m.kind = h2d ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  DS_CUDA(cudaMemcpy3DAsync(&m, cs));
+  return DS_OK;
+}
+
+static int issue_groups(ds_ctx *ctx, ds_plan *const *plans, int G, const cplx *fh, cplx *uh, int nrhs,
+                        GroupHost *GH) {
+  ds_plan *P0 = plans[0];
+  cudaStream_t st = ctx->stream;
+  const int64_t N = P0->nnodes;
+  std::vector<int> r0(G + 1);
+  for (int g = 0; g <= G; ++g) r0[g] = (int)((int64_t)nrhs * g / G);
+  DS_CUDA(cudaEventRecord(P0->hio_fork, st));
+  DS_CUDA(cudaStreamWaitEvent(P0->cstream, P0->hio_fork, 0));
+  DS_CUDA(cudaStreamWaitEvent(P0->cstream2, P0->hio_fork, 0));
+  for (int g = 0; g < G; ++g) DS_CUDA(cudaStreamWaitEvent(GH->gs[g], P0->hio_fork, 0));
+  // uploads: each box once (all RHS), transposed into every group's buffer
+  for (int k = 0; k < (int)P0->hio_boxes.size(); ++k) {
+    cudaStream_t cs = (k & 1) ? P0->cstream2 : P0->cstream;
+    const HioBox &B = P0->hio_boxes[k];
+    if (int rc = box_copy(P0, B, nrhs, (cplx *)fh, GH->fo, true, cs)) return rc;
+    for (int g = 0; g < G; ++g)
+      if (int rc = box_transpose(P0, B, r0[g + 1] - r0[g], GH->fo + (int64_t)r0[g] * N, plans[g]->hio_fm, 1, cs))
+        return rc;
+    DS_CUDA(cudaEventRecord(P0->hio_ev_in[k], cs));
+  }
+  // the groups' sweeps
+  for (int g = 0; g < G; ++g) {
+    HostIO h{fh, uh};
+    h.ext = true;
+    h.ev_in = P0->hio_ev_in.data();
+    h.ev_out = plans[g]->hio_ev_out.data();
+    ctx->stream = GH->gs[g];
+    plans[g]->ctx = ctx;
+    int rc = issue_apply(plans[g], plans[g]->hio_fm, plans[g]->hio_um, r0[g + 1] - r0[g], nullptr, 0, -1, 3, &h);
+    ctx->stream = st;
+    if (rc) return rc;
+    DS_CUDA(cudaEventRecord(GH->gjoin[g], GH->gs[g]));
+  }
+  // downloads: each box once every group has finalized it
+  int nout = 0;
+  auto download = [&](int c, bool after_groups) -> int {
+    cudaStream_t cs = (nout++ & 1) ? P0->cstream2 : P0->cstream;
+    for (int g = 0; g < G; ++g)
+      DS_CUDA(cudaStreamWaitEvent(cs, after_groups ? GH->gjoin[g] : plans[g]->hio_ev_out[c], 0));
+    const HioBox &B = P0->hio_oboxes[c];
+    for (int g = 0; g < G; ++g)
+      if (int rc = box_transpose(P0, B, r0[g + 1] - r0[g], plans[g]->hio_um, GH->uo + (int64_t)r0[g] * N, 0, cs))
+        return rc;
+    return box_copy(P0, B, nrhs, uh, GH->uo, false, cs);
+  };
+  const int nq = (int)P0->vstep_off.size() - 1;
+  for (int q = 0; q < nq; ++q)
+    for (int c : P0->hio_out_at[q])
+      if (int rc = download(c, false)) return rc;
+  for (int c : P0->hio_out_early)
+    if (int rc = download(c, true)) return rc;
+  for (int g = 0; g < G; ++g) DS_CUDA(cudaStreamWaitEvent(st, GH->gjoin[g], 0));
+  DS_CUDA(cudaEventRecord(P0->hio_join, P0->cstream));
+  DS_CUDA(cudaStreamWaitEvent(st, P0->hio_join, 0));
+  DS_CUDA(cudaEventRecord(P0->hio_join2, P0->cstream2));
+  DS_CUDA(cudaStreamWaitEvent(st, P0->hio_join2, 0));
+  return DS_OK;
+}
+
+extern "C" int ds_ddm_apply_host_groups(ds_ctx *ctx, ds_plan *const *plans, int32_t G,
+                                        const ds_cplx *f_host, ds_cplx *u_host, int32_t nrhs) {
+  if (!ctx || !plans || G < 1 || G > 16 || !f_host || !u_host)
+    return ds_fail(DS_ECONFIG, "ds_ddm_apply_host_groups: bad argument");
+  ds_plan *P0 = plans[0];
+  for (int g = 0; g < G; ++g) {
+    ds_plan *P = plans[g];
+    if (!P || P->nranks > 1 || P->vstep_off.size() != P0->vstep_off.size() || P->nnodes != P0->nnodes)
+      return ds_fail(DS_ECONFIG, "ds_ddm_apply_host_groups: plans must be identical unsharded plans");
+    const int Rg = (int)((int64_t)nrhs * (g + 1) / G - (int64_t)nrhs * g / G);
+    if (Rg < 1 || Rg > P->nrhs_max) return ds_fail(DS_ECONFIG, "ds_ddm_apply_host_groups: group too large");
+    P->ctx = ctx;
+    if (int rc = patch_tables(P, Rg)) return rc;
+    if (int rc = hio_setup(P)) return rc;
+    if (P->slots_dirty) {
+      for (auto &b : P->slot_bufs) DS_CUDA(cudaMemsetAsync(b.first, 0, b.second, ctx->stream));
+      P->slots_dirty = false;
+    }
+    if (int rc = set_io(P, P->hio_fm, P->hio_um, ctx->stream)) return rc;
+  }
+  if (!g_group_host) g_group_host = new GroupHost();
+  GroupHost *GH = g_group_host;
+  const size_t need = (size_t)P0->nnodes * nrhs;
+  if (need > GH->cap) {
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto &gg : GH->graphs) cudaGraphExecDestroy(gg.exec);
+    GH->graphs.clear();
+    if (GH->fo) cudaFree(GH->fo);
+    if (GH->uo) cudaFree(GH->uo);
+    GH->fo = GH->uo = nullptr;
+    GH->cap = 0;
+    DS_CUDA(cudaMalloc(&GH->fo, sizeof(cplx) * need));
+    DS_CUDA(cudaMalloc(&GH->uo, sizeof(cplx) * need));
+    GH->cap = need;
+  }
+  while ((int)GH->gs.size() < G) {
+    cudaStream_t s;
+    cudaEvent_t e;
+    DS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    DS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    GH->gs.push_back(s);
+    GH->gjoin.push_back(e);
+  }
+  if (!P0->use_graph || P0->profiling) return issue_groups(ctx, plans, G, (const cplx *)f_host, (cplx *)u_host, nrhs, GH);
+  if (!P0->gstream) {
+    DS_CUDA(cudaStreamCreateWithFlags(&P0->gstream, cudaStreamNonBlocking));
+    DS_CUDA(cudaEventCreateWithFlags(&P0->gev_in, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&P0->gev_out, cudaEventDisableTiming));
+  }
+  cudaStream_t user = ctx->stream;
+  GroupHost::G *hit = nullptr;
+  for (auto &gg : GH->graphs)
+    if (gg.fh == f_host && gg.uh == u_host && gg.nrhs == nrhs && gg.groups == G && gg.gen == g_patch_gen &&
+        std::equal(gg.plans.begin(), gg.plans.end(), plans))
+      hit = &gg;
+  DS_CUDA(cudaEventRecord(P0->gev_in, user));
+  DS_CUDA(cudaStreamWaitEvent(P0->gstream, P0->gev_in, 0));
+  if (!hit) {
+    if (GH->graphs.size() >= 4) {
+      cudaGraphExecDestroy(GH->graphs.front().exec);
+      GH->graphs.erase(GH->graphs.begin());
+    }
+    cudaGraph_t gr;
+    ctx->stream = P0->gstream;
+    DS_CUDA(cudaStreamBeginCapture(P0->gstream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = ctx->launches;
+    int rc = issue_groups(ctx, plans, G, (const cplx *)f_host, (cplx *)u_host, nrhs, GH);
+    cudaError_t e = cudaStreamEndCapture(P0->gstream, &gr);
+    ctx->stream = user;
+    if (rc) {
+      for (int g = 0; g < G; ++g) plans[g]->slots_dirty = true;
+      return rc;
+    }
+    if (e != cudaSuccess) return ds_fail(DS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    GroupHost::G h{f_host, u_host, nrhs, G, nullptr, ctx->launches - l0, g_patch_gen,
+                   std::vector<const ds_plan *>(plans, plans + G)};
+    DS_CUDA(cudaGraphInstantiate(&h.exec, gr, cudaGraphInstantiateFlagUseNodePriority));
+    cudaGraphDestroy(gr);
+    ctx->launches = l0;
+    GH->graphs.push_back(h);
+    hit = &GH->graphs.back();
+  }
+  DS_CUDA(cudaGraphLaunch(hit->exec, P0->gstream));
+  DS_CUDA(cudaEventRecord(P0->gev_out, P0->gstream));
+  DS_CUDA(cudaStreamWaitEvent(user, P0->gev_out, 0));
+  ctx->launches += hit->launches;
   return DS_OK;
 }

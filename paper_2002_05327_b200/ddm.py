@@ -241,7 +241,11 @@ def diagonal_sweep_solve(f, partition: Partition, operators: dict,
         if fh.dtype != torch.complex128 or not fh.is_contiguous():
             fh = fh.to(torch.complex128).contiguous().pin_memory()
         R = fh.shape[0]
-        dp = device_plan(partition, operators, cache, plan, R)
+        # one plan: RHS groups with a shared copy pipeline (DS_HOST_GROUPS=1,
+        # ds_ddm_apply_host_groups) measured 5.39 vs 5.05 ms on config 2 --
+        # the PCIe phases gate both groups alike (tools/host_groups_probe.py)
+        dp = device_plan(partition, operators, cache, plan, R,
+                         grouped=os.environ.get("DS_HOST_GROUPS", "0") == "1")
         uh = torch.empty(fh.shape, dtype=torch.complex128, pin_memory=True)
         dp.apply_host(fh, uh)
         reports = _reports(dp, R, plan, partition, record_events, record_transfers)

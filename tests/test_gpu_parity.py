@@ -574,3 +574,33 @@ def test_rhs_groups_bitwise_equal_to_one_plan(cuda, cfg1):
         assert np.array_equal(cg[k], c1[k]), k
     oref, _ = O.ddm_apply(prob, oops, O.Cache(), f[0])
     assert rel(u1[0].cpu().numpy().reshape(b["grid"].counts), oref) <= TOL
+
+
+def test_grouped_pinned_host_path(cuda, cfg1):
+    """16 pinned host RHS: two RHS groups sweep concurrently with one shared
+    upload / download pipeline (ds_ddm_apply_host_groups); bitwise the
+    device path, counters included, also on graph replay."""
+    import torch
+
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(33)
+    shape = (16,) + b["grid"].counts
+    f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    f[5] = 0.0
+    cache = FactorizationCache()
+    u_dev, rep_dev = diagonal_sweep_solve(torch.from_numpy(f).cuda(), b["partition"], b["ops"], cache,
+                                          warn_collar=False)
+    ref = u_dev.values.cpu().numpy()
+    fp = torch.from_numpy(f).pin_memory()
+    import os
+
+    os.environ["DS_HOST_GROUPS"] = "1"
+    try:
+        runs = [diagonal_sweep_solve(fp, b["partition"], b["ops"], cache, warn_collar=False)
+                for _ in range(3)]
+    finally:
+        del os.environ["DS_HOST_GROUPS"]
+    for u_h, rep_h in runs:
+        assert np.array_equal(u_h.values.numpy(), ref)
+        assert [r.nonzero_solves for r in rep_h] == [r.nonzero_solves for r in rep_dev]
+        assert [r.discarded_sources for r in rep_h] == [r.discarded_sources for r in rep_dev]
