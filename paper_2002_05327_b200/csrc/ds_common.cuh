@@ -210,6 +210,10 @@ int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_
 // one phase of it: 0 forward transforms, 1 recurrences, 2 inverse transforms
 int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host,
                           int njob, int nrhs, int phase);
+// all three phases in one launch, ordered per visit by counters[2 * njob]
+// (zeroed before the application; 2D operators only)
+int ds_launch_modal_fused(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,
+                          int nrhs, int *counters);
 void ds_fill_layout(const OpDev &o, FactDev &f);
 
 int ceil_div(int a, int b);

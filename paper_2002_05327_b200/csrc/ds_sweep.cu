@@ -97,6 +97,7 @@ struct ds_plan {
   std::vector<int> blu_vidx, blu_off;  // visit index of each entry; per-launch offsets
   // modal visits (FactDev kind 1): job table, factor layouts, offsets
   ModalJob *mjobs = nullptr;
+  int *mcount = nullptr;  // fused modal solve: 2 counters per modal job, zeroed per application
   std::vector<ModalJob> h_mjobs;
   std::vector<FactDev> h_mfacts;
   std::vector<int> mod_vidx, mod_off;
@@ -1342,6 +1343,10 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->solvetab = (SolveVisit *)mem;
   if (plan_alloc(P, &mem, sizeof(ModalJob) * std::max<size_t>(P->h_mjobs.size(), 1))) return fail(DS_ECUDA);
   P->mjobs = (ModalJob *)mem;
+  if (!P->h_mjobs.empty()) {
+    if (plan_alloc(P, &mem, sizeof(int) * 2 * P->h_mjobs.size())) return fail(DS_ECUDA);
+    P->mcount = (int *)mem;
+  }
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
   cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice);
@@ -1632,6 +1637,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
     DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
     DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
+    if (P->mcount) DS_CUDA(cudaMemsetAsync(P->mcount, 0, sizeof(int) * 2 * P->h_mjobs.size(), st));
     P->k5_pending[0] = P->k5_pending[1] = false;
   }
   if (hio && !hio->ext) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
@@ -1697,7 +1703,17 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         else rc = ds_launch_solve_table(ctx, P->solvetab + b0, nbl, nrhs, P->max_m);
       }
       if (rc) return rc;
-      if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
+      // fused modal solve (DS_MFUSE=1, opt-in): correct, but under graph
+      // replay its spin-waiting CTAs and larger shared-memory footprint cost
+      // more than the two kernel boundaries it removes (config 2: 3460 vs
+      // 3625 RHS/s ungrouped, 2825 vs 3825 with RHS groups)
+      static const bool mfuse = [] {
+        const char *v = getenv("DS_MFUSE");
+        return v && v[0] == '1';
+      }();
+      if (nmo > 0 && mfuse && P->dim == 2 && nmo <= 64 && !skip_cls) {  // fused modal solve
+        rc = ds_launch_modal_fused(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, P->mcount + 2 * m0);
+      } else if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
         for (int ph = 0; ph < 3 && !rc; ++ph) {
           if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
           if (skip_cls & (ph == 1 ? 4 : 2)) continue;

@@ -604,3 +604,36 @@ def test_grouped_pinned_host_path(cuda, cfg1):
         assert np.array_equal(u_h.values.numpy(), ref)
         assert [r.nonzero_solves for r in rep_h] == [r.nonzero_solves for r in rep_dev]
         assert [r.discarded_sources for r in rep_h] == [r.discarded_sources for r in rep_dev]
+
+
+def test_fused_modal_solve_opt_in(cuda, cfg1):
+    """The opt-in fused modal solve (DS_MFUSE=1: transforms, recurrences and
+    inverse transforms of a launch in one kernel ordered by per-visit
+    counters) matches the three-kernel solve.  The switch is read once per
+    process, so this runs in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch\n"
+        "from paper_2002_05327_b200 import FactorizationCache, configs\n"
+        "from paper_2002_05327_b200.ddm import SweepPlan, device_plan\n"
+        "s = configs.spec(1); b = configs.build(s)\n"
+        "rng = np.random.default_rng(4); f = rng.standard_normal((4,) + b['grid'].counts)\n"
+        "fd = torch.from_numpy(f.astype(np.complex128).reshape(4, -1)).cuda()\n"
+        "dp = device_plan(b['partition'], b['ops'], FactorizationCache(), SweepPlan.default(2), 4)\n"
+        "u, _ = dp.apply(fd); np.save(sys.argv[1], u.cpu().numpy())\n") % str(
+            __import__("pathlib").Path(__file__).resolve().parents[1])
+    import tempfile
+
+    outs = []
+    for flag in ("0", "1"):
+        path = tempfile.mktemp(suffix=".npy")
+        env = dict(os.environ, DS_MFUSE=flag)
+        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=600)
+        outs.append(np.load(path))
+    # the fused kernel segments the recurrences differently (4 segments per
+    # 32 columns instead of n_b / 8): equal to rounding, not bitwise
+    assert rel(outs[1], outs[0]) <= 1e-12
