@@ -1678,8 +1678,24 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       }
       if (hio) trace_mark("launch " + std::to_string(q), st);
       prof_mark(P, 0, st);
+      static const int k6rv = [] {  // RHS columns per thread of K6 (default 4; 2 / 1 for tests)
+        const char *v = getenv("DS_K6_RV");
+        return v && *v ? atoi(v) : 4;
+      }();
       if (skip_cls & 1) {
-      } else if (nrhs % 4 == 0)
+      } else if (k6rv == 8 && nrhs % 8 == 0)
+        DS_CUDA(launch_pdl(outer ? k_assemble<8, true> : k_assemble<8, false>, dim3(bx, G), dim3(256),
+                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
+                           (const SlotRef *)P->slots, f, nrhs, dim,
+                           P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
+      else if (k6rv == 2 && nrhs % 2 == 0)
+        DS_CUDA(launch_pdl(outer ? k_assemble<2, true> : k_assemble<2, false>, dim3(bx, G), dim3(256),
+                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
+                           (const SlotRef *)P->slots, f, nrhs, dim,
+                           P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
+      else if (k6rv >= 4 && nrhs % 4 == 0)
         DS_CUDA(launch_pdl(outer ? k_assemble<4, true> : k_assemble<4, false>, dim3(bx, G), dim3(256),
                            sizeof(uint32_t) * P->max_axis_sum, st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
