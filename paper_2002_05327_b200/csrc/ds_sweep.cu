@@ -345,15 +345,9 @@ __global__ void __launch_bounds__(256)
   const SubDev &sd = subs[V.sub];
   const FactDev fd = *sd.f;
   const int t = threadIdx.x;
-  pdl_wait();
-  // RHS columns that can be nonzero: an own source (sweep 1) or an arrival
-  // (K4's counts).  The others are exactly zero: their rhs entries are not
-  // written -- nothing reads them (the solves skip exact-zero columns, the
-  // transfer only reads emitting ones)
-  for (int r = t; r < nrhs; r += blockDim.x) {
-    s_nz[r] = s_own[r] = 0;
-    s_live[r] = V.sweep == 1 || V.arr[r] > 0;
-  }
+  // static part first (slot table, axis masks): under programmatic
+  // dependent launch it overlaps the previous kernel's tail
+  for (int r = t; r < nrhs; r += blockDim.x) s_nz[r] = s_own[r] = 0;
   const int ns = V.nslot;
   for (int k = t; k < min(ns, SLOT_SMEM); k += blockDim.x) s_slot[k] = slots[V.slot0 + k];
   const bool own = V.sweep == 1;
@@ -371,6 +365,12 @@ __global__ void __launch_bounds__(256)
       s_mask[x] = mk;
     }
   }
+  pdl_wait();
+  // RHS columns that can be nonzero: an own source (sweep 1) or an arrival
+  // (K4's counts).  The others are exactly zero: their rhs entries are not
+  // written -- nothing reads them (the solves skip exact-zero columns, the
+  // transfer only reads emitting ones)
+  for (int r = t; r < nrhs; r += blockDim.x) s_live[r] = V.sweep == 1 || V.arr[r] > 0;
   __syncthreads();
   const int gc[3] = {g0, g1, g2};
   const int lpn = nrhs / RV;
