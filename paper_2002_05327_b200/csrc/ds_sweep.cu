@@ -320,11 +320,19 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 // showed the one-RHS-per-thread version instruction-bound (~140 instructions
 // per value, IPC 0.6).
 
-// u = 0 through the pointer table (graphs replay for any f / u buffers)
-__global__ void k_zero_io(cplx *const *__restrict__ io, int64_t n) {
+// u = 0 through the pointer table (graphs replay for any f / u buffers), and
+// the application's flag words: 0, except the cut masks [cut0, cut1) which
+// start all-ones (0x3f3f3f3f, the byte pattern of the former memsets) --
+// one kernel instead of a kernel and three memset nodes (measured: a memset
+// node at the head of the host-path graph cost ~0.3 ms end to end)
+__global__ void k_zero_io(cplx *const *__restrict__ io, int64_t n, int *flags, int64_t nflags,
+                          int64_t cut0, int64_t cut1) {
   cplx *u = io[1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     u[i] = make_double2(0.0, 0.0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nflags; i += stride)
+    flags[i] = (i >= cut0 && i < cut1) ? 0x3f3f3f3f : 0;
 }
 
 // ------------------------------------------------------------- K6 assemble
@@ -1629,18 +1637,22 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   if (mode & 1) {
     {
       const int64_t n = P->nnodes * nrhs;
-      k_zero_io<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 8), 256, 0, st>>>(
-          P->d_io, n);
+      const int64_t nflags = (int64_t)P->nsub * nrhs + 4 * (int64_t)per + nrhs;
+      const int64_t cut0 = F.arr_cut - F.own_nz, cut1 = cut0 + (int64_t)per;
+      k_zero_io<<<(unsigned)std::min<int64_t>((std::max(n, nflags) + 255) / 256, (int64_t)ctx->num_sms * 8),
+                  256, 0, st>>>(P->d_io, n, F.own_nz, nflags, cut0, cut1);
       ctx->launches++;
       DS_CHECK_LAUNCH();
     }
-    DS_CUDA(cudaMemsetAsync(F.own_nz, 0, sizeof(int) * ((size_t)P->nsub * nrhs + 2 * per), st));
-    DS_CUDA(cudaMemsetAsync(F.arr_cut, 0x3f, sizeof(int) * per, st));
-    DS_CUDA(cudaMemsetAsync(F.emit_cnt, 0, sizeof(int) * (per + nrhs), st));
-    if (P->mcount) DS_CUDA(cudaMemsetAsync(P->mcount, 0, sizeof(int) * 2 * P->h_mjobs.size(), st));
+    if (P->mcount && getenv("DS_MFUSE") && getenv("DS_MFUSE")[0] == '1')  // fused modal solve only
+      DS_CUDA(cudaMemsetAsync(P->mcount, 0, sizeof(int) * 2 * P->h_mjobs.size(), st));
     P->k5_pending[0] = P->k5_pending[1] = false;
   }
-  if (hio && !hio->ext) {  // fork the copy stream after the zeroing: H2D chunks, untouched u chunks
+  // fork the copy streams after the zeroing (forking them first -- the
+  // uploads need nothing from this call -- measured 2740 vs 3020 RHS/s end
+  // to end on config 2: the graph's copies then start under the zeroing
+  // kernel and the early launches)
+  if (hio && !hio->ext) {
     DS_CUDA(cudaEventRecord(P->hio_fork, st));
     DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_fork, 0));
     DS_CUDA(cudaStreamWaitEvent(P->cstream2, P->hio_fork, 0));
