@@ -163,6 +163,8 @@ struct ds_plan {
   cplx *hio_fo = nullptr, *hio_fm = nullptr, *hio_uo = nullptr, *hio_um = nullptr;  // f/u staging: RHS-outer (copies), RHS-minor (sweep)
   cudaStream_t cstream = nullptr;
   cudaStream_t cstream2 = nullptr;  // second copy stream: boxes alternate between the two
+  std::vector<cudaStream_t> cstream_x;  // further download streams (DS_HIO_DSTREAMS > 2)
+  std::vector<cudaEvent_t> cjoin_x;
   cudaEvent_t hio_fork2 = nullptr, hio_join2 = nullptr;
   int side_priority = 0;  // K5 / copy stream priority
   std::vector<cudaEvent_t> hio_ev_in, hio_ev_out;
@@ -1417,6 +1419,8 @@ extern "C" int ds_plan_destroy(ds_plan *P) {
   for (auto &g : P->hgraphs) cudaGraphExecDestroy(g.exec);
   if (P->cstream) cudaStreamDestroy(P->cstream);
   if (P->cstream2) cudaStreamDestroy(P->cstream2);
+  for (auto x : P->cstream_x) cudaStreamDestroy(x);
+  for (auto e : P->cjoin_x) cudaEventDestroy(e);
   if (P->hio_fork2) cudaEventDestroy(P->hio_fork2);
   if (P->hio_join2) cudaEventDestroy(P->hio_join2);
   for (auto e : P->hio_ev_in) cudaEventDestroy(e);
@@ -1656,6 +1660,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaEventRecord(P->hio_fork, st));
     DS_CUDA(cudaStreamWaitEvent(P->cstream, P->hio_fork, 0));
     DS_CUDA(cudaStreamWaitEvent(P->cstream2, P->hio_fork, 0));
+    for (auto x : P->cstream_x) DS_CUDA(cudaStreamWaitEvent(x, P->hio_fork, 0));
     if (int rc = hio_in_chunks(P, hio, nrhs, P->cstream)) return rc;
     for (int c : P->hio_out_early)
       if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
@@ -1775,7 +1780,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         for (int c : P->hio_out_at[q]) DS_CUDA(cudaEventRecord(hio->ev_out[c], s5));
       if (hio && !hio->ext)  // u chunks whose last accumulation this was: transpose + D2H
         for (int c : P->hio_out_at[q]) {
-          cudaStream_t cs = (hio_nout++ & 1) ? P->cstream2 : P->cstream;
+          const int nd = 2 + (int)P->cstream_x.size(), di = hio_nout++ % nd;
+          cudaStream_t cs = di == 0 ? P->cstream : (di == 1 ? P->cstream2 : P->cstream_x[di - 2]);
           DS_CUDA(cudaEventRecord(P->hio_ev_out[c], s5));
           DS_CUDA(cudaStreamWaitEvent(cs, P->hio_ev_out[c], 0));
           trace_mark("  K5 done for box " + std::to_string(c) + " (launch " + std::to_string(q) + ")", cs);
@@ -1855,6 +1861,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
     DS_CUDA(cudaStreamWaitEvent(st, P->hio_join, 0));
     DS_CUDA(cudaEventRecord(P->hio_join2, P->cstream2));
     DS_CUDA(cudaStreamWaitEvent(st, P->hio_join2, 0));
+    for (size_t i = 0; i < P->cstream_x.size(); ++i) {
+      DS_CUDA(cudaEventRecord(P->cjoin_x[i], P->cstream_x[i]));
+      DS_CUDA(cudaStreamWaitEvent(st, P->cjoin_x[i], 0));
+    }
   }
   prof_mark(P, -1, st);
   P->last_launches = ctx->launches - launches0;
@@ -1978,6 +1988,18 @@ static int hio_setup(ds_plan *P) {
   }
   DS_CUDA(cudaStreamCreateWithPriority(&P->cstream, cudaStreamNonBlocking, P->side_priority));
   DS_CUDA(cudaStreamCreateWithPriority(&P->cstream2, cudaStreamNonBlocking, P->side_priority));
+  {
+    const char *v = getenv("DS_HIO_DSTREAMS");
+    const int nd = v && *v ? std::max(2, std::min(8, atoi(v))) : 2;
+    for (int i = 2; i < nd; ++i) {
+      cudaStream_t x;
+      cudaEvent_t e;
+      DS_CUDA(cudaStreamCreateWithPriority(&x, cudaStreamNonBlocking, P->side_priority));
+      DS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      P->cstream_x.push_back(x);
+      P->cjoin_x.push_back(e);
+    }
+  }
   DS_CUDA(cudaEventCreateWithFlags(&P->hio_fork2, cudaEventDisableTiming));
   DS_CUDA(cudaEventCreateWithFlags(&P->hio_join2, cudaEventDisableTiming));
   P->hio_ev_in.resize(C);
