@@ -637,3 +637,38 @@ def test_fused_modal_solve_opt_in(cuda, cfg1):
     # the fused kernel segments the recurrences differently (4 segments per
     # 32 columns instead of n_b / 8): equal to rounding, not bitwise
     assert rel(outs[1], outs[0]) <= 1e-12
+
+
+def test_transfer_kernel_variants_bitwise(cuda):
+    """The three source-transfer kernels (DS_K4=v1: one block per band,
+    v2: flattened records + tiles, v3: RHS columns per thread, the 2D
+    default) evaluate psi in the same order (v1 / v2 bitwise, v3 to FMA
+    contraction).
+    The switch is read once per process, so each runs in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch\n"
+        "from paper_2002_05327_b200 import FactorizationCache, configs\n"
+        "from paper_2002_05327_b200.ddm import SweepPlan, device_plan\n"
+        "s = configs.spec(1); b = configs.build(s)\n"
+        "rng = np.random.default_rng(8); f = rng.standard_normal((4,) + b['grid'].counts)\n"
+        "fd = torch.from_numpy(f.astype(np.complex128).reshape(4, -1)).cuda()\n"
+        "dp = device_plan(b['partition'], b['ops'], FactorizationCache(), SweepPlan.default(2), 4)\n"
+        "u, _ = dp.apply(fd); np.save(sys.argv[1], u.cpu().numpy())\n") % root
+    outs = []
+    for v in ("v1", "v2", "v3"):
+        path = tempfile.mktemp(suffix=".npy")
+        subprocess.run([sys.executable, "-c", code, path], check=True, timeout=600,
+                       env=dict(os.environ, DS_K4=v))
+        outs.append(np.load(path))
+    # same evaluation order; v3's different code shape lets nvcc contract
+    # the complex multiply-adds into FMAs differently -> equal to rounding
+    assert np.array_equal(outs[0], outs[1])
+    assert rel(outs[2], outs[1]) <= 1e-13
