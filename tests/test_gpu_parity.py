@@ -565,7 +565,7 @@ def test_rhs_groups_bitwise_equal_to_one_plan(cuda, cfg1):
     cache = FactorizationCache()
     dg = device_plan(b["partition"], b["ops"], cache, SweepPlan.default(2), 16, grouped=True)
     d1 = device_plan(b["partition"], b["ops"], cache, SweepPlan.default(2), 16)
-    assert getattr(dg, "groups", 1) == 2 and getattr(d1, "groups", 1) == 1
+    assert getattr(dg, "groups", 1) >= 2 and getattr(d1, "groups", 1) == 1  # 2 by default, DS_RHS_GROUPS overrides
     ug, _ = dg.apply(fd)
     u1, _ = d1.apply(fd)
     assert torch.equal(ug, u1)
