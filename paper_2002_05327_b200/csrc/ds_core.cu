@@ -259,6 +259,91 @@ __global__ void __launch_bounds__(K1_TX * K1_TY) k_apply2d_tiled(OpDev o, const 
   }
 }
 
+// K1 v3 (2D, RHS-outer, the default): column marching.  A thread owns one x
+// of a 128-wide strip and walks K1C_YS rows down it with the rows above /
+// below in registers; x neighbours come from the adjacent lanes by shuffle
+// (lanes 0 and 31 load the one node across the warp edge).  All K1C_YS + 2
+// row loads are independent and issued up front -- no shared memory, no
+// barriers, 1 + 2/K1C_YS row reads per output.  Accumulation order as
+// k_apply (pml.py:144-158), neighbours outside the region contribute nothing.
+#define K1C_X 128
+__device__ __forceinline__ cplx shfl_cplx(cplx v, int delta, bool up) {
+  cplx r;
+  r.x = up ? __shfl_up_sync(0xffffffffu, v.x, delta) : __shfl_down_sync(0xffffffffu, v.x, delta);
+  r.y = up ? __shfl_up_sync(0xffffffffu, v.y, delta) : __shfl_down_sync(0xffffffffu, v.y, delta);
+  return r;
+}
+template <int K1C_YS>
+__global__ void __launch_bounds__(K1C_X) k_apply2d_cols(OpDev o, const cplx *__restrict__ v,
+                                                       cplx *__restrict__ out, int rlo0, int rlo1, int rs0,
+                                                       int rs1) {
+  const int64_t plane = (int64_t)rs0 * rs1;
+  const cplx *__restrict__ vb = v + (int64_t)blockIdx.z * plane;
+  cplx *__restrict__ ob = out + (int64_t)blockIdx.z * plane;
+  const int x = blockIdx.x * K1C_X + threadIdx.x, y0 = blockIdx.y * K1C_YS;
+  const int lane = threadIdx.x & 31;
+  const bool xin = x < rs1;
+  const int xc = min(x, rs1 - 1);
+  const cplx zero = make_double2(0.0, 0.0);
+  // rows y0-1 .. y0+K1C_YS of my column (zero outside the region)
+  cplx col[K1C_YS + 2], edge[K1C_YS];
+#pragma unroll
+  for (int i = 0; i < K1C_YS + 2; ++i) {
+    const int y = y0 - 1 + i;
+    col[i] = (xin && y >= 0 && y < rs0) ? vb[(int64_t)y * rs1 + x] : zero;
+  }
+  // across the warp edge: lane 0 needs x-1, lane 31 needs x+1
+  const int xe = lane == 0 ? x - 1 : x + 1;
+  const bool edge_lane = (lane == 0 || lane == 31) && xe >= 0 && xe < rs1;
+#pragma unroll
+  for (int i = 0; i < K1C_YS; ++i) {
+    const int y = y0 + i;
+    edge[i] = (edge_lane && y < rs0) ? vb[(int64_t)y * rs1 + xe] : zero;
+  }
+  const int c1 = xc + rlo1;
+  const cplx lo1 = o.c_lo[1][c1], hi1 = o.c_hi[1][c1];
+  const cplx m1 = make_double2(-(lo1.x + hi1.x), -(lo1.y + hi1.y));
+#pragma unroll
+  for (int i = 0; i < K1C_YS; ++i) {
+    const int y = y0 + i;
+    const cplx vc = col[i + 1];
+    cplx left = shfl_cplx(vc, 1, true), right = shfl_cplx(vc, 1, false);
+    if (lane == 0) left = edge[i];
+    if (lane == 31) right = edge[i];
+    if (!xin || y >= rs0) continue;
+    const int c0 = y + rlo0;
+    double k2;
+    if (o.kappa2_kind == 0) k2 = o.kappa2[0];
+    else if (o.kappa2_kind == 1) k2 = o.kappa2[o.kappa2_axis == 0 ? c0 : c1];
+    else k2 = o.kappa2[(int64_t)c0 * o.shape[1] + c1];
+    const cplx lo0 = o.c_lo[0][c0], hi0 = o.c_hi[0][c0];
+    const cplx m0 = make_double2(-(lo0.x + hi0.x), -(lo0.y + hi0.y));
+    cplx acc = cscale(vc, k2);
+    acc = cadd(acc, cmul(m0, vc));
+    if (y > 0) acc = cadd(acc, cmul(lo0, col[i]));
+    if (y < rs0 - 1) acc = cadd(acc, cmul(hi0, col[i + 2]));
+    acc = cadd(acc, cmul(m1, vc));
+    if (x > 0) acc = cadd(acc, cmul(lo1, left));
+    if (x < rs1 - 1) acc = cadd(acc, cmul(hi1, right));
+    ob[(int64_t)y * rs1 + x] = acc;
+  }
+}
+
+// DS_K1=tiled: the 32 x 8 shared-memory tile (K1 v2); c2 / c4 / c8 / c16:
+// rows per thread of the column-marching kernel (default 4: config 3 K1
+// 0.287 ms = 74.5% of HBM vs c8 61.8%, c16 36.5%, tiled 54.6%)
+static int k1_variant() {
+  static const int v = [] {
+    const char *e = getenv("DS_K1");
+    if (e && *e == 't') return 2;
+    if (e && !strcmp(e, "c16")) return 16;
+    if (e && !strcmp(e, "c8")) return 8;
+    if (e && !strcmp(e, "c2")) return 2;
+    return 4;
+  }();
+  return v;
+}
+
 static int grid_for(ds_ctx *ctx, int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
   int64_t cap = (int64_t)ctx->num_sms * 16;
@@ -282,7 +367,22 @@ extern "C" int ds_op_apply(ds_ctx *ctx, const ds_op *op, const ds_cplx *v, ds_cp
   const int64_t nodes = (int64_t)sh[0] * sh[1] * sh[2];
   if (nodes * (layout != 0 ? 1 : nrhs) >= (int64_t)1 << 31 || nrhs > 65535)
     return ds_fail(DS_ECONFIG, "ds_op_apply: region too large for one launch");
-  if (layout != 0 && o.dim == 2 && nrhs <= 65535) {
+  if (layout != 0 && o.dim == 2 && nrhs <= 65535 && k1_variant() != 2) {
+    const int ys = k1_variant();
+    const dim3 grid((sh[1] + K1C_X - 1) / K1C_X, (sh[0] + ys - 1) / ys, nrhs);
+    if (ys == 16)
+      k_apply2d_cols<16><<<grid, K1C_X, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
+                                                         sh[0], sh[1]);
+    else if (ys == 8)
+      k_apply2d_cols<8><<<grid, K1C_X, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
+                                                        sh[0], sh[1]);
+    else if (ys == 2)
+      k_apply2d_cols<2><<<grid, K1C_X, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
+                                                        sh[0], sh[1]);
+    else
+      k_apply2d_cols<4><<<grid, K1C_X, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
+                                                        sh[0], sh[1]);
+  } else if (layout != 0 && o.dim == 2 && nrhs <= 65535) {
     const dim3 grid((sh[1] + K1_TX - 1) / K1_TX, (sh[0] + K1_TY - 1) / K1_TY, (nrhs + K1_RPB - 1) / K1_RPB);
     k_apply2d_tiled<<<grid, K1_TX * K1_TY, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
                                                              sh[0], sh[1], nrhs);
