@@ -554,6 +554,39 @@ __global__ void k_combine(int64_t n, int nrhs, int nvec, CombineArgs args,
   }
 }
 
+// two elements per thread (i, i + stride): twice the independent loads in
+// flight per thread, same per-element summation order as k_combine
+__global__ void k_combine2(int64_t n, int nrhs, int nvec, CombineArgs args,
+                           const cplx *__restrict__ c, cplx *y) {
+  const int r = blockIdx.y;
+  const int64_t base = (int64_t)r * n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += 2 * stride) {
+    const int64_t i2 = i + stride;
+    const bool two = i2 < n;
+    cplx acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    const cplx yv = y[base + i];
+    const cplx yv2 = two ? y[base + i2] : make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int j = 0; j < nvec; ++j) {
+      const cplx cj = __ldg(c + j * nrhs + r);
+      const cplx *xj = args.x[j] + base;
+      acc = cadd(acc, cmul(cj, xj[i]));
+      if (two) acc2 = cadd(acc2, cmul(cj, xj[i2]));
+    }
+    y[base + i] = cadd(yv, acc);
+    if (two) y[base + i2] = cadd(yv2, acc2);
+  }
+}
+
+static bool combine2_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("DS_COMBINE");
+    return !(e && *e == '1');
+  }();
+  return on;
+}
+
 extern "C" int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec,
                               const ds_cplx *const *xs, const ds_cplx *c, ds_cplx *y) {
   if (!ctx || nrhs < 1 || nrhs > 65535 || nvec < 0 || nvec > MAX_COMBINE)
@@ -561,8 +594,12 @@ extern "C" int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec
   if (nvec == 0) return DS_OK;
   CombineArgs args;
   for (int j = 0; j < nvec; ++j) args.x[j] = (const cplx *)xs[j];
-  k_combine<<<vec_grid(ctx, n, nrhs), 256, 0, ctx->stream>>>(n, nrhs, nvec, args,
-                                                             (const cplx *)c, (cplx *)y);
+  if (combine2_enabled())
+    k_combine2<<<vec_grid(ctx, (n + 1) / 2, nrhs), 256, 0, ctx->stream>>>(n, nrhs, nvec, args,
+                                                                        (const cplx *)c, (cplx *)y);
+  else
+    k_combine<<<vec_grid(ctx, n, nrhs), 256, 0, ctx->stream>>>(n, nrhs, nvec, args,
+                                                               (const cplx *)c, (cplx *)y);
   ctx->launches++;
   DS_CHECK_LAUNCH();
   return DS_OK;
