@@ -260,21 +260,26 @@ __global__ void __launch_bounds__(K1_TX * K1_TY) k_apply2d_tiled(OpDev o, const 
 }
 
 // K1 v3 (2D, RHS-outer, the default): column marching.  A thread owns one x
-// of a 128-wide strip and walks K1C_YS rows down it with the rows above /
+// of a K1C_X-wide strip and walks K1C_YS rows down it with the rows above /
 // below in registers; x neighbours come from the adjacent lanes by shuffle
 // (lanes 0 and 31 load the one node across the warp edge).  All K1C_YS + 2
 // row loads are independent and issued up front -- no shared memory, no
 // barriers, 1 + 2/K1C_YS row reads per output.  Accumulation order as
 // k_apply (pml.py:144-158), neighbours outside the region contribute nothing.
-#define K1C_X 128
+#ifndef K1C_X
+#define K1C_X 64  // strip width: config 3's 441-wide regions fill 7 x 64 = 448 lanes (128: 512)
+#endif
 __device__ __forceinline__ cplx shfl_cplx(cplx v, int delta, bool up) {
   cplx r;
   r.x = up ? __shfl_up_sync(0xffffffffu, v.x, delta) : __shfl_down_sync(0xffffffffu, v.x, delta);
   r.y = up ? __shfl_up_sync(0xffffffffu, v.y, delta) : __shfl_down_sync(0xffffffffu, v.y, delta);
   return r;
 }
+#ifndef K1C_MINB
+#define K1C_MINB (7 * 128 / K1C_X)  // rows <= 4: 72 registers, 28 warps per SM: config 3 K1 0.327 -> 0.272 ms at 128 wide (8 x 128 spills), 0.263 ms at 64 wide
+#endif
 template <int K1C_YS>
-__global__ void __launch_bounds__(K1C_X) k_apply2d_cols(OpDev o, const cplx *__restrict__ v,
+__global__ void __launch_bounds__(K1C_X, K1C_YS <= 4 ? K1C_MINB : 1) k_apply2d_cols(OpDev o, const cplx *__restrict__ v,
                                                        cplx *__restrict__ out, int rlo0, int rlo1, int rs0,
                                                        int rs1) {
   const int64_t plane = (int64_t)rs0 * rs1;
