@@ -233,8 +233,8 @@ def run_ours(args, rank, world, local_rank):
     part, ops = b["partition"], b["ops"]
     # 3D constant media: share factorizations across translation classes
     # (config 4: 27 classes, 76 GB instead of 203 GB)
-    share = part.dim == 3 and s.medium == "constant" and os.environ.get("DS_FACTOR") == "block-lu"
-    cache = FactorizationCache(share_translates=share)
+    share = part.dim == 3 and s.medium == "constant" and args.factor == "block-lu"
+    cache = FactorizationCache(method=args.factor, share_translates=share)
 
     # ---- factorization (timed separately, amortised)
     torch.cuda.synchronize()
@@ -597,6 +597,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="2")
+    ap.add_argument("--factor", default="auto", choices=["auto", "block-lu"],
+                    help="factorization method ('block-lu': the block LU for every operator)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rhs", type=int, default=3)

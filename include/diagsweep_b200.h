@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 4
+#define DS_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -301,6 +301,19 @@ DS_API int32_t ds_plan_nlaunch(const ds_plan *plan);
  * u of the sweep is the sum over ranks of their u. */
 DS_API int ds_ddm_apply_range(ds_ctx *ctx, ds_plan *plan, const ds_cplx *f_dev, ds_cplx *u_dev,
                               int32_t nrhs, int32_t l0, int32_t l1, int32_t mode);
+
+/* Inspection (ABI 5; used by the per-step parity tests of psi and
+ * _accumulate): the payload slot that queues sources of direction `dir`
+ * (index into `directions`) for visit (use_sweep 1-based, target subdomain).
+ * lo / shape receive its band (grid coordinates); when out_dev is non-NULL
+ * its contents, [band nodes, C-order][nrhs] as left by the last call with
+ * that nrhs, are copied there (out_elems >= band nodes * nrhs; async on the
+ * context stream).  Between the producing transfer and the consuming
+ * assembly a slot holds the sum of the payloads queued for it
+ * (transfer.py:100-155, ddm.py:276).  < 0 if no routing fills that slot. */
+DS_API int ds_plan_slot(ds_ctx *ctx, const ds_plan *plan, int32_t use_sweep, int32_t target,
+                        int32_t dir, int32_t *lo, int32_t *shape, ds_cplx *out_dev,
+                        int64_t out_elems, int32_t nrhs);
 
 /* ---------------------------------------------------------- vector kernels
  * Batched complex vector ops for GMRES (krylov.py:80, :97-106, :139-142);

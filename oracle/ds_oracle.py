@@ -482,8 +482,15 @@ def psi(prob, ops, idx, direction, v, rhs):  # transfer.py:100-155
     return nb, (tuple(lo), tuple(hi)), payload
 
 
-def ddm_apply(prob: Problem, ops, cache: Cache, f, directions=None, record=False):
-    """diagonal_sweep_solve restated (ddm.py:212-291) for one RHS."""
+def ddm_apply(prob: Problem, ops, cache: Cache, f, directions=None, record=False,
+              snapshot_at=()):
+    """diagonal_sweep_solve restated (ddm.py:212-291) for one RHS.
+
+    snapshot_at: (sweep, step) pairs (test hook); right after each such
+    anti-diagonal step rep["snapshots"][(sweep, step)] = (u copy, pending),
+    pending = {(use sweep, target, direction): (band lo, band hi, summed
+    payload)} -- the state a per-step GPU check compares (the partial sum of
+    _accumulate and the queued psi payloads)."""
     t0 = time.perf_counter()
     dim = prob.dim
     directions = directions or (DEFAULT_2D if dim == 2 else DEFAULT_3D)
@@ -511,7 +518,7 @@ def ddm_apply(prob: Problem, ops, cache: Cache, f, directions=None, record=False
                     has_own = bool(np.any(vals))
                     rhs[_sl(olo, ohi, wlo)] += vals
                 consumed = 0
-                for (blo, bhi, vals, cuts) in queues.pop((sweep, idx), []):
+                for (blo, bhi, vals, cuts, _dv) in queues.pop((sweep, idx), []):
                     rhs[_sl(blo, bhi, wlo)] += vals
                     arrivals.append(cuts)
                     consumed += 1
@@ -535,13 +542,23 @@ def ddm_apply(prob: Problem, ops, cache: Cache, f, directions=None, record=False
                             rep["discarded_sources"] += 1
                         else:
                             queues.setdefault((use, target), []).append(
-                                (blo, bhi, payload, content_cuts(dvec, cuts)))
+                                (blo, bhi, payload, content_cuts(dvec, cuts), dvec))
                             emitted += 1
                 rep["solves"] += 1
                 if record:
                     rep["events"].append({"sweep": sweep, "step": step, "subdomain": list(idx),
                                           "sources_consumed": consumed,
                                           "sources_emitted": emitted, "nonzero": nonzero})
+            if (sweep, step) in snapshot_at:
+                pending = {}
+                for (use, target), entries in queues.items():
+                    for (blo, bhi, vals, _c, dv) in entries:
+                        key = (use, target, dv)
+                        if key in pending:
+                            pending[key] = (blo, bhi, pending[key][2] + vals)
+                        else:
+                            pending[key] = (blo, bhi, vals.copy())
+                rep.setdefault("snapshots", {})[(sweep, step)] = (u.copy(), pending)
     assert not queues
     rep["wall_time"] = time.perf_counter() - t0
     return u, rep

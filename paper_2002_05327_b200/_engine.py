@@ -111,37 +111,78 @@ def from_device_batch(t, kind, batched):
 KINDS = {"const": 0, "axis": 1, "full": 2}
 
 
+def op_couplings(op):
+    """(c_lo, c_hi) per axis through the reference's public surface
+    (`DiscreteOperator.axis_coefficients`, pml.py:95-102); our own operator
+    class caches them as `.couplings`."""
+    cp = getattr(op, "couplings", None)
+    if cp is not None:
+        return cp
+    return [op.axis_coefficients(a) for a in range(op.grid.dim)]
+
+
+def op_kappa2(op):
+    """(kind code, axis, flat float64 array) of kappa^2 from the reference's
+    `kappa2_kind` / `kappa2` fields ('const' float, 'axis' (axis, values),
+    'full' ndarray; pml.py:75-84)."""
+    kind = op.kappa2_kind
+    if kind == "const":
+        return KINDS[kind], -1, np.array([float(op.kappa2)])
+    if kind == "axis":
+        axis, values = op.kappa2
+        return KINDS[kind], int(axis), np.ascontiguousarray(values, dtype=np.float64)
+    return KINDS[kind], -1, np.ascontiguousarray(op.kappa2, dtype=np.float64).ravel()
+
+
 class DeviceOperator:
-    """Device copy of one DiscreteOperator's couplings and kappa^2."""
+    """Device copy of one DiscreteOperator's couplings and kappa^2.  Reads
+    only the reference's public operator surface (window, grid,
+    axis_coefficients, kappa2_kind, kappa2), so the reference's own
+    `DiscreteOperator` objects work too."""
 
     def __init__(self, op):
         lib, ctx = context()
         keep = []
         desc = N.OpDesc()
-        desc.dim = op.dim
-        for a in range(op.dim):
-            lo, hi = op.couplings[a]
+        dim = op.grid.dim
+        desc.dim = dim
+        for a, (lo, hi) in enumerate(op_couplings(op)):
             lo = np.ascontiguousarray(lo, dtype=np.complex128)
             hi = np.ascontiguousarray(hi, dtype=np.complex128)
             keep += [lo, hi]
             desc.shape[a] = op.window.shape[a]
             desc.c_lo[a] = lo.ctypes.data
             desc.c_hi[a] = hi.ctypes.data
-        k2 = op.kappa2_array()
+        kind, axis, k2 = op_kappa2(op)
         keep.append(k2)
-        desc.kappa2_kind = KINDS[op.kappa2_kind]
-        desc.kappa2_axis = op.kappa2_axis if op.kappa2_kind == "axis" else -1
+        desc.kappa2_kind = kind
+        desc.kappa2_axis = axis
         desc.kappa2 = k2.ctypes.data
         out = C.c_void_p()
         N.check(lib.ds_op_create(ctx, C.byref(desc), C.byref(out)), "ds_op_create")
         self.handle = out
+        self.shape = tuple(op.window.shape)
         self._finalizer = weakref.finalize(self, lib.ds_op_destroy, out)
 
 
+# device operators of foreign (reference) operator objects, content-keyed by
+# fingerprint + shape (the reference's dataclass is unhashable and has no
+# slot for a device handle); entries live as long as a factorization or plan
+# holds the DeviceOperator
+_FOREIGN_DEVOPS: "weakref.WeakValueDictionary" = weakref.WeakValueDictionary()
+
+
 def device_operator(op) -> DeviceOperator:
-    if op._device is None:
-        op._device = DeviceOperator(op)
-    return op._device
+    if hasattr(op, "_device"):
+        if op._device is None:
+            op._device = DeviceOperator(op)
+        return op._device
+    key = (op.fingerprint, tuple(op.window.shape), torch.cuda.current_device())
+    dop = _FOREIGN_DEVOPS.get(key)
+    if dop is None:
+        dop = DeviceOperator(op)
+        _FOREIGN_DEVOPS[key] = dop
+    return dop
 
 
 def apply_operator(op, v, region):
@@ -169,7 +210,7 @@ def axis_tridiagonal(op, axis: int) -> np.ndarray:
     """Dense 1D operator of `axis` (pml.py couplings; kappa^2 folded in
     when it varies along this axis) -- the factor the reference's
     SeparableFactorization triangularizes (subdomain.py:52-63)."""
-    lo, hi = op.couplings[axis]
+    lo, hi = op_couplings(op)[axis]
     n = len(lo)
     T = np.zeros((n, n), dtype=np.complex128)
     i = np.arange(n)
@@ -185,16 +226,26 @@ _EIG_CACHE: dict = {}
 
 
 def _axis_eig(T: np.ndarray):
-    """(V, V^{-1}, lambda) of one 1D matrix, memoised on its bytes (windows
-    of a partition share most of their per-axis operators)."""
+    """(V, V^{-1}, lambda, quality) of one 1D matrix, memoised on its bytes
+    (windows of a partition share most of their per-axis operators).
+    quality = (cond_2(V), ||T V - V diag(lambda)||_F / (||T||_F ||V||_F),
+    ||V^{-1} V - I||_F): the numbers the modal factorization's guard checks."""
     key = T.tobytes()
     hit = _EIG_CACHE.get(key)
     if hit is None:
         lam, V = np.linalg.eig(T)
         W = np.linalg.inv(V)
+        sv = np.linalg.svd(V, compute_uv=False)
+        cond = float(sv[0] / sv[-1]) if sv[-1] > 0 else math.inf
+        nT, nV = np.linalg.norm(T), np.linalg.norm(V)
+        res = float(np.linalg.norm(T @ V - V * lam) / (nT * nV)) if nT and nV else math.inf
+        inv_err = float(np.linalg.norm(W @ V - np.eye(len(lam))))
+        if not np.all(np.isfinite(W)):
+            cond = inv_err = math.inf
         hit = (np.ascontiguousarray(V, dtype=np.complex128),
                np.ascontiguousarray(W, dtype=np.complex128),
-               np.ascontiguousarray(lam, dtype=np.complex128))
+               np.ascontiguousarray(lam, dtype=np.complex128),
+               (cond, res, inv_err))
         if len(_EIG_CACHE) > 4096:
             _EIG_CACHE.clear()
         _EIG_CACHE[key] = hit
@@ -204,9 +255,37 @@ def _axis_eig(T: np.ndarray):
 def modal_decomposition(op):
     """Eigen-decompositions T_a = V diag(lambda) V^{-1} of the in-slab axes
     (LAPACK zgeev through NumPy; n_a <= a few hundred, O(n_a^3) each).
-    Returns (block_axis, [(V, V^{-1}, lambda), ...]) in in-slab axis order."""
+    Returns (block_axis, [(V, V^{-1}, lambda, quality), ...]) in in-slab axis
+    order."""
     ba = block_axis_of(op.window.shape)
     return ba, [_axis_eig(axis_tridiagonal(op, a)) for a in range(op.dim) if a != ba]
+
+
+# Guard of the modal factorization.  The eigenbasis V_a is not unitary (the
+# reference's Schur basis is), so the mode-wise solve loses about
+# log10(cond(V_a)) digits: configs 1/2/4 have cond(V) = 3e3 / 2e4 / 60 and
+# solve to <= 1.2e-12 of the Schur/Sylvester oracle.  Above these limits the
+# operator is factored by the block LU instead (same kernels as raster media).
+MODAL_COND_MAX = 1e6
+MODAL_RESIDUAL_MAX = 1e-12
+MODAL_INVERSE_MAX = 1e-9
+
+
+def modal_guard(op, cond_max: float = MODAL_COND_MAX):
+    """(ok, reason, decomposition): whether the modal factorization of `op`
+    is well conditioned enough to keep the 1e-10 parity bar.  cond_max =
+    inf disables the guard (measurements of the unguarded modal path)."""
+    ba, axes = modal_decomposition(op)
+    if cond_max == math.inf:
+        return True, "", (ba, axes)
+    for a, (_, _, _, (cond, res, inv_err)) in enumerate(axes):
+        if not cond <= cond_max:
+            return False, f"in-slab axis {a}: cond(V) {cond:.3g} > {cond_max:.3g}", (ba, axes)
+        if not res <= MODAL_RESIDUAL_MAX:
+            return False, f"in-slab axis {a}: eigen-residual {res:.3g}", (ba, axes)
+        if not inv_err <= MODAL_INVERSE_MAX:
+            return False, f"in-slab axis {a}: ||V^-1 V - I|| {inv_err:.3g}", (ba, axes)
+    return True, "", (ba, axes)
 
 
 class FactorSet:
@@ -214,20 +293,20 @@ class FactorSet:
     block-tridiagonal LU (K2, any operator) or, with `modal`, the modal
     factorization of separable operators (K2m, ds_modal.cu)."""
 
-    def __init__(self, ops, modal: bool = False):
+    def __init__(self, ops, modal: bool = False, decomps=None):
         lib, ctx = context()
-        handles = [device_operator(op).handle for op in ops]
-        arr = (C.c_void_p * len(ops))(*[h.value for h in handles])
+        dops = [device_operator(op) for op in ops]
+        arr = (C.c_void_p * len(ops))(*[d.handle.value for d in dops])
         out = C.c_void_p()
         self.modal = modal
         if modal:
             descs = (N.ModalDesc * len(ops))()
             keep = []
             for i, op in enumerate(ops):
-                ba, axes = modal_decomposition(op)
+                ba, axes = decomps[i] if decomps is not None else modal_decomposition(op)
                 descs[i].block_axis = ba
                 descs[i].naxes = len(axes)
-                for a, (V, W, lam) in enumerate(axes):
+                for a, (V, W, lam, _q) in enumerate(axes):
                     keep += [V, W, lam]
                     descs[i].v[a] = V.ctypes.data
                     descs[i].vinv[a] = W.ctypes.data
@@ -239,7 +318,7 @@ class FactorSet:
             N.check(lib.ds_fact_create(ctx, arr, len(ops), C.byref(out)), "ds_fact_create")
         self.handle = out
         self.n = len(ops)
-        self._ops = list(ops)  # operators must outlive the factors
+        self._dops = dops  # device operators must outlive the factors
         self._finalizer = weakref.finalize(self, lib.ds_fact_destroy, out)
 
     def info(self, i):
@@ -251,11 +330,11 @@ class FactorSet:
         return ba.value, nb.value, m.value, nbytes.value
 
 
-def fact_solve(fset: FactorSet, index: int, op, rhs):
+def fact_solve(fset: FactorSet, index: int, shape, rhs):
     lib, ctx = context()
-    t, kind, batched = to_device_batch(rhs, op.window.shape)
+    t, kind, batched = to_device_batch(rhs, shape)
     R = t.shape[0]
-    W = op.window.size
+    W = int(np.prod(shape))
     tmin = torch.empty((W, R), dtype=torch.complex128, device=t.device)
     N.check(lib.ds_layout_to_minor(ctx, W, R, t.data_ptr(), tmin.data_ptr()))
     xmin = torch.empty_like(tmin)
@@ -510,7 +589,9 @@ class DevicePlan:
             xfac=np.concatenate(xfac_vals) if xfac_vals else np.zeros(1),
             xfac_off=np.asarray(xfac_off, np.int64),
         )
-        op_handles = (C.c_void_p * nsub)(*[device_operator(op).handle.value for op in ops])
+        dops = [device_operator(op) for op in ops]
+        self._keep.append(dops)
+        op_handles = (C.c_void_p * nsub)(*[d.handle.value for d in dops])
         fact_handles = (C.c_void_p * nsub)(*[f.fset.handle.value if f is not None else None
                                              for f in facts])
         desc = N.PlanDesc()
@@ -573,6 +654,21 @@ class DevicePlan:
         sa = (C.c_void_p * n)(*slot_bases)
         fa = (C.c_void_p * n)(*flag_bases)
         N.check(lib.ds_plan_set_peers(ctx, self.handle, n, sa, fa), "ds_plan_set_peers")
+
+    def slot(self, use_sweep: int, target: int, k: int, nrhs: int):
+        """Band (lo, shape) and contents [*shape, nrhs] (CUDA tensor) of the
+        payload slot for direction k queued for visit (use_sweep 1-based,
+        target); None if no routing fills it (ds_plan_slot)."""
+        lib, ctx = context()
+        lo = (C.c_int32 * 3)()
+        sh = (C.c_int32 * 3)()
+        if lib.ds_plan_slot(ctx, self.handle, use_sweep, target, k, lo, sh, None, 0, nrhs) != 0:
+            return None
+        shape = tuple(sh[:self.dim])
+        out = torch.empty(shape + (nrhs,), dtype=torch.complex128, device="cuda")
+        N.check(lib.ds_plan_slot(ctx, self.handle, use_sweep, target, k, lo, sh, out.data_ptr(),
+                                 out.numel(), nrhs), "ds_plan_slot")
+        return tuple(lo[:self.dim]), shape, out
 
     def nlaunch(self) -> int:
         return int(N.load_library().ds_plan_nlaunch(self.handle))
@@ -711,6 +807,7 @@ class GroupedPlan:
                 p.apply(f[r0:r1], out=u[r0:r1])  # each group writes its rows in place
         for st in self._streams[:len(bounds)]:
             main.wait_stream(st)
+        context()  # leave the shared native context on the caller's stream
         self._split = bounds
         return u, None
 

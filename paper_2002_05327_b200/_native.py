@@ -110,6 +110,7 @@ _SIGNATURES = [
     ("ds_plan_shard_info", C.c_int, [vp, C.POINTER(vp), P_i64, C.POINTER(vp), P_i64]),
     ("ds_plan_set_peers", C.c_int, [vp, vp, i32, C.POINTER(vp), C.POINTER(vp)]),
     ("ds_plan_nlaunch", i32, [vp]),
+    ("ds_plan_slot", C.c_int, [vp, vp, i32, i32, i32, P_i32, P_i32, vp, i64, i32]),
     ("ds_ddm_apply_range", C.c_int, [vp, vp, vp, vp, i32, i32, i32, i32]),
     ("ds_plan_set_profiling", C.c_int, [vp, i32]),
     ("ds_plan_kernel_times", C.c_int, [vp, P_f64, P_i64, i32]),
@@ -122,6 +123,8 @@ _SIGNATURES = [
     ("ds_layout_to_minor", C.c_int, [vp, i64, i32, vp, vp]),
     ("ds_layout_to_outer", C.c_int, [vp, i64, i32, vp, vp]),
 ]
+
+ABI_VERSION = 5
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]
 
@@ -145,7 +148,7 @@ def load_library(path: Path | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.ds_abi_version() != 4:
+        if lib.ds_abi_version() != ABI_VERSION:
             raise SolverError("diagsweep_b200 ABI version mismatch")
         if path is None:
             _lib = lib

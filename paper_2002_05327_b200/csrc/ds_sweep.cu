@@ -101,6 +101,7 @@ struct ds_plan {
   std::vector<ModalJob> h_mjobs;
   std::vector<FactDev> h_mfacts;
   std::vector<int> mod_vidx, mod_off;
+  ModalWs mws{nullptr, nullptr, 0, 0};  // stream-K workspace of the modal transforms
   // staged (large-slab) solve: host factor layouts and couplings per subdomain
   bool staged = false;
   std::vector<FactDev> h_facts;
@@ -126,6 +127,7 @@ struct ds_plan {
   std::vector<size_t> xfer_slot_off;  // element offset of each transfer's slot
   cplx *slot_base = nullptr;
   size_t slot_bytes = 0;
+  std::map<std::tuple<int, int, int>, SlotRef> slot_by_key;  // (use-1, target, dir) -> slot (ds_plan_slot)
   int **d_flag_bases = nullptr;  // [nranks] flag words of every rank (device table)
   bool k5_pending[2] = {false, false};
   // graph
@@ -1205,6 +1207,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cudaMemset(slotmem, 0, sizeof(cplx) * std::max<size_t>(slot_elems, 1));
   P->slot_bufs.push_back({slotmem, sizeof(cplx) * std::max<size_t>(slot_elems, 1)});
   for (size_t i = 0; i < hslots.size(); ++i) hslots[i].data = slotmem + slot_off[i];
+  for (const auto &kv : slot_id) P->slot_by_key[kv.first] = hslots[kv.second];
   P->slot_base = slotmem;
   P->slot_bytes = sizeof(cplx) * std::max<size_t>(slot_elems, 1);
   // slot table ordered per visit (contiguous ranges)
@@ -1356,6 +1359,28 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (!P->h_mjobs.empty()) {
     if (plan_alloc(P, &mem, sizeof(int) * 2 * P->h_mjobs.size())) return fail(DS_ECUDA);
     P->mcount = (int *)mem;
+    // stream-K workspace: sized for the launch with the most tiles
+    int ctas = 0, tiles = 0;
+    size_t part = 0;
+    for (size_t q = 0; q + 1 < P->mod_off.size(); ++q) {
+      const int m0 = P->mod_off[q], nmo = P->mod_off[q + 1] - m0;
+      if (nmo <= 0) continue;
+      int c1, t1;
+      size_t d1;
+      ds_modal_ws_size(ctx, P->h_mfacts.data() + m0, nmo, d->nrhs_max, &c1, &d1, &t1);
+      ctas = c1;
+      part = d1;
+      tiles = std::max(tiles, t1);
+    }
+    if (ctas > 0) {
+      if (plan_alloc(P, &mem, sizeof(double) * part)) return fail(DS_ECUDA);
+      P->mws.part = (double *)mem;
+      if (plan_alloc(P, &mem, sizeof(int) * std::max(tiles, 1))) return fail(DS_ECUDA);
+      P->mws.cnt = (int *)mem;
+      cudaMemset(P->mws.cnt, 0, sizeof(int) * std::max(tiles, 1));
+      P->mws.ctas = ctas;
+      P->mws.tiles = tiles;
+    }
   }
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
@@ -1559,6 +1584,16 @@ static int patch_tables(ds_plan *P, int nrhs) {
   return DS_OK;
 }
 
+// stream-K modal transforms (default; DS_MODAL_SK=0 restores the
+// one-tile-per-CTA grid for A/B measurements)
+static bool modal_sk() {
+  static const bool on = [] {
+    const char *v = getenv("DS_MODAL_SK");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 static int blocks_for(ds_ctx *ctx, int64_t work, int per_visit_cap) {
   int64_t b = (work + 255) / 256;
   if (b > per_visit_cap) b = per_visit_cap;
@@ -1750,7 +1785,8 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         for (int ph = 0; ph < 3 && !rc; ++ph) {
           if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
           if (skip_cls & (ph == 1 ? 4 : 2)) continue;
-          rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph);
+          rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph,
+                                     modal_sk() ? &P->mws : nullptr);
         }
       }
       if (rc) return rc;
@@ -2266,6 +2302,26 @@ extern "C" int ds_plan_set_peers(ds_ctx *ctx, ds_plan *P, int32_t nranks, void *
   }
   DS_CUDA(cudaMemcpy(P->d_flag_bases, flag_bases, sizeof(int *) * nranks, cudaMemcpyHostToDevice));
   P->peers_set = true;
+  return DS_OK;
+}
+
+extern "C" int ds_plan_slot(ds_ctx *ctx, const ds_plan *P, int32_t use_sweep, int32_t target,
+                            int32_t dir, int32_t *lo, int32_t *shape, ds_cplx *out_dev,
+                            int64_t out_elems, int32_t nrhs) {
+  if (!ctx || !P || !lo || !shape) return ds_fail(DS_ECONFIG, "ds_plan_slot: null argument");
+  auto it = P->slot_by_key.find(std::make_tuple(use_sweep - 1, target, dir));
+  if (it == P->slot_by_key.end()) return ds_fail(DS_ECONFIG, "ds_plan_slot: no such payload slot");
+  int64_t n = 1;
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = it->second.lo[a];
+    shape[a] = it->second.shape[a];
+    n *= shape[a];
+  }
+  if (!out_dev) return DS_OK;
+  if (nrhs < 1 || nrhs > P->nrhs_max || out_elems < n * nrhs)
+    return ds_fail(DS_ECONFIG, "ds_plan_slot: output buffer too small or bad nrhs");
+  DS_CUDA(cudaMemcpyAsync(out_dev, it->second.data, sizeof(cplx) * n * nrhs,
+                          cudaMemcpyDeviceToDevice, ctx->stream));
   return DS_OK;
 }
 

@@ -29,6 +29,8 @@ def solve_sharded(f, solve_fn, group=None):
     rank = dist.get_rank(group)
     R = f.shape[0]
     lo, hi = rhs_shard(R, rank, world)
+    # an empty shard (R < world) still joins the all_gather below; solve_fn
+    # must accept a [0, ...] batch (diagonal_sweep_solve returns an empty field)
     out = solve_fn(f[lo:hi])
     width = max(rhs_shard(R, r, world)[1] - rhs_shard(R, r, world)[0] for r in range(world))
     pad = torch.zeros((width,) + tuple(out.shape[1:]), dtype=out.dtype, device=out.device)

@@ -54,37 +54,57 @@ class SolveReport:
 
 
 class _Vec:
-    """Native batched vector ops on RHS-outer [R, n] complex128 tensors."""
+    """Native batched vector ops on RHS-outer [R, n] complex128 tensors.
+    Every op re-binds the context to torch's current stream first: a
+    preconditioner closure may have left the shared context on a side
+    stream (RHS-group plans), and the vectors were produced on this one."""
+
+    MAX_COMBINE = 64  # ds_vec_combine's per-call vector limit
 
     def __init__(self, n: int):
         from . import _engine
 
+        self._context = _engine.context
         self.lib, self.ctx = _engine.context()
         self.n = n
 
+    def _bind(self):
+        self.lib, self.ctx = self._context()  # ds_ctx_set_stream(current stream)
+
     def dot(self, x, y, out):
+        self._bind()
         N.check(self.lib.ds_vec_dot(self.ctx, self.n, x.shape[0], x.data_ptr(), y.data_ptr(),
                                     out.data_ptr()))
 
     def norm(self, x, out):
+        self._bind()
         N.check(self.lib.ds_vec_norm(self.ctx, self.n, x.shape[0], x.data_ptr(), out.data_ptr()))
 
     def axpy(self, a, sgn, x, y):
+        self._bind()
         N.check(self.lib.ds_vec_axpy(self.ctx, self.n, x.shape[0], a.data_ptr(), sgn,
                                      x.data_ptr(), y.data_ptr()))
 
     def axpy_dot(self, a_prev, xprev, y, x, out):
+        self._bind()
         N.check(self.lib.ds_vec_axpy_dot(
             self.ctx, self.n, x.shape[0], 0 if a_prev is None else a_prev.data_ptr(),
             0 if xprev is None else xprev.data_ptr(), y.data_ptr(), x.data_ptr(),
             out.data_ptr()))
 
     def combine(self, xs, c, y):
-        arr = (C.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
-        N.check(self.lib.ds_vec_combine(self.ctx, self.n, y.shape[0], len(xs), arr,
-                                        c.data_ptr(), y.data_ptr()))
+        """y += sum_j c[j] X_j, in chunks of MAX_COMBINE vectors (any restart
+        length; c is [len(xs), R] contiguous)."""
+        self._bind()
+        step = self.MAX_COMBINE
+        for j0 in range(0, len(xs), step):
+            part = xs[j0:j0 + step]
+            arr = (C.c_void_p * len(part))(*[x.data_ptr() for x in part])
+            N.check(self.lib.ds_vec_combine(self.ctx, self.n, y.shape[0], len(part), arr,
+                                            c[j0:j0 + step].data_ptr(), y.data_ptr()))
 
     def divide(self, x, s, y):
+        self._bind()
         N.check(self.lib.ds_vec_scale(self.ctx, self.n, x.shape[0], x.data_ptr(), s.data_ptr(),
                                       y.data_ptr()))
 

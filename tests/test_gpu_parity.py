@@ -1,8 +1,10 @@
 """CUDA path vs the CPU oracle on the same seeded inputs (parity proper).
 
 Tolerances (SURVEY §8 / BASELINE.json north star): relative L2 <= 1e-10 for
-solutions in complex128, GMRES iteration counts within +-1 (we require
-equality), counters / emission events / index maps exact.
+solutions in complex128 -- DDM applications and GMRES solutions alike
+(measured on the B200: GMRES x within 1e-15 of the oracle, u_DDM within
+1e-12) -- GMRES iteration counts within +-1 (we require equality), counters /
+emission events / index maps exact.
 """
 
 import math
@@ -150,7 +152,8 @@ def test_block_lu_solve_roundtrip(cuda, which, method, cfg1, raster):
     for idx in list(b["ops"])[:4]:
         op = b["ops"][idx]
         fact = cache.get(op)
-        assert fact.backend == ("block-lu" if method != "separable" else "separable")
+        assert fact.backend == ("splu" if method != "separable" else "separable")
+        assert fact.device_backend == ("block-lu" if method != "separable" else "modal")
         rhs = rng.standard_normal((2,) + op.window.shape) + 1j * rng.standard_normal((2,) + op.window.shape)
         x = fact.solve(rhs)
         ref = O.factorize(oops[idx]).solve(rhs[0])
@@ -218,21 +221,152 @@ def test_ddm_emission_pattern_compact_source(cuda):
     assert rel(u.values, ref) <= TOL
 
 
-@pytest.mark.parametrize("method", ["auto", "block-lu"])
-def test_ddm_cfg2_batch_subset(cuda, method):
+@pytest.fixture(scope="module")
+def cfg2_oracle():
+    """Config 2 (the headline): the oracle's u and counters for all 16 seeded
+    RHS that bench.py times (~0.3 s per RHS on the box's host)."""
     s = configs.spec(2)
     b = configs.build(s)
-    f = configs.sources(s, b["grid"])[:4]
-    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(method=method),
-                                   warn_collar=False)
+    f = configs.sources(s, b["grid"])
+    assert f.shape[0] == 16
     prob = O.Problem(**configs.oracle_problem(s, b))
     oops = prob.operators()
     cache = O.Cache()
+    out = [O.ddm_apply(prob, oops, cache, f[r]) for r in range(f.shape[0])]
+    return s, b, f, out
+
+
+from parity_util import flush_subnormal_owned, subnormal_owned  # noqa: E402
+
+
+def _check_batch(tag, u, reps, want, f=None, part=None, recheck=None, spec=2):
+    """u within 1e-10 of the oracle for every RHS; counters exactly equal,
+    except on RHS with subnormal-only owned source pieces, which must then
+    match exactly once those pieces are flushed (`recheck(r, f_clean)` ->
+    (nonzero, discarded) of the GPU path, compared with the oracle's)."""
+    worst = 0.0
+    rechecked = []
+    for r, (ref, orep) in enumerate(want):
+        e = rel(u[r], ref)
+        worst = max(worst, e)
+        assert e <= TOL, (tag, r, e)
+        same = (reps[r].nonzero_solves == orep["nonzero_solves"]
+                and reps[r].discarded_sources == orep["discarded_sources"])
+        if same:
+            continue
+        assert f is not None and subnormal_owned(f[r], part), (tag, r, "counters differ")
+        fc = flush_subnormal_owned(f[r], part)
+        got = recheck(r, fc)
+        cfg = configs.spec(spec)
+        prob = O.Problem(**configs.oracle_problem(cfg, configs.build(cfg)))
+        _, oc = O.ddm_apply(prob, prob.operators(), O.Cache(), fc)
+        assert got == (oc["nonzero_solves"], oc["discarded_sources"]), (tag, r, got, oc["nonzero_solves"])
+        rechecked.append(r)
+    print(f"\n{tag}: {len(want)} RHS, worst relative L2 vs oracle {worst:.2e}; counters exact"
+          + (f" (RHS {rechecked}: exact after flushing subnormal-only source pieces)" if rechecked else ""))
+
+
+def test_ddm_cfg2_bench_paths_all_rhs(cuda, cfg2_oracle):
+    """Exactly what bench.py times on config 2, all 16 RHS vs the oracle:
+    `value` = the RHS-grouped device plan (`device_plan(..., grouped=True)`,
+    `.apply` on RHS-outer device rows, default modal cache); `e2e` =
+    `diagonal_sweep_solve` on a pinned host batch (ds_ddm_apply_host)."""
+    import torch
+
+    from paper_2002_05327_b200.ddm import SweepPlan, device_plan
+
+    s, b, f, want = cfg2_oracle
+    part, ops = b["partition"], b["ops"]
+    cache = FactorizationCache()
+    R = f.shape[0]
+    dp_run = device_plan(part, ops, cache, SweepPlan.default(2), R, grouped=True)
+    assert getattr(dp_run, "groups", 1) == 2
+    fd = torch.from_numpy(f.reshape(R, -1)).cuda()
+
+    def recheck(r, fc):
+        _, rp = diagonal_sweep_solve(fc, part, ops, cache, warn_collar=False)
+        return rp.nonzero_solves, rp.discarded_sources
+
+    for _ in range(2):  # first call captures the graphs, the second replays them
+        u, _ = dp_run.apply(fd)
+        reps = _reports_of(dp_run, R, part)
+        _check_batch("cfg2 device (grouped, graph)", u.cpu().numpy().reshape(f.shape), reps, want,
+                     f, part, recheck)
+    fp = torch.from_numpy(f).pin_memory()
+    for _ in range(2):
+        uh, reps = diagonal_sweep_solve(fp, part, ops, cache, warn_collar=False)
+        assert not uh.values.is_cuda and uh.values.is_pinned()
+        _check_batch("cfg2 pinned host (e2e)", uh.values.numpy(), reps, want, f, part, recheck)
+
+
+def _reports_of(dp, R, part):
+    from paper_2002_05327_b200.ddm import SweepPlan, _reports
+
+    return _reports(dp, R, SweepPlan.default(part.dim), part, False, False)
+
+
+def test_ddm_cfg2_block_lu_all_rhs(cuda, cfg2_oracle):
+    """The block-LU backend (K2/K3) on the same 16 RHS."""
+    s, b, f, want = cfg2_oracle
+    cache = FactorizationCache(method="block-lu")
+    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, warn_collar=False)
+
+    def recheck(r, fc):
+        _, rp = diagonal_sweep_solve(fc, b["partition"], b["ops"], cache, warn_collar=False)
+        return rp.nonzero_solves, rp.discarded_sources
+
+    _check_batch("cfg2 block-LU", u.values, reps, want, f, b["partition"], recheck)
+
+
+def test_modal_guard_forced_fallback(cuda, cfg1):
+    """modal_cond_max below every operator's cond(V): each separable operator
+    falls back to the block LU (backend 'splu', reason recorded) and the DDM
+    result is bitwise the block-LU backend's and within 1e-10 of the oracle."""
+    s, b, prob, oops = cfg1
+    f = configs.sources(s, b["grid"])[0]
+    cache = FactorizationCache(modal_cond_max=1.0)
+    u, rep = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, warn_collar=False)
+    assert cache.count == 16
+    for fa in cache._store.values():
+        assert fa.backend == "splu" and fa.device_backend == "block-lu"
+        assert "cond(V)" in fa.fallback
+    ub, _ = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(method="block-lu"),
+                                 warn_collar=False)
+    assert np.array_equal(u.values, ub.values)
+    ref, orep = O.ddm_apply(prob, oops, O.Cache(), f)
+    assert rel(u.values, ref) <= TOL
+    assert rep.nonzero_solves == orep["nonzero_solves"]
+
+
+def test_wide_window_guard_parity(cuda):
+    """Wider windows than configs 1/2/4 (2x2 subdomains of a 321^2-node
+    interior, windows ~193 nodes, sigma0 = 40): the eigenbases reach
+    cond(V) ~ 1e5 and ||V^-1 V - I|| ~ 3e-9, so the guard sends those
+    operators to the block LU; the DDM map stays within 1e-10 of the oracle.
+    The unguarded modal path's error is printed for the record."""
+    import math as _m
+
+    s = configs.Spec("wide-2x2", ((0.0, 1.0),) * 2, (320, 320), 16, 16, (2, 2),
+                     2 * _m.pi * 20, 2, "direct", "constant", 1,
+                     centers=((0.3, 0.4), (0.62, 0.71)))
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"])
+    cache = FactorizationCache()
+    u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, warn_collar=False)
+    fell = [fa.fallback for fa in cache._store.values() if fa.fallback]
+    assert fell, "expected the guard to reject at least one eigenbasis"
+    uu, _ = diagonal_sweep_solve(f, b["partition"], b["ops"], FactorizationCache(modal_cond_max=_m.inf),
+                                 warn_collar=False)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops = prob.operators()
+    oc = O.Cache()
     for r in range(f.shape[0]):
-        ref, orep = O.ddm_apply(prob, oops, cache, f[r])
-        assert rel(u.values[r], ref) <= TOL
+        ref, orep = O.ddm_apply(prob, oops, oc, f[r])
+        e = rel(u.values[r], ref)
+        print(f"\nwide windows rhs {r}: guarded {e:.2e} ({len(fell)} of {cache.count} operators on "
+              f"the block LU), unguarded modal {rel(uu.values[r], ref):.2e}")
+        assert e <= TOL, e
         assert reps[r].nonzero_solves == orep["nonzero_solves"]
-        assert reps[r].discarded_sources == orep["discarded_sources"]
 
 
 def test_ddm_linearity_and_determinism(cuda, cfg1):
@@ -271,7 +405,9 @@ def test_gmres_ddm_raster_parity(cuda, raster):
         xr, orep = O.gmres_ddm(prob, oops, ogop, ocache, f[r])
         assert reps[r].n_iter == orep["n_iter"]
         assert reps[r].converged and orep["converged"]
-        assert rel(x[r], xr) <= 1e-9, rel(x[r], xr)
+        e = rel(x[r], xr)
+        print(f"\nraster-mini GMRES rhs {r}: {reps[r].n_iter} iterations, x vs oracle {e:.2e}")
+        assert e <= TOL, e
         np.testing.assert_allclose(reps[r].residuals, orep["residuals"], rtol=1e-6, atol=1e-12)
 
 
@@ -389,7 +525,9 @@ def test_gpu_vs_reference_golden_raster_gmres(cuda, raster):
                             lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
                             f)
     assert reps[0].n_iter == int(g["n_iter"])
-    assert rel(x[0], g["x_gmres"]) <= 1e-9
+    e = rel(x[0], g["x_gmres"])
+    print(f"\nraster-mini GMRES vs reference golden: x {e:.2e}")
+    assert e <= TOL, e
 
 
 # ------------------------------------------------------------------- 3D
@@ -439,29 +577,47 @@ def test_3d_ddm_vs_reference_golden_both_plans(cuda, method):
 
 
 def test_cfg4_full_size_parity(cuda):
-    """Config 4 at full size (109^3, 4x4x4, 8 RHS): factors shared across
-    the 27 translation classes (76 GB), RHS 0 checked against the oracle's
-    separable (Schur/Sylvester) 3D solver; the other RHS through linearity
-    of the batched map."""
+    """Config 4 at full size (109^3, 4x4x4, 8 RHS) on the path bench.py times:
+    the default cache (modal factorization of all 64 windows, no sharing).
+    RHS 0 and 1 against the oracle's separable (Schur/Sylvester) 3D solver,
+    counters equal; all 8 RHS through linearity of the batched map (u of a
+    combination of the 8 sources = the combination of their u) and bitwise
+    determinism of a second application."""
     import time
 
     s = configs.spec(4)
     b = configs.build(s)
     f = configs.sources(s, b["grid"])
-    cache = FactorizationCache(share_translates=True)
+    R = f.shape[0]
+    cache = FactorizationCache()
     t0 = time.time()
     cache.prepare([b["ops"][i] for i in b["partition"].subdomains()])
     tf = time.time() - t0
-    assert cache.count == 27
+    assert cache.count == 64
+    assert all(fa.backend == "separable" for fa in cache._store.values())
     t0 = time.time()
     u, reps = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, warn_collar=False)
     ta = time.time() - t0
+    u2, _ = diagonal_sweep_solve(f, b["partition"], b["ops"], cache, warn_collar=False)
+    assert np.array_equal(u.values, u2.values)
+    coef = np.random.default_rng(4).standard_normal(R) + 1j * np.random.default_rng(5).standard_normal(R)
+    comb = np.tensordot(coef, f, axes=1)
+    uc, _ = diagonal_sweep_solve(comb, b["partition"], b["ops"], cache, warn_collar=False)
+    lin_err = rel(uc.values, np.tensordot(coef, u.values, axes=1))
+    assert lin_err <= TOL, lin_err
     prob = O.Problem(**configs.oracle_problem(s, b))
-    ref, orep = O.ddm_apply(prob, prob.operators(), O.Cache(), f[0])
-    print(f"\ncfg4: factor {tf:.1f} s, one 8-RHS application {ta:.2f} s, parity {rel(u.values[0], ref):.2e}")
-    assert rel(u.values[0], ref) <= TOL
-    assert reps[0].nonzero_solves == orep["nonzero_solves"]
-    assert reps[0].discarded_sources == orep["discarded_sources"]
+    oops = prob.operators()
+    ocache = O.Cache()
+    want = [O.ddm_apply(prob, oops, ocache, f[r]) for r in (0, 1)]
+
+    def recheck(r, fc):
+        _, rp = diagonal_sweep_solve(fc, b["partition"], b["ops"], cache, warn_collar=False)
+        return rp.nonzero_solves, rp.discarded_sources
+
+    _check_batch("cfg4 (modal, unshared)", u.values[:2], reps[:2], want, f[:2], b["partition"],
+                 recheck, spec=4)
+    print(f"cfg4: factor {tf:.1f} s, one 8-RHS application {ta:.2f} s, "
+          f"linearity (8 RHS) {lin_err:.2e}")
 
 
 def test_cfg5r_gmres_vs_reference_golden(cuda):
@@ -482,18 +638,21 @@ def test_cfg5r_gmres_vs_reference_golden(cuda):
                             lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
                             f, tol=1e-6)
     assert reps[0].n_iter == int(g["n_iter"]) and reps[0].converged
-    assert rel(x[0], g["x"]) <= 1e-9, rel(x[0], g["x"])
+    e = rel(x[0], g["x"])
+    print(f"\ncfg5r GMRES vs reference golden: {reps[0].n_iter} iterations, x {e:.2e}")
+    assert e <= TOL, e
     np.testing.assert_allclose(reps[0].residuals, g["residuals"], rtol=1e-6, atol=1e-12)
     assert all(r.converged for r in reps)
 
 
 def test_cfg3_full_size_gmres_parity(cuda):
-    """Config 3 at full size (1241x441, 16x8 raster windows): RHS 0 of the
-    64-RHS batch against the oracle's SuperLU-based GMRES-DDM (iterations
-    equal, solution <= 1e-9, residual history to 1e-6)."""
+    """Config 3 at full size (1241x441, 16x8 raster windows) on the path
+    bench.py times (batched GMRES over the RHS-grouped DDM preconditioner):
+    RHS 0-3 against the oracle's SuperLU-based GMRES-DDM (iterations equal,
+    solution <= 1e-10, residual history to 1e-6)."""
     s = configs.spec(3)
     b = configs.build(s)
-    f = configs.sources(s, b["grid"])[:2]
+    f = configs.sources(s, b["grid"])[:4]
     part, ops, gop = b["partition"], b["ops"], b["gop"]
     cache = FactorizationCache()
     full = part.grid.full_window()
@@ -501,10 +660,14 @@ def test_cfg3_full_size_gmres_parity(cuda):
                             lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
                             f, tol=1e-6)
     prob = O.Problem(**configs.oracle_problem(s, b))
-    xr, orep = O.gmres_ddm(prob, prob.operators(), prob.global_operator(), O.Cache(), f[0])
-    assert reps[0].n_iter == orep["n_iter"] and reps[0].converged
-    assert rel(x[0], xr) <= 1e-9, rel(x[0], xr)
-    np.testing.assert_allclose(reps[0].residuals, orep["residuals"], rtol=1e-6, atol=1e-12)
+    oops, ogop, ocache = prob.operators(), prob.global_operator(), O.Cache()
+    for r in range(f.shape[0]):
+        xr, orep = O.gmres_ddm(prob, oops, ogop, ocache, f[r])
+        e = rel(x[r], xr)
+        print(f"\ncfg3 rhs {r}: {reps[r].n_iter} iterations (oracle {orep['n_iter']}), x vs oracle {e:.2e}")
+        assert reps[r].n_iter == orep["n_iter"] and reps[r].converged
+        assert e <= TOL, e
+        np.testing.assert_allclose(reps[r].residuals, orep["residuals"], rtol=1e-6, atol=1e-12)
 
 
 def test_edge_cases_zero_sources_and_errors(cuda, cfg1):
@@ -724,3 +887,70 @@ def test_transfer_kernel_variants_bitwise(cuda):
     # the complex multiply-adds into FMAs differently -> equal to rounding
     assert np.array_equal(outs[0], outs[1])
     assert rel(outs[2], outs[1]) <= 1e-13
+
+
+def test_gmres_restart_longer_than_combine_limit(cuda, raster):
+    """restart = 70 > 64 vectors per ds_vec_combine call: the basis update
+    runs in chunks.  (1) The chunked combination of 70 random vectors equals
+    the dense sum to 1e-14.  (2) DDM-preconditioned GMRES with an
+    unreachable tolerance runs the full 70-step cycle (past convergence to
+    rounding level) and x matches the oracle's GMRES to 1e-10."""
+    import torch
+
+    from paper_2002_05327_b200.krylov import _Vec
+
+    rng = np.random.default_rng(70)
+    n, R, K = 5000, 3, 70
+    xs_h = rng.standard_normal((K, R, n)) + 1j * rng.standard_normal((K, R, n))
+    c_h = rng.standard_normal((K, R)) + 1j * rng.standard_normal((K, R))
+    y0 = rng.standard_normal((R, n)) + 1j * rng.standard_normal((R, n))
+    xs = [torch.from_numpy(x).cuda() for x in xs_h]
+    y = torch.from_numpy(y0).cuda()
+    _Vec(n).combine(xs, torch.from_numpy(c_h).cuda(), y)
+    want = y0 + np.einsum("kr,krn->rn", c_h, xs_h)
+    assert np.linalg.norm(y.cpu().numpy() - want) <= 1e-14 * np.linalg.norm(want)
+
+    s, b, prob, oops = raster
+    f = configs.sources(s, b["grid"])[:1]
+    part, ops, gop = b["partition"], b["ops"], b["gop"]
+    cache = FactorizationCache()
+    full = part.grid.full_window()
+    x, reps = gmres_batched(lambda v: gop.apply(v, region=full),
+                            lambda v: diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)[0].values,
+                            f, tol=1e-300, restart=70, max_iter=70)
+    assert reps[0].n_iter == 70 and not reps[0].converged
+    ogop, ocache = prob.global_operator(), O.Cache()
+    xr, orep = O.gmres(lambda v: ogop.apply(v), lambda v: O.ddm_apply(prob, oops, ocache, v)[0],
+                       f[0], tol=1e-300, restart=70, max_iter=70)
+    assert orep["n_iter"] == 70
+    e = rel(x[0], xr)
+    print(f"\nrestart 70 (DDM-preconditioned, 70 steps): x vs oracle {e:.2e}")
+    assert e <= TOL, e
+
+
+def test_pinned_strided_and_empty_batches(cuda, cfg1):
+    """A strided view of a pinned batch goes through one packed pinned copy
+    (not a pageable reshape) and equals the device path; an empty batch
+    returns an empty field (an empty RHS shard of a multi-rank run)."""
+    import torch
+
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(12)
+    shape = (4,) + b["grid"].counts
+    f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    cache = FactorizationCache()
+    fp = torch.from_numpy(f).pin_memory()
+    view = fp[::2]
+    assert not view.is_contiguous()
+    u_h, reps = diagonal_sweep_solve(view, b["partition"], b["ops"], cache, warn_collar=False)
+    u_d, _ = diagonal_sweep_solve(torch.from_numpy(f[::2].copy()).cuda(), b["partition"], b["ops"],
+                                  cache, warn_collar=False)
+    assert np.array_equal(u_h.values.numpy(), u_d.values.cpu().numpy())
+    assert len(reps) == 2
+    u0, r0 = diagonal_sweep_solve(np.zeros((0,) + b["grid"].counts, np.complex128), b["partition"],
+                                  b["ops"], cache, warn_collar=False)
+    assert u0.values.shape == (0,) + b["grid"].counts and r0 == []
+    t0, _ = diagonal_sweep_solve(torch.zeros((0,) + b["grid"].counts, dtype=torch.complex128,
+                                             device="cuda"), b["partition"], b["ops"], cache,
+                                 warn_collar=False)
+    assert t0.values.is_cuda and t0.values.shape[0] == 0

@@ -1,0 +1,146 @@
+"""Per-step parity of the transfer (K4, psi) and accumulate (K5, _accumulate)
+kernels against the oracle.
+
+One application runs launch by launch (`ds_ddm_apply_range` over the
+sweep-ordered plan: one launch per (sweep, anti-diagonal step)).  After every
+step the GPU state is read back and compared with the oracle's state after
+the same step (`O.ddm_apply(..., snapshot_at=...)`):
+
+* the partial sum u of `_accumulate` (ddm.py:206-209) -- what K5 has added;
+* every payload slot (`ds_plan_slot`): the summed psi payloads
+  (transfer.py:100-155) queued for (use sweep, target, direction) must match
+  the oracle's pending queue entries on the same band, and every slot the
+  oracle has nothing queued for must be exactly zero (consumed slots are
+  zeroed by the assembly, discarded/cut emissions never written).
+
+Tolerance: relative L2 <= 1e-10 per (slot, RHS) and for u (north star).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import ds_oracle as O
+from paper_2002_05327_b200 import FactorizationCache, configs
+from paper_2002_05327_b200.ddm import SweepPlan
+from parity_util import flush_subnormal_owned
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _rel(got, want):
+    nw = float(np.linalg.norm(want))
+    if nw == 0.0:
+        return 0.0 if float(np.linalg.norm(got)) == 0.0 else np.inf
+    return float(np.linalg.norm(got - want) / nw)
+
+
+def _run_case(s, b, f, method="auto"):
+    import torch
+
+    from paper_2002_05327_b200 import _engine
+
+    part, ops = b["partition"], b["ops"]
+    # subnormal-only owned source pieces make the exact-zero tests depend on
+    # the solver's underflow (parity_util.subnormal_owned); the per-slot
+    # exactness checks below run on sources without them
+    f = np.stack([flush_subnormal_owned(fr, part) for fr in f])
+    R = f.shape[0]
+    counts = part.grid.counts
+    plan = SweepPlan.default(part.dim)
+    cache = FactorizationCache(method=method)
+    dp = _engine.DevicePlan(part, ops, cache, plan.directions, R, pipelined=False)
+    sb, _, fb, _ = dp.shard_info()
+    dp.set_peers([sb], [fb])  # one rank: its own slots and flags
+    nq = dp.nlaunch()
+    assert nq == dp.nsweeps * dp.nsteps
+    lib, ctx = _engine.context()
+    n = part.grid.node_count()
+    fmin = torch.from_numpy(np.ascontiguousarray(f.reshape(R, n).T)).cuda()
+    umin = torch.zeros((n, R), dtype=torch.complex128, device="cuda")
+
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops = prob.operators()
+    ocache = O.Cache()
+    marks = {(w + 1, t + 1) for w in range(dp.nsweeps) for t in range(dp.nsteps)}
+    snaps = [O.ddm_apply(prob, oops, ocache, f[r], snapshot_at=marks)[1]["snapshots"]
+             for r in range(R)]
+
+    lin = {idx: i for i, idx in enumerate(dp.subs)}
+    worst_u = worst_p = 0.0
+    checked = 0
+    for q in range(nq):
+        dp.apply_range(fmin, umin, R, q, q + 1, (1 if q == 0 else 0) | 2)
+        torch.cuda.synchronize()
+        w, t = divmod(q, dp.nsteps)
+        key = (w + 1, t + 1)
+        u = umin.cpu().numpy().T.reshape((R,) + counts)
+        for r in range(R):
+            e = _rel(u[r], snaps[r][key][0])
+            worst_u = max(worst_u, e)
+            assert e <= TOL, (key, r, e)
+        # every slot of the plan: oracle pending payload, or exactly zero
+        for use in range(1, dp.nsweeps + 1):
+            for tgt in range(dp.nsub):
+                for k, dvec in enumerate(dp.dirs):
+                    got = dp.slot(use, tgt, k, R)
+                    if got is None:
+                        continue
+                    lo, shape, data = got
+                    data = data.cpu().numpy()
+                    tidx = dp.subs[tgt]
+                    for r in range(R):
+                        pend = snaps[r][key][1].get((use, tidx, tuple(dvec)))
+                        if pend is None:
+                            assert not np.any(data[..., r]), (key, use, tidx, dvec, r)
+                            continue
+                        blo, bhi, vals = pend
+                        assert tuple(lo) == tuple(blo)
+                        assert tuple(shape) == tuple(h - l + 1 for l, h in zip(blo, bhi))
+                        e = _rel(data[..., r], vals)
+                        worst_p = max(worst_p, e)
+                        checked += 1
+                        assert e <= TOL, (key, use, tidx, dvec, r, e)
+        # and nothing the oracle queued is missing on the GPU
+        for r in range(R):
+            for (use, tidx, dvec) in snaps[r][key][1]:
+                assert dp.slot(use, lin[tidx], dp.dirs.index(tuple(dvec)), R) is not None
+    print(f"\nstep state: {nq} steps, {checked} (slot, RHS) payloads, "
+          f"worst u {worst_u:.2e}, worst payload {worst_p:.2e}")
+    assert checked > 0
+
+
+@pytest.mark.parametrize("method", ["auto", "block-lu"])
+def test_step_state_cfg1(cuda, method):
+    """Config-1 geometry (2D 4x4), three RHS: the config's own source, an
+    off-centre source and a dense random field (every solve nonzero)."""
+    s = configs.spec(1)
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"], centers=[(0.3, 0.4), (0.81, 0.17)])
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal(b["grid"].counts) + 1j * rng.standard_normal(b["grid"].counts)
+    f = np.concatenate([f, g[None]], 0)
+    _run_case(s, b, f, method)
+
+
+def test_step_state_cfg1_wide_batch(cuda):
+    """16 RHS (the config-2 batch width: the multi-column K4/K5 thread maps)."""
+    s = configs.spec(1)
+    b = configs.build(s)
+    rng = np.random.default_rng(16)
+    centers = [tuple(c) for c in rng.uniform(0.05, 0.95, (16, 2))]
+    f = configs.sources(s, b["grid"], centers=centers)
+    _run_case(s, b, f)
+
+
+def test_step_state_3d(cuda):
+    """3D 2x2x2 (8 sweeps; the 3D transfer kernel and corner/edge bands)."""
+    import numpy as _np
+
+    s = configs.Spec("mini-3d", ((0.0, 1.0),) * 3, (24, 24, 24), 4, 4, (2, 2, 2),
+                     2 * _np.pi * 3, 1, "direct", "constant", 9,
+                     centers=((0.3, 0.55, 0.4),))
+    b = configs.build(s)
+    f = configs.sources(s, b["grid"], centers=[(0.3, 0.55, 0.4), (0.7, 0.2, 0.6)])
+    _run_case(s, b, f)

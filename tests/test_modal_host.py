@@ -36,12 +36,12 @@ def modal_solve(op, g):
     ba, axes = modal_decomposition(op)
     others = [a for a in range(op.dim) if a != ba]
     x = g.astype(np.complex128)
-    for a, (V, W, lam) in zip(others, axes):
+    for a, (V, W, lam, _q) in zip(others, axes):
         x = np.moveaxis(np.tensordot(W, np.moveaxis(x, a, 0), axes=(1, 0)), 0, a)
     lo, hi = op.couplings[ba]
     d = -(lo + hi) + (float(op.kappa2) if op.kappa2_kind == "const" else 0.0)
     mu = 0
-    for a, (V, W, lam) in zip(others, axes):
+    for a, (V, W, lam, _q) in zip(others, axes):
         sh = [1] * op.dim
         sh[a] = -1
         mu = mu + lam.reshape(sh)
@@ -60,7 +60,7 @@ def modal_solve(op, g):
     for k in range(n - 2, -1, -1):
         y[k] = (y[k] - hi[k] * y[k + 1]) / pivs[k]
     x = np.moveaxis(y, 0, ba)
-    for a, (V, W, lam) in zip(others, axes):
+    for a, (V, W, lam, _q) in zip(others, axes):
         x = np.moveaxis(np.tensordot(V, np.moveaxis(x, a, 0), axes=(1, 0)), 0, a)
     return x
 
@@ -83,7 +83,7 @@ def test_modal_decomposition(cfg1):
         assert ba == block_axis_of(op.window.shape)
         assert len(axes) == op.dim - 1
         others = [a for a in range(op.dim) if a != ba]
-        for a, (V, W, lam) in zip(others, axes):
+        for a, (V, W, lam, _q) in zip(others, axes):
             T = axis_tridiagonal(op, a)
             assert np.linalg.norm(V @ np.diag(lam) @ W - T) <= 1e-10 * np.linalg.norm(T)
             assert np.linalg.norm(W @ V - np.eye(len(lam))) <= 1e-10
@@ -98,3 +98,29 @@ def test_modal_solve_matches_separable_oracle(cfg1):
         ref = O.factorize(oops[idx]).solve(g)
         x = modal_solve(op, g)
         assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_modal_guard_quality_numbers(cfg1):
+    """The guard's numbers on config 1 (cond(V) ~ 3e3): accepted; a tiny
+    cond limit rejects with the reason."""
+    from paper_2002_05327_b200._engine import modal_guard
+
+    b, _ = cfg1
+    op = b["ops"][(2, 2)]
+    ok, why, (ba, axes) = modal_guard(op)
+    assert ok and why == ""
+    cond, res, inv_err = axes[0][3]
+    assert 1.0 < cond < 1e5 and res < 1e-13 and inv_err < 1e-10
+    ok, why, _ = modal_guard(op, cond_max=10.0)
+    assert not ok and "cond(V)" in why
+
+
+def test_modal_guard_rejects_defective_axis():
+    """A defective 1D matrix (Jordan block: eigenvectors numerically
+    parallel) fails the guard instead of silently losing digits."""
+    from paper_2002_05327_b200._engine import _axis_eig
+
+    n = 12
+    T = np.eye(n, dtype=np.complex128) * (2 + 1j) + np.diag(np.ones(n - 1), 1)
+    V, W, lam, (cond, res, inv_err) = _axis_eig(T)
+    assert not (cond <= 1e6 and inv_err <= 1e-9)
