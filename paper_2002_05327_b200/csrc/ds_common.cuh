@@ -203,26 +203,13 @@ struct ModalJob {
   cplx *s0, *s1;
   const int *nz;  // per-RHS nonzero flags (NULL = solve all)
 };
-// Stream-K workspace of the modal transforms (K3m-T): partial accumulators
-// of tiles split between CTAs ([2 per CTA][TM * TN * 3] doubles) and one
-// arrival counter per tile (zero between launches; the last arriver resets it)
-struct ModalWs {
-  double *part;
-  int *cnt;
-  int ctas;   // grid size the workspace was sized for (<= 0: no stream-K)
-  int tiles;  // counters available
-};
 // launch the modal solve of njob visits (device job table; facts_host: the
 // jobs' factor layouts, for grid sizing)
 int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,
                     int nrhs);
 // one phase of it: 0 forward transforms, 1 recurrences, 2 inverse transforms
 int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host,
-                          int njob, int nrhs, int phase, const ModalWs *ws = nullptr);
-// stream-K workspace size for launches of up to njob_max jobs of the given
-// layouts at nrhs_max: (CTAs, partial doubles, tile counters)
-void ds_modal_ws_size(const ds_ctx *ctx, const FactDev *facts, int nfacts, int nrhs_max,
-                      int *ctas, size_t *part_doubles, int *tiles);
+                          int njob, int nrhs, int phase);
 // all three phases in one launch, ordered per visit by counters[2 * njob]
 // (zeroed before the application; 2D operators only)
 int ds_launch_modal_fused(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,

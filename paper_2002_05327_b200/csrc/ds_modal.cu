@@ -322,136 +322,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
 }
 
-// ------------------------------------- stream-K transforms (K3m-T, default)
-// The one-tile-per-CTA grid above runs ~1.2 waves of tiles per launch on
-// config 2 (ncu: 696 CTAs on 592 slots, SM active 78% of the elapsed
-// cycles): the second, partial wave idles most SMs.  Here a grid of
-// (resident CTAs) splits the launch's total K-chunk work -- every job's
-// tiles x K chunks, with the active (nonzero) RHS columns known only on the
-// device -- into equal contiguous ranges.  A CTA accumulates the chunks of
-// its range tile by tile; a tile split between CTAs is combined by the last
-// of its CTAs to arrive (partials in a workspace, per-tile arrival counter,
-// summed in CTA order: deterministic, no CTA ever waits for another).
-#define SK_JMAX 64
-#define SK_MIN_CHUNKS 6
-template <int MT, int WR, int WC, int TK, int MINB, int NS>
-__global__ void __launch_bounds__(32 * WR * WC, MINB)
-    k_modal_gemm_sk(const ModalJob *__restrict__ jobs, int njob, int pass, int nrhs, ModalWs ws) {
-  constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
-  constexpr int NW = NTH / 32, PER = MT * 4;  // accumulator doubles per thread and product
-  extern __shared__ __align__(16) cplx smem_mg[];
-  __shared__ int act[RMAX_MODAL + 1];
-  __shared__ int s_A[SK_JMAX];
-  __shared__ long long s_u[SK_JMAX + 1];  // chunk-unit prefix over jobs
-  __shared__ int s_tl[SK_JMAX + 1];       // tile prefix over jobs
-  __shared__ int s_last;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  pdl_wait();
-  for (int j = warp; j < njob; j += NW) {  // active columns of every job (K6 flags)
-    const int *nz = jobs[j].nz;
-    int cnt = 0;
-    for (int r0 = 0; r0 < nrhs; r0 += 32) {
-      const int r = r0 + lane;
-      cnt += __popc(__ballot_sync(0xffffffffu, r < nrhs && (!nz || nz[r])));
-    }
-    if (lane == 0) s_A[j] = cnt;
-  }
-  __syncthreads();
-  if (t == 0) {
-    long long u = 0;
-    int tl = 0;
-    for (int j = 0; j < njob; ++j) {
-      s_u[j] = u;
-      s_tl[j] = tl;
-      const PassGeo G = pass_geo(*jobs[j].f, jobs[j], pass, nrhs);
-      const int rt = (G.n + TM - 1) / TM, ct = (G.outer * G.inner * s_A[j] + TN - 1) / TN;
-      tl += rt * ct;
-      u += (long long)rt * ct * ((G.n + TK - 1) / TK);
-    }
-    s_u[njob] = u;
-    s_tl[njob] = tl;
-  }
-  __syncthreads();
-  const long long U = s_u[njob];
-  const int S = (int)min((long long)gridDim.x, max(1LL, U / SK_MIN_CHUNKS));
-  const int c = blockIdx.x;
-  if (U == 0 || c >= S) return;
-  auto ubeg = [&](int cc) { return (long long)cc * U / S; };
-  auto cta_of = [&](long long uu) {
-    int cc = (int)(uu * S / U);
-    while (cc + 1 < S && ubeg(cc + 1) <= uu) ++cc;
-    while (ubeg(cc) > uu) --cc;
-    return cc;
-  };
-  const long long u0 = ubeg(c), u1 = ubeg(c + 1);
-  long long u = u0;
-  int j = 0;
-  while (u < u1) {
-    while (s_u[j + 1] <= u) ++j;
-    const ModalJob J = jobs[j];
-    const PassGeo G = pass_geo(*J.f, J, pass, nrhs);
-    const int A = active_rhs(J, nrhs, act);
-    const int nkc = (G.n + TK - 1) / TK;
-    const int total = G.outer * G.inner * A;
-    const int ct = (total + TN - 1) / TN;
-    const int tl = (int)((u - s_u[j]) / nkc);
-    const long long ts = s_u[j] + (long long)tl * nkc, te = ts + nkc;
-    const int kc0 = (int)(u - ts), kc1 = (int)(min(u1, te) - ts);
-    const int row0 = (tl / ct) * TM, col0 = (tl % ct) * TN;
-    const int colw = min(TN, total - col0);
-    double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
-    gemm_accum<MT, WR, WC, TK, NS>(G, row0, col0, colw, kc0, kc1, smem_mg, act, A, nrhs, p1, p2, p3);
-    if (kc0 == 0 && kc1 == nkc) {
-      gemm_store<MT, WR, WC>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
-    } else {
-      const int cf = cta_of(ts), cl = cta_of(te - 1);
-      auto slot_ptr = [&](int cc) {
-        return ws.part + ((size_t)(2 * cc + (ubeg(cc) >= ts ? 0 : 1)) * NW + warp) * (3 * PER * 32) + lane;
-      };
-      double *wp = slot_ptr(c);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = mt * 4 + q;
-          __stcg(wp + (0 * PER + i) * 32, p1[mt][q >> 1][q & 1]);
-          __stcg(wp + (1 * PER + i) * 32, p2[mt][q >> 1][q & 1]);
-          __stcg(wp + (2 * PER + i) * 32, p3[mt][q >> 1][q & 1]);
-        }
-      __threadfence();
-      __syncthreads();
-      if (t == 0) {
-        const int tg = s_tl[j] + tl;
-        const int old = atomicAdd(ws.cnt + tg, 1);
-        s_last = old == cl - cf;
-        if (s_last) ws.cnt[tg] = 0;  // every participant has arrived: ready for the next launch
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) p1[mt][q >> 1][q & 1] = p2[mt][q >> 1][q & 1] = p3[mt][q >> 1][q & 1] = 0.0;
-        for (int cc = cf; cc <= cl; ++cc) {  // fixed (CTA) order: deterministic sums
-          const double *rp = slot_ptr(cc);
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i = mt * 4 + q;
-              p1[mt][q >> 1][q & 1] += __ldcg(rp + (0 * PER + i) * 32);
-              p2[mt][q >> 1][q & 1] += __ldcg(rp + (1 * PER + i) * 32);
-              p3[mt][q >> 1][q & 1] += __ldcg(rp + (2 * PER + i) * 32);
-            }
-        }
-        gemm_store<MT, WR, WC>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
-      }
-    }
-    u = ts + kc1;
-  }
-}
-
 // ------------------------------------------- mode-wise recurrences (K3m-R)
 // One thread per (visit, mode j, RHS r): forward elimination and back
 // substitution along the block axis, in place on the transformed buffer.
@@ -1055,65 +925,10 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
   return DS_OK;
 }
 
-// stream-K configuration: the default tile (32 x 32, 2 x 2 warps of 16 x 16,
-// TK 8, 4 CTAs/SM, 4-stage ring)
-#define SK_CFG 2, 2, 2, 8, 4, 4
-static int sk_ctas(const ds_ctx *ctx) {
-  constexpr int MT = 2, WR = 2, WC = 2, TK = 8, NS = 4;
-  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
-  static int per_sm = 0;
-  if (!per_sm) {
-    const size_t smem = sizeof(cplx) * NS * (TM * (TK + 4) + TK * (TN + 2));
-    cudaFuncSetAttribute(k_modal_gemm_sk<SK_CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_modal_gemm_sk<SK_CFG>, 32 * WR * WC, smem) !=
-            cudaSuccess || nb < 1)
-      nb = 1;
-    per_sm = nb;
-  }
-  return per_sm * ctx->num_sms;
-}
-
-void ds_modal_ws_size(const ds_ctx *ctx, const FactDev *facts, int nfacts, int nrhs_max, int *ctas,
-                      size_t *part_doubles, int *tiles) {
-  constexpr int TM = 32, TN = 32, NTH = 128;
-  const int S = sk_ctas(ctx);
-  ModalJob dummy;
-  memset(&dummy, 0, sizeof(dummy));
-  int tmax = 0;
-  for (int pass = 0; pass < 4; ++pass) {
-    int tl = 0;
-    for (int i = 0; i < nfacts; ++i) {
-      if (pass >= 2 * facts[i].naxes) continue;
-      const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs_max);
-      tl += ((G.n + TM - 1) / TM) * ((G.outer * G.inner * nrhs_max + TN - 1) / TN);
-    }
-    tmax = std::max(tmax, tl);
-  }
-  *ctas = S;
-  *part_doubles = (size_t)2 * S * 3 * TM * TN;
-  (void)NTH;
-  *tiles = tmax;
-}
-
-static int launch_gemm_sk(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
-                          int pass, int nrhs, const ModalWs &ws) {
-  constexpr int MT = 2, WR = 2, WC = 2, TK = 8, NS = 4;
-  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
-  const size_t smem = sizeof(cplx) * NS * (TM * (TK + 4) + TK * (TN + 2));
-  const int S = std::min(sk_ctas(ctx), ws.ctas);
-  DS_CUDA(launch_pdl(k_modal_gemm_sk<SK_CFG>, dim3(S), dim3(32 * WR * WC), smem, ctx->stream, jobs_dev,
-                     njob, pass, nrhs, ws));
-  (void)facts;
-  ctx->launches++;
-  DS_CHECK_LAUNCH();
-  return DS_OK;
-}
-
 // phase 0: forward transforms, 1: mode-wise recurrences, 2: inverse
 // transforms, -1: all three
 int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
-                          int nrhs, int phase, const ModalWs *ws) {
+                          int nrhs, int phase) {
   if (njob <= 0) return DS_OK;
   const int na = facts[0].naxes;
   for (int i = 1; i < njob; ++i)
@@ -1125,18 +940,7 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
     const char *v = getenv("DS_MG");
     return v && *v ? v[0] : 'u';
   }();
-  // stream-K tile loop (default) when the plan provides a workspace that
-  // covers this launch; the one-tile-per-CTA grid otherwise
-  int sk_tiles = 0;
-  if (ws && ws->ctas > 0 && njob <= SK_JMAX) {
-    int c_, t_;
-    size_t d_;
-    ds_modal_ws_size(ctx, facts, njob, nrhs, &c_, &d_, &t_);
-    sk_tiles = t_;
-  }
-  const bool use_sk = ws && ws->ctas > 0 && njob <= SK_JMAX && sk_tiles <= ws->tiles;
   auto launch_pass = [&](int pass) -> int {
-    if (use_sk) return launch_gemm_sk(ctx, jobs_dev, facts, njob, pass, nrhs, *ws);
     switch (variant) {
       case 'b': return launch_gemm<1, 5, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
       case 'c': return launch_gemm<3, 5, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);

@@ -101,7 +101,6 @@ struct ds_plan {
   std::vector<ModalJob> h_mjobs;
   std::vector<FactDev> h_mfacts;
   std::vector<int> mod_vidx, mod_off;
-  ModalWs mws{nullptr, nullptr, 0, 0};  // stream-K workspace of the modal transforms
   // staged (large-slab) solve: host factor layouts and couplings per subdomain
   bool staged = false;
   std::vector<FactDev> h_facts;
@@ -1359,28 +1358,6 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (!P->h_mjobs.empty()) {
     if (plan_alloc(P, &mem, sizeof(int) * 2 * P->h_mjobs.size())) return fail(DS_ECUDA);
     P->mcount = (int *)mem;
-    // stream-K workspace: sized for the launch with the most tiles
-    int ctas = 0, tiles = 0;
-    size_t part = 0;
-    for (size_t q = 0; q + 1 < P->mod_off.size(); ++q) {
-      const int m0 = P->mod_off[q], nmo = P->mod_off[q + 1] - m0;
-      if (nmo <= 0) continue;
-      int c1, t1;
-      size_t d1;
-      ds_modal_ws_size(ctx, P->h_mfacts.data() + m0, nmo, d->nrhs_max, &c1, &d1, &t1);
-      ctas = c1;
-      part = d1;
-      tiles = std::max(tiles, t1);
-    }
-    if (ctas > 0) {
-      if (plan_alloc(P, &mem, sizeof(double) * part)) return fail(DS_ECUDA);
-      P->mws.part = (double *)mem;
-      if (plan_alloc(P, &mem, sizeof(int) * std::max(tiles, 1))) return fail(DS_ECUDA);
-      P->mws.cnt = (int *)mem;
-      cudaMemset(P->mws.cnt, 0, sizeof(int) * std::max(tiles, 1));
-      P->mws.ctas = ctas;
-      P->mws.tiles = tiles;
-    }
   }
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
@@ -1584,16 +1561,6 @@ static int patch_tables(ds_plan *P, int nrhs) {
   return DS_OK;
 }
 
-// stream-K modal transforms (default; DS_MODAL_SK=0 restores the
-// one-tile-per-CTA grid for A/B measurements)
-static bool modal_sk() {
-  static const bool on = [] {
-    const char *v = getenv("DS_MODAL_SK");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
-
 static int blocks_for(ds_ctx *ctx, int64_t work, int per_visit_cap) {
   int64_t b = (work + 255) / 256;
   if (b > per_visit_cap) b = per_visit_cap;
@@ -1785,8 +1752,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         for (int ph = 0; ph < 3 && !rc; ++ph) {
           if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
           if (skip_cls & (ph == 1 ? 4 : 2)) continue;
-          rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph,
-                                     modal_sk() ? &P->mws : nullptr);
+          rc = ds_launch_modal_phase(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, ph);
         }
       }
       if (rc) return rc;
