@@ -74,6 +74,24 @@ DS_API int ds_ctx_destroy(ds_ctx *ctx);
 /* Kernels this library has launched on `ctx` so far (graph replays count
  * their captured launches).  Diagnostic: bench.py's `gpu_launches`. */
 DS_API int64_t ds_ctx_launches(const ds_ctx *ctx);
+/* Variant / tuning options of a context (ABI 5), read at every launch (a
+ * plan's captured CUDA graph keeps the choices it was recorded with).
+ * Defaults are the measured-best choices; a DS_<NAME> environment variable
+ * read at ds_ctx_create overrides a default.  Names and values:
+ *   "k1" stencil rows per thread 2 / 4 (default) / 8 / 16, 0 = 32x8 tiles;
+ *   "combine" basis-update elements per thread 1 / 2 (default);
+ *   "k4" transfer kernel 0 (default: 2D v3, 3D v2) / 1 / 2 / 3;
+ *   "k4_rv", "k6_rv" RHS columns per thread (1, 2, 4, 8);
+ *   "pdl" programmatic dependent launch 1 / 0 (process-wide);
+ *   "k5_side" beta00 accumulation on a side stream 1 / 0;
+ *   "staged" stage-per-launch block solve for small slabs too 0 / 1;
+ *   "k3g_mma" staged block product on DMMA 1 / 0; "stage_rows";
+ *   "k3_warps" 4 / 8, "k3_rc_min", "k3_rc_max", "k3_cluster" 0 / 8 / 16:
+ *     the cluster block solve's configuration search;
+ *   "hio_dstreams" download streams of ds_ddm_apply_host (>= 2).
+ * Unknown names or values: < 0. */
+DS_API int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value);
+DS_API int ds_ctx_get_option(const ds_ctx *ctx, const char *name, int32_t *value);
 
 /* --------------------------------------------------------------- operator
  * One assembled PML Helmholtz operator on a window (pml.py:75-188).
@@ -148,6 +166,27 @@ DS_API int ds_fact_create_modal(ds_ctx *ctx, ds_op *const *ops, int32_t n,
 /* 0: block-LU factors (ds_fact_create), 1: modal (ds_fact_create_modal) */
 DS_API int ds_fact_kind(const ds_fact *fact, int32_t i);
 
+/* Factor pool (ABI 5; out-of-core block LU for factor sets larger than HBM,
+ * e.g. config 5: 638 GB of dense block inverses).  Lays out the n operators
+ * (block axis, blocks, block size as ds_fact_create) without factoring them
+ * and allocates nslots factor slots of the largest operator's size.
+ * ds_fact_pool_load factors operator i into `slot` (the K2b blocked path,
+ * bitwise the factors ds_fact_create computes), evicting the slot's previous
+ * operator; it blocks and returns > 0 on a zero / non-finite pivot.
+ * ds_fact_solve works on resident operators only.  3D (large-slab)
+ * operators only. */
+DS_API int ds_fact_create_pool(ds_ctx *ctx, ds_op *const *ops, int32_t n, int32_t nslots,
+                               ds_fact **out);
+DS_API int ds_fact_pool_load(ds_ctx *ctx, ds_fact *fact, int32_t i, int32_t slot);
+/* n loads at once (operators idx[q] into slots[q], distinct): every chain of
+ * the batch advances together, sharing the panel steps' latency. */
+DS_API int ds_fact_pool_load_many(ds_ctx *ctx, ds_fact *fact, int32_t n, const int32_t *idx,
+                                  const int32_t *slots);
+/* slots, slot size, slot_owner[nslots] (operator index or -1; may be NULL),
+ * factorizations run so far */
+DS_API int ds_fact_pool_state(const ds_fact *fact, int32_t *nslots, int64_t *slot_bytes,
+                              int32_t *slot_owner, int64_t *loads);
+
 /* ------------------------------------------------------------- sweep plan
  * Static schedule of one diagonal-sweeping application (ddm.py:212-291),
  * built once by the host from the bit-exact partition / routing metadata.
@@ -214,6 +253,12 @@ typedef struct {
   const int32_t *launch_visits;
   int32_t nranks, rank;
   const int32_t *owner;
+  /* Pooled factors (optional, ABI 5): when non-NULL, fact_of_sub[s] is a
+   * factor pool (ds_fact_create_pool) and visit (sweep w, subdomain s) reads
+   * its block inverses from pool slot visit_slot[w * nsub + s]; the caller
+   * makes the slot hold s's factors (ds_fact_pool_load) before the launch
+   * containing the visit runs (ds_ddm_apply_range, launch by launch). */
+  const int32_t *visit_slot;
 } ds_plan_desc;
 
 DS_API int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *desc, ds_plan **out);

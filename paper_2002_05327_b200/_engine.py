@@ -59,6 +59,24 @@ def context():
     return lib, h
 
 
+def set_option(name: str, value: int) -> int:
+    """Set a variant / tuning option of this device's native context
+    (ds_ctx_set_option); returns the previous value.  Plans capture CUDA
+    graphs with the options in force when they were recorded."""
+    lib, ctx = context()
+    old = C.c_int32()
+    N.check(lib.ds_ctx_get_option(ctx, name.encode(), C.byref(old)), "ds_ctx_get_option")
+    N.check(lib.ds_ctx_set_option(ctx, name.encode(), int(value)), "ds_ctx_set_option")
+    return old.value
+
+
+def get_option(name: str) -> int:
+    lib, ctx = context()
+    v = C.c_int32()
+    N.check(lib.ds_ctx_get_option(ctx, name.encode(), C.byref(v)), "ds_ctx_get_option")
+    return v.value
+
+
 # ----------------------------------------------------------------- tensors
 
 def is_pinned_host(v) -> bool:
@@ -330,6 +348,112 @@ class FactorSet:
         return ba.value, nb.value, m.value, nbytes.value
 
 
+class FactorPool:
+    """Out-of-core block-LU factors (ds_fact_create_pool): the layouts of
+    `ops` and `nslots` device slots of the largest operator's factor size;
+    `load(i, slot)` factors operator i into a slot (K2b), evicting its
+    previous owner.  For factor sets larger than HBM (config 5: 64 raster
+    windows, 638 GB of dense block inverses)."""
+
+    modal = False
+
+    def __init__(self, ops, nslots: int):
+        lib, ctx = context()
+        self._dops = [device_operator(op) for op in ops]
+        arr = (C.c_void_p * len(ops))(*[d.handle.value for d in self._dops])
+        out = C.c_void_p()
+        N.check(lib.ds_fact_create_pool(ctx, arr, len(ops), int(nslots), C.byref(out)),
+                "ds_fact_create_pool")
+        self.handle = out
+        self.n = len(ops)
+        self.nslots = int(nslots)
+        self._finalizer = weakref.finalize(self, lib.ds_fact_destroy, out)
+
+    def load(self, i: int, slot: int):
+        lib, ctx = context()
+        N.check(lib.ds_fact_pool_load(ctx, self.handle, int(i), int(slot)), "ds_fact_pool_load")
+
+    def load_many(self, pairs):
+        """[(operator, slot), ...] factored in one batch (chains advance together)."""
+        if not pairs:
+            return
+        lib, ctx = context()
+        idx = np.asarray([p[0] for p in pairs], np.int32)
+        slots = np.asarray([p[1] for p in pairs], np.int32)
+        N.check(lib.ds_fact_pool_load_many(ctx, self.handle, len(pairs), idx.ctypes.data_as(N.P_i32),
+                                           slots.ctypes.data_as(N.P_i32)), "ds_fact_pool_load_many")
+
+    def state(self):
+        """(slot owners, slot bytes, factorizations run)."""
+        lib = N.load_library()
+        ns, sb, loads = C.c_int32(), C.c_int64(), C.c_int64()
+        owners = (C.c_int32 * self.nslots)()
+        N.check(lib.ds_fact_pool_state(self.handle, C.byref(ns), C.byref(sb), owners, C.byref(loads)))
+        return list(owners), sb.value, loads.value
+
+    def info(self, i):
+        lib = N.load_library()
+        ba, nb, m = C.c_int32(), C.c_int32(), C.c_int32()
+        nbytes = C.c_int64()
+        N.check(lib.ds_fact_info(self.handle, i, C.byref(ba), C.byref(nb), C.byref(m),
+                                 C.byref(nbytes)))
+        return ba.value, nb.value, m.value, nbytes.value
+
+
+def block_lu_bytes(shape) -> int:
+    """Dense block-inverse bytes of the block LU of a window (n_b m^2 complex)."""
+    nb = max(shape)
+    m = int(np.prod(shape)) // nb
+    return nb * m * m * 16
+
+
+def belady_slots(launches, nslots: int):
+    """Static slot assignment for pooled factors over a launch schedule:
+    every visit of a launch gets a distinct slot holding its subdomain's
+    factors; a subdomain not resident is loaded into the slot whose owner is
+    next used furthest in the future (Belady's optimal replacement, known
+    schedule).  Returns ({(sweep, sub): slot}, per-launch [(sub, slot)]
+    loads, total loads)."""
+    order = [sv for L in launches for (_, sv) in L]
+    pos_of = {}
+    for p in range(len(order) - 1, -1, -1):
+        pos_of.setdefault(order[p], []).append(p)  # reversed positions per subdomain
+    owner = [None] * nslots
+    slot_of = {}
+    visit_slot, loads = {}, []
+    p = 0
+    for L in launches:
+        need = {sv for (_, sv) in L}
+        if len(need) > nslots:
+            raise ConfigurationError("factor pool: a launch needs more slots than the pool has")
+        here = []
+        for (w, sv) in L:
+            stack = pos_of[sv]
+            while stack and stack[-1] < p:
+                stack.pop()
+        for (w, sv) in L:
+            if sv not in slot_of:
+                free = [c for c in range(nslots) if owner[c] is None]
+                if free:
+                    c = free[0]
+                else:
+                    def next_use(c):
+                        st = pos_of[owner[c]]
+                        while st and st[-1] < p:
+                            st.pop()
+                        return st[-1] if st else math.inf
+                    cands = [c for c in range(nslots) if owner[c] not in need]
+                    c = max(cands, key=lambda c: (next_use(c), -c))
+                    del slot_of[owner[c]]
+                owner[c] = sv
+                slot_of[sv] = c
+                here.append((sv, c))
+            visit_slot[(w, sv)] = slot_of[sv]
+        loads.append(here)
+        p += len(L)
+    return visit_slot, loads, sum(len(h) for h in loads)
+
+
 def fact_solve(fset: FactorSet, index: int, shape, rhs):
     lib, ctx = context()
     t, kind, batched = to_device_batch(rhs, shape)
@@ -418,7 +542,8 @@ class DevicePlan:
     """
 
     def __init__(self, partition, operators, cache, directions, nrhs_max: int,
-                 schedule: str = "diagonal", pipelined: bool = False, shard=None):
+                 schedule: str = "diagonal", pipelined: bool = False, shard=None,
+                 pool_slots: int | None = None):
         """schedule "diagonal": one device sweep per sweep direction, visits
         grouped by anti-diagonal step (ddm.py:212-291).  schedule "additive":
         the additive overlapping DDM (ddm.py:294-349) on the same kernels --
@@ -441,7 +566,16 @@ class DevicePlan:
         # shard = (nranks, rank, owner[s]): this plan runs only its rank's
         # visits and factorizes only its rank's operators (sharded.py)
         self.shard = shard
-        if shard is not None:
+        # pool_slots: out-of-core factors (FactorPool) -- the block LU of every
+        # operator, `pool_slots` of them resident at a time, loaded launch by
+        # launch (apply runs eagerly, launch by launch)
+        self.pool = None
+        if pool_slots is not None:
+            if shard is not None or schedule != "diagonal":
+                raise ConfigurationError("pooled factors: diagonal, unsharded plans only")
+            self.pool = FactorPool(ops, pool_slots)
+            facts = [_PoolRef(self.pool, i) for i in range(nsub)]
+        elif shard is not None:
             nranks, rank, owner = shard
             owned = [s for s in range(nsub) if owner[s] == rank]
             ofacts = dict(zip(owned, cache.factorizations([ops[s] for s in owned])))
@@ -533,7 +667,7 @@ class DevicePlan:
         # their sources are done (the dependency DAG of the sweep is shallower
         # than sweeps x steps); the cluster solve fits ~7 visits per wave
         self.launches = None
-        if (pipelined or shard is not None) and schedule == "diagonal":
+        if (pipelined or shard is not None or self.pool is not None) and schedule == "diagonal":
             order = []
             for w in range(self.nsweeps):
                 b0 = w * (nsteps + 1)
@@ -555,6 +689,8 @@ class DevicePlan:
             # cluster solve: 8 visits per launch (measured best on config 2:
             # 13.4 ms vs 14.2 at 7; 9-10 give the same as 8); staged 3D: unbounded
             cap = int(cap_env) if cap_env else (8 if max_m <= 160 else nsub * self.nsweeps)
+            if self.pool is not None:  # every visit of a launch holds a slot
+                cap = min(cap, self.pool.nslots)
             if not pipelined:  # sweep-ordered launches (one per (sweep, step))
                 self.launches = []
                 for w in range(self.nsweeps):
@@ -567,6 +703,13 @@ class DevicePlan:
                                                 None, max(1, cap))
             if shard is not None:  # same launch boundaries on every rank, own visits only
                 self.launches = [[v for v in L if shard[2][v[1]] == shard[1]] for L in self.launches]
+        self.pool_loads = None
+        self.pool_seconds = 0.0  # host time spent factoring pool slots (pooled plans)
+        if self.pool is not None:
+            vslot, self.pool_loads, self.pool_misses = belady_slots(self.launches, self.pool.nslots)
+            visit_slot = np.full(self.nsweeps * nsub, -1, np.int32)
+            for (w, sv), c in vslot.items():
+                visit_slot[w * nsub + sv] = c
         self.geoms = geoms
         self.subs = subs
         self.dirs = dirs
@@ -609,6 +752,9 @@ class DevicePlan:
             owner_arr = np.asarray(shard[2], np.int32)
             arrays["owner"] = owner_arr  # keep alive
             desc.nranks, desc.rank, desc.owner = shard[0], shard[1], owner_arr.ctypes.data
+        if self.pool is not None:
+            arrays["visit_slot"] = visit_slot  # keep alive
+            desc.visit_slot = visit_slot.ctypes.data
         if self.launches is not None:
             l_off = np.zeros(len(self.launches) + 1, np.int32)
             l_vis = []
@@ -627,8 +773,11 @@ class DevicePlan:
         self._finalizer = weakref.finalize(self, lib.ds_plan_destroy, out)
         # replay one captured CUDA graph per (buffers, nrhs): ~4 sweeps x
         # n_steps x 4 launches per application (DS_GRAPH=0 disables)
-        if os.environ.get("DS_GRAPH", "1") != "0" and shard is None:
+        if os.environ.get("DS_GRAPH", "1") != "0" and shard is None and self.pool is None:
             self.enable_graph(True)
+        if self.pool is not None:
+            sb, _, fb, _ = self.shard_info()
+            self.set_peers([sb], [fb])  # one rank: launch-range execution
 
     @property
     def workspace_bytes(self) -> int:
@@ -697,6 +846,18 @@ class DevicePlan:
     def apply_minor(self, fmin, umin, nrhs: int, partials=None):
         """One application on RHS-minor device buffers (no layout work)."""
         lib, ctx = context()
+        if self.pool is not None:  # launch by launch, loading the slots each needs
+            if partials is not None:
+                raise ConfigurationError("pooled factors: no per-sweep partials")
+            import time
+
+            last = len(self.launches) - 1
+            for l, loads in enumerate(self.pool_loads):
+                t0 = time.perf_counter()
+                self.pool.load_many(loads)  # synchronous: factors the slots' new owners
+                self.pool_seconds += time.perf_counter() - t0
+                self.apply_range(fmin, umin, nrhs, l, l + 1, (1 if l == 0 else 0) | (2 if l == last else 0))
+            return
         N.check(lib.ds_ddm_apply(ctx, self.handle, fmin.data_ptr(), umin.data_ptr(), nrhs,
                                  0 if partials is None else partials.data_ptr()),
                 "ds_ddm_apply")
@@ -763,6 +924,17 @@ class DevicePlan:
         return dict(nonzero=nonzero, discarded=discarded, visit_nonzero=vnz.reshape(shape),
                     visit_consumed=vcons.reshape(shape), visit_emitted=vemit.reshape(shape),
                     visit_cut=vcut.reshape(shape))
+
+
+class _PoolRef:
+    """A subdomain's factors inside a FactorPool (DevicePlan's fact table)."""
+
+    backend = "splu"
+    device_backend = "block-lu"
+
+    def __init__(self, pool, index):
+        self.fset = pool
+        self.index = index
 
 
 class GroupedPlan:

@@ -66,6 +66,7 @@ class PlanDesc(C.Structure):
         ("nranks", i32),
         ("rank", i32),
         ("owner", vp),
+        ("visit_slot", vp),
     ]
 
 
@@ -87,6 +88,8 @@ _SIGNATURES = [
     ("ds_ctx_set_stream", C.c_int, [vp, vp]),
     ("ds_ctx_synchronize", C.c_int, [vp]),
     ("ds_ctx_launches", i64, [vp]),
+    ("ds_ctx_set_option", C.c_int, [vp, C.c_char_p, i32]),
+    ("ds_ctx_get_option", C.c_int, [vp, C.c_char_p, P_i32]),
     ("ds_ctx_destroy", C.c_int, [vp]),
     ("ds_op_create", C.c_int, [vp, C.POINTER(OpDesc), C.POINTER(vp)]),
     ("ds_op_destroy", C.c_int, [vp]),
@@ -97,6 +100,10 @@ _SIGNATURES = [
     ("ds_fact_destroy", C.c_int, [vp]),
     ("ds_fact_create_modal", C.c_int, [vp, C.POINTER(vp), i32, C.POINTER(ModalDesc), C.POINTER(vp)]),
     ("ds_fact_kind", C.c_int, [vp, i32]),
+    ("ds_fact_create_pool", C.c_int, [vp, C.POINTER(vp), i32, i32, C.POINTER(vp)]),
+    ("ds_fact_pool_load", C.c_int, [vp, vp, i32, i32]),
+    ("ds_fact_pool_load_many", C.c_int, [vp, vp, i32, P_i32, P_i32]),
+    ("ds_fact_pool_state", C.c_int, [vp, P_i32, P_i64, P_i32, P_i64]),
     ("ds_plan_create", C.c_int, [vp, C.POINTER(PlanDesc), C.POINTER(vp)]),
     ("ds_plan_workspace_bytes", i64, [vp]),
     ("ds_plan_destroy", C.c_int, [vp]),

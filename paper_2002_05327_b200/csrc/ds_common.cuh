@@ -85,13 +85,10 @@ int ds_fail(int code, const std::string &msg);
 // DS_PDL=0 disables it.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
-inline bool ds_pdl_enabled() {
-  static const bool on = [] {
-    const char *v = getenv("DS_PDL");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
+// programmatic dependent launch on/off: the "pdl" option of the last
+// context that set it (launch_pdl has no context argument); default on
+extern int g_ds_pdl;
+inline bool ds_pdl_enabled() { return g_ds_pdl != 0; }
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -110,11 +107,36 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 }
 
 // ------------------------------------------------------------- handles
+// Variant and tuning options of a context (ds_ctx_set_option).  Defaults are
+// the measured-best choices; the environment variable named
+// in each comment, read once when the context is created, overrides a
+// default (A/B measurement tools).  Read at every launch, so tests switch
+// variants in-process.
+struct ds_options {
+  int k1 = 4;          // DS_K1: stencil rows per thread (2, 4, 8, 16) or 0 = 32x8 shared tiles
+  int combine = 2;     // DS_COMBINE: basis-update elements per thread (1 or 2)
+  int k4 = 0;          // DS_K4: transfer kernel, 0 default (2D v3, 3D v2), 1 / 2 / 3 = v1 / v2 / v3
+  int k4_rv = 1;       // DS_K4_RV: RHS columns per thread of transfer v1
+  int k6_rv = 4;       // DS_K6_RV: RHS columns per thread of the assembly (1, 2, 4, 8)
+  int pdl = 1;         // DS_PDL: programmatic dependent launch
+  int k5_side = 1;     // DS_K5_SIDE: beta00 accumulation on a high-priority side stream
+  int staged = 0;      // DS_SOLVE_MODE=staged: stage-per-launch block solve for small slabs too
+  int k3g_mma = 1;     // DS_K3G_MMA: staged (3D) block product on DMMA
+  int stage_rows = 0;  // DS_STAGE_ROWS: staged product rows per CTA (0 = auto)
+  int k3_warps = 4;    // DS_K3_NW: warps per half of the cluster block solve (4 or 8)
+  int k3_rc_min = 4;   // DS_K3_RCMIN / DS_K3_RCMAX: RHS chunk range of the cluster block solve
+  int k3_rc_max = 16;
+  int k3_cluster = 0;  // DS_K3_CLUSTER: force 8 or 16 CTAs per cluster (0 = choose)
+  int hio_dstreams = 2;  // DS_HIO_DSTREAMS: download streams of the pinned-host path
+};
+void ds_options_from_env(ds_options &o);
+
 struct ds_ctx {
   int device;
   cudaStream_t stream;
   int num_sms;
   int64_t launches;  // kernel launches issued through this context
+  ds_options opt;
   // scratch for reductions
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -161,12 +183,26 @@ struct FactDev {
   const cplx *mmul, *minv;
 };
 
+struct ds_fact;
+// device memory of slot `slot` of a factor pool (NULL if not a pool / bad slot)
+const cplx *ds_fact_slot_mem(const ds_fact *F, int slot);
+
 struct ds_fact {
   std::vector<FactDev> facts;
   std::vector<std::vector<cplx>> h_l, h_u;  // host copies of l_k, u_k per operator
   std::vector<void *> allocations;
   int64_t bytes_total = 0;
   std::vector<int64_t> bytes;
+  // factor pool (ds_fact_create_pool, ABI 5): the operators' layouts without
+  // resident factors; slot c holds the block inverses of operator
+  // slot_owner[c] (-1: empty), facts[i].sinv points into its slot while
+  // operator i is resident and is NULL otherwise
+  bool pool = false;
+  std::vector<cplx *> slot_mem;
+  std::vector<int> slot_owner;
+  std::vector<ds_op *> ops;
+  size_t slot_bytes = 0;
+  int64_t loads = 0;  // factorizations run by ds_fact_pool_load
 };
 
 // window-local linear (C-order) index <-> block layout offset
@@ -210,10 +246,6 @@ int ds_launch_modal(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_
 // one phase of it: 0 forward transforms, 1 recurrences, 2 inverse transforms
 int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host,
                           int njob, int nrhs, int phase);
-// all three phases in one launch, ordered per visit by counters[2 * njob]
-// (zeroed before the application; 2D operators only)
-int ds_launch_modal_fused(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts_host, int njob,
-                          int nrhs, int *counters);
 void ds_fill_layout(const OpDev &o, FactDev &f);
 
 int ceil_div(int a, int b);

@@ -44,12 +44,90 @@ extern "C" int ds_ctx_create(int device, void *stream, ds_ctx **out) {
   c->stream = (cudaStream_t)stream;
   c->num_sms = prop.multiProcessorCount;
   c->launches = 0;
+  ds_options_from_env(c->opt);
+  g_ds_pdl = c->opt.pdl;
   c->scratch_bytes = 1 << 20;
   if (cudaMalloc(&c->scratch, c->scratch_bytes) != cudaSuccess) {
     delete c;
     return ds_fail(DS_ECUDA, "ds_ctx_create: scratch allocation failed");
   }
   *out = c;
+  return DS_OK;
+}
+
+int g_ds_pdl = 1;
+
+static int env_opt(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+void ds_options_from_env(ds_options &o) {
+  if (const char *v = getenv("DS_K1")) {
+    if (*v == 't') o.k1 = 0;
+    else if (*v == 'c') o.k1 = atoi(v + 1);
+  }
+  o.combine = env_opt("DS_COMBINE", 2) == 1 ? 1 : 2;
+  if (const char *v = getenv("DS_K4"))
+    if (*v == 'v') o.k4 = atoi(v + 1);
+  o.k4_rv = env_opt("DS_K4_RV", o.k4_rv);
+  o.k6_rv = env_opt("DS_K6_RV", o.k6_rv);
+  o.pdl = env_opt("DS_PDL", 1) != 0;
+  o.k5_side = env_opt("DS_K5_SIDE", 1) != 0;
+  if (const char *v = getenv("DS_SOLVE_MODE")) o.staged = std::string(v) == "staged";
+  o.k3g_mma = env_opt("DS_K3G_MMA", 1) != 0;
+  o.stage_rows = env_opt("DS_STAGE_ROWS", 0);
+  o.k3_warps = env_opt("DS_K3_NW", 4) >= 8 ? 8 : 4;
+  o.k3_rc_min = std::max(1, env_opt("DS_K3_RCMIN", o.k3_rc_min));
+  o.k3_rc_max = std::max(1, env_opt("DS_K3_RCMAX", o.k3_rc_max));
+  o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
+  o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
+}
+
+// name -> member of ds_options
+static int *opt_field(ds_options &o, const std::string &k) {
+  if (k == "k1") return &o.k1;
+  if (k == "combine") return &o.combine;
+  if (k == "k4") return &o.k4;
+  if (k == "k4_rv") return &o.k4_rv;
+  if (k == "k6_rv") return &o.k6_rv;
+  if (k == "pdl") return &o.pdl;
+  if (k == "k5_side") return &o.k5_side;
+  if (k == "staged") return &o.staged;
+  if (k == "k3g_mma") return &o.k3g_mma;
+  if (k == "stage_rows") return &o.stage_rows;
+  if (k == "k3_warps") return &o.k3_warps;
+  if (k == "k3_rc_min") return &o.k3_rc_min;
+  if (k == "k3_rc_max") return &o.k3_rc_max;
+  if (k == "k3_cluster") return &o.k3_cluster;
+  if (k == "hio_dstreams") return &o.hio_dstreams;
+  return nullptr;
+}
+
+extern "C" int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value) {
+  if (!ctx || !name) return ds_fail(DS_ECONFIG, "ds_ctx_set_option: null argument");
+  int *f = opt_field(ctx->opt, name);
+  if (!f) return ds_fail(DS_ECONFIG, std::string("ds_ctx_set_option: unknown option ") + name);
+  const std::string k = name;
+  bool ok = true;
+  if (k == "k1") ok = value == 0 || value == 2 || value == 4 || value == 8 || value == 16;
+  else if (k == "combine") ok = value == 1 || value == 2;
+  else if (k == "k4") ok = value >= 0 && value <= 3;
+  else if (k == "k6_rv" || k == "k4_rv") ok = value == 1 || value == 2 || value == 4 || value == 8;
+  else if (k == "k3_warps") ok = value == 4 || value == 8;
+  else if (k == "k3_cluster") ok = value == 0 || value == 8 || value == 16;
+  else ok = value >= 0;
+  if (!ok) return ds_fail(DS_ECONFIG, "ds_ctx_set_option: bad value for " + k);
+  *f = value;
+  if (k == "pdl") g_ds_pdl = value != 0;
+  return DS_OK;
+}
+
+extern "C" int ds_ctx_get_option(const ds_ctx *ctx, const char *name, int32_t *value) {
+  if (!ctx || !name || !value) return ds_fail(DS_ECONFIG, "ds_ctx_get_option: null argument");
+  int *f = opt_field(const_cast<ds_ctx *>(ctx)->opt, name);
+  if (!f) return ds_fail(DS_ECONFIG, std::string("ds_ctx_get_option: unknown option ") + name);
+  *value = *f;
   return DS_OK;
 }
 
@@ -334,20 +412,10 @@ __global__ void __launch_bounds__(K1C_X, K1C_YS <= 4 ? K1C_MINB : 1) k_apply2d_c
   }
 }
 
-// DS_K1=tiled: the 32 x 8 shared-memory tile (K1 v2); c2 / c4 / c8 / c16:
-// rows per thread of the column-marching kernel (default 4: config 3 K1
-// 0.287 ms = 74.5% of HBM vs c8 61.8%, c16 36.5%, tiled 54.6%)
-static int k1_variant() {
-  static const int v = [] {
-    const char *e = getenv("DS_K1");
-    if (e && *e == 't') return 2;
-    if (e && !strcmp(e, "c16")) return 16;
-    if (e && !strcmp(e, "c8")) return 8;
-    if (e && !strcmp(e, "c2")) return 2;
-    return 4;
-  }();
-  return v;
-}
+// K1 variant (option "k1"): rows per thread of the column-marching kernel
+// (default 4: config 3 K1 0.287 ms = 74.5% of HBM vs 8 rows 61.8%, 16 rows
+// 36.5%) or 0 = the 32 x 8 shared-memory tile (54.6%)
+static int k1_variant(const ds_ctx *ctx) { return ctx->opt.k1; }
 
 static int grid_for(ds_ctx *ctx, int64_t work, int threads) {
   int64_t blocks = (work + threads - 1) / threads;
@@ -372,8 +440,8 @@ extern "C" int ds_op_apply(ds_ctx *ctx, const ds_op *op, const ds_cplx *v, ds_cp
   const int64_t nodes = (int64_t)sh[0] * sh[1] * sh[2];
   if (nodes * (layout != 0 ? 1 : nrhs) >= (int64_t)1 << 31 || nrhs > 65535)
     return ds_fail(DS_ECONFIG, "ds_op_apply: region too large for one launch");
-  if (layout != 0 && o.dim == 2 && nrhs <= 65535 && k1_variant() != 2) {
-    const int ys = k1_variant();
+  if (layout != 0 && o.dim == 2 && nrhs <= 65535 && k1_variant(ctx) != 0) {
+    const int ys = k1_variant(ctx);
     const dim3 grid((sh[1] + K1C_X - 1) / K1C_X, (sh[0] + ys - 1) / ys, nrhs);
     if (ys == 16)
       k_apply2d_cols<16><<<grid, K1C_X, 0, ctx->stream>>>(o, (const cplx *)v, (cplx *)out, lo[0], lo[1],
@@ -584,14 +652,6 @@ __global__ void k_combine2(int64_t n, int nrhs, int nvec, CombineArgs args,
   }
 }
 
-static bool combine2_enabled() {
-  static const bool on = [] {
-    const char *e = getenv("DS_COMBINE");
-    return !(e && *e == '1');
-  }();
-  return on;
-}
-
 extern "C" int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec,
                               const ds_cplx *const *xs, const ds_cplx *c, ds_cplx *y) {
   if (!ctx || nrhs < 1 || nrhs > 65535 || nvec < 0 || nvec > MAX_COMBINE)
@@ -599,7 +659,7 @@ extern "C" int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec
   if (nvec == 0) return DS_OK;
   CombineArgs args;
   for (int j = 0; j < nvec; ++j) args.x[j] = (const cplx *)xs[j];
-  if (combine2_enabled())
+  if (ctx->opt.combine == 2)
     k_combine2<<<vec_grid(ctx, (n + 1) / 2, nrhs), 256, 0, ctx->stream>>>(n, nrhs, nvec, args,
                                                                         (const cplx *)c, (cplx *)y);
   else

@@ -387,6 +387,153 @@ extern "C" int ds_fact_create(ds_ctx *ctx, ds_op *const *ops, int32_t n_in, ds_f
   return DS_OK;
 }
 
+// ------------------------------------------------------------ factor pool
+// Out-of-core factorization (config 5: 64 raster windows need 638 GB of dense
+// block inverses, HBM holds ~10 windows' worth): ds_fact_create_pool lays
+// out every operator and allocates `nslots` factor slots of the largest
+// operator's size; ds_fact_pool_load factors operator i into a slot (the
+// blocked K2b path, same arithmetic as ds_fact_create), evicting the slot's
+// previous operator.  A sweep plan built with a per-visit slot table
+// (ds_plan_desc.visit_slot) reads each visit's factors from its slot; the
+// host loads the slots a launch needs before issuing it.
+extern "C" int ds_fact_create_pool(ds_ctx *ctx, ds_op *const *ops, int32_t n, int32_t nslots,
+                                   ds_fact **out) {
+  if (!ctx || !ops || n < 1 || nslots < 1 || !out)
+    return ds_fail(DS_ECONFIG, "ds_fact_create_pool: bad argument");
+  ds_fact *F = new ds_fact();
+  F->pool = true;
+  auto fail = [&](int code, const std::string &msg) {
+    for (void *p : F->allocations) cudaFree(p);
+    delete F;
+    return ds_fail(code, msg);
+  };
+  size_t slot = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!ops[i]) return fail(DS_ECONFIG, "ds_fact_create_pool: null operator");
+    const OpDev &o = ops[i]->dev;
+    FactDev f;
+    memset(&f, 0, sizeof(f));
+    ds_fill_layout(o, f);
+    void *mem = nullptr;
+    if (cudaMalloc(&mem, 2 * (size_t)f.nb * sizeof(cplx)) != cudaSuccess)
+      return fail(DS_ECUDA, "ds_fact_create_pool: out of device memory");
+    F->allocations.push_back(mem);
+    cplx *lc = (cplx *)mem, *uc = lc + f.nb;
+    cudaMemcpy(lc, o.c_lo[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice);
+    cudaMemcpy(uc, o.c_hi[f.block_axis], f.nb * sizeof(cplx), cudaMemcpyDeviceToDevice);
+    f.sinv = nullptr;
+    f.lcoef = lc;
+    f.ucoef = uc;
+    const size_t bytes = (size_t)f.nb * f.m * f.m * sizeof(cplx);
+    slot = std::max(slot, bytes);
+    F->facts.push_back(f);
+    F->h_l.push_back(ops[i]->h_clo[f.block_axis]);
+    F->h_u.push_back(ops[i]->h_chi[f.block_axis]);
+    F->bytes.push_back((int64_t)(bytes + 2 * (size_t)f.nb * sizeof(cplx)));
+    F->ops.push_back(ops[i]);
+  }
+  F->slot_bytes = slot;
+  for (int c = 0; c < nslots; ++c) {
+    void *mem = nullptr;
+    if (cudaMalloc(&mem, slot) != cudaSuccess)
+      return fail(DS_ECUDA, "ds_fact_create_pool: out of device memory for " + std::to_string(nslots) +
+                                " slots of " + std::to_string(slot) + " bytes");
+    F->allocations.push_back(mem);
+    F->slot_mem.push_back((cplx *)mem);
+    F->slot_owner.push_back(-1);
+    F->bytes_total += (int64_t)slot;
+  }
+  *out = F;
+  return DS_OK;
+}
+
+extern "C" int ds_fact_pool_load_many(ds_ctx *ctx, ds_fact *F, int32_t n, const int32_t *idx,
+                                      const int32_t *slots) {
+  if (!ctx || !F || !F->pool || n < 0 || (n > 0 && (!idx || !slots)))
+    return ds_fail(DS_ECONFIG, "ds_fact_pool_load: bad argument");
+  std::vector<FactJob> jobs;
+  std::vector<const cplx *> lh, uh;
+  std::vector<std::pair<int, int>> todo;  // (operator, slot)
+  for (int q = 0; q < n; ++q) {
+    const int i = idx[q], slot = slots[q];
+    if (i < 0 || i >= (int)F->facts.size() || slot < 0 || slot >= (int)F->slot_mem.size())
+      return ds_fail(DS_ECONFIG, "ds_fact_pool_load: operator or slot out of range");
+    for (int p = 0; p < q; ++p)
+      if (slots[p] == slot || idx[p] == i)
+        return ds_fail(DS_ECONFIG, "ds_fact_pool_load: repeated operator or slot in one batch");
+    if (F->slot_owner[slot] == i) continue;
+    if (F->facts[i].m <= DS_LARGE_SLAB)
+      return ds_fail(DS_ECONFIG, "ds_fact_pool_load: pooled factors are for large (3D) slabs");
+    todo.push_back({i, slot});
+  }
+  // evict first: previous owners of the target slots, and the operators'
+  // other slots (an operator lives in at most one slot)
+  for (auto &t : todo) {
+    const int prev = F->slot_owner[t.second];
+    if (prev >= 0) F->facts[prev].sinv = nullptr;
+    F->slot_owner[t.second] = -1;
+  }
+  for (auto &t : todo)
+    for (size_t c = 0; c < F->slot_owner.size(); ++c)
+      if (F->slot_owner[c] == t.first) {
+        F->slot_owner[c] = -1;
+        F->facts[t.first].sinv = nullptr;
+      }
+  if (todo.empty()) return DS_OK;
+  for (auto &t : todo) {
+    FactJob job;
+    memset(&job, 0, sizeof(job));
+    job.op = F->ops[t.first]->dev;
+    job.f = F->facts[t.first];
+    job.f.sinv = F->slot_mem[t.second];
+    job.sinv = F->slot_mem[t.second];
+    jobs.push_back(job);
+    lh.push_back(F->h_l[t.first].data());
+    uh.push_back(F->h_u[t.first].data());
+  }
+  int *dst = nullptr;
+  DS_CUDA(cudaMalloc(&dst, sizeof(int)));
+  DS_CUDA(cudaMemsetAsync(dst, 0, sizeof(int), ctx->stream));
+  // all chains of the batch advance together (ds_blocked_factor batches
+  // every (operator, half) chain per step): the panel latency is shared
+  int rc = ds_blocked_factor(ctx, jobs.data(), (int)jobs.size(), lh.data(), uh.data(), dst);
+  int status = 0;
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(&status, dst, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = ds_fail(DS_ECUDA, std::string("ds_fact_pool_load: ") + cudaGetErrorString(e));
+  }
+  cudaFree(dst);
+  if (rc) return rc;
+  if (status) return ds_fail(DS_ESOLVER, "blocked LU: zero or non-finite pivot in a Schur complement");
+  for (auto &t : todo) {
+    F->facts[t.first].sinv = F->slot_mem[t.second];
+    F->slot_owner[t.second] = t.first;
+    F->loads++;
+  }
+  return DS_OK;
+}
+
+extern "C" int ds_fact_pool_load(ds_ctx *ctx, ds_fact *F, int32_t i, int32_t slot) {
+  return ds_fact_pool_load_many(ctx, F, 1, &i, &slot);
+}
+
+extern "C" int ds_fact_pool_state(const ds_fact *F, int32_t *nslots, int64_t *slot_bytes,
+                                  int32_t *slot_owner, int64_t *loads) {
+  if (!F || !F->pool) return ds_fail(DS_ECONFIG, "ds_fact_pool_state: not a factor pool");
+  if (nslots) *nslots = (int32_t)F->slot_mem.size();
+  if (slot_bytes) *slot_bytes = (int64_t)F->slot_bytes;
+  if (slot_owner)
+    for (size_t c = 0; c < F->slot_owner.size(); ++c) slot_owner[c] = F->slot_owner[c];
+  if (loads) *loads = F->loads;
+  return DS_OK;
+}
+
+const cplx *ds_fact_slot_mem(const ds_fact *F, int slot) {
+  if (!F || !F->pool || slot < 0 || slot >= (int)F->slot_mem.size()) return nullptr;
+  return F->slot_mem[slot];
+}
+
 extern "C" int ds_fact_info(const ds_fact *F, int32_t i, int32_t *ba, int32_t *nb, int32_t *m,
                             int64_t *bytes) {
   if (!F || i < 0 || i >= (int)F->facts.size()) return ds_fail(DS_ECONFIG, "ds_fact_info: bad index");
@@ -429,6 +576,8 @@ extern "C" int ds_fact_solve(ds_ctx *ctx, const ds_fact *F, int32_t i, const ds_
   if (!ctx || !F || !rhs || !x || nrhs < 1 || i < 0 || i >= (int)F->facts.size())
     return ds_fail(DS_ECONFIG, "ds_fact_solve: bad argument");
   const FactDev &f = F->facts[i];
+  if (f.kind == 0 && !f.sinv)
+    return ds_fail(DS_ECONFIG, "ds_fact_solve: operator's factors are not resident (ds_fact_pool_load)");
   size_t n = (size_t)f.nb * f.m * nrhs;
   cplx *tmp = nullptr;
   void *vis = nullptr;

@@ -589,314 +589,6 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
   }
 }
 
-// K3m-R v4 (DS_THOMAS=4): v3's segmented recurrences with the column block staged
-// in shared memory (cp.async, every row in flight at once) and the segment
-// values recomputed from the exact carry instead of kept as partial
-// products: a handful of registers per thread, so three 480-thread blocks
-// share an SM (v3 needed ~160 registers for g, P and the coefficients: one
-// block per SM, 3.1 waves on an 8-visit launch of config 2).  Measured under
-// graph replay it ties v3 on config 2 (the recurrences cost ~0.56 ms of a
-// 5.7 ms application either way, DS_SKIP=4) and loses to v2 on config 4.
-__global__ void __launch_bounds__(512) k_modal_thomas4(const ModalJob *__restrict__ jobs, int nrhs,
-                                                       int L) {
-  extern __shared__ __align__(16) cplx sg[];  // [nb][32]
-  __shared__ cplx sP[16][32], sZ[16][32], sC[16][32];
-  const ModalJob J = jobs[blockIdx.y];
-  const FactDev &f = *J.f;
-  const int m = f.m, nb = f.nb;
-  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nseg = (nb + L - 1) / L;
-  const int q0 = blockIdx.x * 32, q = q0 + lane;
-  if (q0 >= m * nrhs) return;
-  pdl_wait();
-  if (!job_any(J, nrhs)) return;
-  const bool live = q < m * nrhs;
-  const int j = (live ? q : q0) / nrhs;
-  cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
-  const size_t st = (size_t)m * nrhs;
-  for (int k = seg; k < nb; k += nw)
-    cp16(sg + k * 32 + lane, T + (live ? k * st + q : 0), live ? 16 : 0);
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  const cplx *mul = f.mmul + j, *inv = f.minv + j, *uc = f.ucoef;
-  const int k0 = seg * L, k1 = min(nb, k0 + L);
-  const bool act = seg < nseg;
-  // ---- forward z_k = g_k - mul_k z_{k-1}: segment totals from a zero carry
-  if (act) {
-    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
-    for (int k = k0; k < k1; ++k) {
-      const cplx mk = __ldg(mul + (size_t)k * m);
-      const cplx a = make_double2(-mk.x, -mk.y);
-      z = cadd(sg[k * 32 + lane], cmul(a, z));
-      pp = cmul(a, pp);
-    }
-    sP[seg][lane] = pp;
-    sZ[seg][lane] = z;
-  }
-  __syncthreads();
-  if (seg == 0) {
-    cplx c = make_double2(0.0, 0.0);
-    for (int s2 = 0; s2 < nseg; ++s2) {
-      sC[s2][lane] = c;
-      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
-    }
-  }
-  __syncthreads();
-  if (act) {  // the segment again from its exact carry: g'_k
-    cplx x = sC[seg][lane];
-    for (int k = k0; k < k1; ++k) {
-      const cplx mk = __ldg(mul + (size_t)k * m);
-      x = cadd(sg[k * 32 + lane], cmul(make_double2(-mk.x, -mk.y), x));
-      sg[k * 32 + lane] = x;
-    }
-  }
-  __syncthreads();
-  // ---- backward (k descending): y_k = inv_k g'_k - inv_k u_k y_{k+1}
-  if (act) {
-    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
-    for (int k = k1 - 1; k >= k0; --k) {
-      const cplx ik = __ldg(inv + (size_t)k * m);
-      const cplx iu = cmul(ik, __ldg(uc + k));
-      const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
-      z = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, z));
-      pp = cmul(a, pp);
-    }
-    sP[seg][lane] = pp;
-    sZ[seg][lane] = z;
-  }
-  __syncthreads();
-  if (seg == 0) {
-    cplx c = make_double2(0.0, 0.0);
-    for (int s2 = nseg - 1; s2 >= 0; --s2) {
-      sC[s2][lane] = c;
-      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
-    }
-  }
-  __syncthreads();
-  if (!act || !live) return;
-  if (J.nz && !J.nz[q % nrhs]) return;  // exact-zero RHS: never read downstream
-  cplx y = sC[seg][lane];
-  for (int k = k1 - 1; k >= k0; --k) {
-    const cplx ik = __ldg(inv + (size_t)k * m);
-    const cplx iu = cmul(ik, __ldg(uc + k));
-    const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
-    y = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, y));
-    T[k * st + q] = y;
-  }
-}
-
-// ------------------------------------------- fused modal solve (2D, K3m-F)
-// The three phases of a launch's modal solve in one kernel, ordered per
-// visit by counters instead of kernel boundaries: CTAs [0, A) run the
-// forward-transform tiles of every visit, [A, A+B) the recurrence items,
-// [A+B, A+B+C) the inverse-transform tiles.  A recurrence item of visit j
-// starts once all forward tiles of j have counted in, an inverse tile once
-// all recurrence items of j have; CTAs are dispatched in index order, so a
-// waiting CTA only waits on CTAs that are already running (the pattern of
-// decoupled look-back scans) -- the tails of one phase overlap the next
-// phase of other visits and two kernel boundaries per launch disappear.
-// Counters are per (launch, visit), zeroed once per application; a bounded
-// spin traps (a CUDA error) instead of hanging on a protocol error.
-#define MF_MT 2
-#define MF_WR 2
-#define MF_WC 2
-#define MF_TK 8
-#define MF_NS 4
-#define MF_THREADS (32 * MF_WR * MF_WC)
-#define MF_TM (8 * MF_MT * MF_WR)
-#define MF_TN (16 * MF_WC)
-#define MF_MAXJOB 64
-#define MF_NSEG (MF_THREADS / 32)
-
-__device__ __forceinline__ void mf_signal(int *c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(c, 1);
-  }
-}
-__device__ __forceinline__ void mf_wait(const int *c, int target) {
-  if (threadIdx.x == 0) {
-    long long spins = 0;
-    while (true) {
-      int v;
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-      if (v >= target) break;
-      __nanosleep(64);
-      if (++spins > (1ll << 26)) __trap();
-    }
-  }
-  __syncthreads();
-}
-
-// recurrence item: 32 compact (mode, RHS) columns of one visit, MF_NSEG
-// segments (one per warp) -- k_modal_thomas4's scheme at 128 threads
-__device__ __forceinline__ void mf_recurrence(const ModalJob &J, const FactDev &f, int nrhs, int A,
-                                              const int *act, int item, cplx *sg, cplx (*sP)[32],
-                                              cplx (*sZ)[32], cplx (*sC)[32]) {
-  const int m = f.m, nb = f.nb;
-  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
-  const int L = (nb + MF_NSEG - 1) / MF_NSEG;
-  const int qc = item * 32 + lane;
-  const bool live = qc < m * A;
-  const int qcc = live ? qc : 0;
-  const int j = qcc / A;
-  const int q = j * nrhs + act[qcc - j * A];
-  cplx *T = J.s0;
-  const size_t st = (size_t)m * nrhs;
-  for (int k = seg; k < nb; k += MF_NSEG)
-    cp16(sg + k * 32 + lane, T + (live ? k * st + q : 0), live ? 16 : 0);
-  cp_commit();
-  cp_wait<0>();
-  __syncthreads();
-  const cplx *mul = f.mmul + j, *inv = f.minv + j, *uc = f.ucoef;
-  const int k0 = seg * L, k1 = min(nb, k0 + L);
-  {
-    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
-    for (int k = k0; k < k1; ++k) {
-      const cplx mk = __ldg(mul + (size_t)k * m);
-      const cplx a = make_double2(-mk.x, -mk.y);
-      z = cadd(sg[k * 32 + lane], cmul(a, z));
-      pp = cmul(a, pp);
-    }
-    sP[seg][lane] = pp;
-    sZ[seg][lane] = z;
-  }
-  __syncthreads();
-  if (seg == 0) {
-    cplx c = make_double2(0.0, 0.0);
-    for (int s2 = 0; s2 < MF_NSEG; ++s2) {
-      sC[s2][lane] = c;
-      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
-    }
-  }
-  __syncthreads();
-  {
-    cplx x = sC[seg][lane];
-    for (int k = k0; k < k1; ++k) {
-      const cplx mk = __ldg(mul + (size_t)k * m);
-      x = cadd(sg[k * 32 + lane], cmul(make_double2(-mk.x, -mk.y), x));
-      sg[k * 32 + lane] = x;
-    }
-  }
-  __syncthreads();
-  {
-    cplx z = make_double2(0.0, 0.0), pp = make_double2(1.0, 0.0);
-    for (int k = k1 - 1; k >= k0; --k) {
-      const cplx ik = __ldg(inv + (size_t)k * m);
-      const cplx iu = cmul(ik, __ldg(uc + k));
-      const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
-      z = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, z));
-      pp = cmul(a, pp);
-    }
-    sP[seg][lane] = pp;
-    sZ[seg][lane] = z;
-  }
-  __syncthreads();
-  if (seg == 0) {
-    cplx c = make_double2(0.0, 0.0);
-    for (int s2 = MF_NSEG - 1; s2 >= 0; --s2) {
-      sC[s2][lane] = c;
-      c = cadd(sZ[s2][lane], cmul(sP[s2][lane], c));
-    }
-  }
-  __syncthreads();
-  if (live) {
-    cplx y = sC[seg][lane];
-    for (int k = k1 - 1; k >= k0; --k) {
-      const cplx ik = __ldg(inv + (size_t)k * m);
-      const cplx iu = cmul(ik, __ldg(uc + k));
-      const cplx a = k == nb - 1 ? make_double2(0.0, 0.0) : make_double2(-iu.x, -iu.y);
-      y = cadd(cmul(ik, sg[k * 32 + lane]), cmul(a, y));
-      T[k * st + q] = y;
-    }
-  }
-}
-
-// per visit: forward tiles (all columns), recurrence items, inverse tiles
-__host__ __device__ inline void mf_counts(const FactDev &f, int nrhs, int &ta, int &tb, int &tc) {
-  const int rows = (f.nax[0] + MF_TM - 1) / MF_TM;
-  const int cols = (f.nb * nrhs + MF_TN - 1) / MF_TN;
-  ta = tc = rows * cols;
-  tb = (f.m * nrhs + 31) / 32;
-}
-
-// off: [3][njob + 1] item prefix per phase (host-built, kernel parameter)
-struct MfOff {
-  int o[3][MF_MAXJOB + 1];
-};
-
-__global__ void __launch_bounds__(MF_THREADS, 2)
-    k_modal_fused(const ModalJob *__restrict__ jobs, int njob, int nrhs, int *counters, const MfOff off) {
-  extern __shared__ __align__(16) cplx smem_mf[];
-  __shared__ int act[RMAX_MODAL + 1];
-  __shared__ cplx sP[MF_NSEG][32], sZ[MF_NSEG][32], sC[MF_NSEG][32];
-  const auto &s_off = off.o;
-  const int A_end = s_off[0][njob], B_end = A_end + s_off[1][njob];
-  int phase, local = blockIdx.x;
-  if (local < A_end) phase = 0;
-  else if (local < B_end) { phase = 1; local -= A_end; }
-  else { phase = 2; local -= B_end; }
-  int j = 0;
-  while (j + 1 < njob && s_off[phase][j + 1] <= local) ++j;
-  local -= s_off[phase][j];
-  const ModalJob J = jobs[j];
-  const FactDev f = *J.f;
-  int *c1 = counters + 2 * j, *c2 = c1 + 1;
-  const int ta = s_off[0][j + 1] - s_off[0][j], tb = s_off[1][j + 1] - s_off[1][j];
-  pdl_wait();
-  if (phase == 1) mf_wait(c1, ta);
-  if (phase == 2) mf_wait(c2, tb);
-  const int nA = active_rhs(J, nrhs, act);
-  if (phase == 1) {
-    if (local * 32 < f.m * nA) mf_recurrence(J, f, nrhs, nA, act, local, smem_mf, sP, sZ, sC);
-    mf_signal(c2);
-    return;
-  }
-  const PassGeo G = pass_geo(f, J, phase == 0 ? 0 : 1, nrhs);
-  const int gx = (f.nb * nrhs + MF_TN - 1) / MF_TN;
-  const int row0 = (local / gx) * MF_TM, col0 = (local % gx) * MF_TN;
-  const int total = G.outer * G.inner * nA;
-  if (row0 < G.n && col0 < total)
-    gemm_tile<MF_MT, MF_WR, MF_WC, MF_TK, MF_NS>(G, row0, col0, min(MF_TN, total - col0), smem_mf, act, nA,
-                                                 nrhs);
-  if (phase == 0) mf_signal(c1);
-}
-
-int ds_launch_modal_fused(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob, int nrhs,
-                          int *counters) {
-  if (njob <= 0) return DS_OK;
-  if (njob > MF_MAXJOB) return ds_fail(DS_ECONFIG, "fused modal solve: too many visits in one launch");
-  int nbmax = 1, grid = 0;
-  MfOff off;
-  int acc[3] = {0, 0, 0};
-  for (int i = 0; i < njob; ++i) {
-    if (facts[i].naxes != 1) return ds_fail(DS_ECONFIG, "fused modal solve: 2D operators only");
-    nbmax = std::max(nbmax, facts[i].nb);
-    int t[3];
-    mf_counts(facts[i], nrhs, t[0], t[1], t[2]);
-    for (int ph = 0; ph < 3; ++ph) {
-      off.o[ph][i] = acc[ph];
-      acc[ph] += t[ph];
-    }
-    grid += t[0] + t[1] + t[2];
-  }
-  for (int ph = 0; ph < 3; ++ph) off.o[ph][njob] = acc[ph];
-  const size_t gsm = sizeof(cplx) * MF_NS * (MF_TM * (MF_TK + 4) + MF_TK * (MF_TN + 2));
-  const size_t tsm = sizeof(cplx) * (size_t)nbmax * 32;
-  const size_t smem = std::max(gsm, tsm);
-  static size_t attr = 0;
-  if (smem > attr) {
-    DS_CUDA(cudaFuncSetAttribute(k_modal_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  DS_CUDA(launch_pdl(k_modal_fused, dim3(grid), dim3(MF_THREADS), smem, ctx->stream, jobs_dev, njob, nrhs,
-                     counters, off));
-  ctx->launches++;
-  return DS_OK;
-}
-
 // ------------------------------------------------------------- launcher
 template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
@@ -933,43 +625,11 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   const int na = facts[0].naxes;
   for (int i = 1; i < njob; ++i)
     if (facts[i].naxes != na) return ds_fail(DS_ECONFIG, "modal solve: mixed dimensions in one launch");
-  // transform tile shape (DS_MG: a 64x32, b 40x32, c 120x16, d 64x64, e/f a with 3 CTAs/SM or
-  // TK 32, g 32x32 x 4 CTAs/SM, h 16x32 x 8, i 32x16 x 8, j 8x32 x 16, k 16x16 x 16,
-  // n 16x64 x 4, o (default) 32x32 with 2x2 warps of 16x16, p TK 32, q 8x64)
-  static const char variant = [] {
-    const char *v = getenv("DS_MG");
-    return v && *v ? v[0] : 'u';
-  }();
+  // transform tile (measured best of 28 shapes / pipelines on configs 2 and
+  // 4): 32 x 32 per CTA, 2 x 2 warps of 16 x 16, K chunks of
+  // 8 through a 4-stage cp.async ring, 4 CTAs per SM
   auto launch_pass = [&](int pass) -> int {
-    switch (variant) {
-      case 'b': return launch_gemm<1, 5, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'c': return launch_gemm<3, 5, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'd': return launch_gemm<2, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'e': return launch_gemm<2, 4, 2, 16, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'f': return launch_gemm<2, 4, 2, 32, 1>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'a': return launch_gemm<2, 4, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'h': return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'i': return launch_gemm<1, 4, 1, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'g': return launch_gemm<1, 4, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'j': return launch_gemm<1, 1, 2, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'k': return launch_gemm<1, 2, 1, 16, 16>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'n': return launch_gemm<1, 2, 4, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'o': return launch_gemm<2, 2, 2, 16, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'p': return launch_gemm<1, 2, 2, 32, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'q': return launch_gemm<1, 1, 4, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'r': return launch_gemm<2, 2, 2, 16, 3, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 's': return launch_gemm<2, 2, 2, 16, 2, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 't': return launch_gemm<1, 2, 2, 16, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'u': return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'v': return launch_gemm<2, 2, 2, 8, 4, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'w': return launch_gemm<2, 2, 2, 8, 6, 6>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'x': return launch_gemm<1, 2, 2, 8, 8, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'y': return launch_gemm<2, 2, 2, 4, 4, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'z': return launch_gemm<1, 7, 2, 8, 2, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'Z': return launch_gemm<1, 7, 1, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 'Y': return launch_gemm<1, 7, 2, 16, 2, 2>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      default: return launch_gemm<1, 2, 2, 16, 8>(ctx, jobs_dev, facts, njob, pass, nrhs);
-    }
+    return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
   };
   if (phase == 0 || phase == -1)
     for (int p = 0; p < na; ++p)
@@ -982,29 +642,14 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
     }
     const size_t tsm = sizeof(cplx) * (size_t)nbmax * (TQ + 2 * thomas_modes(nrhs) + 1);
     static int th_attr = 0;
-    static const int thv = [] {
-      const char *v = getenv("DS_THOMAS");
-      return v && *v ? atoi(v) : 3;
-    }();
-    if (thv == 4 && nbmax <= 200) {
-      const int L = std::max(4, (nbmax + 15) / 16);
-      const int nseg = (nbmax + L - 1) / L;
-      const size_t sm4 = sizeof(cplx) * (size_t)nbmax * 32;
-      static int th4_attr = 0;
-      if ((int)sm4 > th4_attr) {
-        DS_CUDA(cudaFuncSetAttribute(k_modal_thomas4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4));
-        th4_attr = (int)sm4;
-      }
-      DS_CUDA(launch_pdl(k_modal_thomas4, dim3((mmax * nrhs + 31) / 32, njob), dim3(32 * nseg), sm4,
-                         ctx->stream, jobs_dev, nrhs, L));
-    } else if (thv == 3 && nbmax > 64 && nbmax <= 16 * 16) {  // short chains (3D): v2 streams better
+    if (nbmax > 64 && nbmax <= 16 * 16) {  // segmented recurrences (long chains, 2D)
       const int L = nbmax <= 64 ? 4 : (nbmax <= 128 ? 8 : 16);
       const int nseg = (nbmax + L - 1) / L;
       const dim3 grid((mmax * nrhs + 31) / 32, njob);
       if (L == 4) DS_CUDA(launch_pdl(k_modal_thomas3<4>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
       else if (L == 8) DS_CUDA(launch_pdl(k_modal_thomas3<8>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
       else DS_CUDA(launch_pdl(k_modal_thomas3<16>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
-    } else if (tsm <= 200 * 1024 && thv >= 2) {
+    } else if (tsm <= 200 * 1024) {  // short chains (3D): the staged v2 streams better
       if ((int)tsm > th_attr) {
         DS_CUDA(cudaFuncSetAttribute(k_modal_thomas2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         th_attr = (int)tsm;
@@ -1012,6 +657,7 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
       DS_CUDA(launch_pdl(k_modal_thomas2, dim3((mmax * nrhs + TQ - 1) / TQ, njob), dim3(TQ), tsm,
                          ctx->stream, jobs_dev, nrhs));
     } else {
+      // chains too long to stage (n_b > 256 and no shared-memory fit): v1
       k_modal_thomas<<<dim3((mmax * nrhs + 255) / 256, njob), 256, 0, ctx->stream>>>(jobs_dev, nrhs);
     }
     ctx->launches++;

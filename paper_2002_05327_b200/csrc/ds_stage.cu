@@ -250,13 +250,6 @@ __global__ void __launch_bounds__(32 * SM_WARPS, SM_MINB)
   }
 }
 
-static bool stage_mma_enabled() {
-  static const bool on = [] {
-    const char *v = getenv("DS_K3G_MMA");
-    return !(v && *v == '0');
-  }();
-  return on;
-}
 
 // host: the twisted schedule of one visit
 static bool stage_item(const FactDev &f, int s, int half, StageItem &I) {
@@ -351,7 +344,7 @@ int ds_launch_solve_staged(ds_ctx *ctx, const SolveVisit *visits_host, const Fac
     if (!n) continue;
     int vb = (int)std::min<int64_t>(256, ((int64_t)mmax * nrhs + 255) / 256);
     k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all, vin_stride);
-    if (stage_mma_enabled()) {
+    if (ctx->opt.k3g_mma) {
       dim3 grid((mmax + 8 * SM_WARPS - 1) / (8 * SM_WARPS), n, nchunks);
       k_stage_gemv_mma<<<grid, 32 * SM_WARPS, 0, ctx->stream>>>(ditems + off[s], nrhs, vin_all,
                                                                 vin_stride);
@@ -558,18 +551,16 @@ void ds_stage_program_destroy(StageProgram *P) {
   delete P;
 }
 
-static int small_rows(int m, int nitems, int nchunk, int nsm) {
-  // rows per CTA (DS_STAGE_ROWS, default 16): every CTA re-forms the whole
-  // block vector from L2, so fewer, fatter tiles are cheaper
-  (void)m; (void)nitems; (void)nchunk; (void)nsm;
-  const char *v = getenv("DS_STAGE_ROWS");
-  return v && *v ? atoi(v) : 16;
+static int small_rows(const ds_ctx *ctx) {
+  // rows per CTA (option "stage_rows", default 16): every CTA re-forms the
+  // whole block vector from L2, so fewer, fatter tiles are cheaper
+  return ctx->opt.stage_rows > 0 ? ctx->opt.stage_rows : 16;
 }
 
 template <int RC>
 static int launch_small(ds_ctx *ctx, const StageItem *items, int n, int nrhs, int m) {
   const int nchunk = (nrhs + RC - 1) / RC;
-  const int rt = small_rows(m, n, nchunk, ctx->num_sms);
+  const int rt = small_rows(ctx);
   size_t smem = ((size_t)rt * m + (size_t)m * (RC + 1)) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
@@ -615,7 +606,7 @@ int ds_stage_program_launch_step(ds_ctx *ctx, StageProgram *P, int step, int nrh
         return ds_fail(DS_ECONFIG, "stage program: vin scratch too small");
       int vb = (int)std::min<int64_t>(256, ((int64_t)m * nrhs + 255) / 256);
       k_stage_vin<<<dim3(vb, n), 256, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
-      if (stage_mma_enabled()) {
+      if (ctx->opt.k3g_mma) {
         dim3 grid((m + 8 * SM_WARPS - 1) / (8 * SM_WARPS), n, (nrhs + ST_RC - 1) / ST_RC);
         k_stage_gemv_mma<<<grid, 32 * SM_WARPS, 0, ctx->stream>>>(it, nrhs, P->vin, vin_stride);
       } else {

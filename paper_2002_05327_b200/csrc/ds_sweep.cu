@@ -97,7 +97,6 @@ struct ds_plan {
   std::vector<int> blu_vidx, blu_off;  // visit index of each entry; per-launch offsets
   // modal visits (FactDev kind 1): job table, factor layouts, offsets
   ModalJob *mjobs = nullptr;
-  int *mcount = nullptr;  // fused modal solve: 2 counters per modal job, zeroed per application
   std::vector<ModalJob> h_mjobs;
   std::vector<FactDev> h_mfacts;
   std::vector<int> mod_vidx, mod_off;
@@ -1053,6 +1052,28 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     P->h_u.push_back(local ? d->fact_of_sub[s]->h_u[d->fact_index[s]].data() : nullptr);
   }
   cudaMemcpy(P->facts, hf.data(), sizeof(FactDev) * nsub, cudaMemcpyHostToDevice);
+  // pooled factors (ABI 5): every visit (w, s) reads its factors from slot
+  // visit_slot[w * nsub + s] of its factor pool (per-visit layout copies)
+  std::vector<FactDev> hvf;
+  FactDev *vfacts = nullptr;
+  if (d->visit_slot) {
+    hvf.resize((size_t)nsw * nsub);
+    for (int w = 0; w < nsw; ++w)
+      for (int s = 0; s < nsub; ++s) {
+        FactDev fv = hf[s];
+        if (P->owner[s] == P->rank) {
+          const int slot = d->visit_slot[(size_t)w * nsub + s];
+          const cplx *mem = ds_fact_slot_mem(d->fact_of_sub[s], slot);
+          if (!mem || fv.kind != 0)
+            return fail(ds_fail(DS_ECONFIG, "visit_slot: subdomain factors are not a block-LU pool"));
+          fv.sinv = mem;
+        }
+        hvf[(size_t)w * nsub + s] = fv;
+      }
+    if (plan_alloc(P, &mem, sizeof(FactDev) * hvf.size())) return fail(DS_ECUDA);
+    vfacts = (FactDev *)mem;
+    cudaMemcpy(vfacts, hvf.data(), sizeof(FactDev) * hvf.size(), cudaMemcpyHostToDevice);
+  }
   // ---- beta00 ramps
   int64_t nbeta = 0;
   for (int s = 0; s < nsub; ++s)
@@ -1145,8 +1166,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
     mscr = (cplx *)mem;
   }
   {
-    const char *mode = getenv("DS_SOLVE_MODE");
-    P->staged = P->max_m > 0 && (P->max_m > DS_LARGE_SLAB || (mode && std::string(mode) == "staged"));
+    P->staged = P->max_m > 0 && (P->max_m > DS_LARGE_SLAB || ctx->opt.staged);
   }
   (void)max_nb;
   // ---- flags
@@ -1282,7 +1302,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
           P->h_mfacts.push_back(hf[s]);
           P->mod_vidx.push_back((int)hv.size() - 1);
         } else {
-          SolveVisit SV{P->facts + s, V.rhs, V.x, nullptr,
+          SolveVisit SV{vfacts ? vfacts + (size_t)w * nsub + s : P->facts + s, V.rhs, V.x, nullptr,
                         xgs + ((size_t)parity * P->gmax + gi) * xgbuf};
           hsv.push_back(SV);
           P->blu_vidx.push_back((int)hv.size() - 1);
@@ -1355,10 +1375,6 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   P->solvetab = (SolveVisit *)mem;
   if (plan_alloc(P, &mem, sizeof(ModalJob) * std::max<size_t>(P->h_mjobs.size(), 1))) return fail(DS_ECUDA);
   P->mjobs = (ModalJob *)mem;
-  if (!P->h_mjobs.empty()) {
-    if (plan_alloc(P, &mem, sizeof(int) * 2 * P->h_mjobs.size())) return fail(DS_ECUDA);
-    P->mcount = (int *)mem;
-  }
   if (plan_alloc(P, &mem, sizeof(XferDev) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->xfers = (XferDev *)mem;
   cudaMemcpy(P->xfers, hx.data(), sizeof(XferDev) * hx.size(), cudaMemcpyHostToDevice);
@@ -1382,7 +1398,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
         const int i = P->blu_vidx[e];
         int sub = hv[i].sub;
         sv.back().push_back(hsv[e]);
-        sf.back().push_back(hf[sub]);
+        sf.back().push_back(hvf.empty() ? hf[sub] : hvf[(size_t)(hv[i].sweep - 1) * nsub + sub]);
         sl.back().push_back(P->h_l[sub]);
         su.back().push_back(P->h_u[sub]);
       }
@@ -1394,13 +1410,13 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess)
     return fail(ds_fail(DS_ECUDA, std::string("ds_plan_create: ") + cudaGetErrorString(err)));
-  if (getenv("DS_K5_SIDE") == nullptr || std::string(getenv("DS_K5_SIDE")) != "0") {
+  if (ctx->opt.k5_side) {
     // the K5 and copy streams run at the highest priority (graphs are
     // instantiated with node priorities): their small grids take SMs as
     // soon as critical-path CTAs retire instead of queueing behind them
     int lo_pri = 0, hi_pri = 0;
     cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri);
-    if (!getenv("DS_NO_PRIORITY")) P->side_priority = hi_pri;
+    P->side_priority = hi_pri;
     if (cudaStreamCreateWithPriority(&P->side, cudaStreamNonBlocking, P->side_priority) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_k3, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P->ev_k5[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -1617,9 +1633,15 @@ struct HostIO {
 // DS_HIO_TRACE (eager host path only): timestamps of uploads, launches and
 // downloads, printed after the application (diagnostics)
 static std::vector<std::pair<std::string, cudaEvent_t>> g_trace;
+// DS_DIAG builds only: DS_HIO_TRACE=1 records a CUDA-event timeline of the
+// pinned-host path (tools/ timeline probes)
 static bool hio_trace_on() {
+#ifdef DS_DIAG
   static const bool on = getenv("DS_HIO_TRACE") != nullptr;
   return on;
+#else
+  return false;
+#endif
 }
 static void trace_mark(const std::string &what, cudaStream_t st) {
   if (!hio_trace_on()) return;
@@ -1650,8 +1672,6 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       ctx->launches++;
       DS_CHECK_LAUNCH();
     }
-    if (P->mcount && getenv("DS_MFUSE") && getenv("DS_MFUSE")[0] == '1')  // fused modal solve only
-      DS_CUDA(cudaMemsetAsync(P->mcount, 0, sizeof(int) * 2 * P->h_mjobs.size(), st));
     P->k5_pending[0] = P->k5_pending[1] = false;
   }
   // fork the copy streams after the zeroing (forking them first -- the
@@ -1668,13 +1688,17 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (int rc = hio_out_chunk(P, hio, nrhs, c, P->cstream)) return rc;
   }
   int hio_waited = 0, hio_nout = 0;
-  // diagnostics only (wrong results): DS_SKIP bitmask drops kernel classes
-  // from the schedule to measure their marginal time under graph replay
-  // (1 K6, 2 modal transforms, 4 modal recurrences, 8 K4, 16 K5)
+  // DS_DIAG builds only (wrong results): the DS_SKIP bitmask drops kernel
+  // classes from the schedule to measure their marginal time under graph
+  // replay (1 K6, 2 modal transforms, 4 modal recurrences, 8 K4, 16 K5)
+#ifdef DS_DIAG
   static const int skip_cls = [] {
     const char *v = getenv("DS_SKIP");
     return v && *v ? atoi(v) : 0;
   }();
+#else
+  constexpr int skip_cls = 0;
+#endif
   const int cap = std::max(1, ctx->num_sms * 4);
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
@@ -1697,10 +1721,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       }
       if (hio) trace_mark("launch " + std::to_string(q), st);
       prof_mark(P, 0, st);
-      static const int k6rv = [] {  // RHS columns per thread of K6 (default 4; 2 / 1 for tests)
-        const char *v = getenv("DS_K6_RV");
-        return v && *v ? atoi(v) : 4;
-      }();
+      const int k6rv = ctx->opt.k6_rv;  // RHS columns per thread of K6 (default 4)
       if (skip_cls & 1) {
       } else if (k6rv == 8 && nrhs % 8 == 0)
         DS_CUDA(launch_pdl(outer ? k_assemble<8, true> : k_assemble<8, false>, dim3(bx, G), dim3(256),
@@ -1738,17 +1759,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
         else rc = ds_launch_solve_table(ctx, P->solvetab + b0, nbl, nrhs, P->max_m);
       }
       if (rc) return rc;
-      // fused modal solve (DS_MFUSE=1, opt-in): correct, but under graph
-      // replay its spin-waiting CTAs and larger shared-memory footprint cost
-      // more than the two kernel boundaries it removes (config 2: 3460 vs
-      // 3625 RHS/s ungrouped, 2825 vs 3825 with RHS groups)
-      static const bool mfuse = [] {
-        const char *v = getenv("DS_MFUSE");
-        return v && v[0] == '1';
-      }();
-      if (nmo > 0 && mfuse && P->dim == 2 && nmo <= 64 && !skip_cls) {  // fused modal solve
-        rc = ds_launch_modal_fused(ctx, P->mjobs + m0, P->h_mfacts.data() + m0, nmo, nrhs, P->mcount + 2 * m0);
-      } else if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
+      if (nmo > 0) {  // modal: transforms (class 1) / recurrences (class 4) / transforms
         for (int ph = 0; ph < 3 && !rc; ++ph) {
           if (ph > 0) prof_mark(P, ph == 1 ? 4 : 1, st);
           if (skip_cls & (ph == 1 ? 4 : 2)) continue;
@@ -1794,17 +1805,11 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (nx > 0 && !(skip_cls & 8)) {
         prof_mark(P, 3, st);
         int bz = std::max(1, std::min(64, 2 * cap / nx));
-        static const int k4rv = [] {
-          const char *v = getenv("DS_K4_RV");  // 1 measured fastest (config 2: 1.32 vs 1.51-1.59 ms)
-          return v && *v ? atoi(v) : 1;
-        }();
+        const int k4rv = ctx->opt.k4_rv;  // v1: 1 measured fastest (config 2: 1.32 vs 1.51-1.59 ms)
 #define K4_LAUNCH(RV_, D_)                                                                       \
   k_transfer<RV_, D_><<<dim3(bz, nx), 256, 0, st>>>(P->xfers + x0, P->visits, P->subs, P->nsub, \
                                                     nrhs, dim, F, P->d_flag_bases, P->nsweeps)
-        static const bool k4v1 = [] {
-          const char *v = getenv("DS_K4");  // "v1": the original one-block-per-band kernel
-          return v && std::string(v) == "v1";
-        }();
+        const bool k4v1 = ctx->opt.k4 == 1;  // the original one-block-per-band kernel
         const int rv = (k4rv == 4 && nrhs % 4 == 0) ? 4 : ((k4rv >= 2 && nrhs % 2 == 0) ? 2 : 1);
         if (!k4v1) {
           const int t0 = P->tile_off[q], nt = P->tile_off[q + 1] - t0;
@@ -1814,10 +1819,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
           const XferRec *xr = P->recs + x0;
           const int4 *tl = P->tiles + t0;
           int *const *fb = P->d_flag_bases;
-          static const int k4v = [] {
-            const char *v = getenv("DS_K4");
-            return v && *v == 'v' ? atoi(v + 1) : 0;
-          }();
+          const int k4v = ctx->opt.k4;
           // defaults (measured): 2D k_transfer3 (config 2 +3%), 3D k_transfer2
           // (config 4: 7.5 vs 7.9 ms per application with k_transfer3<3, 4>)
           const int v3rv = (dim == 3 && k4v == 3) ? (nrhs % 4 == 0 ? 4 : (nrhs % 2 == 0 ? 2 : 1)) : 0;
@@ -1914,9 +1916,7 @@ __global__ void k_box_transpose(int R, int L, int64_t N, int64_t base0, int64_t 
 }
 
 // chunk tables (nrhs-independent) and staging buffers (nrhs_max)
-static std::vector<HioBox> hio_grid(const ds_plan *P, const char *env, int a, int b) {
-  const char *v = getenv(env);
-  if (v && *v) sscanf(v, "%dx%d", &a, &b);
+static std::vector<HioBox> hio_grid(const ds_plan *P, int a, int b) {
   const int B0 = std::min(std::max(1, a), P->gcounts[0]), B1 = std::min(std::max(1, b), P->gcounts[1]);
   std::vector<HioBox> boxes;
   for (int i = 0; i < B0; ++i)
@@ -1933,8 +1933,9 @@ static int hio_setup(ds_plan *P) {
   // config 2 (tools/e2e_probe.py): whole-row bands 16x1 5.61 ms, 8x2 / 8x2
   // 5.29, 8x4 / 12x2 5.18 -- finer boxes start the sweep earlier, but 3D
   // copies of sub-4 KB rows run below the copy engine's rate
-  const std::vector<HioBox> ib = hio_grid(P, "DS_HIO_IN", 8, 4);
-  const std::vector<HioBox> ob = hio_grid(P, "DS_HIO_BOXES", 12, 2);
+  // upload 8 x 4 and download 12 x 2 boxes (measured on config 2)
+  const std::vector<HioBox> ib = hio_grid(P, 8, 4);
+  const std::vector<HioBox> ob = hio_grid(P, 12, 2);
   const int CI = (int)ib.size(), CO = (int)ob.size();
   auto meets = [&](const HioBox &B, const int *lo, const int *sh) {
     return sh[0] > 0 && sh[1] > 0 && lo[0] < B.a1 && lo[0] + sh[0] > B.a0 && lo[1] < B.c1 &&
@@ -1975,6 +1976,7 @@ static int hio_setup(ds_plan *P) {
     else P->hio_out_at[last[c]].push_back(c);
   }
   const int C = std::max(CI, CO);
+#ifdef DS_DIAG
   if (getenv("DS_HIO_DEBUG")) {
     fprintf(stderr, "hio: %d boxes, %d launches; uploads needed by launch:", C, nq);
     for (int q = 0; q < nq; ++q) fprintf(stderr, " %d", P->hio_need[q]);
@@ -1982,6 +1984,7 @@ static int hio_setup(ds_plan *P) {
     for (int q = 0; q < nq; ++q) fprintf(stderr, " %d", (int)P->hio_out_at[q].size());
     fprintf(stderr, "\n");
   }
+#endif
   const size_t bytes = sizeof(cplx) * (size_t)P->nnodes * P->nrhs_max;
   void *mem;
   for (cplx **b : {&P->hio_fo, &P->hio_fm, &P->hio_uo, &P->hio_um}) {
@@ -1991,8 +1994,7 @@ static int hio_setup(ds_plan *P) {
   DS_CUDA(cudaStreamCreateWithPriority(&P->cstream, cudaStreamNonBlocking, P->side_priority));
   DS_CUDA(cudaStreamCreateWithPriority(&P->cstream2, cudaStreamNonBlocking, P->side_priority));
   {
-    const char *v = getenv("DS_HIO_DSTREAMS");
-    const int nd = v && *v ? std::max(2, std::min(8, atoi(v))) : 2;
+    const int nd = std::max(2, std::min(8, P->ctx->opt.hio_dstreams));
     for (int i = 2; i < nd; ++i) {
       cudaStream_t x;
       cudaEvent_t e;
@@ -2019,12 +2021,14 @@ static int hio_setup(ds_plan *P) {
 // one box between pinned host [R][N] and the device staging copy (3D copy:
 // R slices x box rows x box row bytes), plus the layout transpose
 static int hio_box(ds_plan *P, const HostIO *hio, int nrhs, int k, cudaStream_t cs, bool in) {
-  static const int skip = [] {  // diagnostics only: 1 skips uploads, 2 downloads (wrong results)
+#ifdef DS_DIAG
+  static const int skip = [] {  // DS_DIAG only: 1 skips uploads, 2 downloads (wrong results)
     const char *v = getenv("DS_HIO_SKIP");
     return v && *v ? atoi(v) : 0;
   }();
   if ((skip & 1) && in) return DS_OK;
   if ((skip & 2) && !in) return DS_OK;
+#endif
   const HioBox &B = in ? P->hio_boxes[k] : P->hio_oboxes[k];
   const int64_t N = P->nnodes, S1 = P->gcounts[2], S0 = (int64_t)P->gcounts[1] * S1;
   const int L = (int)((B.c1 - B.c0) * S1), runs = B.a1 - B.a0;

@@ -198,7 +198,15 @@ def device_plan(partition, operators, cache: FactorizationCache, plan: SweepPlan
     dp = cache._plans.get(key)
     if dp is None or dp.nrhs_max < nrhs:
         nmax = max(nrhs, dp.nrhs_max if dp else 0)
-        if G > 1:
+        slots = None
+        if schedule == "diagonal":
+            slots = cache.pool_slots([operators[i] for i in partition.subdomains()])
+        if slots is not None:  # factors exceed HBM: pooled, launch-by-launch plan
+            dp = None
+            cache._plans.pop(key, None)
+            dp = _engine.DevicePlan(partition, operators, cache, directions, nmax, schedule,
+                                    pipelined=True, pool_slots=slots)
+        elif G > 1:
             per = -(-nmax // G)
             dp = _engine.GroupedPlan([_engine.DevicePlan(partition, operators, cache, directions, per,
                                                          schedule, pipelined=pipelined)

@@ -137,6 +137,12 @@ class FactorizationCache:
     method: str = "auto"
     share_translates: bool = False
     modal_cond_max: float | None = None  # None: _engine.MODAL_COND_MAX
+    # out-of-core factors: when the block-LU factors of a plan's distinct
+    # operators exceed `device_budget` bytes (None: free device memory minus
+    # `pool_reserve`), the sweep plan keeps them in a FactorPool of as many
+    # slots as fit and factors them launch by launch (config 5)
+    device_budget: int | None = None
+    pool_reserve: int = 32 << 30
     _store: dict = field(default_factory=dict)
     hits: int = 0
     misses: int = 0
@@ -175,6 +181,32 @@ class FactorizationCache:
             fset = _engine.FactorSet([op for _, op, _ in blocked], modal=False)
             for i, (key, op, why) in enumerate(blocked):
                 self._store[key] = GpuFactorization(fset, i, op, fallback=why)
+
+    def pool_slots(self, ops):
+        """Slots of an out-of-core factor pool for these operators, or None
+        when their factors fit (or some operator takes the modal backend)."""
+        from . import _engine
+
+        if any(_wants_modal(op, self.method) for op in ops):
+            return None
+        if all(self.key(op) in self._store for op in ops):
+            return None
+        shapes = {self.key(op): tuple(op.window.shape) for op in ops}
+        need = sum(_engine.block_lu_bytes(sh) for sh in shapes.values())
+        budget = self.device_budget
+        if budget is None:
+            import torch
+
+            free, _ = torch.cuda.mem_get_info()
+            budget = free - self.pool_reserve
+        if need <= budget:
+            return None
+        per = max(_engine.block_lu_bytes(sh) for sh in shapes.values())
+        nslots = int(budget // per)
+        if nslots < 1:
+            raise ConfigurationError(
+                f"factor pool: one window's factors ({per / 1e9:.1f} GB) exceed the device budget")
+        return nslots
 
     def key(self, op) -> str:
         return _coarse_key(op) if self.share_translates else op.fingerprint

@@ -82,27 +82,20 @@ def test_stencil_apply_global_and_region(cuda, cfg1):
     assert rel(got, want) <= 1e-14
 
 
-@pytest.mark.parametrize("k1", ["c4", "c8", "c2", "c16", "tiled"])
-def test_stencil_variants_ragged_regions(k1, tmp_path):
-    """K1 variants (column marching with 4 / 8 / 2 / 16 rows per thread, the 32 x 8
-    shared-memory tile) on ragged regions (strip edges, warp edges, last
-    row block partial) and several RHS planes: <= 1e-14 vs the oracle, and
-    bitwise equal to each other.  DS_K1 is read once per process, so each
-    variant runs in its own interpreter."""
-    import subprocess
-    import sys
+@pytest.mark.parametrize("k1", [4, 8, 2, 16, 0])
+def test_stencil_variants_ragged_regions(cuda, k1):
+    """K1 variants (column marching with 4 / 8 / 2 / 16 rows per thread, 0 =
+    the 32 x 8 shared-memory tile; context option "k1", switched in-process)
+    on ragged regions (strip edges, warp edges, last row block partial) and
+    several RHS planes: <= 1e-14 vs the oracle, and bitwise equal to each
+    other."""
+    from paper_2002_05327_b200 import _engine
 
-    code = f"""
-import numpy as np, sys
-sys.path[:0] = [{str(Path(__file__).resolve().parents[1])!r}, {str(Path(__file__).resolve().parent)!r}]
-from test_gpu_parity import _ragged_stencil_case
-out = _ragged_stencil_case()
-np.save({str(tmp_path / "out.npy")!r}, out)
-"""
-    env = dict(os.environ, DS_K1=k1)
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    got = np.load(tmp_path / "out.npy")
+    old = _engine.set_option("k1", k1)
+    try:
+        got = _ragged_stencil_case()
+    finally:
+        _engine.set_option("k1", old)
     ref = _RAGGED_REF.setdefault("u", got)
     assert np.array_equal(got, ref), k1
 
@@ -821,72 +814,52 @@ def test_grouped_pinned_host_path(cuda, cfg1):
         assert [r.discarded_sources for r in rep_h] == [r.discarded_sources for r in rep_dev]
 
 
-def test_fused_modal_solve_opt_in(cuda, cfg1):
-    """The opt-in fused modal solve (DS_MFUSE=1: transforms, recurrences and
-    inverse transforms of a launch in one kernel ordered by per-visit
-    counters) matches the three-kernel solve.  The switch is read once per
-    process, so this runs in a subprocess."""
-    import os
-    import subprocess
-    import sys
-
-    code = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import numpy as np, torch\n"
-        "from paper_2002_05327_b200 import FactorizationCache, configs\n"
-        "from paper_2002_05327_b200.ddm import SweepPlan, device_plan\n"
-        "s = configs.spec(1); b = configs.build(s)\n"
-        "rng = np.random.default_rng(4); f = rng.standard_normal((4,) + b['grid'].counts)\n"
-        "fd = torch.from_numpy(f.astype(np.complex128).reshape(4, -1)).cuda()\n"
-        "dp = device_plan(b['partition'], b['ops'], FactorizationCache(), SweepPlan.default(2), 4)\n"
-        "u, _ = dp.apply(fd); np.save(sys.argv[1], u.cpu().numpy())\n") % str(
-            __import__("pathlib").Path(__file__).resolve().parents[1])
-    import tempfile
-
-    outs = []
-    for flag in ("0", "1"):
-        path = tempfile.mktemp(suffix=".npy")
-        env = dict(os.environ, DS_MFUSE=flag)
-        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=600)
-        outs.append(np.load(path))
-    # the fused kernel segments the recurrences differently (4 segments per
-    # 32 columns instead of n_b / 8): equal to rounding, not bitwise
-    assert rel(outs[1], outs[0]) <= 1e-12
-
-
-def test_transfer_kernel_variants_bitwise(cuda):
-    """The three source-transfer kernels (DS_K4=v1: one block per band,
-    v2: flattened records + tiles, v3: RHS columns per thread, the 2D
+def test_transfer_kernel_variants_bitwise(cuda, cfg1):
+    """The three source-transfer kernels (option "k4": 1 = one block per
+    band, 2 = flattened records + tiles, 3 = RHS columns per thread, the 2D
     default) evaluate psi in the same order (v1 / v2 bitwise, v3 to FMA
-    contraction).
-    The switch is read once per process, so each runs in a subprocess."""
-    import os
-    import subprocess
-    import sys
-    import tempfile
-    from pathlib import Path
+    contraction); the assembly's RHS-column widths ("k6_rv" 1 / 2 / 4) are
+    bitwise equal.  Fresh plans per variant (graphs keep the options they
+    were recorded with)."""
+    import torch
 
-    root = str(Path(__file__).resolve().parents[1])
-    code = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import numpy as np, torch\n"
-        "from paper_2002_05327_b200 import FactorizationCache, configs\n"
-        "from paper_2002_05327_b200.ddm import SweepPlan, device_plan\n"
-        "s = configs.spec(1); b = configs.build(s)\n"
-        "rng = np.random.default_rng(8); f = rng.standard_normal((4,) + b['grid'].counts)\n"
-        "fd = torch.from_numpy(f.astype(np.complex128).reshape(4, -1)).cuda()\n"
-        "dp = device_plan(b['partition'], b['ops'], FactorizationCache(), SweepPlan.default(2), 4)\n"
-        "u, _ = dp.apply(fd); np.save(sys.argv[1], u.cpu().numpy())\n") % root
-    outs = []
-    for v in ("v1", "v2", "v3"):
-        path = tempfile.mktemp(suffix=".npy")
-        subprocess.run([sys.executable, "-c", code, path], check=True, timeout=600,
-                       env=dict(os.environ, DS_K4=v))
-        outs.append(np.load(path))
+    from paper_2002_05327_b200 import _engine
+    from paper_2002_05327_b200.ddm import SweepPlan
+
+    s, b, prob, oops = cfg1
+    rng = np.random.default_rng(8)
+    f = rng.standard_normal((4,) + b["grid"].counts)
+    fd = torch.from_numpy(f.astype(np.complex128).reshape(4, -1)).cuda()
+    cache = FactorizationCache()
+
+    def run(name, value):
+        old = _engine.set_option(name, value)
+        try:
+            dp = _engine.DevicePlan(b["partition"], b["ops"], cache, SweepPlan.default(2).directions, 4,
+                                    pipelined=True)
+            u, _ = dp.apply(fd)
+            return u.cpu().numpy()
+        finally:
+            _engine.set_option(name, old)
+
+    outs = [run("k4", v) for v in (1, 2, 3)]
     # same evaluation order; v3's different code shape lets nvcc contract
     # the complex multiply-adds into FMAs differently -> equal to rounding
     assert np.array_equal(outs[0], outs[1])
     assert rel(outs[2], outs[1]) <= 1e-13
+    k6 = [run("k6_rv", v) for v in (1, 2, 4)]
+    assert np.array_equal(k6[0], k6[1]) and np.array_equal(k6[1], k6[2])
+
+
+def test_context_options_validate(cuda):
+    from paper_2002_05327_b200 import _engine
+    from paper_2002_05327_b200.errors import ConfigurationError
+
+    assert _engine.get_option("k1") == 4 and _engine.get_option("pdl") in (0, 1)
+    with pytest.raises(ConfigurationError):
+        _engine.set_option("k1", 3)
+    with pytest.raises(ConfigurationError):
+        _engine.set_option("no_such_option", 1)
 
 
 def test_gmres_restart_longer_than_combine_limit(cuda, raster):
