@@ -360,6 +360,22 @@ DS_API int ds_plan_slot(ds_ctx *ctx, const ds_plan *plan, int32_t use_sweep, int
                         int32_t dir, int32_t *lo, int32_t *shape, ds_cplx *out_dev,
                         int64_t out_elems, int32_t nrhs);
 
+/* Cross-rank device barrier of a sharded sweep (ABI 5): rank `rank` of
+ * `nranks` owns an arrival array (ds_barrier_info: device pointer + bytes, to
+ * be mapped by its peers); ds_barrier_set_peers takes every rank's array
+ * (index = rank, local / peer / IPC-mapped pointers); ds_barrier_wait
+ * enqueues the barrier on the context stream: all prior work of this rank is
+ * made visible system-wide, then it waits on the device until every rank has
+ * arrived at the same generation.  Replaces a per-launch collective between
+ * the launches of ds_ddm_apply_range. */
+typedef struct ds_barrier ds_barrier;
+DS_API int ds_barrier_create(ds_ctx *ctx, int32_t nranks, int32_t rank, ds_barrier **out);
+DS_API int ds_barrier_info(const ds_barrier *b, void **arrive, int64_t *bytes);
+DS_API int ds_barrier_set_peers(ds_barrier *b, int32_t nranks, void *const *arrive);
+DS_API int ds_barrier_wait(ds_ctx *ctx, ds_barrier *b);
+DS_API int64_t ds_barrier_generation(const ds_barrier *b);
+DS_API int ds_barrier_destroy(ds_barrier *b);
+
 /* ---------------------------------------------------------- vector kernels
  * Batched complex vector ops for GMRES (krylov.py:80, :97-106, :139-142);
  * vectors are RHS-outer [nrhs][n] (the reference's batch layout), one
@@ -386,6 +402,16 @@ DS_API int ds_vec_combine(ds_ctx *ctx, int64_t n, int32_t nrhs, int32_t nvec,
  * the normalisations V[0] = r/beta and V[k+1] = w/norm_w of krylov.py */
 DS_API int ds_vec_scale(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *x_dev,
                  const double *s_dev, ds_cplx *y_dev);
+
+/* out[r] = b[r] - w[r] and norm_out[r] = ||out[r]||_2 in one pass (the
+ * residual r = b - A x of krylov.py:80, :140-141; ABI 5). */
+DS_API int ds_vec_sub_norm(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *b_dev,
+                           const ds_cplx *w_dev, ds_cplx *out_dev, double *norm_out_dev);
+/* Row gather / scatter of RHS-outer batches (ABI 5): dst[r] = src[map[r]]
+ * for r < ndst, zero where map[r] < 0 (device int32 map) -- the active-row
+ * selection of the batched GMRES. */
+DS_API int ds_vec_rows(ds_ctx *ctx, int64_t n, int32_t ndst, const int32_t *map_dev,
+                       const ds_cplx *src_dev, ds_cplx *dst_dev);
 
 /* RHS-outer [R][n] <-> RHS-minor [n][R] layout conversion. */
 DS_API int ds_layout_to_minor(ds_ctx *ctx, int64_t n, int32_t nrhs,

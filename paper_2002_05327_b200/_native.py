@@ -121,12 +121,20 @@ _SIGNATURES = [
     ("ds_ddm_apply_range", C.c_int, [vp, vp, vp, vp, i32, i32, i32, i32]),
     ("ds_plan_set_profiling", C.c_int, [vp, i32]),
     ("ds_plan_kernel_times", C.c_int, [vp, P_f64, P_i64, i32]),
+    ("ds_barrier_create", C.c_int, [vp, i32, i32, C.POINTER(vp)]),
+    ("ds_barrier_info", C.c_int, [vp, C.POINTER(vp), P_i64]),
+    ("ds_barrier_set_peers", C.c_int, [vp, i32, C.POINTER(vp)]),
+    ("ds_barrier_wait", C.c_int, [vp, vp]),
+    ("ds_barrier_generation", i64, [vp]),
+    ("ds_barrier_destroy", C.c_int, [vp]),
     ("ds_vec_dot", C.c_int, [vp, i64, i32, vp, vp, vp]),
     ("ds_vec_norm", C.c_int, [vp, i64, i32, vp, vp]),
     ("ds_vec_axpy", C.c_int, [vp, i64, i32, vp, C.c_double, vp, vp]),
     ("ds_vec_axpy_dot", C.c_int, [vp, i64, i32, vp, vp, vp, vp, vp]),
     ("ds_vec_combine", C.c_int, [vp, i64, i32, i32, C.POINTER(vp), vp, vp]),
     ("ds_vec_scale", C.c_int, [vp, i64, i32, vp, vp, vp]),
+    ("ds_vec_sub_norm", C.c_int, [vp, i64, i32, vp, vp, vp, vp]),
+    ("ds_vec_rows", C.c_int, [vp, i64, i32, vp, vp, vp]),
     ("ds_layout_to_minor", C.c_int, [vp, i64, i32, vp, vp]),
     ("ds_layout_to_outer", C.c_int, [vp, i64, i32, vp, vp]),
 ]

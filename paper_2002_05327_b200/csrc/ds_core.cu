@@ -493,7 +493,8 @@ __device__ __forceinline__ cplx block_reduce(cplx v, cplx *red) {
   return red[0];
 }
 
-// MODE 0: vdot(x, y); 1: |x|^2; 2: y -= a_prev*xprev then vdot(x, y)
+// MODE 0: vdot(x, y); 1: |x|^2; 2: y -= a_prev*xprev then vdot(x, y);
+// 3: y = x - xprev then |y|^2 (the residual r = b - A x and its norm)
 template <int MODE>
 __global__ void __launch_bounds__(VEC_THREADS)
     k_vec_reduce(int64_t n, const cplx *__restrict__ x, cplx *y, const cplx *__restrict__ a_prev,
@@ -507,7 +508,11 @@ __global__ void __launch_bounds__(VEC_THREADS)
   if (MODE == 2 && xprev) s = a_prev[r];
   for (int64_t i = i0 + threadIdx.x; i < i1; i += VEC_THREADS) {
     cplx a = x[base + i];
-    if (MODE == 1) {
+    if (MODE == 3) {
+      a = csub(a, xprev[base + i]);
+      y[base + i] = a;
+    }
+    if (MODE == 1 || MODE == 3) {
       acc.x = fma(a.x, a.x, acc.x);
       acc.x = fma(a.y, a.y, acc.x);
     } else {
@@ -549,8 +554,10 @@ static int reduction_launch(ds_ctx *ctx, int mode, int64_t n, int nrhs, const cp
     k_vec_reduce<0><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, nullptr, nullptr, partials, chunk);
   else if (mode == 1)
     k_vec_reduce<1><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, nullptr, nullptr, partials, chunk);
-  else
+  else if (mode == 2)
     k_vec_reduce<2><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, a_prev, xprev, partials, chunk);
+  else
+    k_vec_reduce<3><<<grid, VEC_THREADS, 0, ctx->stream>>>(n, x, y, nullptr, xprev, partials, chunk);
   k_reduce_final<<<ceil_div(nrhs, 128), 128, 0, ctx->stream>>>(B, nrhs, partials, out_c, out_norm);
   ctx->launches += 2;
   DS_CHECK_LAUNCH();
@@ -589,6 +596,38 @@ __global__ void k_axpy(int64_t n, const cplx *__restrict__ a, double sgn,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[base + i] = cadd(y[base + i], cmul(s, x[base + i]));
+}
+
+extern "C" int ds_vec_sub_norm(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds_cplx *b,
+                               const ds_cplx *w, ds_cplx *out, double *norm_out) {
+  if (!ctx || !b || !w || !out || !norm_out) return ds_fail(DS_ECONFIG, "ds_vec_sub_norm: null argument");
+  return reduction_launch(ctx, 3, n, nrhs, (const cplx *)b, (cplx *)out, nullptr, (const cplx *)w,
+                          nullptr, norm_out);
+}
+
+// rows of RHS-outer batches: dst[r] = src[map[r]] for map[r] >= 0, else 0
+// (gather: map = selected rows; scatter into the full batch: map = inverse)
+__global__ void k_rows_map(int64_t n, const int *__restrict__ map, const cplx *__restrict__ src,
+                           cplx *__restrict__ dst) {
+  const int r = blockIdx.y;
+  const int q = map[r];
+  const cplx *s = q >= 0 ? src + (int64_t)q * n : nullptr;
+  cplx *d = dst + (int64_t)r * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s ? s[i] : make_double2(0.0, 0.0);
+}
+
+static dim3 vec_grid(ds_ctx *ctx, int64_t n, int nrhs);
+
+extern "C" int ds_vec_rows(ds_ctx *ctx, int64_t n, int32_t ndst, const int32_t *map_dev,
+                           const ds_cplx *src, ds_cplx *dst) {
+  if (!ctx || !map_dev || !src || !dst || ndst < 0 || ndst > 65535)
+    return ds_fail(DS_ECONFIG, "ds_vec_rows: bad argument");
+  if (ndst == 0 || n == 0) return DS_OK;
+  k_rows_map<<<vec_grid(ctx, n, ndst), 256, 0, ctx->stream>>>(n, map_dev, (const cplx *)src, (cplx *)dst);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
 }
 
 static dim3 vec_grid(ds_ctx *ctx, int64_t n, int nrhs) {
@@ -737,4 +776,90 @@ extern "C" int ds_layout_to_outer(ds_ctx *ctx, int64_t n, int32_t nrhs, const ds
   if (!ctx || src == dst) return ds_fail(DS_ECONFIG, "ds_layout_to_outer: bad argument");
   // src [n][R] -> dst [R][n]
   return transpose(ctx, n, nrhs, (const cplx *)src, (cplx *)dst);
+}
+
+// ------------------------------------------------------ cross-rank barrier
+// Device-side barrier of a subdomain-sharded sweep (sharded.py): every rank
+// owns an arrival array arrive[nranks] (uint64 generations) in its memory,
+// mapped by its peers (NVLink P2P / CUDA IPC).  ds_barrier_wait enqueues one
+// single-warp kernel: after a system-scope fence (the previous kernels'
+// peer writes -- payloads, arrival flags -- become visible first), lane r
+// stores the generation into arrive[rank] of rank r's array (release, system
+// scope), then spins until its own arrive[r] reaches the generation
+// (acquire).  No host round trip and no NCCL call between launches; the
+// spin is bounded (~10 s of clock64) and traps instead of hanging.
+struct ds_barrier {
+  int nranks, rank;
+  unsigned long long *arrive;            // own array, device memory
+  unsigned long long **peers = nullptr;  // device table of every rank's array
+  unsigned long long gen = 0;
+};
+
+__global__ void k_peer_barrier(unsigned long long *const *peers, unsigned long long *own, int nranks,
+                               int rank, unsigned long long gen) {
+  const int r = threadIdx.x;
+  __threadfence_system();
+  if (r < nranks) {
+    unsigned long long *dst = peers[r] + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(dst), "l"(gen) : "memory");
+    unsigned long long v = 0;
+    const long long t0 = clock64();
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(own + r) : "memory");
+      if (v >= gen) break;
+      if (clock64() - t0 > (1LL << 34)) __trap();  // a peer never arrived
+    } while (true);
+  }
+  __syncwarp();
+}
+
+extern "C" int ds_barrier_create(ds_ctx *ctx, int32_t nranks, int32_t rank, ds_barrier **out) {
+  if (!ctx || !out || nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
+    return ds_fail(DS_ECONFIG, "ds_barrier_create: bad argument");
+  ds_barrier *B = new ds_barrier();
+  B->nranks = nranks;
+  B->rank = rank;
+  if (cudaMalloc(&B->arrive, sizeof(unsigned long long) * nranks) != cudaSuccess ||
+      cudaMemset(B->arrive, 0, sizeof(unsigned long long) * nranks) != cudaSuccess ||
+      cudaMalloc(&B->peers, sizeof(void *) * nranks) != cudaSuccess) {
+    cudaFree(B->arrive);
+    delete B;
+    return ds_fail(DS_ECUDA, "ds_barrier_create: allocation failed");
+  }
+  *out = B;
+  return DS_OK;
+}
+
+extern "C" int ds_barrier_info(const ds_barrier *B, void **arrive, int64_t *bytes) {
+  if (!B) return ds_fail(DS_ECONFIG, "null barrier");
+  if (arrive) *arrive = B->arrive;
+  if (bytes) *bytes = (int64_t)sizeof(unsigned long long) * B->nranks;
+  return DS_OK;
+}
+
+extern "C" int ds_barrier_set_peers(ds_barrier *B, int32_t nranks, void *const *arrive) {
+  if (!B || !arrive || nranks != B->nranks) return ds_fail(DS_ECONFIG, "ds_barrier_set_peers: bad argument");
+  for (int r = 0; r < nranks; ++r)
+    if (!arrive[r]) return ds_fail(DS_ECONFIG, "ds_barrier_set_peers: null peer array");
+  DS_CUDA(cudaMemcpy(B->peers, arrive, sizeof(void *) * nranks, cudaMemcpyHostToDevice));
+  return DS_OK;
+}
+
+extern "C" int ds_barrier_wait(ds_ctx *ctx, ds_barrier *B) {
+  if (!ctx || !B) return ds_fail(DS_ECONFIG, "ds_barrier_wait: null argument");
+  ++B->gen;
+  k_peer_barrier<<<1, 32, 0, ctx->stream>>>(B->peers, B->arrive, B->nranks, B->rank, B->gen);
+  ctx->launches++;
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+extern "C" int64_t ds_barrier_generation(const ds_barrier *B) { return B ? (int64_t)B->gen : -1; }
+
+extern "C" int ds_barrier_destroy(ds_barrier *B) {
+  if (!B) return DS_OK;
+  cudaFree(B->arrive);
+  cudaFree(B->peers);
+  delete B;
+  return DS_OK;
 }

@@ -103,6 +103,18 @@ class _Vec:
             N.check(self.lib.ds_vec_combine(self.ctx, self.n, y.shape[0], len(part), arr,
                                             c[j0:j0 + step].data_ptr(), y.data_ptr()))
 
+    def sub_norm(self, b, w, out, norms):
+        """out = b - w, norms = ||out|| per row, one pass (ds_vec_sub_norm)."""
+        self._bind()
+        N.check(self.lib.ds_vec_sub_norm(self.ctx, self.n, b.shape[0], b.data_ptr(), w.data_ptr(),
+                                         out.data_ptr(), norms.data_ptr()))
+
+    def rows(self, mapping, src, dst):
+        """dst[r] = src[mapping[r]] (0 where mapping[r] < 0), ds_vec_rows."""
+        self._bind()
+        N.check(self.lib.ds_vec_rows(self.ctx, self.n, dst.shape[0], mapping.data_ptr(),
+                                     src.data_ptr(), dst.data_ptr()))
+
     def divide(self, x, s, y):
         self._bind()
         N.check(self.lib.ds_vec_scale(self.ctx, self.n, x.shape[0], x.data_ptr(), s.data_ptr(),
@@ -152,9 +164,25 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
     X = torch.zeros_like(B)
     reports = [SolveReport() for _ in range(R)]
 
+    maps = {}
+
+    def row_maps(rows):
+        """(gather map [len(rows)], scatter map [R]) device int32 tables."""
+        key = tuple(rows)
+        if key not in maps:
+            inv = np.full(R, -1, np.int32)
+            inv[list(rows)] = np.arange(len(rows), dtype=np.int32)
+            maps[key] = (torch.as_tensor(np.asarray(rows, np.int32), device=dev),
+                         torch.as_tensor(inv, device=dev))
+        return maps[key]
+
     def call(fn, rows, V):
         """Apply a closure to the rows `rows` of V ([R, n]) -> [len(rows), n]."""
-        sub = V if len(rows) == R else V.index_select(0, torch.as_tensor(rows, device=dev))
+        if len(rows) == R:
+            sub = V
+        else:  # native row gather of the active RHS (ds_vec_rows)
+            sub = torch.empty((len(rows), n), dtype=torch.complex128, device=dev)
+            vec.rows(row_maps(rows)[0], V, sub)
         arg = sub.reshape((len(rows),) + shape) if batched else sub.reshape(shape)
         out = fn(arg)
         if not hasattr(out, "detach"):
@@ -162,11 +190,8 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
         return out.to(dev, torch.complex128).reshape(len(rows), n).contiguous()
 
     def scatter(dst, rows, src):
-        if len(rows) == R:
-            dst.copy_(src)
-        else:
-            dst.zero_()
-            dst.index_copy_(0, torch.as_tensor(rows, device=dev), src)
+        """dst = src on rows `rows`, zero elsewhere (ds_vec_rows)."""
+        vec.rows(row_maps(rows)[1], src, dst)
 
     nb = torch.empty(R, dtype=torch.float64, device=dev)
     vec.norm(B, nb)
@@ -186,7 +211,6 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
             live.append(r)
 
     W = torch.empty_like(B)
-    ones = torch.ones(R, dtype=torch.complex128, device=dev)
     while True:
         cyc = [r for r in live if total[r] < max_iter and residual[r] / norm_b[r] > tol]
         if not cyc:
@@ -194,10 +218,9 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
         # ---- cycle start for the RHS in `cyc`: r = b - A x  (krylov.py:80)
         AX = call(apply_A, cyc, X)
         scatter(W, cyc, AX)
-        Rv = B.clone()
-        vec.axpy(ones, -1.0, W, Rv)  # r = b - A x
+        Rv = torch.empty_like(B)
         beta_d = torch.empty(R, dtype=torch.float64, device=dev)
-        vec.norm(Rv, beta_d)
+        vec.sub_norm(B, W, Rv, beta_d)  # r = b - A x and ||r||, one pass
         beta = beta_d.cpu().numpy()
         m_r = {r: min(restart, max_iter - int(total[r])) for r in cyc}
         m = max(m_r.values())
@@ -238,8 +261,10 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
             vec.axpy(hcol[k], -1.0, V[k], W)
             n1 = torch.empty(R, dtype=torch.float64, device=dev)
             vec.norm(W, n1)
-            n0h, n1h = n0.cpu().numpy(), n1.cpu().numpy()
-            hk = hcol[: k + 1].cpu().numpy()  # [k+1, R]
+            # one device -> host read per Arnoldi step: ||w0||, ||w||, h[:k+1]
+            pack = torch.cat([n0, n1, torch.view_as_real(hcol[: k + 1]).reshape(-1)]).cpu().numpy()
+            n0h, n1h = pack[:R], pack[R:2 * R]
+            hk = pack[2 * R:].view(np.complex128).reshape(k + 1, R)
             reo = [r for r in active if n1h[r] < 0.5 * n0h[r]]
             if reo:
                 sel = torch.zeros(R, dtype=torch.complex128, device=dev)
@@ -307,10 +332,8 @@ def _gmres_core(apply_A, apply_M, bt, shape, batched, is_torch, tol, restart, ma
         # ---- true residual (krylov.py:140-142)
         AX = call(apply_A, cyc, X)
         scatter(W, cyc, AX)
-        Rv = B.clone()
-        vec.axpy(ones, -1.0, W, Rv)
         tr = torch.empty(R, dtype=torch.float64, device=dev)
-        vec.norm(Rv, tr)
+        vec.sub_norm(B, W, Rv, tr)
         trh = tr.cpu().numpy()
         for r in cyc:
             residual[r] = trh[r]

@@ -18,9 +18,12 @@ Two runners share that protocol:
   waits on another).  It exercises the whole sharded data path on one GPU and
   is what the tests check against the unsharded sweep.
 * `DistributedShardedSweep` -- one process per GPU (torch.distributed, NCCL):
-  peers' slot and flag allocations are mapped with CUDA IPC handles exchanged
-  through the process group, and a stream-ordered all-reduce on a token is
-  the barrier between launches.
+  peers' slot, flag and barrier allocations are mapped with CUDA IPC handles
+  exchanged once through the process group; the barrier between launches is
+  a device-side flag barrier in peer memory (`DeviceBarrier`,
+  ds_barrier_wait: one single-warp kernel per launch, no host round trip
+  and no collective); NCCL only sums u at the end.  barrier="nccl" keeps the
+  former stream-ordered all-reduce on a token.
 """
 from __future__ import annotations
 
@@ -108,13 +111,53 @@ class ShardedSweep:
         return _merge_counters([p.counters(nrhs) for p in self.plans])
 
 
+class DeviceBarrier:
+    """Rank `rank` of an `nranks` device-side barrier (ds_barrier_*): its
+    arrival array lives in this rank's memory; `set_peers` takes every
+    rank's array (local, peer or IPC-mapped); `wait()` enqueues the barrier
+    on the current stream."""
+
+    def __init__(self, nranks: int, rank: int):
+        import ctypes as C
+        import weakref
+
+        lib, ctx = _engine.context()
+        out = C.c_void_p()
+        _engine.N.check(lib.ds_barrier_create(ctx, nranks, rank, C.byref(out)), "ds_barrier_create")
+        self.handle = out
+        self.nranks, self.rank = nranks, rank
+        self._finalizer = weakref.finalize(self, lib.ds_barrier_destroy, out)
+
+    def arrive_ptr(self) -> int:
+        import ctypes as C
+
+        p = C.c_void_p()
+        _engine.N.check(_engine.N.load_library().ds_barrier_info(self.handle, C.byref(p), None))
+        return p.value
+
+    def set_peers(self, ptrs):
+        import ctypes as C
+
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        _engine.N.check(_engine.N.load_library().ds_barrier_set_peers(self.handle, len(ptrs), arr),
+                        "ds_barrier_set_peers")
+
+    def wait(self):
+        lib, ctx = _engine.context()
+        _engine.N.check(lib.ds_barrier_wait(ctx, self.handle), "ds_barrier_wait")
+
+    @property
+    def generation(self) -> int:
+        return int(_engine.N.load_library().ds_barrier_generation(self.handle))
+
+
 class DistributedShardedSweep:
     """One process per GPU (torch.distributed with the NCCL backend; see the
     module docstring).  Each rank holds only its owned factorizations; the
     returned u (on every rank) is the all-reduced sum."""
 
     def __init__(self, partition, operators, nrhs_max: int, group=None, cache=None,
-                 plan: SweepPlan | None = None, pipelined: bool = True):
+                 plan: SweepPlan | None = None, pipelined: bool = True, barrier: str = "device"):
         import torch.distributed as dist
 
         from .subdomain import FactorizationCache
@@ -128,11 +171,20 @@ class DistributedShardedSweep:
                                        plan.directions, nrhs_max, pipelined=pipelined,
                                        shard=(self.nranks, self.rank, self.owner))
         slot, _, flags, _ = self.plan.shard_info()
+        if barrier not in ("device", "nccl"):
+            raise ConfigurationError(f"unknown barrier {barrier!r}")
+        self.barrier = DeviceBarrier(self.nranks, self.rank) if barrier == "device" else None
+        mine = [_ipc_handle(slot), _ipc_handle(flags)]
+        if self.barrier is not None:
+            mine.append(_ipc_handle(self.barrier.arrive_ptr()))
         handles = [None] * self.nranks
-        dist.all_gather_object(handles, (_ipc_handle(slot), _ipc_handle(flags)), group=group)
+        dist.all_gather_object(handles, tuple(mine), group=group)
         slots = [slot if r == self.rank else _ipc_open(handles[r][0]) for r in range(self.nranks)]
         flagp = [flags if r == self.rank else _ipc_open(handles[r][1]) for r in range(self.nranks)]
         self.plan.set_peers(slots, flagp)
+        if self.barrier is not None:
+            self.barrier.set_peers([self.barrier.arrive_ptr() if r == self.rank else _ipc_open(handles[r][2])
+                                    for r in range(self.nranks)])
         self.nlaunch = self.plan.nlaunch()
         self.nnodes = self.plan.nnodes
         self._bufs = {}
@@ -147,23 +199,26 @@ class DistributedShardedSweep:
             self._bufs[R] = (fmin, torch.empty_like(fmin))
         fmin, umin = self._bufs[R]
         _engine.N.check(lib.ds_layout_to_minor(ctx, n, R, f.data_ptr(), fmin.data_ptr()))
-        run_protocol(self.plan, fmin, umin, R, self.dist, self.group, device=f.device)
+        run_protocol(self.plan, fmin, umin, R, self.dist, self.group, device=f.device,
+                     barrier=self.barrier.wait if self.barrier is not None else None)
         u = torch.empty((R, n), dtype=torch.complex128, device=f.device)
         _engine.N.check(lib.ds_layout_to_outer(ctx, n, R, umin.data_ptr(), u.data_ptr()))
         return u
 
 
-def run_protocol(plan, fmin, umin, nrhs: int, dist, group=None, device="cuda"):
+def run_protocol(plan, fmin, umin, nrhs: int, dist, group=None, device="cuda", barrier=None):
     """One sharded application on this rank: initialise (zero u and flags),
     barrier (no peer writes into flags not yet zeroed), every launch followed
     by a barrier (a launch's consumers may sit on any rank), finalise, then
-    sum u over the ranks.  The barrier is an all-reduce on a token queued on
-    the current stream, so it orders the GPUs' work without a host sync."""
+    sum u over the ranks.  `barrier` (a callable enqueuing a device barrier
+    on the current stream, DeviceBarrier.wait) or, if None, an all-reduce on
+    a token queued on the current stream; neither syncs the host."""
     import torch
 
-    def barrier():
-        tok = torch.zeros(1, device=device)
-        dist.all_reduce(tok, group=group)
+    if barrier is None:
+        def barrier():
+            tok = torch.zeros(1, device=device)
+            dist.all_reduce(tok, group=group)
 
     nl = plan.nlaunch()
     plan.apply_range(fmin, umin, nrhs, 0, 0, 1)

@@ -1,14 +1,16 @@
 """Subdomain-sharded sweep (paper_2002_05327_b200/sharded.py) on one device
-with virtual ranks: same u as the unsharded sweep (floating-point sums of the
-ranks' u in a different order: <= 1e-12 relative), identical counters, and
-each rank holding only its own factorizations."""
+with virtual ranks: u within 1e-10 of the CPU oracle (and within 1e-12 of the
+unsharded sweep: the ranks' u are summed in a different order), identical
+counters, and each rank holding only its own factorizations; the device-side
+cross-rank barrier (ds_barrier_*) with two ranks on two streams."""
 import numpy as np
 import pytest
 import torch
 
 from paper_2002_05327_b200 import FactorizationCache, configs, diagonal_sweep_solve
 from paper_2002_05327_b200.ddm import SweepPlan, device_plan
-from paper_2002_05327_b200.sharded import ShardedSweep, block_owners
+from oracle import ds_oracle as O
+from paper_2002_05327_b200.sharded import DeviceBarrier, ShardedSweep, block_owners
 
 pytestmark = pytest.mark.gpu
 
@@ -37,6 +39,11 @@ def test_sharded_matches_unsharded(cuda, cfg, nranks, nrhs):
     sh = ShardedSweep(part, ops, nranks, nrhs, caches=caches)
     u = sh.apply(fd)
     assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) <= 1e-12
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops, oc = prob.operators(), O.Cache()
+    for r in range(nrhs):
+        want, orep = O.ddm_apply(prob, oops, oc, f[r])
+        assert rel(u[r].cpu().numpy().reshape(want.shape), want) <= 1e-10, r
     ctr = sh.counters(nrhs)
     for k in ("nonzero", "discarded", "visit_nonzero", "visit_consumed", "visit_emitted", "visit_cut"):
         assert np.array_equal(ctr[k], ref_ctr[k]), k
@@ -101,3 +108,27 @@ def test_sharded_3d_staged_path(cuda):
     sh = ShardedSweep(part, ops, 2, 1)
     u = sh.apply(fd)
     assert rel(u.cpu().numpy(), u_ref.cpu().numpy()) <= 1e-12
+
+
+def test_device_barrier_two_ranks_two_streams(cuda):
+    """Two barrier ranks on one device, each on its own stream (one
+    single-warp kernel each, co-resident): every generation completes on
+    both, and work queued after a rank's barrier runs only after the other
+    rank's work queued before its own barrier."""
+    bars = [DeviceBarrier(2, r) for r in range(2)]
+    ptrs = [b.arrive_ptr() for b in bars]
+    for b in bars:
+        b.set_peers(ptrs)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    x = torch.zeros(1 << 20, dtype=torch.float64, device="cuda")
+    y = torch.zeros(1, dtype=torch.float64, device="cuda")
+    for gen in range(1, 6):
+        with torch.cuda.stream(streams[0]):
+            x.add_(1.0)          # rank 0's work before the barrier
+            bars[0].wait()
+        with torch.cuda.stream(streams[1]):
+            bars[1].wait()
+            y.copy_(x[-1:])      # rank 1 reads rank 0's result after the barrier
+        torch.cuda.synchronize()
+        assert float(y.item()) == gen
+    assert bars[0].generation == bars[1].generation == 5

@@ -56,6 +56,42 @@ def test_protocol_world2():
         assert u00 == total  # u summed over ranks, initialisation zeroed the stale 7
 
 
+def _worker_custom_barrier(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = StandInPlan(rank)
+    fmin = torch.zeros(3, 2, dtype=torch.complex128)
+    umin = torch.zeros((3, 2), dtype=torch.complex128)
+    log = []
+
+    def barrier():  # the device barrier's place in the protocol (DeviceBarrier.wait)
+        log.append(len(plan.calls))
+        dist.barrier()
+
+    run_protocol(plan, fmin, umin, 2, dist, device="cpu", barrier=barrier)
+    q.put((rank, log, umin[0, 0].real.item()))
+    dist.destroy_process_group()
+
+
+def test_protocol_world2_custom_barrier():
+    """With a device barrier the protocol calls it once after the
+    initialisation and once after every launch (never a token all-reduce)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker_custom_barrier, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    total = sum((r + 1) * (l + 1) for r in range(2) for l in range(5))
+    for rank, log, u00 in res:
+        assert log == [1, 2, 3, 4, 5, 6]
+        assert u00 == total
+
+
 def test_block_owners():
     from paper_2002_05327_b200 import configs
 
