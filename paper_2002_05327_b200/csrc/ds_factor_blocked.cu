@@ -4,15 +4,21 @@
 // (operator, half) walks its blocks; at each step the Schur complement
 //     S = D_k - c1 * S_prev1^{-1} - c2 * S_prev2^{-1}
 // is formed directly in the block's factor slot and inverted in place by a
-// right-looking blocked Gauss-Jordan with partial pivoting, panels of
-// BW = 32 columns:
-//   1. panel kernel: one thread-block cluster per matrix keeps the m x BW
+// right-looking blocked Gauss-Jordan with partial pivoting.  Columns go in
+// macro-panels of MW = 128 (4 sub-panels of BW = 32):
+//   1. per sub-panel: one thread-block cluster per matrix keeps the m x BW
 //      panel in distributed shared memory and runs the BW pivot steps
 //      (cluster-wide argmax, row interchange through DSMEM, elimination);
-//   2. the panel's row interchanges are applied to the other columns;
-//   3. rank-BW trailing update A += P' T  (P' = panel with I subtracted on the
-//      pivot rows, T = the pivot rows outside the panel) — a plain complex
-//      GEMM (cuBLAS zgemm), 8 m^2 BW flop per panel.
+//      its row interchanges go to every other column; its rank-BW update
+//      A += P'_s T_s is applied to the macro-panel's columns only
+//      (P'_s = sub-panel with I subtracted on the pivot rows, T_s = the
+//      pivot rows, zero on the sub-panel) -- the macro-panel then holds the
+//      pivot columns of the composite elimination E = E_3 .. E_0;
+//   2. one rank-MW update of every column outside the macro-panel,
+//      A += (E - I)[:, pivots] A[pivot rows, :]   (8 m^2 MW flop, plain
+//      complex GEMM, cuBLAS zgemm) -- a quarter of the full-matrix passes of
+//      rank-32 updates and a K = 128 GEMM instead of K = 32 (config 5:
+//      1.68 s per window at MW = 32).
 // Column interchanges are undone at the end.  All chains of a step are
 // batched (one panel / swap / copy launch per step for every matrix).
 #include <cooperative_groups.h>
@@ -29,6 +35,7 @@
 namespace cg = cooperative_groups;
 
 #define BW 32
+#define MW 128  // macro-panel: columns per full-matrix update
 #define PANEL_THREADS 256
 
 struct BlkTask {   // one matrix being inverted at the current chain step
@@ -38,8 +45,8 @@ struct BlkTask {   // one matrix being inverted at the current chain step
   int p1, p2;      // previous blocks (-1 if absent)
   cplx *A;         // the m x m matrix (factor slot k)
   int *piv;        // [m] pivot rows
-  cplx *T;         // [BW][m]  pivot rows outside the panel
-  cplx *P;         // [m][BW]  panel with I subtracted on pivot rows
+  cplx *T;         // [MW][m]  pivot rows outside the panel
+  cplx *P;         // [m][MW]  panel with I subtracted on pivot rows
 };
 
 // S = D_k - co1 * A[p1] - co2 * A[p2]   (whole m x m, row-major)
@@ -180,13 +187,16 @@ __global__ void k_row_swaps(const BlkTask *__restrict__ tasks, int p) {
   }
 }
 
-// T = pivot rows outside the panel (zero on panel columns); P' = panel - I_R
-__global__ void k_panel_operands(const BlkTask *__restrict__ tasks, int p) {
+// T = pivot rows [p, p+w) outside the panel (zero on the panel columns);
+// P' = panel columns [p, p+w) with I subtracted on the pivot rows; w <= W,
+// the buffers' row pitch / column count (BW for a sub-panel, MW for a
+// macro-panel)
+__global__ void k_panel_operands(const BlkTask *__restrict__ tasks, int p, int width, int W) {
   const BlkTask &X = tasks[blockIdx.y];
   const int m = X.J.f.m;
   if (p >= m) return;
-  const int bw = min(BW, m - p);
-  const int64_t nT = (int64_t)BW * m, nP = (int64_t)m * BW;
+  const int bw = min(width, m - p);
+  const int64_t nT = (int64_t)W * m, nP = (int64_t)m * W;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nT + nP;
        e += (int64_t)gridDim.x * blockDim.x) {
     if (e < nT) {
@@ -196,7 +206,7 @@ __global__ void k_panel_operands(const BlkTask *__restrict__ tasks, int p) {
       X.T[e] = v;
     } else {
       int64_t f = e - nT;
-      int r = (int)(f / BW), tc = (int)(f % BW);
+      int r = (int)(f / W), tc = (int)(f % W);
       cplx v = make_double2(0.0, 0.0);
       if (tc < bw) {
         v = X.A[(size_t)r * m + p + tc];
@@ -277,8 +287,8 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
   const int nchains = 2 * njobs;
   int *piv = (int *)alloc(sizeof(int) * (size_t)nchains * mmax);
   int *srcb = (int *)alloc(sizeof(int) * (size_t)nchains * mmax);
-  cplx *Tb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * BW * mmax);
-  cplx *Pb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * BW * mmax);
+  cplx *Tb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * MW * mmax);
+  cplx *Pb = (cplx *)alloc(sizeof(cplx) * (size_t)nchains * MW * mmax);
   BlkTask *dtasks = (BlkTask *)alloc(sizeof(BlkTask) * nchains);
   auto cleanup = [&]() {
     for (void *p : ws) cudaFree(p);
@@ -327,8 +337,8 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
           X.A = J.sinv + (size_t)k * f.m * f.m;
           size_t slot = tasks.size();
           X.piv = piv + slot * mmax;
-          X.T = Tb + slot * BW * mmax;
-          X.P = Pb + slot * BW * mmax;
+          X.T = Tb + slot * MW * mmax;
+          X.P = Pb + slot * MW * mmax;
           (void)ba;
           tasks.push_back(X);
           task_job.push_back(i);
@@ -349,27 +359,47 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
       for (auto &X : tasks) mstep = std::max(mstep, X.J.f.m);
       k_form_schur<<<dim3(std::max(1, std::min(1024, (int)((int64_t)mstep * mstep / 256 / 4))), nt), 256, 0, st>>>(dtasks);
       ctx->launches++;
-      for (int p = 0; p < mstep && rc == DS_OK; p += BW) {
-        void *args[] = {(void *)&dtasks, (void *)&p, (void *)&rpc_max, (void *)&status};
-        rc = launch_cluster((const void *)k_panel_gj, dim3(PC, nt, 1), PC, panel_smem, st, args);
+      const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+      // row-major A(m x m) += P'(m x k) T(k x m)  ==  col-major A^T += T^T P'^T;
+      // rows [c0, c0 + nc) of A^T = columns [c0, c0 + nc) of A
+      auto zgemm = [&](int m, int nc, int c0, int k, int ldp, const BlkTask &X) -> int {
+        cublasStatus_t cs = cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, nc, m, k, &one,
+                                        (const cuDoubleComplex *)X.T + c0, m,
+                                        (const cuDoubleComplex *)X.P, ldp, &one,
+                                        (cuDoubleComplex *)X.A + c0, m);
+        ctx->launches++;
+        return cs == CUBLAS_STATUS_SUCCESS
+                   ? DS_OK
+                   : ds_fail(DS_ECUDA, "cublasZgemm failed in the blocked factorization");
+      };
+      for (int p0 = 0; p0 < mstep && rc == DS_OK; p0 += MW) {
+        for (int p = p0; p < std::min(p0 + MW, mstep) && rc == DS_OK; p += BW) {
+          void *args[] = {(void *)&dtasks, (void *)&p, (void *)&rpc_max, (void *)&status};
+          rc = launch_cluster((const void *)k_panel_gj, dim3(PC, nt, 1), PC, panel_smem, st, args);
+          if (rc) break;
+          k_row_swaps<<<dim3((mstep + 255) / 256, nt), 256, 0, st>>>(dtasks, p);
+          int width = BW, W = BW;
+          k_panel_operands<<<dim3(std::max(1, (2 * W * mstep + 255) / 256), nt), 256, 0, st>>>(
+              dtasks, p, width, W);
+          ctx->launches += 3;
+          // the sub-panel's update, restricted to the macro-panel's columns
+          for (auto &X : tasks) {
+            const int m = X.J.f.m;
+            if (p >= m) continue;
+            const int nc = std::min(MW, m - p0);
+            if (nc > std::min(BW, m - p) && (rc = zgemm(m, nc, p0, BW, BW, X))) break;
+          }
+          DS_CHECK_LAUNCH();
+        }
         if (rc) break;
-        k_row_swaps<<<dim3((mstep + 255) / 256, nt), 256, 0, st>>>(dtasks, p);
-        k_panel_operands<<<dim3(std::max(1, (2 * BW * mstep + 255) / 256), nt), 256, 0, st>>>(dtasks, p);
-        ctx->launches += 3;
-        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+        // rank-MW update of every column outside the macro-panel
+        k_panel_operands<<<dim3(std::max(1, (2 * MW * mstep + 255) / 256), nt), 256, 0, st>>>(
+            dtasks, p0, MW, MW);
+        ctx->launches++;
         for (auto &X : tasks) {
           const int m = X.J.f.m;
-          if (p >= m) continue;
-          // row-major A(m x m) += P'(m x BW) T(BW x m)  ==  col-major A^T += T^T P'^T
-          cublasStatus_t cs = cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, m, m, BW, &one,
-                                          (const cuDoubleComplex *)X.T, m,
-                                          (const cuDoubleComplex *)X.P, BW, &one,
-                                          (cuDoubleComplex *)X.A, m);
-          if (cs != CUBLAS_STATUS_SUCCESS) {
-            rc = ds_fail(DS_ECUDA, "cublasZgemm failed in the blocked factorization");
-            break;
-          }
-          ctx->launches++;
+          if (p0 >= m) continue;
+          if (std::min(MW, m - p0) < m && (rc = zgemm(m, m, 0, MW, MW, X))) break;
         }
         DS_CHECK_LAUNCH();
       }

