@@ -18,7 +18,8 @@
 //      A += (E - I)[:, pivots] A[pivot rows, :]   (8 m^2 MW flop, plain
 //      complex GEMM, cuBLAS zgemm) -- a quarter of the full-matrix passes of
 //      rank-32 updates and a K = 128 GEMM instead of K = 32 (config 5:
-//      1.68 s per window at MW = 32).
+//      1.68 s per window at MW = 32; MW = 256 measured no faster: cuBLAS
+//      zgemm stays at ~25 TFLOP/s for m = 2793 at K = 128 and K = 256).
 // Column interchanges are undone at the end.  All chains of a step are
 // batched (one panel / swap / copy launch per step for every matrix).
 #include <cooperative_groups.h>
@@ -36,7 +37,7 @@ namespace cg = cooperative_groups;
 
 #define BW 32
 #define MW 128  // macro-panel: columns per full-matrix update
-#define PANEL_THREADS 256
+#define PANEL_THREADS 512
 
 struct BlkTask {   // one matrix being inverted at the current chain step
   FactJob J;       // operator, layout, factor base
@@ -68,6 +69,16 @@ __global__ void k_form_schur(const BlkTask *__restrict__ tasks) {
 
 // Panel Gauss-Jordan on columns [p, p+BW) of every task's matrix.  Cluster
 // rank q holds rows [q*rpc, q*rpc + rpc) of the panel in shared memory.
+// One cluster barrier per pivot step: every CTA publishes its local argmax
+// (value, row index and a copy of that row) and, if it owns it, a copy of
+// row j, in a buffer of parity jj & 1; after the barrier every CTA reduces
+// the C candidates and reads the two rows it needs from the publishers.  A
+// buffer of parity b is rewritten two steps later, after the next barrier,
+// which every reader of step jj passes only when done reading.  (The
+// original form -- candidates, pivot, row fetch and elimination separated
+// by three cluster barriers and a serial candidate loop -- took 263 us per
+// 32-column panel at m = 2793, 58% of the config-5 factorization.)
+// Pivot choice (largest |.|_1, lowest row on ties) and arithmetic unchanged.
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
     k_panel_gj(const BlkTask *__restrict__ tasks, int p, int rpc_max, int *status) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -78,24 +89,27 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   const int bw = min(BW, m - p);
   const int rpc = (m + C - 1) / C;
   const int r0 = rank * rpc, r1 = min(m, r0 + rpc);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx *pan = (cplx *)smem_raw;            // [rpc_max][BW]
   cplx *rowj = pan + (size_t)rpc_max * BW; // [BW]
   cplx *rowp = rowj + BW;                  // [BW]
-  __shared__ double cand_v[1];
-  __shared__ int cand_i[1];
+  __shared__ cplx pub_row[2][BW];          // my candidate row, per parity
+  __shared__ cplx pub_rowj[2][BW];         // row j (if mine), per parity
+  __shared__ double pub_v[2];
+  __shared__ int pub_i[2];
   __shared__ double red_v[PANEL_THREADS / 32];
   __shared__ int red_i[PANEL_THREADS / 32];
   __shared__ int s_piv;
+  __shared__ double s_best;
 
   for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
     int r = e / BW, c = e % BW;
     pan[e] = c < bw ? X.A[(size_t)(r0 + r) * m + p + c] : make_double2(0.0, 0.0);
   }
-  cluster.sync();
+  __syncthreads();
   for (int jj = 0; jj < bw; ++jj) {
-    const int j = p + jj;
+    const int j = p + jj, b = jj & 1;
     // (a) local argmax of |A[r][j]|_1 over my rows r >= j
     double best = -1.0;
     int bi = m;
@@ -108,41 +122,57 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       int oi = __shfl_down_sync(0xffffffffu, bi, off);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
-    if ((t & 31) == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bi; }
+    if (lane == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bi; }
     __syncthreads();
-    if (t == 0) {
-      double bv = red_v[0];
-      int bidx = red_i[0];
-      for (int w = 1; w < PANEL_THREADS / 32; ++w)
-        if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bidx)) { bv = red_v[w]; bidx = red_i[w]; }
-      cand_v[0] = bv;
-      cand_i[0] = bidx;
+    if (t < 32) {
+      double bv = lane < PANEL_THREADS / 32 ? red_v[lane] : -1.0;
+      int bidx = lane < PANEL_THREADS / 32 ? red_i[lane] : m;
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, bv, off);
+        int oi = __shfl_down_sync(0xffffffffu, bidx, off);
+        if (ov > bv || (ov == bv && oi < bidx)) { bv = ov; bidx = oi; }
+      }
+      bidx = __shfl_sync(0xffffffffu, bidx, 0);
+      if (lane == 0) { pub_v[b] = bv; pub_i[b] = bidx; }
+      // (a2) publish the candidate row and, if mine, row j
+      pub_row[b][lane] = (bidx < m && lane < BW) ? pan[(bidx - r0) * BW + lane] : make_double2(0.0, 0.0);
+      if (j >= r0 && j < r1) pub_rowj[b][lane] = pan[(j - r0) * BW + lane];
     }
     cluster.sync();
-    // (b) global pivot (same decision in every CTA)
-    if (t == 0) {
-      double bv = -1.0;
-      int bidx = m;
-      for (int q = 0; q < C; ++q) {
-        double v = *cluster.map_shared_rank(&cand_v[0], q);
-        int i = *cluster.map_shared_rank(&cand_i[0], q);
-        if (v > bv || (v == bv && i < bidx)) { bv = v; bidx = i; }
+    // (b) global pivot: the C candidates reduced in parallel (same in every CTA)
+    if (t < 32) {
+      double v = -1.0;
+      int i = m, q = C;
+      if (lane < C) {
+        v = *cluster.map_shared_rank(&pub_v[b], lane);
+        i = *cluster.map_shared_rank(&pub_i[b], lane);
+        q = lane;
       }
-      s_piv = bidx;
-      if (rank == 0) X.piv[j] = bidx;
-      if (!(bv > 0.0) || bidx >= m) atomicExch(status, 1);
+      for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_down_sync(0xffffffffu, v, off);
+        int oi = __shfl_down_sync(0xffffffffu, i, off);
+        int oq = __shfl_down_sync(0xffffffffu, q, off);
+        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; q = oq; }
+      }
+      v = __shfl_sync(0xffffffffu, v, 0);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      // (c) rows pv (the winner's published candidate) and j (its owner's copy)
+      if (lane < BW) {
+        rowp[lane] = *cluster.map_shared_rank(&pub_row[b][lane], q < C ? q : 0);
+        rowj[lane] = *cluster.map_shared_rank(&pub_rowj[b][lane], j / rpc);
+      }
+      if (lane == 0) {
+        s_piv = i;
+        s_best = v;
+      }
     }
     __syncthreads();
     const int pv = min(s_piv, m - 1);
-    // (c) fetch rows j and pv from their owners
-    if (t < BW) {
-      int qj = j / rpc, qp = pv / rpc;
-      cplx *pj = cluster.map_shared_rank(pan, qj);
-      cplx *pp = cluster.map_shared_rank(pan, qp);
-      rowj[t] = pj[(j - qj * rpc) * BW + t];
-      rowp[t] = pp[(pv - qp * rpc) * BW + t];
+    if (t == 0) {
+      if (rank == 0) X.piv[j] = s_piv;
+      if (!(s_best > 0.0) || s_piv >= m) atomicExch(status, 1);
     }
-    cluster.sync();  // all reads done before anyone writes
     // (d) eliminate: new row j = old row pv scaled; other rows updated
     const cplx pivot = rowp[jj];
     const cplx inv = cinv(pivot);
@@ -161,12 +191,13 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       }
       pan[e] = nv;
     }
-    cluster.sync();
+    __syncthreads();
   }
   for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
     int r = e / BW, c = e % BW;
     if (c < bw) X.A[(size_t)(r0 + r) * m + p + c] = pan[e];
   }
+  cluster.sync();  // no CTA leaves while another may still read its buffers
 }
 
 // apply the panel's row interchanges to the columns outside the panel
@@ -271,7 +302,9 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
   int mmax = 0;
   for (int i = 0; i < njobs; ++i) mmax = std::max(mmax, jobs[i].f.m);
   // panel cluster: enough CTAs that the panel rows fit in shared memory
-  int PC = 4;
+  // (16 CTAs of 512 threads from m = 1024 up: a pivot step's elimination is
+  // rows/CTA x 32 complex updates; 8 x 256 took 242 us per panel at m = 2793)
+  int PC = mmax >= 1024 ? 16 : 4;
   while (PC < 16 && ((size_t)((mmax + PC - 1) / PC) * BW + 2 * BW) * sizeof(cplx) > 200 * 1024) PC *= 2;
   const int rpc_max = (mmax + PC - 1) / PC;
   const size_t panel_smem = ((size_t)rpc_max * BW + 2 * BW) * sizeof(cplx);
