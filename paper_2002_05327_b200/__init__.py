@@ -3,9 +3,11 @@
 Public names follow `diagsweep/__init__.py:26-54` for the hot path
 (SURVEY §8): geometry and partition metadata, PML operators, the GPU
 factorization cache, `diagonal_sweep_solve` and `gmres`, each additionally
-batched over right-hand sides.  Out of scope (not exported): the CLI/config
-plumbing, the pipeline timing model and the semi-analytic reference
-solution.
+batched over right-hand sides.  The drivers around it (SURVEY §8(f) rank
+4: config loader, `solve` / `decay` / `precond-study` commands and their
+file artifacts) are in `runconfig`, `drivers`, `artifacts` and `cli`
+(`python -m paper_2002_05327_b200`).  Out of scope: the pipeline timing
+model and the semi-analytic reference solution (convergence study).
 """
 
 from .ddm import (
@@ -22,6 +24,8 @@ from .ddm import (
     solve_cuts,
     source_directions,
 )
+from .artifacts import dump_field, load_field, load_velocity, save_velocity, write_pgm
+from .drivers import decay_history, fit_decay_rate, solve_once
 from .errors import ConfigurationError, ModelError, SolverError
 from .grid import ComplexField, Grid, Window, make_grid
 from .krylov import SolveReport, gmres, gmres_batched
@@ -37,6 +41,7 @@ from .media import (
 )
 from .partition import Partition, beta_hat, make_partition, steps_per_sweep, sweep_step_of
 from .pml import DiscreteOperator, PmlProfile, assemble_operator, tuned_sigma_max
+from .runconfig import RunConfig, load_config
 from .subdomain import FactorizationCache, factorize
 from .transfer import next_usable_sweep, rule_allows, similar_direction, transfer_geometry
 
@@ -52,4 +57,6 @@ __all__ = [
     "octant_exactness_check", "point_shots", "raster_model", "restrict_source", "rule_allows",
     "similar_direction", "solve_cuts", "source_directions", "steps_per_sweep", "sweep_step_of",
     "transfer_geometry", "tuned_sigma_max",
+    "RunConfig", "load_config", "solve_once", "decay_history", "fit_decay_rate",
+    "dump_field", "load_field", "write_pgm", "save_velocity", "load_velocity",
 ]

@@ -160,11 +160,18 @@ def phase_gmres(args, s, b, out):
     napp = [0]
     plans = []
 
+    tl = [time.perf_counter()]
+
     def apply_m(v):
         napp[0] += 1
         u, _ = diagonal_sweep_solve(v, part, ops, cache, warn_collar=False)
         if not plans:
             plans.extend(cache._plans.values())
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        print(f"  application {napp[0]}: {now - tl[-1]:.1f} s, factorizations so far "
+              f"{plans[0].pool.state()[2] if plans else -1}", flush=True)
+        tl.append(now)
         return u.values
 
     fd = torch.from_numpy(f).cuda()
