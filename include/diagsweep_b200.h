@@ -10,7 +10,8 @@
  * ds_ddm_counters, ds_*_host helpers).
  *
  * Status codes: 0 ok; < 0 configuration error (bad shape/window/argument,
- * maps to diagsweep.errors.ConfigurationError); > 0 solver error (zero
+ * maps to diagsweep.errors.ConfigurationError; -2 = model error, e.g. a
+ * nonpositive velocity, maps to ModelError); > 0 solver error (zero
  * pivot, non-finite factor, CUDA failure; maps to SolverError).  The
  * message of the last failure on the calling thread is ds_last_error().
  *
@@ -44,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 5
+#define DS_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -418,6 +419,31 @@ DS_API int ds_layout_to_minor(ds_ctx *ctx, int64_t n, int32_t nrhs,
                        const ds_cplx *src_dev, ds_cplx *dst_dev);
 DS_API int ds_layout_to_outer(ds_ctx *ctx, int64_t n, int32_t nrhs,
                        const ds_cplx *src_dev, ds_cplx *dst_dev);
+
+/* ------------------------------------------------ assembly on the device
+ * (ABI 6).  Replace the host-O(N) steps of building a
+ * problem: assemble_operator's raster kappa^2 (pml.py:197-213 with
+ * RasterModel.speed_at, media.py:75-101) and Gaussian source batches
+ * (media.py:147-167 / the configs' seeded sources).
+ *
+ * ds_raster_kappa2: out[node] = (omega / c(node))^2 over a window of
+ * win_counts[dim] nodes (C order), c the multilinear interpolation of the
+ * float32 raster (raster_counts[dim], C order) with the per-axis tables
+ * base_dev[a][i] (lower raster index of window coordinate i along axis a)
+ * and frac_dev[a][i] (its fraction), as the reference computes them; bitwise
+ * the reference's values.  Returns -2 (model error) if some c <= 0.  Blocks
+ * until done (reads the error flag). */
+DS_API int ds_raster_kappa2(ds_ctx *ctx, int32_t dim, const int32_t *win_counts,
+                            const int32_t *raster_counts, const float *samples_dev,
+                            const int32_t *const *base_dev, const double *const *frac_dev,
+                            double omega, double *out_dev);
+/* ds_gaussian_fields: out[r][node] = amp[r] * exp(arg), RHS-outer, complex
+ * with zero imaginary part; r2 = sum over axes (in order) of the per-axis
+ * tables d2_dev[a][r * counts[a] + i]; arg = scale[r] * r2, or -r2 / scale[r]
+ * when divide != 0.  CUDA exp: values within ~2 ulp of NumPy's. */
+DS_API int ds_gaussian_fields(ds_ctx *ctx, int32_t dim, const int32_t *counts, int32_t nrhs,
+                              const double *const *d2_dev, const double *amp_dev,
+                              const double *scale_dev, int32_t divide, ds_cplx *out_dev);
 
 #ifdef __cplusplus
 }

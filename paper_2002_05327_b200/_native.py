@@ -14,7 +14,7 @@ import os
 import threading
 from pathlib import Path
 
-from .errors import ConfigurationError, SolverError
+from .errors import ConfigurationError, ModelError, SolverError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libdiagsweep_b200.so"
 
@@ -137,9 +137,11 @@ _SIGNATURES = [
     ("ds_vec_rows", C.c_int, [vp, i64, i32, vp, vp, vp]),
     ("ds_layout_to_minor", C.c_int, [vp, i64, i32, vp, vp]),
     ("ds_layout_to_outer", C.c_int, [vp, i64, i32, vp, vp]),
+    ("ds_raster_kappa2", C.c_int, [vp, i32, vp, vp, vp, vp, vp, C.c_double, vp]),
+    ("ds_gaussian_fields", C.c_int, [vp, i32, vp, i32, vp, vp, vp, i32, vp]),
 ]
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]
 
@@ -175,6 +177,8 @@ def check(status: int, what: str = "") -> None:
         return
     msg = _lib.ds_last_error().decode(errors="replace") if _lib else "unknown error"
     text = f"{what}: {msg}" if what else msg
+    if status == -2:
+        raise ModelError(text)
     if status < 0:
         raise ConfigurationError(text)
     raise SolverError(text)

@@ -153,15 +153,17 @@ def sources(s: Spec, grid, centers=None) -> np.ndarray:
     return out
 
 
-def build(s: Spec):
-    """(grid, partition, profile, model, omega, operators, global operator, c)."""
+def build(s: Spec, assembly: str = "host"):
+    """(grid, partition, profile, model, omega, operators, global operator, c).
+    assembly="device": raster kappa^2 interpolated on the GPU (K8a, bitwise
+    equal to the host path)."""
     grid = grid_of(s)
     part = make_partition(grid, s.counts, s.d, s.pml)
     profile = PmlProfile(s.pml, s.d, s.sigma_max, s.exponent)
     model, c = model_of(s)
     omega = omega_of(s, c)
-    ops = build_operators(part, profile, model, omega)
-    gop = build_global_operator(part, profile, model, omega)
+    ops = build_operators(part, profile, model, omega, assembly=assembly)
+    gop = build_global_operator(part, profile, model, omega, assembly=assembly)
     return dict(grid=grid, partition=part, profile=profile, model=model, omega=omega, ops=ops,
                 gop=gop, c=c)
 

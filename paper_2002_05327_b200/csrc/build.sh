@@ -10,7 +10,7 @@ FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17
 objs=()
 tmp="$(mktemp -d)"
 trap 'rm -rf "$tmp"' EXIT
-for src in ds_core ds_factor ds_factor_blocked ds_modal ds_solve ds_stage ds_sweep; do
+for src in ds_assemble ds_core ds_factor ds_factor_blocked ds_modal ds_solve ds_stage ds_sweep; do
   "$NVCC" "${FLAGS[@]}" -DDS_BUILDING_LIB -c "$here/$src.cu" -o "$tmp/$src.o" &
   objs+=("$tmp/$src.o")
 done

@@ -99,18 +99,21 @@ def cut_mask_to_set(mask: int, dim: int) -> frozenset:
                      if mask >> (2 * a + s) & 1)
 
 
-def build_operators(partition: Partition, profile: PmlProfile, velocity, omega: float) -> dict:
+def build_operators(partition: Partition, profile: PmlProfile, velocity, omega: float,
+                    assembly: str = "host") -> dict:
     clamp = partition.interior_box()
     return {
         index: assemble_operator(partition.grid, partition.window(index), partition.box(index),
-                                 profile, velocity, omega, clamp_box=clamp)
+                                 profile, velocity, omega, clamp_box=clamp, assembly=assembly)
         for index in partition.subdomains()
     }
 
 
-def build_global_operator(partition: Partition, profile: PmlProfile, velocity, omega):
+def build_global_operator(partition: Partition, profile: PmlProfile, velocity, omega,
+                          assembly: str = "host"):
     return assemble_operator(partition.grid, partition.grid.full_window(), partition.interior,
-                             profile, velocity, omega, clamp_box=partition.interior_box())
+                             profile, velocity, omega, clamp_box=partition.interior_box(),
+                             assembly=assembly)
 
 
 @dataclass
