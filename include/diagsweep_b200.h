@@ -428,13 +428,14 @@ DS_API int ds_layout_to_outer(ds_ctx *ctx, int64_t n, int32_t nrhs,
  *
  * ds_raster_kappa2: out[node] = (omega / c(node))^2 over a window of
  * win_counts[dim] nodes (C order), c the multilinear interpolation of the
- * float32 raster (raster_counts[dim], C order) with the per-axis tables
+ * raster samples (raster_counts[dim], C order, as float64 -- float32 rasters
+ * widened exactly) with the per-axis tables
  * base_dev[a][i] (lower raster index of window coordinate i along axis a)
  * and frac_dev[a][i] (its fraction), as the reference computes them; bitwise
  * the reference's values.  Returns -2 (model error) if some c <= 0.  Blocks
  * until done (reads the error flag). */
 DS_API int ds_raster_kappa2(ds_ctx *ctx, int32_t dim, const int32_t *win_counts,
-                            const int32_t *raster_counts, const float *samples_dev,
+                            const int32_t *raster_counts, const double *samples_dev,
                             const int32_t *const *base_dev, const double *const *frac_dev,
                             double omega, double *out_dev);
 /* ds_gaussian_fields: out[r][node] = amp[r] * exp(arg), RHS-outer, complex

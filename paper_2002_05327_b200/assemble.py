@@ -30,6 +30,9 @@ from . import _native as N
 from .errors import ConfigurationError, ModelError
 
 
+_RASTER_DEV = None
+
+
 def _ptr_array(tensors):
     return (C.c_void_p * 3)(*([t.data_ptr() for t in tensors] + [0] * (3 - len(tensors))))
 
@@ -62,12 +65,11 @@ def raster_kappa2_device(grid, window, model, omega: float, clamp_box):
         bi, fr = raster_axis_tables(x, model.extents[ax], samples.shape[ax])
         bases.append(torch.from_numpy(bi).cuda())
         fracs.append(torch.from_numpy(np.ascontiguousarray(fr)).cuda())
-    key = id(model)
-    cached = _engine.__dict__.setdefault("_RASTER_DEV", {})
-    dev = cached.get(key)
+    global _RASTER_DEV  # the last raster's samples on the device (one model at a time)
+    dev = _RASTER_DEV
     if dev is None or dev[0] is not model:
-        dev = (model, torch.from_numpy(np.ascontiguousarray(samples, dtype=np.float32)).cuda())
-        cached[key] = dev
+        dev = _RASTER_DEV = (model, torch.from_numpy(
+            np.ascontiguousarray(samples, dtype=np.float64)).cuda())
     out = torch.empty(tuple(window.shape), dtype=torch.float64, device="cuda")
     wc, _ = N.i32_array(window.shape)
     rc, _ = N.i32_array(samples.shape)

@@ -3,7 +3,8 @@
 //
 // K8a  raster kappa^2 of an operator window (pml.py _kappa2 "full" kind,
 //      reference pml.py:197-213 with RasterModel.speed_at, media.py:75-101):
-//      per node the multilinear interpolation of the float32 speed raster
+//      per node the multilinear interpolation of the speed raster (float32
+//      or float64 samples, widened exactly to float64 on upload)
 //      at the node's clamped coordinates, then kappa^2 = (omega / c)^2.
 //      Everything that depends on one axis only -- the clamped coordinate,
 //      t, the lower raster index and its fraction -- is a 1D table built on
@@ -34,7 +35,7 @@ struct RasterAxes {
   int64_t rstride[3];      // raster strides (C order, elements)
 };
 
-__global__ void k_raster_kappa2(RasterAxes X, int dim, const float *__restrict__ samples,
+__global__ void k_raster_kappa2(RasterAxes X, int dim, const double *__restrict__ samples,
                                 double omega, int64_t total, double *__restrict__ out,
                                 int *__restrict__ bad) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -62,7 +63,7 @@ __global__ void k_raster_kappa2(RasterAxes X, int dim, const float *__restrict__
           else if (up) w = __dmul_rn(w, 0.0);
         }
       }
-      acc = __dadd_rn(acc, __dmul_rn(w, (double)samples[off]));
+      acc = __dadd_rn(acc, __dmul_rn(w, samples[off]));
     }
     if (!(acc > 0.0)) atomicExch(bad, 1);
     const double q = __ddiv_rn(omega, acc);
@@ -71,7 +72,7 @@ __global__ void k_raster_kappa2(RasterAxes X, int dim, const float *__restrict__
 }
 
 extern "C" int ds_raster_kappa2(ds_ctx *ctx, int32_t dim, const int32_t *win_counts,
-                                const int32_t *raster_counts, const float *samples_dev,
+                                const int32_t *raster_counts, const double *samples_dev,
                                 const int32_t *const *base_dev, const double *const *frac_dev,
                                 double omega, double *out_dev) {
   if (!ctx || dim < 1 || dim > 3 || !win_counts || !raster_counts || !samples_dev || !base_dev ||
@@ -127,7 +128,20 @@ __global__ void k_gauss_fields(GaussAxes X, int dim, int nrhs, const double *__r
     double r2 = 0.0;
     for (int a = 0; a < dim; ++a) r2 = __dadd_rn(r2, X.d2[a][(int64_t)r * X.n[a] + i[a]]);
     const double arg = divide ? __ddiv_rn(-r2, sc) : __dmul_rn(sc, r2);
-    out[(int64_t)r * total + e] = make_double2(__dmul_rn(am, exp(arg)), 0.0);
+    // below exp's normal range CUDA's exp does not round into the subnormals
+    // as NumPy's does: exp(arg) = exp(A) (1 + B) 2^-64 with A = arg + 64 ln2_hi
+    // (exact: Cody-Waite split, ln2_hi has 32 significant bits) and
+    // B = 64 ln2_lo, rounded once into the subnormal range by scalbn -- same
+    // exact-zero (underflow) set as NumPy and a few ulp apart
+    double ex;
+    if (arg >= -708.0) {
+      ex = exp(arg);
+    } else {
+      const double A = arg + 64.0 * 6.93147180369123816490e-01;
+      const double B = 64.0 * 1.90821492927058770002e-10;
+      ex = scalbn(exp(A) * (1.0 + B + 0.5 * B * B), -64);
+    }
+    out[(int64_t)r * total + e] = make_double2(__dmul_rn(am, ex), 0.0);
   }
 }
 
