@@ -82,7 +82,6 @@ void ds_options_from_env(ds_options &o) {
   o.k3_rc_max = std::max(1, env_opt("DS_K3_RCMAX", o.k3_rc_max));
   o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
-  o.modal_tile = env_opt("DS_MODAL_TILE", 0);
 }
 
 // name -> member of ds_options
@@ -102,7 +101,6 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "k3_rc_max") return &o.k3_rc_max;
   if (k == "k3_cluster") return &o.k3_cluster;
   if (k == "hio_dstreams") return &o.hio_dstreams;
-  if (k == "modal_tile") return &o.modal_tile;
   return nullptr;
 }
 

@@ -185,7 +185,7 @@ __device__ __forceinline__ void cp_wait() {
 // 16 columns are all past colw skip the products).
 // NS-stage cp.async ring: chunk kc lives in buffer kc % NS; NS - 1 chunks
 // are in flight while one is multiplied (NS = 2: double buffering).
-template <int MT, int WR, int WC, int TK, int NS = 2, bool FM = false>
+template <int MT, int WR, int WC, int TK, int NS = 2>
 __device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0, int colw, int kc0,
                                            int kc1, cplx *smem_mg, const int *act, int A, int nrhs,
                                            double (&p1)[MT][2][2], double (&p2)[MT][2][2],
@@ -249,32 +249,15 @@ __device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0,
         for (int mt = 0; mt < MT; ++mt) a[mt] = As[mt * 8 * AP + k4 * 4];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[k4 * 4 * BP + nt * 8];
-        if constexpr (FM) {
-          // 4M: Re += Ar Br - Ai Bi, Im += Ar Bi + Ai Br (two accumulators)
+        double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
+        for (int mt = 0; mt < MT; ++mt) {
+          const double as = a[mt].x + a[mt].y;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              dmma(p1[mt][nt], a[mt].x, b[nt].x);
-              dmma(p2[mt][nt], a[mt].x, b[nt].y);
-            }
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              dmma(p1[mt][nt], -a[mt].y, b[nt].y);
-              dmma(p2[mt][nt], a[mt].y, b[nt].x);
-            }
-          }
-        } else {
-          double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const double as = a[mt].x + a[mt].y;
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-              dmma(p1[mt][nt], a[mt].x, b[nt].x);
-              dmma(p2[mt][nt], a[mt].y, b[nt].y);
-              dmma(p3[mt][nt], as, bs[nt]);
-            }
+          for (int nt = 0; nt < 2; ++nt) {
+            dmma(p1[mt][nt], a[mt].x, b[nt].x);
+            dmma(p2[mt][nt], a[mt].y, b[nt].y);
+            dmma(p3[mt][nt], as, bs[nt]);
           }
         }
       }
@@ -285,7 +268,7 @@ __device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0,
 }
 
 // Store a finished tile: Re = P1 - P2, Im = P3 - P1 - P2 (3M complex product).
-template <int MT, int WR, int WC, bool FM = false>
+template <int MT, int WR, int WC>
 __device__ __forceinline__ void gemm_store(const PassGeo &G, int row0, int col0, int colw,
                                            const int *act, int A, int nrhs,
                                            const double (&p1)[MT][2][2], const double (&p2)[MT][2][2],
@@ -304,24 +287,23 @@ __device__ __forceinline__ void gemm_store(const PassGeo &G, int row0, int col0,
         const int cc = wc * 16 + nt * 8 + 2 * tg + e;
         if (cc >= colw) continue;
         const int64_t off = col_offset(G, col0 + cc, A, act, nrhs) + (int64_t)gr * G.ncols;
-        G.out[off] = FM ? make_double2(p1[mt][nt][e], p2[mt][nt][e])
-                        : make_double2(p1[mt][nt][e] - p2[mt][nt][e],
-                                       p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
+        G.out[off] = make_double2(p1[mt][nt][e] - p2[mt][nt][e],
+                                  p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
       }
   }
 }
 
-template <int MT, int WR, int WC, int TK, int NS = 2, bool FM = false>
+template <int MT, int WR, int WC, int TK, int NS = 2>
 __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw,
                                           cplx *smem_mg, const int *act, int A, int nrhs) {
   double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
   const int nkc = (G.n + TK - 1) / TK;
-  gemm_accum<MT, WR, WC, TK, NS, FM>(G, row0, col0, colw, 0, nkc, smem_mg, act, A, nrhs, p1, p2, p3);
-  gemm_store<MT, WR, WC, FM>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
+  gemm_accum<MT, WR, WC, TK, NS>(G, row0, col0, colw, 0, nkc, smem_mg, act, A, nrhs, p1, p2, p3);
+  gemm_store<MT, WR, WC>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
 }
 
 // one tile per CTA: grid (column tiles, row tiles, visits)
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2, bool FM = false>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 __global__ void __launch_bounds__(32 * WR * WC, MINB)
     k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
@@ -337,7 +319,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   const int A = active_rhs(J, nrhs, act);
   const int total = G.outer * G.inner * A;  // compact columns
   if (col0 >= total) return;
-  gemm_tile<MT, WR, WC, TK, NS, FM>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
+  gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
 }
 
 // ------------------------------------------- mode-wise recurrences (K3m-R)
@@ -608,14 +590,14 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
 }
 
 // ------------------------------------------------------------- launcher
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2, bool FM = false>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
                        int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
   const size_t smem = sizeof(cplx) * NS * (TM * (TK + 4) + TK * (TN + 2));
   static bool attr_set = false;
   if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB, NS, FM>,
+    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB, NS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
@@ -627,7 +609,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
     gy = std::max(gy, (G.n + TM - 1) / TM);
   }
-  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS, FM>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
+  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
                      ctx->stream, jobs_dev, pass, nrhs));
 
   ctx->launches++;
@@ -647,16 +629,7 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   // 4): 32 x 32 per CTA, 2 x 2 warps of 16 x 16, K chunks of
   // 8 through a 4-stage cp.async ring, 4 CTAs per SM
   auto launch_pass = [&](int pass) -> int {
-    // tile variants (context option "modal_tile", A/B only; 0 = default)
-    switch (ctx->opt.modal_tile) {
-      case 1: return launch_gemm<1, 2, 2, 8, 6, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 2: return launch_gemm<2, 2, 2, 8, 4, 4, true>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 3: return launch_gemm<1, 4, 2, 8, 3, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 4: return launch_gemm<2, 2, 2, 8, 5, 4, true>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 5: return launch_gemm<1, 2, 2, 8, 6, 4, true>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      case 6: return launch_gemm<2, 2, 2, 16, 4, 3>(ctx, jobs_dev, facts, njob, pass, nrhs);
-      default: return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
-    }
+    return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
   };
   if (phase == 0 || phase == -1)
     for (int p = 0; p < na; ++p)
