@@ -82,6 +82,7 @@ void ds_options_from_env(ds_options &o) {
   o.k3_rc_max = std::max(1, env_opt("DS_K3_RCMAX", o.k3_rc_max));
   o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
+  o.k2b_3m = env_opt("DS_K2B_3M", 1) != 0;
 }
 
 // name -> member of ds_options
@@ -101,6 +102,7 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "k3_rc_max") return &o.k3_rc_max;
   if (k == "k3_cluster") return &o.k3_cluster;
   if (k == "hio_dstreams") return &o.hio_dstreams;
+  if (k == "k2b_3m") return &o.k2b_3m;
   return nullptr;
 }
 
