@@ -461,6 +461,32 @@ def run_ours(args, rank, world, local_rank):
             kernel_rooflines[cls] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                                      "frac": gbs / hbm if gbs else None,
                                      "algorithmic_bytes_per_app": nbytes, "peak_source": hbm_src}
+    # ---- K1 stencil (DiscreteOperator.apply on the global grid, the GMRES
+    # operator of configs 3/5) over the bench batch, L2 flushed before each
+    # call; 32 B per node and RHS (+8 for a raster kappa^2)
+    if ktimes and rank == 0:
+        gop_k1 = b["gop"]
+        full_k1 = part.grid.full_window()
+        vk = f_dev.reshape((R,) + part.grid.counts)
+        gop_k1.apply(vk, region=full_k1)
+        torch.cuda.synchronize()
+        k1ms = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gop_k1.apply(vk, region=full_k1)
+            e1.record()
+            torch.cuda.synchronize()
+            k1ms.append(e0.elapsed_time(e1))
+        kms = sorted(k1ms)[len(k1ms) // 2]
+        k1_bytes = (32 + (8 if gop_k1.kappa2_kind == "full" else 0)) * n * R
+        kernel_rooflines = kernel_rooflines or {}
+        kernel_rooflines["stencil_K1"] = {
+            "bound": "hbm", "achieved": k1_bytes / (kms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": k1_bytes / (kms / 1e3) / 1e9 / hbm, "algorithmic_bytes_per_call": k1_bytes,
+            "ms_per_call": kms, "peak_source": hbm_src,
+            "call": f"global operator apply over the {R}-RHS batch ({n} nodes), L2 flushed, median of 5"}
     # ---- parity spot check of the timed output (first RHS vs oracle is in tests)
     res = {
         "metric": "Helmholtz RHS/s (2D 8x8 subdomains)" if args.config == 2 else
