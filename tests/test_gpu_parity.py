@@ -927,3 +927,29 @@ def test_pinned_strided_and_empty_batches(cuda, cfg1):
                                              device="cuda"), b["partition"], b["ops"], cache,
                                  warn_collar=False)
     assert t0.values.is_cuda and t0.values.shape[0] == 0
+
+
+@pytest.mark.parametrize("cfg", ["5r", "mini3d"])
+def test_stencil_3d_ragged_regions(cuda, cfg):
+    """3D K1 on the global operator over ragged regions (partial blocks at
+    every face), 3 RHS: <= 1e-14 vs the oracle for raster (5r) and constant
+    kappa^2."""
+    if cfg == "5r":
+        s = configs.spec("5r")
+    else:
+        s = configs.Spec("mini-3d", ((0.0, 1.0),) * 3, (20, 22, 18), 3, 3, (2, 2, 2),
+                         2 * np.pi * 2, 1, "direct", "constant", 9, centers=((0.3, 0.55, 0.4),))
+    b = configs.build(s)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    gop, ogop = b["gop"], prob.global_operator()
+    shape = gop.window.shape
+    rng = np.random.default_rng(33)
+    for lo, hi in [((0, 0, 0), tuple(n - 1 for n in shape)),
+                   ((1, 2, 3), (shape[0] - 2, shape[1] - 1, shape[2] - 3)),
+                   ((3, 1, 0), (9, 6, 33 if shape[2] > 33 else shape[2] - 1))]:
+        reg = Window(tuple(a + c for a, c in zip(gop.window.lo, lo)),
+                     tuple(a + c for a, c in zip(gop.window.lo, hi)))
+        v = rng.standard_normal((3,) + reg.shape) + 1j * rng.standard_normal((3,) + reg.shape)
+        got = np.asarray(gop.apply(v, region=reg))
+        for r in range(3):
+            assert rel(got[r], ogop.apply(v[r], reg.lo)) <= 1e-14, (lo, hi, r)
