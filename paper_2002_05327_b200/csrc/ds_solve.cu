@@ -476,8 +476,8 @@ static int solve_max_clusters(const void *fn, int threads, int C, size_t smem) {
   return n;
 }
 // Choose the (cluster size, RHS chunk) that runs a step of nvisit visits in
-// the fewest waves of co-resident clusters, then with the least arithmetic
-// per CTA and stage (rows per CTA x chunk width); larger clusters on ties.
+// the fewest waves of co-resident clusters, then the smallest cluster, then
+// the least arithmetic per CTA and stage (rows per CTA x chunk width).
 template <typename SmemFn>
 static bool pick_cluster_chunk(const ds_ctx *ctx, const void *fn, int threads, int nvisit, int nrhs,
                                int max_m, bool mma, SmemFn smem_of, int *Cout, int *rcout,
@@ -487,7 +487,10 @@ static bool pick_cluster_chunk(const ds_ctx *ctx, const void *fn, int threads, i
   const int c_only = ctx->opt.k3_cluster;
   int bestC = 0, bestRc = 0;
   long best_waves = 0, best_work = 0, best_waste = 0;
-  for (int C : {16, 8}) {
+  // cluster sizes need not be powers of two: a 131-row slab (config 3) fits
+  // 9 CTAs of 16 rows, two clusters per GPC, where 16-CTA clusters (10
+  // rows, 6 of them padding) fit one per GPC -- 7 co-resident on 148 SMs
+  for (int C : {16, 12, 10, 9, 8}) {
     if (c_only && C != c_only) continue;
     const int rows = solve_rows_max(max_m, C);
     for (int rc = std::min(nrhs, rc_max); rc >= 1; rc = rc > 1 ? (rc + 1) / 2 : 0) {
@@ -505,9 +508,14 @@ static bool pick_cluster_chunk(const ds_ctx *ctx, const void *fn, int threads, i
       // ties (same waves and work per CTA): less padding, then the smaller
       // cluster -- config 2 measured 8 CTAs x (16 rows, 8 RHS) faster than
       // 16 CTAs x (8 rows, 16 RHS): half as many CTAs in every exchange
-      bool better = !bestC || waves < best_waves || (waves == best_waves && work < best_work);
-      if (!better && waves == best_waves && work == best_work)
-        better = waste < best_waste || (waste == best_waste && C < bestC);
+      // same waves: the smaller cluster (config 3: with two RHS groups on
+      // two streams, launches that pick 16-CTA clusters for less work per
+      // CTA fragment the GPCs under the other group's 9-CTA clusters --
+      // 125 RHS/s against 151 with 9-CTA clusters throughout)
+      bool better = !bestC || waves < best_waves || (waves == best_waves && C < bestC) ||
+                    (waves == best_waves && C == bestC && work < best_work);
+      if (!better && waves == best_waves && C == bestC && work == best_work)
+        better = waste < best_waste;
       if (better) {
         bestC = C;
         bestRc = rc;
