@@ -1700,6 +1700,10 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   constexpr int skip_cls = 0;
 #endif
   const int cap = std::max(1, ctx->num_sms * 4);
+  // K6 runs 3 CTAs of 256 threads per SM (76 registers): a grid of more
+  // than 3 x SMs leaves a partial second wave (ncu: 588 CTAs, 1.32 waves;
+  // capped: config 2 K6 0.814 -> 0.777 ms per application)
+  const int cap6 = std::max(1, ctx->num_sms * 3);
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
   const int nq = q1 < 0 ? (int)P->vstep_off.size() - 1 : q1;
@@ -1712,7 +1716,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       int v0 = P->vstep_off[q], G = P->vstep_off[q + 1] - v0;
       if (G == 0) continue;
       const int64_t wmax = P->max_w, smax = P->max_w;
-      int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap / G));
+      int bx = blocks_for(ctx, wmax * nrhs / 4, std::max(1, cap6 / G));
       if (hio && P->hio_need[q] > hio_waited) {  // f boxes [0, need) this assembly may read:
         hio_waited = P->hio_need[q];               // the last of them on each copy stream
         const cudaEvent_t *evi = hio->ext ? hio->ev_in : P->hio_ev_in.data();
