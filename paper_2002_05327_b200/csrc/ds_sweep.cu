@@ -1700,10 +1700,11 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
   constexpr int skip_cls = 0;
 #endif
   const int cap = std::max(1, ctx->num_sms * 4);
-  // K6 runs 3 CTAs of 256 threads per SM (76 registers): a grid of more
-  // than 3 x SMs leaves a partial second wave (ncu: 588 CTAs, 1.32 waves;
-  // capped: config 2 K6 0.814 -> 0.777 ms per application)
-  const int cap6 = std::max(1, ctx->num_sms * 3);
+  // K6 runs 3 CTAs of 256 threads per SM (76 registers): in 2D a grid of
+  // more than 3 x SMs leaves a partial second wave (ncu: 588 CTAs, 1.32
+  // waves; capped: config 2 K6 0.814 -> 0.777 ms per application); the 3D
+  // visits keep 4 x SMs (config 4: 5.63 vs 6.0 ms with the cap)
+  const int cap6 = std::max(1, ctx->num_sms * (dim == 2 ? 3 : 4));
   if (partials && P->nlaunch > 0)
     return ds_fail(DS_ECONFIG, "per-sweep partials need the sweep-ordered plan (nlaunch = 0)");
   const int nq = q1 < 0 ? (int)P->vstep_off.size() - 1 : q1;
