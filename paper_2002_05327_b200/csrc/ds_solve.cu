@@ -150,10 +150,13 @@ __global__ void __launch_bounds__(64 * NW, 1)
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int C = (int)cluster.num_blocks();
-  const SolveVisit V = visits[blockIdx.y];
+  // grid (cluster rank, RHS chunk, visit): the block scheduler dispatches
+  // y fastest after x, so the chunks of one visit are co-resident and stream
+  // the visit's factor tiles through L2 together instead of once each
+  const SolveVisit V = visits[blockIdx.z];
   const FactDev f = *V.f;
   const int m = f.m, nb = f.nb, tw = f.twist;
-  const int chunk0 = blockIdx.z * rc;
+  const int chunk0 = blockIdx.y * rc;
   const int rg = min(rc, nrhs - chunk0);
   const int t = threadIdx.x;
   constexpr int HT = 32 * NW, NT_ = 2 * HT;  // threads per half / per CTA
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(64 * NW, 1)
   cplx *red = fac + 2 * FAC_STAGES * fstride;  // [2 halves][NSL][rows_max*rc]
   const int rstride = rows_max * rc;
   auto VEC = [&](int h, int p) { return vec + (h * 2 + p) * vstride; };
-  cplx *xg = V.xg + (size_t)blockIdx.z * 4 * m * rc;
+  cplx *xg = V.xg + (size_t)blockIdx.y * 4 * m * rc;
   auto XG = [&](int h, int p) { return xg + ((size_t)h * 2 + p) * m * rg; };
 
   auto block_of = [&](int h, int st, int &kind) -> int {
@@ -551,7 +554,7 @@ static int launch_v8(ds_ctx *ctx, const void *visits_dev, int nvisit, int nrhs, 
   DS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3(C, nvisit, (nrhs + rc - 1) / rc);
+  cfg.gridDim = dim3(C, (nrhs + rc - 1) / rc, nvisit);
   cfg.blockDim = dim3(threads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
