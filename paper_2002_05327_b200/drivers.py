@@ -44,6 +44,8 @@ def _device(f, counts):
     """(batch [R, *counts] on cuda, batched?) without copying device input."""
     import torch
 
+    if not torch.cuda.is_available():
+        raise SolverError("no CUDA device: the B200 path has no CPU fallback")
     t = f if hasattr(f, "detach") else torch.from_numpy(np.ascontiguousarray(f, np.complex128))
     batched = tuple(t.shape[1:]) == tuple(counts)
     if not batched and tuple(t.shape) != tuple(counts):

@@ -95,3 +95,15 @@ def test_cli_configuration_errors(tmp_path, capsys):
     assert "unknown solver mode" in capsys.readouterr().err
     assert cli.main(["solve", "--set", "nodot=1", "--out", str(tmp_path)]) == 2
     assert cli.main(["pipeline", "--out", str(tmp_path)]) == 2
+
+
+def test_cli_without_a_gpu_fails_cleanly(tmp_path, capsys):
+    """No CUDA device: a solver error (exit 3) naming the missing device,
+    never a CPU fallback."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    rc = cli.main(["solve", "--config", str(G / "solve_gmres" / "input.ini"), "--out", str(tmp_path)])
+    assert rc == 3
+    assert "no CUDA device" in capsys.readouterr().err
