@@ -706,9 +706,12 @@ class DevicePlan:
             # 13.4 ms vs 14.2 at 7; 9-10 give the same as 8); staged 3D: unbounded
             cap = int(cap_env) if cap_env else (8 if max_m <= 160 else nsub * self.nsweeps)
             if self.pool is not None:
-                # out of core: a visit's solve is long next to launch costs and
-                # every miss is a factorization -- small launches, factor-local order
-                cap = min(int(cap_env) if cap_env else 2, self.pool.nslots)
+                # out of core: every miss is a factorization; factor-local order,
+                # up to 8 visits per launch so a launch's misses are factored as one
+                # batch (config 5: 415 factorizations per application at 0.75 s
+                # each, 939 s for the GMRES solve, vs 2 visits per launch: 365
+                # at 1.0 s, 1101 s -- K2b batches keep more GPCs busy)
+                cap = min(int(cap_env) if cap_env else 8, self.pool.nslots)
             if not pipelined:  # sweep-ordered launches (one per (sweep, step))
                 self.launches = []
                 for w in range(self.nsweeps):
