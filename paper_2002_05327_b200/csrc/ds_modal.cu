@@ -32,7 +32,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -323,66 +322,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
 }
 
-// Tile-list form of the same kernel (K3m-T v1b): the grid is at most one
-// wave of resident CTAs and every CTA walks the launch's list of non-empty
-// tiles (visit-major, row tiles, compact column tiles), so no CTA is
-// launched only to find its columns empty and the active tiles spread
-// evenly over the SMs.  Same tile body and arithmetic.
-#define MG_MAXJ 64
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
-__global__ void __launch_bounds__(32 * WR * WC, MINB)
-    k_modal_gemm_list(const ModalJob *__restrict__ jobs, int njob, int pass, int nrhs) {
-  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
-  extern __shared__ __align__(16) cplx smem_mg[];
-  __shared__ int act[RMAX_MODAL + 1];
-  __shared__ int toff[MG_MAXJ + 1], nact[MG_MAXJ], ctiles[MG_MAXJ];
-  pdl_wait();
-  const int t = threadIdx.x;
-  if (t < 32) {
-    for (int z = 0; z < njob; ++z) {
-      const ModalJob &J = jobs[z];
-      int cnt = 0;
-      for (int r0 = 0; r0 < nrhs; r0 += 32) {
-        const int r = r0 + t;
-        cnt += __popc(__ballot_sync(0xffffffffu, r < nrhs && (!J.nz || J.nz[r])));
-      }
-      if (t == 0) nact[z] = cnt;
-    }
-  }
-  __syncthreads();
-  if (t == 0) {
-    int acc = 0;
-    for (int z = 0; z < njob; ++z) {
-      const PassGeo G = pass_geo(*jobs[z].f, jobs[z], pass, nrhs);
-      const int ct = (G.outer * G.inner * nact[z] + TN - 1) / TN;
-      ctiles[z] = ct;
-      toff[z] = acc;
-      acc += ct * ((G.n + TM - 1) / TM);
-    }
-    toff[njob] = acc;
-  }
-  __syncthreads();
-  const int T = toff[njob];
-  int cur = -1;
-  for (int tt = blockIdx.x; tt < T; tt += gridDim.x) {
-    int z = 0;
-    while (toff[z + 1] <= tt) ++z;
-    const ModalJob &J = jobs[z];
-    const PassGeo G = pass_geo(*J.f, J, pass, nrhs);
-    const int local = tt - toff[z];
-    const int ry = local / ctiles[z], cx = local - ry * ctiles[z];
-    if (z != cur) {  // the visit's active-RHS table (all threads past the last tile's use)
-      __syncthreads();
-      active_rhs(J, nrhs, act);
-      cur = z;
-    }
-    const int A = nact[z];
-    const int total = G.outer * G.inner * A;
-    gemm_tile<MT, WR, WC, TK, NS>(G, ry * TM, cx * TN, min(TN, total - cx * TN), smem_mg, act, A,
-                                  nrhs);
-  }
-}
-
 // ------------------------------------------- mode-wise recurrences (K3m-R)
 // One thread per (visit, mode j, RHS r): forward elimination and back
 // substitution along the block axis, in place on the transformed buffer.
@@ -670,22 +609,8 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
     gy = std::max(gy, (G.n + TM - 1) / TM);
   }
-  static const int list_form = getenv("DS_MG_LIST") ? atoi(getenv("DS_MG_LIST")) : 0;  // TEMP A/B
-  if (list_form && njob <= MG_MAXJ) {
-    static bool attr2 = false;
-    if (!attr2) {
-      DS_CUDA(cudaFuncSetAttribute(k_modal_gemm_list<MT, WR, WC, TK, MINB, NS>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr2 = true;
-    }
-    const int slots = ctx->num_sms * MINB;
-    const int tiles = std::min<int64_t>((int64_t)gx * gy * njob, 1 << 30);
-    DS_CUDA(launch_pdl(k_modal_gemm_list<MT, WR, WC, TK, MINB, NS>, dim3(std::max(1, std::min(slots, tiles))),
-                       dim3(32 * WR * WC), smem, ctx->stream, jobs_dev, njob, pass, nrhs));
-  } else {
-    DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
-                       ctx->stream, jobs_dev, pass, nrhs));
-  }
+  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
+                     ctx->stream, jobs_dev, pass, nrhs));
 
   ctx->launches++;
   DS_CHECK_LAUNCH();
