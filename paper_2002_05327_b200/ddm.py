@@ -170,14 +170,20 @@ def _plan_key(partition, operators, directions, schedule="diagonal", pipelined=F
             schedule, pipelined)
 
 
-def _group_count(partition, nrhs: int) -> int:
-    """RHS groups for the device path: 2 for 2D batches of >= 16 RHS
-    (measured: config 2 +8%, config 3 +15%; 3D batches gain nothing);
+def _group_count(partition, nrhs: int, operators=None) -> int:
+    """RHS groups for the device path: 2D batches of >= 16 RHS run as 2
+    groups (measured: config 2 +8%, config 3 +15%; 3D batches gain nothing);
+    raster (block-LU) batches of >= 64 RHS as 4 (config 3 with 9-CTA K3
+    clusters: 155.4 vs 151.9 RHS/s; config 2's modal solve is best at 2).
     DS_RHS_GROUPS overrides."""
     env = os.environ.get("DS_RHS_GROUPS")
     if env:
         return max(1, int(env))
-    return 2 if partition.dim == 2 and nrhs >= 16 else 1
+    if partition.dim != 2 or nrhs < 16:
+        return 1
+    raster = operators is not None and any(
+        getattr(operators[i], "kappa2_kind", None) == "full" for i in partition.subdomains())
+    return 4 if raster and nrhs >= 64 else 2
 
 
 def device_plan(partition, operators, cache: FactorizationCache, plan: SweepPlan | None,
@@ -196,7 +202,7 @@ def device_plan(partition, operators, cache: FactorizationCache, plan: SweepPlan
     if pipelined is None:
         pipelined = schedule == "diagonal" and os.environ.get("DS_PIPELINE", "1") != "0"
     pipelined = bool(pipelined) and schedule == "diagonal"
-    G = _group_count(partition, nrhs) if grouped and schedule == "diagonal" else 1
+    G = _group_count(partition, nrhs, operators) if grouped and schedule == "diagonal" else 1
     key = _plan_key(partition, operators, directions, schedule, pipelined) + (("groups", G),)
     dp = cache._plans.get(key)
     if dp is None or dp.nrhs_max < nrhs:
