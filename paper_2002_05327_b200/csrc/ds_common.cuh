@@ -130,6 +130,7 @@ struct ds_options {
   int k3_cluster = 0;  // DS_K3_CLUSTER: force 8 or 16 CTAs per cluster (0 = choose)
   int k2b_3m = 1;      // DS_K2B_3M: K2b trailing updates as 3M GEMMs (cublasZgemm3m)
   int hio_dstreams = 2;  // DS_HIO_DSTREAMS: download streams of the pinned-host path
+  int kskip = 1;       // DS_KSKIP: forward transforms visit only the nonzero K-chunks (K6 masks)
 };
 void ds_options_from_env(ds_options &o);
 
@@ -240,6 +241,10 @@ struct ModalJob {
   cplx *x;
   cplx *s0, *s1;
   const int *nz;  // per-RHS nonzero flags (NULL = solve all)
+  // nonzero K-chunks of the first forward pass's input (NULL = dense): one
+  // word per input row (2D: block k; 3D: (k, i0)), bit c set when some node
+  // with in-slab index 8c .. 8c+7 of that row is nonzero (written by K6)
+  const uint32_t *km;
 };
 // launch the modal solve of njob visits (device job table; facts_host: the
 // jobs' factor layouts, for grid sizing)

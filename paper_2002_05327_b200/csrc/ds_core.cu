@@ -83,6 +83,7 @@ void ds_options_from_env(ds_options &o) {
   o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
   o.k2b_3m = env_opt("DS_K2B_3M", 1) != 0;
+  o.kskip = env_opt("DS_KSKIP", 1) != 0;
 }
 
 // name -> member of ds_options
@@ -103,6 +104,7 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "k3_cluster") return &o.k3_cluster;
   if (k == "hio_dstreams") return &o.hio_dstreams;
   if (k == "k2b_3m") return &o.k2b_3m;
+  if (k == "kskip") return &o.kskip;
   return nullptr;
 }
 

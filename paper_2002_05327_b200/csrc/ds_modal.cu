@@ -185,11 +185,14 @@ __device__ __forceinline__ void cp_wait() {
 // 16 columns are all past colw skip the products).
 // NS-stage cp.async ring: chunk kc lives in buffer kc % NS; NS - 1 chunks
 // are in flight while one is multiplied (NS = 2: double buffering).
+// The K-chunks visited: sparse -- the set bits of kmask in ascending order
+// (the others hold exact zeros of B: skipping them leaves every sum's value
+// unchanged); dense -- chunks 0 .. nkc-1.
 template <int MT, int WR, int WC, int TK, int NS = 2>
-__device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0, int colw, int kc0,
-                                           int kc1, cplx *smem_mg, const int *act, int A, int nrhs,
-                                           double (&p1)[MT][2][2], double (&p2)[MT][2][2],
-                                           double (&p3)[MT][2][2]) {
+__device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0, int colw, bool sparse,
+                                           uint32_t kmask, int nkc, cplx *smem_mg, const int *act,
+                                           int A, int nrhs, double (&p1)[MT][2][2],
+                                           double (&p2)[MT][2][2], double (&p3)[MT][2][2]) {
   constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
@@ -227,17 +230,26 @@ __device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0,
   const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
   const int wr = warp % WR, wc = warp / WR;
   const bool wact = wc * 16 < colw;
-  // prologue: chunks kc0 .. kc0+NS-2 (empty commit groups keep the group count)
+  const int nk = sparse ? __popc(kmask) : nkc;
+  uint32_t rem = kmask;
+  int seq = 0;
+  auto next_chunk = [&]() -> int {  // the next chunk to stage
+    if (!sparse) return seq++;
+    const int k = __ffs(rem) - 1;
+    rem &= rem - 1;
+    return k;
+  };
+  // prologue: the first NS-1 chunks (empty commit groups keep the group count)
 #pragma unroll
   for (int i = 0; i < NS - 1; ++i) {
-    if (kc0 + i < kc1) stage(kc0 + i, i);
+    if (i < nk) stage(next_chunk(), i);
     else cp_commit();
   }
-  for (int kc = kc0; kc < kc1; ++kc) {
-    const int buf = (kc - kc0) % NS;
-    cp_wait<NS - 2>();  // chunk kc landed (this thread's copies)
-    __syncthreads();    // ... and every thread's; buffer (kc - 1) % NS is free
-    if (kc + NS - 1 < kc1) stage(kc + NS - 1, (kc - kc0 + NS - 1) % NS);
+  for (int it = 0; it < nk; ++it) {
+    const int buf = it % NS;
+    cp_wait<NS - 2>();  // chunk it landed (this thread's copies)
+    __syncthreads();    // ... and every thread's; buffer (it - 1) % NS is free
+    if (it + NS - 1 < nk) stage(next_chunk(), (it + NS - 1) % NS);
     else cp_commit();
     if (wact) {
       const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
@@ -276,6 +288,14 @@ __device__ __forceinline__ void gemm_store(const PassGeo &G, int row0, int col0,
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
   const int wr = warp % WR, wc = warp / WR;
   if (wc * 16 >= colw) return;
+  int64_t coff[2][2];  // the thread's 4 output columns (row 0 offsets)
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int cc = wc * 16 + nt * 8 + 2 * tg + e;
+      coff[nt][e] = cc < colw ? col_offset(G, col0 + cc, A, act, nrhs) : -1;
+    }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     const int gr = row0 + wr * 8 * MT + mt * 8 + g;
@@ -284,9 +304,8 @@ __device__ __forceinline__ void gemm_store(const PassGeo &G, int row0, int col0,
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int cc = wc * 16 + nt * 8 + 2 * tg + e;
-        if (cc >= colw) continue;
-        const int64_t off = col_offset(G, col0 + cc, A, act, nrhs) + (int64_t)gr * G.ncols;
+        if (coff[nt][e] < 0) continue;
+        const int64_t off = coff[nt][e] + (int64_t)gr * G.ncols;
         G.out[off] = make_double2(p1[mt][nt][e] - p2[mt][nt][e],
                                   p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]);
       }
@@ -294,21 +313,29 @@ __device__ __forceinline__ void gemm_store(const PassGeo &G, int row0, int col0,
 }
 
 template <int MT, int WR, int WC, int TK, int NS = 2>
-__device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw,
-                                          cplx *smem_mg, const int *act, int A, int nrhs) {
+__device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, int colw, bool sparse,
+                                          uint32_t kmask, cplx *smem_mg, const int *act, int A,
+                                          int nrhs) {
   double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
   const int nkc = (G.n + TK - 1) / TK;
-  gemm_accum<MT, WR, WC, TK, NS>(G, row0, col0, colw, 0, nkc, smem_mg, act, A, nrhs, p1, p2, p3);
+  gemm_accum<MT, WR, WC, TK, NS>(G, row0, col0, colw, sparse, kmask, nkc, smem_mg, act, A, nrhs, p1,
+                                 p2, p3);
   gemm_store<MT, WR, WC>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
 }
 
-// one tile per CTA: grid (column tiles, row tiles, visits)
+// one tile per CTA: grid (column tiles, row tiles, visits).  kskip: the
+// first forward pass visits only the K-chunks that K6 marked nonzero in any
+// of the tile's input rows (J.km; payload-only visits: ~70% of the chunks
+// are exact zeros -- the payload bands are thin strips of the window), which
+// shortens the tile's latency chain, not just its arithmetic.
 template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
 __global__ void __launch_bounds__(32 * WR * WC, MINB)
-    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs) {
+    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs, int kskip) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
+  static_assert(TK == 8, "K6 chunk masks are in units of 8");
   extern __shared__ __align__(16) cplx smem_mg[];
   __shared__ int act[RMAX_MODAL + 1];
+  __shared__ uint32_t s_kmask;
   const ModalJob J = jobs[blockIdx.z];
   const FactDev f = *J.f;
   const PassGeo G = pass_geo(f, J, pass, nrhs);
@@ -319,7 +346,21 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   const int A = active_rhs(J, nrhs, act);
   const int total = G.outer * G.inner * A;  // compact columns
   if (col0 >= total) return;
-  gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, min(TN, total - col0), smem_mg, act, A, nrhs);
+  const int colw = min(TN, total - col0);
+  // pass 0 has inner == 1: compact column c is (input row c / A, RHS)
+  const bool sparse = kskip && pass == 0 && J.km != nullptr && G.inner == 1;
+  if (sparse) {
+    if (threadIdx.x < 32) {
+      const int b0 = col0 / A, b1 = (col0 + colw - 1) / A;
+      uint32_t mk = 0;
+      for (int b = b0 + (int)threadIdx.x; b <= b1; b += 32) mk |= J.km[b];
+      mk = __reduce_or_sync(0xffffffffu, mk);
+      if (threadIdx.x == 0) s_kmask = mk;
+    }
+    __syncthreads();
+  }
+  gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, colw, sparse, sparse ? s_kmask : 0u, smem_mg, act, A,
+                                nrhs);
 }
 
 // ------------------------------------------- mode-wise recurrences (K3m-R)
@@ -610,7 +651,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     gy = std::max(gy, (G.n + TM - 1) / TM);
   }
   DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
-                     ctx->stream, jobs_dev, pass, nrhs));
+                     ctx->stream, jobs_dev, pass, nrhs, ctx->opt.kskip));
 
   ctx->launches++;
   DS_CHECK_LAUNCH();

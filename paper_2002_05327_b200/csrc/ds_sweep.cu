@@ -54,6 +54,7 @@ struct VisitDev {
   cplx *rhs, *x;
   int *nz;
   const int *arr;  // arrival counts of this visit [nrhs] (per-call stride)
+  uint32_t *km;    // modal visits: nonzero K-chunk masks of the assembled rhs (ModalJob::km)
 };
 
 struct XferDev {
@@ -127,6 +128,11 @@ struct ds_plan {
   size_t slot_bytes = 0;
   std::map<std::tuple<int, int, int>, SlotRef> slot_by_key;  // (use-1, target, dir) -> slot (ds_plan_slot)
   int **d_flag_bases = nullptr;  // [nranks] flag words of every rank (device table)
+  // K-chunk masks of the modal visits' rhs (K6 -> first forward transform),
+  // zeroed with the flags at the start of every application
+  uint32_t *kmask = nullptr;
+  int64_t kmask_words = 0;
+  int km_rows_max = 0;
   bool k5_pending[2] = {false, false};
   // graph
   bool use_graph = false;
@@ -328,13 +334,14 @@ __device__ __forceinline__ void arrival_words(int *base, int nsweeps, int nsub, 
 // one kernel instead of a kernel and three memset nodes (measured: a memset
 // node at the head of the host-path graph cost ~0.3 ms end to end)
 __global__ void k_zero_io(cplx *const *__restrict__ io, int64_t n, int *flags, int64_t nflags,
-                          int64_t cut0, int64_t cut1) {
+                          int64_t cut0, int64_t cut1, uint32_t *km, int64_t nkm) {
   cplx *u = io[1];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     u[i] = make_double2(0.0, 0.0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nflags; i += stride)
     flags[i] = (i >= cut0 && i < cut1) ? 0x3f3f3f3f : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nkm; i += stride) km[i] = 0u;
 }
 
 // ------------------------------------------------------------- K6 assemble
@@ -363,6 +370,12 @@ __global__ void __launch_bounds__(256)
   const bool own = V.sweep == 1;
   const bool masks = ns <= 31;
   const int E0 = sd.win_shape[0], E1 = sd.win_shape[1], E2 = dim == 3 ? sd.win_shape[2] : 0;
+  // modal visits: per input row of the first forward transform, the 8-wide
+  // K-chunks holding a nonzero rhs value (ModalJob::km), OR-ed in shared memory
+  uint32_t *s_km = s_mask + (E0 + E1 + E2);
+  const int km_nl = V.km ? (fd.naxes == 2 ? fd.nax[1] : fd.m) : 0;
+  const int km_rows = V.km ? fd.nb * (fd.m / km_nl) : 0;
+  for (int x = t; x < km_rows; x += blockDim.x) s_km[x] = 0u;
   __syncthreads();
   if (masks) {
     for (int x = t; x < E0 + E1 + E2; x += blockDim.x) {
@@ -394,8 +407,16 @@ __global__ void __launch_bounds__(256)
     osh[a] = sd.own_shape[a];
   }
   bool any[RV] = {}, anyown[RV] = {};
-  if (ln < npb) {
-    for (int blk = blockIdx.x * npb + ln; blk < nodes; blk += gridDim.x * npb) {
+  // warp-uniform trip count (the K-chunk mask aggregation below is a
+  // full-warp collective); lanes past their own trips run it idle
+  const int first = blockIdx.x * npb + ln, nstride = gridDim.x * npb;
+  const int trips = (ln < npb && first < nodes) ? (nodes - first + nstride - 1) / nstride : 0;
+  const int wtrips = __reduce_max_sync(0xffffffffu, trips);
+  for (int it = 0; it < wtrips; ++it) {
+    const int blk = first + it * nstride;
+    int km_row = -1;
+    uint32_t km_bit = 0u;
+    if (it < trips) {
       int c[3], g[3];
       block_coords(fd, blk, c);
 #pragma unroll
@@ -453,10 +474,33 @@ __global__ void __launch_bounds__(256)
         }
       }
       cplx *dst = V.rhs + (int64_t)blk * nrhs + rl;
+      bool nzn = false;
 #pragma unroll
       for (int j = 0; j < RV; ++j) {
         if (s_live[rl + j]) dst[j] = val[j];
-        any[j] |= cnonzero(val[j]);
+        const bool nzv = cnonzero(val[j]);
+        any[j] |= nzv;
+        nzn |= nzv;
+      }
+      if (km_nl && nzn) {
+        // input row of the first forward pass and the node's K index: 2D
+        // (row k, i); 3D (row (k, i0), i1)
+        int kidx = sel3(c, fd.other[0]);
+        km_row = sel3(c, fd.block_axis);
+        if (fd.other[1] >= 0) {
+          km_row = km_row * sel3(fd.win_shape, fd.other[0]) + kidx;
+          kidx = sel3(c, fd.other[1]);
+        }
+        km_bit = 1u << (kidx >> 3);
+      }
+    }
+    if (km_nl) {  // one shared atomic per distinct row of the warp (consecutive nodes: 1-2 rows)
+      unsigned todo = __ballot_sync(0xffffffffu, km_bit != 0u);
+      while (todo) {
+        const int r0 = __shfl_sync(0xffffffffu, km_row, __ffs(todo) - 1);
+        const uint32_t b = __reduce_or_sync(0xffffffffu, km_row == r0 ? km_bit : 0u);
+        if ((int)(threadIdx.x & 31) == __ffs(todo) - 1 && (s_km[r0] & b) != b) atomicOr(&s_km[r0], b);
+        todo &= ~__ballot_sync(0xffffffffu, km_row == r0);
       }
     }
   }
@@ -470,6 +514,8 @@ __global__ void __launch_bounds__(256)
     if (s_nz[q]) atomicOr(&V.nz[q], 1);
     if (s_own[q]) atomicOr(&F.own_nz[(size_t)V.sub * nrhs + q], 1);
   }
+  for (int x = t; x < km_rows; x += blockDim.x)
+    if (s_km[x]) atomicOr(&V.km[x], s_km[x]);
 }
 
 // ----------------------------------------------------------- K5 accumulate
@@ -1245,6 +1291,7 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (nfac) cudaMemcpy(dfac, d->xfac, sizeof(double) * nfac, cudaMemcpyHostToDevice);
   // ---- visits in execution order
   std::vector<VisitDev> hv;
+  std::vector<std::pair<size_t, size_t>> km_at;  // (visit, mask word offset)
   std::vector<SolveVisit> hsv;
   P->blu_off.assign((size_t)(sched ? d->nlaunch : nsw * nst) + 1, 0);
   P->mod_off.assign(P->blu_off.size(), 0);
@@ -1296,6 +1343,13 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
         visit_of[(size_t)w * nsub + s] = (int)hv.size();
         hv.push_back(V);
         if (hf[s].kind == 1) {
+          const int nl = hf[s].naxes == 2 ? hf[s].nax[1] : hf[s].m;  // K extent of forward pass 0
+          const int rows = hf[s].nb * (hf[s].m / nl);
+          if (nl <= 256 && rows <= 8192) {  // 32 chunks of 8 per mask word; K6 shared memory
+            km_at.emplace_back(hv.size() - 1, (size_t)P->kmask_words);
+            P->kmask_words += rows;
+            P->km_rows_max = std::max(P->km_rows_max, rows);
+          }
           cplx *s0 = mscr + ((size_t)(parity * 2 + 0) * P->gmax + gi) * vbuf;
           cplx *s1 = mscr + ((size_t)(parity * 2 + 1) * P->gmax + gi) * vbuf;
           P->h_mjobs.push_back(ModalJob{P->facts + s, V.rhs, V.x, s0, s1, nullptr});
@@ -1382,6 +1436,13 @@ extern "C" int ds_plan_create(ds_ctx *ctx, const ds_plan_desc *d, ds_plan **out)
   if (plan_alloc(P, &mem, sizeof(XferRec) * std::max<size_t>(hx.size(), 1))) return fail(DS_ECUDA);
   P->recs = (XferRec *)mem;
   P->peers_set = !sharded;
+  if (P->kmask_words > 0) {
+    if (plan_alloc(P, &mem, sizeof(uint32_t) * P->kmask_words)) return fail(DS_ECUDA);
+    P->kmask = (uint32_t *)mem;
+    cudaMemset(P->kmask, 0, sizeof(uint32_t) * P->kmask_words);
+    for (auto &e : km_at) hv[e.first].km = P->kmask + e.second;
+    for (size_t j = 0; j < P->h_mjobs.size(); ++j) P->h_mjobs[j].km = hv[P->mod_vidx[j]].km;
+  }
   P->h_visits = hv;
   P->h_solve = hsv;
   P->patched_nrhs = 0;
@@ -1668,7 +1729,7 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       const int64_t nflags = (int64_t)P->nsub * nrhs + 4 * (int64_t)per + nrhs;
       const int64_t cut0 = F.arr_cut - F.own_nz, cut1 = cut0 + (int64_t)per;
       k_zero_io<<<(unsigned)std::min<int64_t>((std::max(n, nflags) + 255) / 256, (int64_t)ctx->num_sms * 8),
-                  256, 0, st>>>(P->d_io, n, F.own_nz, nflags, cut0, cut1);
+                  256, 0, st>>>(P->d_io, n, F.own_nz, nflags, cut0, cut1, P->kmask, P->kmask_words);
       ctx->launches++;
       DS_CHECK_LAUNCH();
     }
@@ -1730,25 +1791,25 @@ static int issue_apply(ds_plan *P, const cplx *f, cplx *u, int nrhs, cplx *parti
       if (skip_cls & 1) {
       } else if (k6rv == 8 && nrhs % 8 == 0)
         DS_CUDA(launch_pdl(outer ? k_assemble<8, true> : k_assemble<8, false>, dim3(bx, G), dim3(256),
-                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           sizeof(uint32_t) * (P->max_axis_sum + P->km_rows_max), st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
                            (const SlotRef *)P->slots, f, nrhs, dim,
                            P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
       else if (k6rv == 2 && nrhs % 2 == 0)
         DS_CUDA(launch_pdl(outer ? k_assemble<2, true> : k_assemble<2, false>, dim3(bx, G), dim3(256),
-                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           sizeof(uint32_t) * (P->max_axis_sum + P->km_rows_max), st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
                            (const SlotRef *)P->slots, f, nrhs, dim,
                            P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
       else if (k6rv >= 4 && nrhs % 4 == 0)
         DS_CUDA(launch_pdl(outer ? k_assemble<4, true> : k_assemble<4, false>, dim3(bx, G), dim3(256),
-                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           sizeof(uint32_t) * (P->max_axis_sum + P->km_rows_max), st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
                            (const SlotRef *)P->slots, f, nrhs, dim,
                            P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));
       else
         DS_CUDA(launch_pdl(outer ? k_assemble<1, true> : k_assemble<1, false>, dim3(bx, G), dim3(256),
-                           sizeof(uint32_t) * P->max_axis_sum, st,
+                           sizeof(uint32_t) * (P->max_axis_sum + P->km_rows_max), st,
                            (const VisitDev *)(P->visits + v0), (const SubDev *)P->subs,
                            (const SlotRef *)P->slots, f, nrhs, dim,
                            P->gcounts[0], P->gcounts[1], P->gcounts[2], F, (int64_t)P->nnodes));

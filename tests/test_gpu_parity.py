@@ -953,3 +953,47 @@ def test_stencil_3d_ragged_regions(cuda, cfg):
         got = np.asarray(gop.apply(v, region=reg))
         for r in range(3):
             assert rel(got[r], ogop.apply(v[r], reg.lo)) <= 1e-14, (lo, hi, r)
+
+
+@pytest.mark.parametrize("which", ["cfg1", "mini3d"])
+@pytest.mark.parametrize("option", ["kskip"])
+def test_transform_work_skips_exact(cuda, cfg1, which, option):
+    """Option "kskip" (default on): the first forward transform of a modal
+    visit walks only the 8-wide K-chunks that K6 marked nonzero; the
+    skipped terms are products with exact zeros, so u equals the dense walk
+    value for value (2D: config 1 with random and point sources; 3D: the
+    2x2x2 mini problem, whose first pass runs along in-slab axis 1).  Fresh
+    plans per setting (graphs keep the options they were recorded with)."""
+    import torch
+
+    from paper_2002_05327_b200 import _engine
+    from paper_2002_05327_b200.ddm import SweepPlan
+
+    if which == "cfg1":
+        s, b = cfg1[0], cfg1[1]
+        rng = np.random.default_rng(11)
+        f = np.concatenate([rng.standard_normal((2,) + b["grid"].counts),
+                            configs.sources(s, b["grid"], centers=[(0.3, 0.4), (0.8, 0.15)])])
+        dim = 2
+    else:
+        s, b = mini3d()
+        f = np.concatenate([configs.sources(s, b["grid"]),
+                            np.random.default_rng(12).standard_normal((1,) + b["grid"].counts)])
+        dim = 3
+    R = f.shape[0]
+    fd = torch.from_numpy(f.astype(np.complex128).reshape(R, -1)).cuda()
+    cache = FactorizationCache()
+
+    def run(value):
+        old = _engine.set_option(option, value)
+        try:
+            dp = _engine.DevicePlan(b["partition"], b["ops"], cache, SweepPlan.default(dim).directions, R,
+                                    pipelined=True)
+            u, _ = dp.apply(fd)
+            return u.cpu().numpy()
+        finally:
+            _engine.set_option(option, old)
+
+    dense, sparse = run(0), run(1)
+    assert np.array_equal(dense, sparse)
+    assert np.count_nonzero(sparse) > 0
