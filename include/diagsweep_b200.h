@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DS_ABI_VERSION 6
+#define DS_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define DS_API __attribute__((visibility("default")))
@@ -75,6 +75,13 @@ DS_API int ds_ctx_destroy(ds_ctx *ctx);
 /* Kernels this library has launched on `ctx` so far (graph replays count
  * their captured launches).  Diagnostic: bench.py's `gpu_launches`. */
 DS_API int64_t ds_ctx_launches(const ds_ctx *ctx);
+/* (ABI 7) Complex multiply-adds the modal transforms (K3m-T) executed on
+ * `ctx` while the option "count_work" was 1: per tile, valid rows x valid
+ * columns x the K extent actually multiplied (exact-zero RHS columns and
+ * skipped all-zero K-chunks not counted).  Synchronizes the context's
+ * stream; `reset` != 0 zeroes the counter.  Measurement only: bench.py's
+ * roofline numerator (the reference has no counterpart). */
+DS_API int ds_ctx_work(ds_ctx *ctx, int64_t *cmacs, int32_t reset);
 /* Variant / tuning options of a context (ABI 5), read at every launch (a
  * plan's captured CUDA graph keeps the choices it was recorded with).
  * Defaults are the measured-best choices; a DS_<NAME> environment variable
@@ -89,7 +96,11 @@ DS_API int64_t ds_ctx_launches(const ds_ctx *ctx);
  *   "k3g_mma" staged block product on DMMA 1 / 0; "stage_rows";
  *   "k3_warps" 4 / 8, "k3_rc_min", "k3_rc_max", "k3_cluster" 0 / 8 / 16:
  *     the cluster block solve's configuration search;
- *   "hio_dstreams" download streams of ds_ddm_apply_host (>= 2).
+ *   "hio_dstreams" download streams of ds_ddm_apply_host (>= 2);
+ *   "kskip" forward transforms skip all-zero K-chunks 1 / 0;
+ *   "r3_cols" (mode, RHS) columns per block of the segmented mode-wise
+ *     recurrences 16 (default) / 32;
+ *   "count_work" 0 / 1 (see ds_ctx_work).
  * Unknown names or values: < 0. */
 DS_API int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value);
 DS_API int ds_ctx_get_option(const ds_ctx *ctx, const char *name, int32_t *value);

@@ -70,6 +70,16 @@ def set_option(name: str, value: int) -> int:
     return old.value
 
 
+def executed_work(reset: bool = False) -> int:
+    """Complex multiply-adds the modal transforms executed on this device's
+    context while the option "count_work" was 1 (ds_ctx_work); measurement
+    only (bench.py's roofline numerator)."""
+    lib, ctx = context()
+    v = C.c_int64()
+    N.check(lib.ds_ctx_work(ctx, C.byref(v), 1 if reset else 0), "ds_ctx_work")
+    return int(v.value)
+
+
 def get_option(name: str) -> int:
     lib, ctx = context()
     v = C.c_int32()

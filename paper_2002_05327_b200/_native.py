@@ -88,6 +88,7 @@ _SIGNATURES = [
     ("ds_ctx_set_stream", C.c_int, [vp, vp]),
     ("ds_ctx_synchronize", C.c_int, [vp]),
     ("ds_ctx_launches", i64, [vp]),
+    ("ds_ctx_work", C.c_int, [vp, vp, i32]),
     ("ds_ctx_set_option", C.c_int, [vp, C.c_char_p, i32]),
     ("ds_ctx_get_option", C.c_int, [vp, C.c_char_p, P_i32]),
     ("ds_ctx_destroy", C.c_int, [vp]),
@@ -141,7 +142,7 @@ _SIGNATURES = [
     ("ds_gaussian_fields", C.c_int, [vp, i32, vp, i32, vp, vp, vp, i32, vp]),
 ]
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]
 

@@ -131,6 +131,8 @@ struct ds_options {
   int k2b_3m = 1;      // DS_K2B_3M: K2b trailing updates as 3M GEMMs (cublasZgemm3m)
   int hio_dstreams = 2;  // DS_HIO_DSTREAMS: download streams of the pinned-host path
   int kskip = 1;       // DS_KSKIP: forward transforms visit only the nonzero K-chunks (K6 masks)
+  int r3_cols = 16;    // DS_R3_COLS: (mode, RHS) columns per block of the segmented recurrences (16 default, 32)
+  int count_work = 0;  // modal transforms add the complex multiply-adds they execute to ds_ctx::work
 };
 void ds_options_from_env(ds_options &o);
 
@@ -143,6 +145,9 @@ struct ds_ctx {
   // scratch for reductions
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
+  // device counter of executed complex multiply-adds (option "count_work",
+  // read by ds_ctx_work; measurement only)
+  unsigned long long *work = nullptr;
 };
 
 // device-side operator view (coefficient arrays are device pointers)

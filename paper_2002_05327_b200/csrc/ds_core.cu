@@ -51,6 +51,12 @@ extern "C" int ds_ctx_create(int device, void *stream, ds_ctx **out) {
     delete c;
     return ds_fail(DS_ECUDA, "ds_ctx_create: scratch allocation failed");
   }
+  if (cudaMalloc((void **)&c->work, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(c->work, 0, sizeof(unsigned long long)) != cudaSuccess) {
+    cudaFree(c->scratch);
+    delete c;
+    return ds_fail(DS_ECUDA, "ds_ctx_create: counter allocation failed");
+  }
   *out = c;
   return DS_OK;
 }
@@ -84,6 +90,7 @@ void ds_options_from_env(ds_options &o) {
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
   o.k2b_3m = env_opt("DS_K2B_3M", 1) != 0;
   o.kskip = env_opt("DS_KSKIP", 1) != 0;
+  o.r3_cols = env_opt("DS_R3_COLS", 16) == 32 ? 32 : 16;
 }
 
 // name -> member of ds_options
@@ -105,6 +112,8 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "hio_dstreams") return &o.hio_dstreams;
   if (k == "k2b_3m") return &o.k2b_3m;
   if (k == "kskip") return &o.kskip;
+  if (k == "count_work") return &o.count_work;
+  if (k == "r3_cols") return &o.r3_cols;
   return nullptr;
 }
 
@@ -119,6 +128,7 @@ extern "C" int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value) {
   else if (k == "k4") ok = value >= 0 && value <= 3;
   else if (k == "k6_rv" || k == "k4_rv") ok = value == 1 || value == 2 || value == 4 || value == 8;
   else if (k == "k3_warps") ok = value == 4 || value == 8;
+  else if (k == "r3_cols") ok = value == 16 || value == 32;
   else if (k == "k3_cluster") ok = value == 0 || (value >= 8 && value <= 16);
   else ok = value >= 0;
   if (!ok) return ds_fail(DS_ECONFIG, "ds_ctx_set_option: bad value for " + k);
@@ -149,9 +159,20 @@ extern "C" int ds_ctx_synchronize(ds_ctx *ctx) {
 
 extern "C" int64_t ds_ctx_launches(const ds_ctx *ctx) { return ctx ? ctx->launches : -1; }
 
+extern "C" int ds_ctx_work(ds_ctx *ctx, int64_t *cmacs, int32_t reset) {
+  if (!ctx || !cmacs) return ds_fail(DS_ECONFIG, "ds_ctx_work: null argument");
+  unsigned long long v = 0;
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  DS_CUDA(cudaMemcpy(&v, ctx->work, sizeof(v), cudaMemcpyDeviceToHost));
+  if (reset) DS_CUDA(cudaMemset(ctx->work, 0, sizeof(v)));
+  *cmacs = (int64_t)v;
+  return DS_OK;
+}
+
 extern "C" int ds_ctx_destroy(ds_ctx *ctx) {
   if (!ctx) return DS_OK;
   cudaFree(ctx->scratch);
+  cudaFree(ctx->work);
   delete ctx;
   return DS_OK;
 }

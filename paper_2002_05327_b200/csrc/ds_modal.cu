@@ -130,12 +130,12 @@ __device__ __forceinline__ bool job_any(const ModalJob &J, int nrhs) {
 // transforms and recurrences also skip the exact-zero RHS columns of
 // visits with some nonzero RHS (config 2: 42% of the (visit, RHS) pairs are
 // nonzero, 87% of the visits).  Returns the count; call from all threads.
-__device__ __forceinline__ int active_rhs(const ModalJob &J, int nrhs, int *act) {
+__device__ __forceinline__ int active_rhs(const int *nz, int nrhs, int *act) {
   if (threadIdx.x < 32) {
     int base = 0;
     for (int r0 = 0; r0 < nrhs; r0 += 32) {
       const int r = r0 + (int)threadIdx.x;
-      const bool on = r < nrhs && (!J.nz || J.nz[r]);
+      const bool on = r < nrhs && (!nz || nz[r]);
       const unsigned mk = __ballot_sync(0xffffffffu, on);
       if (on) act[base + __popc(mk & ((1u << threadIdx.x) - 1))] = r;
       base += __popc(mk);
@@ -168,6 +168,18 @@ __device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes) 
                "r"(src_bytes)
                : "memory");
 }
+// the same with a shared-memory byte address
+__device__ __forceinline__ void cp16s(uint32_t dst, const void *src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+// DMMA without `volatile`: the scheduler may move it across the cp.async
+// issue of the same loop iteration (its operands are registers only)
+__device__ __forceinline__ void dmma_nv(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -181,8 +193,7 @@ __device__ __forceinline__ void cp_wait() {
 // product (as K3, ds_mma.cuh).  Row pitches: A % 8 == 4, B % 8 == 2 complex
 // (conflict-free fragment loads).
 // The tile body: rows [row0, row0 + TM) x columns [col0, col0 + colw),
-// colw <= TN (columns past colw are zero-filled and not stored; warps whose
-// 16 columns are all past colw skip the products).
+// colw <= TN (columns past colw are zero-filled and not stored).
 // NS-stage cp.async ring: chunk kc lives in buffer kc % NS; NS - 1 chunks
 // are in flight while one is multiplied (NS = 2: double buffering).
 // The K-chunks visited: sparse -- the set bits of kmask in ascending order
@@ -196,81 +207,97 @@ __device__ __forceinline__ void gemm_accum(const PassGeo &G, int row0, int col0,
   constexpr int NTH = 32 * WR * WC, TM = 8 * MT * WR, TN = 16 * WC;
   constexpr int AP = TK + 4, BP = TN + 2;
   static_assert(NTH % TK == 0 && NTH % TN == 0, "tile/thread mapping");
-  auto sA = [&](int buf) { return smem_mg + buf * (TM * AP); };
-  auto sB = [&](int buf) { return smem_mg + NS * TM * AP + buf * (TK * BP); };
+  constexpr int A_STEP = NTH / TK, A_N = TM / A_STEP;
+  constexpr int B_STEP = NTH / TN, B_N = TK / B_STEP;
+  static_assert(TM % A_STEP == 0 && TK % B_STEP == 0, "staging maps cover the tiles exactly");
+  constexpr uint32_t A_BUF = TM * AP * sizeof(cplx), B_BUF = TK * BP * sizeof(cplx);
   const int n = G.n;
   const int t = threadIdx.x;
-  // staging maps: A -- fixed column t % TK, rows t / TK + q * (NTH / TK);
-  // B -- fixed column t % TN, rows t / TN + q * (NTH / TN)
+  // staging maps: A -- fixed column t % TK, rows t / TK + q * A_STEP;
+  // B -- fixed column t % TN, rows t / TN + q * B_STEP.  Everything that
+  // does not depend on the chunk is hoisted: per-thread source pointers at
+  // chunk 0, shared-memory byte addresses in ring buffer 0, and the row /
+  // column validity bits; a chunk then costs one multiply-add per copy.
   const int a_col = t % TK, a_row = t / TK;
-  constexpr int A_STEP = NTH / TK, A_N = TM / A_STEP;
   const int b_col = t % TN, b_row = t / TN;
-  constexpr int B_STEP = NTH / TN, B_N = (TK + B_STEP - 1) / B_STEP;
-  const int gcol = col0 + b_col;
   const bool bcol_ok = b_col < colw;
-  const int64_t bbase = bcol_ok ? col_offset(G, gcol, A, act, nrhs) : 0;
-  auto stage = [&](int kc, int buf) {
+  const cplx *srcA[A_N];
+  bool okA[A_N];
+#pragma unroll
+  for (int q = 0; q < A_N; ++q) {
+    const int gr = row0 + a_row + q * A_STEP;
+    okA[q] = gr < n;
+    srcA[q] = G.A + (okA[q] ? (int64_t)gr * n + a_col : 0);
+  }
+  const cplx *srcB = G.in + (bcol_ok ? col_offset(G, col0 + b_col, A, act, nrhs) + (int64_t)b_row * G.ncols : 0);
+  const int ncols = G.ncols;
+  const uint32_t dstA = smem_addr(smem_mg + a_row * AP + a_col);
+  const uint32_t dstB = smem_addr(smem_mg + NS * TM * AP + b_row * BP + b_col);
+  // stage chunk kc into ring buffer buf; on == false issues zero-filling
+  // copies from a valid address (the loop below stays branch-free, so the
+  // copies and their address arithmetic interleave with the DMMAs)
+  auto stage = [&](int kc, int buf, bool on) {
     const int k0 = kc * TK;
 #pragma unroll
     for (int q = 0; q < A_N; ++q) {
-      const int r = a_row + q * A_STEP, gr = row0 + r, gk = k0 + a_col;
-      const bool ok = gr < n && gk < n;
-      cp16(sA(buf) + r * AP + a_col, G.A + (ok ? (int64_t)gr * n + gk : 0), ok ? 16 : 0);
+      const bool ok = on && okA[q] && k0 + a_col < n;
+      cp16s(dstA + buf * A_BUF + q * (A_STEP * AP * (uint32_t)sizeof(cplx)), srcA[q] + (ok ? k0 : 0),
+            ok ? 16 : 0);
     }
 #pragma unroll
     for (int q = 0; q < B_N; ++q) {
-      const int r = b_row + q * B_STEP;
-      if (B_STEP * B_N > TK && r >= TK) break;
-      const int gk = k0 + r;
-      const bool ok = bcol_ok && gk < n;
-      cp16(sB(buf) + r * BP + b_col, G.in + (ok ? bbase + (int64_t)gk * G.ncols : 0), ok ? 16 : 0);
+      const int r = q * B_STEP;  // row offset from b_row
+      const bool ok = on && bcol_ok && k0 + b_row + r < n;
+      cp16s(dstB + buf * B_BUF + r * (BP * (uint32_t)sizeof(cplx)),
+            srcB + (ok ? (int64_t)(k0 + r) * ncols : 0), ok ? 16 : 0);
     }
     cp_commit();
   };
   const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
   const int wr = warp % WR, wc = warp / WR;
-  const bool wact = wc * 16 < colw;
   const int nk = sparse ? __popc(kmask) : nkc;
   uint32_t rem = kmask;
   int seq = 0;
-  auto next_chunk = [&]() -> int {  // the next chunk to stage
-    if (!sparse) return seq++;
-    const int k = __ffs(rem) - 1;
+  auto next_chunk = [&]() -> int {  // the next chunk to stage (branch-free)
+    const int ks = __ffs(rem) - 1;
     rem &= rem - 1;
-    return k;
+    const int kd = seq++;
+    return sparse ? ks : kd;
   };
   // prologue: the first NS-1 chunks (empty commit groups keep the group count)
 #pragma unroll
-  for (int i = 0; i < NS - 1; ++i) {
-    if (i < nk) stage(next_chunk(), i);
-    else cp_commit();
-  }
+  for (int i = 0; i < NS - 1; ++i) stage(next_chunk(), i, i < nk);
+  const cplx *fragA = smem_mg + (wr * 8 * MT + g) * AP + tg;
+  const cplx *fragB = smem_mg + NS * TM * AP + tg * BP + wc * 16 + g;
   for (int it = 0; it < nk; ++it) {
     const int buf = it % NS;
     cp_wait<NS - 2>();  // chunk it landed (this thread's copies)
     __syncthreads();    // ... and every thread's; buffer (it - 1) % NS is free
-    if (it + NS - 1 < nk) stage(next_chunk(), (it + NS - 1) % NS);
-    else cp_commit();
-    if (wact) {
-      const cplx *As = sA(buf) + (wr * 8 * MT + g) * AP + tg;
-      const cplx *Bs = sB(buf) + tg * BP + wc * 16 + g;
+    // the chunk's fragments first, then the next copies, then the products
+    // (free to move up between the copies' address arithmetic)
+    const cplx *As = fragA + buf * (TM * AP), *Bs = fragB + buf * (TK * BP);
+    constexpr int NK4 = TK / 4;
+    cplx a[NK4][MT], b[NK4][2];
 #pragma unroll
-      for (int k4 = 0; k4 < TK / 4; ++k4) {
-        cplx a[MT], b[2];
+    for (int k4 = 0; k4 < NK4; ++k4) {
+      const int kk = k4 * 4;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) a[mt] = As[mt * 8 * AP + k4 * 4];
+      for (int mt = 0; mt < MT; ++mt) a[k4][mt] = As[mt * 8 * AP + kk];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[k4 * 4 * BP + nt * 8];
-        double bs[2] = {b[0].x + b[0].y, b[1].x + b[1].y};
+      for (int nt = 0; nt < 2; ++nt) b[k4][nt] = Bs[kk * BP + nt * 8];
+    }
+    stage(next_chunk(), (it + NS - 1) % NS, it + NS - 1 < nk);
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const double as = a[mt].x + a[mt].y;
+    for (int k4 = 0; k4 < NK4; ++k4) {
+      double bs[2] = {b[k4][0].x + b[k4][0].y, b[k4][1].x + b[k4][1].y};
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            dmma(p1[mt][nt], a[mt].x, b[nt].x);
-            dmma(p2[mt][nt], a[mt].y, b[nt].y);
-            dmma(p3[mt][nt], as, bs[nt]);
-          }
+      for (int mt = 0; mt < MT; ++mt) {
+        const double as = a[k4][mt].x + a[k4][mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma_nv(p1[mt][nt], a[k4][mt].x, b[k4][nt].x);
+          dmma_nv(p2[mt][nt], a[k4][mt].y, b[k4][nt].y);
+          dmma_nv(p3[mt][nt], as, bs[nt]);
         }
       }
     }
@@ -323,41 +350,148 @@ __device__ __forceinline__ void gemm_tile(const PassGeo &G, int row0, int col0, 
   gemm_store<MT, WR, WC>(G, row0, col0, colw, act, A, nrhs, p1, p2, p3);
 }
 
-// one tile per CTA: grid (column tiles, row tiles, visits).  kskip: the
-// first forward pass visits only the K-chunks that K6 marked nonzero in any
-// of the tile's input rows (J.km; payload-only visits: ~70% of the chunks
-// are exact zeros -- the payload bands are thin strips of the window), which
-// shortens the tile's latency chain, not just its arithmetic.
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
+// One tile per CTA on a 1D grid over the launch's non-empty tiles: the
+// tiles of visit 0 (column tile fastest, then row tile), then visit 1, ..
+// Which tiles exist depends on the data (the exact-zero RHS columns of each
+// visit are compacted away), so the host sizes the grid for all RHS active
+// and every CTA derives the compact tile table from the K6 flags; CTAs past
+// the last tile exit.  They carry the highest block indices, so they are
+// dispatched after every working CTA -- with a (column, row, visit) grid the
+// exiting CTAs of each visit sat between the working ones of the next and
+// held their CTA slots (about 55% of config 2's grid) for a prologue each.
+// Before the dependency wait the CTA stages the static pass geometry of all
+// visits of the launch in shared memory, one visit per thread.
+// kskip: the first forward pass visits only the K-chunks that K6 marked
+// nonzero in any of the tile's input rows (J.km; payload-only visits: ~70%
+// of the chunks are exact zeros -- the payload bands are thin strips of the
+// window), which shortens the tile's latency chain, not just its arithmetic.
+#define MG_MAXJ 32  // visits per kernel launch (the host splits longer lists)
+struct TileJob {
+  PassGeo G;
+  const int *nz;
+  const uint32_t *km;
+  int ny;  // row tiles
+};
+
+// Active RHS of the launch's visits from the K6 flags: warp w takes visits
+// w, w + nw, ..; cnt[v] = active count, mask[v][..] = the ballot words.
+// Call from all threads; the caller synchronizes afterwards.
+template <typename JobT>
+__device__ __forceinline__ void count_active(const JobT *job, int njob, int nrhs, int nw, int *cnt,
+                                             uint32_t (*mask)[RMAX_MODAL / 32]) {
+  const int lane = threadIdx.x & 31;
+  if ((int)(threadIdx.x >> 5) >= nw) return;  // a trailing partial warp sits out
+  for (int v = threadIdx.x >> 5; v < njob; v += nw) {
+    const int *nz = job[v].nz;
+    int c = 0;
+    for (int r0 = 0; r0 < nrhs; r0 += 32) {
+      const int r = r0 + lane;
+      const uint32_t mk = __ballot_sync(0xffffffffu, r < nrhs && (!nz || nz[r]));
+      if (lane == 0) mask[v][r0 >> 5] = mk;
+      c += __popc(mk);
+    }
+    if (lane == 0) cnt[v] = c;
+  }
+}
+// the ordered list of a visit's active RHS from its ballot words (no global
+// reads); call from all threads, synchronizes
+__device__ __forceinline__ void active_list(const uint32_t *mask, int nrhs, int *act) {
+  for (int r = threadIdx.x; r < nrhs; r += blockDim.x) {
+    const uint32_t mk = mask[r >> 5];
+    if ((mk >> (r & 31)) & 1u) {
+      int pos = __popc(mk & ((1u << (r & 31)) - 1));
+      for (int w = 0; w < (r >> 5); ++w) pos += __popc(mask[w]);
+      act[pos] = r;
+    }
+  }
+  __syncthreads();
+}
+
+// COMPACT (2D): the 1D grid described above.  Otherwise (3D: nearly every
+// RHS is active and the passes are short, so the table costs more than the
+// exiting CTAs) the grid is (column tiles, row tiles, visits).
+// early: the K6 flags were final before the previous kernel of the stream
+// started (inverse passes), so they are read before the dependency wait.
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2, bool COMPACT = true>
 __global__ void __launch_bounds__(32 * WR * WC, MINB)
-    k_modal_gemm(const ModalJob *__restrict__ jobs, int pass, int nrhs, int kskip) {
-  constexpr int TM = 8 * MT * WR, TN = 16 * WC;
+    k_modal_gemm(const ModalJob *__restrict__ jobs, int njob, int pass, int nrhs, int kskip, int early,
+                 unsigned long long *work) {
+  constexpr int TM = 8 * MT * WR, TN = 16 * WC, NW = WR * WC;
   static_assert(TK == 8, "K6 chunk masks are in units of 8");
   extern __shared__ __align__(16) cplx smem_mg[];
   __shared__ int act[RMAX_MODAL + 1];
   __shared__ uint32_t s_kmask;
-  const ModalJob J = jobs[blockIdx.z];
-  const FactDev f = *J.f;
-  const PassGeo G = pass_geo(f, J, pass, nrhs);
-  const int row0 = blockIdx.y * TM;
-  const int col0 = blockIdx.x * TN;
-  if (row0 >= G.n || col0 >= G.outer * G.ncols) return;
-  pdl_wait();
-  const int A = active_rhs(J, nrhs, act);
+  PassGeo G;
+  const uint32_t *km;
+  int row0, col0, A;
+  if (COMPACT) {
+    __shared__ TileJob s_job[MG_MAXJ];
+    __shared__ int s_cnt[MG_MAXJ];
+    __shared__ uint32_t s_mask[MG_MAXJ][RMAX_MODAL / 32];
+    const int t = threadIdx.x;
+    if (t < njob) {  // static tables only
+      const ModalJob J = jobs[t];
+      const FactDev f = *J.f;
+      TileJob tj;
+      tj.G = pass_geo(f, J, pass, nrhs);
+      tj.nz = J.nz;
+      tj.km = J.km;
+      tj.ny = (tj.G.n + TM - 1) / TM;
+      s_job[t] = tj;
+    }
+    if (!early) pdl_wait();
+    __syncthreads();
+    count_active(s_job, njob, nrhs, NW, s_cnt, s_mask);
+    __syncthreads();
+    int L = blockIdx.x, v = 0, nx = 1;
+    for (; v < njob; ++v) {
+      const PassGeo &Gv = s_job[v].G;
+      nx = (Gv.outer * Gv.inner * s_cnt[v] + TN - 1) / TN;
+      const int nt = nx * s_job[v].ny;
+      if (L < nt) break;
+      L -= nt;
+    }
+    if (v == njob) return;
+    G = s_job[v].G;
+    km = s_job[v].km;
+    row0 = (L / nx) * TM;
+    col0 = (L - (L / nx) * nx) * TN;
+    A = s_cnt[v];
+    active_list(s_mask[v], nrhs, act);
+    if (early) pdl_wait();
+  } else {
+    const ModalJob J = jobs[blockIdx.z];
+    const FactDev f = *J.f;
+    G = pass_geo(f, J, pass, nrhs);
+    km = J.km;
+    row0 = blockIdx.y * TM;
+    col0 = blockIdx.x * TN;
+    if (row0 >= G.n || col0 >= G.outer * G.ncols) return;
+    pdl_wait();
+    A = active_rhs(J.nz, nrhs, act);
+    if (col0 >= G.outer * G.inner * A) return;
+  }
   const int total = G.outer * G.inner * A;  // compact columns
-  if (col0 >= total) return;
   const int colw = min(TN, total - col0);
   // pass 0 has inner == 1: compact column c is (input row c / A, RHS)
-  const bool sparse = kskip && pass == 0 && J.km != nullptr && G.inner == 1;
+  const bool sparse = kskip && pass == 0 && km != nullptr && G.inner == 1;
   if (sparse) {
     if (threadIdx.x < 32) {
       const int b0 = col0 / A, b1 = (col0 + colw - 1) / A;
       uint32_t mk = 0;
-      for (int b = b0 + (int)threadIdx.x; b <= b1; b += 32) mk |= J.km[b];
+      for (int b = b0 + (int)threadIdx.x; b <= b1; b += 32) mk |= km[b];
       mk = __reduce_or_sync(0xffffffffu, mk);
       if (threadIdx.x == 0) s_kmask = mk;
     }
     __syncthreads();
+  }
+  if (work && threadIdx.x == 0) {  // executed complex multiply-adds of this tile (ds_ctx_work)
+    int kx = G.n;
+    if (sparse) {
+      const int last = (G.n - 1) / TK;  // the last chunk may be partial
+      kx = __popc(s_kmask) * TK - (((s_kmask >> last) & 1u) ? (last + 1) * TK - G.n : 0);
+    }
+    atomicAdd(work, (unsigned long long)min(TM, G.n - row0) * colw * kx);
   }
   gemm_tile<MT, WR, WC, TK, NS>(G, row0, col0, colw, sparse, sparse ? s_kmask : 0u, smem_mg, act, A,
                                 nrhs);
@@ -520,37 +654,75 @@ __global__ void __launch_bounds__(TQ) k_modal_thomas2(const ModalJob *__restrict
 // (NSEG steps), and every warp adds partial product x carry.  Critical path
 // L + NSEG + 1 steps instead of n_b; forward values stay in registers for
 // the backward sweep; loads are 512-byte coalesced rows.
-template <int L>
-__global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restrict__ jobs, int nrhs) {
-  __shared__ cplx sP[16][32], sZ[16][32], sC[16][32];
-  const ModalJob J = jobs[blockIdx.y];
-  const FactDev &f = *J.f;
-  const int m = f.m, nb = f.nb;
-  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
-  const int nseg = (nb + L - 1) / L;
+struct RecJob {
+  const int *nz;
+  cplx *T;
+  const cplx *mmul, *minv, *ucoef;
+  int m, nb;
+};
+// 1D grid over the launch's non-empty column blocks (the compact tile table
+// of k_modal_gemm): the K6 flags were final two kernels ago, so the table is
+// built before the dependency wait and the blocks past the last one exit
+// without holding an SM (one 512-thread block per SM).
+// CW columns per block (32, or 16: half the threads, two blocks per SM).
+template <int L, int CW>
+__global__ void __launch_bounds__(16 * CW, 32 / CW) k_modal_thomas3(const ModalJob *__restrict__ jobs,
+                                                                    int njob, int nrhs) {
+  __shared__ cplx sP[16][CW], sZ[16][CW], sC[16][CW];
   __shared__ int actl[RMAX_MODAL + 1];
-  if (blockIdx.x * 32 >= m * nrhs) return;
-  pdl_wait();
-  const int A = active_rhs(J, nrhs, actl);  // compact (mode, active RHS) columns
-  if (blockIdx.x * 32 >= m * A) return;
-  const int qc = blockIdx.x * 32 + lane;
+  __shared__ RecJob s_job[MG_MAXJ];
+  __shared__ int s_cnt[MG_MAXJ];
+  __shared__ uint32_t s_mask[MG_MAXJ][RMAX_MODAL / 32];
+  const int lane = threadIdx.x % CW, seg = threadIdx.x / CW;
+  if ((int)threadIdx.x < njob) {
+    const ModalJob J = jobs[threadIdx.x];
+    const FactDev &f = *J.f;
+    RecJob r;
+    r.nz = J.nz;
+    r.T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
+    r.mmul = f.mmul;
+    r.minv = f.minv;
+    r.ucoef = f.ucoef;
+    r.m = f.m;
+    r.nb = f.nb;
+    s_job[threadIdx.x] = r;
+  }
+  __syncthreads();
+  count_active(s_job, njob, nrhs, (int)blockDim.x >> 5, s_cnt, s_mask);
+  __syncthreads();
+  int blk = blockIdx.x, v = 0;
+  for (; v < njob; ++v) {
+    const int nblk = (s_job[v].m * s_cnt[v] + CW - 1) / CW;
+    if (blk < nblk) break;
+    blk -= nblk;
+  }
+  if (v == njob) return;
+  const RecJob f = s_job[v];
+  const int m = f.m, nb = f.nb, A = s_cnt[v];
+  const int nseg = (nb + L - 1) / L;
+  active_list(s_mask[v], nrhs, actl);  // compact (mode, active RHS) columns
+  const int qc = blk * CW + lane;
   const bool live = qc < m * A;
   const int qcc = live ? qc : 0;
   const int j = qcc / A;
   const int q = j * nrhs + actl[qcc - j * A];  // full-layout column of this thread
   const int qq = q;
-  cplx *T = ((f.naxes - 1) & 1 ? J.s1 : J.s0);
+  cplx *T = f.T;
   const size_t st = (size_t)m * nrhs;
   const int k0 = seg * L;
   const bool act = seg < nseg;
   // loads of the segment: data, multipliers, inverse pivots, couplings
   cplx g[L], mu[L], iv[L], uc[L];
 #pragma unroll
+  for (int i = 0; i < L; ++i) {  // factor data: in flight across the dependency wait
+    const int k = k0 + i;
+    mu[i] = act && k < nb ? f.mmul[(size_t)k * m + j] : make_double2(0.0, 0.0);
+  }
+  pdl_wait();
+#pragma unroll
   for (int i = 0; i < L; ++i) {
     const int k = k0 + i;
-    const bool in = act && k < nb;
-    g[i] = in ? T[k * st + qq] : make_double2(0.0, 0.0);
-    mu[i] = in ? f.mmul[(size_t)k * m + j] : make_double2(0.0, 0.0);
+    g[i] = act && k < nb ? T[k * st + qq] : make_double2(0.0, 0.0);
   }
   // ---- forward: z_k = g_k - mul_k z_{k-1}  (mul_0 = 0)
   cplx P[L];
@@ -631,30 +803,46 @@ __global__ void __launch_bounds__(512) k_modal_thomas3(const ModalJob *__restric
 }
 
 // ------------------------------------------------------------- launcher
-template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2>
+template <int MT, int WR, int WC, int TK = 16, int MINB = 1, int NS = 2, bool COMPACT = true>
 static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *facts, int njob,
                        int pass, int nrhs) {
   constexpr int TM = 8 * MT * WR, TN = 16 * WC;
   const size_t smem = sizeof(cplx) * NS * (TM * (TK + 4) + TK * (TN + 2));
+  auto kern = k_modal_gemm<MT, WR, WC, TK, MINB, NS, COMPACT>;
   static bool attr_set = false;
   if (!attr_set) {
-    DS_CUDA(cudaFuncSetAttribute(k_modal_gemm<MT, WR, WC, TK, MINB, NS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
+  unsigned long long *work = ctx->opt.count_work ? ctx->work : nullptr;
+  const int early = pass >= facts[0].naxes;  // inverse passes: the K6 flags are long final
   ModalJob dummy;
   memset(&dummy, 0, sizeof(dummy));
-  int gx = 1, gy = 1;
-  for (int i = 0; i < njob; ++i) {
-    const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
-    gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
-    gy = std::max(gy, (G.n + TM - 1) / TM);
+  if (!COMPACT) {
+    int gx = 1, gy = 1;
+    for (int i = 0; i < njob; ++i) {
+      const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
+      gx = std::max(gx, (G.outer * G.ncols + TN - 1) / TN);
+      gy = std::max(gy, (G.n + TM - 1) / TM);
+    }
+    DS_CUDA(launch_pdl(kern, dim3(gx, gy, njob), dim3(32 * WR * WC), smem, ctx->stream, jobs_dev,
+                       njob, pass, nrhs, ctx->opt.kskip, 0, work));
+    ctx->launches++;
+    DS_CHECK_LAUNCH();
+    return DS_OK;
   }
-  DS_CUDA(launch_pdl(k_modal_gemm<MT, WR, WC, TK, MINB, NS>, dim3(gx, gy, njob), dim3(32 * WR * WC), smem,
-                     ctx->stream, jobs_dev, pass, nrhs, ctx->opt.kskip));
-
-  ctx->launches++;
-  DS_CHECK_LAUNCH();
+  for (int j0 = 0; j0 < njob; j0 += MG_MAXJ) {  // at most MG_MAXJ visits per kernel launch
+    const int nj = std::min(MG_MAXJ, njob - j0);
+    int tiles = 0;  // every RHS active: the upper bound of the compact tile count
+    for (int i = j0; i < j0 + nj; ++i) {
+      const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
+      tiles += ((G.outer * G.ncols + TN - 1) / TN) * ((G.n + TM - 1) / TM);
+    }
+    DS_CUDA(launch_pdl(kern, dim3(std::max(1, tiles)), dim3(32 * WR * WC), smem, ctx->stream,
+                       jobs_dev + j0, nj, pass, nrhs, ctx->opt.kskip, early, work));
+    ctx->launches++;
+    DS_CHECK_LAUNCH();
+  }
   return DS_OK;
 }
 
@@ -670,7 +858,8 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
   // 4): 32 x 32 per CTA, 2 x 2 warps of 16 x 16, K chunks of
   // 8 through a 4-stage cp.async ring, 4 CTAs per SM
   auto launch_pass = [&](int pass) -> int {
-    return launch_gemm<2, 2, 2, 8, 4, 4>(ctx, jobs_dev, facts, njob, pass, nrhs);
+    if (na == 2) return launch_gemm<2, 2, 2, 8, 4, 4, false>(ctx, jobs_dev, facts, njob, pass, nrhs);
+    return launch_gemm<2, 2, 2, 8, 4, 4, true>(ctx, jobs_dev, facts, njob, pass, nrhs);
   };
   if (phase == 0 || phase == -1)
     for (int p = 0; p < na; ++p)
@@ -686,10 +875,26 @@ int ds_launch_modal_phase(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *
     if (nbmax > 64 && nbmax <= 16 * 16) {  // segmented recurrences (long chains, 2D)
       const int L = nbmax <= 64 ? 4 : (nbmax <= 128 ? 8 : 16);
       const int nseg = (nbmax + L - 1) / L;
-      const dim3 grid((mmax * nrhs + 31) / 32, njob);
-      if (L == 4) DS_CUDA(launch_pdl(k_modal_thomas3<4>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
-      else if (L == 8) DS_CUDA(launch_pdl(k_modal_thomas3<8>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
-      else DS_CUDA(launch_pdl(k_modal_thomas3<16>, grid, dim3(32 * nseg), 0, ctx->stream, jobs_dev, nrhs));
+      const int cw = ctx->opt.r3_cols == 16 ? 16 : 32;
+      for (int j0 = 0; j0 < njob; j0 += MG_MAXJ) {
+        const int nj = std::min(MG_MAXJ, njob - j0);
+        int blocks = 0;  // every RHS active: the upper bound of the compact block count
+        for (int i = j0; i < j0 + nj; ++i) blocks += (facts[i].m * nrhs + cw - 1) / cw;
+        const dim3 grid(std::max(1, blocks)), block(cw * nseg);
+#define R3_LAUNCH(L_, CW_) \
+  DS_CUDA(launch_pdl(k_modal_thomas3<L_, CW_>, grid, block, 0, ctx->stream, jobs_dev + j0, nj, nrhs))
+        if (cw == 16) {
+          if (L == 4) R3_LAUNCH(4, 16);
+          else if (L == 8) R3_LAUNCH(8, 16);
+          else R3_LAUNCH(16, 16);
+        } else {
+          if (L == 4) R3_LAUNCH(4, 32);
+          else if (L == 8) R3_LAUNCH(8, 32);
+          else R3_LAUNCH(16, 32);
+        }
+#undef R3_LAUNCH
+        if (j0 > 0) ctx->launches++;
+      }
     } else if (tsm <= 200 * 1024) {  // short chains (3D): the staged v2 streams better
       if ((int)tsm > th_attr) {
         DS_CUDA(cudaFuncSetAttribute(k_modal_thomas2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));

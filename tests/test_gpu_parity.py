@@ -984,16 +984,40 @@ def test_transform_work_skips_exact(cuda, cfg1, which, option):
     fd = torch.from_numpy(f.astype(np.complex128).reshape(R, -1)).cuda()
     cache = FactorizationCache()
 
+    work = {}
+
     def run(value):
         old = _engine.set_option(option, value)
         try:
             dp = _engine.DevicePlan(b["partition"], b["ops"], cache, SweepPlan.default(dim).directions, R,
                                     pipelined=True)
+            dp.enable_graph(False)  # a captured graph keeps the counter argument it was recorded with
             u, _ = dp.apply(fd)
+            # the executed-work counter (ds_ctx_work, bench.py's roofline numerator)
+            _engine.set_option("count_work", 1)
+            _engine.executed_work(reset=True)
+            u2, _ = dp.apply(fd)
+            work[value] = (_engine.executed_work(reset=True), dp)
+            _engine.set_option("count_work", 0)
+            assert torch.equal(u, u2)
             return u.cpu().numpy()
         finally:
+            _engine.set_option("count_work", 0)
             _engine.set_option(option, old)
 
     dense, sparse = run(0), run(1)
     assert np.array_equal(dense, sparse)
     assert np.count_nonzero(sparse) > 0
+    # dense walk: n_b m (sum of in-slab extents) multiply-adds per transform
+    # direction for every nonzero (visit, RHS) column; the sparse walk drops
+    # the all-zero K-chunks of the first forward pass only
+    cm_dense, dp = work[0]
+    vnz = dp.counters(R)["visit_nonzero"]
+    expect = 0
+    for si, fct in enumerate(dp._keep[1]):
+        per = 2 * fct.n_blocks * fct.block_size * (sum(fct.shape) - fct.shape[fct.block_axis])
+        expect += per * int(vnz[:, si, :].sum())
+    assert cm_dense == expect
+    assert 0 < work[1][0] < cm_dense
+    _engine.executed_work(reset=True)
+    assert _engine.executed_work() == 0

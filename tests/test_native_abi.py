@@ -19,7 +19,7 @@ def header_symbols():
 
 def test_library_loads_and_exports_header_symbols():
     lib = _native.load_library()
-    assert lib.ds_abi_version() == _native.ABI_VERSION == 6
+    assert lib.ds_abi_version() == _native.ABI_VERSION == 7
     syms = header_symbols()
     assert len(syms) >= 25
     for name in syms:
