@@ -376,9 +376,10 @@ struct TileJob {
 // Active RHS of the launch's visits from the K6 flags: warp w takes visits
 // w, w + nw, ..; cnt[v] = active count, mask[v][..] = the ballot words.
 // Call from all threads; the caller synchronizes afterwards.
-template <typename JobT>
+// fin(v, count) runs on lane 0 (derived per-visit quantities).
+template <typename JobT, typename Fin>
 __device__ __forceinline__ void count_active(const JobT *job, int njob, int nrhs, int nw, int *cnt,
-                                             uint32_t (*mask)[RMAX_MODAL / 32]) {
+                                             uint32_t (*mask)[RMAX_MODAL / 32], Fin fin) {
   const int lane = threadIdx.x & 31;
   if ((int)(threadIdx.x >> 5) >= nw) return;  // a trailing partial warp sits out
   for (int v = threadIdx.x >> 5; v < njob; v += nw) {
@@ -390,7 +391,10 @@ __device__ __forceinline__ void count_active(const JobT *job, int njob, int nrhs
       if (lane == 0) mask[v][r0 >> 5] = mk;
       c += __popc(mk);
     }
-    if (lane == 0) cnt[v] = c;
+    if (lane == 0) {
+      cnt[v] = c;
+      fin(v, c);
+    }
   }
 }
 // the ordered list of a visit's active RHS from its ballot words (no global
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
   int row0, col0, A;
   if (COMPACT) {
     __shared__ TileJob s_job[MG_MAXJ];
-    __shared__ int s_cnt[MG_MAXJ];
+    __shared__ int s_cnt[MG_MAXJ], s_nx[MG_MAXJ], s_nt[MG_MAXJ];
     __shared__ uint32_t s_mask[MG_MAXJ][RMAX_MODAL / 32];
     const int t = threadIdx.x;
     if (t < njob) {  // static tables only
@@ -441,17 +445,20 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     }
     if (!early) pdl_wait();
     __syncthreads();
-    count_active(s_job, njob, nrhs, NW, s_cnt, s_mask);
+    count_active(s_job, njob, nrhs, NW, s_cnt, s_mask, [&](int v, int c) {
+      const PassGeo &Gv = s_job[v].G;  // column tiles and tiles of visit v
+      s_nx[v] = (Gv.outer * Gv.inner * c + TN - 1) / TN;
+      s_nt[v] = s_nx[v] * s_job[v].ny;
+    });
     __syncthreads();
-    int L = blockIdx.x, v = 0, nx = 1;
+    int L = blockIdx.x, v = 0;
     for (; v < njob; ++v) {
-      const PassGeo &Gv = s_job[v].G;
-      nx = (Gv.outer * Gv.inner * s_cnt[v] + TN - 1) / TN;
-      const int nt = nx * s_job[v].ny;
+      const int nt = s_nt[v];
       if (L < nt) break;
       L -= nt;
     }
     if (v == njob) return;
+    const int nx = s_nx[v];
     G = s_job[v].G;
     km = s_job[v].km;
     row0 = (L / nx) * TM;
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(16 * CW, 32 / CW) k_modal_thomas3(const ModalJ
   __shared__ cplx sP[16][CW], sZ[16][CW], sC[16][CW];
   __shared__ int actl[RMAX_MODAL + 1];
   __shared__ RecJob s_job[MG_MAXJ];
-  __shared__ int s_cnt[MG_MAXJ];
+  __shared__ int s_cnt[MG_MAXJ], s_nblk[MG_MAXJ];
   __shared__ uint32_t s_mask[MG_MAXJ][RMAX_MODAL / 32];
   const int lane = threadIdx.x % CW, seg = threadIdx.x / CW;
   if ((int)threadIdx.x < njob) {
@@ -688,11 +695,12 @@ __global__ void __launch_bounds__(16 * CW, 32 / CW) k_modal_thomas3(const ModalJ
     s_job[threadIdx.x] = r;
   }
   __syncthreads();
-  count_active(s_job, njob, nrhs, (int)blockDim.x >> 5, s_cnt, s_mask);
+  count_active(s_job, njob, nrhs, (int)blockDim.x >> 5, s_cnt, s_mask,
+               [&](int v, int c) { s_nblk[v] = (s_job[v].m * c + CW - 1) / CW; });
   __syncthreads();
   int blk = blockIdx.x, v = 0;
   for (; v < njob; ++v) {
-    const int nblk = (s_job[v].m * s_cnt[v] + CW - 1) / CW;
+    const int nblk = s_nblk[v];
     if (blk < nblk) break;
     blk -= nblk;
   }
@@ -818,7 +826,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
   const int early = pass >= facts[0].naxes;  // inverse passes: the K6 flags are long final
   ModalJob dummy;
   memset(&dummy, 0, sizeof(dummy));
-  if (!COMPACT) {
+  if constexpr (!COMPACT) {
     int gx = 1, gy = 1;
     for (int i = 0; i < njob; ++i) {
       const PassGeo G = pass_geo(facts[i], dummy, pass, nrhs);
@@ -830,7 +838,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     ctx->launches++;
     DS_CHECK_LAUNCH();
     return DS_OK;
-  }
+  } else {
   for (int j0 = 0; j0 < njob; j0 += MG_MAXJ) {  // at most MG_MAXJ visits per kernel launch
     const int nj = std::min(MG_MAXJ, njob - j0);
     int tiles = 0;  // every RHS active: the upper bound of the compact tile count
@@ -844,6 +852,7 @@ static int launch_gemm(ds_ctx *ctx, const ModalJob *jobs_dev, const FactDev *fac
     DS_CHECK_LAUNCH();
   }
   return DS_OK;
+  }
 }
 
 // phase 0: forward transforms, 1: mode-wise recurrences, 2: inverse
