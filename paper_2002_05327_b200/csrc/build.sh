@@ -17,6 +17,6 @@ done
 wait
 CUDA_LIB="$(dirname "$(dirname "$(command -v "$NVCC")")")/lib64"
 "$NVCC" -gencode arch=compute_100a,code=sm_100a -shared "${objs[@]}" -o "$out.tmp" -lcudart \
-  -L"$CUDA_LIB" -lcublas -Xlinker -rpath -Xlinker "$CUDA_LIB"
+  -L"$CUDA_LIB" -Xlinker -rpath -Xlinker "$CUDA_LIB"
 mv "$out.tmp" "$out"
 echo "built $out"

@@ -128,7 +128,6 @@ struct ds_options {
   int k3_rc_min = 4;   // DS_K3_RCMIN / DS_K3_RCMAX: RHS chunk range of the cluster block solve
   int k3_rc_max = 16;
   int k3_cluster = 0;  // DS_K3_CLUSTER: force 8 or 16 CTAs per cluster (0 = choose)
-  int k2b_3m = 1;      // DS_K2B_3M: K2b trailing updates as 3M GEMMs (cublasZgemm3m)
   int hio_dstreams = 2;  // DS_HIO_DSTREAMS: download streams of the pinned-host path
   int kskip = 1;       // DS_KSKIP: forward transforms visit only the nonzero K-chunks (K6 masks)
   int r3_cols = 16;    // DS_R3_COLS: (mode, RHS) columns per block of the segmented recurrences (16 default, 32)

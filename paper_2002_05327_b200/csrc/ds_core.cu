@@ -88,7 +88,6 @@ void ds_options_from_env(ds_options &o) {
   o.k3_rc_max = std::max(1, env_opt("DS_K3_RCMAX", o.k3_rc_max));
   o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
-  o.k2b_3m = env_opt("DS_K2B_3M", 1) != 0;
   o.kskip = env_opt("DS_KSKIP", 1) != 0;
   o.r3_cols = env_opt("DS_R3_COLS", 16) == 32 ? 32 : 16;
 }
@@ -110,7 +109,6 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "k3_rc_max") return &o.k3_rc_max;
   if (k == "k3_cluster") return &o.k3_cluster;
   if (k == "hio_dstreams") return &o.hio_dstreams;
-  if (k == "k2b_3m") return &o.k2b_3m;
   if (k == "kskip") return &o.kskip;
   if (k == "count_work") return &o.count_work;
   if (k == "r3_cols") return &o.r3_cols;

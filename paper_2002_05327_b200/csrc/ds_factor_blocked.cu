@@ -15,16 +15,16 @@
 //      pivot rows, zero on the sub-panel) -- the macro-panel then holds the
 //      pivot columns of the composite elimination E = E_3 .. E_0;
 //   2. one rank-MW update of every column outside the macro-panel,
-//      A += (E - I)[:, pivots] A[pivot rows, :]   (8 m^2 MW flop, plain
-//      complex GEMM, cuBLAS zgemm) -- a quarter of the full-matrix passes of
-//      rank-32 updates and a K = 128 GEMM instead of K = 32, as a 3M
-//      product (cublasZgemm3m) (config 5:
-//      1.68 s per window at MW = 32; MW = 256 measured no faster: cuBLAS
-//      zgemm stays at ~25 TFLOP/s for m = 2793 at K = 128 and K = 256).
+//      A += (E - I)[:, pivots] A[pivot rows, :]   (8 m^2 MW flop, a plain
+//      complex GEMM: k_zgemm_acc below, every matrix of the step in one
+//      launch) -- a quarter of the full-matrix passes of rank-32 updates and
+//      a K = 128 product instead of K = 32 (config 5: 1.68 s per window at
+//      MW = 32).  Until round 2 the updates were cublasZgemm3m calls, one
+//      per matrix: six config-5 windows 8.08 s one by one / 4.23 s batched
+//      with cuBLAS, 5.70 / 3.71 s with k_zgemm_acc (14.1 / 23.6 TFLOP/s).
 // Column interchanges are undone at the end.  All chains of a step are
 // batched (one panel / swap / copy launch per step for every matrix).
 #include <cooperative_groups.h>
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,6 +34,7 @@
 
 #include "ds_common.cuh"
 #include "ds_factor.cuh"
+#include "ds_mma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -250,6 +251,124 @@ __global__ void k_panel_operands(const BlkTask *__restrict__ tasks, int p, int w
   }
 }
 
+// K2b trailing update on the FP64 tensor cores, every matrix of the step in
+// one launch:  A[r][c0 + c] += sum_kk P[r][kk] T[kk][c0 + c]   (r < m,
+// c < nc, kk < K; A, T row-major with pitch m, P with pitch ldp).  The tile
+// kernel of the modal transforms (ds_modal.cu, K3m-T): 32 x 32 per CTA,
+// 4 warps of 16 x 16, K chunks of 8 through a 4-stage cp.async ring, DMMA
+// m8n8k4, 3M complex product (6 real flop per complex multiply-add, the
+// imaginary part formed by subtraction -- the factorization residuals stay
+// <= 1e-10, tests/test_gpu_pool.py).
+// mode 0: a sub-panel's rank-BW update of its macro-panel's columns
+// (c0 = p0, nc = min(MW, m - p0), skipped when the macro-panel is the
+// sub-panel); mode 1: the macro-panel's rank-MW update of every column.
+#define ZG_TM 32
+#define ZG_TN 32
+#define ZG_TK 8
+#define ZG_NS 4
+__global__ void __launch_bounds__(128, 4)
+    k_zgemm_acc(const BlkTask *__restrict__ tasks, int p, int c0, int ncmax, int K, int ldp, int mode) {
+  constexpr int TM = ZG_TM, TN = ZG_TN, TK = ZG_TK, NS = ZG_NS, NTH = 128, MT = 2;
+  constexpr int AP = TK + 4, BP = TN + 2;
+  constexpr int A_STEP = NTH / TK, A_N = TM / A_STEP, B_STEP = NTH / TN, B_N = TK / B_STEP;
+  constexpr uint32_t A_BUF = TM * AP * sizeof(cplx), B_BUF = TK * BP * sizeof(cplx);
+  __shared__ __align__(16) cplx smem[NS * (TM * AP + TK * BP)];
+  const BlkTask &X = tasks[blockIdx.z];
+  const int m = X.J.f.m;
+  if (p >= m) return;
+  const int nc = min(ncmax, m - c0);
+  if (mode == 0 ? nc <= min(BW, m - p) : min(MW, m - p) >= m) return;
+  const int row0 = blockIdx.y * TM, col0 = blockIdx.x * TN;
+  if (row0 >= m || col0 >= nc) return;
+  const int t = threadIdx.x;
+  const int a_col = t % TK, a_row = t / TK, b_col = t % TN, b_row = t / TN;
+  const cplx *srcA[A_N];
+  bool okA[A_N];
+#pragma unroll
+  for (int q = 0; q < A_N; ++q) {
+    const int gr = row0 + a_row + q * A_STEP;
+    okA[q] = gr < m;
+    srcA[q] = X.P + (okA[q] ? (size_t)gr * ldp + a_col : 0);
+  }
+  const bool bok = col0 + b_col < nc;
+  const cplx *srcB = X.T + (bok ? (size_t)b_row * m + c0 + col0 + b_col : 0);
+  const uint32_t dstA = smem_addr(smem + a_row * AP + a_col);
+  const uint32_t dstB = smem_addr(smem + NS * TM * AP + b_row * BP + b_col);
+  auto stage = [&](int kc, int buf, bool on) {
+    const int k0 = kc * TK;
+#pragma unroll
+    for (int q = 0; q < A_N; ++q) {
+      const bool ok = on && okA[q] && k0 + a_col < K;
+      cp16s(dstA + buf * A_BUF + q * (A_STEP * AP * (uint32_t)sizeof(cplx)), srcA[q] + (ok ? k0 : 0),
+            ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int q = 0; q < B_N; ++q) {
+      const int r = q * B_STEP;
+      const bool ok = on && bok && k0 + b_row + r < K;
+      cp16s(dstB + buf * B_BUF + r * (BP * (uint32_t)sizeof(cplx)), srcB + (ok ? (size_t)(k0 + r) * m : 0),
+            ok ? 16 : 0);
+    }
+    cp_commit();
+  };
+  const int warp = t >> 5, lane = t & 31, g = lane >> 2, tg = lane & 3;
+  const int wr = warp % 2, wc = warp / 2;
+  const int nk = (K + TK - 1) / TK;
+#pragma unroll
+  for (int i = 0; i < NS - 1; ++i) stage(i, i, i < nk);
+  const cplx *fragA = smem + (wr * 8 * MT + g) * AP + tg;
+  const cplx *fragB = smem + NS * TM * AP + tg * BP + wc * 16 + g;
+  double p1[MT][2][2] = {}, p2[MT][2][2] = {}, p3[MT][2][2] = {};
+  for (int it = 0; it < nk; ++it) {
+    const int buf = it % NS;
+    cp_wait<NS - 2>();
+    __syncthreads();
+    const cplx *As = fragA + buf * (TM * AP), *Bs = fragB + buf * (TK * BP);
+    cplx a[TK / 4][MT], b[TK / 4][2];
+#pragma unroll
+    for (int k4 = 0; k4 < TK / 4; ++k4) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) a[k4][mt] = As[mt * 8 * AP + k4 * 4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[k4][nt] = Bs[k4 * 4 * BP + nt * 8];
+    }
+    stage(it + NS - 1, (it + NS - 1) % NS, it + NS - 1 < nk);
+#pragma unroll
+    for (int k4 = 0; k4 < TK / 4; ++k4) {
+      double bs[2] = {b[k4][0].x + b[k4][0].y, b[k4][1].x + b[k4][1].y};
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double as = a[k4][mt].x + a[k4][mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma_nv(p1[mt][nt], a[k4][mt].x, b[k4][nt].x);
+          dmma_nv(p2[mt][nt], a[k4][mt].y, b[k4][nt].y);
+          dmma_nv(p3[mt][nt], as, bs[nt]);
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+  // A += product: Re = P1 - P2, Im = P3 - P1 - P2
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int gr = row0 + wr * 8 * MT + mt * 8 + g;
+    if (gr >= m) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int cc = col0 + wc * 16 + nt * 8 + 2 * tg;  // two adjacent columns
+      cplx *dst = X.A + (size_t)gr * m + c0 + cc;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (cc + e >= nc) continue;
+        const cplx o = dst[e];
+        dst[e] = make_double2(o.x + (p1[mt][nt][e] - p2[mt][nt][e]),
+                              o.y + (p3[mt][nt][e] - p1[mt][nt][e] - p2[mt][nt][e]));
+      }
+    }
+  }
+}
+
 // undo the column interchanges: A[r][c] <- A[r][src[c]] (one CTA per row)
 __global__ void k_col_unpermute(const BlkTask *__restrict__ tasks, int *srcbuf, int mmax) {
   const BlkTask &X = tasks[blockIdx.y];
@@ -332,12 +451,6 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
     cleanup();
     return ds_fail(DS_ECUDA, "blocked factorization: out of device memory for workspaces");
   }
-  cublasHandle_t hb;
-  if (cublasCreate(&hb) != CUBLAS_STATUS_SUCCESS) {
-    cleanup();
-    return ds_fail(DS_ECUDA, "cublasCreate failed");
-  }
-  cublasSetStream(hb, st);
   cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem);
   cudaFuncSetAttribute(k_col_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -394,22 +507,6 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
       for (auto &X : tasks) mstep = std::max(mstep, X.J.f.m);
       k_form_schur<<<dim3(std::max(1, std::min(1024, (int)((int64_t)mstep * mstep / 256 / 4))), nt), 256, 0, st>>>(dtasks);
       ctx->launches++;
-      const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
-      // 3M complex GEMM (cublasZgemm3m: three real products): config 5
-      // window factorization 1.18 -> 0.92 s; residuals stay <= 1e-10
-      const bool use3m = ctx->opt.k2b_3m != 0;
-      // row-major A(m x m) += P'(m x k) T(k x m)  ==  col-major A^T += T^T P'^T;
-      // rows [c0, c0 + nc) of A^T = columns [c0, c0 + nc) of A
-      auto zgemm = [&](int m, int nc, int c0, int k, int ldp, const BlkTask &X) -> int {
-        cublasStatus_t cs = (use3m ? cublasZgemm3m : cublasZgemm)(hb, CUBLAS_OP_N, CUBLAS_OP_N, nc, m, k, &one,
-                                        (const cuDoubleComplex *)X.T + c0, m,
-                                        (const cuDoubleComplex *)X.P, ldp, &one,
-                                        (cuDoubleComplex *)X.A + c0, m);
-        ctx->launches++;
-        return cs == CUBLAS_STATUS_SUCCESS
-                   ? DS_OK
-                   : ds_fail(DS_ECUDA, "cublasZgemm failed in the blocked factorization");
-      };
       for (int p0 = 0; p0 < mstep && rc == DS_OK; p0 += MW) {
         for (int p = p0; p < std::min(p0 + MW, mstep) && rc == DS_OK; p += BW) {
           void *args[] = {(void *)&dtasks, (void *)&p, (void *)&rpc_max, (void *)&status};
@@ -421,11 +518,11 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
               dtasks, p, width, W);
           ctx->launches += 3;
           // the sub-panel's update, restricted to the macro-panel's columns
-          for (auto &X : tasks) {
-            const int m = X.J.f.m;
-            if (p >= m) continue;
-            const int nc = std::min(MW, m - p0);
-            if (nc > std::min(BW, m - p) && (rc = zgemm(m, nc, p0, BW, BW, X))) break;
+          {
+            const int ncm = std::min(MW, mstep - p0);
+            k_zgemm_acc<<<dim3((ncm + ZG_TN - 1) / ZG_TN, (mstep + ZG_TM - 1) / ZG_TM, nt), 128, 0, st>>>(
+                dtasks, p, p0, MW, BW, BW, 0);
+            ctx->launches++;
           }
           DS_CHECK_LAUNCH();
         }
@@ -434,11 +531,9 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
         k_panel_operands<<<dim3(std::max(1, (2 * MW * mstep + 255) / 256), nt), 256, 0, st>>>(
             dtasks, p0, MW, MW);
         ctx->launches++;
-        for (auto &X : tasks) {
-          const int m = X.J.f.m;
-          if (p0 >= m) continue;
-          if (std::min(MW, m - p0) < m && (rc = zgemm(m, m, 0, MW, MW, X))) break;
-        }
+        k_zgemm_acc<<<dim3((mstep + ZG_TN - 1) / ZG_TN, (mstep + ZG_TM - 1) / ZG_TM, nt), 128, 0, st>>>(
+            dtasks, p0, 0, mstep, MW, MW, 1);
+        ctx->launches++;
         DS_CHECK_LAUNCH();
       }
       if (rc) break;
@@ -449,7 +544,6 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
       DS_CUDA(cudaStreamSynchronize(st));  // tasks vector reused next step
     }
   }
-  cublasDestroy(hb);
   cudaStreamSynchronize(st);
   cleanup();
   return rc;

@@ -159,33 +159,6 @@ __device__ __forceinline__ int64_t col_offset(const PassGeo &G, int c, int A, co
   return (int64_t)b * G.n * G.ncols + (int64_t)ii * nrhs + act[a];
 }
 
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-// 16-byte async copy; src_bytes = 0 zero-fills the destination
-__device__ __forceinline__ void cp16(void *dst, const void *src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(dst)), "l"(src),
-               "r"(src_bytes)
-               : "memory");
-}
-// the same with a shared-memory byte address
-__device__ __forceinline__ void cp16s(uint32_t dst, const void *src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-// DMMA without `volatile`: the scheduler may move it across the cp.async
-// issue of the same loop iteration (its operands are registers only)
-__device__ __forceinline__ void dmma_nv(double (&c)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c[0]), "+d"(c[1])
-      : "d"(a), "d"(b));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 // ---------------------------------------------------- transforms (K3m-T)
 // One CTA computes a TM x TN tile of one pass of one visit: A tile (TM x TK)
 // and B tile (TK x TN) double-buffered through shared memory by cp.async,
