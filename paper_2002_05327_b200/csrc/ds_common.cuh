@@ -131,6 +131,7 @@ struct ds_options {
   int hio_dstreams = 2;  // DS_HIO_DSTREAMS: download streams of the pinned-host path
   int kskip = 1;       // DS_KSKIP: forward transforms visit only the nonzero K-chunks (K6 masks)
   int r3_cols = 16;    // DS_R3_COLS: (mode, RHS) columns per block of the segmented recurrences (16 default, 32)
+  int k2b_groups = 2;  // DS_K2B_GROUPS: concurrent groups of a blocked-factorization batch (1 .. 8)
   int count_work = 0;  // modal transforms add the complex multiply-adds they execute to ds_ctx::work
 };
 void ds_options_from_env(ds_options &o);

@@ -89,6 +89,7 @@ void ds_options_from_env(ds_options &o) {
   o.k3_cluster = env_opt("DS_K3_CLUSTER", 0);
   o.hio_dstreams = std::max(2, env_opt("DS_HIO_DSTREAMS", 2));
   o.kskip = env_opt("DS_KSKIP", 1) != 0;
+  o.k2b_groups = std::max(1, std::min(8, env_opt("DS_K2B_GROUPS", 2)));
   o.r3_cols = env_opt("DS_R3_COLS", 16) == 32 ? 32 : 16;
 }
 
@@ -111,6 +112,7 @@ static int *opt_field(ds_options &o, const std::string &k) {
   if (k == "hio_dstreams") return &o.hio_dstreams;
   if (k == "kskip") return &o.kskip;
   if (k == "count_work") return &o.count_work;
+  if (k == "k2b_groups") return &o.k2b_groups;
   if (k == "r3_cols") return &o.r3_cols;
   return nullptr;
 }

@@ -30,6 +30,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "ds_common.cuh"
@@ -416,20 +418,44 @@ static int launch_cluster(const void *kern, dim3 grid, int C, size_t smem, cudaS
   return DS_OK;
 }
 
-int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *const *lh,
-                      const cplx *const *uh, int *status) {
-  if (njobs == 0) return DS_OK;
-  cudaStream_t st = ctx->stream;
-  int mmax = 0;
-  for (int i = 0; i < njobs; ++i) mmax = std::max(mmax, jobs[i].f.m);
-  // panel cluster: enough CTAs that the panel rows fit in shared memory
-  // (16 CTAs of 512 threads from m = 1024 up: a pivot step's elimination is
-  // rows/CTA x 32 complex updates; 8 x 256 took 242 us per panel at m = 2793)
-  int PC = mmax >= 1024 ? 16 : 4;
+// panel cluster size and shared memory for slabs up to mmax rows; sets the
+// kernels' dynamic shared-memory limits (callers do this once for the
+// largest slab before any group starts: the limits are per function, not
+// per stream)
+static int panel_setup(int mmax, int &PC, size_t &panel_smem) {
+  // enough CTAs that the panel rows fit in shared memory (16 CTAs of 512
+  // threads from m = 1024 up: a pivot step's elimination is rows/CTA x 32
+  // complex updates; 8 x 256 took 242 us per panel at m = 2793)
+  PC = mmax >= 1024 ? 16 : 4;
   while (PC < 16 && ((size_t)((mmax + PC - 1) / PC) * BW + 2 * BW) * sizeof(cplx) > 200 * 1024) PC *= 2;
   const int rpc_max = (mmax + PC - 1) / PC;
-  const size_t panel_smem = ((size_t)rpc_max * BW + 2 * BW) * sizeof(cplx);
+  panel_smem = ((size_t)rpc_max * BW + 2 * BW) * sizeof(cplx);
   if (panel_smem > 220 * 1024) return ds_fail(DS_ECONFIG, "blocked factorization: slab too large");
+  return DS_OK;
+}
+static int panel_attributes(int mmax) {
+  int PC;
+  size_t smem;
+  if (int rc = panel_setup(mmax, PC, smem)) return rc;
+  DS_CUDA(cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  DS_CUDA(cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DS_CUDA(cudaFuncSetAttribute(k_col_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(mmax * sizeof(cplx))));
+  return DS_OK;
+}
+
+// one group of matrices on stream st (host-synchronous: returns with the
+// stream drained); `launches` counts the kernels issued
+static int blocked_factor_group(ds_ctx *ctx, cudaStream_t st, const FactJob *jobs, int njobs,
+                                const cplx *const *lh, const cplx *const *uh, int *status,
+                                int64_t &launches) {
+  if (njobs == 0) return DS_OK;
+  int mmax = 0;
+  for (int i = 0; i < njobs; ++i) mmax = std::max(mmax, jobs[i].f.m);
+  int PC;
+  size_t panel_smem;
+  if (int rc0 = panel_setup(mmax, PC, panel_smem)) return rc0;
+  const int rpc_max = (mmax + PC - 1) / PC;
   // per-chain workspaces (pivots, T, P', unpermute map)
   std::vector<void *> ws;
   auto alloc = [&](size_t bytes) -> void * {
@@ -451,10 +477,6 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
     cleanup();
     return ds_fail(DS_ECUDA, "blocked factorization: out of device memory for workspaces");
   }
-  cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem);
-  cudaFuncSetAttribute(k_col_unpermute, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(mmax * sizeof(cplx)));
   int rc = DS_OK;
   // phases: 0 = chains (top and bottom halves together), 1 = middle blocks
   for (int phase = 0; phase < 2 && rc == DS_OK; ++phase) {
@@ -506,7 +528,7 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
       int mstep = 0;
       for (auto &X : tasks) mstep = std::max(mstep, X.J.f.m);
       k_form_schur<<<dim3(std::max(1, std::min(1024, (int)((int64_t)mstep * mstep / 256 / 4))), nt), 256, 0, st>>>(dtasks);
-      ctx->launches++;
+      launches++;
       for (int p0 = 0; p0 < mstep && rc == DS_OK; p0 += MW) {
         for (int p = p0; p < std::min(p0 + MW, mstep) && rc == DS_OK; p += BW) {
           void *args[] = {(void *)&dtasks, (void *)&p, (void *)&rpc_max, (void *)&status};
@@ -516,13 +538,13 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
           int width = BW, W = BW;
           k_panel_operands<<<dim3(std::max(1, (2 * W * mstep + 255) / 256), nt), 256, 0, st>>>(
               dtasks, p, width, W);
-          ctx->launches += 3;
+          launches += 3;
           // the sub-panel's update, restricted to the macro-panel's columns
           {
             const int ncm = std::min(MW, mstep - p0);
             k_zgemm_acc<<<dim3((ncm + ZG_TN - 1) / ZG_TN, (mstep + ZG_TM - 1) / ZG_TM, nt), 128, 0, st>>>(
                 dtasks, p, p0, MW, BW, BW, 0);
-            ctx->launches++;
+            launches++;
           }
           DS_CHECK_LAUNCH();
         }
@@ -530,16 +552,16 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
         // rank-MW update of every column outside the macro-panel
         k_panel_operands<<<dim3(std::max(1, (2 * MW * mstep + 255) / 256), nt), 256, 0, st>>>(
             dtasks, p0, MW, MW);
-        ctx->launches++;
+        launches++;
         k_zgemm_acc<<<dim3((mstep + ZG_TN - 1) / ZG_TN, (mstep + ZG_TM - 1) / ZG_TM, nt), 128, 0, st>>>(
             dtasks, p0, 0, mstep, MW, MW, 1);
-        ctx->launches++;
+        launches++;
         DS_CHECK_LAUNCH();
       }
       if (rc) break;
       k_src_map<<<nt, 32, 0, st>>>(dtasks, srcb, mmax);
       k_col_unpermute<<<dim3(std::min(mstep, 512), nt), 256, mmax * sizeof(cplx), st>>>(dtasks, srcb, mmax);
-      ctx->launches += 2;
+      launches += 2;
       DS_CHECK_LAUNCH();
       DS_CUDA(cudaStreamSynchronize(st));  // tasks vector reused next step
     }
@@ -547,4 +569,71 @@ int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *c
   cudaStreamSynchronize(st);
   cleanup();
   return rc;
+}
+
+// Batches of two or more windows run as up to "k2b_groups" groups, each on
+// its own stream and driven by its own host thread: a group's panel kernels
+// (one 16-CTA cluster per matrix) leave most SMs idle, and the other groups'
+// trailing-update GEMMs fill them ("k2b_groups" = 1: one group).
+int ds_blocked_factor(ds_ctx *ctx, const FactJob *jobs, int njobs, const cplx *const *lh,
+                      const cplx *const *uh, int *status) {
+  if (njobs == 0) return DS_OK;
+  int mall = 0;
+  for (int i = 0; i < njobs; ++i) mall = std::max(mall, jobs[i].f.m);
+  if (int rc0 = panel_attributes(mall)) return rc0;
+  const int G = std::max(1, std::min(ctx->opt.k2b_groups, njobs));
+  if (G == 1) {
+    int64_t l0 = 0;
+    const int rc = blocked_factor_group(ctx, ctx->stream, jobs, njobs, lh, uh, status, l0);
+    ctx->launches += l0;
+    return rc;
+  }
+  struct Group {
+    std::vector<FactJob> jobs;
+    std::vector<const cplx *> l, u;
+    cudaStream_t st = nullptr;
+    int rc = DS_OK;
+    int64_t launches = 0;
+    std::string err;
+  };
+  std::vector<Group> gs(G);
+  // largest first, dealt in snake order: even work per group
+  std::vector<int> order(njobs);
+  for (int i = 0; i < njobs; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return (double)jobs[x].f.nb * jobs[x].f.m * jobs[x].f.m > (double)jobs[y].f.nb * jobs[y].f.m * jobs[y].f.m;
+  });
+  for (int q = 0; q < njobs; ++q) {
+    const int r = q % (2 * G), g = r < G ? r : 2 * G - 1 - r, i = order[q];
+    gs[g].jobs.push_back(jobs[i]);
+    gs[g].l.push_back(lh[i]);
+    gs[g].u.push_back(uh[i]);
+  }
+  cudaEvent_t ev;
+  DS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  DS_CUDA(cudaEventRecord(ev, ctx->stream));  // every group after the caller's prior work
+  gs[0].st = ctx->stream;
+  for (int g = 1; g < G; ++g) {
+    DS_CUDA(cudaStreamCreateWithFlags(&gs[g].st, cudaStreamNonBlocking));
+    DS_CUDA(cudaStreamWaitEvent(gs[g].st, ev, 0));
+  }
+  auto run = [&](Group &gr) {
+    gr.rc = blocked_factor_group(ctx, gr.st, gr.jobs.data(), (int)gr.jobs.size(), gr.l.data(), gr.u.data(),
+                                 status, gr.launches);
+    if (gr.rc) gr.err = ds_last_error();
+  };
+  std::vector<std::thread> th;
+  for (int g = 1; g < G; ++g)
+    th.emplace_back([&, g]() {
+      cudaSetDevice(ctx->device);
+      run(gs[g]);
+    });
+  run(gs[0]);
+  for (auto &t : th) t.join();
+  cudaEventDestroy(ev);
+  for (int g = 1; g < G; ++g) cudaStreamDestroy(gs[g].st);
+  for (auto &gr : gs) ctx->launches += gr.launches;
+  for (auto &gr : gs)
+    if (gr.rc) return ds_fail(gr.rc, gr.err);
+  return DS_OK;
 }
