@@ -100,6 +100,8 @@ DS_API int ds_ctx_work(ds_ctx *ctx, int64_t *cmacs, int32_t reset);
  *   "kskip" forward transforms skip all-zero K-chunks 1 / 0;
  *   "r3_cols" (mode, RHS) columns per block of the segmented mode-wise
  *     recurrences 16 (default) / 32;
+ *   "k2b_groups" concurrent groups of a blocked-factorization batch 1 .. 8
+ *     (default 2);
  *   "count_work" 0 / 1 (see ds_ctx_work).
  * Unknown names or values: < 0. */
 DS_API int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value);
