@@ -129,6 +129,7 @@ extern "C" int ds_ctx_set_option(ds_ctx *ctx, const char *name, int32_t value) {
   else if (k == "k6_rv" || k == "k4_rv") ok = value == 1 || value == 2 || value == 4 || value == 8;
   else if (k == "k3_warps") ok = value == 4 || value == 8;
   else if (k == "r3_cols") ok = value == 16 || value == 32;
+  else if (k == "k2b_groups") ok = value >= 1 && value <= 8;
   else if (k == "k3_cluster") ok = value == 0 || (value >= 8 && value <= 16);
   else ok = value >= 0;
   if (!ok) return ds_fail(DS_ECONFIG, "ds_ctx_set_option: bad value for " + k);

@@ -107,3 +107,28 @@ def test_pool_factor_residuals(cuda, cfg5r):
     with pytest.raises(ConfigurationError):
         _engine.fact_solve(pool, 0, ops[0].window.shape, np.ones(ops[0].window.shape, np.complex128))
     print(f"\npool residuals (12 windows): worst {worst:.2e}")
+
+
+def test_batched_factorization_groups_agree(cuda, cfg5r):
+    """A batch of windows factored as one group or as concurrent groups
+    ("k2b_groups": own streams and host threads, ds_blocked_factor) gives
+    the same factors: each matrix's arithmetic does not depend on the
+    grouping, so solves with them are bitwise equal, and they solve the
+    window operators (residual <= 1e-10)."""
+    s, b = cfg5r
+    ops = [b["ops"][i] for i in b["partition"].subdomains()][:5]
+    rng = np.random.default_rng(56)
+    rhs = [rng.standard_normal(op.window.shape) + 1j * rng.standard_normal(op.window.shape) for op in ops]
+    sols = {}
+    for groups in (1, 2, 3):
+        old = _engine.set_option("k2b_groups", groups)
+        try:
+            pool = _engine.FactorPool(ops, len(ops))
+            pool.load_many([(i, i) for i in range(len(ops))])
+            sols[groups] = [_engine.fact_solve(pool, i, op.window.shape, rhs[i]) for i, op in enumerate(ops)]
+        finally:
+            _engine.set_option("k2b_groups", old)
+    for i, op in enumerate(ops):
+        res = float(np.linalg.norm(op.apply(sols[2][i]) - rhs[i]) / np.linalg.norm(rhs[i]))
+        assert res <= 1e-10, (i, res)
+        assert np.array_equal(sols[1][i], sols[2][i]) and np.array_equal(sols[1][i], sols[3][i]), i
