@@ -1021,3 +1021,27 @@ def test_transform_work_skips_exact(cuda, cfg1, which, option):
     assert 0 < work[1][0] < cm_dense
     _engine.executed_work(reset=True)
     assert _engine.executed_work() == 0
+
+
+def test_additive_cfg2_many_visits_per_launch(cuda):
+    """The additive schedule visits every subdomain in every step: 64 modal
+    visits per launch on config 2's 8 x 8 partition, i.e. more than the 32
+    visits one transform / recurrence kernel launch tabulates (MG_MAXJ), so
+    the launcher splits the list.  Two RHS (a seeded Gaussian and a random
+    field) vs the oracle's additive restatement (ddm.py:294-349)."""
+    from paper_2002_05327_b200 import additive_ddm_solve
+
+    s = configs.spec(2)
+    b = configs.build(s)
+    grid, part, ops = b["grid"], b["partition"], b["ops"]
+    rng = np.random.default_rng(21)
+    f = np.stack([configs.sources(s, grid)[3],
+                  rng.normal(size=grid.counts) + 1j * rng.normal(size=grid.counts)])
+    u, reps = additive_ddm_solve(f, part, ops, FactorizationCache(), warn_collar=False)
+    prob = O.Problem(**configs.oracle_problem(s, b))
+    oops, cache = prob.operators(), O.Cache()
+    for r in range(2):
+        ref, orep = O.additive_apply(prob, oops, cache, f[r])
+        e = rel(u.values[r], ref)
+        assert e <= TOL, (r, e)
+        assert reps[r].nonzero_solves == orep["nonzero_solves"], r
