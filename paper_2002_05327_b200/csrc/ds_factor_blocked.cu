@@ -43,6 +43,7 @@ namespace cg = cooperative_groups;
 #define BW 32
 #define MW 128  // macro-panel: columns per full-matrix update
 #define PANEL_THREADS 512
+static_assert(PANEL_THREADS == 16 * BW, "panel kernel: one candidate-row element per thread, 16-CTA clusters at most");
 
 struct BlkTask {   // one matrix being inverted at the current chain step
   FactJob J;       // operator, layout, factor base
@@ -105,8 +106,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
   __shared__ int pub_i[2];
   __shared__ double red_v[PANEL_THREADS / 32];
   __shared__ int red_i[PANEL_THREADS / 32];
-  __shared__ int s_piv;
+  __shared__ int s_piv, s_win;
   __shared__ double s_best;
+  __shared__ cplx cand[16][BW];            // every CTA's candidate row of this step
 
   for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
     int r = e / BW, c = e % BW;
@@ -144,7 +146,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
       if (j >= r0 && j < r1) pub_rowj[b][lane] = pan[(j - r0) * BW + lane];
     }
     cluster.sync();
-    // (b) global pivot: the C candidates reduced in parallel (same in every CTA)
+    // (b) + (c) in one remote round trip: every candidate row (C x BW
+    // values, one per thread) and row j (its owner is known) are fetched
+    // while warp 0 reduces the C candidates; the winner's row is then picked
+    // from the local copy
+    {
+      const int q = t / BW, c = t % BW;  // PANEL_THREADS = 16 x BW: one element per thread
+      if (q < C) cand[q][c] = *cluster.map_shared_rank(&pub_row[b][c], q);
+    }
+    if (t >= PANEL_THREADS - BW) {  // (the last warp: its candidate fetch above is one more load)
+      const int c = t - (PANEL_THREADS - BW);
+      rowj[c] = *cluster.map_shared_rank(&pub_rowj[b][c], j / rpc);
+    }
     if (t < 32) {
       double v = -1.0;
       int i = m, q = C;
@@ -159,42 +172,42 @@ __global__ void __launch_bounds__(PANEL_THREADS, 1)
         int oq = __shfl_down_sync(0xffffffffu, q, off);
         if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; q = oq; }
       }
-      v = __shfl_sync(0xffffffffu, v, 0);
-      i = __shfl_sync(0xffffffffu, i, 0);
-      q = __shfl_sync(0xffffffffu, q, 0);
-      // (c) rows pv (the winner's published candidate) and j (its owner's copy)
-      if (lane < BW) {
-        rowp[lane] = *cluster.map_shared_rank(&pub_row[b][lane], q < C ? q : 0);
-        rowj[lane] = *cluster.map_shared_rank(&pub_rowj[b][lane], j / rpc);
-      }
       if (lane == 0) {
         s_piv = i;
         s_best = v;
+        s_win = q < C ? q : 0;
       }
     }
+    __syncthreads();
+    if (t < BW) rowp[t] = cand[s_win][t];
     __syncthreads();
     const int pv = min(s_piv, m - 1);
     if (t == 0) {
       if (rank == 0) X.piv[j] = s_piv;
       if (!(s_best > 0.0) || s_piv >= m) atomicExch(status, 1);
     }
-    // (d) eliminate: new row j = old row pv scaled; other rows updated
+    // (d) eliminate: new row j = old row pv scaled; other rows updated.  A
+    // thread's elements share one column (PANEL_THREADS % BW == 0), so the
+    // scaled pivot-row entry is formed once per step
     const cplx pivot = rowp[jj];
     const cplx inv = cinv(pivot);
-    for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
-      const int r = r0 + e / BW, c = e % BW;
-      if (c >= bw) continue;
-      const cplx v = r == j ? rowp[c] : (r == pv ? rowj[c] : pan[e]);
-      const cplx fr = r == j ? rowp[jj] : (r == pv ? rowj[jj] : pan[(r - r0) * BW + jj]);
-      cplx nv;
-      if (r == j) {
-        nv = c == jj ? inv : cmul(v, inv);
-      } else if (c == jj) {
-        nv = cmul(make_double2(-fr.x, -fr.y), inv);
-      } else {
-        nv = csub(v, cmul(fr, cmul(rowp[c], inv)));
-      }
-      pan[e] = nv;
+    {
+      const int c = t % BW;
+      const cplx rpc_c = rowp[c], rjc = rowj[c], rjj = rowj[jj];
+      const cplx rs = cmul(rpc_c, inv);  // rowp[c] / pivot
+      if (c < bw)
+        for (int e = t; e < (r1 - r0) * BW; e += PANEL_THREADS) {
+          const int r = r0 + e / BW;
+          cplx nv;
+          if (r == j) {
+            nv = c == jj ? inv : rs;
+          } else {
+            const cplx fr = r == pv ? rjj : pan[(r - r0) * BW + jj];
+            if (c == jj) nv = cmul(make_double2(-fr.x, -fr.y), inv);
+            else nv = csub(r == pv ? rjc : pan[e], cmul(fr, rs));
+          }
+          pan[e] = nv;
+        }
     }
     __syncthreads();
   }
